@@ -1,0 +1,157 @@
+/*
+ * oracle.h -- plain, slow, fp64 CPU oracle of the per-env-step domain-randomization
+ * pipeline ("Randomizations" appendix).
+ *
+ * TEST INFRASTRUCTURE ONLY.  Only tests/, __graft_entry__.smoke() and bench.py's
+ * cpu_baseline / --impl reference legs may load liboracle.so.  The product path
+ * (include/dr.h + paper_1906_11633_b200/) never includes, links or calls anything here,
+ * and this file includes nothing from the product path: the oracle re-declares its
+ * own parameter struct, implements its own Philox4x32-10 from the Salmon et al.
+ * (SC'11) specification, its own draw transforms, and its own host-side threshold
+ * tables.  Every function cites the passage it follows.
+ *
+ * Arithmetic: fp64 throughout, scalar, one env at a time, compiled with
+ * -O2 -ffp-contract=off (no FMA contraction), so the occlusion distance test is the
+ * exactly-rounded ((dx*dx + dy*dy) + dz*dz) the readings in DESIGN.md fix.
+ *
+ * Parity pins: see tests/test_oracle_*.py.  Unpinned by the paper (workload choices,
+ * DESIGN.md "parity unpinned"): the physical-parameter table (table
+ * missing) and the calibrated backlash widths (values not given).
+ */
+#ifndef DR_ORACLE_H
+#define DR_ORACLE_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define ORC_N_ACT      20   /* Shadow hand actuators */
+#define ORC_N_TIPS     5    /* fingertips */
+#define ORC_N_SUB      10   /* MuJoCo substeps per env step */
+#define ORC_MAX_PHYS   256
+#define ORC_OBS_IN     26   /* raw_obs row: tips 15, obj pos 3, obj quat 4 (w,x,y,z), goal quat 4 */
+#define ORC_OBS_OUT    22   /* policy obs row: rel goal 4, tips 15, obj pos 3 */
+#define ORC_N_STATS    32
+
+/* layer bits (same meaning as DESIGN.md's table; declared independently here) */
+#define ORC_TIMING     (1u << 0)
+#define ORC_ACT_NOISE  (1u << 1)
+#define ORC_DELAY      (1u << 2)
+#define ORC_BACKLASH   (1u << 3)
+#define ORC_OBS_NOISE  (1u << 4)
+#define ORC_DROPOUT    (1u << 5)
+#define ORC_OCCLUSION  (1u << 6)
+#define ORC_FORCE      (1u << 7)
+#define ORC_PHYS       (1u << 8)
+
+/* physical-parameter descriptor kinds (SPEC.md:126 schema; table itself missing) */
+#define ORC_PHYS_FIXED            0
+#define ORC_PHYS_UNIFORM_SCALE    1
+#define ORC_PHYS_LOGUNIFORM_SCALE 2
+#define ORC_PHYS_ADD_GAUSS        3
+#define ORC_PHYS_MUL_LOGNORMAL    4
+
+typedef struct {
+    int32_t kind;
+    double a, b, base;
+} orc_phys_desc;
+
+typedef struct {
+    uint32_t layer_mask;
+    /* action noise + delay, Table action-noise */
+    double act_sigma_uadd, act_sigma_cadd, act_sigma_mult, delay_prob;
+    /* timing */
+    double dt_base, lambda_lo, lambda_hi, step_nominal;
+    /* backlash */
+    double delta_cal_neg[ORC_N_ACT], delta_cal_pos[ORC_N_ACT];
+    double delta_jitter_std, backlash_eps;
+    /* observation noise, Table obs-noise PAPER.md:29-45 (metres / radians) */
+    double tip_corr, tip_uncorr, obj_corr, obj_uncorr, rot_corr, rot_uncorr;
+    double tip_marker, base_marker;
+    int32_t base_marker_to_tips;
+    /* PhaseSpace errors */
+    double dropout_rate_hz;
+    int32_t dropout_hold_steps;
+    double occl_dist;
+    /* random forces */
+    double force_p_lo, force_p_hi, force_accel_std, force_decay_per_step;
+    /* physical parameters */
+    int32_t n_phys, mass_index;
+    orc_phys_desc phys[ORC_MAX_PHYS];
+} orc_params;
+
+/* One environment's episode record + mutable state, fp64. */
+typedef struct {
+    int64_t  gid;          /* global env id (Philox counter word 0) */
+    uint32_t episode;      /* k_e */
+    /* ---- episode record (reset draws) ---- */
+    uint32_t delay_bits;   /* bit j = actuator j delayed */
+    uint32_t p_index;      /* j_p = x >> 16 */
+    uint32_t t_force;      /* floor(p_j * 2^32) (saturated to 2^32-1 only if p=1) */
+    uint32_t _pad0;
+    double   p_force;      /* p_j */
+    double   lambda;
+    double   mass;
+    double   dneg[ORC_N_ACT], dpos[ORC_N_ACT];
+    double   c_act[ORC_N_ACT];
+    double   off_tip[ORC_N_TIPS * 3];
+    double   c_obj[3];
+    double   q_c[4];
+    double   phys[ORC_MAX_PHYS];
+    /* ---- mutable state ---- */
+    double   prev[ORC_N_ACT];
+    double   slack[ORC_N_ACT];
+    double   last[ORC_N_TIPS * 3];
+    int32_t  has_last;
+    int32_t  timer[ORC_N_TIPS];
+    double   f_trig[3];
+    uint32_t k_f;
+    uint32_t _pad1;
+} orc_env;
+
+typedef struct orc_ctx orc_ctx;
+
+/* ---- context API (mirrors the shape of the product ABI; host memory only) ---- */
+int  orc_init(const orc_params* p, int64_t n_env, const int64_t* gids, uint64_t seed, orc_ctx** out);
+void orc_free(orc_ctx* c);
+int  orc_reset(orc_ctx* c, const uint8_t* mask);          /* NULL = all envs */
+/* One env step for all envs of the context.  Outputs may be NULL.
+ * bl_margin [n][20]: fp64 |(s + a_n*d*dt_env) - sgn(a_n)| (the backlash rail margin), +inf when
+ * sgn(a_n) = 0 or BACKLASH off -- used by tests to classify knife-edge rail hits. */
+int  orc_step(orc_ctx* c, const float* actions, const float* raw_obs,
+              double* out_actions, double* out_obs, double* out_dt, double* out_force,
+              double* stats, double* bl_margin);
+uint64_t orc_step_index(const orc_ctx* c);
+void     orc_set_step_index(orc_ctx* c, uint64_t t);
+int      orc_get_env(const orc_ctx* c, int64_t i, orc_env* dst);
+int64_t  orc_n_env(const orc_ctx* c);
+uint64_t orc_force_threshold(const orc_ctx* c, uint32_t j); /* T_j of the 65,536-entry table */
+double   orc_force_p(const orc_ctx* c, uint32_t j);
+
+/* ---- scalar hooks (pinned individually by tests) ---- */
+void   orc_philox(const uint32_t ctr[4], const uint32_t key[2], uint32_t out[4]);
+double orc_uniform(uint32_t x);
+void   orc_normal_pair(uint32_t x, uint32_t y, double* z0, double* z1);
+double orc_exponential(uint32_t x, double lambda);
+void   orc_rotation(double sigma, const uint32_t w[4], double q[4]);
+void   orc_quat_mul(const double a[4], const double b[4], double out[4]);
+void   orc_backlash(double s, double a, double dneg, double dpos, double dt, double eps,
+                    double* s_new, double* alpha, double* out);
+int    orc_occluded(const float* tips15, const float* obj3, double r, int tip);
+uint64_t orc_bernoulli_threshold(double p);
+
+/* stats slot indices */
+enum {
+    ORC_S_ENVS = 0, ORC_S_DELAYED = 1, ORC_S_DROP_INIT = 2, ORC_S_MASKED = 3, ORC_S_OCCLUDED = 4,
+    ORC_S_HELD = 5, ORC_S_FORCE_TRIG = 6, ORC_S_RAIL_HITS = 7, ORC_S_ALPHA_ONE = 8,
+    ORC_S_ALPHA_LT1 = 9, ORC_S_RESETS = 10, ORC_S_ACT_CLAMPS = 11,
+    ORC_S_SUM_DT = 16, ORC_S_SUM_DT2 = 17, ORC_S_SUM_DA = 18, ORC_S_SUM_DA2 = 19,
+    ORC_S_SUM_ABS_BL = 20, ORC_S_SUM_ZU2 = 21, ORC_S_SUM_ZTIP2 = 22, ORC_S_SUM_F2 = 23
+};
+
+#ifdef __cplusplus
+}
+#endif
+#endif

@@ -1,0 +1,268 @@
+"""ctypes wrapper of liboracle.so -- TEST INFRASTRUCTURE ONLY.
+
+Only tests/, ``__graft_entry__.smoke()`` and bench.py's ``cpu_baseline`` / ``--impl reference``
+legs may import this module.  It declares its own struct layouts (mirroring oracle.h) and
+imports nothing from the product package ``paper_1906_11633_b200``.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+import subprocess
+
+import numpy as np
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(HERE, "liboracle.so")
+SOURCES = [os.path.join(HERE, "oracle.c")]
+HEADERS = [os.path.join(HERE, "oracle.h")]
+
+N_ACT, N_TIPS, N_SUB, MAX_PHYS, OBS_IN, OBS_OUT, N_STATS = 20, 5, 10, 256, 26, 22, 32
+
+
+def build(force: bool = False) -> str:
+    """gcc -O2 -ffp-contract=off: plain scalar fp64, no FMA contraction."""
+    newest = max(os.path.getmtime(p) for p in SOURCES + HEADERS)
+    if force or not os.path.exists(LIB_PATH) or os.path.getmtime(LIB_PATH) < newest:
+        cmd = ["gcc", "-O2", "-std=c99", "-D_DEFAULT_SOURCE", "-ffp-contract=off", "-fno-fast-math",
+               "-fPIC", "-shared", "-Wall", "-o", LIB_PATH] + SOURCES + ["-lm"]
+        subprocess.check_call(cmd)
+    return LIB_PATH
+
+
+class PhysDesc(C.Structure):
+    _fields_ = [("kind", C.c_int32), ("a", C.c_double), ("b", C.c_double), ("base", C.c_double)]
+
+
+class OrcParams(C.Structure):
+    _fields_ = [
+        ("layer_mask", C.c_uint32),
+        ("act_sigma_uadd", C.c_double), ("act_sigma_cadd", C.c_double),
+        ("act_sigma_mult", C.c_double), ("delay_prob", C.c_double),
+        ("dt_base", C.c_double), ("lambda_lo", C.c_double), ("lambda_hi", C.c_double),
+        ("step_nominal", C.c_double),
+        ("delta_cal_neg", C.c_double * N_ACT), ("delta_cal_pos", C.c_double * N_ACT),
+        ("delta_jitter_std", C.c_double), ("backlash_eps", C.c_double),
+        ("tip_corr", C.c_double), ("tip_uncorr", C.c_double), ("obj_corr", C.c_double),
+        ("obj_uncorr", C.c_double), ("rot_corr", C.c_double), ("rot_uncorr", C.c_double),
+        ("tip_marker", C.c_double), ("base_marker", C.c_double),
+        ("base_marker_to_tips", C.c_int32),
+        ("dropout_rate_hz", C.c_double), ("dropout_hold_steps", C.c_int32), ("occl_dist", C.c_double),
+        ("force_p_lo", C.c_double), ("force_p_hi", C.c_double), ("force_accel_std", C.c_double),
+        ("force_decay_per_step", C.c_double),
+        ("n_phys", C.c_int32), ("mass_index", C.c_int32),
+        ("phys", PhysDesc * MAX_PHYS),
+    ]
+
+
+class OrcEnv(C.Structure):
+    _fields_ = [
+        ("gid", C.c_int64), ("episode", C.c_uint32),
+        ("delay_bits", C.c_uint32), ("p_index", C.c_uint32), ("t_force", C.c_uint32), ("_pad0", C.c_uint32),
+        ("p_force", C.c_double), ("lambda_", C.c_double), ("mass", C.c_double),
+        ("dneg", C.c_double * N_ACT), ("dpos", C.c_double * N_ACT), ("c_act", C.c_double * N_ACT),
+        ("off_tip", C.c_double * 15), ("c_obj", C.c_double * 3), ("q_c", C.c_double * 4),
+        ("phys", C.c_double * MAX_PHYS),
+        ("prev", C.c_double * N_ACT), ("slack", C.c_double * N_ACT), ("last", C.c_double * 15),
+        ("has_last", C.c_int32), ("timer", C.c_int32 * N_TIPS),
+        ("f_trig", C.c_double * 3), ("k_f", C.c_uint32), ("_pad1", C.c_uint32),
+    ]
+
+
+_lib = None
+
+
+def lib():
+    global _lib
+    if _lib is None:
+        build()
+        L = C.CDLL(LIB_PATH)
+        dp, fp, u8p = C.POINTER(C.c_double), C.POINTER(C.c_float), C.POINTER(C.c_uint8)
+        L.orc_init.argtypes = [C.POINTER(OrcParams), C.c_int64, C.POINTER(C.c_int64), C.c_uint64,
+                               C.POINTER(C.c_void_p)]
+        L.orc_init.restype = C.c_int
+        L.orc_free.argtypes = [C.c_void_p]
+        L.orc_reset.argtypes = [C.c_void_p, u8p]
+        L.orc_reset.restype = C.c_int
+        L.orc_step.argtypes = [C.c_void_p, fp, fp, dp, dp, dp, dp, dp, dp]
+        L.orc_step.restype = C.c_int
+        L.orc_step_index.argtypes = [C.c_void_p]
+        L.orc_step_index.restype = C.c_uint64
+        L.orc_set_step_index.argtypes = [C.c_void_p, C.c_uint64]
+        L.orc_get_env.argtypes = [C.c_void_p, C.c_int64, C.POINTER(OrcEnv)]
+        L.orc_get_env.restype = C.c_int
+        L.orc_force_threshold.argtypes = [C.c_void_p, C.c_uint32]
+        L.orc_force_threshold.restype = C.c_uint64
+        L.orc_force_p.argtypes = [C.c_void_p, C.c_uint32]
+        L.orc_force_p.restype = C.c_double
+        L.orc_philox.argtypes = [C.POINTER(C.c_uint32), C.POINTER(C.c_uint32), C.POINTER(C.c_uint32)]
+        L.orc_uniform.argtypes = [C.c_uint32]
+        L.orc_uniform.restype = C.c_double
+        L.orc_normal_pair.argtypes = [C.c_uint32, C.c_uint32, dp, dp]
+        L.orc_exponential.argtypes = [C.c_uint32, C.c_double]
+        L.orc_exponential.restype = C.c_double
+        L.orc_rotation.argtypes = [C.c_double, C.POINTER(C.c_uint32), dp]
+        L.orc_quat_mul.argtypes = [dp, dp, dp]
+        L.orc_backlash.argtypes = [C.c_double] * 6 + [dp, dp, dp]
+        L.orc_occluded.argtypes = [fp, fp, C.c_double, C.c_int]
+        L.orc_occluded.restype = C.c_int
+        L.orc_bernoulli_threshold.argtypes = [C.c_double]
+        L.orc_bernoulli_threshold.restype = C.c_uint64
+        _lib = L
+    return _lib
+
+
+def make_params(preset: dict) -> OrcParams:
+    p = OrcParams()
+    for name, _ in OrcParams._fields_:
+        if name in ("phys", "delta_cal_neg", "delta_cal_pos"):
+            continue
+        setattr(p, name, preset[name])
+    for j in range(N_ACT):
+        p.delta_cal_neg[j] = preset["delta_cal_neg"][j]
+        p.delta_cal_pos[j] = preset["delta_cal_pos"][j]
+    for i, (k, a, b, base) in enumerate(preset["phys"]):
+        p.phys[i].kind, p.phys[i].a, p.phys[i].b, p.phys[i].base = k, a, b, base
+    return p
+
+
+def _ptr(a, ct):
+    return a.ctypes.data_as(C.POINTER(ct)) if a is not None else None
+
+
+# ---- scalar hooks --------------------------------------------------------------------------
+def philox(ctr, key):
+    c = (C.c_uint32 * 4)(*ctr)
+    k = (C.c_uint32 * 2)(*key)
+    o = (C.c_uint32 * 4)()
+    lib().orc_philox(c, k, o)
+    return tuple(o)
+
+
+def uniform(x):
+    return lib().orc_uniform(x)
+
+
+def normal_pair(x, y):
+    z0, z1 = C.c_double(), C.c_double()
+    lib().orc_normal_pair(x, y, C.byref(z0), C.byref(z1))
+    return z0.value, z1.value
+
+
+def exponential(x, lam):
+    return lib().orc_exponential(x, lam)
+
+
+def rotation(sigma, words):
+    w = (C.c_uint32 * 4)(*words)
+    q = (C.c_double * 4)()
+    lib().orc_rotation(sigma, w, q)
+    return tuple(q)
+
+
+def quat_mul(a, b):
+    A, B, O = (C.c_double * 4)(*a), (C.c_double * 4)(*b), (C.c_double * 4)()
+    lib().orc_quat_mul(A, B, O)
+    return tuple(O)
+
+
+def backlash(s, a, dneg, dpos, dt, eps=1e-12):
+    sn, al, out = C.c_double(), C.c_double(), C.c_double()
+    lib().orc_backlash(s, a, dneg, dpos, dt, eps, C.byref(sn), C.byref(al), C.byref(out))
+    return sn.value, al.value, out.value
+
+
+def occluded(tips15, obj3, r, tip):
+    t = np.ascontiguousarray(tips15, dtype=np.float32)
+    o = np.ascontiguousarray(obj3, dtype=np.float32)
+    return bool(lib().orc_occluded(_ptr(t, C.c_float), _ptr(o, C.c_float), r, tip))
+
+
+def bernoulli_threshold(p):
+    return lib().orc_bernoulli_threshold(p)
+
+
+# ---- context -------------------------------------------------------------------------------
+class Oracle:
+    """fp64 CPU oracle over a list of global env ids (any subset of a larger run)."""
+
+    def __init__(self, preset: dict, n_env: int, seed: int, gids=None):
+        L = lib()
+        self._params = make_params(preset)
+        self.n = int(n_env)
+        if gids is None:
+            gids = np.arange(self.n, dtype=np.int64)
+        self.gids = np.ascontiguousarray(gids, dtype=np.int64)
+        assert self.gids.shape == (self.n,)
+        h = C.c_void_p()
+        rc = L.orc_init(C.byref(self._params), self.n, _ptr(self.gids, C.c_int64), C.c_uint64(seed), C.byref(h))
+        if rc != 0:
+            raise ValueError(f"orc_init failed: {rc}")
+        self._h = h
+
+    def close(self):
+        if getattr(self, "_h", None):
+            lib().orc_free(self._h)
+            self._h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def reset(self, mask=None):
+        m = None if mask is None else np.ascontiguousarray(mask, dtype=np.uint8)
+        if m is not None:
+            assert m.shape == (self.n,)
+        rc = lib().orc_reset(self._h, _ptr(m, C.c_uint8))
+        assert rc == 0
+
+    def step(self, actions, raw_obs, want_margin=False):
+        a = np.ascontiguousarray(actions, dtype=np.float32)
+        o = np.ascontiguousarray(raw_obs, dtype=np.float32)
+        assert a.shape == (self.n, N_ACT) and o.shape == (self.n, OBS_IN)
+        out = {
+            "out_actions": np.empty((self.n, N_ACT)),
+            "out_obs": np.empty((self.n, OBS_OUT)),
+            "out_dt": np.empty((self.n, N_SUB)),
+            "out_force": np.empty((self.n, 3)),
+            "stats": np.empty(N_STATS),
+        }
+        margin = np.empty((self.n, N_ACT)) if want_margin else None
+        dp = C.c_double
+        rc = lib().orc_step(self._h, _ptr(a, C.c_float), _ptr(o, C.c_float),
+                            _ptr(out["out_actions"], dp), _ptr(out["out_obs"], dp),
+                            _ptr(out["out_dt"], dp), _ptr(out["out_force"], dp),
+                            _ptr(out["stats"], dp), _ptr(margin, dp))
+        assert rc == 0
+        if want_margin:
+            out["margin"] = margin
+        return out
+
+    @property
+    def step_index(self):
+        return lib().orc_step_index(self._h)
+
+    @step_index.setter
+    def step_index(self, t):
+        lib().orc_set_step_index(self._h, t)
+
+    def env(self, i) -> dict:
+        e = OrcEnv()
+        assert lib().orc_get_env(self._h, i, C.byref(e)) == 0
+        d = {}
+        for name, ty in OrcEnv._fields_:
+            if name.startswith("_pad"):
+                continue
+            v = getattr(e, name)
+            if hasattr(v, "_length_"):
+                v = np.array(v[:])
+            d["lambda" if name == "lambda_" else name] = v
+        return d
+
+    def force_threshold(self, j):
+        return lib().orc_force_threshold(self._h, j)
+
+    def force_p(self, j):
+        return lib().orc_force_p(self._h, j)
