@@ -1,0 +1,351 @@
+#!/usr/bin/env python
+"""bench.py -- randomized env-steps/s of the fused DR step on B200 (BASELINE.json metric).
+
+Default workload (N=1): BASELINE config 4's single-GPU reference -- 1,048,576 envs, full
+pipeline (all 9 layers), Shadow-hand shapes; under torchrun the 1M envs are sharded over the N
+ranks (env_offset = rank * 1M/N, same seed) with the per-step NCCL all-reduce of the 32 x fp64
+stats vector on a comm stream -- the path's one collective.
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--config full1m|cfg2|cfg3|reset]
+  python bench.py --impl reference ...   # the fp64 CPU oracle on the box's host cores
+
+One JSON line on rank 0.  `value` = env-steps/s over all ranks with inputs resident in HBM
+(CUDA events on the library stream, max over ranks); `e2e` = the same metric through
+dr_step_host with pinned host buffers (H2D of inputs + D2H of all outputs inside the timed
+region); `roofline` for the step kernel; `cpu_baseline` = the oracle on a bounded sample.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+N_GLOBAL_1M = 1 << 20
+# algorithmic bytes per env-step: inputs + outputs + episode record read
+# + state read/write, for the layer sets the configs use
+BYTES_FULL = 184 + 220 + 344 + 480
+BYTES_CFG2 = 184 + 220 + 332 + 160
+RESET_BYTES = 1024 + 356 + 240 + 1      # phys row + record planes + state planes + mask byte
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=2000)
+    ap.add_argument("--warmup", type=int, default=20)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--config", default="full1m", choices=["full1m", "cfg2", "cfg3", "reset"])
+    ap.add_argument("--n-env", type=int, default=0, help="override the global env count")
+    ap.add_argument("--e2e-steps", type=int, default=10)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--cpu-sample-envs", type=int, default=65536)
+    ap.add_argument("--cpu-sample-steps", type=int, default=24)
+    ap.add_argument("--profile", action="store_true", help="short run for ncu (no e2e/cpu legs)")
+    return ap.parse_args()
+
+
+def config_of(name, n_override):
+    from workload import presets
+    if name == "full1m":
+        return dict(workload="cfg4-1M-envs-full-pipeline", mask=presets.FULL, n=n_override or N_GLOBAL_1M,
+                    bytes=BYTES_FULL, scaling="strong", resets=False)
+    if name == "cfg2":
+        return dict(workload="cfg2-4096-envs-backlash+act/obs-noise", mask=presets.CFG2, n=n_override or 4096,
+                    bytes=BYTES_CFG2, scaling="strong", resets=False)
+    if name == "cfg3":
+        return dict(workload="cfg3-65536-envs-full-pipeline", mask=presets.FULL, n=n_override or 65536,
+                    bytes=BYTES_FULL, scaling="strong", resets=False)
+    return dict(workload="cfg5-1M-envs-10pct-resets-per-step", mask=presets.FULL, n=n_override or N_GLOBAL_1M,
+                bytes=BYTES_FULL, scaling="strong", resets=True)
+
+
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons sampled every 100 ms during the timed region."""
+
+    def __init__(self, index):
+        self.index = index
+        self.proc = None
+        self.lines = []
+
+    def start(self):
+        q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+             "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+             "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+        try:
+            self.proc = subprocess.Popen(["nvidia-smi", "-i", str(self.index), f"--query-gpu={q}",
+                                          "--format=csv,noheader,nounits", "-lms", "100"],
+                                         stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except FileNotFoundError:
+            self.proc = None
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def stop(self):
+        if not self.proc:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=2)
+        except Exception:
+            self.proc.kill()
+        time.sleep(0.05)
+        sm, mx, reasons = [], None, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for ln in self.lines:
+            parts = [x.strip() for x in ln.split(",")]
+            if len(parts) < 9:
+                continue
+            try:
+                sm.append(float(parts[1]))
+                mx = float(parts[2])
+            except ValueError:
+                continue
+            for nm, v in zip(names, parts[5:9]):
+                if v.lower() == "active":
+                    reasons.add(nm)
+        sm.sort()
+        med = sm[len(sm) // 2] if sm else None
+        return {"sm_mhz": med, "sm_max_mhz": mx, "reasons": sorted(reasons), "samples": len(sm)}
+
+
+def measured_peak():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            return float(json.load(f)["hbm_gbs"]), "measured"
+    except Exception:
+        return 6650.0, "fallback"
+
+
+def ncu_traffic(workload):
+    """Per-launch dram bytes of the step kernel from the committed ncu summary, if any."""
+    try:
+        with open(os.path.join(ROOT, "profiles", "ncu_step_summary.json")) as f:
+            d = json.load(f)
+        return d.get(workload, {}).get("dram_bytes_per_launch")
+    except Exception:
+        return None
+
+
+def run_reference(args):
+    """--impl reference: the fp64 CPU oracle, as it stands, on this box's host cores (rank 0 only)."""
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return
+    import numpy as np
+    from oracle.oracle import Oracle
+    from workload import gen, presets
+    cfg = config_of(args.config, args.n_env)
+    n = min(cfg["n"], args.cpu_sample_envs)
+    P = presets.preset(cfg["mask"])
+    acts, obs = gen.frames(n, 4)
+    orc = Oracle(P, n, presets.SEED_DR)
+    for t in range(args.warmup):
+        orc.step(acts[t % 4], obs[t % 4])
+    steps = max(1, min(args.steps, args.cpu_sample_steps))
+    t0 = time.perf_counter()
+    for t in range(steps):
+        if cfg["resets"]:
+            orc.reset(gen.reset_mask_ring(n, t))
+        orc.step(acts[t % 4], obs[t % 4])
+    dt = time.perf_counter() - t0
+    v = n * steps / dt
+    line = {"impl": "reference", "metric": "randomized env-steps/sec", "value": v, "unit": "env-steps/s",
+            "n_gpus": args.gpus, "steps": steps, "warmup": args.warmup, "ms_per_step": dt / steps * 1e3,
+            "higher_is_better": True, "scaling": cfg["scaling"], "vs_baseline": None, "dtype": "f64",
+            "data": "synthetic", "config": {"workload": cfg["workload"], "n_env_sample": n, "layers": hex(cfg["mask"])},
+            "cpu_baseline": {"value": v, "unit": "env-steps/s", "cores": 1, "kind": "oracle",
+                             "sample": f"{n} envs x {steps} steps of {cfg['workload']} (single thread, fp64)"},
+            "e2e": {"value": v, "unit": "env-steps/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+
+
+def cpu_baseline(cfg, args):
+    import numpy as np  # noqa: F401
+    from oracle.oracle import Oracle
+    from workload import gen, presets
+    n = min(cfg["n"], args.cpu_sample_envs)
+    P = presets.preset(cfg["mask"])
+    acts, obs = gen.frames(n, 4)
+    orc = Oracle(P, n, presets.SEED_DR)
+    steps = args.cpu_sample_steps
+    t0 = time.perf_counter()
+    for t in range(steps):
+        if cfg["resets"]:
+            orc.reset(gen.reset_mask_ring(n, t))
+        orc.step(acts[t % 4], obs[t % 4])
+    dt = time.perf_counter() - t0
+    orc.close()
+    return {"value": n * steps / dt, "unit": "env-steps/s", "cores": 1, "kind": "oracle",
+            "sample": f"{n} envs x {steps} steps of {cfg['workload']} (fp64 oracle, single thread)"}
+
+
+def main():
+    args = parse()
+    if args.impl == "reference":
+        return run_reference(args)
+
+    import torch
+    import torch.distributed as dist
+    from paper_1906_11633_b200 import DRContext, dr
+    from workload import presets
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    cfg = config_of(args.config, args.n_env)
+    n_glob = cfg["n"]
+    assert n_glob % world == 0
+    n = n_glob // world
+    off = rank * n
+    P = presets.preset(cfg["mask"])
+
+    lib_stream = torch.cuda.Stream()
+    comm_stream = torch.cuda.Stream() if world > 1 else None
+    with torch.cuda.stream(lib_stream):
+        ctx = DRContext(P, n, presets.SEED_DR, env_offset=off, n_env_global=n_glob, stream=lib_stream)
+        # synthetic device-resident frame ring (4 frames), Shadow-hand shapes (workload.gen recipe)
+        F = 4
+        g = torch.Generator(device="cuda").manual_seed(presets.SEED_WORKLOAD + rank)
+        k = torch.randint(0, 11, (F, n, 20), device="cuda", generator=g)
+        A = (-1.0 + (2.0 * k + 1.0) / 11.0).float().contiguous()
+        del k
+        O = torch.empty(F, n, 26, device="cuda")
+        from workload.gen import TIP_NOMINAL, OBJ_NOMINAL, TIP_JITTER, OBJ_JITTER
+        O[:, :, 0:15] = torch.tensor(TIP_NOMINAL.reshape(-1), device="cuda", dtype=torch.float32) + \
+            TIP_JITTER * torch.randn(F, n, 15, device="cuda", generator=g)
+        O[:, :, 15:18] = torch.tensor(OBJ_NOMINAL, device="cuda", dtype=torch.float32) + \
+            OBJ_JITTER * torch.randn(F, n, 3, device="cuda", generator=g)
+        q = torch.randn(F, n, 8, device="cuda", generator=g)
+        O[:, :, 18:22] = q[..., 0:4] / q[..., 0:4].norm(dim=-1, keepdim=True)
+        O[:, :, 22:26] = q[..., 4:8] / q[..., 4:8].norm(dim=-1, keepdim=True)
+        del q
+        masks = None
+        if cfg["resets"]:
+            e = torch.arange(off, off + n, device="cuda")
+            masks = [((e + t) % 10 == 0).to(torch.uint8) for t in range(10)]
+        torch.cuda.synchronize()
+
+    def one_step(t):
+        if masks is not None:
+            ctx.reset(masks[t % 10])
+        ctx.step(A[t % F], O[t % F])
+        if comm_stream is not None:
+            # the path's one collective: sum of the 32 x fp64 stats of step t over ranks,
+            # on its own stream so it overlaps step t+1 (slot t % 2 is double-buffered)
+            ev = torch.cuda.Event()
+            ev.record(lib_stream)
+            comm_stream.wait_event(ev)
+            with torch.cuda.stream(comm_stream):
+                dist.all_reduce(ctx.stats[t % 2])
+
+    with torch.cuda.stream(lib_stream):
+        for t in range(args.warmup):
+            one_step(t)
+        torch.cuda.synchronize()
+        sampler = ClockSampler(local)
+        sampler.start()
+        # keep the GPU busy briefly so the sampler sees load clocks even for short K
+        for t in range(args.warmup, args.warmup + min(args.warmup, 50)):
+            one_step(t)
+        t_base = args.warmup + min(args.warmup, 50)
+        if world > 1:
+            dist.barrier()
+        torch.cuda.synchronize()
+        launches0 = dr.dr_kernel_launches()
+        evs = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps + 1)]
+        evs[0].record(lib_stream)
+        for i in range(args.steps):
+            one_step(t_base + i)
+            evs[i + 1].record(lib_stream)
+        if comm_stream is not None:
+            lib_stream.wait_stream(comm_stream)
+        end = torch.cuda.Event(enable_timing=True)
+        end.record(lib_stream)
+        torch.cuda.synchronize()
+        if world > 1:
+            dist.barrier()
+        launches = dr.dr_kernel_launches() - launches0
+        clocks = sampler.stop()
+        elapsed_ms = evs[0].elapsed_time(end)
+        per = [evs[i].elapsed_time(evs[i + 1]) for i in range(args.steps)]
+        t_ms = torch.tensor([elapsed_ms], dtype=torch.float64, device="cuda")
+        if world > 1:
+            dist.all_reduce(t_ms, op=dist.ReduceOp.MAX)
+        elapsed_ms = float(t_ms.item())
+        stats = ctx.last_stats()
+
+    value = n_glob * args.steps / (elapsed_ms / 1e3)
+    per.sort()
+    kern_ms = sum(per) / len(per)
+    peak, peak_kind = measured_peak()
+    achieved = cfg["bytes"] * n / (kern_ms / 1e3) / 1e9
+    roofline = {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
+                "traffic": ncu_traffic(cfg["workload"]), "peak_kind": peak_kind,
+                "bytes_per_env_step": cfg["bytes"], "kernel": "dr::step_kernel",
+                "kernel_ms_avg": kern_ms, "kernel_ms_median": per[len(per) // 2]}
+
+    # ---- e2e: through dr_step_host with pinned host buffers (copies inside the timed region) ----
+    e2e = None
+    if not args.profile and args.e2e_steps > 0:
+        with torch.cuda.stream(lib_stream):
+            ha = A[0].cpu().pin_memory()
+            ho = O[0].cpu().pin_memory()
+            outs = [torch.empty(n, c).pin_memory() for c in (20, 22, 10, 3)]
+            dr.dr_step_host(ha, ho, *outs)
+            dr.dr_synchronize()
+            if world > 1:
+                dist.barrier()
+            t0 = time.perf_counter()
+            for i in range(args.e2e_steps):
+                dr.dr_step_host(ha, ho, *outs)
+            dr.dr_synchronize()
+            e2e_s = time.perf_counter() - t0
+            te = torch.tensor([e2e_s], dtype=torch.float64, device="cuda")
+            if world > 1:
+                dist.all_reduce(te, op=dist.ReduceOp.MAX)
+            e2e_s = float(te.item())
+        e2e = {"value": n_glob * args.e2e_steps / e2e_s, "unit": "env-steps/s",
+               "h2d_bytes_per_step": n_glob * (20 + 26) * 4, "d2h_bytes_per_step": n_glob * (20 + 22 + 10 + 3) * 4,
+               "api": "dr_step_host (pinned host buffers)", "steps": args.e2e_steps}
+
+    ctx.close()
+    if rank == 0:
+        cpu = None
+        if world == 1 and not args.no_cpu_baseline and not args.profile:
+            cpu = cpu_baseline(cfg, args)
+        line = {
+            "metric": "randomized env-steps/sec", "value": value, "unit": "env-steps/s", "n_gpus": world,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": elapsed_ms / args.steps,
+            "higher_is_better": True, "scaling": cfg["scaling"], "vs_baseline": None, "dtype": "f32",
+            "data": "synthetic",
+            "config": {"workload": cfg["workload"], "n_env_global": n_glob, "n_env_per_gpu": n,
+                       "layers": hex(cfg["mask"]), "parallelism": f"env-shard x{world}",
+                       "l2": "inputs larger than L2" if cfg["bytes"] * n > 126e6 else "L2-resident (warm)",
+                       "bytes_per_step_per_gpu": cfg["bytes"] * n},
+            "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": int(launches),
+            "clocks": clocks,
+            "stats_check": {"envs_last_step": stats[0], "force_trig_rate": stats[6] / max(stats[0], 1)},
+        }
+        if cfg["resets"]:
+            line["resets_per_sec"] = (n_glob / 10) * args.steps / (elapsed_ms / 1e3)
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

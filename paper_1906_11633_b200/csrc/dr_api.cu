@@ -1,0 +1,573 @@
+// dr_api.cu -- host side of libdr.so: the C-ABI of include/dr.h.
+// Validation, workspace layout/allocation (or adoption of a caller-owned PyTorch buffer),
+// host-side constant tables (Philox round keys, Bernoulli thresholds, the 65,536-entry
+// loguniform force table, the 0.99^k decay table), kernel launches on the library stream.
+// There is no CPU fallback: every step of the path runs in the kernels of dr_kernels.cu.
+#include <cuda_runtime.h>
+
+#include <cmath>
+#include <cstdarg>
+#include <cstdio>
+#include <cstdlib>
+#include <cstring>
+#include <vector>
+
+#include "dr.h"
+#include "dr_internal.h"
+
+using namespace dr;
+
+namespace {
+
+struct Layout {
+    size_t rec, st, phys, pd_kr, pd_a, pd_b, pd_base, t_tab, dec, partials, stats, ctl, total;
+    uint64_t pitch;
+};
+
+size_t align_up(size_t x, size_t a) { return (x + a - 1) / a * a; }
+
+int device_sm_count() {
+    int dev = 0, n = 148;
+    if (cudaGetDevice(&dev) == cudaSuccess) cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
+    return n > 0 ? n : 148;
+}
+
+Layout make_layout(int64_t n_env, int n_phys, int max_ctas) {
+    Layout L{};
+    L.pitch = align_up((size_t)n_env, 64);
+    size_t off = 0;
+    auto take = [&](size_t bytes) { size_t o = off; off = align_up(off + bytes, 256); return o; };
+    L.rec = take((size_t)REC_PLANES * L.pitch * 4);
+    L.st = take((size_t)ST_PLANES * L.pitch * 4);
+    L.phys = take((size_t)n_env * n_phys * 4);
+    L.pd_kr = take(MAX_PHYS * 4);
+    L.pd_a = take(MAX_PHYS * 4);
+    L.pd_b = take(MAX_PHYS * 4);
+    L.pd_base = take(MAX_PHYS * 4);
+    L.t_tab = take(65536 * 4);
+    L.dec = take(512 * 8);
+    L.partials = take((size_t)max_ctas * N_STATS * 8);
+    L.stats = take(2 * N_STATS * 8);
+    L.ctl = take(4 * 8);
+    L.total = off;
+    return L;
+}
+
+struct Ctx {
+    dr_params prm;
+    int64_t n_env = 0;
+    uint64_t seed = 0;
+    int device = 0;
+    cudaStream_t stream = nullptr;
+    Layout lay{};
+    char* ws = nullptr;
+    bool owns_ws = false;
+    DevPtrs p{};
+    double* internal_stats = nullptr;
+    int sm_count = 148;
+    int max_ctas = 0;
+    int step_grid = 1, reset_grid = 1;
+    uint64_t t_host = 0;
+    uint64_t launches = 0;
+    // dr_step_host buffers
+    float* io = nullptr;
+    size_t io_bytes = 0;
+};
+
+Ctx* g_ctx = nullptr;
+char g_err[512] = "";
+bool g_sticky = false;
+
+int fail(int code, const char* fmt, ...) {
+    va_list ap;
+    va_start(ap, fmt);
+    vsnprintf(g_err, sizeof(g_err), fmt, ap);
+    va_end(ap);
+    return code;
+}
+
+int cuda_fail(cudaError_t e, const char* where) {
+    g_sticky = true;
+    return fail(DR_ECUDA, "%s: %s", where, cudaGetErrorString(e));
+}
+
+#define CK(call)                                            \
+    do {                                                    \
+        cudaError_t _e = (call);                            \
+        if (_e != cudaSuccess) return cuda_fail(_e, #call); \
+    } while (0)
+
+int validate(const dr_params* p, int64_t n_env) {
+    if (!p) return fail(DR_EINVAL, "params: NULL");
+    if (p->abi_version != DR_ABI_VERSION) return fail(DR_EINVAL, "abi_version: %u != %u", p->abi_version, DR_ABI_VERSION);
+    if (p->struct_size != sizeof(dr_params)) return fail(DR_EINVAL, "struct_size: %u != %zu", p->struct_size, sizeof(dr_params));
+    if (p->layer_mask & ~DR_ALL) return fail(DR_EINVAL, "layer_mask: unknown bits 0x%x", p->layer_mask);
+    if (p->n_act != DR_N_ACT || p->n_tips != DR_N_TIPS || p->n_substeps != DR_N_SUBSTEPS)
+        return fail(DR_EUNSUPPORTED, "n_act/n_tips/n_substeps: kernels specialise (20, 5, 10)");
+    if (n_env < 1 || n_env > (int64_t(1) << 31)) return fail(DR_EINVAL, "n_env: %lld outside [1, 2^31]", (long long)n_env);
+    const int64_t ng = p->n_env_global ? p->n_env_global : n_env;
+    if (p->env_offset < 0 || p->env_offset + n_env > ng || ng > (int64_t(1) << 32))
+        return fail(DR_EINVAL, "env_offset/n_env_global: shard [%lld, %lld) outside [0, %lld)",
+                    (long long)p->env_offset, (long long)(p->env_offset + n_env), (long long)ng);
+    struct { const char* n; double v; } stds[] = {
+        {"act_sigma_uadd", p->act_sigma_uadd}, {"act_sigma_cadd", p->act_sigma_cadd},
+        {"act_sigma_mult", p->act_sigma_mult}, {"delta_jitter_std", p->delta_jitter_std},
+        {"tip_corr", p->tip_corr}, {"tip_uncorr", p->tip_uncorr}, {"obj_corr", p->obj_corr},
+        {"obj_uncorr", p->obj_uncorr}, {"rot_corr", p->rot_corr}, {"rot_uncorr", p->rot_uncorr},
+        {"tip_marker", p->tip_marker}, {"base_marker", p->base_marker},
+        {"force_accel_std", p->force_accel_std}, {"backlash_eps", p->backlash_eps},
+        {"dropout_rate_hz", p->dropout_rate_hz}, {"occl_dist", p->occl_dist}};
+    for (auto& s : stds)
+        if (!(s.v >= 0.0) || !std::isfinite(s.v)) return fail(DR_EINVAL, "%s: must be a finite value >= 0", s.n);
+    if (!(p->delay_prob >= 0.0 && p->delay_prob <= 1.0)) return fail(DR_EINVAL, "delay_prob: outside [0, 1]");
+    if (!(p->dt_base > 0.0)) return fail(DR_EINVAL, "dt_base: must be > 0");
+    if (!(p->step_nominal > 0.0)) return fail(DR_EINVAL, "step_nominal: must be > 0");
+    if (!(p->lambda_lo > 0.0 && p->lambda_lo <= p->lambda_hi && std::isfinite(p->lambda_hi)))
+        return fail(DR_EINVAL, "lambda_lo/lambda_hi: need 0 < lo <= hi");
+    for (int j = 0; j < DR_N_ACT; ++j) {
+        if (!(p->delta_cal_neg[j] >= 0.0)) return fail(DR_EINVAL, "delta_cal_neg[%d]: must be >= 0", j);
+        if (!(p->delta_cal_pos[j] >= 0.0)) return fail(DR_EINVAL, "delta_cal_pos[%d]: must be >= 0", j);
+    }
+    if (p->dropout_hold_steps < 0 || p->dropout_hold_steps > 15) return fail(DR_EINVAL, "dropout_hold_steps: outside [0, 15]");
+    if (!(p->force_p_lo > 0.0 && p->force_p_lo <= p->force_p_hi && p->force_p_hi <= 1.0))
+        return fail(DR_EINVAL, "force_p_lo/force_p_hi: need 0 < lo <= hi <= 1");
+    if (!(p->force_decay_per_step > 0.0 && p->force_decay_per_step <= 1.0))
+        return fail(DR_EINVAL, "force_decay_per_step: outside (0, 1]");
+    if (p->n_phys < 1 || p->n_phys > DR_MAX_PHYS) return fail(DR_EINVAL, "n_phys: outside [1, 256]");
+    if (p->mass_index < 0 || p->mass_index >= p->n_phys) return fail(DR_EINVAL, "mass_index: outside [0, n_phys)");
+    if (!(p->phys[p->mass_index].base > 0.0)) return fail(DR_EINVAL, "phys[mass_index].base: mass must be > 0");
+    for (int i = 0; i < p->n_phys; ++i) {
+        const dr_phys_desc& d = p->phys[i];
+        if (d.kind > DR_PHYS_MUL_LOGNORMAL) return fail(DR_EINVAL, "phys[%d].kind: unknown %u", i, d.kind);
+        if ((d.kind == DR_PHYS_UNIFORM_SCALE) && !(d.a <= d.b)) return fail(DR_EINVAL, "phys[%d]: lo > hi", i);
+        if ((d.kind == DR_PHYS_LOGUNIFORM_SCALE) && !(d.a > 0.0 && d.a <= d.b))
+            return fail(DR_EINVAL, "phys[%d]: loguniform needs 0 < lo <= hi", i);
+        if ((d.kind == DR_PHYS_ADD_GAUSS || d.kind == DR_PHYS_MUL_LOGNORMAL) && !(d.a >= 0.0))
+            return fail(DR_EINVAL, "phys[%d]: std < 0", i);
+    }
+    if (p->workspace && ((uintptr_t)p->workspace % 256)) return fail(DR_EINVAL, "workspace: not 256-byte aligned");
+    return DR_OK;
+}
+
+// Bernoulli threshold floor(p * 2^32) for the exact integer decision x < T.
+unsigned long long bernoulli_threshold(double p) {
+    if (!(p > 0.0)) return 0ull;
+    if (p >= 1.0) return 1ull << 32;
+    return (unsigned long long)std::floor(p * 4294967296.0);
+}
+
+bool aligned16(const void* q) { return ((uintptr_t)q & 15u) == 0; }
+
+}  // namespace
+
+extern "C" {
+
+uint32_t dr_abi_version(void) { return DR_ABI_VERSION; }
+
+const char* dr_last_error(void) { return g_err; }
+
+int dr_params_default(dr_params* p) {
+    if (!p) return fail(DR_EINVAL, "params: NULL");
+    std::memset(p, 0, sizeof(*p));
+    p->abi_version = DR_ABI_VERSION;
+    p->struct_size = sizeof(dr_params);
+    p->layer_mask = DR_ALL;
+    p->n_act = DR_N_ACT;
+    p->n_tips = DR_N_TIPS;
+    p->n_substeps = DR_N_SUBSTEPS;
+    // Table action-noise: % of the action range 2 (Q8)
+    p->act_sigma_uadd = 0.10;
+    p->act_sigma_cadd = 0.03;
+    p->act_sigma_mult = 0.015;
+    p->delay_prob = 0.5;
+    p->dt_base = 0.008;
+    p->lambda_lo = 1250.0;
+    p->lambda_hi = 10000.0;
+    p->step_nominal = 0.08;
+    for (int j = 0; j < DR_N_ACT; ++j) {   // calibrated widths: not given, Q21
+        p->delta_cal_neg[j] = 3.5 + 0.1 * j;
+        p->delta_cal_pos[j] = 4.0 + 0.1 * j;
+    }
+    p->delta_jitter_std = 0.1;
+    p->backlash_eps = 1e-12;
+    // Table obs-noise
+    p->tip_corr = 1e-3;
+    p->tip_uncorr = 2e-3;
+    p->obj_corr = 5e-3;
+    p->obj_uncorr = 1e-3;
+    p->rot_corr = 0.1;
+    p->rot_uncorr = 0.1;
+    p->tip_marker = 3e-3;
+    p->base_marker = 1e-3;
+    p->base_marker_to_tips = 1;            // Q14
+    p->dropout_hold_steps = 13;            // ceil(1 s / 80 ms), Q11
+    p->dropout_rate_hz = 0.2;
+    p->occl_dist = 0.015;                  // Q13
+    p->force_p_lo = 0.001;
+    p->force_p_hi = 0.1;
+    p->force_accel_std = 1.0;
+    p->force_decay_per_step = 0.99;
+    // physical parameters: the paper's table is missing; synthetic 256 slots, Q20
+    p->n_phys = DR_MAX_PHYS;
+    p->mass_index = 0;
+    for (int i = 0; i < DR_MAX_PHYS; ++i) {
+        dr_phys_desc& d = p->phys[i];
+        d.base = 0.5 + 0.01 * i;
+        switch (i % 4) {
+        case 0: d.kind = DR_PHYS_UNIFORM_SCALE; d.a = 0.5; d.b = 1.5; break;
+        case 1: d.kind = DR_PHYS_LOGUNIFORM_SCALE; d.a = 0.3; d.b = 3.0; break;
+        case 2: d.kind = DR_PHYS_ADD_GAUSS; d.a = 0.15; d.b = 0.0; break;
+        default: d.kind = DR_PHYS_MUL_LOGNORMAL; d.a = 0.2; d.b = 0.0; break;
+        }
+    }
+    return DR_OK;
+}
+
+size_t dr_workspace_bytes(const dr_params* params, int64_t n_env) {
+    if (!params || n_env < 1 || params->n_phys < 1 || params->n_phys > DR_MAX_PHYS) return 0;
+    return make_layout(n_env, params->n_phys, device_sm_count() * 32).total;
+}
+
+int dr_init(const dr_params* params, int64_t n_env, uint64_t seed) {
+    if (g_ctx) return fail(DR_EALREADY, "dr_init: context already initialised (call dr_finalize)");
+    int rc = validate(params, n_env);
+    if (rc != DR_OK) return rc;
+    g_sticky = false;
+    Ctx* c = new Ctx();
+    c->prm = *params;
+    if (c->prm.n_env_global == 0) c->prm.n_env_global = n_env;
+    c->n_env = n_env;
+    c->seed = seed;
+    c->stream = static_cast<cudaStream_t>(params->stream);
+    cudaError_t e = cudaGetDevice(&c->device);
+    if (e != cudaSuccess) { delete c; return cuda_fail(e, "cudaGetDevice"); }
+    c->sm_count = device_sm_count();
+    c->max_ctas = c->sm_count * 32;
+    c->lay = make_layout(n_env, params->n_phys, c->max_ctas);
+    if (params->workspace) {
+        if (params->workspace_bytes < c->lay.total) {
+            size_t need = c->lay.total;
+            delete c;
+            return fail(DR_ENOMEM, "workspace_bytes: %zu < required %zu", params->workspace_bytes, need);
+        }
+        c->ws = static_cast<char*>(params->workspace);
+        c->owns_ws = false;
+    } else {
+        e = cudaMalloc(&c->ws, c->lay.total);
+        if (e != cudaSuccess) { delete c; return fail(DR_ENOMEM, "cudaMalloc(%zu): %s", c->lay.total, cudaGetErrorString(e)); }
+        c->owns_ws = true;
+    }
+    const Layout& L = c->lay;
+    DevPtrs& P = c->p;
+    P.rec = reinterpret_cast<uint32_t*>(c->ws + L.rec);
+    P.st = reinterpret_cast<uint32_t*>(c->ws + L.st);
+    P.phys = reinterpret_cast<float*>(c->ws + L.phys);
+    P.pd_kind_rank = reinterpret_cast<uint32_t*>(c->ws + L.pd_kr);
+    P.pd_a = reinterpret_cast<float*>(c->ws + L.pd_a);
+    P.pd_b = reinterpret_cast<float*>(c->ws + L.pd_b);
+    P.pd_base = reinterpret_cast<float*>(c->ws + L.pd_base);
+    P.t_tab = reinterpret_cast<uint32_t*>(c->ws + L.t_tab);
+    P.dec_tab = reinterpret_cast<double*>(c->ws + L.dec);
+    P.partials = reinterpret_cast<double*>(c->ws + L.partials);
+    P.stats = reinterpret_cast<double*>(c->ws + L.stats);
+    P.ctl = reinterpret_cast<unsigned long long*>(c->ws + L.ctl);
+    c->internal_stats = P.stats;
+
+    // ---- host-side constants ----
+    const dr_params& p = c->prm;
+    DevConst dc{};
+    dc.layer_mask = p.layer_mask;
+    dc.n_env = (uint32_t)n_env;
+    dc.pitch = L.pitch;
+    dc.env_offset = (uint32_t)p.env_offset;
+    dc.hold_steps = (uint32_t)p.dropout_hold_steps;
+    const uint32_t k0 = (uint32_t)(seed & 0xFFFFFFFFull), k1 = (uint32_t)(seed >> 32);
+    for (int r = 0; r < 10; ++r) {   // Philox key schedule: key + r * (W0, W1)
+        dc.rk0[r] = k0 + (uint32_t)r * 0x9E3779B9u;
+        dc.rk1[r] = k1 + (uint32_t)r * 0xBB67AE85u;
+    }
+    dc.t_delay = bernoulli_threshold(p.delay_prob);
+    dc.t_drop = bernoulli_threshold(1.0 - std::exp(-p.dropout_rate_hz * p.step_nominal));  // Q11
+    dc.su = (float)p.act_sigma_uadd;
+    dc.sc = (float)p.act_sigma_cadd;
+    dc.sm = (float)p.act_sigma_mult;
+    dc.dt_base = (float)p.dt_base;
+    dc.lam_lo = (float)p.lambda_lo;
+    dc.lam_range = (float)(p.lambda_hi - p.lambda_lo);
+    for (int j = 0; j < DR_N_ACT; ++j) {
+        dc.dcal_neg[j] = (float)p.delta_cal_neg[j];
+        dc.dcal_pos[j] = (float)p.delta_cal_pos[j];
+    }
+    dc.jitter = (float)p.delta_jitter_std;
+    dc.eps = (float)p.backlash_eps;
+    dc.tip_corr = (float)p.tip_corr;
+    dc.tip_uncorr = (float)p.tip_uncorr;
+    dc.obj_corr = (float)p.obj_corr;
+    dc.obj_uncorr = (float)p.obj_uncorr;
+    dc.rot_corr = (float)p.rot_corr;
+    dc.rot_uncorr = (float)p.rot_uncorr;
+    dc.tip_marker = (float)p.tip_marker;
+    dc.base_marker = (float)p.base_marker;
+    dc.base_to_tips = p.base_marker_to_tips ? 1 : 0;
+    dc.occl_on = p.occl_dist > 0.0 ? 1 : 0;
+    dc.occl_r2 = p.occl_dist * p.occl_dist;
+    dc.accel_std = (float)p.force_accel_std;
+    dc.n_phys = p.n_phys;
+    dc.mass_index = p.mass_index;
+
+    std::vector<uint32_t> kr(MAX_PHYS, 0);
+    std::vector<float> pa(MAX_PHYS, 0.f), pb(MAX_PHYS, 0.f), pbase(MAX_PHYS, 0.f);
+    int nu = 0, nn = 0;
+    for (int i = 0; i < p.n_phys; ++i) {
+        const dr_phys_desc& d = p.phys[i];
+        uint32_t rank = 0;
+        switch (d.kind) {
+        case DR_PHYS_UNIFORM_SCALE: rank = nu++; pa[i] = (float)d.a; pb[i] = (float)(d.b - d.a); break;
+        case DR_PHYS_LOGUNIFORM_SCALE:
+            rank = nu++; pa[i] = (float)std::log(d.a); pb[i] = (float)(std::log(d.b) - std::log(d.a)); break;
+        case DR_PHYS_ADD_GAUSS:
+        case DR_PHYS_MUL_LOGNORMAL: rank = nn++; pa[i] = (float)d.a; break;
+        default: break;
+        }
+        kr[i] = d.kind | (rank << 8);
+        pbase[i] = (float)d.base;
+    }
+    dc.n_phys_u = nu;
+    dc.n_phys_n = nn;
+    // loguniform force probability quantised to 65,536 midpoints of ln p (Q19)
+    std::vector<uint32_t> ttab(65536);
+    {
+        const double llo = std::log(p.force_p_lo), lhi = std::log(p.force_p_hi);
+        for (uint32_t j = 0; j < 65536u; ++j) {
+            const double pj = std::exp(llo + (((double)j + 0.5) / 65536.0) * (lhi - llo));
+            const unsigned long long T = bernoulli_threshold(pj);
+            ttab[j] = (uint32_t)(T > 0xFFFFFFFFull ? 0xFFFFFFFFull : T);
+        }
+    }
+    // decay 0.99^k = dec[k & 255] * dec[256 + (k >> 8)], fp64 (Q17)
+    std::vector<double> dec(512);
+    for (int j = 0; j < 256; ++j) {
+        dec[j] = std::pow(p.force_decay_per_step, (double)j);
+        dec[256 + j] = std::pow(p.force_decay_per_step, 256.0 * j);
+    }
+    cudaStream_t s = c->stream;
+    auto bail = [&](cudaError_t err, const char* what) {
+        if (c->owns_ws) cudaFree(c->ws);
+        delete c;
+        return cuda_fail(err, what);
+    };
+    if ((e = upload_const(dc, s)) != cudaSuccess) return bail(e, "upload_const");
+    if ((e = cudaMemcpyAsync(P.pd_kind_rank, kr.data(), MAX_PHYS * 4, cudaMemcpyHostToDevice, s)) != cudaSuccess) return bail(e, "memcpy pd");
+    if ((e = cudaMemcpyAsync(P.pd_a, pa.data(), MAX_PHYS * 4, cudaMemcpyHostToDevice, s)) != cudaSuccess) return bail(e, "memcpy pd");
+    if ((e = cudaMemcpyAsync(P.pd_b, pb.data(), MAX_PHYS * 4, cudaMemcpyHostToDevice, s)) != cudaSuccess) return bail(e, "memcpy pd");
+    if ((e = cudaMemcpyAsync(P.pd_base, pbase.data(), MAX_PHYS * 4, cudaMemcpyHostToDevice, s)) != cudaSuccess) return bail(e, "memcpy pd");
+    if ((e = cudaMemcpyAsync(P.t_tab, ttab.data(), 65536 * 4, cudaMemcpyHostToDevice, s)) != cudaSuccess) return bail(e, "memcpy t_tab");
+    if ((e = cudaMemcpyAsync(P.dec_tab, dec.data(), 512 * 8, cudaMemcpyHostToDevice, s)) != cudaSuccess) return bail(e, "memcpy dec");
+    if ((e = cudaMemsetAsync(P.stats, 0, 2 * N_STATS * 8, s)) != cudaSuccess) return bail(e, "memset stats");
+    if ((e = cudaMemsetAsync(P.ctl, 0, 4 * 8, s)) != cudaSuccess) return bail(e, "memset ctl");
+    // state planes start zeroed so that never-reset lanes of a partial tile stay defined
+    if ((e = cudaMemsetAsync(P.st, 0, (size_t)ST_PLANES * L.pitch * 4, s)) != cudaSuccess) return bail(e, "memset st");
+    if ((e = cudaStreamSynchronize(s)) != cudaSuccess) return bail(e, "sync init");
+
+    const int occ_step = step_max_ctas_per_sm(p.layer_mask);
+    const uint32_t n_tiles = (uint32_t)((n_env + TILE - 1) / TILE);
+    c->step_grid = (int)std::min<long long>((long long)n_tiles, (long long)c->sm_count * occ_step);
+    if (c->step_grid > c->max_ctas) c->step_grid = c->max_ctas;
+    const uint32_t n_chunks = (uint32_t)((n_env + 31) / 32);
+    const int occ_reset = reset_max_ctas_per_sm();
+    c->reset_grid = (int)std::min<long long>((long long)(n_chunks + 7) / 8, (long long)c->sm_count * occ_reset);
+    if (c->reset_grid < 1) c->reset_grid = 1;
+
+    // episode 0 for every env (sampled at the beginning of every episode)
+    if ((e = launch_reset(P, nullptr, true, (uint32_t)n_env, c->reset_grid, s)) != cudaSuccess) return bail(e, "reset_kernel");
+    c->launches = 1;
+    g_ctx = c;
+    g_err[0] = 0;
+    return DR_OK;
+}
+
+int dr_reset(const uint8_t* env_mask) {
+    Ctx* c = g_ctx;
+    if (!c) return fail(DR_ENOTINIT, "dr_reset: no context");
+    if (g_sticky) return fail(DR_ECUDA, "sticky CUDA error: %s", g_err);
+    cudaError_t e = launch_reset(c->p, env_mask, false, (uint32_t)c->n_env, c->reset_grid, c->stream);
+    if (e != cudaSuccess) return cuda_fail(e, "reset_kernel");
+    c->launches++;
+    return DR_OK;
+}
+
+int dr_step(const float* actions, const float* raw_obs, float* out_actions, float* out_obs, float* out_dt,
+            float* out_force) {
+    Ctx* c = g_ctx;
+    if (!c) return fail(DR_ENOTINIT, "dr_step: no context");
+    if (g_sticky) return fail(DR_ECUDA, "sticky CUDA error: %s", g_err);
+    const void* ptrs[6] = {actions, raw_obs, out_actions, out_obs, out_dt, out_force};
+    const char* names[6] = {"actions", "raw_obs", "out_actions", "out_obs", "out_dt", "out_force"};
+    for (int i = 0; i < 6; ++i) {
+        if (!ptrs[i]) return fail(DR_EINVAL, "%s: NULL", names[i]);
+        if (!aligned16(ptrs[i])) return fail(DR_EINVAL, "%s: not 16-byte aligned", names[i]);
+    }
+    cudaError_t e = launch_step(c->p, c->prm.layer_mask, actions, raw_obs, out_actions, out_obs, out_dt, out_force,
+                                (uint32_t)c->n_env, c->step_grid, c->stream);
+    if (e != cudaSuccess) return cuda_fail(e, "step_kernel");
+    c->t_host++;
+    c->launches++;
+    return DR_OK;
+}
+
+int dr_step_host(const float* actions, const float* raw_obs, float* out_actions, float* out_obs, float* out_dt,
+                 float* out_force) {
+    Ctx* c = g_ctx;
+    if (!c) return fail(DR_ENOTINIT, "dr_step_host: no context");
+    if (g_sticky) return fail(DR_ECUDA, "sticky CUDA error: %s", g_err);
+    if (!actions || !raw_obs || !out_actions || !out_obs || !out_dt || !out_force)
+        return fail(DR_EINVAL, "dr_step_host: NULL buffer");
+    const size_t n = (size_t)c->n_env;
+    const size_t fa = n * N_ACT, fo = n * OBS_IN, foa = n * N_ACT, foo = n * OBS_OUT, fdt = n * N_SUB, ff = n * 3;
+    auto up16 = [](size_t f) { return (f + 3) / 4 * 4; };
+    const size_t total = (up16(fa) + up16(fo) + up16(foa) + up16(foo) + up16(fdt) + up16(ff)) * 4;
+    if (!c->io) {
+        CK(cudaMalloc(&c->io, total));
+        c->io_bytes = total;
+    }
+    float* d_a = c->io;
+    float* d_o = d_a + up16(fa);
+    float* d_oa = d_o + up16(fo);
+    float* d_oo = d_oa + up16(foa);
+    float* d_dt = d_oo + up16(foo);
+    float* d_f = d_dt + up16(fdt);
+    cudaStream_t s = c->stream;
+    CK(cudaMemcpyAsync(d_a, actions, fa * 4, cudaMemcpyHostToDevice, s));
+    CK(cudaMemcpyAsync(d_o, raw_obs, fo * 4, cudaMemcpyHostToDevice, s));
+    int rc = dr_step(d_a, d_o, d_oa, d_oo, d_dt, d_f);
+    if (rc != DR_OK) return rc;
+    CK(cudaMemcpyAsync(out_actions, d_oa, foa * 4, cudaMemcpyDeviceToHost, s));
+    CK(cudaMemcpyAsync(out_obs, d_oo, foo * 4, cudaMemcpyDeviceToHost, s));
+    CK(cudaMemcpyAsync(out_dt, d_dt, fdt * 4, cudaMemcpyDeviceToHost, s));
+    CK(cudaMemcpyAsync(out_force, d_f, ff * 4, cudaMemcpyDeviceToHost, s));
+    return DR_OK;
+}
+
+int dr_finalize(void) {
+    Ctx* c = g_ctx;
+    if (!c) return fail(DR_ENOTINIT, "dr_finalize: no context");
+    cudaStreamSynchronize(c->stream);
+    if (c->owns_ws) cudaFree(c->ws);
+    if (c->io) cudaFree(c->io);
+    delete c;
+    g_ctx = nullptr;
+    g_sticky = false;
+    return DR_OK;
+}
+
+int dr_set_stream(void* cuda_stream) {
+    if (!g_ctx) return fail(DR_ENOTINIT, "dr_set_stream: no context");
+    g_ctx->stream = static_cast<cudaStream_t>(cuda_stream);
+    return DR_OK;
+}
+
+int dr_synchronize(void) {
+    if (!g_ctx) return fail(DR_ENOTINIT, "dr_synchronize: no context");
+    CK(cudaStreamSynchronize(g_ctx->stream));
+    return DR_OK;
+}
+
+const float* dr_phys_params(void) { return g_ctx ? g_ctx->p.phys : nullptr; }
+int dr_n_phys(void) { return g_ctx ? g_ctx->prm.n_phys : 0; }
+
+const double* dr_stats(int slot) {
+    if (!g_ctx || slot < 0 || slot > 1) return nullptr;
+    return g_ctx->p.stats + slot * N_STATS;
+}
+
+int dr_set_stats_buffer(double* dev_buf) {
+    if (!g_ctx) return fail(DR_ENOTINIT, "dr_set_stats_buffer: no context");
+    if (dev_buf && ((uintptr_t)dev_buf & 7u)) return fail(DR_EINVAL, "stats buffer: not 8-byte aligned");
+    g_ctx->p.stats = dev_buf ? dev_buf : g_ctx->internal_stats;
+    return DR_OK;
+}
+
+uint64_t dr_step_index(void) { return g_ctx ? g_ctx->t_host : 0; }
+
+int dr_set_step_index(uint64_t t) {
+    Ctx* c = g_ctx;
+    if (!c) return fail(DR_ENOTINIT, "dr_set_step_index: no context");
+    unsigned long long v = t;
+    CK(cudaMemcpyAsync(c->p.ctl, &v, 8, cudaMemcpyHostToDevice, c->stream));
+    CK(cudaStreamSynchronize(c->stream));
+    c->t_host = t;
+    return DR_OK;
+}
+
+size_t dr_state_bytes(void) { return g_ctx ? sizeof(dr_env_state) * (size_t)g_ctx->n_env : 0; }
+
+static int state_range(int64_t& lo, int64_t& hi) {
+    if (lo == 0 && hi == 0) hi = g_ctx->n_env;
+    if (lo < 0 || hi > g_ctx->n_env || lo >= hi) return fail(DR_EINVAL, "env range [%lld, %lld) invalid", (long long)lo, (long long)hi);
+    return DR_OK;
+}
+
+int dr_state_export(void* host_dst, int64_t env_lo, int64_t env_hi) {
+    Ctx* c = g_ctx;
+    if (!c) return fail(DR_ENOTINIT, "dr_state_export: no context");
+    if (!host_dst) return fail(DR_EINVAL, "host_dst: NULL");
+    int rc = state_range(env_lo, env_hi);
+    if (rc) return rc;
+    const size_t bytes = sizeof(dr_env_state) * (size_t)(env_hi - env_lo);
+    void* d = nullptr;
+    CK(cudaMallocAsync(&d, bytes, c->stream));
+    cudaError_t e = launch_export(c->p, d, (uint32_t)env_lo, (uint32_t)env_hi, c->stream);
+    if (e != cudaSuccess) return cuda_fail(e, "export_kernel");
+    c->launches++;
+    CK(cudaMemcpyAsync(host_dst, d, bytes, cudaMemcpyDeviceToHost, c->stream));
+    CK(cudaFreeAsync(d, c->stream));
+    CK(cudaStreamSynchronize(c->stream));
+    return DR_OK;
+}
+
+int dr_state_import(const void* host_src, int64_t env_lo, int64_t env_hi) {
+    Ctx* c = g_ctx;
+    if (!c) return fail(DR_ENOTINIT, "dr_state_import: no context");
+    if (!host_src) return fail(DR_EINVAL, "host_src: NULL");
+    int rc = state_range(env_lo, env_hi);
+    if (rc) return rc;
+    const size_t bytes = sizeof(dr_env_state) * (size_t)(env_hi - env_lo);
+    void* d = nullptr;
+    CK(cudaMallocAsync(&d, bytes, c->stream));
+    CK(cudaMemcpyAsync(d, host_src, bytes, cudaMemcpyHostToDevice, c->stream));
+    cudaError_t e = launch_import(c->p, d, (uint32_t)env_lo, (uint32_t)env_hi, c->stream);
+    if (e != cudaSuccess) return cuda_fail(e, "import_kernel");
+    c->launches++;
+    CK(cudaFreeAsync(d, c->stream));
+    CK(cudaStreamSynchronize(c->stream));
+    return DR_OK;
+}
+
+int dr_phys_export(void* host_dst, int64_t env_lo, int64_t env_hi) {
+    Ctx* c = g_ctx;
+    if (!c) return fail(DR_ENOTINIT, "dr_phys_export: no context");
+    if (!host_dst) return fail(DR_EINVAL, "host_dst: NULL");
+    int rc = state_range(env_lo, env_hi);
+    if (rc) return rc;
+    const size_t row = (size_t)c->prm.n_phys * 4;
+    CK(cudaMemcpyAsync(host_dst, reinterpret_cast<const char*>(c->p.phys) + (size_t)env_lo * row,
+                       (size_t)(env_hi - env_lo) * row, cudaMemcpyDeviceToHost, c->stream));
+    CK(cudaStreamSynchronize(c->stream));
+    return DR_OK;
+}
+
+uint64_t dr_kernel_launches(void) { return g_ctx ? g_ctx->launches : 0; }
+
+int dr_debug_philox(uint32_t domain, uint32_t channel, uint32_t block, uint32_t* out_dev) {
+    Ctx* c = g_ctx;
+    if (!c) return fail(DR_ENOTINIT, "dr_debug_philox: no context");
+    if (!out_dev || !aligned16(out_dev)) return fail(DR_EINVAL, "out_dev: NULL or not 16-byte aligned");
+    cudaError_t e = launch_debug_philox((uint32_t)c->n_env, domain, channel, block, out_dev, c->stream);
+    if (e != cudaSuccess) return cuda_fail(e, "debug_philox_kernel");
+    c->launches++;
+    return DR_OK;
+}
+
+}  // extern "C"
+
+static_assert(sizeof(dr_env_state) == 148 * 4, "dr_env_state must be 148 words");

@@ -1,0 +1,115 @@
+// dr_internal.h -- shared between the host library (dr_api.cu) and the kernels (dr_kernels.cu).
+// Device data layout:
+//   rec  : episode record, structure-of-arrays planes [REC_PLANES][pitch] (4-byte words)
+//   st   : mutable per-env state, planes [ST_PLANES][pitch]
+//   phys : [n_env][n_phys] fp32, row-major (the simulator reads rows)
+// pitch = n_env rounded up to 64, so every plane starts 256-byte aligned and a warp's 32
+// consecutive envs read one 128-byte line per plane (coalesced, no staging needed).
+#pragma once
+#include <cstddef>
+#include <cstdint>
+#include <cuda_runtime.h>
+
+namespace dr {
+
+constexpr int N_ACT = 20, N_TIPS = 5, N_SUB = 10, MAX_PHYS = 256, OBS_IN = 26, OBS_OUT = 22;
+constexpr int N_STATS = 32;
+constexpr int TILE = 128;           // envs per CTA tile (one thread per env)
+constexpr uint32_t RUNTIME_MASK = 0xFFFFFFFFu;
+
+// ---- record planes (read by the step kernel: 86 of them) ----
+enum : int {
+    REC_DELAY = 0,   // u32 delay bits
+    REC_INVLAM = 1,  // 1/lambda (the step only needs the reciprocal rate)
+    REC_TFORCE = 2,  // u32 force threshold
+    REC_MASS = 3,
+    REC_DNEG = 4,    // 20
+    REC_DPOS = 24,   // 20
+    REC_CACT = 44,   // 20
+    REC_OFFTIP = 64, // 15
+    REC_COBJ = 79,   // 3
+    REC_QC = 82,     // 4
+    REC_STEP_PLANES = 86,
+    // not read by the step kernel
+    REC_LAMBDA = 86,
+    REC_PINDEX = 87, // u32
+    REC_EPISODE = 88,// u32
+    REC_PLANES = 89
+};
+// ---- state planes (read + written by the step kernel) ----
+enum : int {
+    ST_PREV = 0,     // 20
+    ST_SLACK = 20,   // 20
+    ST_LAST = 40,    // 15
+    ST_FLAGS = 55,   // u32: tip i timer in bits 4i..4i+3, has_last in bit 20
+    ST_FTRIG = 56,   // 3
+    ST_KF = 59,      // u32
+    ST_PLANES = 60
+};
+constexpr uint32_t HAS_LAST_BIT = 1u << 20;
+
+// Philox channels
+enum : uint32_t {
+    CH_TIMING = 0x01, CH_ACT_UADD = 0x02, CH_ACT_MULT = 0x03, CH_DROPOUT = 0x04,
+    CH_TIP_NOISE = 0x05, CH_OBJ_NOISE = 0x06, CH_ROT_NOISE = 0x07, CH_FORCE = 0x08,
+    CH_PHYS_U = 0x101, CH_DELAY = 0x102, CH_BACKLASH = 0x103, CH_LAMBDA = 0x104,
+    CH_FORCE_P = 0x105, CH_CORR_ACT = 0x106, CH_CORR_TIP = 0x107, CH_MARKER_TIP = 0x108,
+    CH_MARKER_BASE = 0x109, CH_CORR_OBJ = 0x10A, CH_CORR_ROT = 0x10B, CH_PHYS_N = 0x10C
+};
+
+// Constants uploaded once at dr_init (warp-uniform accesses only -> __constant__).
+struct DevConst {
+    uint32_t layer_mask;
+    uint32_t n_env;
+    uint64_t pitch;
+    uint32_t env_offset;
+    uint32_t hold_steps;
+    uint32_t rk0[10], rk1[10];        // Philox round keys (key schedule precomputed on host)
+    unsigned long long t_delay, t_drop;
+    float su, sc, sm;                 // action noise stds
+    float dt_base, lam_lo, lam_range;
+    float dcal_neg[N_ACT], dcal_pos[N_ACT], jitter;
+    float eps;
+    float tip_corr, tip_uncorr, obj_corr, obj_uncorr, rot_corr, rot_uncorr, tip_marker, base_marker;
+    int32_t base_to_tips;
+    int32_t occl_on;
+    double occl_r2;
+    float accel_std;
+    int32_t n_phys, mass_index;
+    int32_t n_phys_u, n_phys_n;       // counts of uniform-kind / normal-kind params
+};
+
+// Pointers of the device workspace.
+struct DevPtrs {
+    uint32_t* rec;            // [REC_PLANES][pitch]
+    uint32_t* st;             // [ST_PLANES][pitch]
+    float* phys;              // [n_env][n_phys]
+    // physics descriptor table (global, lane-indexed in the reset kernel)
+    uint32_t* pd_kind_rank;   // [256]: kind | (rank << 8)
+    float* pd_a;              // [256]  a (or ln a for loguniform)
+    float* pd_b;              // [256]  b (or ln b - ln a for loguniform)
+    float* pd_base;           // [256]
+    uint32_t* t_tab;          // [65536] force thresholds
+    double* dec_tab;          // [512]: 0.99^j (j < 256), then 0.99^(256 i)
+    double* partials;         // [max_ctas][N_STATS]
+    double* stats;            // [2][N_STATS] (internal or caller-owned)
+    unsigned long long* ctl;  // [0] = step t, [1] = CTAs done counter, [2] = resets pending
+};
+
+// launchers (dr_kernels.cu)
+cudaError_t upload_const(const DevConst& c, cudaStream_t s);
+cudaError_t launch_reset(const DevPtrs& p, const uint8_t* mask, bool first, uint32_t n_env,
+                         int grid, cudaStream_t s);
+cudaError_t launch_step(const DevPtrs& p, uint32_t layer_mask, const float* actions,
+                        const float* raw_obs, float* out_actions, float* out_obs, float* out_dt,
+                        float* out_force, uint32_t n_env, int grid, cudaStream_t s);
+cudaError_t launch_export(const DevPtrs& p, void* dst, uint32_t lo, uint32_t hi, cudaStream_t s);
+cudaError_t launch_import(const DevPtrs& p, const void* src, uint32_t lo, uint32_t hi, cudaStream_t s);
+cudaError_t launch_debug_philox(uint32_t n_env, uint32_t dom, uint32_t ch, uint32_t blk, uint32_t* out,
+                                cudaStream_t s);
+int step_max_ctas_per_sm(uint32_t layer_mask);
+int reset_max_ctas_per_sm();
+constexpr int RESET_THREADS = 256;
+constexpr int STEP_THREADS = TILE;
+
+}  // namespace dr

@@ -1,0 +1,348 @@
+"""GPU parity: the CUDA path (through the C-ABI, libdr.so) against the fp64 oracle on the same
+seeded inputs, element by element (tests/parity.py states the contract)."""
+import numpy as np
+import pytest
+
+from parity import (KnifeTracker, assert_close, compare_obs, compare_records, compare_stats)
+from workload import gen, presets
+from workload.presets import (ACT_NOISE, BACKLASH, CFG2, DELAY, DROPOUT, FORCE, FULL, OBS_NOISE,
+                              OCCLUSION, PHYS, TIMING)
+
+pytestmark = pytest.mark.gpu
+SEED = presets.SEED_DR
+
+
+@pytest.fixture(scope="module")
+def torch_cuda():
+    import torch
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    return torch
+
+
+def _ctx(preset, n, seed=SEED, **kw):
+    from paper_1906_11633_b200 import DRContext
+    return DRContext(preset, n, seed, **kw)
+
+
+def _oracle(preset, gids, seed=SEED):
+    from oracle.oracle import Oracle
+    return Oracle(preset, len(gids), seed, gids=np.asarray(gids, dtype=np.int64))
+
+
+def run_pair(torch, mask, n_env, T, n_frames=8, resets=None, sample=None, state_every=1,
+             stats=True, seed=SEED, frame_seed=presets.SEED_WORKLOAD, **kw):
+    """Run the GPU on all n_env envs and the oracle on `sample` (default: all); compare every
+    step.  `resets`: {t: uint8 mask [n_env]} applied before step t."""
+    P = presets.preset(mask, **kw)
+    acts, obs = gen.frames(n_env, n_frames, seed=frame_seed)
+    A = torch.from_numpy(acts).cuda()
+    O = torch.from_numpy(obs).cuda()
+    gids = np.arange(n_env) if sample is None else np.asarray(sample)
+    full = sample is None
+    ctx = _ctx(P, n_env, seed)
+    orc = _oracle(P, gids, seed)
+    knife = KnifeTracker(len(gids))
+    try:
+        G = ctx.export()
+        compare_records({k: v[gids] for k, v in G.items()}, [orc.env(i) for i in range(len(gids))],
+                        phys_g=ctx.phys()[gids])
+        for t in range(T):
+            if resets and t in resets:
+                m = resets[t]
+                ctx.reset(torch.from_numpy(m).cuda())
+                orc.reset(m[gids])
+            f = t % n_frames
+            ctx.step(A[f], O[f])
+            r = orc.step(acts[f][gids], obs[f][gids], want_margin=True)
+            torch.cuda.synchronize()
+            oa = ctx.out_actions.cpu().numpy()[gids]
+            oo = ctx.out_obs.cpu().numpy()[gids]
+            od = ctx.out_dt.cpu().numpy()[gids]
+            of = ctx.out_force.cpu().numpy()[gids]
+            knife.update_before_compare(r["margin"])
+            knife.compare_actions(oa, r["out_actions"], t)
+            compare_obs(oo, r["out_obs"], t)
+            assert_close(f"out_dt t={t}", od, r["out_dt"], 0.008)
+            mass = np.array([orc.env(i)["mass"] for i in range(len(gids))]) if (mask & FORCE) else np.ones(len(gids))
+            assert_close(f"out_force t={t}", of, r["out_force"], mass[:, None] * P["force_accel_std"])
+            if full and stats:
+                compare_stats(ctx.last_stats(), r["stats"], n_env, knife.events)
+            if state_every and (t % state_every == 0 or t == T - 1):
+                G = ctx.export()
+                compare_records({k: v[gids] for k, v in G.items()}, [orc.env(i) for i in range(len(gids))],
+                                knife=knife)
+        return knife
+    finally:
+        ctx.close()
+        orc.close()
+
+
+def test_debug_philox_words_bit_exact(torch_cuda):
+    """RNG integer streams are bit-exact: the device Philox words the kernels draw equal the
+    oracle's from-spec Philox for every env, in both the step and the reset domain."""
+    torch = torch_cuda
+    from oracle import oracle as O
+    from paper_1906_11633_b200 import dr
+    n = 257
+    seed = 0x0123456789ABCDEF
+    ctx = _ctx(presets.preset(FULL), n, seed=seed, env_offset=1000, n_env_global=5000)
+    try:
+        out = torch.empty(n, 4, dtype=torch.int32, device="cuda")
+        for dom, ch, blk in [(0, 0x01, 0), (7, 0x02, 3), (123456, 0x08, 1), (2, 0x101, 63), (0xFFFFFFFF, 0x10C, 5)]:
+            dr.dr_debug_philox(dom, ch, blk, out)
+            torch.cuda.synchronize()
+            g = out.cpu().numpy().view(np.uint32)
+            for e in range(0, n, 16):
+                ref = O.philox((1000 + e, dom, ch, blk), (seed & 0xFFFFFFFF, seed >> 32))
+                assert tuple(int(x) for x in g[e]) == ref, (dom, ch, blk, e)
+    finally:
+        ctx.close()
+
+
+def test_reset_records_and_phys(torch_cuda):
+    """Episode-0 records + physical parameters for 2000 envs (all layers, PHYS on)."""
+    torch = torch_cuda
+    P = presets.preset(FULL)
+    n = 2000
+    ctx = _ctx(P, n)
+    orc = _oracle(P, np.arange(n))
+    try:
+        compare_records(ctx.export(), [orc.env(i) for i in range(n)], phys_g=ctx.phys())
+        # masked reset: episode counters + resampled records only where masked
+        m = (np.arange(n) % 7 == 3).astype(np.uint8)
+        ctx.reset(torch.from_numpy(m).cuda())
+        orc.reset(m)
+        torch.cuda.synchronize()
+        G = ctx.export()
+        compare_records(G, [orc.env(i) for i in range(n)], phys_g=ctx.phys())
+        assert (G["episode"] == m).all()
+    finally:
+        ctx.close()
+
+
+def test_config1_free_running(torch_cuda):
+    """BASELINE config 1: 4 envs x 50 steps, all layers, fixed seed; every output, state and
+    stats slot each step (M1 free-running), with resets mid-run."""
+    r = {20: np.array([0, 1, 0, 0], np.uint8), 35: np.ones(4, np.uint8)}
+    k = run_pair(torch_cuda, FULL, 4, 50, n_frames=50, resets=r)
+    assert k.events == 0
+
+
+@pytest.mark.parametrize("mask", [0, TIMING, ACT_NOISE, DELAY, BACKLASH | TIMING, OBS_NOISE, DROPOUT,
+                                  OCCLUSION, FORCE, PHYS, DROPOUT | OCCLUSION | OBS_NOISE, CFG2,
+                                  FULL & ~TIMING, FULL & ~PHYS])
+def test_layer_subsets(torch_cuda, mask):
+    run_pair(torch_cuda, mask, 200, 25, n_frames=25, resets={12: (np.arange(200) % 5 == 0).astype(np.uint8)})
+
+
+@pytest.mark.parametrize("n", [1, 3, 127, 129, 1000])
+def test_ragged_sizes(torch_cuda, n):
+    """Tile tails (TILE = 128), single env, odd counts: scalar staging paths."""
+    run_pair(torch_cuda, FULL, n, 12, n_frames=12, resets={6: (np.arange(n) % 2 == 0).astype(np.uint8)})
+
+
+def test_config2_cfg2_4096(torch_cuda):
+    """BASELINE config 2 shape (4,096 envs, backlash + action/obs noise): 100 steps on all envs,
+    then 1,000 steps on a 64-env sample (the full run length), knife-edge aware."""
+    k = run_pair(torch_cuda, CFG2, 4096, 100, n_frames=16, state_every=10)
+    print("config2 knife-edges (100 steps x 4096 envs):", k.events, "excused mismatches:", k.excused_mismatches)
+    rng = np.random.default_rng(2)
+    sample = np.sort(rng.choice(4096, 64, replace=False))
+    k = run_pair(torch_cuda, CFG2, 4096, 1000, n_frames=16, sample=sample, state_every=50)
+    print("config2 knife-edges (1000 steps x 64 envs):", k.events)
+
+
+def test_config3_full_65536_sampled(torch_cuda):
+    """BASELINE config 3 (65,536 envs, full pipeline incl. dropout/occlusion hold and forces) in
+    the launch configuration bench.py times, compared on 256 sampled envs, with 10 % Bernoulli
+    resets every 10 steps."""
+    n = 65536
+    rng = np.random.default_rng(3)
+    sample = np.sort(np.concatenate([[0, 1, 127, 128, n - 1], rng.choice(n, 251, replace=False)]))
+    resets = {t: gen.reset_mask_bernoulli(rng, n, 0.1) for t in (10, 20)}
+    run_pair(torch_cuda, FULL, n, 30, n_frames=8, sample=sample, resets=resets, state_every=10)
+
+
+def test_config5_reset_stress_sampled(torch_cuda):
+    """BASELINE config 5 pattern (env e resets when (e + t) mod 10 == 0) at 262,144 envs,
+    sampled comparison of records and outputs."""
+    n = 1 << 18
+    rng = np.random.default_rng(5)
+    sample = np.sort(rng.choice(n, 128, replace=False))
+    resets = {t: gen.reset_mask_ring(n, t) for t in range(1, 6)}
+    run_pair(torch_cuda, FULL, n, 6, n_frames=4, sample=sample, resets=resets, state_every=1)
+
+
+def _run_outputs(torch, P, n, T, seed=SEED, env_offset=0, n_env_global=0, rows=None, resets=None, graph=False):
+    acts, obs = gen.frames(n_env_global or n, 6)
+    lo = env_offset
+    A = torch.from_numpy(acts[:, lo:lo + n].copy()).cuda()
+    O = torch.from_numpy(obs[:, lo:lo + n].copy()).cuda()
+    ctx = _ctx(P, n, seed, env_offset=env_offset, n_env_global=n_env_global)
+    outs = []
+    try:
+        for t in range(T):
+            if resets and t in resets:
+                ctx.reset(torch.from_numpy(resets[t][lo:lo + n].copy()).cuda())
+            ctx.step(A[t % 6], O[t % 6])
+            outs.append([x.clone() for x in (ctx.out_actions, ctx.out_obs, ctx.out_dt, ctx.out_force)])
+        torch.cuda.synchronize()
+        st = ctx.last_stats()
+        return [[x.cpu().numpy() for x in o] for o in outs], st
+    finally:
+        ctx.close()
+
+
+def test_determinism_and_shard_invariance(torch_cuda):
+    """Same seed -> bitwise-identical outputs and stats; an env's outputs depend only
+    on its global id, so a 2-way shard (env_offset) reproduces the single-GPU run bit for bit."""
+    torch = torch_cuda
+    P = presets.preset(FULL)
+    n = 1024
+    res = {4: (np.arange(n) % 3 == 0).astype(np.uint8)}
+    a, sa = _run_outputs(torch, P, n, 8, resets=res)
+    b, sb = _run_outputs(torch, P, n, 8, resets=res)
+    for x, y in zip(a, b):
+        for u, v in zip(x, y):
+            assert np.array_equal(u, v)
+    assert np.array_equal(sa, sb)
+    h0, _ = _run_outputs(torch, P, n // 2, 8, env_offset=0, n_env_global=n, resets=res)
+    h1, _ = _run_outputs(torch, P, n // 2, 8, env_offset=n // 2, n_env_global=n, resets=res)
+    for x, y0, y1 in zip(a, h0, h1):
+        for u, v0, v1 in zip(x, y0, y1):
+            assert np.array_equal(u, np.concatenate([v0, v1]))
+
+
+def test_export_import_resume(torch_cuda):
+    """Checkpoint/resume: export at step 10, import into a fresh context, continue -> identical
+    to the uninterrupted run (counter-based RNG has no hidden state)."""
+    torch = torch_cuda
+    from paper_1906_11633_b200 import dr
+    P = presets.preset(FULL)
+    n = 300
+    acts, obs = gen.frames(n, 20)
+    A, O = torch.from_numpy(acts).cuda(), torch.from_numpy(obs).cuda()
+    ctx = _ctx(P, n)
+    ref = []
+    for t in range(20):
+        if t == 10:
+            snap = dr.dr_state_export()
+            tsnap = dr.dr_step_index()
+        ctx.step(A[t], O[t])
+        if t >= 10:
+            ref.append([x.cpu().numpy() for x in (ctx.out_actions, ctx.out_obs, ctx.out_dt, ctx.out_force)])
+    ctx.close()
+    ctx = _ctx(P, n)
+    dr.dr_state_import(snap)
+    dr.dr_set_step_index(tsnap)
+    for t in range(10, 20):
+        ctx.step(A[t], O[t])
+        got = [x.cpu().numpy() for x in (ctx.out_actions, ctx.out_obs, ctx.out_dt, ctx.out_force)]
+        for u, v in zip(got, ref[t - 10]):
+            assert np.array_equal(u, v)
+    ctx.close()
+
+
+def test_cuda_graph_replay_advances_step(torch_cuda):
+    """A CUDA graph of dr_step calls replays with a device-resident step counter: two replays of
+    a 4-step graph equal 8 eager steps."""
+    torch = torch_cuda
+    from paper_1906_11633_b200 import dr
+    P = presets.preset(FULL)
+    n = 512
+    acts, obs = gen.frames(n, 4)
+    A, O = torch.from_numpy(acts).cuda(), torch.from_numpy(obs).cuda()
+    eager = []
+    ctx = _ctx(P, n)
+    for t in range(8):
+        ctx.step(A[t % 4], O[t % 4])
+        eager.append(ctx.out_obs.cpu().numpy())
+    ctx.close()
+    ctx = _ctx(P, n)
+    s = torch.cuda.Stream()
+    s.wait_stream(torch.cuda.current_stream())
+    g = torch.cuda.CUDAGraph()
+    outs = [torch.empty_like(ctx.out_obs) for _ in range(4)]
+    with torch.cuda.stream(s):
+        dr.dr_set_stream(s.cuda_stream)
+        torch.cuda.synchronize()
+        with torch.cuda.graph(g, stream=s):
+            for t in range(4):
+                dr.dr_step(A[t], O[t], ctx.out_actions, outs[t], ctx.out_dt, ctx.out_force)
+    for rep in range(2):
+        g.replay()
+        torch.cuda.synchronize()
+        for t in range(4):
+            assert np.array_equal(outs[t].cpu().numpy(), eager[4 * rep + t]), (rep, t)
+    ctx.close()
+
+
+def test_workspace_adoption_and_host_path(torch_cuda):
+    """A caller-owned (torch) workspace and the host-buffer dr_step_host path give the same
+    bits as the default device path."""
+    torch = torch_cuda
+    from paper_1906_11633_b200 import dr
+    P = presets.preset(FULL)
+    n = 777
+    acts, obs = gen.frames(n, 3)
+    A, O = torch.from_numpy(acts).cuda(), torch.from_numpy(obs).cuda()
+    ref = []
+    ctx = _ctx(P, n)
+    for t in range(3):
+        ctx.step(A[t], O[t])
+        ref.append([x.cpu().numpy() for x in (ctx.out_actions, ctx.out_obs, ctx.out_dt, ctx.out_force)])
+    ctx.close()
+    ctx = _ctx(P, n, workspace=True)
+    for t in range(3):
+        ctx.step(A[t], O[t])
+        got = [x.cpu().numpy() for x in (ctx.out_actions, ctx.out_obs, ctx.out_dt, ctx.out_force)]
+        for u, v in zip(got, ref[t]):
+            assert np.array_equal(u, v)
+    ctx.close()
+    ctx = _ctx(P, n)
+    ha = torch.from_numpy(acts).pin_memory()
+    ho = torch.from_numpy(obs).pin_memory()
+    outs = [torch.empty(n, c).pin_memory() for c in (20, 22, 10, 3)]
+    for t in range(3):
+        dr.dr_step_host(ha[t], ho[t], *outs)
+        dr.dr_synchronize()
+        for u, v in zip(outs, ref[t]):
+            assert np.array_equal(u.numpy(), v)
+    ctx.close()
+
+
+def test_value_view_isolation_and_invariants_1M(torch_cuda):
+    """Inputs are never written; GPU-only invariants over every env of a 1M-env
+    full-pipeline run: |a_out| <= 1, dt_k >= 8 ms, relative-goal w >= 0 and unit norm, slack in
+    [-1, 1], dropout timers <= 12."""
+    torch = torch_cuda
+    P = presets.preset(FULL)
+    n = 1 << 20
+    g = torch.Generator(device="cuda").manual_seed(1)
+    k = torch.randint(0, 11, (n, 20), device="cuda", generator=g)
+    A = (-1.0 + (2.0 * k + 1.0) / 11.0).float()
+    O = torch.randn(n, 26, device="cuda", generator=g) * 0.01
+    O[:, 18:22] /= O[:, 18:22].norm(dim=1, keepdim=True)
+    O[:, 22:26] /= O[:, 22:26].norm(dim=1, keepdim=True)
+    A0, O0 = A.clone(), O.clone()
+    ctx = _ctx(P, n)
+    try:
+        for t in range(4):
+            ctx.step(A, O)
+            torch.cuda.synchronize()
+            assert ctx.out_actions.abs().max().item() <= 1.0
+            assert ctx.out_dt.min().item() >= np.float32(0.008)
+            rel = ctx.out_obs[:, :4]
+            assert rel[:, 0].min().item() >= 0.0
+            assert (rel.norm(dim=1) - 1).abs().max().item() < 1e-5
+            assert torch.isfinite(ctx.out_obs).all() and torch.isfinite(ctx.out_force).all()
+        assert torch.equal(A, A0) and torch.equal(O, O0)
+        st = ctx.export(0, 4096)
+        assert np.abs(st["slack"]).max() <= 1.0
+        tim = np.stack([(st["flags"] >> (4 * i)) & 15 for i in range(5)])
+        assert tim.max() <= 12
+        s = ctx.last_stats()
+        assert s[0] == n
+    finally:
+        ctx.close()
