@@ -108,8 +108,13 @@ cudaError_t launch_import(const DevPtrs& p, const void* src, uint32_t lo, uint32
 cudaError_t launch_debug_philox(uint32_t n_env, uint32_t dom, uint32_t ch, uint32_t blk, uint32_t* out,
                                 cudaStream_t s);
 int step_max_ctas_per_sm(uint32_t layer_mask);
+void set_step_prefetch(int mode);
 int reset_max_ctas_per_sm();
 constexpr int RESET_THREADS = 256;
 constexpr int STEP_THREADS = TILE;
+#ifndef DR_STEP_MIN_CTAS
+#define DR_STEP_MIN_CTAS 4
+#endif
+constexpr int STEP_MIN_CTAS = DR_STEP_MIN_CTAS;   // __launch_bounds__ occupancy target (<= 128 regs at 4)
 
 }  // namespace dr

@@ -1,0 +1,545 @@
+// dr_step.cuh -- the fused per-env-step kernel, included by dr_kernels.cu.
+//
+// Mapping: persistent CTAs of TILE (=128) threads, one thread per env, static round-robin tiles.
+// Data movement per tile:
+//   * row-major I/O ([n][20] actions, [n][26] raw_obs in; [n][20]/[n][22]/[n][10]/[n][3] out) is
+//     staged through shared memory with 128-bit coalesced loads/stores; outputs are written in
+//     place over the input rows (out_actions over actions, out_obs + out_force over raw_obs).
+//   * the SoA record/state planes are read straight into registers (one 128-B line per warp per
+//     plane), batched per phase and prefetched one phase ahead, after a TMA bulk L2 prefetch
+//     (cp.async.bulk.prefetch.L2) of every plane chunk and input row range the tile needs, so the
+//     per-phase loads see L2 rather than HBM latency.  State makes one HBM round trip per step.
+//   * stats: per-thread accumulators, CTA reduction in shared memory, per-CTA partials reduced by
+//     the last CTA in a fixed order (deterministic fp64 sums).
+// (included inside namespace dr, after on<L>() and the B_* layer bits)
+#pragma once
+
+// Per-thread stats accumulators live in shared memory (not registers): counts [9][TILE] u32 and
+// fp64 moment sums [8][TILE], updated once per env.
+enum : int { K_DELAYED = 0, K_DROP_INIT, K_MASKED, K_OCCLUDED, K_HELD, K_TRIG, K_RAIL, K_ALPHA1, K_CLAMPS, K_COUNT };
+struct Acc {
+    uint32_t* n;   // s_accn + tid, stride TILE
+    double* m;     // s_accm + tid, stride TILE
+    __device__ __forceinline__ void add(int k, uint32_t v) { n[k * TILE] += v; }
+    __device__ __forceinline__ void addm(int k, double v) { m[k * TILE] += v; }
+};
+
+__device__ __forceinline__ void l2_prefetch(const void* ptr, uint32_t bytes) {
+    if (bytes >= 16u)
+        asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(ptr), "r"(bytes & ~15u) : "memory");
+}
+
+// Prefetch into L2 every plane chunk + input row range tile `tile` will read (layer-dependent).
+template <uint32_t L>
+__device__ __forceinline__ void prefetch_tile(const DevPtrs& p, const float* actions, const float* raw_obs,
+                                              uint32_t tile, uint32_t n_env) {
+    const uint32_t e0 = tile * TILE;
+    if (e0 >= n_env) return;
+    const uint32_t cnt = min((uint32_t)TILE, n_env - e0);
+    const size_t P = c_dc.pitch;
+    const uint32_t pb = (cnt * 4u + 15u) & ~15u;   // plane chunks stay inside the 64-padded pitch
+    for (int item = threadIdx.x; item < REC_STEP_PLANES + ST_PLANES + 2; item += blockDim.x) {
+        if (item < REC_STEP_PLANES) {
+            const int q = item;
+            bool need;
+            if (q == REC_DELAY) need = on<L>(B_DELAY);
+            else if (q == REC_INVLAM) need = on<L>(B_TIMING);
+            else if (q == REC_TFORCE || q == REC_MASS) need = on<L>(B_FORCE);
+            else if (q < REC_CACT) need = on<L>(B_BACKLASH);
+            else if (q < REC_OFFTIP) need = on<L>(B_ACT_NOISE);
+            else need = on<L>(B_OBS_NOISE);
+            if (need) l2_prefetch(p.rec + (size_t)q * P + e0, pb);
+        } else if (item < REC_STEP_PLANES + ST_PLANES) {
+            const int q = item - REC_STEP_PLANES;
+            bool need;
+            if (q < ST_SLACK) need = on<L>(B_DELAY);
+            else if (q < ST_LAST) need = on<L>(B_BACKLASH);
+            else if (q <= ST_FLAGS) need = on<L>(B_DROPOUT) || on<L>(B_OCCLUSION);
+            else need = on<L>(B_FORCE);
+            if (need) l2_prefetch(p.st + (size_t)q * P + e0, pb);
+        } else if (item == REC_STEP_PLANES + ST_PLANES) {
+            l2_prefetch(actions + (size_t)e0 * N_ACT, cnt * N_ACT * 4u);
+        } else {
+            l2_prefetch(raw_obs + (size_t)e0 * OBS_IN, cnt * OBS_IN * 4u);   // rounded down: stays in bounds
+        }
+    }
+}
+
+// Record loads use the coherent L2 path (ld.global.cg) on a non-restrict pointer on purpose: the
+// compiler may not hoist them above the state stores of earlier phases, which keeps each phase's
+// loads in one batch and the live register set small (the L2 prefetch hides their latency).
+__device__ __forceinline__ uint32_t ld_rec(const uint32_t* q) { return __ldcg(q); }
+
+// Per-actuator-block SoA values (4 actuators), loaded in one batch at the start of the block.
+struct ActBlock {
+    float prev[4], slack[4], cact[4], dneg[4], dpos[4];
+};
+
+template <uint32_t L>
+__device__ __forceinline__ void load_act_block(ActBlock& B, const uint32_t* R, const uint32_t* S,
+                                               size_t P, int b) {
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+        const int j = 4 * b + q;
+        if (on<L>(B_DELAY)) B.prev[q] = __uint_as_float(__ldcg(S + (ST_PREV + j) * P));
+        if (on<L>(B_BACKLASH)) {
+            B.slack[q] = __uint_as_float(__ldcg(S + (ST_SLACK + j) * P));
+            B.dneg[q] = __uint_as_float(ld_rec(R +(REC_DNEG + j) * P));
+            B.dpos[q] = __uint_as_float(ld_rec(R +(REC_DPOS + j) * P));
+        }
+        if (on<L>(B_ACT_NOISE)) B.cact[q] = __uint_as_float(ld_rec(R +(REC_CACT + j) * P));
+    }
+}
+
+struct ObsBlock {
+    float off[15], cobj[3], qc[4];
+};
+
+template <uint32_t L>
+__device__ __forceinline__ void load_obs_block(ObsBlock& B, const uint32_t* R, size_t P) {
+    if (on<L>(B_OBS_NOISE)) {
+#pragma unroll
+        for (int c = 0; c < 15; ++c) B.off[c] = __uint_as_float(ld_rec(R +(REC_OFFTIP + c) * P));
+#pragma unroll
+        for (int c = 0; c < 3; ++c) B.cobj[c] = __uint_as_float(ld_rec(R +(REC_COBJ + c) * P));
+#pragma unroll
+        for (int c = 0; c < 4; ++c) B.qc[c] = __uint_as_float(ld_rec(R +(REC_QC + c) * P));
+    }
+}
+
+template <uint32_t L>
+__device__ __forceinline__ void env_step(const DevPtrs& p, uint32_t e, uint32_t t, int tid, float* s_act,
+                                         float* s_obs, float* s_dt, const double* s_dec, Acc& acc) {
+    const size_t P = c_dc.pitch;
+    const uint32_t* R = p.rec + e;
+    uint32_t* S = p.st + e;
+    const uint32_t g = c_dc.env_offset + e;
+    constexpr bool kHold = (L == RUNTIME_MASK) || (L & (B_DROPOUT | B_OCCLUSION));
+    const bool hold_layers = on<L>(B_DROPOUT) || on<L>(B_OCCLUSION);
+
+    // ---- phase 0: scalar loads + actuator block 0 ----
+    const float il = on<L>(B_TIMING) ? __uint_as_float(ld_rec(R +REC_INVLAM * P)) : 0.f;
+    const uint32_t dbits = on<L>(B_DELAY) ? ld_rec(R +REC_DELAY * P) : 0u;
+    uint32_t flags = 0;
+    if (kHold && hold_layers) flags = __ldcg(S + ST_FLAGS * P);
+    uint32_t tf = 0, kf = 0;
+    float mass = 0.f;
+    if (on<L>(B_FORCE)) {
+        tf = ld_rec(R +REC_TFORCE * P);
+        kf = __ldcg(S + ST_KF * P);
+        mass = __uint_as_float(ld_rec(R +REC_MASS * P));
+    }
+    ActBlock cur;
+
+    // ---- 1. timing: 10 substeps of 8 ms + Exp(lambda); dt_env = sum [Q2] ----
+    float dt_env;
+    {
+        float d[N_SUB];
+        if (on<L>(B_TIMING)) {
+#pragma unroll
+            for (int b = 0; b < 3; ++b) {
+                const uint4 w = philox(g, t, CH_TIMING, b);
+#pragma unroll
+                for (int q = 0; q < 4; ++q)
+                    if (4 * b + q < N_SUB) d[4 * b + q] = c_dc.dt_base + (-logf(uni(word_of(w, q)))) * il;
+            }
+        } else {
+#pragma unroll
+            for (int k = 0; k < N_SUB; ++k) d[k] = c_dc.dt_base;
+        }
+        dt_env = d[0];
+#pragma unroll
+        for (int k = 1; k < N_SUB; ++k) dt_env = dt_env + d[k];
+        float2* d2 = reinterpret_cast<float2*>(s_dt + tid * N_SUB);
+#pragma unroll
+        for (int k = 0; k < N_SUB / 2; ++k) d2[k] = make_float2(d[2 * k], d[2 * k + 1]);
+        acc.addm(0, (double)dt_env);
+        acc.addm(1, (double)dt_env * (double)dt_env);
+    }
+
+    // ---- 2-4. actions: delay -> noise -> clamp -> backlash [Q1] ----
+    acc.add(K_DELAYED, __popc(dbits));
+    uint32_t n_clamp = 0, n_rail = 0, n_a1 = 0;
+    float s_da = 0.f, s_da2 = 0.f, s_bl = 0.f, s_zu2 = 0.f;
+    float4* a4p = reinterpret_cast<float4*>(s_act + tid * N_ACT);
+#pragma unroll
+    for (int b = 0; b < 5; ++b) {
+        load_act_block<L>(cur, R, S, P, b);   // one batch of 20 loads per block (L2-prefetched)
+        float zu[4], zm[4];
+        if (on<L>(B_ACT_NOISE)) {
+            normals4(philox(g, t, CH_ACT_UADD, b), zu);
+            normals4(philox(g, t, CH_ACT_MULT, b), zm);
+        }
+        const float4 a4 = a4p[b];
+        const float av[4] = {a4.x, a4.y, a4.z, a4.w};
+        float ov[4];
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+            const int j = 4 * b + q;
+            const float a = av[q];
+            float ad = a;
+            if (on<L>(B_DELAY)) {
+                // one-step delay of flagged actuators [Q9]
+                if ((dbits >> j) & 1u) ad = cur.prev[q];
+                S[(ST_PREV + j) * P] = __float_as_uint(a);
+            }
+            float an = ad;
+            if (on<L>(B_ACT_NOISE)) {
+                // Table action-noise [Q8]
+                an = ad + ad * (c_dc.sm * zm[q]);
+                an = an + c_dc.su * zu[q];
+                an = an + cur.cact[q];
+                n_clamp += (an > 1.f || an < -1.f) ? 1u : 0u;
+                an = fminf(fmaxf(an, -1.f), 1.f);
+                s_zu2 += zu[q] * zu[q];
+            }
+            const float da = an - ad;
+            s_da += da;
+            s_da2 += da * da;
+            float out = an;
+            if (on<L>(B_BACKLASH)) {
+                // backlash, verbatim [Q4], sgn(0) = 0 [Q3]
+                const float s = cur.slack[q];
+                const float sg = (an > 0.f) ? 1.f : ((an < 0.f) ? -1.f : 0.f);
+                const float d = (an > 0.f) ? cur.dpos[q] : ((an < 0.f) ? cur.dneg[q] : 0.f);
+                const float sp = fminf(fmaxf(s + an * d * dt_env, -1.f), 1.f);
+                const float ratio = fminf(fmaxf(fabsf(sg - s) / (fabsf(sp - s) + c_dc.eps), 0.f), 1.f);
+                const float al = 1.f - ratio;
+                out = al * an;
+                n_rail += (sg != 0.f && fabsf(sp) == 1.f && sp != s) ? 1u : 0u;
+                n_a1 += (al == 1.f) ? 1u : 0u;
+                S[(ST_SLACK + j) * P] = __float_as_uint(sp);
+            }
+            s_bl += fabsf(out - an);
+            ov[q] = out;
+        }
+        a4p[b] = make_float4(ov[0], ov[1], ov[2], ov[3]);
+    }
+    ObsBlock ob;
+    load_obs_block<L>(ob, R, P);
+    acc.add(K_CLAMPS, n_clamp);
+    acc.add(K_RAIL, n_rail);
+    acc.add(K_ALPHA1, n_a1);
+    acc.addm(2, (double)s_da);
+    acc.addm(3, (double)s_da2);
+    acc.addm(4, (double)s_bl);
+    acc.addm(5, (double)s_zu2);
+
+    // ---- 5-8. fingertip markers and object position ----
+    float* ro = s_obs + tid * OBS_IN;   // raw row in, out_obs (22) + out_force (3) written in place
+    float tip[15], obj[3], qo[4], goal[4];
+    {
+        const float2* r2 = reinterpret_cast<const float2*>(ro);
+#pragma unroll
+        for (int k = 0; k < 13; ++k) {
+            const float2 v = r2[k];
+            const float x[2] = {v.x, v.y};
+#pragma unroll
+            for (int h = 0; h < 2; ++h) {
+                const int c = 2 * k + h;
+                if (c < 15) tip[c] = x[h];
+                else if (c < 18) obj[c - 15] = x[h];
+                else if (c < 22) qo[c - 18] = x[h];
+                else goal[c - 22] = x[h];
+            }
+        }
+    }
+    uint32_t occ = 0;
+    if (on<L>(B_OCCLUSION) && c_dc.occl_on) {
+        // occlusion: another tip or the object centre strictly closer than r [Q13],
+        // exactly rounded fp64 ((dx*dx + dy*dy) + dz*dz), no FMA contraction
+        const double r2 = c_dc.occl_r2;
+#pragma unroll
+        for (int i = 0; i < N_TIPS; ++i) {
+#pragma unroll
+            for (int j = i + 1; j <= N_TIPS; ++j) {
+                const float* o = (j < N_TIPS) ? &tip[3 * j] : obj;
+                const double dx = __dsub_rn((double)tip[3 * i], (double)o[0]);
+                const double dy = __dsub_rn((double)tip[3 * i + 1], (double)o[1]);
+                const double dz = __dsub_rn((double)tip[3 * i + 2], (double)o[2]);
+                const double d2 = __dadd_rn(__dadd_rn(__dmul_rn(dx, dx), __dmul_rn(dy, dy)), __dmul_rn(dz, dz));
+                if (d2 < r2) occ |= (1u << i) | ((j < N_TIPS) ? (1u << j) : 0u);
+            }
+        }
+        acc.add(K_OCCLUDED, __popc(occ));
+    }
+    uint32_t masked = 0;
+    if (kHold && hold_layers) {
+        uint32_t nflags = 0, n_init = 0;
+        if (on<L>(B_DROPOUT)) {
+            // dropout: a 13-step mask starts with probability 1 - exp(-0.2 * 0.08) per step;
+            // a retrigger restarts it [Q11]
+            const uint4 w0 = philox(g, t, CH_DROPOUT, 0);
+            const uint32_t x4 = philox(g, t, CH_DROPOUT, 1).x;
+#pragma unroll
+            for (int i = 0; i < N_TIPS; ++i) {
+                const uint32_t x = (i < 4) ? word_of(w0, i) : x4;
+                uint32_t tm = (flags >> (4 * i)) & 0xFu;
+                if ((unsigned long long)x < c_dc.t_drop) { tm = c_dc.hold_steps; ++n_init; }
+                if (tm > 0u) { masked |= 1u << i; tm -= 1u; }
+                nflags |= tm << (4 * i);
+            }
+            acc.add(K_MASKED, __popc(masked));
+            acc.add(K_DROP_INIT, n_init);
+        }
+        S[ST_FLAGS * P] = nflags | HAS_LAST_BIT;
+    }
+    const uint32_t hold = (flags & HAS_LAST_BIT) ? (masked | occ) : 0u;
+    acc.add(K_HELD, __popc(hold));
+    // fingertips: + (correlated + misplacement offset) + 2 mm uncorrelated; held tips return
+    // their last available reading [Q12]
+    float s_zt = 0.f;
+    if (on<L>(B_OBS_NOISE)) {
+#pragma unroll
+        for (int b = 0; b < 4; ++b) {
+            float z[4];
+            normals4(philox(g, t, CH_TIP_NOISE, b), z);
+#pragma unroll
+            for (int q = 0; q < 4; ++q) {
+                const int n = 4 * b + q;
+                if (n < 15) {
+                    tip[n] = (tip[n] + ob.off[n]) + c_dc.tip_uncorr * z[q];
+                    s_zt += z[q] * z[q];
+                }
+            }
+        }
+    }
+    acc.addm(6, (double)s_zt);
+#pragma unroll
+    for (int i = 0; i < N_TIPS; ++i) {
+        if (kHold && hold_layers) {
+            if ((hold >> i) & 1u) {
+#pragma unroll
+                for (int c = 0; c < 3; ++c) tip[3 * i + c] = __uint_as_float(__ldcg(S + (ST_LAST + 3 * i + c) * P));
+            }
+#pragma unroll
+            for (int c = 0; c < 3; ++c) S[(ST_LAST + 3 * i + c) * P] = __float_as_uint(tip[3 * i + c]);
+        }
+    }
+    // object position: + 5 mm correlated + 1 mm uncorrelated
+    if (on<L>(B_OBS_NOISE)) {
+        float z[4];
+        normals4(philox(g, t, CH_OBJ_NOISE, 0), z);
+#pragma unroll
+        for (int c = 0; c < 3; ++c) obj[c] = (obj[c] + ob.cobj[c]) + c_dc.obj_uncorr * z[c];
+    }
+
+    // ---- 9. orientation noise -> noisy relative goal [Q15, Q16] ----
+    float rel[4];
+    {
+        float qn[4];
+        if (on<L>(B_OBS_NOISE)) {
+            float qu[4], tmp[4];
+            rotation(c_dc.rot_uncorr, philox(g, t, CH_ROT_NOISE, 0), qu);
+            qmul(ob.qc, qo, tmp);
+            qmul(qu, tmp, qn);
+        } else {
+#pragma unroll
+            for (int c = 0; c < 4; ++c) qn[c] = qo[c];
+        }
+        const float cj[4] = {qn[0], -qn[1], -qn[2], -qn[3]};
+        qmul(goal, cj, rel);
+        const float sgn = (rel[0] < 0.f) ? -1.f : 1.f;
+#pragma unroll
+        for (int c = 0; c < 4; ++c) rel[c] *= sgn;
+    }
+
+    // ---- 10. random force: replace on trigger, decay 0.99 per step in closed form
+    //           [Q17, Q18] ----
+    float f[3] = {0.f, 0.f, 0.f};
+    if (on<L>(B_FORCE)) {
+        const uint32_t x = philox(g, t, CH_FORCE, 0).x;
+        float ft[3];
+        if (x < tf) {
+            const uint4 w = philox(g, t, CH_FORCE, 1);
+            float z0, z1, z2, z3;
+            box_muller(w.x, w.y, z0, z1);
+            box_muller(w.z, w.w, z2, z3);
+            const float ms = mass * c_dc.accel_std;
+            ft[0] = ms * z0;
+            ft[1] = ms * z1;
+            ft[2] = ms * z2;
+#pragma unroll
+            for (int c = 0; c < 3; ++c) S[(ST_FTRIG + c) * P] = __float_as_uint(ft[c]);
+            kf = 0;
+            acc.add(K_TRIG, 1u);
+        } else {
+#pragma unroll
+            for (int c = 0; c < 3; ++c) ft[c] = __uint_as_float(__ldcg(S + (ST_FTRIG + c) * P));
+            kf = (kf < 65535u) ? kf + 1u : 65535u;
+        }
+        S[ST_KF * P] = kf;
+        const double dec = s_dec[kf & 255u] * s_dec[256u + (kf >> 8)];
+#pragma unroll
+        for (int c = 0; c < 3; ++c) f[c] = (float)((double)ft[c] * dec);
+    }
+    acc.addm(7, (double)f[0] * f[0] + (double)f[1] * f[1] + (double)f[2] * f[2]);
+
+    // ---- outputs in place over the raw row: [rel 4, tips 15, obj 3 | force 3] ----
+    {
+        float2* o2 = reinterpret_cast<float2*>(ro);
+        o2[0] = make_float2(rel[0], rel[1]);
+        o2[1] = make_float2(rel[2], rel[3]);
+#pragma unroll
+        for (int k = 0; k < 7; ++k) o2[2 + k] = make_float2(tip[2 * k], tip[2 * k + 1]);
+        o2[9] = make_float2(tip[14], obj[0]);
+        o2[10] = make_float2(obj[1], obj[2]);
+        o2[11] = make_float2(f[0], f[1]);
+        ro[24] = f[2];
+    }
+}
+
+// Prefetch policy (DR_PREFETCH env at dr_init): 0 = none, 1 = the current tile at its start,
+// 2 = the next tile at the start of the current one.
+template <uint32_t L, int PF>
+__global__ void __launch_bounds__(STEP_THREADS, STEP_MIN_CTAS) step_kernel(const DevPtrs p, const float* __restrict__ actions,
+                                                            const float* __restrict__ raw_obs,
+                                                            float* __restrict__ out_actions,
+                                                            float* __restrict__ out_obs,
+                                                            float* __restrict__ out_dt,
+                                                            float* __restrict__ out_force, uint32_t n_env) {
+    __shared__ __align__(16) float s_act[TILE * N_ACT];   // actions in, out_actions out (in place)
+    __shared__ __align__(16) float s_obs[TILE * OBS_IN];  // raw_obs in, out_obs + out_force out (stride 26)
+    __shared__ __align__(16) float s_dt[TILE * N_SUB];
+    __shared__ double s_dec[512];
+    __shared__ double s_accm[8 * TILE];
+    __shared__ uint32_t s_accn[K_COUNT * TILE];
+    __shared__ int s_last;
+
+    const int tid = threadIdx.x;
+    const uint32_t t = (uint32_t)p.ctl[0];
+    const uint32_t n_tiles = (n_env + TILE - 1) / TILE;
+    if (PF == 2) prefetch_tile<L>(p, actions, raw_obs, blockIdx.x, n_env);
+    if (on<L>(B_FORCE))
+        for (int i = tid; i < 512; i += STEP_THREADS) s_dec[i] = p.dec_tab[i];
+    Acc acc{s_accn + tid, s_accm + tid};
+#pragma unroll
+    for (int k = 0; k < K_COUNT; ++k) s_accn[k * TILE + tid] = 0u;
+#pragma unroll
+    for (int k = 0; k < 8; ++k) s_accm[k * TILE + tid] = 0.0;
+    uint32_t my_envs = 0;
+
+    for (uint32_t tile = blockIdx.x; tile < n_tiles; tile += gridDim.x) {
+        const uint32_t e0 = tile * TILE;
+        const uint32_t cnt = min((uint32_t)TILE, n_env - e0);
+        const bool full = cnt == (uint32_t)TILE;
+        if (PF == 1) prefetch_tile<L>(p, actions, raw_obs, tile, n_env);
+        if (PF == 2) prefetch_tile<L>(p, actions, raw_obs, tile + gridDim.x, n_env);
+        __syncthreads();   // previous tile's smem fully stored
+        // stage the row-major input tiles (128-bit, coalesced)
+        if (full) {
+            const float4* a4 = reinterpret_cast<const float4*>(actions + (size_t)e0 * N_ACT);
+            float4* s4 = reinterpret_cast<float4*>(s_act);
+#pragma unroll
+            for (int i = tid; i < TILE * N_ACT / 4; i += STEP_THREADS) s4[i] = __ldcs(a4 + i);
+            const float4* o4 = reinterpret_cast<const float4*>(raw_obs + (size_t)e0 * OBS_IN);
+            float4* so4 = reinterpret_cast<float4*>(s_obs);
+#pragma unroll
+            for (int i = tid; i < TILE * OBS_IN / 4; i += STEP_THREADS) so4[i] = __ldcs(o4 + i);
+        } else {
+            for (uint32_t i = tid; i < cnt * N_ACT; i += STEP_THREADS) s_act[i] = __ldcs(actions + (size_t)e0 * N_ACT + i);
+            for (uint32_t i = tid; i < cnt * OBS_IN; i += STEP_THREADS) s_obs[i] = __ldcs(raw_obs + (size_t)e0 * OBS_IN + i);
+        }
+        __syncthreads();
+        if ((uint32_t)tid < cnt) {
+            env_step<L>(p, e0 + tid, t, tid, s_act, s_obs, s_dt, s_dec, acc);
+            ++my_envs;
+        }
+        __syncthreads();
+        // store the output tiles (coalesced)
+        if (full) {
+            const float4* s4 = reinterpret_cast<const float4*>(s_act);
+            float4* a4 = reinterpret_cast<float4*>(out_actions + (size_t)e0 * N_ACT);
+#pragma unroll
+            for (int i = tid; i < TILE * N_ACT / 4; i += STEP_THREADS) __stcs(a4 + i, s4[i]);
+            const float4* d4s = reinterpret_cast<const float4*>(s_dt);
+            float4* d4 = reinterpret_cast<float4*>(out_dt + (size_t)e0 * N_SUB);
+#pragma unroll
+            for (int i = tid; i < TILE * N_SUB / 4; i += STEP_THREADS) __stcs(d4 + i, d4s[i]);
+            // out_obs rows (22 floats = 11 float2) read from stride-26 smem rows
+            float2* oo = reinterpret_cast<float2*>(out_obs + (size_t)e0 * OBS_OUT);
+            for (int i = tid; i < TILE * 11; i += STEP_THREADS) {
+                const int r = i / 11, k = i - r * 11;
+                __stcs(oo + i, reinterpret_cast<const float2*>(s_obs + r * OBS_IN)[k]);
+            }
+            float* of = out_force + (size_t)e0 * 3;
+            for (int i = tid; i < TILE * 3; i += STEP_THREADS) {
+                const int r = i / 3, k = i - r * 3;
+                __stcs(of + i, s_obs[r * OBS_IN + 22 + k]);
+            }
+        } else {
+            for (uint32_t i = tid; i < cnt * N_ACT; i += STEP_THREADS) out_actions[(size_t)e0 * N_ACT + i] = s_act[i];
+            for (uint32_t i = tid; i < cnt * N_SUB; i += STEP_THREADS) out_dt[(size_t)e0 * N_SUB + i] = s_dt[i];
+            for (uint32_t i = tid; i < cnt * OBS_OUT; i += STEP_THREADS) {
+                const uint32_t r = i / OBS_OUT, k = i - r * OBS_OUT;
+                out_obs[(size_t)e0 * OBS_OUT + i] = s_obs[r * OBS_IN + k];
+            }
+            for (uint32_t i = tid; i < cnt * 3; i += STEP_THREADS) {
+                const uint32_t r = i / 3, k = i - r * 3;
+                out_force[(size_t)e0 * 3 + i] = s_obs[r * OBS_IN + 22 + k];
+            }
+        }
+    }
+
+    // ---- 12. stats: CTA reduction in shared memory, last CTA reduces the partials ----
+    __syncthreads();
+    double* s_red = reinterpret_cast<double*>(s_obs);   // [N_STATS][STEP_THREADS / 32] (reuses s_obs)
+    const int lane = tid & 31, wid = tid >> 5;
+    {
+        auto red = [&](int i, double x) {
+#pragma unroll
+            for (int o = 16; o > 0; o >>= 1) x += __shfl_xor_sync(0xFFFFFFFFu, x, o);
+            if (lane == 0) s_red[i * (STEP_THREADS / 32) + wid] = x;
+        };
+        red(0, (double)my_envs);
+        const uint32_t* an = s_accn + tid;
+        red(1, (double)an[K_DELAYED * TILE]);
+        red(2, (double)an[K_DROP_INIT * TILE]);
+        red(3, (double)an[K_MASKED * TILE]);
+        red(4, (double)an[K_OCCLUDED * TILE]);
+        red(5, (double)an[K_HELD * TILE]);
+        red(6, (double)an[K_TRIG * TILE]);
+        red(7, (double)an[K_RAIL * TILE]);
+        red(8, (double)an[K_ALPHA1 * TILE]);
+        red(9, on<L>(B_BACKLASH) ? (double)my_envs * N_ACT - (double)an[K_ALPHA1 * TILE] : 0.0);
+        red(10, 0.0);
+        red(11, (double)an[K_CLAMPS * TILE]);
+        red(12, 0.0); red(13, 0.0); red(14, 0.0); red(15, 0.0);
+#pragma unroll 1
+        for (int i = 0; i < 8; ++i) red(16 + i, s_accm[i * TILE + tid]);
+    }
+    __syncthreads();
+    if (tid < N_STATS) {
+        double sum = 0.0;
+        if (tid < N_STATS - 8)
+#pragma unroll
+            for (int w = 0; w < STEP_THREADS / 32; ++w) sum += s_red[tid * (STEP_THREADS / 32) + w];
+        p.partials[(size_t)blockIdx.x * N_STATS + tid] = sum;
+    }
+    __threadfence();
+    __syncthreads();
+    if (tid == 0) {
+        const unsigned long long prev = atomicAdd(&p.ctl[1], 1ull);
+        s_last = (prev == (unsigned long long)gridDim.x - 1ull);
+    }
+    __syncthreads();
+    if (s_last) {
+        __threadfence();
+        const uint32_t slot = t & 1u;
+        for (int s = wid; s < N_STATS; s += STEP_THREADS / 32) {
+            double sum = 0.0;
+            for (uint32_t b = lane; b < gridDim.x; b += 32) sum += __ldcg(p.partials + (size_t)b * N_STATS + s);
+#pragma unroll
+            for (int o = 16; o > 0; o >>= 1) sum += __shfl_xor_sync(0xFFFFFFFFu, sum, o);
+            if (lane == 0) p.stats[slot * N_STATS + s] = sum;
+        }
+        __syncthreads();
+        if (tid == 0) {
+            const unsigned long long res = atomicExch(&p.ctl[2], 0ull);
+            p.stats[slot * N_STATS + 10] = (double)res;
+            p.ctl[1] = 0ull;
+            p.ctl[0] = (unsigned long long)t + 1ull;
+            __threadfence();
+        }
+    }
+}

@@ -79,8 +79,13 @@ class KnifeTracker:
         self.excused &= ~same
 
 
-def compare_records(G: dict, O: list, phys_g=None, strict_state=True, knife=None):
-    """Compare exported GPU per-env state G (dict of arrays) with oracle env dicts O."""
+HOLD_LAYERS = (1 << 5) | (1 << 6)   # DROPOUT | OCCLUSION
+
+
+def compare_records(G: dict, O: list, phys_g=None, strict_state=True, knife=None, mask=0x1FF):
+    """Compare exported GPU per-env state G (dict of arrays) with oracle env dicts O.
+    With neither DROPOUT nor OCCLUSION enabled the hold state (has_last, last readings) is
+    unobservable; the kernel does not move those bytes, so they are not compared."""
     n = len(O)
     get = lambda k: np.array([o[k] for o in O])  # noqa: E731
     for k in ("episode", "delay_bits", "p_index", "t_force", "k_f"):
@@ -90,7 +95,9 @@ def compare_records(G: dict, O: list, phys_g=None, strict_state=True, knife=None
     flags_o = np.zeros(n, dtype=np.int64)
     for i in range(5):
         flags_o |= tim[:, i].astype(np.int64) << (4 * i)
-    flags_o |= get("has_last").astype(np.int64) << 20
+    hold = bool(mask & HOLD_LAYERS)
+    if hold:
+        flags_o |= get("has_last").astype(np.int64) << 20
     assert np.array_equal(G["flags"].astype(np.int64), flags_o), "flags (dropout timers / has_last)"
     mass = get("mass")
     assert_close("lambda", G["lambda"], get("lambda"), 1e-30)
@@ -108,7 +115,8 @@ def compare_records(G: dict, O: list, phys_g=None, strict_state=True, knife=None
         assert_close("slack", G["slack"], slack_o, 1.0, tol=1e-5, mask=~knife.excused)
     elif strict_state:
         assert_close("slack", G["slack"], slack_o, 1.0)
-    assert_close("last", G["last"], get("last"), 0.1)
+    if hold:
+        assert_close("last", G["last"], get("last"), 0.1)
     assert_close("f_trig", G["f_trig"], get("f_trig"), np.maximum(mass[:, None], 1e-30))
     if phys_g is not None:
         ph = get("phys")[:, : phys_g.shape[1]]

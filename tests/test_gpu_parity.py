@@ -20,9 +20,23 @@ def torch_cuda():
     return torch
 
 
+@pytest.fixture(autouse=True)
+def _finalize_leaked_context():
+    """A failing test must not leave its context behind (dr_init would return DR_EALREADY)."""
+    yield
+    from paper_1906_11633_b200 import dr
+    dr.load().dr_finalize()   # DR_ENOTINIT when nothing leaked
+
+
 def _ctx(preset, n, seed=SEED, **kw):
     from paper_1906_11633_b200 import DRContext
     return DRContext(preset, n, seed, **kw)
+
+
+def _frames_cuda(torch, arr):
+    """One separately allocated (256-B aligned) device tensor per frame: dr_step requires
+    16-byte aligned rows."""
+    return [torch.from_numpy(np.ascontiguousarray(a)).cuda() for a in arr]
 
 
 def _oracle(preset, gids, seed=SEED):
@@ -36,8 +50,8 @@ def run_pair(torch, mask, n_env, T, n_frames=8, resets=None, sample=None, state_
     step.  `resets`: {t: uint8 mask [n_env]} applied before step t."""
     P = presets.preset(mask, **kw)
     acts, obs = gen.frames(n_env, n_frames, seed=frame_seed)
-    A = torch.from_numpy(acts).cuda()
-    O = torch.from_numpy(obs).cuda()
+    A = _frames_cuda(torch, acts)
+    O = _frames_cuda(torch, obs)
     gids = np.arange(n_env) if sample is None else np.asarray(sample)
     full = sample is None
     ctx = _ctx(P, n_env, seed)
@@ -46,7 +60,7 @@ def run_pair(torch, mask, n_env, T, n_frames=8, resets=None, sample=None, state_
     try:
         G = ctx.export()
         compare_records({k: v[gids] for k, v in G.items()}, [orc.env(i) for i in range(len(gids))],
-                        phys_g=ctx.phys()[gids])
+                        phys_g=ctx.phys()[gids], mask=mask)
         for t in range(T):
             if resets and t in resets:
                 m = resets[t]
@@ -71,7 +85,7 @@ def run_pair(torch, mask, n_env, T, n_frames=8, resets=None, sample=None, state_
             if state_every and (t % state_every == 0 or t == T - 1):
                 G = ctx.export()
                 compare_records({k: v[gids] for k, v in G.items()}, [orc.env(i) for i in range(len(gids))],
-                                knife=knife)
+                                knife=knife, mask=mask)
         return knife
     finally:
         ctx.close()
@@ -177,8 +191,8 @@ def test_config5_reset_stress_sampled(torch_cuda):
 def _run_outputs(torch, P, n, T, seed=SEED, env_offset=0, n_env_global=0, rows=None, resets=None, graph=False):
     acts, obs = gen.frames(n_env_global or n, 6)
     lo = env_offset
-    A = torch.from_numpy(acts[:, lo:lo + n].copy()).cuda()
-    O = torch.from_numpy(obs[:, lo:lo + n].copy()).cuda()
+    A = _frames_cuda(torch, acts[:, lo:lo + n])
+    O = _frames_cuda(torch, obs[:, lo:lo + n])
     ctx = _ctx(P, n, seed, env_offset=env_offset, n_env_global=n_env_global)
     outs = []
     try:
@@ -222,7 +236,7 @@ def test_export_import_resume(torch_cuda):
     P = presets.preset(FULL)
     n = 300
     acts, obs = gen.frames(n, 20)
-    A, O = torch.from_numpy(acts).cuda(), torch.from_numpy(obs).cuda()
+    A, O = _frames_cuda(torch, acts), _frames_cuda(torch, obs)
     ctx = _ctx(P, n)
     ref = []
     for t in range(20):
@@ -252,7 +266,7 @@ def test_cuda_graph_replay_advances_step(torch_cuda):
     P = presets.preset(FULL)
     n = 512
     acts, obs = gen.frames(n, 4)
-    A, O = torch.from_numpy(acts).cuda(), torch.from_numpy(obs).cuda()
+    A, O = _frames_cuda(torch, acts), _frames_cuda(torch, obs)
     eager = []
     ctx = _ctx(P, n)
     for t in range(8):
@@ -286,7 +300,7 @@ def test_workspace_adoption_and_host_path(torch_cuda):
     P = presets.preset(FULL)
     n = 777
     acts, obs = gen.frames(n, 3)
-    A, O = torch.from_numpy(acts).cuda(), torch.from_numpy(obs).cuda()
+    A, O = _frames_cuda(torch, acts), _frames_cuda(torch, obs)
     ref = []
     ctx = _ctx(P, n)
     for t in range(3):
@@ -301,8 +315,8 @@ def test_workspace_adoption_and_host_path(torch_cuda):
             assert np.array_equal(u, v)
     ctx.close()
     ctx = _ctx(P, n)
-    ha = torch.from_numpy(acts).pin_memory()
-    ho = torch.from_numpy(obs).pin_memory()
+    ha = [torch.from_numpy(a).pin_memory() for a in acts]
+    ho = [torch.from_numpy(o).pin_memory() for o in obs]
     outs = [torch.empty(n, c).pin_memory() for c in (20, 22, 10, 3)]
     for t in range(3):
         dr.dr_step_host(ha[t], ho[t], *outs)
