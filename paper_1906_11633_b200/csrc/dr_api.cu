@@ -311,6 +311,9 @@ int dr_init(const dr_params* params, int64_t n_env, uint64_t seed) {
     dc.base_to_tips = p.base_marker_to_tips ? 1 : 0;
     dc.occl_on = p.occl_dist > 0.0 ? 1 : 0;
     dc.occl_r2 = p.occl_dist * p.occl_dist;
+    dc.occl_r2_lo = (float)(dc.occl_r2 * (1.0 - 1e-5));
+    dc.occl_r2_hi = (float)(dc.occl_r2 * (1.0 + 1e-5));
+    dc.occl_exact_only = (dc.occl_r2 < 1e-30 || dc.occl_r2 > 1e30) ? 1u : 0u;
     dc.accel_std = (float)p.force_accel_std;
     dc.n_phys = p.n_phys;
     dc.mass_index = p.mass_index;

@@ -74,6 +74,8 @@ struct DevConst {
     int32_t base_to_tips;
     int32_t occl_on;
     double occl_r2;
+    float occl_r2_lo, occl_r2_hi;      // r^2 (1 -+ 1e-5): fp32 fast-path decision band
+    uint32_t occl_exact_only;          // r^2 outside the fp32 normal range: always exact fp64
     float accel_std;
     int32_t n_phys, mass_index;
     int32_t n_phys_u, n_phys_n;       // counts of uniform-kind / normal-kind params

@@ -266,9 +266,13 @@ static constexpr uint32_t MASK_CFG2 = B_TIMING | B_ACT_NOISE | B_BACKLASH | B_OB
 
 typedef void (*StepFn)(const DevPtrs, const float*, const float*, float*, float*, float*, float*, uint32_t);
 
-static int g_prefetch = 1;   // L2 bulk-prefetch policy of the step kernel (DR_PREFETCH=0/1/2)
+// L2 bulk-prefetch policy of the step kernel (DR_PREFETCH=0/1/2).  Measured on B200 at 1M envs
+// (profiles/round1_notes.md): 0 = none 2.48e9 env-steps/s, 1 = current tile 2.10e9,
+// 2 = next tile 1.92e9 -- the batched per-phase loads already keep enough lines in flight, and
+// the prefetched lines compete with the in-flight state for L2.
+static int g_prefetch = 0;
 
-void set_step_prefetch(int mode) { g_prefetch = (mode < 0 || mode > 2) ? 1 : mode; }
+void set_step_prefetch(int mode) { g_prefetch = (mode < 0 || mode > 2) ? 0 : mode; }
 
 template <int PF>
 static StepFn step_fn_pf(uint32_t m) {

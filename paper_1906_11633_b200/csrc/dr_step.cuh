@@ -141,7 +141,7 @@ __device__ __forceinline__ void env_step(const DevPtrs& p, uint32_t e, uint32_t 
                 const uint4 w = philox(g, t, CH_TIMING, b);
 #pragma unroll
                 for (int q = 0; q < 4; ++q)
-                    if (4 * b + q < N_SUB) d[4 * b + q] = c_dc.dt_base + (-logf(uni(word_of(w, q)))) * il;
+                    if (4 * b + q < N_SUB) d[4 * b + q] = c_dc.dt_base + (-ln_unit(uni(word_of(w, q)))) * il;
             }
         } else {
 #pragma unroll
@@ -162,8 +162,8 @@ __device__ __forceinline__ void env_step(const DevPtrs& p, uint32_t e, uint32_t 
     uint32_t n_clamp = 0, n_rail = 0, n_a1 = 0;
     float s_da = 0.f, s_da2 = 0.f, s_bl = 0.f, s_zu2 = 0.f;
     float4* a4p = reinterpret_cast<float4*>(s_act + tid * N_ACT);
-#pragma unroll
-    for (int b = 0; b < 5; ++b) {
+#pragma unroll 1
+    for (int b = 0; b < 5; ++b) {   // rolled: keeps the kernel inside the instruction cache
         load_act_block<L>(cur, R, S, P, b);   // one batch of 20 loads per block (L2-prefetched)
         float zu[4], zm[4];
         if (on<L>(B_ACT_NOISE)) {
@@ -246,19 +246,37 @@ __device__ __forceinline__ void env_step(const DevPtrs& p, uint32_t e, uint32_t 
     }
     uint32_t occ = 0;
     if (on<L>(B_OCCLUSION) && c_dc.occl_on) {
-        // occlusion: another tip or the object centre strictly closer than r [Q13],
-        // exactly rounded fp64 ((dx*dx + dy*dy) + dz*dz), no FMA contraction
-        const double r2 = c_dc.occl_r2;
+        // occlusion: another tip or the object centre strictly closer than r [Q13].
+        // The decision is the exactly rounded fp64 ((dx*dx + dy*dy) + dz*dz) < r^2 of the oracle.
+        // Fast path: every fp32 op is correctly rounded, so the fp32 sum is within a few ulp
+        // (relative) of the exact one; only pairs inside a 1e-5 relative band around r^2 (never,
+        // in practice) are decided by the exact fp64 evaluation.
+        const float lo = c_dc.occl_r2_lo, hi = c_dc.occl_r2_hi;
+        uint32_t amb = 0;   // ambiguous pairs, bit 6 i + (j - i - 1)
 #pragma unroll
         for (int i = 0; i < N_TIPS; ++i) {
 #pragma unroll
             for (int j = i + 1; j <= N_TIPS; ++j) {
                 const float* o = (j < N_TIPS) ? &tip[3 * j] : obj;
-                const double dx = __dsub_rn((double)tip[3 * i], (double)o[0]);
-                const double dy = __dsub_rn((double)tip[3 * i + 1], (double)o[1]);
-                const double dz = __dsub_rn((double)tip[3 * i + 2], (double)o[2]);
-                const double d2 = __dadd_rn(__dadd_rn(__dmul_rn(dx, dx), __dmul_rn(dy, dy)), __dmul_rn(dz, dz));
-                if (d2 < r2) occ |= (1u << i) | ((j < N_TIPS) ? (1u << j) : 0u);
+                const float dx = tip[3 * i] - o[0], dy = tip[3 * i + 1] - o[1], dz = tip[3 * i + 2] - o[2];
+                const float d2 = fmaf(dz, dz, fmaf(dy, dy, dx * dx));
+                const uint32_t pair = (1u << i) | ((j < N_TIPS) ? (1u << j) : 0u);
+                if (d2 < lo) occ |= pair;
+                else if (!(d2 > hi)) amb |= 1u << (6 * i + (j - i - 1));
+            }
+        }
+        if (amb | c_dc.occl_exact_only) {
+            const double r2 = c_dc.occl_r2;
+            for (int i = 0; i < N_TIPS; ++i) {
+                for (int j = i + 1; j <= N_TIPS; ++j) {
+                    if (!c_dc.occl_exact_only && !((amb >> (6 * i + (j - i - 1))) & 1u)) continue;
+                    const float* o = (j < N_TIPS) ? &tip[3 * j] : obj;
+                    const double dx = __dsub_rn((double)tip[3 * i], (double)o[0]);
+                    const double dy = __dsub_rn((double)tip[3 * i + 1], (double)o[1]);
+                    const double dz = __dsub_rn((double)tip[3 * i + 2], (double)o[2]);
+                    const double d2 = __dadd_rn(__dadd_rn(__dmul_rn(dx, dx), __dmul_rn(dy, dy)), __dmul_rn(dz, dz));
+                    if (d2 < r2) occ |= (1u << i) | ((j < N_TIPS) ? (1u << j) : 0u);
+                }
             }
         }
         acc.add(K_OCCLUDED, __popc(occ));
