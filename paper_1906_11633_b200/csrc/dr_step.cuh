@@ -19,9 +19,10 @@
 enum : int { K_DELAYED = 0, K_DROP_INIT, K_MASKED, K_OCCLUDED, K_HELD, K_TRIG, K_RAIL, K_ALPHA1, K_CLAMPS, K_COUNT };
 struct Acc {
     uint32_t* n;   // s_accn + tid, stride TILE
-    double* m;     // s_accm + tid, stride TILE
+    float* m;      // s_accm + tid, stride TILE (a thread sums only its ~n/(grid*TILE) envs in fp32;
+                   // CTA and grid sums are fp64)
     __device__ __forceinline__ void add(int k, uint32_t v) { n[k * TILE] += v; }
-    __device__ __forceinline__ void addm(int k, double v) { m[k * TILE] += v; }
+    __device__ __forceinline__ void addm(int k, float v) { m[k * TILE] += v; }
 };
 
 __device__ __forceinline__ void l2_prefetch(const void* ptr, uint32_t bytes) {
@@ -153,8 +154,8 @@ __device__ __forceinline__ void env_step(const DevPtrs& p, uint32_t e, uint32_t 
         float2* d2 = reinterpret_cast<float2*>(s_dt + tid * N_SUB);
 #pragma unroll
         for (int k = 0; k < N_SUB / 2; ++k) d2[k] = make_float2(d[2 * k], d[2 * k + 1]);
-        acc.addm(0, (double)dt_env);
-        acc.addm(1, (double)dt_env * (double)dt_env);
+        acc.addm(0, dt_env);
+        acc.addm(1, dt_env * dt_env);
     }
 
     // ---- 2-4. actions: delay -> noise -> clamp -> backlash [Q1] ----
@@ -220,27 +221,25 @@ __device__ __forceinline__ void env_step(const DevPtrs& p, uint32_t e, uint32_t 
     acc.add(K_CLAMPS, n_clamp);
     acc.add(K_RAIL, n_rail);
     acc.add(K_ALPHA1, n_a1);
-    acc.addm(2, (double)s_da);
-    acc.addm(3, (double)s_da2);
-    acc.addm(4, (double)s_bl);
-    acc.addm(5, (double)s_zu2);
+    acc.addm(2, s_da);
+    acc.addm(3, s_da2);
+    acc.addm(4, s_bl);
+    acc.addm(5, s_zu2);
 
     // ---- 5-8. fingertip markers and object position ----
     float* ro = s_obs + tid * OBS_IN;   // raw row in, out_obs (22) + out_force (3) written in place
-    float tip[15], obj[3], qo[4], goal[4];
+    float tip[15], obj[3];
     {
         const float2* r2 = reinterpret_cast<const float2*>(ro);
 #pragma unroll
-        for (int k = 0; k < 13; ++k) {
+        for (int k = 0; k < 9; ++k) {
             const float2 v = r2[k];
             const float x[2] = {v.x, v.y};
 #pragma unroll
             for (int h = 0; h < 2; ++h) {
                 const int c = 2 * k + h;
                 if (c < 15) tip[c] = x[h];
-                else if (c < 18) obj[c - 15] = x[h];
-                else if (c < 22) qo[c - 18] = x[h];
-                else goal[c - 22] = x[h];
+                else obj[c - 15] = x[h];
             }
         }
     }
@@ -322,7 +321,7 @@ __device__ __forceinline__ void env_step(const DevPtrs& p, uint32_t e, uint32_t 
             }
         }
     }
-    acc.addm(6, (double)s_zt);
+    acc.addm(6, s_zt);
 #pragma unroll
     for (int i = 0; i < N_TIPS; ++i) {
         if (kHold && hold_layers) {
@@ -345,6 +344,11 @@ __device__ __forceinline__ void env_step(const DevPtrs& p, uint32_t e, uint32_t 
     // ---- 9. orientation noise -> noisy relative goal [Q15, Q16] ----
     float rel[4];
     {
+        // raw q_obj = ro[18..21], goal = ro[22..25] (rows are 8-byte aligned: float2 reads)
+        const float2 qa = reinterpret_cast<const float2*>(ro + 18)[0], qb = reinterpret_cast<const float2*>(ro + 20)[0];
+        const float2 ga = reinterpret_cast<const float2*>(ro + 22)[0], gb = reinterpret_cast<const float2*>(ro + 24)[0];
+        const float qo[4] = {qa.x, qa.y, qb.x, qb.y};
+        const float goal[4] = {ga.x, ga.y, gb.x, gb.y};
         float qn[4];
         if (on<L>(B_OBS_NOISE)) {
             float qu[4], tmp[4];
@@ -387,11 +391,11 @@ __device__ __forceinline__ void env_step(const DevPtrs& p, uint32_t e, uint32_t 
             kf = (kf < 65535u) ? kf + 1u : 65535u;
         }
         S[ST_KF * P] = kf;
-        const double dec = s_dec[kf & 255u] * s_dec[256u + (kf >> 8)];
+        const double dec = __ldg(p.dec_tab + (kf & 255u)) * __ldg(p.dec_tab + 256u + (kf >> 8));   // L1-resident
 #pragma unroll
         for (int c = 0; c < 3; ++c) f[c] = (float)((double)ft[c] * dec);
     }
-    acc.addm(7, (double)f[0] * f[0] + (double)f[1] * f[1] + (double)f[2] * f[2]);
+    acc.addm(7, f[0] * f[0] + f[1] * f[1] + f[2] * f[2]);
 
     // ---- outputs in place over the raw row: [rel 4, tips 15, obj 3 | force 3] ----
     {
@@ -419,8 +423,7 @@ __global__ void __launch_bounds__(STEP_THREADS, STEP_MIN_CTAS) step_kernel(const
     __shared__ __align__(16) float s_act[TILE * N_ACT];   // actions in, out_actions out (in place)
     __shared__ __align__(16) float s_obs[TILE * OBS_IN];  // raw_obs in, out_obs + out_force out (stride 26)
     __shared__ __align__(16) float s_dt[TILE * N_SUB];
-    __shared__ double s_dec[512];
-    __shared__ double s_accm[8 * TILE];
+    __shared__ float s_accm[8 * TILE];
     __shared__ uint32_t s_accn[K_COUNT * TILE];
     __shared__ int s_last;
 
@@ -428,13 +431,12 @@ __global__ void __launch_bounds__(STEP_THREADS, STEP_MIN_CTAS) step_kernel(const
     const uint32_t t = (uint32_t)p.ctl[0];
     const uint32_t n_tiles = (n_env + TILE - 1) / TILE;
     if (PF == 2) prefetch_tile<L>(p, actions, raw_obs, blockIdx.x, n_env);
-    if (on<L>(B_FORCE))
-        for (int i = tid; i < 512; i += STEP_THREADS) s_dec[i] = p.dec_tab[i];
+    const double* s_dec = nullptr;   // decay table is read through L1 (__ldg) in env_step
     Acc acc{s_accn + tid, s_accm + tid};
 #pragma unroll
     for (int k = 0; k < K_COUNT; ++k) s_accn[k * TILE + tid] = 0u;
 #pragma unroll
-    for (int k = 0; k < 8; ++k) s_accm[k * TILE + tid] = 0.0;
+    for (int k = 0; k < 8; ++k) s_accm[k * TILE + tid] = 0.f;
     uint32_t my_envs = 0;
 
     for (uint32_t tile = blockIdx.x; tile < n_tiles; tile += gridDim.x) {
@@ -524,7 +526,7 @@ __global__ void __launch_bounds__(STEP_THREADS, STEP_MIN_CTAS) step_kernel(const
         red(11, (double)an[K_CLAMPS * TILE]);
         red(12, 0.0); red(13, 0.0); red(14, 0.0); red(15, 0.0);
 #pragma unroll 1
-        for (int i = 0; i < 8; ++i) red(16 + i, s_accm[i * TILE + tid]);
+        for (int i = 0; i < 8; ++i) red(16 + i, (double)s_accm[i * TILE + tid]);
     }
     __syncthreads();
     if (tid < N_STATS) {

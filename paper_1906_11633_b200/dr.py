@@ -13,6 +13,8 @@ import os
 
 PKG = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.path.join(PKG, "libdr.so")
+# A/B experiments load an alternative in-tree build (e.g. variants/libdr_m6.so); never a fallback.
+_LIB_OVERRIDE = os.environ.get("DR_LIB")
 
 ABI_VERSION = 1
 N_ACT, N_TIPS, N_SUB, MAX_PHYS, OBS_IN, OBS_OUT, N_STATS = 20, 5, 10, 256, 26, 22, 32
@@ -86,7 +88,7 @@ def load():
     except Exception as ex:  # nvcc missing on a box with a prebuilt .so is fine
         if not os.path.exists(LIB_PATH):
             raise RuntimeError(f"libdr.so missing and cannot be built: {ex}") from ex
-    L = C.CDLL(LIB_PATH)
+    L = C.CDLL(os.path.join(PKG, _LIB_OVERRIDE) if _LIB_OVERRIDE else LIB_PATH)
     vp, fp = C.c_void_p, C.c_void_p
     L.dr_params_default.argtypes = [C.POINTER(DrParams)]
     L.dr_init.argtypes = [C.POINTER(DrParams), C.c_int64, C.c_uint64]
