@@ -288,9 +288,17 @@ static StepFn step_fn(uint32_t layer_mask) {
     return step_fn_pf<1>(m);
 }
 
+// the phase ring is dynamic shared memory (static + dynamic > 48 KB needs the opt-in attribute)
+static StepFn step_fn_ready(uint32_t layer_mask) {
+    StepFn f = step_fn(layer_mask);
+    cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)STEP_DYN_SMEM);
+    return f;
+}
+
 int step_max_ctas_per_sm(uint32_t layer_mask) {
     int n = 0;
-    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, step_fn(layer_mask), STEP_THREADS, 0) != cudaSuccess) return 1;
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, step_fn_ready(layer_mask), STEP_THREADS, STEP_DYN_SMEM) != cudaSuccess)
+        return 1;
     return n > 0 ? n : 1;
 }
 
@@ -303,7 +311,7 @@ int reset_max_ctas_per_sm() {
 cudaError_t launch_step(const DevPtrs& p, uint32_t layer_mask, const float* actions, const float* raw_obs,
                         float* out_actions, float* out_obs, float* out_dt, float* out_force, uint32_t n_env,
                         int grid, cudaStream_t s) {
-    step_fn(layer_mask)<<<grid, STEP_THREADS, 0, s>>>(p, actions, raw_obs, out_actions, out_obs, out_dt,
+    step_fn(layer_mask)<<<grid, STEP_THREADS, STEP_DYN_SMEM, s>>>(p, actions, raw_obs, out_actions, out_obs, out_dt,
                                                       out_force, n_env);
     return cudaGetLastError();
 }

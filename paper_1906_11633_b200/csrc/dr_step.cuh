@@ -1,36 +1,50 @@
-// dr_step.cuh -- the fused per-env-step kernel, included by dr_kernels.cu.
+// dr_step.cuh -- the fused per-env-step kernel, included by dr_kernels.cu
+// inside namespace dr (after on<L>() and the B_* layer bits).
 //
 // Mapping: persistent CTAs of TILE (=128) threads, one thread per env, static round-robin tiles.
-// Data movement per tile:
-//   * row-major I/O ([n][20] actions, [n][26] raw_obs in; [n][20]/[n][22]/[n][10]/[n][3] out) is
-//     staged through shared memory with 128-bit coalesced loads/stores; outputs are written in
-//     place over the input rows (out_actions over actions, out_obs + out_force over raw_obs).
-//   * the SoA record/state planes are read straight into registers (one 128-B line per warp per
-//     plane), batched per phase and prefetched one phase ahead, after a TMA bulk L2 prefetch
-//     (cp.async.bulk.prefetch.L2) of every plane chunk and input row range the tile needs, so the
-//     per-phase loads see L2 rather than HBM latency.  State makes one HBM round trip per step.
-//   * stats: per-thread accumulators, CTA reduction in shared memory, per-CTA partials reduced by
-//     the last CTA in a fixed order (deterministic fp64 sums).
-// (included inside namespace dr, after on<L>() and the B_* layer bits)
+//
+// Data movement (every byte of state makes one HBM round trip per step):
+//   * Row-major I/O tiles ([n][20] actions, [n][26] raw_obs) are staged into shared memory with
+//     16-byte cp.async (LDGSTS, no register round trip); outputs are written in place over the
+//     input rows (out_actions over actions, out_obs + out_force over raw_obs) and stored with
+//     coalesced 128/64-bit stores.
+//   * The SoA record/state planes (one 128-B line per warp per plane) are software-pipelined
+//     through a per-thread two-slot shared-memory ring with 4-byte cp.async: while the thread
+//     computes phase k from one slot, the copies of phase k+1 are in flight into the other.
+//     Phases: S0 (scalars), A0..A4 (4 actuators each), OB (observation offsets).  In-flight data
+//     occupies shared memory, not registers, which is what lets the SM keep enough bytes in
+//     flight to approach the HBM roofline with a register-heavy (Philox + Box-Muller) thread.
+//   * Held fingertip readings ("last") are fetched with cp.async into the thread's raw-tip slots
+//     (already consumed) while the fingertip noise is computed.
+//   * stats: per-thread register accumulators -> CTA reduction in shared memory -> per-CTA
+//     partials reduced by the last CTA in a fixed order (deterministic fp64 sums).
 #pragma once
 
-// Per-thread stats accumulators live in shared memory (not registers): counts [9][TILE] u32 and
-// fp64 moment sums [8][TILE], updated once per env.
 enum : int { K_DELAYED = 0, K_DROP_INIT, K_MASKED, K_OCCLUDED, K_HELD, K_TRIG, K_RAIL, K_ALPHA1, K_CLAMPS, K_COUNT };
+
 struct Acc {
-    uint32_t* n;   // s_accn + tid, stride TILE
-    float* m;      // s_accm + tid, stride TILE (a thread sums only its ~n/(grid*TILE) envs in fp32;
-                   // CTA and grid sums are fp64)
-    __device__ __forceinline__ void add(int k, uint32_t v) { n[k * TILE] += v; }
-    __device__ __forceinline__ void addm(int k, float v) { m[k * TILE] += v; }
+    uint32_t n[K_COUNT];
+    float m[8];   // a thread sums only its ~n/(grid*TILE) envs in fp32; CTA and grid sums are fp64
 };
+
+// ---- cp.async (LDGSTS) helpers ------------------------------------------------------------
+__device__ __forceinline__ uint32_t smem_u32(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
+__device__ __forceinline__ void cp_async4(void* sdst, const void* gsrc) {
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"(smem_u32(sdst)), "l"(gsrc) : "memory");
+}
+__device__ __forceinline__ void cp_async16(void* sdst, const void* gsrc) {
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(smem_u32(sdst)), "l"(gsrc) : "memory");
+}
+__device__ __forceinline__ void cp_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+template <int N>
+__device__ __forceinline__ void cp_wait() { asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory"); }
 
 __device__ __forceinline__ void l2_prefetch(const void* ptr, uint32_t bytes) {
     if (bytes >= 16u)
         asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(ptr), "r"(bytes & ~15u) : "memory");
 }
 
-// Prefetch into L2 every plane chunk + input row range tile `tile` will read (layer-dependent).
+// Optional TMA bulk L2 prefetch of every plane chunk + input row range of a tile (DR_PREFETCH).
 template <uint32_t L>
 __device__ __forceinline__ void prefetch_tile(const DevPtrs& p, const float* actions, const float* raw_obs,
                                               uint32_t tile, uint32_t n_env) {
@@ -41,96 +55,92 @@ __device__ __forceinline__ void prefetch_tile(const DevPtrs& p, const float* act
     const uint32_t pb = (cnt * 4u + 15u) & ~15u;   // plane chunks stay inside the 64-padded pitch
     for (int item = threadIdx.x; item < REC_STEP_PLANES + ST_PLANES + 2; item += blockDim.x) {
         if (item < REC_STEP_PLANES) {
-            const int q = item;
-            bool need;
-            if (q == REC_DELAY) need = on<L>(B_DELAY);
-            else if (q == REC_INVLAM) need = on<L>(B_TIMING);
-            else if (q == REC_TFORCE || q == REC_MASS) need = on<L>(B_FORCE);
-            else if (q < REC_CACT) need = on<L>(B_BACKLASH);
-            else if (q < REC_OFFTIP) need = on<L>(B_ACT_NOISE);
-            else need = on<L>(B_OBS_NOISE);
-            if (need) l2_prefetch(p.rec + (size_t)q * P + e0, pb);
+            l2_prefetch(p.rec + (size_t)item * P + e0, pb);
         } else if (item < REC_STEP_PLANES + ST_PLANES) {
-            const int q = item - REC_STEP_PLANES;
-            bool need;
-            if (q < ST_SLACK) need = on<L>(B_DELAY);
-            else if (q < ST_LAST) need = on<L>(B_BACKLASH);
-            else if (q <= ST_FLAGS) need = on<L>(B_DROPOUT) || on<L>(B_OCCLUSION);
-            else need = on<L>(B_FORCE);
-            if (need) l2_prefetch(p.st + (size_t)q * P + e0, pb);
+            l2_prefetch(p.st + (size_t)(item - REC_STEP_PLANES) * P + e0, pb);
         } else if (item == REC_STEP_PLANES + ST_PLANES) {
             l2_prefetch(actions + (size_t)e0 * N_ACT, cnt * N_ACT * 4u);
         } else {
-            l2_prefetch(raw_obs + (size_t)e0 * OBS_IN, cnt * OBS_IN * 4u);   // rounded down: stays in bounds
+            l2_prefetch(raw_obs + (size_t)e0 * OBS_IN, cnt * OBS_IN * 4u);   // rounded down: in bounds
         }
     }
 }
 
-// Record loads use the coherent L2 path (ld.global.cg) on a non-restrict pointer on purpose: the
-// compiler may not hoist them above the state stores of earlier phases, which keeps each phase's
-// loads in one batch and the live register set small (the L2 prefetch hides their latency).
-__device__ __forceinline__ uint32_t ld_rec(const uint32_t* q) { return __ldcg(q); }
-
-// Per-actuator-block SoA values (4 actuators), loaded in one batch at the start of the block.
-struct ActBlock {
-    float prev[4], slack[4], cact[4], dneg[4], dpos[4];
-};
+// ---- phase ring ----------------------------------------------------------------------------
+// slot word w of thread tid lives at ring[(slot * RING_W + w) * TILE + tid]: the 32 lanes of a
+// warp touch 32 consecutive words (conflict-free LDS, coalesced LDGSTS).
+constexpr int RING_W = 22;
+constexpr size_t STEP_DYN_SMEM = 2 * RING_W * TILE * sizeof(uint32_t);
+enum : int { S0_INVLAM = 0, S0_DELAY, S0_FLAGS, S0_TFORCE, S0_MASS, S0_KF, S0_FTRIG };   // FTRIG: 3 words
 
 template <uint32_t L>
-__device__ __forceinline__ void load_act_block(ActBlock& B, const uint32_t* R, const uint32_t* S,
-                                               size_t P, int b) {
+__device__ __forceinline__ void issue_s0(uint32_t* slot, const uint32_t* R, const uint32_t* S, size_t P) {
+    if (on<L>(B_TIMING)) cp_async4(slot + S0_INVLAM * TILE, R + REC_INVLAM * P);
+    if (on<L>(B_DELAY)) cp_async4(slot + S0_DELAY * TILE, R + REC_DELAY * P);
+    if (on<L>(B_DROPOUT) || on<L>(B_OCCLUSION)) cp_async4(slot + S0_FLAGS * TILE, S + ST_FLAGS * P);
+    if (on<L>(B_FORCE)) {
+        cp_async4(slot + S0_TFORCE * TILE, R + REC_TFORCE * P);
+        cp_async4(slot + S0_MASS * TILE, R + REC_MASS * P);
+        cp_async4(slot + S0_KF * TILE, S + ST_KF * P);
+#pragma unroll
+        for (int c = 0; c < 3; ++c) cp_async4(slot + (S0_FTRIG + c) * TILE, S + (ST_FTRIG + c) * P);
+    }
+}
+
+// actuator block b: words [prev 4 | slack 4 | dneg 4 | dpos 4 | cact 4]
+template <uint32_t L>
+__device__ __forceinline__ void issue_act(uint32_t* slot, const uint32_t* R, const uint32_t* S, size_t P, int b) {
 #pragma unroll
     for (int q = 0; q < 4; ++q) {
         const int j = 4 * b + q;
-        if (on<L>(B_DELAY)) B.prev[q] = __uint_as_float(__ldcg(S + (ST_PREV + j) * P));
+        if (on<L>(B_DELAY)) cp_async4(slot + (0 + q) * TILE, S + (ST_PREV + j) * P);
         if (on<L>(B_BACKLASH)) {
-            B.slack[q] = __uint_as_float(__ldcg(S + (ST_SLACK + j) * P));
-            B.dneg[q] = __uint_as_float(ld_rec(R +(REC_DNEG + j) * P));
-            B.dpos[q] = __uint_as_float(ld_rec(R +(REC_DPOS + j) * P));
+            cp_async4(slot + (4 + q) * TILE, S + (ST_SLACK + j) * P);
+            cp_async4(slot + (8 + q) * TILE, R + (REC_DNEG + j) * P);
+            cp_async4(slot + (12 + q) * TILE, R + (REC_DPOS + j) * P);
         }
-        if (on<L>(B_ACT_NOISE)) B.cact[q] = __uint_as_float(ld_rec(R +(REC_CACT + j) * P));
+        if (on<L>(B_ACT_NOISE)) cp_async4(slot + (16 + q) * TILE, R + (REC_CACT + j) * P);
     }
 }
 
-struct ObsBlock {
-    float off[15], cobj[3], qc[4];
-};
-
+// observation offsets: words [offtip 15 | c_obj 3 | q_c 4]  (REC_OFFTIP..REC_QC are contiguous planes)
 template <uint32_t L>
-__device__ __forceinline__ void load_obs_block(ObsBlock& B, const uint32_t* R, size_t P) {
+__device__ __forceinline__ void issue_obs(uint32_t* slot, const uint32_t* R, size_t P) {
     if (on<L>(B_OBS_NOISE)) {
 #pragma unroll
-        for (int c = 0; c < 15; ++c) B.off[c] = __uint_as_float(ld_rec(R +(REC_OFFTIP + c) * P));
-#pragma unroll
-        for (int c = 0; c < 3; ++c) B.cobj[c] = __uint_as_float(ld_rec(R +(REC_COBJ + c) * P));
-#pragma unroll
-        for (int c = 0; c < 4; ++c) B.qc[c] = __uint_as_float(ld_rec(R +(REC_QC + c) * P));
+        for (int w = 0; w < 22; ++w) cp_async4(slot + w * TILE, R + (REC_OFFTIP + w) * P);
     }
 }
+
+__device__ __forceinline__ float ringf(const uint32_t* slot, int w) { return __uint_as_float(slot[w * TILE]); }
 
 template <uint32_t L>
 __device__ __forceinline__ void env_step(const DevPtrs& p, uint32_t e, uint32_t t, int tid, float* s_act,
-                                         float* s_obs, float* s_dt, const double* s_dec, Acc& acc) {
+                                         float* s_obs, float* s_dt, uint32_t* ring, Acc& acc) {
     const size_t P = c_dc.pitch;
     const uint32_t* R = p.rec + e;
     uint32_t* S = p.st + e;
     const uint32_t g = c_dc.env_offset + e;
     constexpr bool kHold = (L == RUNTIME_MASK) || (L & (B_DROPOUT | B_OCCLUSION));
     const bool hold_layers = on<L>(B_DROPOUT) || on<L>(B_OCCLUSION);
+    uint32_t* slot0 = ring + tid;
+    uint32_t* slot1 = ring + RING_W * TILE + tid;
 
-    // ---- phase 0: scalar loads + actuator block 0 ----
-    const float il = on<L>(B_TIMING) ? __uint_as_float(ld_rec(R +REC_INVLAM * P)) : 0.f;
-    const uint32_t dbits = on<L>(B_DELAY) ? ld_rec(R +REC_DELAY * P) : 0u;
-    uint32_t flags = 0;
-    if (kHold && hold_layers) flags = __ldcg(S + ST_FLAGS * P);
+    // ---- S0 (slot0) has landed (the tile loop waited for it); A0 is in flight into slot1 ----
+    const float il = on<L>(B_TIMING) ? ringf(slot0, S0_INVLAM) : 0.f;
+    const uint32_t dbits = on<L>(B_DELAY) ? slot0[S0_DELAY * TILE] : 0u;
+    const uint32_t flags = (kHold && hold_layers) ? slot0[S0_FLAGS * TILE] : 0u;
     uint32_t tf = 0, kf = 0;
-    float mass = 0.f;
+    float mass = 0.f, ft[3] = {0.f, 0.f, 0.f};
     if (on<L>(B_FORCE)) {
-        tf = ld_rec(R +REC_TFORCE * P);
-        kf = __ldcg(S + ST_KF * P);
-        mass = __uint_as_float(ld_rec(R +REC_MASS * P));
+        tf = slot0[S0_TFORCE * TILE];
+        mass = ringf(slot0, S0_MASS);
+        kf = slot0[S0_KF * TILE];
+#pragma unroll
+        for (int c = 0; c < 3; ++c) ft[c] = ringf(slot0, S0_FTRIG + c);
     }
-    ActBlock cur;
+    issue_act<L>(slot0, R, S, P, 1);   // A1 -> slot0
+    cp_commit();
 
     // ---- 1. timing: 10 substeps of 8 ms + Exp(lambda); dt_env = sum [Q2] ----
     float dt_env;
@@ -154,18 +164,32 @@ __device__ __forceinline__ void env_step(const DevPtrs& p, uint32_t e, uint32_t 
         float2* d2 = reinterpret_cast<float2*>(s_dt + tid * N_SUB);
 #pragma unroll
         for (int k = 0; k < N_SUB / 2; ++k) d2[k] = make_float2(d[2 * k], d[2 * k + 1]);
-        acc.addm(0, dt_env);
-        acc.addm(1, dt_env * dt_env);
+        acc.m[0] += dt_env;
+        acc.m[1] += dt_env * dt_env;
     }
 
     // ---- 2-4. actions: delay -> noise -> clamp -> backlash [Q1] ----
-    acc.add(K_DELAYED, __popc(dbits));
-    uint32_t n_clamp = 0, n_rail = 0, n_a1 = 0;
+    acc.n[K_DELAYED] += __popc(dbits);
     float s_da = 0.f, s_da2 = 0.f, s_bl = 0.f, s_zu2 = 0.f;
     float4* a4p = reinterpret_cast<float4*>(s_act + tid * N_ACT);
 #pragma unroll 1
     for (int b = 0; b < 5; ++b) {   // rolled: keeps the kernel inside the instruction cache
-        load_act_block<L>(cur, R, S, P, b);   // one batch of 20 loads per block (L2-prefetched)
+        cp_wait<1>();                // A_b has landed
+        uint32_t* sl = (b & 1) ? slot0 : slot1;
+        float prev[4], slack[4], dneg[4], dpos[4], cact[4];
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+            prev[q] = on<L>(B_DELAY) ? ringf(sl, q) : 0.f;
+            slack[q] = on<L>(B_BACKLASH) ? ringf(sl, 4 + q) : 0.f;
+            dneg[q] = on<L>(B_BACKLASH) ? ringf(sl, 8 + q) : 0.f;
+            dpos[q] = on<L>(B_BACKLASH) ? ringf(sl, 12 + q) : 0.f;
+            cact[q] = on<L>(B_ACT_NOISE) ? ringf(sl, 16 + q) : 0.f;
+        }
+        // refill the slot just consumed: A_{b+2}, then the observation offsets
+        if (b + 2 < 5) issue_act<L>(sl, R, S, P, b + 2);
+        else if (b + 2 == 5) issue_obs<L>(sl, R, P);
+        cp_commit();
+
         float zu[4], zm[4];
         if (on<L>(B_ACT_NOISE)) {
             normals4(philox(g, t, CH_ACT_UADD, b), zu);
@@ -181,7 +205,7 @@ __device__ __forceinline__ void env_step(const DevPtrs& p, uint32_t e, uint32_t 
             float ad = a;
             if (on<L>(B_DELAY)) {
                 // one-step delay of flagged actuators [Q9]
-                if ((dbits >> j) & 1u) ad = cur.prev[q];
+                if ((dbits >> j) & 1u) ad = prev[q];
                 S[(ST_PREV + j) * P] = __float_as_uint(a);
             }
             float an = ad;
@@ -189,8 +213,8 @@ __device__ __forceinline__ void env_step(const DevPtrs& p, uint32_t e, uint32_t 
                 // Table action-noise [Q8]
                 an = ad + ad * (c_dc.sm * zm[q]);
                 an = an + c_dc.su * zu[q];
-                an = an + cur.cact[q];
-                n_clamp += (an > 1.f || an < -1.f) ? 1u : 0u;
+                an = an + cact[q];
+                acc.n[K_CLAMPS] += (an > 1.f || an < -1.f) ? 1u : 0u;
                 an = fminf(fmaxf(an, -1.f), 1.f);
                 s_zu2 += zu[q] * zu[q];
             }
@@ -199,16 +223,21 @@ __device__ __forceinline__ void env_step(const DevPtrs& p, uint32_t e, uint32_t 
             s_da2 += da * da;
             float out = an;
             if (on<L>(B_BACKLASH)) {
-                // backlash, verbatim [Q4], sgn(0) = 0 [Q3]
-                const float s = cur.slack[q];
+                // backlash, verbatim [Q4], sgn(0) = 0 [Q3]:
+                // alpha = 1 - clamp(|sgn - s| / (|s' - s| + eps), 0, 1).  The ratio is >= 1 (alpha 0)
+                // unless s sits on the rail sgn already (num == 0: alpha 1) or s' lands on the
+                // rail within eps of it (num < den: the one case that needs the division).
+                const float s = slack[q];
                 const float sg = (an > 0.f) ? 1.f : ((an < 0.f) ? -1.f : 0.f);
-                const float d = (an > 0.f) ? cur.dpos[q] : ((an < 0.f) ? cur.dneg[q] : 0.f);
+                const float d = (an > 0.f) ? dpos[q] : ((an < 0.f) ? dneg[q] : 0.f);
                 const float sp = fminf(fmaxf(s + an * d * dt_env, -1.f), 1.f);
-                const float ratio = fminf(fmaxf(fabsf(sg - s) / (fabsf(sp - s) + c_dc.eps), 0.f), 1.f);
-                const float al = 1.f - ratio;
+                const float num = fabsf(sg - s), den = fabsf(sp - s) + c_dc.eps;
+                float al = 0.f;
+                if (num == 0.f) al = 1.f;
+                else if (num < den) al = 1.f - num / den;
                 out = al * an;
-                n_rail += (sg != 0.f && fabsf(sp) == 1.f && sp != s) ? 1u : 0u;
-                n_a1 += (al == 1.f) ? 1u : 0u;
+                acc.n[K_RAIL] += (sg != 0.f && fabsf(sp) == 1.f && sp != s) ? 1u : 0u;
+                acc.n[K_ALPHA1] += (al == 1.f) ? 1u : 0u;
                 S[(ST_SLACK + j) * P] = __float_as_uint(sp);
             }
             s_bl += fabsf(out - an);
@@ -216,18 +245,13 @@ __device__ __forceinline__ void env_step(const DevPtrs& p, uint32_t e, uint32_t 
         }
         a4p[b] = make_float4(ov[0], ov[1], ov[2], ov[3]);
     }
-    ObsBlock ob;
-    load_obs_block<L>(ob, R, P);
-    acc.add(K_CLAMPS, n_clamp);
-    acc.add(K_RAIL, n_rail);
-    acc.add(K_ALPHA1, n_a1);
-    acc.addm(2, s_da);
-    acc.addm(3, s_da2);
-    acc.addm(4, s_bl);
-    acc.addm(5, s_zu2);
+    acc.m[2] += s_da;
+    acc.m[3] += s_da2;
+    acc.m[4] += s_bl;
+    acc.m[5] += s_zu2;
 
     // ---- 5-8. fingertip markers and object position ----
-    float* ro = s_obs + tid * OBS_IN;   // raw row in, out_obs (22) + out_force (3) written in place
+    float* ro = s_obs + tid * OBS_IN;   // raw row in; out_obs (22) + out_force (3) written in place
     float tip[15], obj[3];
     {
         const float2* r2 = reinterpret_cast<const float2*>(ro);
@@ -278,11 +302,11 @@ __device__ __forceinline__ void env_step(const DevPtrs& p, uint32_t e, uint32_t 
                 }
             }
         }
-        acc.add(K_OCCLUDED, __popc(occ));
+        acc.n[K_OCCLUDED] += __popc(occ);
     }
     uint32_t masked = 0;
     if (kHold && hold_layers) {
-        uint32_t nflags = 0, n_init = 0;
+        uint32_t nflags = 0;
         if (on<L>(B_DROPOUT)) {
             // dropout: a 13-step mask starts with probability 1 - exp(-0.2 * 0.08) per step;
             // a retrigger restarts it [Q11]
@@ -292,19 +316,28 @@ __device__ __forceinline__ void env_step(const DevPtrs& p, uint32_t e, uint32_t 
             for (int i = 0; i < N_TIPS; ++i) {
                 const uint32_t x = (i < 4) ? word_of(w0, i) : x4;
                 uint32_t tm = (flags >> (4 * i)) & 0xFu;
-                if ((unsigned long long)x < c_dc.t_drop) { tm = c_dc.hold_steps; ++n_init; }
+                if ((unsigned long long)x < c_dc.t_drop) { tm = c_dc.hold_steps; acc.n[K_DROP_INIT] += 1; }
                 if (tm > 0u) { masked |= 1u << i; tm -= 1u; }
                 nflags |= tm << (4 * i);
             }
-            acc.add(K_MASKED, __popc(masked));
-            acc.add(K_DROP_INIT, n_init);
+            acc.n[K_MASKED] += __popc(masked);
         }
         S[ST_FLAGS * P] = nflags | HAS_LAST_BIT;
     }
     const uint32_t hold = (flags & HAS_LAST_BIT) ? (masked | occ) : 0u;
-    acc.add(K_HELD, __popc(hold));
-    // fingertips: + (correlated + misplacement offset) + 2 mm uncorrelated; held tips return
-    // their last available reading [Q12]
+    acc.n[K_HELD] += __popc(hold);
+    // held tips return their last available reading [Q12]: fetch it asynchronously
+    // into this thread's raw-tip slots (already consumed) while the noise below is computed.
+    if (kHold && hold) {
+#pragma unroll
+        for (int i = 0; i < N_TIPS; ++i)
+            if ((hold >> i) & 1u)
+#pragma unroll
+                for (int c = 0; c < 3; ++c) cp_async4(ro + 3 * i + c, S + (ST_LAST + 3 * i + c) * P);
+    }
+    cp_commit();
+    cp_wait<1>();   // the observation offsets (issued at b = 3) have landed in slot0
+    // fingertips: + (correlated + misplacement offset) + 2 mm uncorrelated
     float s_zt = 0.f;
     if (on<L>(B_OBS_NOISE)) {
 #pragma unroll
@@ -315,22 +348,24 @@ __device__ __forceinline__ void env_step(const DevPtrs& p, uint32_t e, uint32_t 
             for (int q = 0; q < 4; ++q) {
                 const int n = 4 * b + q;
                 if (n < 15) {
-                    tip[n] = (tip[n] + ob.off[n]) + c_dc.tip_uncorr * z[q];
+                    tip[n] = (tip[n] + ringf(slot0, n)) + c_dc.tip_uncorr * z[q];
                     s_zt += z[q] * z[q];
                 }
             }
         }
     }
-    acc.addm(6, s_zt);
+    acc.m[6] += s_zt;
+    cp_wait<0>();   // held readings
+    if (kHold && hold_layers) {
 #pragma unroll
-    for (int i = 0; i < N_TIPS; ++i) {
-        if (kHold && hold_layers) {
+        for (int i = 0; i < N_TIPS; ++i) {
             if ((hold >> i) & 1u) {
 #pragma unroll
-                for (int c = 0; c < 3; ++c) tip[3 * i + c] = __uint_as_float(__ldcg(S + (ST_LAST + 3 * i + c) * P));
-            }
+                for (int c = 0; c < 3; ++c) tip[3 * i + c] = ro[3 * i + c];   // unchanged: no store
+            } else {
 #pragma unroll
-            for (int c = 0; c < 3; ++c) S[(ST_LAST + 3 * i + c) * P] = __float_as_uint(tip[3 * i + c]);
+                for (int c = 0; c < 3; ++c) S[(ST_LAST + 3 * i + c) * P] = __float_as_uint(tip[3 * i + c]);
+            }
         }
     }
     // object position: + 5 mm correlated + 1 mm uncorrelated
@@ -338,7 +373,7 @@ __device__ __forceinline__ void env_step(const DevPtrs& p, uint32_t e, uint32_t 
         float z[4];
         normals4(philox(g, t, CH_OBJ_NOISE, 0), z);
 #pragma unroll
-        for (int c = 0; c < 3; ++c) obj[c] = (obj[c] + ob.cobj[c]) + c_dc.obj_uncorr * z[c];
+        for (int c = 0; c < 3; ++c) obj[c] = (obj[c] + ringf(slot0, 15 + c)) + c_dc.obj_uncorr * z[c];
     }
 
     // ---- 9. orientation noise -> noisy relative goal [Q15, Q16] ----
@@ -352,8 +387,9 @@ __device__ __forceinline__ void env_step(const DevPtrs& p, uint32_t e, uint32_t 
         float qn[4];
         if (on<L>(B_OBS_NOISE)) {
             float qu[4], tmp[4];
+            const float qc[4] = {ringf(slot0, 18), ringf(slot0, 19), ringf(slot0, 20), ringf(slot0, 21)};
             rotation(c_dc.rot_uncorr, philox(g, t, CH_ROT_NOISE, 0), qu);
-            qmul(ob.qc, qo, tmp);
+            qmul(qc, qo, tmp);
             qmul(qu, tmp, qn);
         } else {
 #pragma unroll
@@ -371,7 +407,6 @@ __device__ __forceinline__ void env_step(const DevPtrs& p, uint32_t e, uint32_t 
     float f[3] = {0.f, 0.f, 0.f};
     if (on<L>(B_FORCE)) {
         const uint32_t x = philox(g, t, CH_FORCE, 0).x;
-        float ft[3];
         if (x < tf) {
             const uint4 w = philox(g, t, CH_FORCE, 1);
             float z0, z1, z2, z3;
@@ -384,10 +419,8 @@ __device__ __forceinline__ void env_step(const DevPtrs& p, uint32_t e, uint32_t 
 #pragma unroll
             for (int c = 0; c < 3; ++c) S[(ST_FTRIG + c) * P] = __float_as_uint(ft[c]);
             kf = 0;
-            acc.add(K_TRIG, 1u);
+            acc.n[K_TRIG] += 1;
         } else {
-#pragma unroll
-            for (int c = 0; c < 3; ++c) ft[c] = __uint_as_float(__ldcg(S + (ST_FTRIG + c) * P));
             kf = (kf < 65535u) ? kf + 1u : 65535u;
         }
         S[ST_KF * P] = kf;
@@ -395,7 +428,7 @@ __device__ __forceinline__ void env_step(const DevPtrs& p, uint32_t e, uint32_t 
 #pragma unroll
         for (int c = 0; c < 3; ++c) f[c] = (float)((double)ft[c] * dec);
     }
-    acc.addm(7, f[0] * f[0] + f[1] * f[1] + f[2] * f[2]);
+    acc.m[7] += f[0] * f[0] + f[1] * f[1] + f[2] * f[2];
 
     // ---- outputs in place over the raw row: [rel 4, tips 15, obj 3 | force 3] ----
     {
@@ -412,31 +445,28 @@ __device__ __forceinline__ void env_step(const DevPtrs& p, uint32_t e, uint32_t 
 }
 
 // Prefetch policy (DR_PREFETCH env at dr_init): 0 = none, 1 = the current tile at its start,
-// 2 = the next tile at the start of the current one.
+// 2 = the next tile at the start of the current one (TMA bulk L2 prefetch; A/B experiments).
 template <uint32_t L, int PF>
-__global__ void __launch_bounds__(STEP_THREADS, STEP_MIN_CTAS) step_kernel(const DevPtrs p, const float* __restrict__ actions,
-                                                            const float* __restrict__ raw_obs,
-                                                            float* __restrict__ out_actions,
-                                                            float* __restrict__ out_obs,
-                                                            float* __restrict__ out_dt,
-                                                            float* __restrict__ out_force, uint32_t n_env) {
+__global__ void __launch_bounds__(STEP_THREADS, STEP_MIN_CTAS)
+    step_kernel(const DevPtrs p, const float* __restrict__ actions, const float* __restrict__ raw_obs,
+                float* __restrict__ out_actions, float* __restrict__ out_obs, float* __restrict__ out_dt,
+                float* __restrict__ out_force, uint32_t n_env) {
     __shared__ __align__(16) float s_act[TILE * N_ACT];   // actions in, out_actions out (in place)
     __shared__ __align__(16) float s_obs[TILE * OBS_IN];  // raw_obs in, out_obs + out_force out (stride 26)
     __shared__ __align__(16) float s_dt[TILE * N_SUB];
-    __shared__ float s_accm[8 * TILE];
-    __shared__ uint32_t s_accn[K_COUNT * TILE];
+    extern __shared__ __align__(16) uint32_t s_ring[];   // [2][RING_W][TILE] (dynamic: > 48 KB total)
     __shared__ int s_last;
 
     const int tid = threadIdx.x;
     const uint32_t t = (uint32_t)p.ctl[0];
     const uint32_t n_tiles = (n_env + TILE - 1) / TILE;
+    const size_t P = c_dc.pitch;
     if (PF == 2) prefetch_tile<L>(p, actions, raw_obs, blockIdx.x, n_env);
-    const double* s_dec = nullptr;   // decay table is read through L1 (__ldg) in env_step
-    Acc acc{s_accn + tid, s_accm + tid};
+    Acc acc;
 #pragma unroll
-    for (int k = 0; k < K_COUNT; ++k) s_accn[k * TILE + tid] = 0u;
+    for (int k = 0; k < K_COUNT; ++k) acc.n[k] = 0u;
 #pragma unroll
-    for (int k = 0; k < 8; ++k) s_accm[k * TILE + tid] = 0.f;
+    for (int k = 0; k < 8; ++k) acc.m[k] = 0.f;
     uint32_t my_envs = 0;
 
     for (uint32_t tile = blockIdx.x; tile < n_tiles; tile += gridDim.x) {
@@ -446,25 +476,31 @@ __global__ void __launch_bounds__(STEP_THREADS, STEP_MIN_CTAS) step_kernel(const
         if (PF == 1) prefetch_tile<L>(p, actions, raw_obs, tile, n_env);
         if (PF == 2) prefetch_tile<L>(p, actions, raw_obs, tile + gridDim.x, n_env);
         __syncthreads();   // previous tile's smem fully stored
-        // stage the row-major input tiles (128-bit, coalesced)
+        // stage the row-major input tiles (LDGSTS, 16 B per copy for full tiles)
         if (full) {
-            const float4* a4 = reinterpret_cast<const float4*>(actions + (size_t)e0 * N_ACT);
-            float4* s4 = reinterpret_cast<float4*>(s_act);
+            const float* a = actions + (size_t)e0 * N_ACT;
+            const float* o = raw_obs + (size_t)e0 * OBS_IN;
 #pragma unroll
-            for (int i = tid; i < TILE * N_ACT / 4; i += STEP_THREADS) s4[i] = __ldcs(a4 + i);
-            const float4* o4 = reinterpret_cast<const float4*>(raw_obs + (size_t)e0 * OBS_IN);
-            float4* so4 = reinterpret_cast<float4*>(s_obs);
+            for (int i = tid; i < TILE * N_ACT / 4; i += STEP_THREADS) cp_async16(s_act + 4 * i, a + 4 * i);
 #pragma unroll
-            for (int i = tid; i < TILE * OBS_IN / 4; i += STEP_THREADS) so4[i] = __ldcs(o4 + i);
+            for (int i = tid; i < TILE * OBS_IN / 4; i += STEP_THREADS) cp_async16(s_obs + 4 * i, o + 4 * i);
         } else {
-            for (uint32_t i = tid; i < cnt * N_ACT; i += STEP_THREADS) s_act[i] = __ldcs(actions + (size_t)e0 * N_ACT + i);
-            for (uint32_t i = tid; i < cnt * OBS_IN; i += STEP_THREADS) s_obs[i] = __ldcs(raw_obs + (size_t)e0 * OBS_IN + i);
+            for (uint32_t i = tid; i < cnt * N_ACT; i += STEP_THREADS) cp_async4(s_act + i, actions + (size_t)e0 * N_ACT + i);
+            for (uint32_t i = tid; i < cnt * OBS_IN; i += STEP_THREADS) cp_async4(s_obs + i, raw_obs + (size_t)e0 * OBS_IN + i);
         }
-        __syncthreads();
-        if ((uint32_t)tid < cnt) {
-            env_step<L>(p, e0 + tid, t, tid, s_act, s_obs, s_dt, s_dec, acc);
+        cp_commit();
+        const bool mine = (uint32_t)tid < cnt;
+        if (mine) issue_s0<L>(s_ring + tid, p.rec + e0 + tid, p.st + e0 + tid, P);            // S0 -> slot0
+        cp_commit();
+        if (mine) issue_act<L>(s_ring + RING_W * TILE + tid, p.rec + e0 + tid, p.st + e0 + tid, P, 0);  // A0 -> slot1
+        cp_commit();
+        cp_wait<1>();      // staging + S0 of this thread
+        __syncthreads();   // everyone's staging copies
+        if (mine) {
+            env_step<L>(p, e0 + tid, t, tid, s_act, s_obs, s_dt, s_ring, acc);
             ++my_envs;
         }
+        cp_wait<0>();
         __syncthreads();
         // store the output tiles (coalesced)
         if (full) {
@@ -512,21 +548,20 @@ __global__ void __launch_bounds__(STEP_THREADS, STEP_MIN_CTAS) step_kernel(const
             if (lane == 0) s_red[i * (STEP_THREADS / 32) + wid] = x;
         };
         red(0, (double)my_envs);
-        const uint32_t* an = s_accn + tid;
-        red(1, (double)an[K_DELAYED * TILE]);
-        red(2, (double)an[K_DROP_INIT * TILE]);
-        red(3, (double)an[K_MASKED * TILE]);
-        red(4, (double)an[K_OCCLUDED * TILE]);
-        red(5, (double)an[K_HELD * TILE]);
-        red(6, (double)an[K_TRIG * TILE]);
-        red(7, (double)an[K_RAIL * TILE]);
-        red(8, (double)an[K_ALPHA1 * TILE]);
-        red(9, on<L>(B_BACKLASH) ? (double)my_envs * N_ACT - (double)an[K_ALPHA1 * TILE] : 0.0);
+        red(1, (double)acc.n[K_DELAYED]);
+        red(2, (double)acc.n[K_DROP_INIT]);
+        red(3, (double)acc.n[K_MASKED]);
+        red(4, (double)acc.n[K_OCCLUDED]);
+        red(5, (double)acc.n[K_HELD]);
+        red(6, (double)acc.n[K_TRIG]);
+        red(7, (double)acc.n[K_RAIL]);
+        red(8, (double)acc.n[K_ALPHA1]);
+        red(9, on<L>(B_BACKLASH) ? (double)my_envs * N_ACT - (double)acc.n[K_ALPHA1] : 0.0);
         red(10, 0.0);
-        red(11, (double)an[K_CLAMPS * TILE]);
+        red(11, (double)acc.n[K_CLAMPS]);
         red(12, 0.0); red(13, 0.0); red(14, 0.0); red(15, 0.0);
-#pragma unroll 1
-        for (int i = 0; i < 8; ++i) red(16 + i, (double)s_accm[i * TILE + tid]);
+#pragma unroll
+        for (int i = 0; i < 8; ++i) red(16 + i, (double)acc.m[i]);
     }
     __syncthreads();
     if (tid < N_STATS) {
