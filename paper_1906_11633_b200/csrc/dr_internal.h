@@ -115,8 +115,10 @@ int reset_max_ctas_per_sm();
 constexpr int RESET_THREADS = 256;
 constexpr int STEP_THREADS = TILE;
 #ifndef DR_STEP_MIN_CTAS
-#define DR_STEP_MIN_CTAS 4
+#define DR_STEP_MIN_CTAS 3
 #endif
-constexpr int STEP_MIN_CTAS = DR_STEP_MIN_CTAS;   // __launch_bounds__ occupancy target (<= 128 regs at 4)
+// __launch_bounds__ occupancy target: 3 CTAs/SM (<= 168 regs) measured fastest for v3 on B200
+// (3.22e9 vs 3.05e9 env-steps/s at 4 CTAs/SM; profiles/round1_notes.md)
+constexpr int STEP_MIN_CTAS = DR_STEP_MIN_CTAS;
 
 }  // namespace dr
