@@ -208,9 +208,8 @@ def main():
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     cfg = config_of(args.config, args.n_env)
     n_glob = cfg["n"]
-    assert n_glob % world == 0
-    n = n_glob // world
-    off = rank * n
+    from paper_1906_11633_b200.parallel import shard, stats_all_reduce
+    off, n = shard(n_glob, world, rank)
     P = presets.preset(cfg["mask"])
 
     lib_stream = torch.cuda.Stream()
@@ -250,7 +249,7 @@ def main():
             ev.record(lib_stream)
             comm_stream.wait_event(ev)
             with torch.cuda.stream(comm_stream):
-                dist.all_reduce(ctx.stats[t % 2])
+                stats_all_reduce(ctx.stats[t % 2])
 
     with torch.cuda.stream(lib_stream):
         for t in range(args.warmup):
