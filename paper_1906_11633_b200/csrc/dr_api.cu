@@ -34,11 +34,11 @@ int device_sm_count() {
 
 Layout make_layout(int64_t n_env, int n_phys, int max_ctas) {
     Layout L{};
-    L.pitch = align_up((size_t)n_env, 64);
+    L.pitch = align_up((size_t)n_env, TILE);   // envs rounded up to whole tiles
     size_t off = 0;
     auto take = [&](size_t bytes) { size_t o = off; off = align_up(off + bytes, 256); return o; };
-    L.rec = take((size_t)REC_PLANES * L.pitch * 4);
-    L.st = take((size_t)ST_PLANES * L.pitch * 4);
+    L.rec = take((size_t)REC_PLANES * L.pitch * 4);   // [n_tiles][REC_PLANES][TILE]
+    L.st = take((size_t)ST_PLANES * L.pitch * 4);     // [n_tiles][ST_PLANES][TILE]
     L.phys = take((size_t)n_env * n_phys * 4);
     L.pd_kr = take(MAX_PHYS * 4);
     L.pd_a = take(MAX_PHYS * 4);

@@ -1,10 +1,12 @@
 // dr_internal.h -- shared between the host library (dr_api.cu) and the kernels (dr_kernels.cu).
-// Device data layout:
-//   rec  : episode record, structure-of-arrays planes [REC_PLANES][pitch] (4-byte words)
-//   st   : mutable per-env state, planes [ST_PLANES][pitch]
+// Device data layout: tiled structure-of-arrays ("AoSoA").
+//   rec  : episode record, [n_tiles][REC_PLANES][TILE] 4-byte words
+//   st   : mutable per-env state, [n_tiles][ST_PLANES][TILE]
 //   phys : [n_env][n_phys] fp32, row-major (the simulator reads rows)
-// pitch = n_env rounded up to 64, so every plane starts 256-byte aligned and a warp's 32
-// consecutive envs read one 128-byte line per plane (coalesced, no staging needed).
+// Within a tile, plane k of env e sits at k * TILE + (e % TILE): a warp's 32 consecutive envs
+// read one 128-byte line per plane (coalesced), every plane offset from an env's base is a
+// compile-time immediate (no per-access address arithmetic), and a tile's whole record /
+// state is one contiguous block (one bulk copy / L2 prefetch).
 #pragma once
 #include <cstddef>
 #include <cstdint>
@@ -48,6 +50,15 @@ enum : int {
 };
 constexpr uint32_t HAS_LAST_BIT = 1u << 20;
 
+// AoSoA addressing: word offset of env e's plane 0; plane k is at + k * TILE.
+__host__ __device__ __forceinline__ size_t rec_index(uint32_t e) {
+    return (size_t)(e / TILE) * (REC_PLANES * TILE) + (e % TILE);
+}
+__host__ __device__ __forceinline__ size_t st_index(uint32_t e) {
+    return (size_t)(e / TILE) * (ST_PLANES * TILE) + (e % TILE);
+}
+constexpr size_t PLANE = TILE;   // plane stride in words
+
 // Philox channels
 enum : uint32_t {
     CH_TIMING = 0x01, CH_ACT_UADD = 0x02, CH_ACT_MULT = 0x03, CH_DROPOUT = 0x04,
@@ -83,8 +94,8 @@ struct DevConst {
 
 // Pointers of the device workspace.
 struct DevPtrs {
-    uint32_t* rec;            // [REC_PLANES][pitch]
-    uint32_t* st;             // [ST_PLANES][pitch]
+    uint32_t* rec;            // [n_tiles][REC_PLANES][TILE]
+    uint32_t* st;             // [n_tiles][ST_PLANES][TILE]
     float* phys;              // [n_env][n_phys]
     // physics descriptor table (global, lane-indexed in the reset kernel)
     uint32_t* pd_kind_rank;   // [256]: kind | (rank << 8)

@@ -80,9 +80,9 @@ __device__ __forceinline__ float slot_normal(const uint4* w, int base, int n) {
 
 __device__ __forceinline__ void reset_one(const DevPtrs& p, uint32_t e, bool first, int lane, uint4* w) {
     const uint32_t lm = c_dc.layer_mask;
-    const size_t P = c_dc.pitch;
-    uint32_t* R = p.rec + e;
-    uint32_t* S = p.st + e;
+    constexpr size_t P = PLANE;
+    uint32_t* R = p.rec + rec_index(e);
+    uint32_t* S = p.st + st_index(e);
     const uint32_t g = c_dc.env_offset + e;
     const uint32_t k = first ? 0u : R[REC_EPISODE * P] + 1u;
     __syncwarp();
@@ -209,9 +209,9 @@ constexpr int EXP_WORDS = 148;
 __global__ void export_kernel(DevPtrs p, uint32_t* __restrict__ dst, uint32_t lo, uint32_t hi) {
     const uint32_t e = lo + blockIdx.x * blockDim.x + threadIdx.x;
     if (e >= hi) return;
-    const size_t P = c_dc.pitch;
-    const uint32_t* R = p.rec + e;
-    const uint32_t* S = p.st + e;
+    constexpr size_t P = PLANE;
+    const uint32_t* R = p.rec + rec_index(e);
+    const uint32_t* S = p.st + st_index(e);
     uint32_t* o = dst + (size_t)(e - lo) * EXP_WORDS;
     o[0] = R[REC_EPISODE * P];
     o[1] = R[REC_DELAY * P];
@@ -229,9 +229,9 @@ __global__ void export_kernel(DevPtrs p, uint32_t* __restrict__ dst, uint32_t lo
 __global__ void import_kernel(DevPtrs p, const uint32_t* __restrict__ src, uint32_t lo, uint32_t hi) {
     const uint32_t e = lo + blockIdx.x * blockDim.x + threadIdx.x;
     if (e >= hi) return;
-    const size_t P = c_dc.pitch;
-    uint32_t* R = p.rec + e;
-    uint32_t* S = p.st + e;
+    constexpr size_t P = PLANE;
+    uint32_t* R = p.rec + rec_index(e);
+    uint32_t* S = p.st + st_index(e);
     const uint32_t* o = src + (size_t)(e - lo) * EXP_WORDS;
     R[REC_EPISODE * P] = o[0];
     R[REC_DELAY * P] = o[1];

@@ -51,14 +51,13 @@ __device__ __forceinline__ void prefetch_tile(const DevPtrs& p, const float* act
     const uint32_t e0 = tile * TILE;
     if (e0 >= n_env) return;
     const uint32_t cnt = min((uint32_t)TILE, n_env - e0);
-    const size_t P = c_dc.pitch;
-    const uint32_t pb = (cnt * 4u + 15u) & ~15u;   // plane chunks stay inside the 64-padded pitch
-    for (int item = threadIdx.x; item < REC_STEP_PLANES + ST_PLANES + 2; item += blockDim.x) {
-        if (item < REC_STEP_PLANES) {
-            l2_prefetch(p.rec + (size_t)item * P + e0, pb);
-        } else if (item < REC_STEP_PLANES + ST_PLANES) {
-            l2_prefetch(p.st + (size_t)(item - REC_STEP_PLANES) * P + e0, pb);
-        } else if (item == REC_STEP_PLANES + ST_PLANES) {
+    // AoSoA: the tile's record planes and state planes are two contiguous blocks
+    for (int item = threadIdx.x; item < 4; item += blockDim.x) {
+        if (item == 0) {
+            l2_prefetch(p.rec + rec_index(e0), REC_STEP_PLANES * TILE * 4u);
+        } else if (item == 1) {
+            l2_prefetch(p.st + st_index(e0), ST_PLANES * TILE * 4u);
+        } else if (item == 2) {
             l2_prefetch(actions + (size_t)e0 * N_ACT, cnt * N_ACT * 4u);
         } else {
             l2_prefetch(raw_obs + (size_t)e0 * OBS_IN, cnt * OBS_IN * 4u);   // rounded down: in bounds
@@ -117,9 +116,9 @@ __device__ __forceinline__ float ringf(const uint32_t* slot, int w) { return __u
 template <uint32_t L>
 __device__ __forceinline__ void env_step(const DevPtrs& p, uint32_t e, uint32_t t, int tid, float* s_act,
                                          float* s_obs, float* s_dt, uint32_t* ring, Acc& acc) {
-    const size_t P = c_dc.pitch;
-    const uint32_t* R = p.rec + e;
-    uint32_t* S = p.st + e;
+    constexpr size_t P = PLANE;
+    const uint32_t* R = p.rec + rec_index(e);
+    uint32_t* S = p.st + st_index(e);
     const uint32_t g = c_dc.env_offset + e;
     constexpr bool kHold = (L == RUNTIME_MASK) || (L & (B_DROPOUT | B_OCCLUSION));
     const bool hold_layers = on<L>(B_DROPOUT) || on<L>(B_OCCLUSION);
@@ -460,7 +459,7 @@ __global__ void __launch_bounds__(STEP_THREADS, STEP_MIN_CTAS)
     const int tid = threadIdx.x;
     const uint32_t t = (uint32_t)p.ctl[0];
     const uint32_t n_tiles = (n_env + TILE - 1) / TILE;
-    const size_t P = c_dc.pitch;
+    constexpr size_t P = PLANE;
     if (PF == 2) prefetch_tile<L>(p, actions, raw_obs, blockIdx.x, n_env);
     Acc acc;
 #pragma unroll
@@ -490,9 +489,9 @@ __global__ void __launch_bounds__(STEP_THREADS, STEP_MIN_CTAS)
         }
         cp_commit();
         const bool mine = (uint32_t)tid < cnt;
-        if (mine) issue_s0<L>(s_ring + tid, p.rec + e0 + tid, p.st + e0 + tid, P);            // S0 -> slot0
+        if (mine) issue_s0<L>(s_ring + tid, p.rec + rec_index(e0 + tid), p.st + st_index(e0 + tid), P);  // S0 -> slot0
         cp_commit();
-        if (mine) issue_act<L>(s_ring + RING_W * TILE + tid, p.rec + e0 + tid, p.st + e0 + tid, P, 0);  // A0 -> slot1
+        if (mine) issue_act<L>(s_ring + RING_W * TILE + tid, p.rec + rec_index(e0 + tid), p.st + st_index(e0 + tid), P, 0);  // A0 -> slot1
         cp_commit();
         cp_wait<1>();      // staging + S0 of this thread
         __syncthreads();   // everyone's staging copies
