@@ -131,5 +131,11 @@ constexpr int STEP_THREADS = TILE;
 // __launch_bounds__ occupancy target: 3 CTAs/SM (<= 168 regs) measured fastest for v3 on B200
 // (3.22e9 vs 3.05e9 env-steps/s at 4 CTAs/SM; profiles/round1_notes.md)
 constexpr int STEP_MIN_CTAS = DR_STEP_MIN_CTAS;
+#ifndef DR_SFU_NORMALS
+#define DR_SFU_NORMALS 1
+#endif
+// step-kernel normals for actions / fingertips / object / rotation axis take the Box-Muller angle
+// from the SFU (dr_device.cuh: box_muller_sfu); force and reset draws never do
+constexpr bool kSfuNormals = DR_SFU_NORMALS != 0;
 
 }  // namespace dr

@@ -191,8 +191,8 @@ __device__ __forceinline__ void env_step(const DevPtrs& p, uint32_t e, uint32_t 
 
         float zu[4], zm[4];
         if (on<L>(B_ACT_NOISE)) {
-            normals4(philox(g, t, CH_ACT_UADD, b), zu);
-            normals4(philox(g, t, CH_ACT_MULT, b), zm);
+            normals4_t<kSfuNormals>(philox(g, t, CH_ACT_UADD, b), zu);
+            normals4_t<kSfuNormals>(philox(g, t, CH_ACT_MULT, b), zm);
         }
         const float4 a4 = a4p[b];
         const float av[4] = {a4.x, a4.y, a4.z, a4.w};
@@ -342,7 +342,7 @@ __device__ __forceinline__ void env_step(const DevPtrs& p, uint32_t e, uint32_t 
 #pragma unroll
         for (int b = 0; b < 4; ++b) {
             float z[4];
-            normals4(philox(g, t, CH_TIP_NOISE, b), z);
+            normals4_t<kSfuNormals>(philox(g, t, CH_TIP_NOISE, b), z);
 #pragma unroll
             for (int q = 0; q < 4; ++q) {
                 const int n = 4 * b + q;
@@ -370,7 +370,7 @@ __device__ __forceinline__ void env_step(const DevPtrs& p, uint32_t e, uint32_t 
     // object position: + 5 mm correlated + 1 mm uncorrelated
     if (on<L>(B_OBS_NOISE)) {
         float z[4];
-        normals4(philox(g, t, CH_OBJ_NOISE, 0), z);
+        normals4_t<kSfuNormals>(philox(g, t, CH_OBJ_NOISE, 0), z);
 #pragma unroll
         for (int c = 0; c < 3; ++c) obj[c] = (obj[c] + ringf(slot0, 15 + c)) + c_dc.obj_uncorr * z[c];
     }
@@ -387,7 +387,7 @@ __device__ __forceinline__ void env_step(const DevPtrs& p, uint32_t e, uint32_t 
         if (on<L>(B_OBS_NOISE)) {
             float qu[4], tmp[4];
             const float qc[4] = {ringf(slot0, 18), ringf(slot0, 19), ringf(slot0, 20), ringf(slot0, 21)};
-            rotation(c_dc.rot_uncorr, philox(g, t, CH_ROT_NOISE, 0), qu);
+            rotation<kSfuNormals>(c_dc.rot_uncorr, philox(g, t, CH_ROT_NOISE, 0), qu);
             qmul(qc, qo, tmp);
             qmul(qu, tmp, qn);
         } else {
