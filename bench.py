@@ -31,7 +31,7 @@ N_GLOBAL_1M = 1 << 20
 # algorithmic bytes per env-step: inputs + outputs + episode record read
 # + state read/write, for the layer sets the configs use
 BYTES_FULL = 184 + 220 + 344 + 480
-BYTES_CFG2 = 184 + 220 + 332 + 160
+BYTES_CFG2 = 184 + 220 + 332 + 160 + 4   # + the flags word (FRESH marker) read per step
 RESET_BYTES = 1024 + 356 + 240 + 1      # phys row + record planes + state planes + mask byte
 
 

@@ -12,7 +12,7 @@ CSRC = os.path.join(PKG, "csrc")
 INCLUDE = os.path.join(ROOT, "include")
 LIB = os.path.join(PKG, "libdr.so")
 SOURCES = [os.path.join(CSRC, f) for f in ("dr_kernels.cu", "dr_api.cu")]
-DEPS = SOURCES + [os.path.join(CSRC, f) for f in ("dr_internal.h", "dr_device.cuh", "dr_step.cuh")] + [os.path.join(INCLUDE, "dr.h")]
+DEPS = SOURCES + [os.path.join(CSRC, f) for f in ("dr_internal.h", "dr_device.cuh", "dr_step.cuh", "dr_reset.cuh")] + [os.path.join(INCLUDE, "dr.h")]
 
 NVCC = os.environ.get("NVCC", "nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]

@@ -49,6 +49,10 @@ enum : int {
     ST_PLANES = 60
 };
 constexpr uint32_t HAS_LAST_BIT = 1u << 20;
+// Set by the reset kernel instead of zeroing the 60 state planes ("slack s initialized
+// to 0; force vector zeroed"): the step kernel reads a fresh env's state as all-zero and writes it
+// back, so a reset costs one scattered state word instead of sixty.
+constexpr uint32_t FRESH_BIT = 1u << 21;
 
 // AoSoA addressing: word offset of env e's plane 0; plane k is at + k * TILE.
 __host__ __device__ __forceinline__ size_t rec_index(uint32_t e) {

@@ -76,7 +76,7 @@ template <uint32_t L>
 __device__ __forceinline__ void issue_s0(uint32_t* slot, const uint32_t* R, const uint32_t* S, size_t P) {
     if (on<L>(B_TIMING)) cp_async4(slot + S0_INVLAM * TILE, R + REC_INVLAM * P);
     if (on<L>(B_DELAY)) cp_async4(slot + S0_DELAY * TILE, R + REC_DELAY * P);
-    if (on<L>(B_DROPOUT) || on<L>(B_OCCLUSION)) cp_async4(slot + S0_FLAGS * TILE, S + ST_FLAGS * P);
+    if (on<L>(B_STATEFUL)) cp_async4(slot + S0_FLAGS * TILE, S + ST_FLAGS * P);   // timers, has_last, FRESH
     if (on<L>(B_FORCE)) {
         cp_async4(slot + S0_TFORCE * TILE, R + REC_TFORCE * P);
         cp_async4(slot + S0_MASS * TILE, R + REC_MASS * P);
@@ -128,15 +128,21 @@ __device__ __forceinline__ void env_step(const DevPtrs& p, uint32_t e, uint32_t 
     // ---- S0 (slot0) has landed (the tile loop waited for it); A0 is in flight into slot1 ----
     const float il = on<L>(B_TIMING) ? ringf(slot0, S0_INVLAM) : 0.f;
     const uint32_t dbits = on<L>(B_DELAY) ? slot0[S0_DELAY * TILE] : 0u;
-    const uint32_t flags = (kHold && hold_layers) ? slot0[S0_FLAGS * TILE] : 0u;
+    // a FRESH env (reset since its last step) has all-zero state: slack 0, prev 0, no reading,
+    // timers 0, force 0 -- the reset kernel does not write the state planes
+    const uint32_t flags_raw = on<L>(B_STATEFUL) ? slot0[S0_FLAGS * TILE] : 0u;
+    const bool fresh = (flags_raw & FRESH_BIT) != 0u;
+    const uint32_t flags = (kHold && hold_layers && !fresh) ? flags_raw : 0u;
     uint32_t tf = 0, kf = 0;
     float mass = 0.f, ft[3] = {0.f, 0.f, 0.f};
     if (on<L>(B_FORCE)) {
         tf = slot0[S0_TFORCE * TILE];
         mass = ringf(slot0, S0_MASS);
-        kf = slot0[S0_KF * TILE];
+        if (!fresh) {
+            kf = slot0[S0_KF * TILE];
 #pragma unroll
-        for (int c = 0; c < 3; ++c) ft[c] = ringf(slot0, S0_FTRIG + c);
+            for (int c = 0; c < 3; ++c) ft[c] = ringf(slot0, S0_FTRIG + c);
+        }
     }
     issue_act<L>(slot0, R, S, P, 1);   // A1 -> slot0
     cp_commit();
@@ -178,8 +184,8 @@ __device__ __forceinline__ void env_step(const DevPtrs& p, uint32_t e, uint32_t 
         float prev[4], slack[4], dneg[4], dpos[4], cact[4];
 #pragma unroll
         for (int q = 0; q < 4; ++q) {
-            prev[q] = on<L>(B_DELAY) ? ringf(sl, q) : 0.f;
-            slack[q] = on<L>(B_BACKLASH) ? ringf(sl, 4 + q) : 0.f;
+            prev[q] = (on<L>(B_DELAY) && !fresh) ? ringf(sl, q) : 0.f;
+            slack[q] = (on<L>(B_BACKLASH) && !fresh) ? ringf(sl, 4 + q) : 0.f;
             dneg[q] = on<L>(B_BACKLASH) ? ringf(sl, 8 + q) : 0.f;
             dpos[q] = on<L>(B_BACKLASH) ? ringf(sl, 12 + q) : 0.f;
             cact[q] = on<L>(B_ACT_NOISE) ? ringf(sl, 16 + q) : 0.f;
@@ -322,6 +328,8 @@ __device__ __forceinline__ void env_step(const DevPtrs& p, uint32_t e, uint32_t 
             acc.n[K_MASKED] += __popc(masked);
         }
         S[ST_FLAGS * P] = nflags | HAS_LAST_BIT;
+    } else if (on<L>(B_STATEFUL) && fresh) {
+        S[ST_FLAGS * P] = 0u;   // clear FRESH (no hold layers: timers / has_last unused)
     }
     const uint32_t hold = (flags & HAS_LAST_BIT) ? (masked | occ) : 0u;
     acc.n[K_HELD] += __popc(hold);
@@ -421,6 +429,10 @@ __device__ __forceinline__ void env_step(const DevPtrs& p, uint32_t e, uint32_t 
             acc.n[K_TRIG] += 1;
         } else {
             kf = (kf < 65535u) ? kf + 1u : 65535u;
+            if (fresh) {   // materialise the zeroed force of a fresh episode
+#pragma unroll
+                for (int c = 0; c < 3; ++c) S[(ST_FTRIG + c) * P] = 0u;
+            }
         }
         S[ST_KF * P] = kf;
         const double dec = __ldg(p.dec_tab + (kf & 255u)) * __ldg(p.dec_tab + 256u + (kf >> 8));   // L1-resident
