@@ -20,7 +20,8 @@ using namespace dr;
 namespace {
 
 struct Layout {
-    size_t rec, st, phys, pd_kr, pd_a, pd_b, pd_base, t_tab, dec, partials, stats, ctl, total;
+    size_t rec, st, phys, pd_kr, pd_a, pd_b, pd_base, t_tab, rs_philox, rs_pairs, rs_phys, rs_src, dec, partials,
+        stats, ctl, total;
     uint64_t pitch;
 };
 
@@ -45,6 +46,10 @@ Layout make_layout(int64_t n_env, int n_phys, int max_ctas) {
     L.pd_b = take(MAX_PHYS * 4);
     L.pd_base = take(MAX_PHYS * 4);
     L.t_tab = take(65536 * 4);
+    L.rs_philox = take(RS_MAX_PHILOX * 4);
+    L.rs_pairs = take(RS_MAX_PAIRS * 4);
+    L.rs_phys = take(MAX_PHYS * 16);
+    L.rs_src = take(MAX_PHYS * 4);
     L.dec = take(512 * 8);
     L.partials = take((size_t)max_ctas * N_STATS * 8);
     L.stats = take(2 * N_STATS * 8);
@@ -267,6 +272,10 @@ int dr_init(const dr_params* params, int64_t n_env, uint64_t seed) {
     P.pd_b = reinterpret_cast<float*>(c->ws + L.pd_b);
     P.pd_base = reinterpret_cast<float*>(c->ws + L.pd_base);
     P.t_tab = reinterpret_cast<uint32_t*>(c->ws + L.t_tab);
+    P.rs_philox = reinterpret_cast<uint32_t*>(c->ws + L.rs_philox);
+    P.rs_pairs = reinterpret_cast<uint32_t*>(c->ws + L.rs_pairs);
+    P.rs_phys = reinterpret_cast<float4*>(c->ws + L.rs_phys);
+    P.rs_src = reinterpret_cast<uint32_t*>(c->ws + L.rs_src);
     P.dec_tab = reinterpret_cast<double*>(c->ws + L.dec);
     P.partials = reinterpret_cast<double*>(c->ws + L.partials);
     P.stats = reinterpret_cast<double*>(c->ws + L.stats);
@@ -337,6 +346,79 @@ int dr_init(const dr_params* params, int64_t n_env, uint64_t seed) {
     }
     dc.n_phys_u = nu;
     dc.n_phys_n = nn;
+
+    // ---- reset task tables (dr_internal.h): only the blocks / pairs the enabled layers draw ----
+    const uint32_t lm = p.layer_mask;
+    std::vector<uint32_t> rph, rpr;
+    auto ph = [&](int slot, uint32_t ch, int nblk) {
+        for (int b = 0; b < nblk; ++b) rph.push_back((uint32_t)(slot + b) | ((uint32_t)b << 8) | (ch << 16));
+    };
+    auto pr = [&](int slot, int npairs, int zbase) {
+        for (int q = 0; q < npairs; ++q) rpr.push_back((uint32_t)slot | ((uint32_t)q << 8) | ((uint32_t)zbase << 16));
+    };
+    if (lm & DR_PHYS) {
+        ph(SL_PHYS_U, CH_PHYS_U, (nu + 3) / 4);
+        ph(SL_PHYS_N, CH_PHYS_N, (nn + 3) / 4);
+        pr(SL_PHYS_N, (nn + 1) / 2, ZB_PHYS);
+    }
+    if (lm & DR_DELAY) ph(SL_DELAY, CH_DELAY, 5);
+    if (lm & DR_BACKLASH) { ph(SL_BACKLASH, CH_BACKLASH, 10); pr(SL_BACKLASH, 20, ZB_BL); }
+    if (lm & DR_TIMING) ph(SL_LAMBDA, CH_LAMBDA, 1);
+    if (lm & DR_FORCE) ph(SL_FORCE_P, CH_FORCE_P, 1);
+    if (lm & DR_ACT_NOISE) { ph(SL_CORR_ACT, CH_CORR_ACT, 5); pr(SL_CORR_ACT, 10, ZB_CA); }
+    if (lm & DR_OBS_NOISE) {
+        ph(SL_CORR_TIP, CH_CORR_TIP, 4);
+        ph(SL_MARKER_TIP, CH_MARKER_TIP, 4);
+        ph(SL_MARKER_BASE, CH_MARKER_BASE, 1);
+        ph(SL_CORR_OBJ, CH_CORR_OBJ, 1);
+        ph(SL_CORR_ROT, CH_CORR_ROT, 1);
+        pr(SL_CORR_TIP, 8, ZB_CT);
+        pr(SL_MARKER_TIP, 8, ZB_MT);
+        pr(SL_MARKER_BASE, 2, ZB_MB);
+        pr(SL_CORR_OBJ, 2, ZB_CO);
+    }
+    dc.n_rs_philox = (int)rph.size();
+    dc.n_rs_pairs = (int)rpr.size();
+    // physics: v = C0 + C1 * f(A + B x) (dr_internal.h), from the descriptor schema
+    std::vector<float> rphys(MAX_PHYS * 4, 0.f);
+    std::vector<uint32_t> rsrc(MAX_PHYS, 0u);
+    {
+        int u = 0, n = 0;
+        for (int i = 0; i < p.n_phys; ++i) {
+            const dr_phys_desc& d = p.phys[i];
+            float A = 0.f, B = 0.f, C0 = (float)d.base, C1 = 0.f;
+            uint32_t src = 0u;
+            const bool on_phys = (lm & DR_PHYS) != 0;
+            switch (d.kind) {
+            case DR_PHYS_UNIFORM_SCALE:   // base * (a + (b - a) U)
+                if (on_phys) { A = (float)d.a; B = (float)(d.b - d.a); C0 = 0.f; C1 = (float)d.base; src = SL_PHYS_U * 4 + u; }
+                ++u;
+                break;
+            case DR_PHYS_LOGUNIFORM_SCALE:   // base * exp(ln a + (ln b - ln a) U)
+                if (on_phys) {
+                    A = (float)std::log(d.a); B = (float)(std::log(d.b) - std::log(d.a)); C0 = 0.f; C1 = (float)d.base;
+                    src = (SL_PHYS_U * 4 + u) | RS_SRC_EXP;
+                }
+                ++u;
+                break;
+            case DR_PHYS_ADD_GAUSS:   // base + sigma z
+                if (on_phys) { B = (float)d.a; C0 = (float)d.base; C1 = 1.f; src = (ZB_PHYS + n) | RS_SRC_NORMAL; }
+                ++n;
+                break;
+            case DR_PHYS_MUL_LOGNORMAL:   // base * exp(sigma z)
+                if (on_phys) { B = (float)d.a; C0 = 0.f; C1 = (float)d.base; src = (ZB_PHYS + n) | RS_SRC_NORMAL | RS_SRC_EXP; }
+                ++n;
+                break;
+            default:   // FIXED
+                break;
+            }
+            rphys[4 * i + 0] = A;
+            rphys[4 * i + 1] = B;
+            rphys[4 * i + 2] = C0;
+            rphys[4 * i + 3] = C1;
+            rsrc[i] = src;
+        }
+    }
     // loguniform force probability quantised to 65,536 midpoints of ln p (Q19)
     std::vector<uint32_t> ttab(65536);
     {
@@ -365,6 +447,12 @@ int dr_init(const dr_params* params, int64_t n_env, uint64_t seed) {
     if ((e = cudaMemcpyAsync(P.pd_b, pb.data(), MAX_PHYS * 4, cudaMemcpyHostToDevice, s)) != cudaSuccess) return bail(e, "memcpy pd");
     if ((e = cudaMemcpyAsync(P.pd_base, pbase.data(), MAX_PHYS * 4, cudaMemcpyHostToDevice, s)) != cudaSuccess) return bail(e, "memcpy pd");
     if ((e = cudaMemcpyAsync(P.t_tab, ttab.data(), 65536 * 4, cudaMemcpyHostToDevice, s)) != cudaSuccess) return bail(e, "memcpy t_tab");
+    if (!rph.empty() && (e = cudaMemcpyAsync(P.rs_philox, rph.data(), rph.size() * 4, cudaMemcpyHostToDevice, s)) != cudaSuccess)
+        return bail(e, "memcpy rs_philox");
+    if (!rpr.empty() && (e = cudaMemcpyAsync(P.rs_pairs, rpr.data(), rpr.size() * 4, cudaMemcpyHostToDevice, s)) != cudaSuccess)
+        return bail(e, "memcpy rs_pairs");
+    if ((e = cudaMemcpyAsync(P.rs_phys, rphys.data(), MAX_PHYS * 16, cudaMemcpyHostToDevice, s)) != cudaSuccess) return bail(e, "memcpy rs_phys");
+    if ((e = cudaMemcpyAsync(P.rs_src, rsrc.data(), MAX_PHYS * 4, cudaMemcpyHostToDevice, s)) != cudaSuccess) return bail(e, "memcpy rs_src");
     if ((e = cudaMemcpyAsync(P.dec_tab, dec.data(), 512 * 8, cudaMemcpyHostToDevice, s)) != cudaSuccess) return bail(e, "memcpy dec");
     if ((e = cudaMemsetAsync(P.stats, 0, 2 * N_STATS * 8, s)) != cudaSuccess) return bail(e, "memset stats");
     if ((e = cudaMemsetAsync(P.ctl, 0, 4 * 8, s)) != cudaSuccess) return bail(e, "memset ctl");

@@ -94,7 +94,44 @@ struct DevConst {
     float accel_std;
     int32_t n_phys, mass_index;
     int32_t n_phys_u, n_phys_n;       // counts of uniform-kind / normal-kind params
+    int32_t n_rs_philox, n_rs_pairs;  // reset task-table lengths (host-built, layer-dependent)
 };
+
+// Reset task tables (built on the host at dr_init, staged in shared memory by the reset kernel):
+//   philox task : slot | blk << 8 | channel << 16        (one Philox block per entry)
+//   pair task   : slot | pair << 8 | zbuf_base << 16     (one Box-Muller pair per entry)
+//   phys entry  : float4 (A, B, C0, C1) + src word: v = C0 + C1 * f, f = (exp?) (A + B x), where
+//                 x = U(word src) for uniform kinds or z[src] for normal kinds
+//                 (src bit 31: normal kind, bit 30: exp, bits 0..29: index)
+constexpr int RS_MAX_PHILOX = 161, RS_MAX_PAIRS = 128 + 50;
+// Philox block slots of one reset env (shared-memory layout; the task table says which are live)
+enum : int {
+    SL_PHYS_U = 0,        // up to 64 blocks (256 uniform-kind params)
+    SL_PHYS_N = 64,       // up to 64 blocks (256 normal-kind params)
+    SL_DELAY = 128,       // 5
+    SL_BACKLASH = 133,    // 10 (40 normals)
+    SL_LAMBDA = 143,      // 1
+    SL_FORCE_P = 144,     // 1
+    SL_CORR_ACT = 145,    // 5
+    SL_CORR_TIP = 150,    // 4
+    SL_MARKER_TIP = 154,  // 4
+    SL_MARKER_BASE = 158, // 1
+    SL_CORR_OBJ = 159,    // 1
+    SL_CORR_ROT = 160,    // 1
+    SL_COUNT = 161
+};
+// z buffer of one reset env: normal n of a channel at its base + n
+enum : int {
+    ZB_PHYS = 0,    // by normal rank, up to 256
+    ZB_BL = 256,    // 40: delta_-1 normals 0..19, delta_+1 normals 20..39
+    ZB_CA = 296,    // 20
+    ZB_CT = 316,    // 16 (15 used)
+    ZB_MT = 332,    // 16 (15 used)
+    ZB_MB = 348,    // 4 (3 used)
+    ZB_CO = 352,    // 4 (3 used)
+    ZB_COUNT = 356
+};
+constexpr uint32_t RS_SRC_NORMAL = 1u << 31, RS_SRC_EXP = 1u << 30, RS_SRC_IDX = (1u << 30) - 1u;
 
 // Pointers of the device workspace.
 struct DevPtrs {
@@ -107,6 +144,10 @@ struct DevPtrs {
     float* pd_b;              // [256]  b (or ln b - ln a for loguniform)
     float* pd_base;           // [256]
     uint32_t* t_tab;          // [65536] force thresholds
+    uint32_t* rs_philox;      // [RS_MAX_PHILOX] reset Philox tasks
+    uint32_t* rs_pairs;       // [RS_MAX_PAIRS] reset Box-Muller pair tasks
+    float4* rs_phys;          // [256] physics coefficients
+    uint32_t* rs_src;         // [256] physics draw source
     double* dec_tab;          // [512]: 0.99^j (j < 256), then 0.99^(256 i)
     double* partials;         // [max_ctas][N_STATS]
     double* stats;            // [2][N_STATS] (internal or caller-owned)

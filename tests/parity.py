@@ -119,8 +119,11 @@ def compare_records(G: dict, O: list, phys_g=None, strict_state=True, knife=None
         assert_close("last", G["last"], get("last"), 0.1)
     assert_close("f_trig", G["f_trig"], get("f_trig"), np.maximum(mass[:, None], 1e-30))
     if phys_g is not None:
+        # floor |base|: ADD_GAUSS can cancel base + sigma z towards 0
+        from workload import presets
         ph = get("phys")[:, : phys_g.shape[1]]
-        assert_close("phys", phys_g, ph, np.abs(ph) + 1e-30)
+        base = np.abs(np.array([d[3] for d in presets.PAPER["phys"]]))[: phys_g.shape[1]]
+        assert_close("phys", phys_g, ph, np.maximum(base[None, :], 1e-30))
 
 
 STAT_INT = list(range(0, 12))
