@@ -15,7 +15,7 @@
 // and the step kernel reads a fresh env's state as zero (dr_internal.h).
 #pragma once
 
-__device__ __forceinline__ void reset_one(const DevPtrs& p, uint32_t e, bool first, int lane, uint4* w, float* zb,
+__device__ __forceinline__ void reset_one(const DevPtrs& p, uint32_t e, uint32_t k, int lane, uint4* w, float* zb,
                                           const uint32_t* s_ph, const uint32_t* s_pr, const float4* s_pd,
                                           const uint32_t* s_src) {
     const uint32_t lm = c_dc.layer_mask;
@@ -23,14 +23,15 @@ __device__ __forceinline__ void reset_one(const DevPtrs& p, uint32_t e, bool fir
     uint32_t* R = p.rec + rec_index(e);
     uint32_t* S = p.st + st_index(e);
     const uint32_t g = c_dc.env_offset + e;
-    const uint32_t k = first ? 0u : R[REC_EPISODE * P] + 1u;
     __syncwarp();
-    // A. Philox blocks, one per lane
+    // A. Philox blocks, one per lane (k = this env's new episode index, loaded per chunk)
     for (int i = lane; i < c_dc.n_rs_philox; i += 32) {
         const uint32_t task = s_ph[i];
         w[task & 0xFFu] = philox(g, k, task >> 16, (task >> 8) & 0xFFu);
     }
     __syncwarp();
+    // the force threshold gather is issued now and consumed in D2 (latency off the critical path)
+    const uint32_t tf_pre = (lane == 20 && (lm & B_FORCE)) ? __ldg(p.t_tab + (w[SL_FORCE_P].x >> 16)) : 0u;
     // B. Box-Muller pairs, one per lane: pair q of a channel uses block q / 2, words (x, y) for
     //    even q and (z, w) for odd q, giving normals 2q (cos) and 2q + 1 (sin)
     for (int i = lane; i < c_dc.n_rs_pairs; i += 32) {
@@ -105,13 +106,9 @@ __device__ __forceinline__ void reset_one(const DevPtrs& p, uint32_t e, bool fir
         R[REC_INVLAM * P] = __float_as_uint(il);
     } else if (lane == 20) {
         // loguniform force probability [Q19]: index + exact integer threshold
-        uint32_t j = 0, tf = 0;
-        if (lm & B_FORCE) {
-            j = w[SL_FORCE_P].x >> 16;
-            tf = __ldg(p.t_tab + j);
-        }
+        const uint32_t j = (lm & B_FORCE) ? (w[SL_FORCE_P].x >> 16) : 0u;
         R[REC_PINDEX * P] = j;
-        R[REC_TFORCE * P] = tf;
+        R[REC_TFORCE * P] = tf_pre;
     } else if (lane == 21) {
         R[REC_EPISODE * P] = k;
     } else if (lane == 22) {
@@ -141,16 +138,32 @@ __global__ void __launch_bounds__(RESET_THREADS) reset_kernel(DevPtrs p, const u
     const uint32_t n_chunks = (n_env + 31u) >> 5;
     const uint32_t nw = gridDim.x * RESET_WARPS;
     uint32_t applied = 0;
-    for (uint32_t c = blockIdx.x * RESET_WARPS + wib; c < n_chunks; c += nw) {
+    // one coalesced load of 32 mask bytes and 32 episode counters per chunk, prefetched a chunk ahead
+    auto load_chunk = [&](uint32_t c, uint32_t& m, uint32_t& ep) {
         const uint32_t e = (c << 5) + lane;
-        const bool m = e < n_env && (mask == nullptr || mask[e] != 0);
-        uint32_t bal = __ballot_sync(0xFFFFFFFFu, m);
+        m = 0u;
+        ep = 0u;
+        if (c < n_chunks && e < n_env) {
+            m = (mask == nullptr) ? 1u : (uint32_t)mask[e];
+            if (!first) ep = p.rec[rec_index(e) + REC_EPISODE * PLANE];
+        }
+    };
+    uint32_t c = blockIdx.x * RESET_WARPS + wib;
+    uint32_t m_cur, ep_cur;
+    load_chunk(c, m_cur, ep_cur);
+    for (; c < n_chunks; c += nw) {
+        uint32_t m_nxt, ep_nxt;
+        load_chunk(c + nw, m_nxt, ep_nxt);
+        uint32_t bal = __ballot_sync(0xFFFFFFFFu, m_cur != 0u);
         applied += __popc(bal);
         while (bal) {
             const int b = __ffs(bal) - 1;
             bal &= bal - 1;
-            reset_one(p, (c << 5) + b, first != 0, lane, s_w[wib], s_zb[wib], s_ph, s_pr, s_pd, s_src);
+            const uint32_t k = first ? 0u : __shfl_sync(0xFFFFFFFFu, ep_cur, b) + 1u;
+            reset_one(p, (c << 5) + b, k, lane, s_w[wib], s_zb[wib], s_ph, s_pr, s_pd, s_src);
         }
+        m_cur = m_nxt;
+        ep_cur = ep_nxt;
     }
     if (!first && lane == 0 && applied) atomicAdd(&p.ctl[2], (unsigned long long)applied);
 }
