@@ -157,7 +157,8 @@ __device__ __forceinline__ void env_step(const DevPtrs& p, uint32_t e, uint32_t 
                 const uint4 w = philox(g, t, CH_TIMING, b);
 #pragma unroll
                 for (int q = 0; q < 4; ++q)
-                    if (4 * b + q < N_SUB) d[4 * b + q] = c_dc.dt_base + (-ln_unit(uni(word_of(w, q)))) * il;
+                    if (4 * b + q < N_SUB)
+                        d[4 * b + q] = c_dc.dt_base + (-(kSfuNormals ? ln_unit_sfu(uni(word_of(w, q))) : ln_unit(uni(word_of(w, q))))) * il;
             }
         } else {
 #pragma unroll
@@ -237,9 +238,10 @@ __device__ __forceinline__ void env_step(const DevPtrs& p, uint32_t e, uint32_t 
                 const float d = (an > 0.f) ? dpos[q] : ((an < 0.f) ? dneg[q] : 0.f);
                 const float sp = fminf(fmaxf(s + an * d * dt_env, -1.f), 1.f);
                 const float num = fabsf(sg - s), den = fabsf(sp - s) + c_dc.eps;
-                float al = 0.f;
-                if (num == 0.f) al = 1.f;
-                else if (num < den) al = 1.f - num / den;
+                // num < den only when num < ~1.7e-5 (else num + eps rounds to num in fp32); there
+                // alpha = 1 - num/den is a cancellation whose absolute error (<= 2 ulp of 1 with the
+                // fast divide) is far inside the 1e-6 budget of alpha * a_n -- so no branch.
+                const float al = (num == 0.f) ? 1.f : ((num < den) ? 1.f - __fdividef(num, den) : 0.f);
                 out = al * an;
                 acc.n[K_RAIL] += (sg != 0.f && fabsf(sp) == 1.f && sp != s) ? 1u : 0u;
                 acc.n[K_ALPHA1] += (al == 1.f) ? 1u : 0u;
