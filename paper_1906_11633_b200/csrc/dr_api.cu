@@ -461,6 +461,7 @@ int dr_init(const dr_params* params, int64_t n_env, uint64_t seed) {
     if ((e = cudaStreamSynchronize(s)) != cudaSuccess) return bail(e, "sync init");
 
     if (const char* pf = std::getenv("DR_PREFETCH")) set_step_prefetch(std::atoi(pf));
+    if (const char* pp = std::getenv("DR_PIPE")) set_step_pipe(std::atoi(pp));
     const int occ_step = step_max_ctas_per_sm(p.layer_mask);
     const uint32_t n_tiles = (uint32_t)((n_env + TILE - 1) / TILE);
     c->step_grid = (int)std::min<long long>((long long)n_tiles, (long long)c->sm_count * occ_step);

@@ -167,6 +167,7 @@ cudaError_t launch_debug_philox(uint32_t n_env, uint32_t dom, uint32_t ch, uint3
                                 cudaStream_t s);
 int step_max_ctas_per_sm(uint32_t layer_mask);
 void set_step_prefetch(int mode);
+void set_step_pipe(int mode);
 int reset_max_ctas_per_sm();
 constexpr int RESET_THREADS = 256;
 constexpr int STEP_THREADS = TILE;

@@ -109,6 +109,12 @@ static int g_prefetch = 0;
 
 void set_step_prefetch(int mode) { g_prefetch = (mode < 0 || mode > 2) ? 0 : mode; }
 
+// Ring pipeline of the step kernel (DR_PIPE at dr_init): 1 = CTA-wide TMA bulk-copy ring
+// (step_kernel_tma, default), 0 = per-thread cp.async ring (step_kernel; A/B experiments).
+static int g_pipe = 1;
+
+void set_step_pipe(int mode) { g_pipe = (mode == 0) ? 0 : 1; }
+
 template <int PF>
 static StepFn step_fn_pf(uint32_t m) {
     if (m == MASK_FULL) return step_kernel<MASK_FULL, PF>;
@@ -116,23 +122,33 @@ static StepFn step_fn_pf(uint32_t m) {
     return step_kernel<RUNTIME_MASK, PF>;
 }
 
+static StepFn step_fn_tma(uint32_t m) {
+    if (m == MASK_FULL) return step_kernel_tma<MASK_FULL>;
+    if (m == MASK_CFG2) return step_kernel_tma<MASK_CFG2>;
+    return step_kernel_tma<RUNTIME_MASK>;
+}
+
 static StepFn step_fn(uint32_t layer_mask) {
     const uint32_t m = layer_mask & 0xFFu;
+    if (g_pipe == 1) return step_fn_tma(m);
     if (g_prefetch == 0) return step_fn_pf<0>(m);
     if (g_prefetch == 2) return step_fn_pf<2>(m);
     return step_fn_pf<1>(m);
 }
 
+static size_t step_dyn_smem() { return g_pipe == 1 ? STEP_TMA_DYN_SMEM : STEP_DYN_SMEM; }
+
 // the phase ring is dynamic shared memory (static + dynamic > 48 KB needs the opt-in attribute)
 static StepFn step_fn_ready(uint32_t layer_mask) {
     StepFn f = step_fn(layer_mask);
-    cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)STEP_DYN_SMEM);
+    cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)step_dyn_smem());
     return f;
 }
 
 int step_max_ctas_per_sm(uint32_t layer_mask) {
     int n = 0;
-    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, step_fn_ready(layer_mask), STEP_THREADS, STEP_DYN_SMEM) != cudaSuccess)
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, step_fn_ready(layer_mask), STEP_THREADS, step_dyn_smem()) !=
+        cudaSuccess)
         return 1;
     return n > 0 ? n : 1;
 }
@@ -146,8 +162,8 @@ int reset_max_ctas_per_sm() {
 cudaError_t launch_step(const DevPtrs& p, uint32_t layer_mask, const float* actions, const float* raw_obs,
                         float* out_actions, float* out_obs, float* out_dt, float* out_force, uint32_t n_env,
                         int grid, cudaStream_t s) {
-    step_fn(layer_mask)<<<grid, STEP_THREADS, STEP_DYN_SMEM, s>>>(p, actions, raw_obs, out_actions, out_obs,
-                                                                  out_dt, out_force, n_env);
+    step_fn(layer_mask)<<<grid, STEP_THREADS, step_dyn_smem(), s>>>(p, actions, raw_obs, out_actions, out_obs,
+                                                                    out_dt, out_force, n_env);
     return cudaGetLastError();
 }
 

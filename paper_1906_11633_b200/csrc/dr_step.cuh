@@ -1,23 +1,23 @@
 // dr_step.cuh -- the fused per-env-step kernel, included by dr_kernels.cu
 // inside namespace dr (after on<L>() and the B_* layer bits).
 //
-// Mapping: persistent CTAs of TILE (=128) threads, one thread per env, static round-robin tiles.
+// Mapping: persistent CTAs of TILE (= 128) threads, one thread per env, static round-robin tiles
+// of 128 envs.  Every byte of state makes one HBM round trip per step.
 //
-// Data movement (every byte of state makes one HBM round trip per step):
-//   * Row-major I/O tiles ([n][20] actions, [n][26] raw_obs) are staged into shared memory with
-//     16-byte cp.async (LDGSTS, no register round trip); outputs are written in place over the
-//     input rows (out_actions over actions, out_obs + out_force over raw_obs) and stored with
-//     coalesced 128/64-bit stores.
-//   * The SoA record/state planes (one 128-B line per warp per plane) are software-pipelined
-//     through a per-thread two-slot shared-memory ring with 4-byte cp.async: while the thread
-//     computes phase k from one slot, the copies of phase k+1 are in flight into the other.
-//     Phases: S0 (scalars), A0..A4 (4 actuators each), OB (observation offsets).  In-flight data
-//     occupies shared memory, not registers, which is what lets the SM keep enough bytes in
-//     flight to approach the HBM roofline with a register-heavy (Philox + Box-Muller) thread.
-//   * Held fingertip readings ("last") are fetched with cp.async into the thread's raw-tip slots
-//     (already consumed) while the fingertip noise is computed.
-//   * stats: per-thread register accumulators -> CTA reduction in shared memory -> per-CTA
-//     partials reduced by the last CTA in a fixed order (deterministic fp64 sums).
+// The per-env record/state planes (AoSoA: a tile's plane is one contiguous 512-B chunk) are
+// consumed in seven phases -- S0 (scalars), A0..A4 (4 actuators each), OB (observation offsets)
+// -- streamed through a shared-memory ring so that in-flight bytes live in shared memory, not in
+// registers.  Two interchangeable pipelines feed the ring:
+//   * PipeTma (default, step_kernel_tma): a 3-slot CTA-wide ring filled by TMA bulk copies
+//     (cp.async.bulk + mbarrier complete_tx); a slot is refilled two phases ahead by the last
+//     warp to release it (smem atomic), so no thread ever blocks to produce; the row-major input
+//     tile is also a TMA bulk copy, and the next tile's inputs are issued as soon as the current
+//     tile's outputs are stored.
+//   * PipeThread (step_kernel): a per-thread 2-slot ring filled with 4-byte cp.async (LDGSTS).
+// Outputs are written in place over the input rows in shared memory (out_actions over actions,
+// out_obs + out_force over raw_obs) and stored with coalesced 128/64-bit stores.  Held fingertip
+// readings are fetched with per-thread cp.async while the fingertip noise is computed.  Stats:
+// register accumulators -> CTA shared-memory reduction -> last-CTA fixed-order fp64 reduction.
 #pragma once
 
 enum : int { K_DELAYED = 0, K_DROP_INIT, K_MASKED, K_OCCLUDED, K_HELD, K_TRIG, K_RAIL, K_ALPHA1, K_CLAMPS, K_COUNT };
@@ -39,39 +39,65 @@ __device__ __forceinline__ void cp_commit() { asm volatile("cp.async.commit_grou
 template <int N>
 __device__ __forceinline__ void cp_wait() { asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory"); }
 
+// ---- mbarrier + TMA bulk-copy helpers (sm_90+ PTX; SASS: SYNCS.* and UBLKCP) --------------
+__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count) : "memory");
+}
+__device__ __forceinline__ void mbar_arrive_expect_tx(uint64_t* bar, uint32_t bytes) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+    asm volatile(
+        "{\n\t.reg .pred p;\n"
+        "WAIT_%=:\n\t"
+        "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t"
+        "@!p bra WAIT_%=;\n}" ::"r"(smem_u32(bar)),
+        "r"(parity)
+        : "memory");
+}
+__device__ __forceinline__ void tma_load(void* sdst, const void* gsrc, uint32_t bytes, uint64_t* bar) {
+    asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                     smem_u32(sdst)),
+                 "l"(gsrc), "r"(bytes), "r"(smem_u32(bar))
+                 : "memory");
+}
+// order this thread's generic-proxy shared-memory accesses before subsequent async-proxy (TMA)
+// writes to the same buffers (ring / I/O slot reuse)
+__device__ __forceinline__ void fence_proxy_async() { asm volatile("fence.proxy.async.shared::cta;" ::: "memory"); }
+__device__ __forceinline__ void fence_mbar_init() { asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory"); }
+
 __device__ __forceinline__ void l2_prefetch(const void* ptr, uint32_t bytes) {
     if (bytes >= 16u)
         asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(ptr), "r"(bytes & ~15u) : "memory");
 }
 
-// Optional TMA bulk L2 prefetch of every plane chunk + input row range of a tile (DR_PREFETCH).
+// Optional TMA bulk L2 prefetch of a tile's record/state blocks + input rows (DR_PREFETCH; A/B).
 template <uint32_t L>
 __device__ __forceinline__ void prefetch_tile(const DevPtrs& p, const float* actions, const float* raw_obs,
                                               uint32_t tile, uint32_t n_env) {
     const uint32_t e0 = tile * TILE;
     if (e0 >= n_env) return;
     const uint32_t cnt = min((uint32_t)TILE, n_env - e0);
-    // AoSoA: the tile's record planes and state planes are two contiguous blocks
     for (int item = threadIdx.x; item < 4; item += blockDim.x) {
-        if (item == 0) {
-            l2_prefetch(p.rec + rec_index(e0), REC_STEP_PLANES * TILE * 4u);
-        } else if (item == 1) {
-            l2_prefetch(p.st + st_index(e0), ST_PLANES * TILE * 4u);
-        } else if (item == 2) {
-            l2_prefetch(actions + (size_t)e0 * N_ACT, cnt * N_ACT * 4u);
-        } else {
-            l2_prefetch(raw_obs + (size_t)e0 * OBS_IN, cnt * OBS_IN * 4u);   // rounded down: in bounds
-        }
+        if (item == 0) l2_prefetch(p.rec + rec_index(e0), REC_STEP_PLANES * TILE * 4u);
+        else if (item == 1) l2_prefetch(p.st + st_index(e0), ST_PLANES * TILE * 4u);
+        else if (item == 2) l2_prefetch(actions + (size_t)e0 * N_ACT, cnt * N_ACT * 4u);
+        else l2_prefetch(raw_obs + (size_t)e0 * OBS_IN, cnt * OBS_IN * 4u);   // rounded down: in bounds
     }
 }
 
-// ---- phase ring ----------------------------------------------------------------------------
-// slot word w of thread tid lives at ring[(slot * RING_W + w) * TILE + tid]: the 32 lanes of a
-// warp touch 32 consecutive words (conflict-free LDS, coalesced LDGSTS).
+// ---- phase ring layout ---------------------------------------------------------------------
+// slot row w of thread tid lives at slot[w * TILE + tid]: a warp reads 32 consecutive words
+// (conflict-free LDS), and a tile's plane chunk (512 B) maps onto one row.
 constexpr int RING_W = 22;
-constexpr size_t STEP_DYN_SMEM = 2 * RING_W * TILE * sizeof(uint32_t);
-enum : int { S0_INVLAM = 0, S0_DELAY, S0_FLAGS, S0_TFORCE, S0_MASS, S0_KF, S0_FTRIG };   // FTRIG: 3 words
+constexpr int N_PHASES = 7;   // S0, A0..A4, OB
+constexpr size_t STEP_DYN_SMEM = 2 * RING_W * TILE * sizeof(uint32_t);   // PipeThread: 2 slots
+// S0 rows: record planes 0..3 then state planes 55..59 (both contiguous ranges)
+enum : int { S0_DELAY = 0, S0_INVLAM = 1, S0_TFORCE = 2, S0_MASS = 3, S0_FLAGS = 4, S0_FTRIG = 5, S0_KF = 8 };
+// A_b rows: prev 0..3 | slack 4..7 | dneg 8..11 | dpos 12..15 | cact 16..19 ; OB rows: offtip 0..14 |
+// c_obj 15..17 | q_c 18..21 (record planes 64..85)
 
+// -- per-thread 4-byte copies (PipeThread) --
 template <uint32_t L>
 __device__ __forceinline__ void issue_s0(uint32_t* slot, const uint32_t* R, const uint32_t* S, size_t P) {
     if (on<L>(B_TIMING)) cp_async4(slot + S0_INVLAM * TILE, R + REC_INVLAM * P);
@@ -85,8 +111,6 @@ __device__ __forceinline__ void issue_s0(uint32_t* slot, const uint32_t* R, cons
         for (int c = 0; c < 3; ++c) cp_async4(slot + (S0_FTRIG + c) * TILE, S + (ST_FTRIG + c) * P);
     }
 }
-
-// actuator block b: words [prev 4 | slack 4 | dneg 4 | dpos 4 | cact 4]
 template <uint32_t L>
 __device__ __forceinline__ void issue_act(uint32_t* slot, const uint32_t* R, const uint32_t* S, size_t P, int b) {
 #pragma unroll
@@ -101,8 +125,6 @@ __device__ __forceinline__ void issue_act(uint32_t* slot, const uint32_t* R, con
         if (on<L>(B_ACT_NOISE)) cp_async4(slot + (16 + q) * TILE, R + (REC_CACT + j) * P);
     }
 }
-
-// observation offsets: words [offtip 15 | c_obj 3 | q_c 4]  (REC_OFFTIP..REC_QC are contiguous planes)
 template <uint32_t L>
 __device__ __forceinline__ void issue_obs(uint32_t* slot, const uint32_t* R, size_t P) {
     if (on<L>(B_OBS_NOISE)) {
@@ -111,41 +133,166 @@ __device__ __forceinline__ void issue_obs(uint32_t* slot, const uint32_t* R, siz
     }
 }
 
+// -- CTA-wide TMA bulk copies of phase k of a tile (PipeTma): contiguous plane ranges --
+template <uint32_t L>
+__device__ __forceinline__ uint32_t phase_bytes(int k) {
+    constexpr uint32_t C = TILE * 4u;   // one plane chunk
+    if (k == 0) {
+        uint32_t b = (on<L>(B_TIMING) || on<L>(B_DELAY) || on<L>(B_FORCE)) ? 4 * C : 0u;
+        if (on<L>(B_FORCE)) b += 5 * C;
+        else if (on<L>(B_STATEFUL)) b += C;
+        return b;
+    }
+    if (k == N_PHASES - 1) return on<L>(B_OBS_NOISE) ? 22 * C : 0u;
+    return (on<L>(B_DELAY) ? 4 * C : 0u) + (on<L>(B_BACKLASH) ? 12 * C : 0u) + (on<L>(B_ACT_NOISE) ? 4 * C : 0u);
+}
+template <uint32_t L>
+__device__ __forceinline__ void issue_phase_tma(uint32_t* slot, const uint32_t* Rt, const uint32_t* St, int k,
+                                                uint64_t* bar) {
+    constexpr uint32_t C = TILE * 4u;
+    mbar_arrive_expect_tx(bar, phase_bytes<L>(k));
+    if (k == 0) {
+        if (on<L>(B_TIMING) || on<L>(B_DELAY) || on<L>(B_FORCE)) tma_load(slot, Rt, 4 * C, bar);   // planes 0..3
+        if (on<L>(B_FORCE)) tma_load(slot + S0_FLAGS * TILE, St + ST_FLAGS * TILE, 5 * C, bar);    // 55..59
+        else if (on<L>(B_STATEFUL)) tma_load(slot + S0_FLAGS * TILE, St + ST_FLAGS * TILE, C, bar);
+    } else if (k == N_PHASES - 1) {
+        if (on<L>(B_OBS_NOISE)) tma_load(slot, Rt + REC_OFFTIP * TILE, 22 * C, bar);
+    } else {
+        const int b = k - 1;
+        if (on<L>(B_DELAY)) tma_load(slot, St + (ST_PREV + 4 * b) * TILE, 4 * C, bar);
+        if (on<L>(B_BACKLASH)) {
+            tma_load(slot + 4 * TILE, St + (ST_SLACK + 4 * b) * TILE, 4 * C, bar);
+            tma_load(slot + 8 * TILE, Rt + (REC_DNEG + 4 * b) * TILE, 4 * C, bar);
+            tma_load(slot + 12 * TILE, Rt + (REC_DPOS + 4 * b) * TILE, 4 * C, bar);
+        }
+        if (on<L>(B_ACT_NOISE)) tma_load(slot + 16 * TILE, Rt + (REC_CACT + 4 * b) * TILE, 4 * C, bar);
+    }
+}
+
 __device__ __forceinline__ float ringf(const uint32_t* slot, int w) { return __uint_as_float(slot[w * TILE]); }
 
+// ---- pipeline policies -----------------------------------------------------------------------
+// Per-thread ring (v3-v5): slot0 holds S0, A1, A3, OB; slot1 holds A0, A2, A4.
 template <uint32_t L>
-__device__ __forceinline__ void env_step(const DevPtrs& p, uint32_t e, uint32_t t, int tid, float* s_act,
-                                         float* s_obs, float* s_dt, uint32_t* ring, Acc& acc) {
+struct PipeThread {
+    uint32_t* slot0;
+    uint32_t* slot1;
+    const uint32_t* R;
+    const uint32_t* S;
+    __device__ __forceinline__ const uint32_t* s0() { return slot0; }   // the tile loop waited for it
+    __device__ __forceinline__ void s0_done() {
+        issue_act<L>(slot0, R, S, PLANE, 1);
+        cp_commit();
+    }
+    __device__ __forceinline__ void io_wait() {}
+    __device__ __forceinline__ const uint32_t* act(int b) {
+        cp_wait<1>();
+        return (b & 1) ? slot0 : slot1;
+    }
+    __device__ __forceinline__ void act_done(int b) {
+        uint32_t* sl = (b & 1) ? slot0 : slot1;
+        if (b + 2 < 5) issue_act<L>(sl, R, S, PLANE, b + 2);
+        else if (b + 2 == 5) issue_obs<L>(sl, R, PLANE);
+        cp_commit();
+    }
+    // called after the held-reading copies were committed: wait for everything but them
+    __device__ __forceinline__ const uint32_t* obs() {
+        cp_wait<1>();
+        return slot0;
+    }
+    __device__ __forceinline__ void obs_done() {}
+};
+
+// CTA-wide TMA ring: phase ph (counted over this CTA's tiles) lives in slot ph % NS.
+constexpr int TMA_SLOTS = 3;
+struct TmaShared {
+    uint64_t full[TMA_SLOTS];
+    uint64_t io_full;
+    uint32_t rel[TMA_SLOTS];   // warps that released the slot's current phase
+    uint32_t io_rel;
+};
+
+template <uint32_t L>
+__device__ __forceinline__ void tma_issue_phase(const DevPtrs& p, uint32_t* ring, TmaShared* ts, uint32_t ph,
+                                                uint32_t n_my, uint32_t n_tiles) {
+    const uint32_t it = ph / N_PHASES, k = ph % N_PHASES;
+    if (it >= n_my) return;
+    const uint32_t tile = blockIdx.x + it * gridDim.x;
+    if (tile >= n_tiles) return;
+    const uint32_t e0 = tile * TILE;
+    issue_phase_tma<L>(ring + (ph % TMA_SLOTS) * (RING_W * TILE), p.rec + rec_index(e0), p.st + st_index(e0), (int)k,
+                       &ts->full[ph % TMA_SLOTS]);
+}
+
+template <uint32_t L>
+struct PipeTma {
+    const DevPtrs* p;
+    uint32_t* ring;
+    TmaShared* ts;
+    uint32_t ph0;   // global phase index of this tile's S0
+    uint32_t it;    // tile iteration (I/O parity)
+    uint32_t n_my, n_tiles;
+    int tid;
+    __device__ __forceinline__ const uint32_t* wait(uint32_t ph) {
+        mbar_wait(&ts->full[ph % TMA_SLOTS], (ph / TMA_SLOTS) & 1u);
+        return ring + (ph % TMA_SLOTS) * (RING_W * TILE) + tid;
+    }
+    // the last of the 4 warps to release phase ph refills its slot with phase ph + NS
+    __device__ __forceinline__ void release(uint32_t ph) {
+        __syncwarp();
+        if ((tid & 31) == 0) {
+            const uint32_t s = ph % TMA_SLOTS;
+            if (atomicAdd(&ts->rel[s], 1u) == (uint32_t)(TILE / 32) - 1u) {
+                ts->rel[s] = 0u;
+                fence_proxy_async();
+                tma_issue_phase<L>(*p, ring, ts, ph + TMA_SLOTS, n_my, n_tiles);
+            }
+        }
+    }
+    __device__ __forceinline__ const uint32_t* s0() { return wait(ph0); }
+    __device__ __forceinline__ void s0_done() { release(ph0); }
+    __device__ __forceinline__ void io_wait() { mbar_wait(&ts->io_full, it & 1u); }
+    __device__ __forceinline__ const uint32_t* act(int b) { return wait(ph0 + 1 + b); }
+    __device__ __forceinline__ void act_done(int b) { release(ph0 + 1 + b); }
+    __device__ __forceinline__ const uint32_t* obs() { return wait(ph0 + N_PHASES - 1); }
+    __device__ __forceinline__ void obs_done() { release(ph0 + N_PHASES - 1); }
+};
+
+// ---- the per-env transform -------------------------------------------------------------------
+// valid = false only for the lanes past n_env in the tail tile of the TMA kernel: they follow the
+// same path (the ring protocol is warp-synchronous) but store nothing and count nothing.
+template <uint32_t L, class Pipe>
+__device__ __forceinline__ void env_step(const DevPtrs& p, uint32_t e, bool valid, uint32_t t, int tid, float* s_act,
+                                         float* s_obs, float* s_dt, Pipe& pipe, Acc& acc) {
     constexpr size_t P = PLANE;
-    const uint32_t* R = p.rec + rec_index(e);
     uint32_t* S = p.st + st_index(e);
     const uint32_t g = c_dc.env_offset + e;
+    const uint32_t vm = valid ? 0xFFFFFFFFu : 0u;
+    const float vf = valid ? 1.f : 0.f;
     constexpr bool kHold = (L == RUNTIME_MASK) || (L & (B_DROPOUT | B_OCCLUSION));
     const bool hold_layers = on<L>(B_DROPOUT) || on<L>(B_OCCLUSION);
-    uint32_t* slot0 = ring + tid;
-    uint32_t* slot1 = ring + RING_W * TILE + tid;
 
-    // ---- S0 (slot0) has landed (the tile loop waited for it); A0 is in flight into slot1 ----
-    const float il = on<L>(B_TIMING) ? ringf(slot0, S0_INVLAM) : 0.f;
-    const uint32_t dbits = on<L>(B_DELAY) ? slot0[S0_DELAY * TILE] : 0u;
+    // ---- S0: scalars ----
+    const uint32_t* s0 = pipe.s0();
+    const float il = on<L>(B_TIMING) ? ringf(s0, S0_INVLAM) : 0.f;
+    const uint32_t dbits = on<L>(B_DELAY) ? s0[S0_DELAY * TILE] : 0u;
     // a FRESH env (reset since its last step) has all-zero state: slack 0, prev 0, no reading,
     // timers 0, force 0 -- the reset kernel does not write the state planes
-    const uint32_t flags_raw = on<L>(B_STATEFUL) ? slot0[S0_FLAGS * TILE] : 0u;
+    const uint32_t flags_raw = on<L>(B_STATEFUL) ? s0[S0_FLAGS * TILE] : 0u;
     const bool fresh = (flags_raw & FRESH_BIT) != 0u;
     const uint32_t flags = (kHold && hold_layers && !fresh) ? flags_raw : 0u;
     uint32_t tf = 0, kf = 0;
     float mass = 0.f, ft[3] = {0.f, 0.f, 0.f};
     if (on<L>(B_FORCE)) {
-        tf = slot0[S0_TFORCE * TILE];
-        mass = ringf(slot0, S0_MASS);
+        tf = s0[S0_TFORCE * TILE];
+        mass = ringf(s0, S0_MASS);
         if (!fresh) {
-            kf = slot0[S0_KF * TILE];
+            kf = s0[S0_KF * TILE];
 #pragma unroll
-            for (int c = 0; c < 3; ++c) ft[c] = ringf(slot0, S0_FTRIG + c);
+            for (int c = 0; c < 3; ++c) ft[c] = ringf(s0, S0_FTRIG + c);
         }
     }
-    issue_act<L>(slot0, R, S, P, 1);   // A1 -> slot0
-    cp_commit();
+    pipe.s0_done();
 
     // ---- 1. timing: 10 substeps of 8 ms + Exp(lambda); dt_env = sum [Q2] ----
     float dt_env;
@@ -170,18 +317,19 @@ __device__ __forceinline__ void env_step(const DevPtrs& p, uint32_t e, uint32_t 
         float2* d2 = reinterpret_cast<float2*>(s_dt + tid * N_SUB);
 #pragma unroll
         for (int k = 0; k < N_SUB / 2; ++k) d2[k] = make_float2(d[2 * k], d[2 * k + 1]);
-        acc.m[0] += dt_env;
-        acc.m[1] += dt_env * dt_env;
+        acc.m[0] += vf * dt_env;
+        acc.m[1] += vf * (dt_env * dt_env);
     }
 
     // ---- 2-4. actions: delay -> noise -> clamp -> backlash [Q1] ----
-    acc.n[K_DELAYED] += __popc(dbits);
+    acc.n[K_DELAYED] += __popc(dbits) & vm;
+    uint32_t n_clamp = 0, n_rail = 0, n_a1 = 0;
     float s_da = 0.f, s_da2 = 0.f, s_bl = 0.f, s_zu2 = 0.f;
     float4* a4p = reinterpret_cast<float4*>(s_act + tid * N_ACT);
+    pipe.io_wait();   // the input rows of this tile have landed
 #pragma unroll 1
     for (int b = 0; b < 5; ++b) {   // rolled: keeps the kernel inside the instruction cache
-        cp_wait<1>();                // A_b has landed
-        uint32_t* sl = (b & 1) ? slot0 : slot1;
+        const uint32_t* sl = pipe.act(b);
         float prev[4], slack[4], dneg[4], dpos[4], cact[4];
 #pragma unroll
         for (int q = 0; q < 4; ++q) {
@@ -191,10 +339,7 @@ __device__ __forceinline__ void env_step(const DevPtrs& p, uint32_t e, uint32_t 
             dpos[q] = on<L>(B_BACKLASH) ? ringf(sl, 12 + q) : 0.f;
             cact[q] = on<L>(B_ACT_NOISE) ? ringf(sl, 16 + q) : 0.f;
         }
-        // refill the slot just consumed: A_{b+2}, then the observation offsets
-        if (b + 2 < 5) issue_act<L>(sl, R, S, P, b + 2);
-        else if (b + 2 == 5) issue_obs<L>(sl, R, P);
-        cp_commit();
+        pipe.act_done(b);
 
         float zu[4], zm[4];
         if (on<L>(B_ACT_NOISE)) {
@@ -212,7 +357,7 @@ __device__ __forceinline__ void env_step(const DevPtrs& p, uint32_t e, uint32_t 
             if (on<L>(B_DELAY)) {
                 // one-step delay of flagged actuators [Q9]
                 if ((dbits >> j) & 1u) ad = prev[q];
-                S[(ST_PREV + j) * P] = __float_as_uint(a);
+                if (valid) S[(ST_PREV + j) * P] = __float_as_uint(a);
             }
             float an = ad;
             if (on<L>(B_ACT_NOISE)) {
@@ -220,7 +365,7 @@ __device__ __forceinline__ void env_step(const DevPtrs& p, uint32_t e, uint32_t 
                 an = ad + ad * (c_dc.sm * zm[q]);
                 an = an + c_dc.su * zu[q];
                 an = an + cact[q];
-                acc.n[K_CLAMPS] += (an > 1.f || an < -1.f) ? 1u : 0u;
+                n_clamp += (an > 1.f || an < -1.f) ? 1u : 0u;
                 an = fminf(fmaxf(an, -1.f), 1.f);
                 s_zu2 += zu[q] * zu[q];
             }
@@ -231,31 +376,33 @@ __device__ __forceinline__ void env_step(const DevPtrs& p, uint32_t e, uint32_t 
             if (on<L>(B_BACKLASH)) {
                 // backlash, verbatim [Q4], sgn(0) = 0 [Q3]:
                 // alpha = 1 - clamp(|sgn - s| / (|s' - s| + eps), 0, 1).  The ratio is >= 1 (alpha 0)
-                // unless s sits on the rail sgn already (num == 0: alpha 1) or s' lands on the
-                // rail within eps of it (num < den: the one case that needs the division).
+                // unless s sits on the rail sgn already (num == 0: alpha 1) or s' lands on the rail
+                // within eps of it (num < den, only when num < ~1.7e-5 in fp32): there alpha is a
+                // cancellation whose absolute error (<= 2 ulp of 1 with the fast divide) is far
+                // inside the 1e-6 budget of alpha * a_n -- so no branch.
                 const float s = slack[q];
                 const float sg = (an > 0.f) ? 1.f : ((an < 0.f) ? -1.f : 0.f);
                 const float d = (an > 0.f) ? dpos[q] : ((an < 0.f) ? dneg[q] : 0.f);
                 const float sp = fminf(fmaxf(s + an * d * dt_env, -1.f), 1.f);
                 const float num = fabsf(sg - s), den = fabsf(sp - s) + c_dc.eps;
-                // num < den only when num < ~1.7e-5 (else num + eps rounds to num in fp32); there
-                // alpha = 1 - num/den is a cancellation whose absolute error (<= 2 ulp of 1 with the
-                // fast divide) is far inside the 1e-6 budget of alpha * a_n -- so no branch.
                 const float al = (num == 0.f) ? 1.f : ((num < den) ? 1.f - __fdividef(num, den) : 0.f);
                 out = al * an;
-                acc.n[K_RAIL] += (sg != 0.f && fabsf(sp) == 1.f && sp != s) ? 1u : 0u;
-                acc.n[K_ALPHA1] += (al == 1.f) ? 1u : 0u;
-                S[(ST_SLACK + j) * P] = __float_as_uint(sp);
+                n_rail += (sg != 0.f && fabsf(sp) == 1.f && sp != s) ? 1u : 0u;
+                n_a1 += (al == 1.f) ? 1u : 0u;
+                if (valid) S[(ST_SLACK + j) * P] = __float_as_uint(sp);
             }
             s_bl += fabsf(out - an);
             ov[q] = out;
         }
         a4p[b] = make_float4(ov[0], ov[1], ov[2], ov[3]);
     }
-    acc.m[2] += s_da;
-    acc.m[3] += s_da2;
-    acc.m[4] += s_bl;
-    acc.m[5] += s_zu2;
+    acc.n[K_CLAMPS] += n_clamp & vm;
+    acc.n[K_RAIL] += n_rail & vm;
+    acc.n[K_ALPHA1] += n_a1 & vm;
+    acc.m[2] += vf * s_da;
+    acc.m[3] += vf * s_da2;
+    acc.m[4] += vf * s_bl;
+    acc.m[5] += vf * s_zu2;
 
     // ---- 5-8. fingertip markers and object position ----
     float* ro = s_obs + tid * OBS_IN;   // raw row in; out_obs (22) + out_force (3) written in place
@@ -309,11 +456,11 @@ __device__ __forceinline__ void env_step(const DevPtrs& p, uint32_t e, uint32_t 
                 }
             }
         }
-        acc.n[K_OCCLUDED] += __popc(occ);
+        acc.n[K_OCCLUDED] += __popc(occ) & vm;
     }
     uint32_t masked = 0;
     if (kHold && hold_layers) {
-        uint32_t nflags = 0;
+        uint32_t nflags = 0, n_init = 0;
         if (on<L>(B_DROPOUT)) {
             // dropout: a 13-step mask starts with probability 1 - exp(-0.2 * 0.08) per step;
             // a retrigger restarts it [Q11]
@@ -323,18 +470,19 @@ __device__ __forceinline__ void env_step(const DevPtrs& p, uint32_t e, uint32_t 
             for (int i = 0; i < N_TIPS; ++i) {
                 const uint32_t x = (i < 4) ? word_of(w0, i) : x4;
                 uint32_t tm = (flags >> (4 * i)) & 0xFu;
-                if ((unsigned long long)x < c_dc.t_drop) { tm = c_dc.hold_steps; acc.n[K_DROP_INIT] += 1; }
+                if ((unsigned long long)x < c_dc.t_drop) { tm = c_dc.hold_steps; ++n_init; }
                 if (tm > 0u) { masked |= 1u << i; tm -= 1u; }
                 nflags |= tm << (4 * i);
             }
-            acc.n[K_MASKED] += __popc(masked);
+            acc.n[K_MASKED] += __popc(masked) & vm;
+            acc.n[K_DROP_INIT] += n_init & vm;
         }
-        S[ST_FLAGS * P] = nflags | HAS_LAST_BIT;
+        if (valid) S[ST_FLAGS * P] = nflags | HAS_LAST_BIT;
     } else if (on<L>(B_STATEFUL) && fresh) {
-        S[ST_FLAGS * P] = 0u;   // clear FRESH (no hold layers: timers / has_last unused)
+        if (valid) S[ST_FLAGS * P] = 0u;   // clear FRESH (no hold layers: timers / has_last unused)
     }
     const uint32_t hold = (flags & HAS_LAST_BIT) ? (masked | occ) : 0u;
-    acc.n[K_HELD] += __popc(hold);
+    acc.n[K_HELD] += __popc(hold) & vm;
     // held tips return their last available reading [Q12]: fetch it asynchronously
     // into this thread's raw-tip slots (already consumed) while the noise below is computed.
     if (kHold && hold) {
@@ -345,7 +493,7 @@ __device__ __forceinline__ void env_step(const DevPtrs& p, uint32_t e, uint32_t 
                 for (int c = 0; c < 3; ++c) cp_async4(ro + 3 * i + c, S + (ST_LAST + 3 * i + c) * P);
     }
     cp_commit();
-    cp_wait<1>();   // the observation offsets (issued at b = 3) have landed in slot0
+    const uint32_t* ob = pipe.obs();   // the observation offsets
     // fingertips: + (correlated + misplacement offset) + 2 mm uncorrelated
     float s_zt = 0.f;
     if (on<L>(B_OBS_NOISE)) {
@@ -357,13 +505,13 @@ __device__ __forceinline__ void env_step(const DevPtrs& p, uint32_t e, uint32_t 
             for (int q = 0; q < 4; ++q) {
                 const int n = 4 * b + q;
                 if (n < 15) {
-                    tip[n] = (tip[n] + ringf(slot0, n)) + c_dc.tip_uncorr * z[q];
+                    tip[n] = (tip[n] + ringf(ob, n)) + c_dc.tip_uncorr * z[q];
                     s_zt += z[q] * z[q];
                 }
             }
         }
     }
-    acc.m[6] += s_zt;
+    acc.m[6] += vf * s_zt;
     cp_wait<0>();   // held readings
     if (kHold && hold_layers) {
 #pragma unroll
@@ -371,7 +519,7 @@ __device__ __forceinline__ void env_step(const DevPtrs& p, uint32_t e, uint32_t 
             if ((hold >> i) & 1u) {
 #pragma unroll
                 for (int c = 0; c < 3; ++c) tip[3 * i + c] = ro[3 * i + c];   // unchanged: no store
-            } else {
+            } else if (valid) {
 #pragma unroll
                 for (int c = 0; c < 3; ++c) S[(ST_LAST + 3 * i + c) * P] = __float_as_uint(tip[3 * i + c]);
             }
@@ -382,7 +530,7 @@ __device__ __forceinline__ void env_step(const DevPtrs& p, uint32_t e, uint32_t 
         float z[4];
         normals4_t<kSfuNormals>(philox(g, t, CH_OBJ_NOISE, 0), z);
 #pragma unroll
-        for (int c = 0; c < 3; ++c) obj[c] = (obj[c] + ringf(slot0, 15 + c)) + c_dc.obj_uncorr * z[c];
+        for (int c = 0; c < 3; ++c) obj[c] = (obj[c] + ringf(ob, 15 + c)) + c_dc.obj_uncorr * z[c];
     }
 
     // ---- 9. orientation noise -> noisy relative goal [Q15, Q16] ----
@@ -396,7 +544,7 @@ __device__ __forceinline__ void env_step(const DevPtrs& p, uint32_t e, uint32_t 
         float qn[4];
         if (on<L>(B_OBS_NOISE)) {
             float qu[4], tmp[4];
-            const float qc[4] = {ringf(slot0, 18), ringf(slot0, 19), ringf(slot0, 20), ringf(slot0, 21)};
+            const float qc[4] = {ringf(ob, 18), ringf(ob, 19), ringf(ob, 20), ringf(ob, 21)};
             rotation<kSfuNormals>(c_dc.rot_uncorr, philox(g, t, CH_ROT_NOISE, 0), qu);
             qmul(qc, qo, tmp);
             qmul(qu, tmp, qn);
@@ -410,6 +558,7 @@ __device__ __forceinline__ void env_step(const DevPtrs& p, uint32_t e, uint32_t 
 #pragma unroll
         for (int c = 0; c < 4; ++c) rel[c] *= sgn;
     }
+    pipe.obs_done();
 
     // ---- 10. random force: replace on trigger, decay 0.99 per step in closed form
     //           [Q17, Q18] ----
@@ -425,23 +574,25 @@ __device__ __forceinline__ void env_step(const DevPtrs& p, uint32_t e, uint32_t 
             ft[0] = ms * z0;
             ft[1] = ms * z1;
             ft[2] = ms * z2;
+            if (valid) {
 #pragma unroll
-            for (int c = 0; c < 3; ++c) S[(ST_FTRIG + c) * P] = __float_as_uint(ft[c]);
+                for (int c = 0; c < 3; ++c) S[(ST_FTRIG + c) * P] = __float_as_uint(ft[c]);
+            }
             kf = 0;
-            acc.n[K_TRIG] += 1;
+            acc.n[K_TRIG] += vm & 1u;
         } else {
             kf = (kf < 65535u) ? kf + 1u : 65535u;
-            if (fresh) {   // materialise the zeroed force of a fresh episode
+            if (fresh && valid) {   // materialise the zeroed force of a fresh episode
 #pragma unroll
                 for (int c = 0; c < 3; ++c) S[(ST_FTRIG + c) * P] = 0u;
             }
         }
-        S[ST_KF * P] = kf;
+        if (valid) S[ST_KF * P] = kf;
         const double dec = __ldg(p.dec_tab + (kf & 255u)) * __ldg(p.dec_tab + 256u + (kf >> 8));   // L1-resident
 #pragma unroll
         for (int c = 0; c < 3; ++c) f[c] = (float)((double)ft[c] * dec);
     }
-    acc.m[7] += f[0] * f[0] + f[1] * f[1] + f[2] * f[2];
+    acc.m[7] += vf * (f[0] * f[0] + f[1] * f[1] + f[2] * f[2]);
 
     // ---- outputs in place over the raw row: [rel 4, tips 15, obj 3 | force 3] ----
     {
@@ -457,8 +608,121 @@ __device__ __forceinline__ void env_step(const DevPtrs& p, uint32_t e, uint32_t 
     }
 }
 
-// Prefetch policy (DR_PREFETCH env at dr_init): 0 = none, 1 = the current tile at its start,
-// 2 = the next tile at the start of the current one (TMA bulk L2 prefetch; A/B experiments).
+// ---- tile output store (shared by both kernels) ----
+__device__ __forceinline__ void store_tile(uint32_t e0, uint32_t cnt, int tid, const float* s_act, const float* s_obs,
+                                           const float* s_dt, float* out_actions, float* out_obs, float* out_dt,
+                                           float* out_force) {
+    if (cnt == (uint32_t)TILE) {
+        const float4* s4 = reinterpret_cast<const float4*>(s_act);
+        float4* a4 = reinterpret_cast<float4*>(out_actions + (size_t)e0 * N_ACT);
+#pragma unroll
+        for (int i = tid; i < TILE * N_ACT / 4; i += STEP_THREADS) __stcs(a4 + i, s4[i]);
+        const float4* d4s = reinterpret_cast<const float4*>(s_dt);
+        float4* d4 = reinterpret_cast<float4*>(out_dt + (size_t)e0 * N_SUB);
+#pragma unroll
+        for (int i = tid; i < TILE * N_SUB / 4; i += STEP_THREADS) __stcs(d4 + i, d4s[i]);
+        // out_obs rows (22 floats = 11 float2) read from stride-26 smem rows
+        float2* oo = reinterpret_cast<float2*>(out_obs + (size_t)e0 * OBS_OUT);
+        for (int i = tid; i < TILE * 11; i += STEP_THREADS) {
+            const int r = i / 11, k = i - r * 11;
+            __stcs(oo + i, reinterpret_cast<const float2*>(s_obs + r * OBS_IN)[k]);
+        }
+        float* of = out_force + (size_t)e0 * 3;
+        for (int i = tid; i < TILE * 3; i += STEP_THREADS) {
+            const int r = i / 3, k = i - r * 3;
+            __stcs(of + i, s_obs[r * OBS_IN + 22 + k]);
+        }
+    } else {
+        for (uint32_t i = tid; i < cnt * N_ACT; i += STEP_THREADS) out_actions[(size_t)e0 * N_ACT + i] = s_act[i];
+        for (uint32_t i = tid; i < cnt * N_SUB; i += STEP_THREADS) out_dt[(size_t)e0 * N_SUB + i] = s_dt[i];
+        for (uint32_t i = tid; i < cnt * OBS_OUT; i += STEP_THREADS) {
+            const uint32_t r = i / OBS_OUT, k = i - r * OBS_OUT;
+            out_obs[(size_t)e0 * OBS_OUT + i] = s_obs[r * OBS_IN + k];
+        }
+        for (uint32_t i = tid; i < cnt * 3; i += STEP_THREADS) {
+            const uint32_t r = i / 3, k = i - r * 3;
+            out_force[(size_t)e0 * 3 + i] = s_obs[r * OBS_IN + 22 + k];
+        }
+    }
+}
+
+// ---- stats: register accumulators -> CTA reduction -> last-CTA fixed-order reduction ----
+template <uint32_t L>
+__device__ __forceinline__ void reduce_stats(const DevPtrs& p, const Acc& acc, uint32_t my_envs, uint32_t t,
+                                             double* s_red, int* s_last) {
+    const int tid = threadIdx.x;
+    const int lane = tid & 31, wid = tid >> 5;
+    constexpr int NW = STEP_THREADS / 32;
+    __syncthreads();
+    {
+        auto red = [&](int i, double x) {
+#pragma unroll
+            for (int o = 16; o > 0; o >>= 1) x += __shfl_xor_sync(0xFFFFFFFFu, x, o);
+            if (lane == 0) s_red[i * NW + wid] = x;
+        };
+        red(0, (double)my_envs);
+        red(1, (double)acc.n[K_DELAYED]);
+        red(2, (double)acc.n[K_DROP_INIT]);
+        red(3, (double)acc.n[K_MASKED]);
+        red(4, (double)acc.n[K_OCCLUDED]);
+        red(5, (double)acc.n[K_HELD]);
+        red(6, (double)acc.n[K_TRIG]);
+        red(7, (double)acc.n[K_RAIL]);
+        red(8, (double)acc.n[K_ALPHA1]);
+        red(9, on<L>(B_BACKLASH) ? (double)my_envs * N_ACT - (double)acc.n[K_ALPHA1] : 0.0);
+        red(10, 0.0);
+        red(11, (double)acc.n[K_CLAMPS]);
+        red(12, 0.0); red(13, 0.0); red(14, 0.0); red(15, 0.0);
+#pragma unroll
+        for (int i = 0; i < 8; ++i) red(16 + i, (double)acc.m[i]);
+    }
+    __syncthreads();
+    if (tid < N_STATS) {
+        double sum = 0.0;
+        if (tid < N_STATS - 8)
+#pragma unroll
+            for (int w = 0; w < NW; ++w) sum += s_red[tid * NW + w];
+        p.partials[(size_t)blockIdx.x * N_STATS + tid] = sum;
+    }
+    __threadfence();
+    __syncthreads();
+    if (tid == 0) {
+        const unsigned long long prev = atomicAdd(&p.ctl[1], 1ull);
+        *s_last = (prev == (unsigned long long)gridDim.x - 1ull);
+    }
+    __syncthreads();
+    if (*s_last) {
+        __threadfence();
+        const uint32_t slot = t & 1u;
+        for (int s = wid; s < N_STATS; s += NW) {
+            double sum = 0.0;
+            for (uint32_t b = lane; b < gridDim.x; b += 32) sum += __ldcg(p.partials + (size_t)b * N_STATS + s);
+#pragma unroll
+            for (int o = 16; o > 0; o >>= 1) sum += __shfl_xor_sync(0xFFFFFFFFu, sum, o);
+            if (lane == 0) p.stats[slot * N_STATS + s] = sum;
+        }
+        __syncthreads();
+        if (tid == 0) {
+            const unsigned long long res = atomicExch(&p.ctl[2], 0ull);
+            p.stats[slot * N_STATS + 10] = (double)res;
+            p.ctl[1] = 0ull;
+            p.ctl[0] = (unsigned long long)t + 1ull;
+            __threadfence();
+        }
+    }
+}
+
+__device__ __forceinline__ void acc_zero(Acc& acc) {
+#pragma unroll
+    for (int k = 0; k < K_COUNT; ++k) acc.n[k] = 0u;
+#pragma unroll
+    for (int k = 0; k < 8; ++k) acc.m[k] = 0.f;
+}
+
+// ============================================================================================
+// Kernel A (PipeThread): per-thread cp.async ring.  Prefetch policy (DR_PREFETCH): 0 = none,
+// 1 = TMA L2 prefetch of the current tile, 2 = of the next tile (A/B experiments).
+// ============================================================================================
 template <uint32_t L, int PF>
 __global__ void __launch_bounds__(STEP_THREADS, STEP_MIN_CTAS)
     step_kernel(const DevPtrs p, const float* __restrict__ actions, const float* __restrict__ raw_obs,
@@ -467,7 +731,7 @@ __global__ void __launch_bounds__(STEP_THREADS, STEP_MIN_CTAS)
     __shared__ __align__(16) float s_act[TILE * N_ACT];   // actions in, out_actions out (in place)
     __shared__ __align__(16) float s_obs[TILE * OBS_IN];  // raw_obs in, out_obs + out_force out (stride 26)
     __shared__ __align__(16) float s_dt[TILE * N_SUB];
-    extern __shared__ __align__(16) uint32_t s_ring[];   // [2][RING_W][TILE] (dynamic: > 48 KB total)
+    extern __shared__ __align__(128) uint32_t s_ring[];   // [2][RING_W][TILE] (dynamic: > 48 KB total)
     __shared__ int s_last;
 
     const int tid = threadIdx.x;
@@ -476,10 +740,7 @@ __global__ void __launch_bounds__(STEP_THREADS, STEP_MIN_CTAS)
     constexpr size_t P = PLANE;
     if (PF == 2) prefetch_tile<L>(p, actions, raw_obs, blockIdx.x, n_env);
     Acc acc;
-#pragma unroll
-    for (int k = 0; k < K_COUNT; ++k) acc.n[k] = 0u;
-#pragma unroll
-    for (int k = 0; k < 8; ++k) acc.m[k] = 0.f;
+    acc_zero(acc);
     uint32_t my_envs = 0;
 
     for (uint32_t tile = blockIdx.x; tile < n_tiles; tile += gridDim.x) {
@@ -503,111 +764,103 @@ __global__ void __launch_bounds__(STEP_THREADS, STEP_MIN_CTAS)
         }
         cp_commit();
         const bool mine = (uint32_t)tid < cnt;
-        if (mine) issue_s0<L>(s_ring + tid, p.rec + rec_index(e0 + tid), p.st + st_index(e0 + tid), P);  // S0 -> slot0
+        const uint32_t* R = p.rec + rec_index(e0 + tid);
+        const uint32_t* S = p.st + st_index(e0 + tid);
+        if (mine) issue_s0<L>(s_ring + tid, R, S, P);                          // S0 -> slot0
         cp_commit();
-        if (mine) issue_act<L>(s_ring + RING_W * TILE + tid, p.rec + rec_index(e0 + tid), p.st + st_index(e0 + tid), P, 0);  // A0 -> slot1
+        if (mine) issue_act<L>(s_ring + RING_W * TILE + tid, R, S, P, 0);      // A0 -> slot1
         cp_commit();
         cp_wait<1>();      // staging + S0 of this thread
         __syncthreads();   // everyone's staging copies
         if (mine) {
-            env_step<L>(p, e0 + tid, t, tid, s_act, s_obs, s_dt, s_ring, acc);
+            PipeThread<L> pipe{s_ring + tid, s_ring + RING_W * TILE + tid, R, S};
+            env_step<L>(p, e0 + tid, true, t, tid, s_act, s_obs, s_dt, pipe, acc);
             ++my_envs;
         }
         cp_wait<0>();
         __syncthreads();
-        // store the output tiles (coalesced)
-        if (full) {
-            const float4* s4 = reinterpret_cast<const float4*>(s_act);
-            float4* a4 = reinterpret_cast<float4*>(out_actions + (size_t)e0 * N_ACT);
-#pragma unroll
-            for (int i = tid; i < TILE * N_ACT / 4; i += STEP_THREADS) __stcs(a4 + i, s4[i]);
-            const float4* d4s = reinterpret_cast<const float4*>(s_dt);
-            float4* d4 = reinterpret_cast<float4*>(out_dt + (size_t)e0 * N_SUB);
-#pragma unroll
-            for (int i = tid; i < TILE * N_SUB / 4; i += STEP_THREADS) __stcs(d4 + i, d4s[i]);
-            // out_obs rows (22 floats = 11 float2) read from stride-26 smem rows
-            float2* oo = reinterpret_cast<float2*>(out_obs + (size_t)e0 * OBS_OUT);
-            for (int i = tid; i < TILE * 11; i += STEP_THREADS) {
-                const int r = i / 11, k = i - r * 11;
-                __stcs(oo + i, reinterpret_cast<const float2*>(s_obs + r * OBS_IN)[k]);
-            }
-            float* of = out_force + (size_t)e0 * 3;
-            for (int i = tid; i < TILE * 3; i += STEP_THREADS) {
-                const int r = i / 3, k = i - r * 3;
-                __stcs(of + i, s_obs[r * OBS_IN + 22 + k]);
-            }
-        } else {
-            for (uint32_t i = tid; i < cnt * N_ACT; i += STEP_THREADS) out_actions[(size_t)e0 * N_ACT + i] = s_act[i];
-            for (uint32_t i = tid; i < cnt * N_SUB; i += STEP_THREADS) out_dt[(size_t)e0 * N_SUB + i] = s_dt[i];
-            for (uint32_t i = tid; i < cnt * OBS_OUT; i += STEP_THREADS) {
-                const uint32_t r = i / OBS_OUT, k = i - r * OBS_OUT;
-                out_obs[(size_t)e0 * OBS_OUT + i] = s_obs[r * OBS_IN + k];
-            }
-            for (uint32_t i = tid; i < cnt * 3; i += STEP_THREADS) {
-                const uint32_t r = i / 3, k = i - r * 3;
-                out_force[(size_t)e0 * 3 + i] = s_obs[r * OBS_IN + 22 + k];
-            }
-        }
+        store_tile(e0, cnt, tid, s_act, s_obs, s_dt, out_actions, out_obs, out_dt, out_force);
     }
+    reduce_stats<L>(p, acc, my_envs, t, reinterpret_cast<double*>(s_obs), &s_last);
+}
 
-    // ---- 12. stats: CTA reduction in shared memory, last CTA reduces the partials ----
-    __syncthreads();
-    double* s_red = reinterpret_cast<double*>(s_obs);   // [N_STATS][STEP_THREADS / 32] (reuses s_obs)
-    const int lane = tid & 31, wid = tid >> 5;
-    {
-        auto red = [&](int i, double x) {
+// ============================================================================================
+// Kernel B (PipeTma, default): CTA-wide TMA ring of TMA_SLOTS phase slots + TMA input tiles.
+// ============================================================================================
+constexpr size_t STEP_TMA_DYN_SMEM = (size_t)TMA_SLOTS * RING_W * TILE * sizeof(uint32_t);
+
+template <uint32_t L>
+__device__ __forceinline__ void tma_issue_io(const float* actions, const float* raw_obs, float* s_act, float* s_obs,
+                                             TmaShared* ts, uint32_t it, uint32_t n_my, uint32_t n_env) {
+    if (it >= n_my) return;
+    const uint32_t tile = blockIdx.x + it * gridDim.x;
+    const uint32_t e0 = tile * TILE;
+    const uint32_t cnt = min((uint32_t)TILE, n_env - e0);
+    const uint32_t ba = cnt * N_ACT * 4u;             // multiple of 16
+    const uint32_t bo = (cnt * OBS_IN * 4u) & ~15u;   // odd tail: the last 8 bytes are loaded by hand
+    mbar_arrive_expect_tx(&ts->io_full, ba + bo);
+    tma_load(s_act, actions + (size_t)e0 * N_ACT, ba, &ts->io_full);
+    tma_load(s_obs, raw_obs + (size_t)e0 * OBS_IN, bo, &ts->io_full);
+}
+
+template <uint32_t L>
+__global__ void __launch_bounds__(STEP_THREADS, STEP_MIN_CTAS)
+    step_kernel_tma(const DevPtrs p, const float* __restrict__ actions, const float* __restrict__ raw_obs,
+                    float* __restrict__ out_actions, float* __restrict__ out_obs, float* __restrict__ out_dt,
+                    float* __restrict__ out_force, uint32_t n_env) {
+    __shared__ __align__(128) float s_act[TILE * N_ACT];   // TMA destination; out_actions in place
+    __shared__ __align__(128) float s_obs[TILE * OBS_IN];  // TMA destination; out_obs + out_force in place
+    __shared__ __align__(16) float s_dt[TILE * N_SUB];
+    __shared__ TmaShared ts;
+    __shared__ int s_last;
+    extern __shared__ __align__(128) uint32_t s_ring[];    // [TMA_SLOTS][RING_W][TILE]
+
+    const int tid = threadIdx.x;
+    const uint32_t t = (uint32_t)p.ctl[0];
+    const uint32_t n_tiles = (n_env + TILE - 1) / TILE;
+    const uint32_t n_my = (blockIdx.x < n_tiles) ? (n_tiles - blockIdx.x + gridDim.x - 1) / gridDim.x : 0u;
+    if (tid == 0) {
 #pragma unroll
-            for (int o = 16; o > 0; o >>= 1) x += __shfl_xor_sync(0xFFFFFFFFu, x, o);
-            if (lane == 0) s_red[i * (STEP_THREADS / 32) + wid] = x;
-        };
-        red(0, (double)my_envs);
-        red(1, (double)acc.n[K_DELAYED]);
-        red(2, (double)acc.n[K_DROP_INIT]);
-        red(3, (double)acc.n[K_MASKED]);
-        red(4, (double)acc.n[K_OCCLUDED]);
-        red(5, (double)acc.n[K_HELD]);
-        red(6, (double)acc.n[K_TRIG]);
-        red(7, (double)acc.n[K_RAIL]);
-        red(8, (double)acc.n[K_ALPHA1]);
-        red(9, on<L>(B_BACKLASH) ? (double)my_envs * N_ACT - (double)acc.n[K_ALPHA1] : 0.0);
-        red(10, 0.0);
-        red(11, (double)acc.n[K_CLAMPS]);
-        red(12, 0.0); red(13, 0.0); red(14, 0.0); red(15, 0.0);
-#pragma unroll
-        for (int i = 0; i < 8; ++i) red(16 + i, (double)acc.m[i]);
+        for (int s = 0; s < TMA_SLOTS; ++s) {
+            mbar_init(&ts.full[s], 1);
+            ts.rel[s] = 0u;
+        }
+        mbar_init(&ts.io_full, 1);
+        ts.io_rel = 0u;
+        fence_mbar_init();
     }
-    __syncthreads();
-    if (tid < N_STATS) {
-        double sum = 0.0;
-        if (tid < N_STATS - 8)
-#pragma unroll
-            for (int w = 0; w < STEP_THREADS / 32; ++w) sum += s_red[tid * (STEP_THREADS / 32) + w];
-        p.partials[(size_t)blockIdx.x * N_STATS + tid] = sum;
-    }
-    __threadfence();
     __syncthreads();
     if (tid == 0) {
-        const unsigned long long prev = atomicAdd(&p.ctl[1], 1ull);
-        s_last = (prev == (unsigned long long)gridDim.x - 1ull);
+        for (uint32_t ph = 0; ph < (uint32_t)TMA_SLOTS; ++ph) tma_issue_phase<L>(p, s_ring, &ts, ph, n_my, n_tiles);
+        tma_issue_io<L>(actions, raw_obs, s_act, s_obs, &ts, 0, n_my, n_env);
     }
-    __syncthreads();
-    if (s_last) {
-        __threadfence();
-        const uint32_t slot = t & 1u;
-        for (int s = wid; s < N_STATS; s += STEP_THREADS / 32) {
-            double sum = 0.0;
-            for (uint32_t b = lane; b < gridDim.x; b += 32) sum += __ldcg(p.partials + (size_t)b * N_STATS + s);
-#pragma unroll
-            for (int o = 16; o > 0; o >>= 1) sum += __shfl_xor_sync(0xFFFFFFFFu, sum, o);
-            if (lane == 0) p.stats[slot * N_STATS + s] = sum;
+    Acc acc;
+    acc_zero(acc);
+    uint32_t my_envs = 0;
+
+    for (uint32_t it = 0; it < n_my; ++it) {
+        const uint32_t tile = blockIdx.x + it * gridDim.x;
+        const uint32_t e0 = tile * TILE;
+        const uint32_t cnt = min((uint32_t)TILE, n_env - e0);
+        const bool mine = (uint32_t)tid < cnt;
+        if ((cnt & 1u) && tid == (int)cnt - 1) {
+            // odd tail tile: the TMA copy was rounded down to 16 B; this env's last 2 words by hand
+            mbar_wait(&ts.io_full, it & 1u);
+            const float2 v = *reinterpret_cast<const float2*>(raw_obs + (size_t)(e0 + cnt) * OBS_IN - 2);
+            *reinterpret_cast<float2*>(s_obs + cnt * OBS_IN - 2) = v;
         }
-        __syncthreads();
-        if (tid == 0) {
-            const unsigned long long res = atomicExch(&p.ctl[2], 0ull);
-            p.stats[slot * N_STATS + 10] = (double)res;
-            p.ctl[1] = 0ull;
-            p.ctl[0] = (unsigned long long)t + 1ull;
-            __threadfence();
+        PipeTma<L> pipe{&p, s_ring, &ts, it * N_PHASES, it, n_my, n_tiles, tid};
+        env_step<L>(p, e0 + tid, mine, t, tid, s_act, s_obs, s_dt, pipe, acc);
+        my_envs += mine ? 1u : 0u;
+        __syncthreads();   // all output rows are in shared memory
+        store_tile(e0, cnt, tid, s_act, s_obs, s_dt, out_actions, out_obs, out_dt, out_force);
+        // the last warp done storing issues the next tile's input rows into the same buffers
+        __syncwarp();
+        if ((tid & 31) == 0 && atomicAdd(&ts.io_rel, 1u) == (uint32_t)(STEP_THREADS / 32) - 1u) {
+            ts.io_rel = 0u;
+            fence_proxy_async();
+            tma_issue_io<L>(actions, raw_obs, s_act, s_obs, &ts, it + 1, n_my, n_env);
         }
     }
+    reduce_stats<L>(p, acc, my_envs, t, reinterpret_cast<double*>(s_dt), &s_last);
 }
