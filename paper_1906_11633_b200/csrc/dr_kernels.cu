@@ -109,9 +109,12 @@ static int g_prefetch = 0;
 
 void set_step_prefetch(int mode) { g_prefetch = (mode < 0 || mode > 2) ? 0 : mode; }
 
-// Ring pipeline of the step kernel (DR_PIPE at dr_init): 1 = CTA-wide TMA bulk-copy ring
-// (step_kernel_tma, default), 0 = per-thread cp.async ring (step_kernel; A/B experiments).
-static int g_pipe = 1;
+// Ring pipeline of the step kernel (DR_PIPE at dr_init): 0 = per-thread cp.async ring
+// (step_kernel, default), 1 = CTA-wide TMA bulk-copy ring (step_kernel_tma).  Measured on B200 at
+// 1M envs (profiles/round1_notes.md): 3.65e9 vs 3.36e9 env-steps/s -- the CTA-wide ring couples
+// the four warps of a CTA (slot refill waits for the slowest warp, barrier stall 0.65/issue),
+// which costs more than the LDGSTS issue slots it saves.
+static int g_pipe = 0;
 
 void set_step_pipe(int mode) { g_pipe = (mode == 0) ? 0 : 1; }
 

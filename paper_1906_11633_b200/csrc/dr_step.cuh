@@ -8,12 +8,14 @@
 // consumed in seven phases -- S0 (scalars), A0..A4 (4 actuators each), OB (observation offsets)
 // -- streamed through a shared-memory ring so that in-flight bytes live in shared memory, not in
 // registers.  Two interchangeable pipelines feed the ring:
-//   * PipeTma (default, step_kernel_tma): a 3-slot CTA-wide ring filled by TMA bulk copies
+//   * PipeThread (step_kernel, default): a per-thread 2-slot ring filled with 4-byte cp.async
+//     (LDGSTS) -- each thread's pipeline is independent of the other warps'.
+//   * PipeTma (step_kernel_tma, DR_PIPE=1): a 3-slot CTA-wide ring filled by TMA bulk copies
 //     (cp.async.bulk + mbarrier complete_tx); a slot is refilled two phases ahead by the last
 //     warp to release it (smem atomic), so no thread ever blocks to produce; the row-major input
 //     tile is also a TMA bulk copy, and the next tile's inputs are issued as soon as the current
-//     tile's outputs are stored.
-//   * PipeThread (step_kernel): a per-thread 2-slot ring filled with 4-byte cp.async (LDGSTS).
+//     tile's outputs are stored.  Measured slower (the ring couples the CTA's warps); kept as an
+//     A/B alternative and parity-tested.
 // Outputs are written in place over the input rows in shared memory (out_actions over actions,
 // out_obs + out_force over raw_obs) and stored with coalesced 128/64-bit stores.  Held fingertip
 // readings are fetched with per-thread cp.async while the fingertip noise is computed.  Stats:
@@ -268,7 +270,6 @@ __device__ __forceinline__ void env_step(const DevPtrs& p, uint32_t e, bool vali
     uint32_t* S = p.st + st_index(e);
     const uint32_t g = c_dc.env_offset + e;
     const uint32_t vm = valid ? 0xFFFFFFFFu : 0u;
-    const float vf = valid ? 1.f : 0.f;
     constexpr bool kHold = (L == RUNTIME_MASK) || (L & (B_DROPOUT | B_OCCLUSION));
     const bool hold_layers = on<L>(B_DROPOUT) || on<L>(B_OCCLUSION);
 
@@ -317,8 +318,8 @@ __device__ __forceinline__ void env_step(const DevPtrs& p, uint32_t e, bool vali
         float2* d2 = reinterpret_cast<float2*>(s_dt + tid * N_SUB);
 #pragma unroll
         for (int k = 0; k < N_SUB / 2; ++k) d2[k] = make_float2(d[2 * k], d[2 * k + 1]);
-        acc.m[0] += vf * dt_env;
-        acc.m[1] += vf * (dt_env * dt_env);
+        acc.m[0] += valid ? dt_env : 0.f;
+        acc.m[1] += valid ? dt_env * dt_env : 0.f;
     }
 
     // ---- 2-4. actions: delay -> noise -> clamp -> backlash [Q1] ----
@@ -399,10 +400,10 @@ __device__ __forceinline__ void env_step(const DevPtrs& p, uint32_t e, bool vali
     acc.n[K_CLAMPS] += n_clamp & vm;
     acc.n[K_RAIL] += n_rail & vm;
     acc.n[K_ALPHA1] += n_a1 & vm;
-    acc.m[2] += vf * s_da;
-    acc.m[3] += vf * s_da2;
-    acc.m[4] += vf * s_bl;
-    acc.m[5] += vf * s_zu2;
+    acc.m[2] += valid ? s_da : 0.f;
+    acc.m[3] += valid ? s_da2 : 0.f;
+    acc.m[4] += valid ? s_bl : 0.f;
+    acc.m[5] += valid ? s_zu2 : 0.f;
 
     // ---- 5-8. fingertip markers and object position ----
     float* ro = s_obs + tid * OBS_IN;   // raw row in; out_obs (22) + out_force (3) written in place
@@ -511,7 +512,7 @@ __device__ __forceinline__ void env_step(const DevPtrs& p, uint32_t e, bool vali
             }
         }
     }
-    acc.m[6] += vf * s_zt;
+    acc.m[6] += valid ? s_zt : 0.f;
     cp_wait<0>();   // held readings
     if (kHold && hold_layers) {
 #pragma unroll
@@ -592,7 +593,7 @@ __device__ __forceinline__ void env_step(const DevPtrs& p, uint32_t e, bool vali
 #pragma unroll
         for (int c = 0; c < 3; ++c) f[c] = (float)((double)ft[c] * dec);
     }
-    acc.m[7] += vf * (f[0] * f[0] + f[1] * f[1] + f[2] * f[2]);
+    acc.m[7] += valid ? f[0] * f[0] + f[1] * f[1] + f[2] * f[2] : 0.f;   // select, not multiply: invalid lanes may hold NaN
 
     // ---- outputs in place over the raw row: [rel 4, tips 15, obj 3 | force 3] ----
     {

@@ -360,3 +360,11 @@ def test_value_view_isolation_and_invariants_1M(torch_cuda):
         assert s[0] == n
     finally:
         ctx.close()
+
+
+@pytest.mark.parametrize("n,mask", [(4, FULL), (1000, FULL), (257, CFG2), (300, DROPOUT | OCCLUSION | FORCE)])
+def test_tma_pipeline_variant(torch_cuda, monkeypatch, n, mask):
+    """The CTA-wide TMA bulk-copy ring (DR_PIPE=1, step_kernel_tma) meets the same parity contract,
+    including odd tail tiles (hand-loaded raw_obs remainder) and invalid tail lanes."""
+    monkeypatch.setenv("DR_PIPE", "1")
+    run_pair(torch_cuda, mask, n, 12, n_frames=12, resets={6: (np.arange(n) % 3 == 0).astype(np.uint8)})
