@@ -116,7 +116,13 @@ void set_step_prefetch(int mode) { g_prefetch = (mode < 0 || mode > 2) ? 0 : mod
 // which costs more than the LDGSTS issue slots it saves.
 static int g_pipe = 0;
 
-void set_step_pipe(int mode) { g_pipe = (mode == 0) ? 0 : 1; }
+void set_step_pipe(int mode) { g_pipe = (mode < 0 || mode > 2) ? 0 : mode; }
+
+static StepFn step_fn_warp(uint32_t m) {
+    if (m == MASK_FULL) return step_kernel_warp<MASK_FULL>;
+    if (m == MASK_CFG2) return step_kernel_warp<MASK_CFG2>;
+    return step_kernel_warp<RUNTIME_MASK>;
+}
 
 template <int PF>
 static StepFn step_fn_pf(uint32_t m) {
@@ -134,6 +140,7 @@ static StepFn step_fn_tma(uint32_t m) {
 static StepFn step_fn(uint32_t layer_mask) {
     const uint32_t m = layer_mask & 0xFFu;
     if (g_pipe == 1) return step_fn_tma(m);
+    if (g_pipe == 2) return step_fn_warp(m);
     if (g_prefetch == 0) return step_fn_pf<0>(m);
     if (g_prefetch == 2) return step_fn_pf<2>(m);
     return step_fn_pf<1>(m);

@@ -205,6 +205,68 @@ struct PipeThread {
     __device__ __forceinline__ void obs_done() {}
 };
 
+// Warp-cooperative ring (DR_PIPE=2): the same 2-slot layout as PipeThread, but a warp fills its
+// 32-env column segment of a slot with 16-byte cp.async.cg (L1 bypass): one instruction moves 4
+// planes x 128 B (lane l: plane l >> 3, bytes 16 (l & 7)), i.e. 4x fewer LDGSTS and no L1 lines.
+// Lanes read words other lanes copied, so every hand-over is a __syncwarp.
+template <uint32_t L>
+struct PipeWarp {
+    uint32_t* slot0;   // s_ring (row 0, column 0)
+    uint32_t* slot1;
+    const uint32_t* Rw;   // record tile block + this warp's first column
+    const uint32_t* Sw;   // state tile block + this warp's first column
+    int tid, lane, wcol;  // wcol = 32 * warp
+    __device__ __forceinline__ void planes(uint32_t* slot, int row, const uint32_t* src, int n) {
+        const int sub = 4 * (lane & 7);
+        for (int i = 0; i < n; i += 4) {
+            const int pi = i + (lane >> 3);
+            if (pi < n) cp_async16(slot + (row + pi) * TILE + wcol + sub, src + pi * TILE + sub);
+        }
+    }
+    __device__ __forceinline__ void issue_s0() {
+        if (on<L>(B_TIMING) || on<L>(B_DELAY) || on<L>(B_FORCE)) planes(slot0, 0, Rw, 4);   // record planes 0..3
+        if (on<L>(B_FORCE)) planes(slot0, S0_FLAGS, Sw + ST_FLAGS * TILE, 5);                // state planes 55..59
+        else if (on<L>(B_STATEFUL)) planes(slot0, S0_FLAGS, Sw + ST_FLAGS * TILE, 1);
+    }
+    __device__ __forceinline__ void issue_act(uint32_t* sl, int b) {
+        if (on<L>(B_DELAY)) planes(sl, 0, Sw + (ST_PREV + 4 * b) * TILE, 4);
+        if (on<L>(B_BACKLASH)) {
+            planes(sl, 4, Sw + (ST_SLACK + 4 * b) * TILE, 4);
+            planes(sl, 8, Rw + (REC_DNEG + 4 * b) * TILE, 4);
+            planes(sl, 12, Rw + (REC_DPOS + 4 * b) * TILE, 4);
+        }
+        if (on<L>(B_ACT_NOISE)) planes(sl, 16, Rw + (REC_CACT + 4 * b) * TILE, 4);
+    }
+    __device__ __forceinline__ void issue_obs(uint32_t* sl) {
+        if (on<L>(B_OBS_NOISE)) planes(sl, 0, Rw + REC_OFFTIP * TILE, 22);
+    }
+    __device__ __forceinline__ const uint32_t* s0() { return slot0 + tid; }   // the tile loop waited
+    __device__ __forceinline__ void s0_done() {
+        __syncwarp();
+        issue_act(slot0, 1);
+        cp_commit();
+    }
+    __device__ __forceinline__ void io_wait() {}
+    __device__ __forceinline__ const uint32_t* act(int b) {
+        cp_wait<1>();
+        __syncwarp();
+        return ((b & 1) ? slot0 : slot1) + tid;
+    }
+    __device__ __forceinline__ void act_done(int b) {
+        uint32_t* sl = (b & 1) ? slot0 : slot1;
+        __syncwarp();
+        if (b + 2 < 5) issue_act(sl, b + 2);
+        else if (b + 2 == 5) issue_obs(sl);
+        cp_commit();
+    }
+    __device__ __forceinline__ const uint32_t* obs() {
+        cp_wait<1>();
+        __syncwarp();
+        return slot0 + tid;
+    }
+    __device__ __forceinline__ void obs_done() {}
+};
+
 // CTA-wide TMA ring: phase ph (counted over this CTA's tiles) lives in slot ph % NS.
 constexpr int TMA_SLOTS = 3;
 struct TmaShared {
@@ -864,4 +926,60 @@ __global__ void __launch_bounds__(STEP_THREADS, STEP_MIN_CTAS)
         }
     }
     reduce_stats<L>(p, acc, my_envs, t, reinterpret_cast<double*>(s_dt), &s_last);
+}
+
+// ============================================================================================
+// Kernel C (PipeWarp, DR_PIPE=2): warp-cooperative 16-byte cp.async.cg ring.
+// ============================================================================================
+template <uint32_t L>
+__global__ void __launch_bounds__(STEP_THREADS, STEP_MIN_CTAS)
+    step_kernel_warp(const DevPtrs p, const float* __restrict__ actions, const float* __restrict__ raw_obs,
+                     float* __restrict__ out_actions, float* __restrict__ out_obs, float* __restrict__ out_dt,
+                     float* __restrict__ out_force, uint32_t n_env) {
+    __shared__ __align__(16) float s_act[TILE * N_ACT];
+    __shared__ __align__(16) float s_obs[TILE * OBS_IN];
+    __shared__ __align__(16) float s_dt[TILE * N_SUB];
+    extern __shared__ __align__(128) uint32_t s_ring[];   // [2][RING_W][TILE]
+    __shared__ int s_last;
+
+    const int tid = threadIdx.x, lane = tid & 31, wcol = tid & ~31;
+    const uint32_t t = (uint32_t)p.ctl[0];
+    const uint32_t n_tiles = (n_env + TILE - 1) / TILE;
+    Acc acc;
+    acc_zero(acc);
+    uint32_t my_envs = 0;
+
+    for (uint32_t tile = blockIdx.x; tile < n_tiles; tile += gridDim.x) {
+        const uint32_t e0 = tile * TILE;
+        const uint32_t cnt = min((uint32_t)TILE, n_env - e0);
+        const bool full = cnt == (uint32_t)TILE;
+        __syncthreads();   // previous tile's smem fully stored
+        if (full) {
+            const float* a = actions + (size_t)e0 * N_ACT;
+            const float* o = raw_obs + (size_t)e0 * OBS_IN;
+#pragma unroll
+            for (int i = tid; i < TILE * N_ACT / 4; i += STEP_THREADS) cp_async16(s_act + 4 * i, a + 4 * i);
+#pragma unroll
+            for (int i = tid; i < TILE * OBS_IN / 4; i += STEP_THREADS) cp_async16(s_obs + 4 * i, o + 4 * i);
+        } else {
+            for (uint32_t i = tid; i < cnt * N_ACT; i += STEP_THREADS) cp_async4(s_act + i, actions + (size_t)e0 * N_ACT + i);
+            for (uint32_t i = tid; i < cnt * OBS_IN; i += STEP_THREADS) cp_async4(s_obs + i, raw_obs + (size_t)e0 * OBS_IN + i);
+        }
+        cp_commit();
+        PipeWarp<L> pipe{s_ring, s_ring + RING_W * TILE, p.rec + rec_index(e0) + wcol, p.st + st_index(e0) + wcol, tid,
+                         lane, wcol};
+        pipe.issue_s0();                   // S0 -> slot0 (this warp's columns)
+        cp_commit();
+        pipe.issue_act(pipe.slot1, 0);     // A0 -> slot1
+        cp_commit();
+        cp_wait<1>();      // staging + S0
+        __syncthreads();   // everyone's staging copies (and each warp's S0)
+        const bool mine = (uint32_t)tid < cnt;
+        env_step<L>(p, e0 + tid, mine, t, tid, s_act, s_obs, s_dt, pipe, acc);
+        my_envs += mine ? 1u : 0u;
+        cp_wait<0>();
+        __syncthreads();
+        store_tile(e0, cnt, tid, s_act, s_obs, s_dt, out_actions, out_obs, out_dt, out_force);
+    }
+    reduce_stats<L>(p, acc, my_envs, t, reinterpret_cast<double*>(s_obs), &s_last);
 }
