@@ -464,7 +464,7 @@ int dr_init(const dr_params* params, int64_t n_env, uint64_t seed) {
     const char* pf = std::getenv("DR_PREFETCH");
     const char* pp = std::getenv("DR_PIPE");
     set_step_prefetch(pf ? std::atoi(pf) : 0);
-    set_step_pipe(pp ? std::atoi(pp) : 0);
+    set_step_pipe(pp ? std::atoi(pp) : 2);
     const int occ_step = step_max_ctas_per_sm(p.layer_mask);
     const uint32_t n_tiles = (uint32_t)((n_env + TILE - 1) / TILE);
     c->step_grid = (int)std::min<long long>((long long)n_tiles, (long long)c->sm_count * occ_step);

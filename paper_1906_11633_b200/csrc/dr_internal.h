@@ -172,10 +172,10 @@ int reset_max_ctas_per_sm();
 constexpr int RESET_THREADS = 256;
 constexpr int STEP_THREADS = TILE;
 #ifndef DR_STEP_MIN_CTAS
-#define DR_STEP_MIN_CTAS 3
+#define DR_STEP_MIN_CTAS 4
 #endif
-// __launch_bounds__ occupancy target: 3 CTAs/SM (<= 168 regs) measured fastest for v3 on B200
-// (3.22e9 vs 3.05e9 env-steps/s at 4 CTAs/SM; profiles/round1_notes.md)
+// __launch_bounds__ occupancy target: 4 CTAs/SM (<= 128 regs) measured fastest with the
+// warp-cooperative ring (4.10e9 vs 4.04e9 env-steps/s at 3 CTAs/SM; profiles/round1_notes.md)
 constexpr int STEP_MIN_CTAS = DR_STEP_MIN_CTAS;
 #ifndef DR_SFU_NORMALS
 #define DR_SFU_NORMALS 1

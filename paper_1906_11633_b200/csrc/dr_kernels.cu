@@ -109,14 +109,17 @@ static int g_prefetch = 0;
 
 void set_step_prefetch(int mode) { g_prefetch = (mode < 0 || mode > 2) ? 0 : mode; }
 
-// Ring pipeline of the step kernel (DR_PIPE at dr_init): 0 = per-thread cp.async ring
-// (step_kernel, default), 1 = CTA-wide TMA bulk-copy ring (step_kernel_tma).  Measured on B200 at
-// 1M envs (profiles/round1_notes.md): 3.65e9 vs 3.36e9 env-steps/s -- the CTA-wide ring couples
-// the four warps of a CTA (slot refill waits for the slowest warp, barrier stall 0.65/issue),
-// which costs more than the LDGSTS issue slots it saves.
-static int g_pipe = 0;
+// Ring pipeline of the step kernel (DR_PIPE at dr_init): 2 = warp-cooperative 16-byte cp.async.cg
+// ring (step_kernel_warp, default), 0 = per-thread 4-byte cp.async ring (step_kernel), 1 = CTA-wide
+// TMA bulk-copy ring (step_kernel_tma).  Measured on B200, 1M envs, full pipeline
+// (profiles/round1_notes.md), env-steps/s at 3 / 4 CTAs per SM:
+//   pipe 2: 4.04e9 / 4.10e9   pipe 0: 3.65e9 / 3.47e9   pipe 1: - / 3.27e9
+// Pipe 2 issues 4x fewer LDGSTS and bypasses L1 (the 4-byte .ca copies of pipe 0 allocate L1 lines,
+// which thrash once 4 CTAs leave ~24 KB of L1); pipe 1 couples the CTA's warps (a slot is refilled
+// only after the slowest warp releases it).
+static int g_pipe = 2;
 
-void set_step_pipe(int mode) { g_pipe = (mode < 0 || mode > 2) ? 0 : mode; }
+void set_step_pipe(int mode) { g_pipe = (mode < 0 || mode > 2) ? 2 : mode; }
 
 static StepFn step_fn_warp(uint32_t m) {
     if (m == MASK_FULL) return step_kernel_warp<MASK_FULL>;
