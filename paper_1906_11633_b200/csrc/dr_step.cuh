@@ -949,27 +949,21 @@ __global__ void __launch_bounds__(STEP_THREADS, STEP_MIN_CTAS)
     acc_zero(acc);
     uint32_t my_envs = 0;
 
-    // Every warp owns the 32-env quarter [wcol, wcol + 32) of each of the CTA's tiles: its input
-    // rows, output rows, ring columns and state are disjoint from the other warps', so the warps
-    // advance through the tiles independently (no CTA barrier until the stats reduction).
     for (uint32_t tile = blockIdx.x; tile < n_tiles; tile += gridDim.x) {
         const uint32_t e0 = tile * TILE;
         const uint32_t cnt = min((uint32_t)TILE, n_env - e0);
-        const int nw = max(0, min(32, (int)cnt - wcol));   // valid envs of this warp
-        const uint32_t ew = e0 + wcol;                      // this warp's first env
-        float* wa = s_act + wcol * N_ACT;
-        float* wo = s_obs + wcol * OBS_IN;
-        __syncwarp();   // previous quarter's rows fully stored by all lanes
-        if (nw == 32) {
-            const float* a = actions + (size_t)ew * N_ACT;
-            const float* o = raw_obs + (size_t)ew * OBS_IN;
+        const bool full = cnt == (uint32_t)TILE;
+        __syncthreads();   // previous tile's smem fully stored
+        if (full) {
+            const float* a = actions + (size_t)e0 * N_ACT;
+            const float* o = raw_obs + (size_t)e0 * OBS_IN;
 #pragma unroll
-            for (int i = lane; i < 32 * N_ACT / 4; i += 32) cp_async16(wa + 4 * i, a + 4 * i);
+            for (int i = tid; i < TILE * N_ACT / 4; i += STEP_THREADS) cp_async16(s_act + 4 * i, a + 4 * i);
 #pragma unroll
-            for (int i = lane; i < 32 * OBS_IN / 4; i += 32) cp_async16(wo + 4 * i, o + 4 * i);
+            for (int i = tid; i < TILE * OBS_IN / 4; i += STEP_THREADS) cp_async16(s_obs + 4 * i, o + 4 * i);
         } else {
-            for (int i = lane; i < nw * N_ACT; i += 32) cp_async4(wa + i, actions + (size_t)ew * N_ACT + i);
-            for (int i = lane; i < nw * OBS_IN; i += 32) cp_async4(wo + i, raw_obs + (size_t)ew * OBS_IN + i);
+            for (uint32_t i = tid; i < cnt * N_ACT; i += STEP_THREADS) cp_async4(s_act + i, actions + (size_t)e0 * N_ACT + i);
+            for (uint32_t i = tid; i < cnt * OBS_IN; i += STEP_THREADS) cp_async4(s_obs + i, raw_obs + (size_t)e0 * OBS_IN + i);
         }
         cp_commit();
         PipeWarp<L> pipe{s_ring, s_ring + RING_W * TILE, p.rec + rec_index(e0) + wcol, p.st + st_index(e0) + wcol, tid,
@@ -979,46 +973,13 @@ __global__ void __launch_bounds__(STEP_THREADS, STEP_MIN_CTAS)
         pipe.issue_act(pipe.slot1, 0);     // A0 -> slot1
         cp_commit();
         cp_wait<1>();      // staging + S0
-        __syncwarp();      // the warp's staging copies and S0 columns
-        const bool mine = lane < nw;
+        __syncthreads();   // everyone's staging copies (and each warp's S0)
+        const bool mine = (uint32_t)tid < cnt;
         env_step<L>(p, e0 + tid, mine, t, tid, s_act, s_obs, s_dt, pipe, acc);
         my_envs += mine ? 1u : 0u;
         cp_wait<0>();
-        __syncwarp();
-        // store this warp's output rows (contiguous global ranges)
-        if (nw == 32) {
-            float4* a4 = reinterpret_cast<float4*>(out_actions + (size_t)ew * N_ACT);
-            const float4* s4 = reinterpret_cast<const float4*>(wa);
-#pragma unroll
-            for (int i = lane; i < 32 * N_ACT / 4; i += 32) __stcs(a4 + i, s4[i]);
-            float4* d4 = reinterpret_cast<float4*>(out_dt + (size_t)ew * N_SUB);
-            const float4* sd4 = reinterpret_cast<const float4*>(s_dt + wcol * N_SUB);
-#pragma unroll
-            for (int i = lane; i < 32 * N_SUB / 4; i += 32) __stcs(d4 + i, sd4[i]);
-            float2* oo = reinterpret_cast<float2*>(out_obs + (size_t)ew * OBS_OUT);
-#pragma unroll
-            for (int i = lane; i < 32 * 11; i += 32) {
-                const int r = i / 11, k = i - r * 11;
-                __stcs(oo + i, reinterpret_cast<const float2*>(wo + r * OBS_IN)[k]);
-            }
-            float* of = out_force + (size_t)ew * 3;
-#pragma unroll
-            for (int i = lane; i < 32 * 3; i += 32) {
-                const int r = i / 3, k = i - r * 3;
-                __stcs(of + i, wo[r * OBS_IN + 22 + k]);
-            }
-        } else if (nw > 0) {
-            for (int i = lane; i < nw * N_ACT; i += 32) out_actions[(size_t)ew * N_ACT + i] = wa[i];
-            for (int i = lane; i < nw * N_SUB; i += 32) out_dt[(size_t)ew * N_SUB + i] = s_dt[wcol * N_SUB + i];
-            for (int i = lane; i < nw * OBS_OUT; i += 32) {
-                const int r = i / OBS_OUT, k = i - r * OBS_OUT;
-                out_obs[(size_t)ew * OBS_OUT + i] = wo[r * OBS_IN + k];
-            }
-            for (int i = lane; i < nw * 3; i += 32) {
-                const int r = i / 3, k = i - r * 3;
-                out_force[(size_t)ew * 3 + i] = wo[r * OBS_IN + 22 + k];
-            }
-        }
+        __syncthreads();
+        store_tile(e0, cnt, tid, s_act, s_obs, s_dt, out_actions, out_obs, out_dt, out_force);
     }
     reduce_stats<L>(p, acc, my_envs, t, reinterpret_cast<double*>(s_obs), &s_last);
 }
