@@ -2,9 +2,11 @@
 """bench.py -- randomized env-steps/s of the fused DR step on B200 (BASELINE.json metric).
 
 Default workload (N=1): BASELINE config 4's single-GPU reference -- 1,048,576 envs, full
-pipeline (all 9 layers), Shadow-hand shapes; under torchrun the 1M envs are sharded over the N
-ranks (env_offset = rank * 1M/N, same seed) with the per-step NCCL all-reduce of the 32 x fp64
-stats vector on a comm stream -- the path's one collective.
+pipeline (all 9 layers), Shadow-hand shapes.  Under torchrun the envs are sharded by global id
+(env_offset = rank * n_local, same seed): by default every rank owns 1M envs ("weak", per-GPU
+work fixed); --scaling strong splits the 1M envs of config 4 over the N ranks.  The per-step
+NCCL all-reduce of the 32 x fp64 stats vector runs on a comm stream -- the path's one
+collective (DESIGN.md "Multi-GPU").
 
   python bench.py [--gpus N] [--steps K] [--warmup W] [--config full1m|cfg2|cfg3|reset]
   python bench.py --impl reference ...   # the fp64 CPU oracle on the box's host cores
@@ -42,7 +44,10 @@ def parse():
     ap.add_argument("--warmup", type=int, default=20)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--config", default="full1m", choices=["full1m", "cfg2", "cfg3", "reset"])
-    ap.add_argument("--n-env", type=int, default=0, help="override the global env count")
+    ap.add_argument("--n-env", type=int, default=0, help="override the env count (per GPU if weak, global if strong)")
+    ap.add_argument("--scaling", default="weak", choices=["weak", "strong"],
+                    help="weak: every rank owns the config's env count (global = N x that); "
+                         "strong: the config's env count is split over the ranks")
     ap.add_argument("--e2e-steps", type=int, default=10)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-sample-envs", type=int, default=65536)
@@ -146,6 +151,7 @@ def run_reference(args):
     from oracle.oracle import Oracle
     from workload import gen, presets
     cfg = config_of(args.config, args.n_env)
+    cfg["scaling"] = args.scaling
     n = min(cfg["n"], args.cpu_sample_envs)
     P = presets.preset(cfg["mask"])
     acts, obs = gen.frames(n, 4)
@@ -207,13 +213,13 @@ def main():
     if world > 1:
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     cfg = config_of(args.config, args.n_env)
-    n_glob = cfg["n"]
-    from paper_1906_11633_b200.parallel import shard, stats_all_reduce
+    cfg["scaling"] = args.scaling
+    n_glob = cfg["n"] * world if args.scaling == "weak" else cfg["n"]
+    from paper_1906_11633_b200.parallel import StatsReducer, shard
     off, n = shard(n_glob, world, rank)
     P = presets.preset(cfg["mask"])
 
     lib_stream = torch.cuda.Stream()
-    comm_stream = torch.cuda.Stream() if world > 1 else None
     with torch.cuda.stream(lib_stream):
         ctx = DRContext(P, n, presets.SEED_DR, env_offset=off, n_env_global=n_glob, stream=lib_stream)
         # synthetic device-resident frame ring (4 frames), Shadow-hand shapes (workload.gen recipe)
@@ -232,6 +238,7 @@ def main():
         O[:, :, 18:22] = q[..., 0:4] / q[..., 0:4].norm(dim=-1, keepdim=True)
         O[:, :, 22:26] = q[..., 4:8] / q[..., 4:8].norm(dim=-1, keepdim=True)
         del q
+        reducer = StatsReducer(ctx.stats, lib_stream) if world > 1 else None
         masks = None
         if cfg["resets"]:
             e = torch.arange(off, off + n, device="cuda")
@@ -239,17 +246,15 @@ def main():
         torch.cuda.synchronize()
 
     def one_step(t):
+        if reducer is not None:
+            reducer.before_step(t)   # slot t % 2's previous all-reduce is done before it is rewritten
         if masks is not None:
             ctx.reset(masks[t % 10])
         ctx.step(A[t % F], O[t % F])
-        if comm_stream is not None:
+        if reducer is not None:
             # the path's one collective: sum of the 32 x fp64 stats of step t over ranks,
             # on its own stream so it overlaps step t+1 (slot t % 2 is double-buffered)
-            ev = torch.cuda.Event()
-            ev.record(lib_stream)
-            comm_stream.wait_event(ev)
-            with torch.cuda.stream(comm_stream):
-                stats_all_reduce(ctx.stats[t % 2])
+            reducer.after_step(t)
 
     with torch.cuda.stream(lib_stream):
         for t in range(args.warmup):
@@ -270,8 +275,8 @@ def main():
         for i in range(args.steps):
             one_step(t_base + i)
             evs[i + 1].record(lib_stream)
-        if comm_stream is not None:
-            lib_stream.wait_stream(comm_stream)
+        if reducer is not None:
+            reducer.sync()
         end = torch.cuda.Event(enable_timing=True)
         end.record(lib_stream)
         torch.cuda.synchronize()

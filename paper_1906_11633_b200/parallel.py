@@ -27,6 +27,42 @@ def stats_all_reduce(stats_slot, group=None, async_op: bool = False):
     return dist.all_reduce(stats_slot, op=dist.ReduceOp.SUM, group=group, async_op=async_op)
 
 
+class StatsReducer:
+    """The overlapped per-step stats all-reduce on a dedicated comm stream.
+
+    Step t's kernel writes slot t % 2; the all-reduce of slot t % 2 runs on the comm stream after
+    an event recorded behind step t, so it overlaps step t+1.  Before step t+2 overwrites that
+    slot, the library stream waits for the all-reduce's completion event (``before_step``), so
+    the double buffer is never raced."""
+
+    def __init__(self, stats, lib_stream, group=None):
+        import torch
+        self.stats = stats
+        self.lib_stream = lib_stream
+        self.comm_stream = torch.cuda.Stream()
+        self.group = group
+        self.done = [None, None]
+
+    def before_step(self, t: int):
+        ev = self.done[t % 2]
+        if ev is not None:
+            self.lib_stream.wait_event(ev)
+
+    def after_step(self, t: int):
+        import torch
+        ev = torch.cuda.Event()
+        ev.record(self.lib_stream)
+        self.comm_stream.wait_event(ev)
+        with torch.cuda.stream(self.comm_stream):
+            stats_all_reduce(self.stats[t % 2], group=self.group)
+        done = torch.cuda.Event()
+        done.record(self.comm_stream)
+        self.done[t % 2] = done
+
+    def sync(self):
+        self.lib_stream.wait_stream(self.comm_stream)
+
+
 class ShardedDR:
     """One rank's context plus the overlapped stats all-reduce (needs CUDA + an initialised
     process group)."""
@@ -39,26 +75,23 @@ class ShardedDR:
         self.rank = dist.get_rank() if dist.is_initialized() else 0
         self.offset, self.n = shard(n_global, self.world, self.rank)
         self.lib_stream = lib_stream or torch.cuda.current_stream()
-        self.comm_stream = torch.cuda.Stream() if self.world > 1 else None
         self.ctx = DRContext(preset, self.n, seed, env_offset=self.offset, n_env_global=n_global,
                              stream=self.lib_stream)
+        self.reducer = StatsReducer(self.ctx.stats, self.lib_stream) if self.world > 1 else None
         self.t = 0
 
     def step(self, actions, raw_obs):
-        import torch
+        if self.reducer is not None:
+            self.reducer.before_step(self.t)
         out = self.ctx.step(actions, raw_obs)
-        if self.comm_stream is not None:
-            ev = torch.cuda.Event()
-            ev.record(self.lib_stream)
-            self.comm_stream.wait_event(ev)
-            with torch.cuda.stream(self.comm_stream):
-                stats_all_reduce(self.ctx.stats[self.t % 2])
+        if self.reducer is not None:
+            self.reducer.after_step(self.t)
         self.t += 1
         return out
 
     def sync_comm(self):
-        if self.comm_stream is not None:
-            self.lib_stream.wait_stream(self.comm_stream)
+        if self.reducer is not None:
+            self.reducer.sync()
 
     def close(self):
         self.ctx.close()
