@@ -53,6 +53,9 @@ def parse():
     ap.add_argument("--cpu-sample-envs", type=int, default=65536)
     ap.add_argument("--cpu-sample-steps", type=int, default=24)
     ap.add_argument("--profile", action="store_true", help="short run for ncu (no e2e/cpu legs)")
+    ap.add_argument("--graph", type=int, default=-1,
+                    help="steps per CUDA graph in the timed region (0 = eager launches; default: 100 for the "
+                         "launch-bound small configs at N=1, else 0)")
     return ap.parse_args()
 
 
@@ -270,11 +273,31 @@ def main():
             dist.barrier()
         torch.cuda.synchronize()
         launches0 = dr.dr_kernel_launches()
-        evs = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps + 1)]
-        evs[0].record(lib_stream)
-        for i in range(args.steps):
-            one_step(t_base + i)
-            evs[i + 1].record(lib_stream)
+        G = args.graph if args.graph >= 0 else (100 if (world == 1 and n * cfg["bytes"] < 2e8) else 0)
+        if G > 0 and (world > 1 or args.steps % G or (cfg["resets"] and G % 10)):
+            G = 0   # graphs need K % G == 0 (and whole 10-step reset-mask cycles); multi-rank runs eager
+        if G > 0:
+            # launch-bound configs: one CUDA graph of G steps (the step index is device-resident, so
+            # every replay advances it); events around each replay, per-step time = replay / G
+            graph = torch.cuda.CUDAGraph()
+            with torch.cuda.graph(graph, stream=lib_stream):
+                for i in range(G):
+                    one_step(t_base + i)
+            per_graph_launches = dr.dr_kernel_launches() - launches0
+            graph.replay()   # warm replay
+            torch.cuda.synchronize()
+            reps = args.steps // G
+            evs = [torch.cuda.Event(enable_timing=True) for _ in range(reps + 1)]
+            evs[0].record(lib_stream)
+            for i in range(reps):
+                graph.replay()
+                evs[i + 1].record(lib_stream)
+        else:
+            evs = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps + 1)]
+            evs[0].record(lib_stream)
+            for i in range(args.steps):
+                one_step(t_base + i)
+                evs[i + 1].record(lib_stream)
         if reducer is not None:
             reducer.sync()
         end = torch.cuda.Event(enable_timing=True)
@@ -282,10 +305,10 @@ def main():
         torch.cuda.synchronize()
         if world > 1:
             dist.barrier()
-        launches = dr.dr_kernel_launches() - launches0
+        launches = per_graph_launches * reps if G > 0 else dr.dr_kernel_launches() - launches0
         clocks = sampler.stop()
         elapsed_ms = evs[0].elapsed_time(end)
-        per = [evs[i].elapsed_time(evs[i + 1]) for i in range(args.steps)]
+        per = [evs[i].elapsed_time(evs[i + 1]) / max(G, 1) for i in range(len(evs) - 1)]
         t_ms = torch.tensor([elapsed_ms], dtype=torch.float64, device="cuda")
         if world > 1:
             dist.all_reduce(t_ms, op=dist.ReduceOp.MAX)
@@ -299,7 +322,7 @@ def main():
     achieved = cfg["bytes"] * n / (kern_ms / 1e3) / 1e9
     roofline = {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
                 "traffic": ncu_traffic(cfg["workload"]), "peak_kind": peak_kind,
-                "bytes_per_env_step": cfg["bytes"], "kernel": "dr::step_kernel",
+                "bytes_per_env_step": cfg["bytes"], "kernel": "dr::step_kernel_warp" + (" (+ dr::reset_kernel)" if cfg["resets"] else ""),
                 "kernel_ms_avg": kern_ms, "kernel_ms_median": per[len(per) // 2]}
 
     # ---- e2e: through dr_step_host with pinned host buffers (copies inside the timed region) ----
@@ -339,6 +362,7 @@ def main():
             "config": {"workload": cfg["workload"], "n_env_global": n_glob, "n_env_per_gpu": n,
                        "layers": hex(cfg["mask"]), "parallelism": f"env-shard x{world}",
                        "l2": "inputs larger than L2" if cfg["bytes"] * n > 126e6 else "L2-resident (warm)",
+                       "cuda_graph_steps": G,
                        "bytes_per_step_per_gpu": cfg["bytes"] * n},
             "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": int(launches),
             "clocks": clocks,

@@ -153,6 +153,20 @@ int dr_params_default(dr_params* p);
  * workspace, upload constants, then enqueue episode 0 sampling for every env. */
 int dr_init(const dr_params* params, int64_t n_env, uint64_t seed);
 
+/* On-the-fly parameter update ("change randomization parameters during training", ORRB's
+ * adaptive randomization).  Validates *params like dr_init (same DR_EINVAL
+ * messages); layer_mask, n_phys, env_offset and n_env_global must equal the context's
+ * (DR_EINVAL otherwise); workspace and stream fields are ignored.  The new constants and
+ * tables are uploaded in stream order on the library stream, so every dr_step / dr_reset
+ * enqueued after this call sees them and every one enqueued before does not:
+ *   - per-step draws (action-noise stds, substep base dt, dropout rate and hold, occlusion
+ *     radius, uncorrelated obs noise, force accel std and decay) change from the next dr_step;
+ *   - per-episode draws (calibrated backlash widths and jitter, lambda range, force p range,
+ *     correlated noise, delay probability, physics descriptors) change at each env's next
+ *     reset: the current episode records are not resampled.
+ * Not graph-capturable (host tables are staged synchronously).  Asynchronous otherwise. */
+int dr_update_params(const dr_params* params);
+
 /* Episode reset: for every env with
  * env_mask[e] != 0 (device u8 [n_env]; NULL = all), k_e += 1, then resample its episode record
  * and physical parameters and zero its state.  Asynchronous. */

@@ -222,11 +222,29 @@ static double draw_normal(const orc_ctx* c, int64_t gid, uint32_t dom, uint32_t 
     return (n % 2 == 0) ? z0 : z1;
 }
 
+/* Parameters and their host constants: delay Bernoulli(p), dropout per-step
+ * probability 1 - exp(-rate * 80 ms) at the nominal step [Q11], and the
+ * loguniform force probability as a 65,536-level midpoint table [Q19]. */
+static void set_params(orc_ctx* c, const orc_params* p)
+{
+    uint32_t j;
+    double llo, lhi;
+    c->p = *p;
+    c->t_delay = orc_bernoulli_threshold(p->delay_prob);
+    c->t_drop = orc_bernoulli_threshold(1.0 - exp(-p->dropout_rate_hz * p->step_nominal));
+    llo = log(p->force_p_lo);
+    lhi = log(p->force_p_hi);
+    for (j = 0; j < P_TABLE_N; ++j) {
+        double pj = exp(llo + (((double)j + 0.5) / 65536.0) * (lhi - llo));
+        c->p_tab[j] = pj;
+        c->t_tab[j] = orc_bernoulli_threshold(pj);
+    }
+}
+
 int orc_init(const orc_params* p, int64_t n_env, const int64_t* gids, uint64_t seed, orc_ctx** out)
 {
     orc_ctx* c;
     int64_t i;
-    uint32_t j;
     if (!p || !out || n_env < 1) return -1;
     if (p->n_phys < 1 || p->n_phys > ORC_MAX_PHYS) return -1;
     if (p->mass_index < 0 || p->mass_index >= p->n_phys) return -1;
@@ -234,25 +252,12 @@ int orc_init(const orc_params* p, int64_t n_env, const int64_t* gids, uint64_t s
     if (!c) return -4;
     c->env = (orc_env*)calloc((size_t)n_env, sizeof(orc_env));
     if (!c->env) { free(c); return -4; }
-    c->p = *p;
     c->n = n_env;
     c->key[0] = (uint32_t)(seed & 0xFFFFFFFFu);
     c->key[1] = (uint32_t)(seed >> 32);
     c->t = 0;
     c->resets_pending = 0;
-    /* host constants: delay Bernoulli(p), dropout per-step probability
-     * 1 - exp(-rate * 80 ms) at the nominal step [Q11]. */
-    c->t_delay = orc_bernoulli_threshold(p->delay_prob);
-    c->t_drop = orc_bernoulli_threshold(1.0 - exp(-p->dropout_rate_hz * p->step_nominal));
-    /* loguniform force probability, 65,536-level midpoint table [Q19]. */
-    {
-        double llo = log(p->force_p_lo), lhi = log(p->force_p_hi);
-        for (j = 0; j < P_TABLE_N; ++j) {
-            double pj = exp(llo + (((double)j + 0.5) / 65536.0) * (lhi - llo));
-            c->p_tab[j] = pj;
-            c->t_tab[j] = orc_bernoulli_threshold(pj);
-        }
-    }
+    set_params(c, p);
     for (i = 0; i < n_env; ++i) {
         c->env[i].gid = gids ? gids[i] : i;
         c->env[i].episode = 0;
@@ -271,6 +276,18 @@ int orc_init(const orc_params* p, int64_t n_env, const int64_t* gids, uint64_t s
         c->resets_pending = 0;
         return rc;
     }
+}
+
+/* Parameter update mid-run ("change randomization parameters during training"):
+ * the new set replaces the old one for every draw made afterwards.  Step draws read c->p at
+ * each step; episode records keep the values drawn at their reset until the next reset. */
+int orc_update_params(orc_ctx* c, const orc_params* p)
+{
+    if (!c || !p) return -1;
+    if (p->n_phys < 1 || p->n_phys > ORC_MAX_PHYS) return -1;
+    if (p->mass_index < 0 || p->mass_index >= p->n_phys) return -1;
+    set_params(c, p);
+    return 0;
 }
 
 void orc_free(orc_ctx* c)

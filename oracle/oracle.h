@@ -116,6 +116,7 @@ typedef struct orc_ctx orc_ctx;
 /* ---- context API (mirrors the shape of the product ABI; host memory only) ---- */
 int  orc_init(const orc_params* p, int64_t n_env, const int64_t* gids, uint64_t seed, orc_ctx** out);
 void orc_free(orc_ctx* c);
+int  orc_update_params(orc_ctx* c, const orc_params* p); /* mid-run parameter swap */
 int  orc_reset(orc_ctx* c, const uint8_t* mask);          /* NULL = all envs */
 /* One env step for all envs of the context.  Outputs may be NULL.
  * bl_margin [n][20]: fp64 |(s + a_n*d*dt_env) - sgn(a_n)| (the backlash rail margin), +inf when

@@ -82,6 +82,8 @@ def lib():
                                C.POINTER(C.c_void_p)]
         L.orc_init.restype = C.c_int
         L.orc_free.argtypes = [C.c_void_p]
+        L.orc_update_params.argtypes = [C.c_void_p, C.POINTER(OrcParams)]
+        L.orc_update_params.restype = C.c_int
         L.orc_reset.argtypes = [C.c_void_p, u8p]
         L.orc_reset.restype = C.c_int
         L.orc_step.argtypes = [C.c_void_p, fp, fp, dp, dp, dp, dp, dp, dp]
@@ -210,6 +212,13 @@ class Oracle:
             self.close()
         except Exception:
             pass
+
+    def update_params(self, preset: dict):
+        """Swap the parameter set mid-run: later draws use it."""
+        self._params = make_params(preset)
+        rc = lib().orc_update_params(self._h, C.byref(self._params))
+        if rc != 0:
+            raise ValueError(f"orc_update_params failed: {rc}")
 
     def reset(self, mask=None):
         m = None if mask is None else np.ascontiguousarray(mask, dtype=np.uint8)

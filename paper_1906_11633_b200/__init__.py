@@ -28,6 +28,7 @@ class DRContext:
             params = dr.params_from_preset(preset, env_offset=env_offset, n_env_global=n_env_global,
                                            stream=self.stream.cuda_stream, workspace=ws)
         self._ws = ws
+        self._env_offset, self._n_env_global = env_offset, n_env_global
         self.preset = preset
         dr.dr_init(params, self.n, seed)
         self._open = True
@@ -43,6 +44,14 @@ class DRContext:
         o = outs or (self.out_actions, self.out_obs, self.out_dt, self.out_force)
         dr.dr_step(actions, raw_obs, *o)
         return o
+
+    def update_params(self, preset: dict, env_offset: int = None, n_env_global: int = None):
+        """dr_update_params with a preset dict (same shape/layers/shard as at init)."""
+        params = dr.params_from_preset(preset, env_offset=self._env_offset if env_offset is None else env_offset,
+                                       n_env_global=self._n_env_global if n_env_global is None else n_env_global,
+                                       stream=self.stream.cuda_stream)
+        dr.dr_update_params(params)
+        self.preset = preset
 
     def reset(self, mask=None):
         dr.dr_reset(mask, self.n if mask is not None else None)

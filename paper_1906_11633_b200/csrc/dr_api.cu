@@ -161,136 +161,19 @@ unsigned long long bernoulli_threshold(double p) {
     return (unsigned long long)std::floor(p * 4294967296.0);
 }
 
-bool aligned16(const void* q) { return ((uintptr_t)q & 15u) == 0; }
-
-}  // namespace
-
-extern "C" {
-
-uint32_t dr_abi_version(void) { return DR_ABI_VERSION; }
-
-const char* dr_last_error(void) { return g_err; }
-
-int dr_params_default(dr_params* p) {
-    if (!p) return fail(DR_EINVAL, "params: NULL");
-    std::memset(p, 0, sizeof(*p));
-    p->abi_version = DR_ABI_VERSION;
-    p->struct_size = sizeof(dr_params);
-    p->layer_mask = DR_ALL;
-    p->n_act = DR_N_ACT;
-    p->n_tips = DR_N_TIPS;
-    p->n_substeps = DR_N_SUBSTEPS;
-    // Table action-noise (PAPER.md:47-61): % of the action range 2 (DESIGN.md Q8)
-    p->act_sigma_uadd = 0.10;
-    p->act_sigma_cadd = 0.03;
-    p->act_sigma_mult = 0.015;
-    p->delay_prob = 0.5;                   // PAPER.md:77-78
-    p->dt_base = 0.008;                    // PAPER.md:85
-    p->lambda_lo = 1250.0;                 // PAPER.md:88
-    p->lambda_hi = 10000.0;
-    p->step_nominal = 0.08;                // PAPER.md:79, 747
-    for (int j = 0; j < DR_N_ACT; ++j) {   // calibrated widths: not given (PAPER.md:98-99), Q21
-        p->delta_cal_neg[j] = 3.5 + 0.1 * j;
-        p->delta_cal_pos[j] = 4.0 + 0.1 * j;
-    }
-    p->delta_jitter_std = 0.1;             // PAPER.md:101
-    p->backlash_eps = 1e-12;               // PAPER.md:107
-    // Table obs-noise (PAPER.md:36-41)
-    p->tip_corr = 1e-3;
-    p->tip_uncorr = 2e-3;
-    p->obj_corr = 5e-3;
-    p->obj_uncorr = 1e-3;
-    p->rot_corr = 0.1;
-    p->rot_uncorr = 0.1;
-    p->tip_marker = 3e-3;
-    p->base_marker = 1e-3;
-    p->base_marker_to_tips = 1;            // Q14
-    p->dropout_hold_steps = 13;            // ceil(1 s / 80 ms), PAPER.md:64, Q11
-    p->dropout_rate_hz = 0.2;              // PAPER.md:64
-    p->occl_dist = 0.015;                  // Q13 (SPEC.md:227)
-    p->force_p_lo = 0.001;                 // PAPER.md:113
-    p->force_p_hi = 0.1;
-    p->force_accel_std = 1.0;              // PAPER.md:115
-    p->force_decay_per_step = 0.99;
-    // physical parameters: the paper's table is missing (PAPER.md:8); synthetic 256 slots, Q20
-    p->n_phys = DR_MAX_PHYS;
-    p->mass_index = 0;
-    for (int i = 0; i < DR_MAX_PHYS; ++i) {
-        dr_phys_desc& d = p->phys[i];
-        d.base = 0.5 + 0.01 * i;
-        switch (i % 4) {
-        case 0: d.kind = DR_PHYS_UNIFORM_SCALE; d.a = 0.5; d.b = 1.5; break;
-        case 1: d.kind = DR_PHYS_LOGUNIFORM_SCALE; d.a = 0.3; d.b = 3.0; break;
-        case 2: d.kind = DR_PHYS_ADD_GAUSS; d.a = 0.15; d.b = 0.0; break;
-        default: d.kind = DR_PHYS_MUL_LOGNORMAL; d.a = 0.2; d.b = 0.0; break;
-        }
-    }
-    return DR_OK;
-}
-
-size_t dr_workspace_bytes(const dr_params* params, int64_t n_env) {
-    if (!params || n_env < 1 || params->n_phys < 1 || params->n_phys > DR_MAX_PHYS) return 0;
-    return make_layout(n_env, params->n_phys, device_sm_count() * 32).total;
-}
-
-int dr_init(const dr_params* params, int64_t n_env, uint64_t seed) {
-    if (g_ctx) return fail(DR_EALREADY, "dr_init: context already initialised (call dr_finalize)");
-    int rc = validate(params, n_env);
-    if (rc != DR_OK) return rc;
-    g_sticky = false;
-    Ctx* c = new Ctx();
-    c->prm = *params;
-    if (c->prm.n_env_global == 0) c->prm.n_env_global = n_env;
-    c->n_env = n_env;
-    c->seed = seed;
-    c->stream = static_cast<cudaStream_t>(params->stream);
-    cudaError_t e = cudaGetDevice(&c->device);
-    if (e != cudaSuccess) { delete c; return cuda_fail(e, "cudaGetDevice"); }
-    c->sm_count = device_sm_count();
-    c->max_ctas = c->sm_count * 32;
-    c->lay = make_layout(n_env, params->n_phys, c->max_ctas);
-    if (params->workspace) {
-        if (params->workspace_bytes < c->lay.total) {
-            size_t need = c->lay.total;
-            delete c;
-            return fail(DR_ENOMEM, "workspace_bytes: %zu < required %zu", params->workspace_bytes, need);
-        }
-        c->ws = static_cast<char*>(params->workspace);
-        c->owns_ws = false;
-    } else {
-        e = cudaMalloc(&c->ws, c->lay.total);
-        if (e != cudaSuccess) { delete c; return fail(DR_ENOMEM, "cudaMalloc(%zu): %s", c->lay.total, cudaGetErrorString(e)); }
-        c->owns_ws = true;
-    }
-    const Layout& L = c->lay;
-    DevPtrs& P = c->p;
-    P.rec = reinterpret_cast<uint32_t*>(c->ws + L.rec);
-    P.st = reinterpret_cast<uint32_t*>(c->ws + L.st);
-    P.phys = reinterpret_cast<float*>(c->ws + L.phys);
-    P.pd_kind_rank = reinterpret_cast<uint32_t*>(c->ws + L.pd_kr);
-    P.pd_a = reinterpret_cast<float*>(c->ws + L.pd_a);
-    P.pd_b = reinterpret_cast<float*>(c->ws + L.pd_b);
-    P.pd_base = reinterpret_cast<float*>(c->ws + L.pd_base);
-    P.t_tab = reinterpret_cast<uint32_t*>(c->ws + L.t_tab);
-    P.rs_philox = reinterpret_cast<uint32_t*>(c->ws + L.rs_philox);
-    P.rs_pairs = reinterpret_cast<uint32_t*>(c->ws + L.rs_pairs);
-    P.rs_phys = reinterpret_cast<float4*>(c->ws + L.rs_phys);
-    P.rs_src = reinterpret_cast<uint32_t*>(c->ws + L.rs_src);
-    P.dec_tab = reinterpret_cast<double*>(c->ws + L.dec);
-    P.partials = reinterpret_cast<double*>(c->ws + L.partials);
-    P.stats = reinterpret_cast<double*>(c->ws + L.stats);
-    P.ctl = reinterpret_cast<unsigned long long*>(c->ws + L.ctl);
-    c->internal_stats = P.stats;
-
+// Host-side constants and tables of parameter set p (Philox round keys, Bernoulli thresholds,
+// the loguniform force table, the decay table, the reset task tables and physics coefficients),
+// uploaded in stream order on the library stream: kernels enqueued before see the previous set,
+// kernels enqueued after see p.  Used by dr_init and dr_update_params.
+cudaError_t upload_params(Ctx* c, const dr_params& p, const char** what) {
     // ---- host-side constants ----
-    const dr_params& p = c->prm;
     DevConst dc{};
     dc.layer_mask = p.layer_mask;
-    dc.n_env = (uint32_t)n_env;
-    dc.pitch = L.pitch;
+    dc.n_env = (uint32_t)c->n_env;
+    dc.pitch = c->lay.pitch;
     dc.env_offset = (uint32_t)p.env_offset;
     dc.hold_steps = (uint32_t)p.dropout_hold_steps;
-    const uint32_t k0 = (uint32_t)(seed & 0xFFFFFFFFull), k1 = (uint32_t)(seed >> 32);
+    const uint32_t k0 = (uint32_t)(c->seed & 0xFFFFFFFFull), k1 = (uint32_t)(c->seed >> 32);
     for (int r = 0; r < 10; ++r) {   // Philox key schedule: key + r * (W0, W1)
         dc.rk0[r] = k0 + (uint32_t)r * 0x9E3779B9u;
         dc.rk1[r] = k1 + (uint32_t)r * 0xBB67AE85u;
@@ -436,24 +319,153 @@ int dr_init(const dr_params* params, int64_t n_env, uint64_t seed) {
         dec[256 + j] = std::pow(p.force_decay_per_step, 256.0 * j);
     }
     cudaStream_t s = c->stream;
+    cudaError_t e;
+    const DevPtrs& P = c->p;
+    if ((e = upload_const(dc, s)) != cudaSuccess) { *what = "upload_const"; return e; };
+    if ((e = cudaMemcpyAsync(P.pd_kind_rank, kr.data(), MAX_PHYS * 4, cudaMemcpyHostToDevice, s)) != cudaSuccess) { *what = "memcpy pd"; return e; };
+    if ((e = cudaMemcpyAsync(P.pd_a, pa.data(), MAX_PHYS * 4, cudaMemcpyHostToDevice, s)) != cudaSuccess) { *what = "memcpy pd"; return e; };
+    if ((e = cudaMemcpyAsync(P.pd_b, pb.data(), MAX_PHYS * 4, cudaMemcpyHostToDevice, s)) != cudaSuccess) { *what = "memcpy pd"; return e; };
+    if ((e = cudaMemcpyAsync(P.pd_base, pbase.data(), MAX_PHYS * 4, cudaMemcpyHostToDevice, s)) != cudaSuccess) { *what = "memcpy pd"; return e; };
+    if ((e = cudaMemcpyAsync(P.t_tab, ttab.data(), 65536 * 4, cudaMemcpyHostToDevice, s)) != cudaSuccess) { *what = "memcpy t_tab"; return e; };
+    if (!rph.empty() && (e = cudaMemcpyAsync(P.rs_philox, rph.data(), rph.size() * 4, cudaMemcpyHostToDevice, s)) != cudaSuccess)
+        { *what = "memcpy rs_philox"; return e; };
+    if (!rpr.empty() && (e = cudaMemcpyAsync(P.rs_pairs, rpr.data(), rpr.size() * 4, cudaMemcpyHostToDevice, s)) != cudaSuccess)
+        { *what = "memcpy rs_pairs"; return e; };
+    if ((e = cudaMemcpyAsync(P.rs_phys, rphys.data(), MAX_PHYS * 16, cudaMemcpyHostToDevice, s)) != cudaSuccess) { *what = "memcpy rs_phys"; return e; };
+    if ((e = cudaMemcpyAsync(P.rs_src, rsrc.data(), MAX_PHYS * 4, cudaMemcpyHostToDevice, s)) != cudaSuccess) { *what = "memcpy rs_src"; return e; };
+    if ((e = cudaMemcpyAsync(P.dec_tab, dec.data(), 512 * 8, cudaMemcpyHostToDevice, s)) != cudaSuccess) { *what = "memcpy dec"; return e; };
+    return cudaSuccess;
+}
+
+bool aligned16(const void* q) { return ((uintptr_t)q & 15u) == 0; }
+
+}  // namespace
+
+extern "C" {
+
+uint32_t dr_abi_version(void) { return DR_ABI_VERSION; }
+
+const char* dr_last_error(void) { return g_err; }
+
+int dr_params_default(dr_params* p) {
+    if (!p) return fail(DR_EINVAL, "params: NULL");
+    std::memset(p, 0, sizeof(*p));
+    p->abi_version = DR_ABI_VERSION;
+    p->struct_size = sizeof(dr_params);
+    p->layer_mask = DR_ALL;
+    p->n_act = DR_N_ACT;
+    p->n_tips = DR_N_TIPS;
+    p->n_substeps = DR_N_SUBSTEPS;
+    // Table action-noise (PAPER.md:47-61): % of the action range 2 (DESIGN.md Q8)
+    p->act_sigma_uadd = 0.10;
+    p->act_sigma_cadd = 0.03;
+    p->act_sigma_mult = 0.015;
+    p->delay_prob = 0.5;                   // PAPER.md:77-78
+    p->dt_base = 0.008;                    // PAPER.md:85
+    p->lambda_lo = 1250.0;                 // PAPER.md:88
+    p->lambda_hi = 10000.0;
+    p->step_nominal = 0.08;                // PAPER.md:79, 747
+    for (int j = 0; j < DR_N_ACT; ++j) {   // calibrated widths: not given (PAPER.md:98-99), Q21
+        p->delta_cal_neg[j] = 3.5 + 0.1 * j;
+        p->delta_cal_pos[j] = 4.0 + 0.1 * j;
+    }
+    p->delta_jitter_std = 0.1;             // PAPER.md:101
+    p->backlash_eps = 1e-12;               // PAPER.md:107
+    // Table obs-noise (PAPER.md:36-41)
+    p->tip_corr = 1e-3;
+    p->tip_uncorr = 2e-3;
+    p->obj_corr = 5e-3;
+    p->obj_uncorr = 1e-3;
+    p->rot_corr = 0.1;
+    p->rot_uncorr = 0.1;
+    p->tip_marker = 3e-3;
+    p->base_marker = 1e-3;
+    p->base_marker_to_tips = 1;            // Q14
+    p->dropout_hold_steps = 13;            // ceil(1 s / 80 ms), PAPER.md:64, Q11
+    p->dropout_rate_hz = 0.2;              // PAPER.md:64
+    p->occl_dist = 0.015;                  // Q13 (SPEC.md:227)
+    p->force_p_lo = 0.001;                 // PAPER.md:113
+    p->force_p_hi = 0.1;
+    p->force_accel_std = 1.0;              // PAPER.md:115
+    p->force_decay_per_step = 0.99;
+    // physical parameters: the paper's table is missing (PAPER.md:8); synthetic 256 slots, Q20
+    p->n_phys = DR_MAX_PHYS;
+    p->mass_index = 0;
+    for (int i = 0; i < DR_MAX_PHYS; ++i) {
+        dr_phys_desc& d = p->phys[i];
+        d.base = 0.5 + 0.01 * i;
+        switch (i % 4) {
+        case 0: d.kind = DR_PHYS_UNIFORM_SCALE; d.a = 0.5; d.b = 1.5; break;
+        case 1: d.kind = DR_PHYS_LOGUNIFORM_SCALE; d.a = 0.3; d.b = 3.0; break;
+        case 2: d.kind = DR_PHYS_ADD_GAUSS; d.a = 0.15; d.b = 0.0; break;
+        default: d.kind = DR_PHYS_MUL_LOGNORMAL; d.a = 0.2; d.b = 0.0; break;
+        }
+    }
+    return DR_OK;
+}
+
+size_t dr_workspace_bytes(const dr_params* params, int64_t n_env) {
+    if (!params || n_env < 1 || params->n_phys < 1 || params->n_phys > DR_MAX_PHYS) return 0;
+    return make_layout(n_env, params->n_phys, device_sm_count() * 32).total;
+}
+
+int dr_init(const dr_params* params, int64_t n_env, uint64_t seed) {
+    if (g_ctx) return fail(DR_EALREADY, "dr_init: context already initialised (call dr_finalize)");
+    int rc = validate(params, n_env);
+    if (rc != DR_OK) return rc;
+    g_sticky = false;
+    Ctx* c = new Ctx();
+    c->prm = *params;
+    if (c->prm.n_env_global == 0) c->prm.n_env_global = n_env;
+    c->n_env = n_env;
+    c->seed = seed;
+    c->stream = static_cast<cudaStream_t>(params->stream);
+    cudaError_t e = cudaGetDevice(&c->device);
+    if (e != cudaSuccess) { delete c; return cuda_fail(e, "cudaGetDevice"); }
+    c->sm_count = device_sm_count();
+    c->max_ctas = c->sm_count * 32;
+    c->lay = make_layout(n_env, params->n_phys, c->max_ctas);
+    if (params->workspace) {
+        if (params->workspace_bytes < c->lay.total) {
+            size_t need = c->lay.total;
+            delete c;
+            return fail(DR_ENOMEM, "workspace_bytes: %zu < required %zu", params->workspace_bytes, need);
+        }
+        c->ws = static_cast<char*>(params->workspace);
+        c->owns_ws = false;
+    } else {
+        e = cudaMalloc(&c->ws, c->lay.total);
+        if (e != cudaSuccess) { delete c; return fail(DR_ENOMEM, "cudaMalloc(%zu): %s", c->lay.total, cudaGetErrorString(e)); }
+        c->owns_ws = true;
+    }
+    const Layout& L = c->lay;
+    DevPtrs& P = c->p;
+    P.rec = reinterpret_cast<uint32_t*>(c->ws + L.rec);
+    P.st = reinterpret_cast<uint32_t*>(c->ws + L.st);
+    P.phys = reinterpret_cast<float*>(c->ws + L.phys);
+    P.pd_kind_rank = reinterpret_cast<uint32_t*>(c->ws + L.pd_kr);
+    P.pd_a = reinterpret_cast<float*>(c->ws + L.pd_a);
+    P.pd_b = reinterpret_cast<float*>(c->ws + L.pd_b);
+    P.pd_base = reinterpret_cast<float*>(c->ws + L.pd_base);
+    P.t_tab = reinterpret_cast<uint32_t*>(c->ws + L.t_tab);
+    P.rs_philox = reinterpret_cast<uint32_t*>(c->ws + L.rs_philox);
+    P.rs_pairs = reinterpret_cast<uint32_t*>(c->ws + L.rs_pairs);
+    P.rs_phys = reinterpret_cast<float4*>(c->ws + L.rs_phys);
+    P.rs_src = reinterpret_cast<uint32_t*>(c->ws + L.rs_src);
+    P.dec_tab = reinterpret_cast<double*>(c->ws + L.dec);
+    P.partials = reinterpret_cast<double*>(c->ws + L.partials);
+    P.stats = reinterpret_cast<double*>(c->ws + L.stats);
+    P.ctl = reinterpret_cast<unsigned long long*>(c->ws + L.ctl);
+    c->internal_stats = P.stats;
+
+    cudaStream_t s = c->stream;
     auto bail = [&](cudaError_t err, const char* what) {
         if (c->owns_ws) cudaFree(c->ws);
         delete c;
         return cuda_fail(err, what);
     };
-    if ((e = upload_const(dc, s)) != cudaSuccess) return bail(e, "upload_const");
-    if ((e = cudaMemcpyAsync(P.pd_kind_rank, kr.data(), MAX_PHYS * 4, cudaMemcpyHostToDevice, s)) != cudaSuccess) return bail(e, "memcpy pd");
-    if ((e = cudaMemcpyAsync(P.pd_a, pa.data(), MAX_PHYS * 4, cudaMemcpyHostToDevice, s)) != cudaSuccess) return bail(e, "memcpy pd");
-    if ((e = cudaMemcpyAsync(P.pd_b, pb.data(), MAX_PHYS * 4, cudaMemcpyHostToDevice, s)) != cudaSuccess) return bail(e, "memcpy pd");
-    if ((e = cudaMemcpyAsync(P.pd_base, pbase.data(), MAX_PHYS * 4, cudaMemcpyHostToDevice, s)) != cudaSuccess) return bail(e, "memcpy pd");
-    if ((e = cudaMemcpyAsync(P.t_tab, ttab.data(), 65536 * 4, cudaMemcpyHostToDevice, s)) != cudaSuccess) return bail(e, "memcpy t_tab");
-    if (!rph.empty() && (e = cudaMemcpyAsync(P.rs_philox, rph.data(), rph.size() * 4, cudaMemcpyHostToDevice, s)) != cudaSuccess)
-        return bail(e, "memcpy rs_philox");
-    if (!rpr.empty() && (e = cudaMemcpyAsync(P.rs_pairs, rpr.data(), rpr.size() * 4, cudaMemcpyHostToDevice, s)) != cudaSuccess)
-        return bail(e, "memcpy rs_pairs");
-    if ((e = cudaMemcpyAsync(P.rs_phys, rphys.data(), MAX_PHYS * 16, cudaMemcpyHostToDevice, s)) != cudaSuccess) return bail(e, "memcpy rs_phys");
-    if ((e = cudaMemcpyAsync(P.rs_src, rsrc.data(), MAX_PHYS * 4, cudaMemcpyHostToDevice, s)) != cudaSuccess) return bail(e, "memcpy rs_src");
-    if ((e = cudaMemcpyAsync(P.dec_tab, dec.data(), 512 * 8, cudaMemcpyHostToDevice, s)) != cudaSuccess) return bail(e, "memcpy dec");
+    const char* what = "";
+    if ((e = upload_params(c, c->prm, &what)) != cudaSuccess) return bail(e, what);
     if ((e = cudaMemsetAsync(P.stats, 0, 2 * N_STATS * 8, s)) != cudaSuccess) return bail(e, "memset stats");
     if ((e = cudaMemsetAsync(P.ctl, 0, 4 * 8, s)) != cudaSuccess) return bail(e, "memset ctl");
     // state planes start zeroed so that never-reset lanes of a partial tile stay defined
@@ -465,7 +477,7 @@ int dr_init(const dr_params* params, int64_t n_env, uint64_t seed) {
     const char* pp = std::getenv("DR_PIPE");
     set_step_prefetch(pf ? std::atoi(pf) : 0);
     set_step_pipe(pp ? std::atoi(pp) : 2);
-    const int occ_step = step_max_ctas_per_sm(p.layer_mask);
+    const int occ_step = step_max_ctas_per_sm(c->prm.layer_mask);
     const uint32_t n_tiles = (uint32_t)((n_env + TILE - 1) / TILE);
     c->step_grid = (int)std::min<long long>((long long)n_tiles, (long long)c->sm_count * occ_step);
     if (c->step_grid > c->max_ctas) c->step_grid = c->max_ctas;
@@ -479,6 +491,31 @@ int dr_init(const dr_params* params, int64_t n_env, uint64_t seed) {
     c->launches = 1;
     g_ctx = c;
     g_err[0] = 0;
+    return DR_OK;
+}
+
+int dr_update_params(const dr_params* params) {
+    Ctx* c = g_ctx;
+    if (!c) return fail(DR_ENOTINIT, "dr_update_params: no context");
+    if (g_sticky) return fail(DR_ECUDA, "sticky CUDA error: %s", g_err);
+    int rc = validate(params, c->n_env);
+    if (rc != DR_OK) return rc;
+    // what the context's shape, kernels and memory depend on cannot change without dr_init
+    if (params->layer_mask != c->prm.layer_mask)
+        return fail(DR_EINVAL, "layer_mask: cannot change on update (0x%x != 0x%x)", params->layer_mask, c->prm.layer_mask);
+    if (params->n_phys != c->prm.n_phys) return fail(DR_EINVAL, "n_phys: cannot change on update");
+    const int64_t ng = params->n_env_global ? params->n_env_global : c->n_env;
+    if (params->env_offset != c->prm.env_offset || ng != c->prm.n_env_global)
+        return fail(DR_EINVAL, "env_offset/n_env_global: cannot change on update");
+    dr_params np = *params;
+    np.n_env_global = c->prm.n_env_global;
+    np.workspace = c->prm.workspace;           // memory and stream stay the context's
+    np.workspace_bytes = c->prm.workspace_bytes;
+    np.stream = c->prm.stream;
+    const char* what = "";
+    cudaError_t e = upload_params(c, np, &what);
+    if (e != cudaSuccess) return cuda_fail(e, what);
+    c->prm = np;
     return DR_OK;
 }
 

@@ -93,6 +93,7 @@ def load():
     L.dr_params_default.argtypes = [C.POINTER(DrParams)]
     L.dr_init.argtypes = [C.POINTER(DrParams), C.c_int64, C.c_uint64]
     L.dr_reset.argtypes = [vp]
+    L.dr_update_params.argtypes = [C.POINTER(DrParams)]
     L.dr_step.argtypes = [fp] * 6
     L.dr_step_host.argtypes = [fp] * 6
     L.dr_finalize.argtypes = []
@@ -116,7 +117,7 @@ def load():
     L.dr_phys_export.argtypes = [vp, C.c_int64, C.c_int64]
     L.dr_debug_philox.argtypes = [C.c_uint32, C.c_uint32, C.c_uint32, vp]
     L.dr_debug_philox.restype = C.c_int
-    for f in ("dr_params_default", "dr_init", "dr_reset", "dr_step", "dr_step_host", "dr_finalize",
+    for f in ("dr_params_default", "dr_init", "dr_update_params", "dr_reset", "dr_step", "dr_step_host", "dr_finalize",
               "dr_set_stream", "dr_synchronize", "dr_set_stats_buffer", "dr_set_step_index",
               "dr_state_export", "dr_state_import", "dr_phys_export"):
         getattr(L, f).restype = C.c_int
@@ -186,6 +187,10 @@ def params_from_preset(preset: dict, env_offset: int = 0, n_env_global: int = 0,
 # ---------------------------------------------------------------------------------------------
 def dr_init(params: DrParams, n_env: int, seed: int):
     return _check(load().dr_init(C.byref(params), n_env, seed))
+
+
+def dr_update_params(params: DrParams):
+    return _check(load().dr_update_params(C.byref(params)))
 
 
 def dr_reset(env_mask=None, n_env=None):

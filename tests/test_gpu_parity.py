@@ -45,9 +45,10 @@ def _oracle(preset, gids, seed=SEED):
 
 
 def run_pair(torch, mask, n_env, T, n_frames=8, resets=None, sample=None, state_every=1,
-             stats=True, seed=SEED, frame_seed=presets.SEED_WORKLOAD, **kw):
+             stats=True, seed=SEED, frame_seed=presets.SEED_WORKLOAD, updates=None, **kw):
     """Run the GPU on all n_env envs and the oracle on `sample` (default: all); compare every
-    step.  `resets`: {t: uint8 mask [n_env]} applied before step t."""
+    step.  `resets`: {t: uint8 mask [n_env]} applied before step t; `updates`: {t: parameter
+    overrides} swapped in with dr_update_params / orc_update_params before step t."""
     P = presets.preset(mask, **kw)
     acts, obs = gen.frames(n_env, n_frames, seed=frame_seed)
     A = _frames_cuda(torch, acts)
@@ -62,6 +63,10 @@ def run_pair(torch, mask, n_env, T, n_frames=8, resets=None, sample=None, state_
         compare_records({k: v[gids] for k, v in G.items()}, [orc.env(i) for i in range(len(gids))],
                         phys_g=ctx.phys()[gids], mask=mask)
         for t in range(T):
+            if updates and t in updates:
+                P = presets.preset(mask, **{**kw, **updates[t]})
+                ctx.update_params(P)
+                orc.update_params(P)
             if resets and t in resets:
                 m = resets[t]
                 ctx.reset(torch.from_numpy(m).cuda())
@@ -156,6 +161,35 @@ def test_ragged_sizes(torch_cuda, n):
     run_pair(torch_cuda, FULL, n, 12, n_frames=12, resets={6: (np.arange(n) % 2 == 0).astype(np.uint8)})
 
 
+def test_update_params_mid_run(torch_cuda):
+    """On-the-fly parameter updates: step-draw parameters change from the next
+    step, episode-draw parameters at each env's next reset -- identically on both sides."""
+    n = 300
+    upd = {
+        5: dict(act_sigma_uadd=0.2, act_sigma_mult=0.05, tip_uncorr=4e-3, obj_uncorr=3e-3, rot_uncorr=0.2,
+                dropout_rate_hz=2.0, dropout_hold_steps=5, occl_dist=0.03, force_accel_std=2.0,
+                force_decay_per_step=0.9, force_p_lo=0.05, force_p_hi=0.5, lambda_lo=2000.0, lambda_hi=3000.0,
+                delay_prob=0.9, act_sigma_cadd=0.01, delta_jitter_std=0.3, dt_base=0.01),
+        14: dict(act_sigma_uadd=0.0, act_sigma_mult=0.0, force_p_lo=1e-3, force_p_hi=1e-3),
+    }
+    resets = {9: (np.arange(n) % 3 == 0).astype(np.uint8), 16: (np.arange(n) % 2 == 1).astype(np.uint8)}
+    run_pair(torch_cuda, FULL, n, 22, n_frames=22, resets=resets, updates=upd)
+
+
+def test_update_params_rejects_shape_changes(torch_cuda):
+    from paper_1906_11633_b200 import dr
+    ctx = _ctx(presets.preset(CFG2), 64)
+    try:
+        with pytest.raises(dr.DRError, match="layer_mask"):
+            ctx.update_params(presets.preset(FULL))
+        with pytest.raises(dr.DRError, match="n_phys"):
+            ctx.update_params(presets.preset(CFG2, n_phys=8))
+        with pytest.raises(dr.DRError, match="delay_prob"):
+            ctx.update_params(presets.preset(CFG2, delay_prob=1.5))
+    finally:
+        ctx.close()
+
+
 def test_config2_cfg2_4096(torch_cuda):
     """BASELINE config 2 shape (4,096 envs, backlash + action/obs noise): 100 steps on all envs,
     then 1,000 steps on a 64-env sample (the full run length), knife-edge aware."""
@@ -197,6 +231,10 @@ def _run_outputs(torch, P, n, T, seed=SEED, env_offset=0, n_env_global=0, rows=N
     outs = []
     try:
         for t in range(T):
+            if updates and t in updates:
+                P = presets.preset(mask, **{**kw, **updates[t]})
+                ctx.update_params(P)
+                orc.update_params(P)
             if resets and t in resets:
                 ctx.reset(torch.from_numpy(resets[t][lo:lo + n].copy()).cuda())
             ctx.step(A[t % 6], O[t % 6])

@@ -499,3 +499,63 @@ def test_reset_mask_semantics():
             assert e["episode"] == 0
             assert np.array_equal(e["c_act"], before[i]["c_act"])
     assert orc.step(acts[1], obs[1])["stats"][10] == 0
+
+
+# ---- on-the-fly parameter updates ----------------------
+def test_update_params_identity_and_step_vs_episode_split():
+    """An update with the same parameters changes nothing (bitwise); a step-draw parameter takes
+    effect at the next step (a0 with the uncorrelated/multiplicative action noise zeroed is the
+    closed form clamp(a + c_act)); an episode-draw parameter only at the next
+    reset (lambda range collapsed to one point: reset envs get exactly that lambda, the others
+    keep theirs)."""
+    n, T = 16, 6
+    acts, obs = gen.frames(n, T)
+    a = _oracle(FULL, n)
+    b = _oracle(FULL, n)
+    for t in range(T):
+        if t == 3:
+            b.update_params(presets.preset(FULL))
+        ra, rb = a.step(acts[t], obs[t]), b.step(acts[t], obs[t])
+        for k in ("out_actions", "out_obs", "out_dt", "out_force", "stats"):
+            assert np.array_equal(ra[k], rb[k]), (t, k)
+    a.close(), b.close()
+
+    o = _oracle(ACT_NOISE, n)
+    o.step(acts[0], obs[0])
+    o.update_params(presets.preset(ACT_NOISE, act_sigma_uadd=0.0, act_sigma_mult=0.0))
+    r = o.step(acts[1], obs[1])
+    cact = np.array([o.env(i)["c_act"] for i in range(n)])
+    assert np.array_equal(r["out_actions"], np.clip(acts[1].astype(np.float64) + cact, -1.0, 1.0))
+    o.close()
+
+    o = _oracle(TIMING, n)
+    lam0 = np.array([o.env(i)["lambda"] for i in range(n)])
+    o.update_params(presets.preset(TIMING, lambda_lo=5000.0, lambda_hi=5000.0))
+    m = (np.arange(n) % 2).astype(np.uint8)
+    o.reset(m)
+    lam1 = np.array([o.env(i)["lambda"] for i in range(n)])
+    assert np.array_equal(lam1[m == 0], lam0[m == 0])
+    assert (lam1[m == 1] == 5000.0).all()
+    o.close()
+
+
+def test_update_params_force_and_dropout_thresholds():
+    """Force p range collapsed to p0 after an update: reset envs carry T = floor(p0 2^32) (the
+    table's midpoints all equal p0); a dropout rate of 0 after the update stops new
+    initiations from the next step while running timers count down."""
+    from oracle import oracle as O
+    n = 64
+    acts, obs = gen.frames(n, 30)
+    o = _oracle(FULL, n)
+    o.update_params(presets.preset(FULL, force_p_lo=0.25, force_p_hi=0.25, dropout_rate_hz=0.0))
+    assert o.force_threshold(0) == o.force_threshold(65535) == O.bernoulli_threshold(0.25)
+    before = [o.env(i)["t_force"] for i in range(n)]
+    o.reset((np.arange(n) < 32).astype(np.uint8))
+    after = [o.env(i)["t_force"] for i in range(n)]
+    assert all(after[i] == O.bernoulli_threshold(0.25) for i in range(32))
+    assert after[32:] == before[32:]
+    inits = 0
+    for t in range(30):
+        inits += o.step(acts[t], obs[t])["stats"][2]
+    assert inits == 0
+    o.close()
