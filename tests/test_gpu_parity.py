@@ -231,10 +231,6 @@ def _run_outputs(torch, P, n, T, seed=SEED, env_offset=0, n_env_global=0, rows=N
     outs = []
     try:
         for t in range(T):
-            if updates and t in updates:
-                P = presets.preset(mask, **{**kw, **updates[t]})
-                ctx.update_params(P)
-                orc.update_params(P)
             if resets and t in resets:
                 ctx.reset(torch.from_numpy(resets[t][lo:lo + n].copy()).cuda())
             ctx.step(A[t % 6], O[t % 6])
