@@ -143,6 +143,39 @@ void   orc_backlash(double s, double a, double dneg, double dpos, double dt, dou
 int    orc_occluded(const float* tips15, const float* obj3, double r, int tip);
 uint64_t orc_bernoulli_threshold(double p);
 
+/* ---- vision randomization (Table vision-randomization) ----
+ * Appearance draws per sample and the post-render image augmentation per camera image;
+ * readings V1-V6 in DESIGN.md.  Draws: Philox keyed by the seed, counter = (global sample or
+ * image id, batch index, channel, block), channels below. */
+#define ORC_VIS_N_CAMERAS  3
+#define ORC_VIS_MAX_LIGHTS 6
+#define ORC_SCENE_WORDS    64   /* scene record: see orc_scene_draw */
+typedef struct {
+    double cam_pos_range, cam_rot_max, cam_fov_range;            /* 1.5 mm, 3 deg, 1 deg */
+    double robot_metallic_lo, robot_metallic_hi, robot_gloss_lo, robot_gloss_hi;
+    double obj_hue_cal, obj_sat_cal, obj_val_cal;                 /* calibrated HSV in [0, 1] */
+    double obj_hue_range, obj_sat_range, obj_val_range;           /* 0.01, 0.15, 0.15 */
+    double obj_metallic_lo, obj_metallic_hi, obj_gloss_lo, obj_gloss_hi;
+    int32_t lights_min, lights_max;                               /* 4, 6 */
+    double light_rel_lo, light_rel_hi, light_total_lo, light_total_hi;   /* 1..5, 0..15 */
+    double contrast_lo, contrast_hi;                              /* 0.5, 1.5 */
+    double noise_std_lo, noise_std_hi;                            /* 0.1, 0.1 (normalized units) */
+    double std_floor;                                             /* 1e-8 */
+} orc_vision_params;
+
+/* Appearance draws of samples [sample_offset, sample_offset + n): out [n][64] fp64, fields in
+ * the order cam_pos[3][3], cam_quat[3][4], cam_fov[3], robot_rgb[3], robot_metallic,
+ * robot_gloss, obj_hsv[3], obj_metallic, obj_gloss, n_lights, light_dir[6][3],
+ * light_intensity[6], total_intensity, 4 zero pad words. */
+int orc_scene_draw(const orc_vision_params* p, uint64_t seed, uint64_t batch, int64_t sample_offset, int64_t n,
+                   double* out);
+/* Post-render augmentation of n u8 images [n][H][W][C]: normalise each image
+ * to zero mean / unit variance, scale by a contrast factor, add per-pixel Gaussian noise.
+ * out [n][H][W][C] fp64; img_stats [n][4] = (mean, std, contrast, noise std), may be NULL. */
+int orc_image_augment(const orc_vision_params* p, uint64_t seed, uint64_t batch, int64_t image_offset,
+                      const uint8_t* images, int64_t n, int32_t h, int32_t w, int32_t c, double* out,
+                      double* img_stats);
+
 /* stats slot indices */
 enum {
     ORC_S_ENVS = 0, ORC_S_DELAYED = 1, ORC_S_DROP_INIT = 2, ORC_S_MASKED = 3, ORC_S_OCCLUDED = 4,

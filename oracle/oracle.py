@@ -14,7 +14,7 @@ import numpy as np
 
 HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.path.join(HERE, "liboracle.so")
-SOURCES = [os.path.join(HERE, "oracle.c")]
+SOURCES = [os.path.join(HERE, "oracle.c"), os.path.join(HERE, "oracle_vision.c")]
 HEADERS = [os.path.join(HERE, "oracle.h")]
 
 N_ACT, N_TIPS, N_SUB, MAX_PHYS, OBS_IN, OBS_OUT, N_STATS = 20, 5, 10, 256, 26, 22, 32
@@ -69,6 +69,18 @@ class OrcEnv(C.Structure):
     ]
 
 
+class OrcVisionParams(C.Structure):
+    _fields_ = [(n, C.c_double) for n in (
+        "cam_pos_range", "cam_rot_max", "cam_fov_range", "robot_metallic_lo", "robot_metallic_hi",
+        "robot_gloss_lo", "robot_gloss_hi", "obj_hue_cal", "obj_sat_cal", "obj_val_cal", "obj_hue_range",
+        "obj_sat_range", "obj_val_range", "obj_metallic_lo", "obj_metallic_hi", "obj_gloss_lo", "obj_gloss_hi")] + [
+        ("lights_min", C.c_int32), ("lights_max", C.c_int32)] + [(n, C.c_double) for n in (
+        "light_rel_lo", "light_rel_hi", "light_total_lo", "light_total_hi", "contrast_lo", "contrast_hi",
+        "noise_std_lo", "noise_std_hi", "std_floor")]
+
+
+SCENE_WORDS = 64
+
 _lib = None
 
 
@@ -82,6 +94,11 @@ def lib():
                                C.POINTER(C.c_void_p)]
         L.orc_init.restype = C.c_int
         L.orc_free.argtypes = [C.c_void_p]
+        L.orc_scene_draw.argtypes = [C.POINTER(OrcVisionParams), C.c_uint64, C.c_uint64, C.c_int64, C.c_int64, dp]
+        L.orc_scene_draw.restype = C.c_int
+        L.orc_image_augment.argtypes = [C.POINTER(OrcVisionParams), C.c_uint64, C.c_uint64, C.c_int64, u8p,
+                                        C.c_int64, C.c_int32, C.c_int32, C.c_int32, dp, dp]
+        L.orc_image_augment.restype = C.c_int
         L.orc_update_params.argtypes = [C.c_void_p, C.POINTER(OrcParams)]
         L.orc_update_params.restype = C.c_int
         L.orc_reset.argtypes = [C.c_void_p, u8p]
@@ -182,6 +199,39 @@ def occluded(tips15, obj3, r, tip):
 
 def bernoulli_threshold(p):
     return lib().orc_bernoulli_threshold(p)
+
+
+# ---- vision randomization (Table vision-randomization, PAPER.md:118-157) ----------------------
+def make_vision_params(preset: dict) -> OrcVisionParams:
+    p = OrcVisionParams()
+    for name, _ in OrcVisionParams._fields_:
+        setattr(p, name, preset[name])
+    return p
+
+
+def scene_draw(preset: dict, seed: int, batch: int, n: int, sample_offset: int = 0):
+    """[n][64] fp64 appearance draws (field order: oracle.h orc_scene_draw)."""
+    p = make_vision_params(preset)
+    out = np.zeros((n, SCENE_WORDS))
+    rc = lib().orc_scene_draw(C.byref(p), C.c_uint64(seed), C.c_uint64(batch), sample_offset, n,
+                              _ptr(out, C.c_double))
+    if rc != 0:
+        raise ValueError(f"orc_scene_draw failed: {rc}")
+    return out
+
+
+def image_augment(preset: dict, seed: int, batch: int, images, image_offset: int = 0):
+    """images: u8 [n][H][W][C] -> (fp64 [n][H][W][C], fp64 [n][4] = mean, std, contrast, noise std)."""
+    x = np.ascontiguousarray(images, dtype=np.uint8)
+    n, h, w, c = x.shape
+    p = make_vision_params(preset)
+    out = np.empty(x.shape, dtype=np.float64)
+    st = np.empty((n, 4))
+    rc = lib().orc_image_augment(C.byref(p), C.c_uint64(seed), C.c_uint64(batch), image_offset,
+                                 _ptr(x, C.c_uint8), n, h, w, c, _ptr(out, C.c_double), _ptr(st, C.c_double))
+    if rc != 0:
+        raise ValueError(f"orc_image_augment failed: {rc}")
+    return out, st
 
 
 # ---- context -------------------------------------------------------------------------------

@@ -85,3 +85,38 @@ def preset(layer_mask: int = FULL, **overrides) -> dict:
             raise KeyError(f"unknown parameter {k!r}")
         p[k] = v
     return p
+
+
+# ---- vision randomizations: Table vision-randomization -------------------------
+import math as _math  # noqa: E402
+
+VISION = {
+    "cam_pos_range": 1.5e-3,                      # "camera position +-1.5 mm"
+    "cam_rot_max": 3.0 * _math.pi / 180.0,        # "camera rotation 0-3 deg around a random axis"
+    "cam_fov_range": 1.0 * _math.pi / 180.0,      # "camera field of view +-1 deg" (radians)
+    "robot_metallic_lo": 0.05, "robot_metallic_hi": 0.25,   # "robot material metallic level 5%-25%"
+    "robot_gloss_lo": 0.0, "robot_gloss_hi": 1.0,           # "robot material glossiness level 0%-100%"
+    # calibrated object HSV: "around calibrated values from real-world measurements",
+    # values not given -- workload choice (parity unpinned), picked so hue wraps and saturation clamps
+    "obj_hue_cal": 0.005, "obj_sat_cal": 0.9, "obj_val_cal": 0.5,
+    "obj_hue_range": 0.01, "obj_sat_range": 0.15, "obj_val_range": 0.15,   # "+-1 %", "+-15 %", "+-15 %"
+    "obj_metallic_lo": 0.05, "obj_metallic_hi": 0.15,       # "object metallic level 5%-15%"
+    "obj_gloss_lo": 0.05, "obj_gloss_hi": 0.15,             # "object glossiness level 5%-15%"
+    "lights_min": 4, "lights_max": 6,                       # "number of lights 4-6"
+    "light_rel_lo": 1.0, "light_rel_hi": 5.0,               # "light relative intensity 1-5"
+    "light_total_lo": 0.0, "light_total_hi": 15.0,          # "total light intensity 0-15"
+    "contrast_lo": 0.5, "contrast_hi": 1.5,                 # "image contrast adjustment 50%-150%"
+    "noise_std_lo": 0.1, "noise_std_hi": 0.1,               # "additive per-pixel Gaussian noise +-10%" [V6]
+    "std_floor": 1e-8,                                      # constant images
+}
+# the paper's vision batch: 64 samples x 3 cameras = 192 RGB images of 200 x 200 x 8-bit
+VISION_BATCH_SAMPLES, VISION_CAMERAS, VISION_H, VISION_W, VISION_C = 64, 3, 200, 200, 3
+
+
+def vision_preset(**overrides) -> dict:
+    p = copy.deepcopy(VISION)
+    for k, v in overrides.items():
+        if k not in p:
+            raise KeyError(f"unknown vision parameter {k!r}")
+        p[k] = v
+    return p
