@@ -217,6 +217,8 @@ int      dr_phys_export(void* host_dst, int64_t env_lo, int64_t env_hi);
 const char* dr_last_error(void);
 /* Launches of library kernels enqueued since dr_init (host count; graph replays not counted). */
 uint64_t dr_kernel_launches(void);
+/* Every libdr kernel launch of the process (context calls and the context-free vision calls). */
+uint64_t dr_total_kernel_launches(void);
 /* Test hook: out_dev[e][0..3] = the device Philox4x32-10 block the kernels draw for counter
  * (global id of env e, domain, channel, block) under the context's seed.  out_dev: device
  * uint32 [n_env][4].  Asynchronous.  Lets tests check the RNG words bit-exactly. */

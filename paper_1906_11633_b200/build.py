@@ -11,8 +11,8 @@ ROOT = os.path.dirname(PKG)
 CSRC = os.path.join(PKG, "csrc")
 INCLUDE = os.path.join(ROOT, "include")
 LIB = os.path.join(PKG, "libdr.so")
-SOURCES = [os.path.join(CSRC, f) for f in ("dr_kernels.cu", "dr_api.cu")]
-DEPS = SOURCES + [os.path.join(CSRC, f) for f in ("dr_internal.h", "dr_device.cuh", "dr_step.cuh", "dr_reset.cuh")] + [os.path.join(INCLUDE, "dr.h")]
+SOURCES = [os.path.join(CSRC, f) for f in ("dr_kernels.cu", "dr_api.cu", "dr_vision.cu")]
+DEPS = SOURCES + [os.path.join(CSRC, f) for f in ("dr_internal.h", "dr_device.cuh", "dr_math.cuh", "dr_step.cuh", "dr_reset.cuh")] + [os.path.join(INCLUDE, f) for f in ("dr.h", "dr_vision.h")]
 
 NVCC = os.environ.get("NVCC", "nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]

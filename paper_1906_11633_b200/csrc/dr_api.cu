@@ -339,7 +339,23 @@ cudaError_t upload_params(Ctx* c, const dr_params& p, const char** what) {
 
 bool aligned16(const void* q) { return ((uintptr_t)q & 15u) == 0; }
 
+uint64_t g_total_launches = 0;   // every libdr kernel launch of the process (context or not)
+
 }  // namespace
+
+namespace dr {
+int set_error(int code, const char* fmt, ...) {
+    va_list ap;
+    va_start(ap, fmt);
+    vsnprintf(g_err, sizeof(g_err), fmt, ap);
+    va_end(ap);
+    return code;
+}
+void count_launch() {
+    ++g_total_launches;
+    if (g_ctx) g_ctx->launches++;
+}
+}  // namespace dr
 
 extern "C" {
 
@@ -489,6 +505,7 @@ int dr_init(const dr_params* params, int64_t n_env, uint64_t seed) {
     // episode 0 for every env (sampled at the beginning of every episode)
     if ((e = launch_reset(P, nullptr, true, (uint32_t)n_env, c->reset_grid, s)) != cudaSuccess) return bail(e, "reset_kernel");
     c->launches = 1;
+    ++g_total_launches;
     g_ctx = c;
     g_err[0] = 0;
     return DR_OK;
@@ -526,6 +543,7 @@ int dr_reset(const uint8_t* env_mask) {
     cudaError_t e = launch_reset(c->p, env_mask, false, (uint32_t)c->n_env, c->reset_grid, c->stream);
     if (e != cudaSuccess) return cuda_fail(e, "reset_kernel");
     c->launches++;
+    ++g_total_launches;
     return DR_OK;
 }
 
@@ -545,6 +563,7 @@ int dr_step(const float* actions, const float* raw_obs, float* out_actions, floa
     if (e != cudaSuccess) return cuda_fail(e, "step_kernel");
     c->t_host++;
     c->launches++;
+    ++g_total_launches;
     return DR_OK;
 }
 
@@ -652,6 +671,7 @@ int dr_state_export(void* host_dst, int64_t env_lo, int64_t env_hi) {
     cudaError_t e = launch_export(c->p, d, (uint32_t)env_lo, (uint32_t)env_hi, c->stream);
     if (e != cudaSuccess) return cuda_fail(e, "export_kernel");
     c->launches++;
+    ++g_total_launches;
     CK(cudaMemcpyAsync(host_dst, d, bytes, cudaMemcpyDeviceToHost, c->stream));
     CK(cudaFreeAsync(d, c->stream));
     CK(cudaStreamSynchronize(c->stream));
@@ -671,6 +691,7 @@ int dr_state_import(const void* host_src, int64_t env_lo, int64_t env_hi) {
     cudaError_t e = launch_import(c->p, d, (uint32_t)env_lo, (uint32_t)env_hi, c->stream);
     if (e != cudaSuccess) return cuda_fail(e, "import_kernel");
     c->launches++;
+    ++g_total_launches;
     CK(cudaFreeAsync(d, c->stream));
     CK(cudaStreamSynchronize(c->stream));
     return DR_OK;
@@ -690,6 +711,7 @@ int dr_phys_export(void* host_dst, int64_t env_lo, int64_t env_hi) {
 }
 
 uint64_t dr_kernel_launches(void) { return g_ctx ? g_ctx->launches : 0; }
+uint64_t dr_total_kernel_launches(void) { return g_total_launches; }
 
 int dr_debug_philox(uint32_t domain, uint32_t channel, uint32_t block, uint32_t* out_dev) {
     Ctx* c = g_ctx;
@@ -698,6 +720,7 @@ int dr_debug_philox(uint32_t domain, uint32_t channel, uint32_t block, uint32_t*
     cudaError_t e = launch_debug_philox((uint32_t)c->n_env, domain, channel, block, out_dev, c->stream);
     if (e != cudaSuccess) return cuda_fail(e, "debug_philox_kernel");
     c->launches++;
+    ++g_total_launches;
     return DR_OK;
 }
 

@@ -154,6 +154,10 @@ struct DevPtrs {
     unsigned long long* ctl;  // [0] = step t, [1] = CTAs done counter, [2] = resets pending
 };
 
+// error / launch bookkeeping shared by every C-ABI entry point (dr_api.cu)
+int set_error(int code, const char* fmt, ...);   // records the message for dr_last_error(), returns code
+void count_launch();                              // one library kernel enqueued
+
 // launchers (dr_kernels.cu)
 cudaError_t upload_const(const DevConst& c, cudaStream_t s);
 cudaError_t launch_reset(const DevPtrs& p, const uint8_t* mask, bool first, uint32_t n_env,

@@ -1,0 +1,456 @@
+// dr_vision.cu -- vision randomizations (include/dr_vision.h): appearance draws (Table
+// vision-randomization) and the post-render image augmentation
+// for sm_100a.
+//
+// image_augment_kernel: one thread-block cluster of K CTAs per image (K = 1..8, chosen so a
+// CTA's slice of the image fits in <= 32 KB of shared memory when it can).  Each CTA
+//   1. pulls its slice of the u8 image into shared memory with one TMA bulk copy
+//      (cp.async.bulk + mbarrier complete_tx), so the image crosses HBM exactly once;
+//   2. reduces exact integer sum / sum of squares (DP4A: 2 instructions per 4 pixels), then the
+//      cluster exchanges the K partials through distributed shared memory (mapa +
+//      ld.shared::cluster between two cluster barriers) -- every CTA gets the same exact totals;
+//   3. writes out = (x - mean) * (f / std) + s * z with streaming float4 stores, one Philox
+//      block per 4 elements for the noise.
+// HBM traffic per image: E bytes in + 4E bytes out (E = H W C), the algorithmic minimum.
+#include <cuda_runtime.h>
+
+#include <cmath>
+#include <cstdio>
+
+#include "dr.h"
+#include "dr_internal.h"
+#include "dr_math.cuh"
+#include "dr_vision.h"
+
+namespace dr {
+
+enum : uint32_t { CH_IMG_PARAM = 0x201, CH_IMG_NOISE = 0x202, CH_SCENE_CAM = 0x301, CH_SCENE_MAT = 0x302,
+                  CH_SCENE_LIGHT = 0x303 };
+
+constexpr int IMG_THREADS = 256;
+constexpr uint32_t IMG_SLICE_TARGET = 32 * 1024;
+constexpr uint32_t IMG_SLICE_MAX = 200 * 1024;
+
+struct ImgArgs {
+    const uint8_t* images;
+    float* out;
+    float* img_stats;
+    uint64_t E;          // bytes (= elements) per image
+    uint32_t slice;      // bytes per CTA slice (multiple of 16)
+    uint32_t aligned;    // TMA + float4 path (E % 16 == 0, pointers 16-byte aligned)
+    uint32_t batch;
+    uint32_t image_offset;
+    double contrast_lo, contrast_range, noise_lo, noise_range;   // lo + (hi - lo) U, as the oracle
+    double std_floor;
+    PhiloxKeys keys;
+};
+
+// ---- cluster / DSMEM / TMA helpers (PTX, sm_90+) ------------------------------------------
+__device__ __forceinline__ uint32_t smem_addr(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
+__device__ __forceinline__ uint32_t cluster_rank() {
+    uint32_t r;
+    asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
+    return r;
+}
+__device__ __forceinline__ uint32_t cluster_size() {
+    uint32_t n;
+    asm volatile("mov.u32 %0, %%cluster_nctarank;" : "=r"(n));
+    return n;
+}
+__device__ __forceinline__ void cluster_arrive() { asm volatile("barrier.cluster.arrive.release.aligned;" ::: "memory"); }
+__device__ __forceinline__ void cluster_wait() { asm volatile("barrier.cluster.wait.acquire.aligned;" ::: "memory"); }
+// 64-bit load from CTA `rank`'s copy of the shared variable at local address `a`
+__device__ __forceinline__ unsigned long long ld_dsmem_u64(uint32_t a, uint32_t rank) {
+    uint32_t ra;
+    unsigned long long v;
+    asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(ra) : "r"(a), "r"(rank));
+    asm volatile("ld.shared::cluster.u64 %0, [%1];" : "=l"(v) : "r"(ra) : "memory");
+    return v;
+}
+__device__ __forceinline__ void mbar_init1(uint64_t* bar) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_addr(bar)) : "memory");
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+}
+__device__ __forceinline__ void mbar_expect(uint64_t* bar, uint32_t bytes) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_addr(bar)), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void mbar_wait0(uint64_t* bar) {
+    asm volatile(
+        "{\n\t.reg .pred p;\n"
+        "W_%=:\n\t"
+        "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], 0;\n\t"
+        "@!p bra W_%=;\n}" ::"r"(smem_addr(bar))
+        : "memory");
+}
+__device__ __forceinline__ void tma_bulk(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
+    asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                     smem_addr(dst)),
+                 "l"(src), "r"(bytes), "r"(smem_addr(bar))
+                 : "memory");
+}
+
+// the 4 normals of noise block b of image g: element 4b + k takes normal k
+__device__ __forceinline__ void noise4(const ImgArgs& a, uint32_t g, uint32_t b, float z[4]) {
+    const uint4 w = philox_k(g, a.batch, CH_IMG_NOISE, b, a.keys);
+    box_muller_sfu(w.x, w.y, z[0], z[1]);
+    box_muller_sfu(w.z, w.w, z[2], z[3]);
+}
+
+__global__ void __launch_bounds__(IMG_THREADS) image_augment_kernel(const ImgArgs a) {
+    extern __shared__ __align__(128) uint8_t s_img[];
+    __shared__ __align__(8) uint64_t s_bar;
+    __shared__ unsigned long long s_part[2];
+    __shared__ unsigned long long s_warp[2][IMG_THREADS / 32];
+
+    const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
+    const uint32_t K = cluster_size(), r = cluster_rank();
+    const uint64_t img = blockIdx.x / K;
+    const uint64_t E = a.E;
+    const uint64_t lo0 = (uint64_t)r * a.slice;
+    const uint64_t lo = lo0 < E ? lo0 : E;
+    const uint64_t hi = (lo + a.slice) < E ? (lo + a.slice) : E;
+    const uint32_t n = (uint32_t)(hi - lo);
+    const uint8_t* src = a.images + img * E + lo;
+
+    // ---- 1. slice -> shared memory (one TMA bulk copy) ----
+    if (a.aligned) {
+        if (tid == 0) mbar_init1(&s_bar);
+        __syncthreads();
+        if (tid == 0) {
+            mbar_expect(&s_bar, n);
+            if (n) tma_bulk(s_img, src, n, &s_bar);
+        }
+        mbar_wait0(&s_bar);
+    } else {
+        for (uint32_t i = tid; i < n; i += IMG_THREADS) s_img[i] = __ldg(src + i);
+        __syncthreads();
+    }
+
+    // ---- 2. exact integer moments, CTA then cluster ----
+    uint32_t sum = 0, sq = 0;
+    const uint32_t n4 = n >> 2;
+    const uint32_t* w4 = reinterpret_cast<const uint32_t*>(s_img);
+    for (uint32_t i = tid; i < n4; i += IMG_THREADS) {
+        const uint32_t x = w4[i];
+        sum = __dp4a(x, 0x01010101u, sum);
+        sq = __dp4a(x, x, sq);
+    }
+    for (uint32_t i = 4 * n4 + tid; i < n; i += IMG_THREADS) {
+        const uint32_t x = s_img[i];
+        sum += x;
+        sq += x * x;
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+        sum += __shfl_xor_sync(0xFFFFFFFFu, sum, o);
+        sq += __shfl_xor_sync(0xFFFFFFFFu, sq, o);
+    }
+    if (lane == 0) {
+        s_warp[0][wid] = sum;
+        s_warp[1][wid] = sq;
+    }
+    __syncthreads();
+    if (tid == 0) {
+        unsigned long long S = 0, Q = 0;
+#pragma unroll
+        for (int k = 0; k < IMG_THREADS / 32; ++k) {
+            S += s_warp[0][k];
+            Q += s_warp[1][k];
+        }
+        s_part[0] = S;
+        s_part[1] = Q;
+    }
+    cluster_arrive();   // publishes s_part to the cluster
+    cluster_wait();
+    unsigned long long S = 0, Q = 0;
+    for (uint32_t q = 0; q < K; ++q) {   // fixed rank order: identical totals in every CTA
+        S += ld_dsmem_u64(smem_addr(&s_part[0]), q);
+        Q += ld_dsmem_u64(smem_addr(&s_part[1]), q);
+    }
+    cluster_arrive();   // done reading the other CTAs' shared memory (matched by the wait at exit)
+
+    // ---- 3. normalise, contrast, noise ----
+    const uint32_t g = a.image_offset + (uint32_t)img;
+    const double mean = (double)S / (double)E;
+    const unsigned long long vnum = Q * E - S * S;   // E^2 var, exact (no overflow below the size limit)
+    const double sd = sqrt((double)vnum / ((double)E * (double)E));
+    const uint4 pw = philox_k(g, a.batch, CH_IMG_PARAM, 0, a.keys);
+    const double f = a.contrast_lo + a.contrast_range * (double)uni(pw.x);
+    const double s = a.noise_lo + a.noise_range * (double)uni(pw.y);
+    const float scale = (float)(f / (sd > a.std_floor ? sd : a.std_floor));
+    const float mu_hi = (float)mean, mu_lo = (float)(mean - (double)mu_hi);   // x - mu_hi is exact
+    const float sf = (float)s;
+    if (r == 0 && tid == 0 && a.img_stats)
+        reinterpret_cast<float4*>(a.img_stats)[img] = make_float4((float)mean, (float)sd, (float)f, sf);
+
+    float* out = a.out + img * E + lo;
+    const uint32_t b0 = (uint32_t)(lo >> 2);   // lo is a multiple of 16
+    if (a.aligned) {
+        float4* o4 = reinterpret_cast<float4*>(out);
+        for (uint32_t i = tid; i < n4; i += IMG_THREADS) {
+            const uint32_t x = w4[i];
+            float z[4];
+            noise4(a, g, b0 + i, z);
+            float v[4];
+#pragma unroll
+            for (int k = 0; k < 4; ++k) {
+                const float d = ((float)((x >> (8 * k)) & 0xFFu) - mu_hi) - mu_lo;
+                v[k] = fmaf(d, scale, sf * z[k]);
+            }
+            __stcs(o4 + i, make_float4(v[0], v[1], v[2], v[3]));
+        }
+    } else {
+        for (uint32_t i = tid; i < (n + 3) / 4; i += IMG_THREADS) {
+            float z[4];
+            noise4(a, g, b0 + i, z);
+#pragma unroll
+            for (int k = 0; k < 4; ++k) {
+                const uint32_t e = 4 * i + k;
+                if (e < n) {
+                    const float d = ((float)s_img[e] - mu_hi) - mu_lo;
+                    out[e] = fmaf(d, scale, sf * z[k]);
+                }
+            }
+        }
+    }
+    cluster_wait();   // no CTA leaves while another may still read its s_part
+}
+
+// ---- appearance draws: one thread per sample, fp64 (no contraction in the decision chain) ----
+struct SceneArgs {
+    dr_vision_params p;
+    uint32_t batch;
+    uint32_t sample_offset;
+    uint32_t n;
+    PhiloxKeys keys;
+};
+
+__device__ __forceinline__ double ud(uint32_t x) { return (double)uni(x); }   // exact
+__device__ __forceinline__ double range_d(double lo, double hi, uint32_t x) {
+    return __dadd_rn(lo, __dmul_rn(__dsub_rn(hi, lo), ud(x)));
+}
+
+__global__ void scene_draw_kernel(const SceneArgs a, dr_scene_draw* __restrict__ out) {
+    const uint32_t k = blockIdx.x * blockDim.x + threadIdx.x;
+    if (k >= a.n) return;
+    const uint32_t g = a.sample_offset + k;
+    const dr_vision_params& p = a.p;
+    float o[64];
+#pragma unroll
+    for (int i = 0; i < 64; ++i) o[i] = 0.f;
+    constexpr double TWO_PI = 6.283185307179586476925;
+#pragma unroll
+    for (int c = 0; c < DR_VIS_N_CAMERAS; ++c) {
+        uint4 w = philox_k(g, a.batch, CH_SCENE_CAM, 2 * c, a.keys);
+        o[3 * c + 0] = (float)range_d(-p.cam_pos_range, p.cam_pos_range, w.x);   // [V1]
+        o[3 * c + 1] = (float)range_d(-p.cam_pos_range, p.cam_pos_range, w.y);
+        o[3 * c + 2] = (float)range_d(-p.cam_pos_range, p.cam_pos_range, w.z);
+        o[21 + c] = (float)range_d(-p.cam_fov_range, p.cam_fov_range, w.w);
+        w = philox_k(g, a.batch, CH_SCENE_CAM, 2 * c + 1, a.keys);
+        const double th = range_d(0.0, p.cam_rot_max, w.x);                       // [V2]
+        const double zc = __dsub_rn(__dmul_rn(2.0, ud(w.y)), 1.0);
+        const double phi = __dmul_rn(TWO_PI, ud(w.z));
+        const double rho = sqrt(__dsub_rn(1.0, __dmul_rn(zc, zc)));
+        double sh, ch, sp, cp;
+        sincos(0.5 * th, &sh, &ch);
+        sincos(phi, &sp, &cp);
+        o[9 + 4 * c + 0] = (float)ch;
+        o[9 + 4 * c + 1] = (float)(sh * rho * cp);
+        o[9 + 4 * c + 2] = (float)(sh * rho * sp);
+        o[9 + 4 * c + 3] = (float)(sh * zc);
+    }
+    const uint4 m0 = philox_k(g, a.batch, CH_SCENE_MAT, 0, a.keys);
+    const uint4 m1 = philox_k(g, a.batch, CH_SCENE_MAT, 1, a.keys);
+    const uint4 m2 = philox_k(g, a.batch, CH_SCENE_MAT, 2, a.keys);
+    o[24] = uni(m0.x);
+    o[25] = uni(m0.y);
+    o[26] = uni(m0.z);
+    o[27] = (float)range_d(p.robot_metallic_lo, p.robot_metallic_hi, m0.w);
+    o[28] = (float)range_d(p.robot_gloss_lo, p.robot_gloss_hi, m1.x);
+    {   // [V3] additive offsets; hue wraps, saturation / value clamp -- decided in exact-order fp64
+        const double h = __dadd_rn(p.obj_hue_cal, range_d(-p.obj_hue_range, p.obj_hue_range, m1.y));
+        const double s = __dadd_rn(p.obj_sat_cal, range_d(-p.obj_sat_range, p.obj_sat_range, m1.z));
+        const double v = __dadd_rn(p.obj_val_cal, range_d(-p.obj_val_range, p.obj_val_range, m1.w));
+        o[29] = (float)__dsub_rn(h, floor(h));
+        o[30] = (float)fmin(fmax(s, 0.0), 1.0);
+        o[31] = (float)fmin(fmax(v, 0.0), 1.0);
+    }
+    o[32] = (float)range_d(p.obj_metallic_lo, p.obj_metallic_hi, m2.x);
+    o[33] = (float)range_d(p.obj_gloss_lo, p.obj_gloss_hi, m2.y);
+    const int nl = p.lights_min + (int)(((unsigned long long)m2.z * (unsigned long long)(p.lights_max - p.lights_min + 1)) >> 32);
+    const double total = range_d(p.light_total_lo, p.light_total_hi, m2.w);   // [V5]
+    double rel[DR_VIS_MAX_LIGHTS];
+    double rsum = 0.0;
+    for (int i = 0; i < nl; ++i) {
+        const uint4 w = philox_k(g, a.batch, CH_SCENE_LIGHT, i, a.keys);
+        const double z = ud(w.x);
+        const double phi = __dmul_rn(TWO_PI, ud(w.y));
+        const double rho = sqrt(__dsub_rn(1.0, __dmul_rn(z, z)));
+        double sp, cp;
+        sincos(phi, &sp, &cp);
+        o[35 + 3 * i + 0] = (float)(rho * cp);
+        o[35 + 3 * i + 1] = (float)(rho * sp);
+        o[35 + 3 * i + 2] = (float)z;
+        rel[i] = range_d(p.light_rel_lo, p.light_rel_hi, w.z);
+        rsum += rel[i];
+    }
+    for (int i = 0; i < nl; ++i) o[53 + i] = (float)(total * rel[i] / rsum);
+    o[59] = (float)total;
+    float4* d4 = reinterpret_cast<float4*>(out + k);
+#pragma unroll
+    for (int i = 0; i < 16; ++i) {
+        float4 v = make_float4(o[4 * i], o[4 * i + 1], o[4 * i + 2], o[4 * i + 3]);
+        if (i == 8) v.z = __uint_as_float((uint32_t)nl);   // word 34: n_lights (u32)
+        d4[i] = v;
+    }
+}
+
+static PhiloxKeys make_keys(uint64_t seed) {
+    PhiloxKeys k;
+    const uint32_t k0 = (uint32_t)(seed & 0xFFFFFFFFull), k1 = (uint32_t)(seed >> 32);
+    for (int r = 0; r < 10; ++r) {
+        k.rk0[r] = k0 + (uint32_t)r * 0x9E3779B9u;
+        k.rk1[r] = k1 + (uint32_t)r * 0xBB67AE85u;
+    }
+    return k;
+}
+
+static int check_vision(const dr_vision_params* p) {
+    if (!p) return set_error(DR_EINVAL, "vision params: NULL");
+    if (p->abi_version != DR_ABI_VERSION || p->struct_size != sizeof(dr_vision_params))
+        return set_error(DR_EINVAL, "vision params: abi_version / struct_size mismatch");
+    struct { const char* n; double lo, hi; } rg[] = {
+        {"robot_metallic", p->robot_metallic_lo, p->robot_metallic_hi}, {"robot_gloss", p->robot_gloss_lo, p->robot_gloss_hi},
+        {"obj_metallic", p->obj_metallic_lo, p->obj_metallic_hi}, {"obj_gloss", p->obj_gloss_lo, p->obj_gloss_hi},
+        {"light_rel", p->light_rel_lo, p->light_rel_hi}, {"light_total", p->light_total_lo, p->light_total_hi},
+        {"contrast", p->contrast_lo, p->contrast_hi}, {"noise_std", p->noise_std_lo, p->noise_std_hi}};
+    for (auto& x : rg)
+        if (!(x.lo <= x.hi) || !std::isfinite(x.lo) || !std::isfinite(x.hi))
+            return set_error(DR_EINVAL, "%s_lo/%s_hi: need finite lo <= hi", x.n, x.n);
+    struct { const char* n; double v; } nn[] = {
+        {"cam_pos_range", p->cam_pos_range}, {"cam_rot_max", p->cam_rot_max}, {"cam_fov_range", p->cam_fov_range},
+        {"obj_hue_range", p->obj_hue_range}, {"obj_sat_range", p->obj_sat_range}, {"obj_val_range", p->obj_val_range},
+        {"contrast_lo", p->contrast_lo}, {"noise_std_lo", p->noise_std_lo}, {"light_rel_lo", p->light_rel_lo},
+        {"light_total_lo", p->light_total_lo}};
+    for (auto& x : nn)
+        if (!(x.v >= 0.0) || !std::isfinite(x.v)) return set_error(DR_EINVAL, "%s: must be a finite value >= 0", x.n);
+    if (!(p->light_rel_lo > 0.0)) return set_error(DR_EINVAL, "light_rel_lo: must be > 0");
+    if (!(p->std_floor > 0.0)) return set_error(DR_EINVAL, "std_floor: must be > 0");
+    if (p->lights_min < 1 || p->lights_max > DR_VIS_MAX_LIGHTS || p->lights_min > p->lights_max)
+        return set_error(DR_EINVAL, "lights_min/lights_max: need 1 <= min <= max <= 6");
+    return DR_OK;
+}
+
+}  // namespace dr
+
+using namespace dr;
+
+extern "C" {
+
+int dr_vision_params_default(dr_vision_params* p) {
+    if (!p) return set_error(DR_EINVAL, "params: NULL");
+    *p = dr_vision_params{};
+    p->abi_version = DR_ABI_VERSION;
+    p->struct_size = sizeof(dr_vision_params);
+    const double deg = 3.14159265358979323846 / 180.0;
+    p->cam_pos_range = 1.5e-3;   // Table vision-randomization
+    p->cam_rot_max = 3.0 * deg;
+    p->cam_fov_range = 1.0 * deg;
+    p->robot_metallic_lo = 0.05; p->robot_metallic_hi = 0.25;
+    p->robot_gloss_lo = 0.0; p->robot_gloss_hi = 1.0;
+    p->obj_hue_cal = 0.005; p->obj_sat_cal = 0.9; p->obj_val_cal = 0.5;   // workload choice
+    p->obj_hue_range = 0.01; p->obj_sat_range = 0.15; p->obj_val_range = 0.15;
+    p->obj_metallic_lo = 0.05; p->obj_metallic_hi = 0.15;
+    p->obj_gloss_lo = 0.05; p->obj_gloss_hi = 0.15;
+    p->lights_min = 4; p->lights_max = 6;
+    p->light_rel_lo = 1.0; p->light_rel_hi = 5.0;
+    p->light_total_lo = 0.0; p->light_total_hi = 15.0;
+    p->contrast_lo = 0.5; p->contrast_hi = 1.5;
+    p->noise_std_lo = 0.1; p->noise_std_hi = 0.1;   // [V6]
+    p->std_floor = 1e-8;
+    return DR_OK;
+}
+
+int dr_scene_draw_batch(const dr_vision_params* p, uint64_t seed, uint64_t batch_index, int64_t sample_offset,
+                        int64_t n_samples, dr_scene_draw* out_dev, void* stream) {
+    int rc = check_vision(p);
+    if (rc != DR_OK) return rc;
+    if (n_samples < 0 || sample_offset < 0 || sample_offset + n_samples > (int64_t(1) << 32))
+        return set_error(DR_EINVAL, "n_samples/sample_offset: outside [0, 2^32)");
+    if (n_samples == 0) return DR_OK;
+    if (!out_dev || ((uintptr_t)out_dev & 15u)) return set_error(DR_EINVAL, "out: NULL or not 16-byte aligned");
+    SceneArgs a{};
+    a.p = *p;
+    a.batch = (uint32_t)batch_index;
+    a.sample_offset = (uint32_t)sample_offset;
+    a.n = (uint32_t)n_samples;
+    a.keys = make_keys(seed);
+    const int threads = 128;
+    scene_draw_kernel<<<(unsigned)((n_samples + threads - 1) / threads), threads, 0, static_cast<cudaStream_t>(stream)>>>(
+        a, out_dev);
+    cudaError_t e = cudaGetLastError();
+    if (e != cudaSuccess) return set_error(DR_ECUDA, "scene_draw_kernel: %s", cudaGetErrorString(e));
+    count_launch();
+    return DR_OK;
+}
+
+int dr_image_augment(const dr_vision_params* p, uint64_t seed, uint64_t batch_index, int64_t image_offset,
+                     const uint8_t* images, int64_t n_images, int32_t height, int32_t width, int32_t channels,
+                     float* out, float* img_stats, void* stream) {
+    int rc = check_vision(p);
+    if (rc != DR_OK) return rc;
+    if (height < 1 || width < 1 || channels < 1) return set_error(DR_EINVAL, "height/width/channels: must be >= 1");
+    if (n_images < 0 || image_offset < 0 || image_offset + n_images > (int64_t(1) << 32))
+        return set_error(DR_EINVAL, "n_images/image_offset: outside [0, 2^32)");
+    const uint64_t E = (uint64_t)height * (uint64_t)width * (uint64_t)channels;
+    if (E > (uint64_t)DR_VIS_MAX_IMAGE_BYTES)
+        return set_error(DR_EUNSUPPORTED, "image of %llu bytes exceeds DR_VIS_MAX_IMAGE_BYTES", (unsigned long long)E);
+    if (n_images == 0) return DR_OK;
+    if (!images || !out) return set_error(DR_EINVAL, "images/out: NULL");
+    if (img_stats && ((uintptr_t)img_stats & 15u)) return set_error(DR_EINVAL, "img_stats: not 16-byte aligned");
+    if (n_images * (int64_t)2 > (int64_t)0x7FFFFFFF / 8) return set_error(DR_EINVAL, "n_images: too many for one launch");
+    // cluster size: the smallest K in {1, 2, 4, 8} whose slice fits the 32 KB target, else the
+    // smallest whose slice fits 200 KB
+    auto slice_of = [&](uint32_t K) { return (uint32_t)(((E + K - 1) / K + 15) / 16 * 16); };
+    uint32_t K = 1;
+    while (K < 8 && slice_of(K) > IMG_SLICE_TARGET) K *= 2;
+    const uint32_t slice = slice_of(K);
+    if (slice > IMG_SLICE_MAX) return set_error(DR_EUNSUPPORTED, "image slice of %u bytes too large", slice);
+    ImgArgs a{};
+    a.images = images;
+    a.out = out;
+    a.img_stats = img_stats;
+    a.E = E;
+    a.slice = slice;
+    a.aligned = (E % 16 == 0 && ((uintptr_t)images & 15u) == 0 && ((uintptr_t)out & 15u) == 0) ? 1u : 0u;
+    a.batch = (uint32_t)batch_index;
+    a.image_offset = (uint32_t)image_offset;
+    a.contrast_lo = p->contrast_lo;
+    a.contrast_range = p->contrast_hi - p->contrast_lo;
+    a.noise_lo = p->noise_std_lo;
+    a.noise_range = p->noise_std_hi - p->noise_std_lo;
+    a.std_floor = p->std_floor;
+    a.keys = make_keys(seed);
+    cudaError_t e = cudaFuncSetAttribute(image_augment_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)IMG_SLICE_MAX);
+    if (e != cudaSuccess) return set_error(DR_ECUDA, "cudaFuncSetAttribute: %s", cudaGetErrorString(e));
+    cudaLaunchConfig_t cfg{};
+    cfg.gridDim = dim3((unsigned)(n_images * K), 1, 1);
+    cfg.blockDim = dim3(IMG_THREADS, 1, 1);
+    cfg.dynamicSmemBytes = slice;
+    cfg.stream = static_cast<cudaStream_t>(stream);
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeClusterDimension;
+    attr[0].val.clusterDim.x = K;
+    attr[0].val.clusterDim.y = 1;
+    attr[0].val.clusterDim.z = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    e = cudaLaunchKernelEx(&cfg, image_augment_kernel, a);
+    if (e != cudaSuccess) return set_error(DR_ECUDA, "image_augment_kernel: %s", cudaGetErrorString(e));
+    count_launch();
+    return DR_OK;
+}
+
+}  // extern "C"
+
+static_assert(sizeof(dr_scene_draw) == 256, "dr_scene_draw must be 64 words");

@@ -82,3 +82,25 @@ def occlusion_rate(obs: np.ndarray, r: float = 0.015) -> float:
                 occ[..., i] |= np.sum((tips[..., i, :] - tips[..., j, :]) ** 2, axis=-1) < r * r
         occ[..., i] |= np.sum((tips[..., i, :] - obj) ** 2, axis=-1) < r * r
     return float(occ.mean())
+
+
+def images(n: int, h: int, w: int, c: int, seed: int = SEED_WORKLOAD) -> np.ndarray:
+    """Synthetic rendered-like u8 images [n][h][w][c] (the paper's camera frames are 200 x 200 x
+    8-bit RGB): a per-image linear gradient background, a few flat-coloured
+    rectangles (a block / hand stand-in), plus mild sensor-like noise, clipped to [0, 255].
+    Per-image brightness and contrast vary, so the normalisation sees a spread of means / stds."""
+    rng = np.random.default_rng(seed)
+    yy = np.linspace(0.0, 1.0, h)[:, None, None]
+    xx = np.linspace(0.0, 1.0, w)[None, :, None]
+    out = np.empty((n, h, w, c), dtype=np.uint8)
+    for i in range(n):
+        base = rng.uniform(20, 200, size=(1, 1, c))
+        gy, gx = rng.uniform(-60, 60, size=(2, 1, 1, c))
+        img = base + gy * yy + gx * xx
+        for _ in range(rng.integers(1, 4)):
+            y0, x0 = rng.integers(0, h), rng.integers(0, w)
+            y1, x1 = min(h, y0 + rng.integers(1, max(2, h // 2))), min(w, x0 + rng.integers(1, max(2, w // 2)))
+            img[y0:y1, x0:x1, :] = rng.uniform(0, 255, size=c)
+        img = img + rng.normal(0.0, 3.0, size=(h, w, c))
+        out[i] = np.clip(np.rint(img), 0, 255).astype(np.uint8)
+    return out
