@@ -43,7 +43,7 @@ def parse():
     ap.add_argument("--steps", type=int, default=2000)
     ap.add_argument("--warmup", type=int, default=20)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--config", default="full1m", choices=["full1m", "cfg2", "cfg3", "reset"])
+    ap.add_argument("--config", default="full1m", choices=["full1m", "cfg2", "cfg3", "reset", "vision"])
     ap.add_argument("--n-env", type=int, default=0, help="override the env count (per GPU if weak, global if strong)")
     ap.add_argument("--scaling", default="weak", choices=["weak", "strong"],
                     help="weak: every rank owns the config's env count (global = N x that); "
@@ -153,6 +153,23 @@ def run_reference(args):
     import numpy as np
     from oracle.oracle import Oracle
     from workload import gen, presets
+    if args.config == "vision":
+        from oracle import oracle as O
+        k = max(1, min(args.steps, 8))
+        imgs = gen.images(k, presets.VISION_H, presets.VISION_W, presets.VISION_C)
+        t0 = time.perf_counter()
+        O.image_augment(presets.vision_preset(), presets.SEED_DR, 0, imgs)
+        dt = time.perf_counter() - t0
+        v = k / dt
+        print(json.dumps({"impl": "reference", "metric": "augmented images/sec", "value": v, "unit": "images/s",
+                          "n_gpus": args.gpus, "steps": k, "warmup": 0, "ms_per_step": dt / k * 1e3,
+                          "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+                          "data": "synthetic", "config": {"workload": "vision-200x200x3 images (oracle sample)"},
+                          "cpu_baseline": {"value": v, "unit": "images/s", "cores": 1, "kind": "oracle",
+                                           "sample": f"{k} images of 200x200x3 (fp64 oracle, single thread)"},
+                          "e2e": {"value": v, "unit": "images/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}),
+              flush=True)
+        return
     cfg = config_of(args.config, args.n_env)
     cfg["scaling"] = args.scaling
     n = min(cfg["n"], args.cpu_sample_envs)
@@ -199,8 +216,127 @@ def cpu_baseline(cfg, args):
             "sample": f"{n} envs x {steps} steps of {cfg['workload']} (fp64 oracle, single thread)"}
 
 
+def run_vision(args):
+    """--config vision: one step = the appearance draws of the paper's
+    batch of 64 samples + the post-render augmentation of its 192 camera images (200 x 200 x 3
+    u8), per rank.  A ring of 4 distinct input/output batches (92 MB in, 368 MB out)
+    keeps the working set above L2.  Metric: augmented images/s."""
+    import torch
+    import torch.distributed as dist
+    from paper_1906_11633_b200 import vision
+    from workload import gen, presets
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    S, NI, H, W, Cc = presets.VISION_BATCH_SAMPLES, presets.VISION_BATCH_SAMPLES * presets.VISION_CAMERAS, \
+        presets.VISION_H, presets.VISION_W, presets.VISION_C
+    E = H * W * Cc
+    R = 4
+    P = vision.params_from_preset(presets.vision_preset())
+    stream = torch.cuda.Stream()
+    with torch.cuda.stream(stream):
+        host = [gen.images(NI, H, W, Cc, seed=presets.SEED_WORKLOAD + 101 * rank + k) for k in range(R)]
+        X = [torch.from_numpy(h).cuda() for h in host]
+        Y = [torch.empty(NI, H, W, Cc, dtype=torch.float32, device="cuda") for _ in range(R)]
+        ST = torch.empty(NI, 4, dtype=torch.float32, device="cuda")
+        SC = torch.empty(S, 64, dtype=torch.float32, device="cuda")
+        torch.cuda.synchronize()
+
+        def one_step(t):
+            b = t   # batch index: fresh draws every step; images of rank r have global ids r * NI + i
+            vision.dr_scene_draw_batch(P, presets.SEED_DR, b, SC, sample_offset=rank * S, stream=stream)
+            vision.dr_image_augment(P, presets.SEED_DR, b, X[t % R], Y[t % R], ST, image_offset=rank * NI,
+                                    stream=stream)
+
+        for t in range(args.warmup):
+            one_step(t)
+        torch.cuda.synchronize()
+        sampler = ClockSampler(local)
+        sampler.start()
+        for t in range(args.warmup, args.warmup + min(args.warmup, 50)):
+            one_step(t)
+        t_base = args.warmup + min(args.warmup, 50)
+        if world > 1:
+            dist.barrier()
+        torch.cuda.synchronize()
+        l0 = vision.dr_total_kernel_launches()
+        evs = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps + 1)]
+        evs[0].record(stream)
+        for i in range(args.steps):
+            one_step(t_base + i)
+            evs[i + 1].record(stream)
+        torch.cuda.synchronize()
+        if world > 1:
+            dist.barrier()
+        launches = vision.dr_total_kernel_launches() - l0
+        clocks = sampler.stop()
+        elapsed_ms = evs[0].elapsed_time(evs[-1])
+        per = sorted(evs[i].elapsed_time(evs[i + 1]) for i in range(args.steps))
+        t_ms = torch.tensor([elapsed_ms], dtype=torch.float64, device="cuda")
+        if world > 1:
+            dist.all_reduce(t_ms, op=dist.ReduceOp.MAX)
+        elapsed_ms = float(t_ms.item())
+        # e2e: pinned host u8 batch -> device -> augment -> fp32 result back to pinned host memory
+        e2e = None
+        if not args.profile and args.e2e_steps > 0:
+            hx = torch.from_numpy(host[0]).pin_memory()
+            hy = torch.empty(NI, H, W, Cc, dtype=torch.float32).pin_memory()
+            torch.cuda.synchronize()
+            t0 = time.perf_counter()
+            for i in range(args.e2e_steps):
+                X[0].copy_(hx, non_blocking=True)
+                vision.dr_scene_draw_batch(P, presets.SEED_DR, i, SC, sample_offset=rank * S, stream=stream)
+                vision.dr_image_augment(P, presets.SEED_DR, i, X[0], Y[0], ST, image_offset=rank * NI, stream=stream)
+                hy.copy_(Y[0], non_blocking=True)
+            torch.cuda.synchronize()
+            e2e_s = time.perf_counter() - t0
+            te = torch.tensor([e2e_s], dtype=torch.float64, device="cuda")
+            if world > 1:
+                dist.all_reduce(te, op=dist.ReduceOp.MAX)
+            e2e = {"value": world * NI * args.e2e_steps / float(te.item()), "unit": "images/s",
+                   "h2d_bytes_per_step": world * NI * E, "d2h_bytes_per_step": world * NI * E * 4,
+                   "api": "dr_image_augment (pinned host u8 in, fp32 out)", "steps": args.e2e_steps}
+    value = world * NI * args.steps / (elapsed_ms / 1e3)
+    kern_ms = sum(per) / len(per)
+    peak, peak_kind = measured_peak()
+    bytes_step = NI * E * 5 + S * 256
+    achieved = bytes_step / (kern_ms / 1e3) / 1e9
+    if rank == 0:
+        cpu = None
+        if world == 1 and not args.no_cpu_baseline and not args.profile:
+            from oracle import oracle as O
+            k = 8
+            t0 = time.perf_counter()
+            O.image_augment(presets.vision_preset(), presets.SEED_DR, 0, host[0][:k])
+            O.scene_draw(presets.vision_preset(), presets.SEED_DR, 0, S)
+            dt = time.perf_counter() - t0
+            cpu = {"value": k / dt, "unit": "images/s", "cores": 1, "kind": "oracle",
+                   "sample": f"{k} images of 200x200x3 + {S} scene draws (fp64 oracle, single thread)"}
+        line = {"metric": "augmented images/sec", "value": value, "unit": "images/s", "n_gpus": world,
+                "steps": args.steps, "warmup": args.warmup, "ms_per_step": elapsed_ms / args.steps,
+                "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "u8->f32",
+                "data": "synthetic",
+                "config": {"workload": "vision-192x200x200x3-per-rank (64 samples x 3 cameras, PAPER.md:290)",
+                           "images_per_step_per_gpu": NI, "scene_draws_per_step_per_gpu": S,
+                           "l2": "4-batch ring, 460 MB working set > L2"},
+                "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
+                             "frac": achieved / peak, "traffic": None, "peak_kind": peak_kind,
+                             "bytes_per_step": bytes_step, "kernel": "dr::image_augment_kernel (+ scene_draw_kernel)",
+                             "kernel_ms_avg": kern_ms, "kernel_ms_median": per[len(per) // 2]},
+                "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": int(launches), "clocks": clocks}
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+
+
 def main():
     args = parse()
+    if args.config == "vision" and args.impl != "reference":
+        return run_vision(args)
     if args.impl == "reference":
         return run_reference(args)
 
