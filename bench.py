@@ -246,11 +246,22 @@ def run_vision(args):
         SC = torch.empty(S, 64, dtype=torch.float32, device="cuda")
         torch.cuda.synchronize()
 
+        side = torch.cuda.Stream()
+
         def one_step(t):
-            b = t   # batch index: fresh draws every step; images of rank r have global ids r * NI + i
-            vision.dr_scene_draw_batch(P, presets.SEED_DR, b, SC, sample_offset=rank * S, stream=stream)
+            # batch index b = t: fresh draws every step; images of rank r have global ids r * NI + i.
+            # The 64 scene draws (latency-bound, independent of the images) run on a side stream
+            # forked from and joined back into the step's stream, overlapping the augmentation.
+            b = t
+            fork = torch.cuda.Event()
+            fork.record(stream)
+            side.wait_event(fork)
+            vision.dr_scene_draw_batch(P, presets.SEED_DR, b, SC, sample_offset=rank * S, stream=side)
             vision.dr_image_augment(P, presets.SEED_DR, b, X[t % R], Y[t % R], ST, image_offset=rank * NI,
                                     stream=stream)
+            join = torch.cuda.Event()
+            join.record(side)
+            stream.wait_event(join)
 
         for t in range(args.warmup):
             one_step(t)
