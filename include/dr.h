@@ -30,7 +30,7 @@
 extern "C" {
 #endif
 
-#define DR_ABI_VERSION 1u
+#define DR_ABI_VERSION 2u
 
 #define DR_N_ACT       20  /* actuators of the Shadow hand */
 #define DR_N_TIPS      5   /* fingertip markers */
@@ -63,7 +63,12 @@ enum {
     DR_OCCLUSION = 1u << 6, /* marker occlusion -> hold last reading */
     DR_FORCE     = 1u << 7, /* random forces on the object */
     DR_PHYS      = 1u << 8, /* per-episode physical parameters */
-    DR_ALL       = 0x1FFu
+    DR_ALL       = 0x1FFu,  /* the paper's randomization set */
+    /* variants, off unless requested: */
+    DR_SMOOTH    = 1u << 9, /* EMA smoothing of the policy action, 0.3 per 80 ms, before delay/noise */
+    DR_SUBSTEP_BACKLASH = 1u << 10, /* backlash slack updated once per substep with dt_k;
+                                       requires dr_step_substeps */
+    DR_ALL_EXT   = 0x7FFu
 };
 
 /* physical-parameter descriptor (SPEC.md:126 schema; the paper's table is missing) */
@@ -111,6 +116,8 @@ typedef struct dr_params {
     double force_p_lo, force_p_hi;  /* 0.001, 0.1 (loguniform), 0 < lo <= hi <= 1 */
     double force_accel_std;         /* 1.0 m/s^2 (times the object mass) */
     double force_decay_per_step;    /* 0.99 per 80 ms step, in (0, 1] */
+    /* action smoothing (DR_SMOOTH) */
+    double act_smooth_coef;         /* 0.3: a_s <- (1 - c) a_s + c a per step, in [0, 1] */
     /* physical parameters */
     int32_t n_phys, mass_index;     /* 1 <= n_phys <= 256; phys[mass_index] is the object mass */
     dr_phys_desc phys[DR_MAX_PHYS];
@@ -120,7 +127,7 @@ typedef struct dr_params {
     void*  stream;                  /* cudaStream_t; NULL = legacy default stream */
 } dr_params;
 
-/* Exported per-env state (dr_state_export / dr_state_import), 592 bytes. */
+/* Exported per-env state (dr_state_export / dr_state_import), 672 bytes. */
 typedef struct {
     uint32_t episode;        /* k_e: number of resets since dr_init */
     uint32_t delay_bits;     /* bit j: actuator j delayed this episode */
@@ -132,6 +139,7 @@ typedef struct {
     float dneg[DR_N_ACT], dpos[DR_N_ACT], c_act[DR_N_ACT];
     float off_tip[DR_N_TIPS * 3], c_obj[3], q_c[4];
     float prev[DR_N_ACT], slack[DR_N_ACT], last[DR_N_TIPS * 3], f_trig[3];
+    float ema[DR_N_ACT];     /* smoothed action (DR_SMOOTH) */
 } dr_env_state;
 
 /* Stats slot indices (dr_stats).  Integer counts are exact (held in fp64 < 2^53). */
@@ -183,6 +191,16 @@ int dr_reset(const uint8_t* env_mask);
  * of dr_step calls advances it on every replay).  Asynchronous. */
 int dr_step(const float* actions, const float* raw_obs, float* out_actions, float* out_obs,
             float* out_dt, float* out_force);
+
+/* dr_step for contexts with DR_SUBSTEP_BACKLASH (DR_EINVAL otherwise; dr_step returns DR_EINVAL
+ * for such contexts): the backlash slack model runs once per MuJoCo substep k with that
+ * substep's dt_k ("each of the substeps", 104 "dt"), the noised action held over
+ * the step, so the simulator receives one gated action per substep:
+ *   out_actions_sub [n][10][20] out  alpha_k * a_n for substep k
+ *   out_actions     [n][20]     out  the last substep's action (= out_actions_sub[:, 9])
+ * Other arguments as dr_step.  Asynchronous. */
+int dr_step_substeps(const float* actions, const float* raw_obs, float* out_actions, float* out_actions_sub,
+                     float* out_obs, float* out_dt, float* out_force);
 
 /* End-to-end variant on HOST buffers (same layouts): copies inputs host->device, runs dr_step,
  * copies outputs device->host, all on the library stream through library-owned device buffers.

@@ -434,7 +434,7 @@ static void reset_env(orc_ctx* c, orc_env* e)
 
     /* 10. state: slack 0, previous action 0, no last reading, timers 0, force 0
      *     (delay at episode start returns 0, SPEC.md:183 [Q9]; initial slack [Q6]). */
-    for (j = 0; j < ORC_N_ACT; ++j) { e->prev[j] = 0.0; e->slack[j] = 0.0; }
+    for (j = 0; j < ORC_N_ACT; ++j) { e->prev[j] = 0.0; e->slack[j] = 0.0; e->ema[j] = 0.0; }
     for (i = 0; i < ORC_N_TIPS * 3; ++i) e->last[i] = 0.0;
     e->has_last = 0;
     for (i = 0; i < ORC_N_TIPS; ++i) e->timer[i] = 0;
@@ -458,7 +458,7 @@ int orc_reset(orc_ctx* c, const uint8_t* mask)
  * [Q1]: timing -> delay -> action noise (+clamp) -> backlash; occlusion -> dropout ->
  * fingertip noise + hold -> object position -> orientation -> force. */
 static void step_env(orc_ctx* c, orc_env* e, const float* act, const float* obs,
-                     double* o_act, double* o_obs, double* o_dt, double* o_force,
+                     double* o_act, double* o_sub, double* o_obs, double* o_dt, double* o_force,
                      double* st, double* margin)
 {
     const orc_params* p = &c->p;
@@ -488,6 +488,12 @@ static void step_env(orc_ctx* c, orc_env* e, const float* act, const float* obs,
     for (j = 0; j < ORC_N_ACT; ++j) {
         double a = (double)act[j];
         double ad, an, out;
+        /* 1b. EMA smoothing of the policy action before it is applied (PAPER.md:742-744,
+         *     coefficient 0.3 per 80 ms) [Q25]: a <- (1 - c) a_s + c a, state 0 at reset. */
+        if (L & ORC_SMOOTH) {
+            a = (1.0 - p->act_smooth_coef) * e->ema[j] + p->act_smooth_coef * a;
+            e->ema[j] = a;
+        }
         /* 2. one-step delay of flagged actuators [Q9]; the buffer holds
          *    the policy action. */
         if (L & ORC_DELAY) {
@@ -515,6 +521,29 @@ static void step_env(orc_ctx* c, orc_env* e, const float* act, const float* obs,
         }
         st[ORC_S_SUM_DA] += an - ad;
         st[ORC_S_SUM_DA2] += (an - ad) * (an - ad);
+        /* 4'. per-substep backlash [Q2 alternative, Q26]: the slack model runs once per
+         *     substep k with dt_k, the action a_n held over the step; out_sub[k] = alpha_k a_n,
+         *     the step's out_actions = the last substep's. */
+        if ((L & ORC_BACKLASH) && (L & ORC_SUBSTEP_BL)) {
+            double s = e->slack[j], sn, al, ok = an, mg = INFINITY;
+            double sg = (an > 0.0) ? 1.0 : ((an < 0.0) ? -1.0 : 0.0);
+            int k;
+            for (k = 0; k < ORC_N_SUB; ++k) {
+                orc_backlash(s, an, e->dneg[j], e->dpos[j], dt[k], p->backlash_eps, &sn, &al, &ok);
+                if (sg != 0.0) {
+                    double d = (sg > 0.0) ? e->dpos[j] : e->dneg[j];
+                    double m = fabs((s + an * d * dt[k]) - sg);
+                    if (m < mg) mg = m;
+                }
+                if (sg != 0.0 && fabs(sn) == 1.0 && sn != s) st[ORC_S_RAIL_HITS] += 1.0;
+                if (al == 1.0) st[ORC_S_ALPHA_ONE] += 1.0; else st[ORC_S_ALPHA_LT1] += 1.0;
+                if (o_sub) o_sub[k * ORC_N_ACT + j] = ok;
+                s = sn;
+            }
+            if (margin) margin[j] = mg;
+            e->slack[j] = s;
+            out = ok;
+        } else
         /* 4. backlash with dt = dt_env [Q2]. */
         if (L & ORC_BACKLASH) {
             double s = e->slack[j], sn, al;
@@ -534,6 +563,10 @@ static void step_env(orc_ctx* c, orc_env* e, const float* act, const float* obs,
         } else {
             out = an;
             if (margin) margin[j] = INFINITY;
+            if (o_sub) {
+                int k;
+                for (k = 0; k < ORC_N_SUB; ++k) o_sub[k * ORC_N_ACT + j] = an;
+            }
         }
         st[ORC_S_SUM_ABS_BL] += fabs(out - an);
         if (o_act) o_act[j] = out;
@@ -662,6 +695,13 @@ int orc_step(orc_ctx* c, const float* actions, const float* raw_obs,
              double* out_actions, double* out_obs, double* out_dt, double* out_force,
              double* stats, double* bl_margin)
 {
+    return orc_step_sub(c, actions, raw_obs, out_actions, NULL, out_obs, out_dt, out_force, stats, bl_margin);
+}
+
+int orc_step_sub(orc_ctx* c, const float* actions, const float* raw_obs,
+                 double* out_actions, double* out_actions_sub, double* out_obs, double* out_dt,
+                 double* out_force, double* stats, double* bl_margin)
+{
     double st[ORC_N_STATS];
     int64_t i;
     if (!c || !actions || !raw_obs) return -1;
@@ -669,6 +709,7 @@ int orc_step(orc_ctx* c, const float* actions, const float* raw_obs,
     for (i = 0; i < c->n; ++i) {
         step_env(c, &c->env[i], actions + i * ORC_N_ACT, raw_obs + i * ORC_OBS_IN,
                  out_actions ? out_actions + i * ORC_N_ACT : NULL,
+                 out_actions_sub ? out_actions_sub + i * ORC_N_SUB * ORC_N_ACT : NULL,
                  out_obs ? out_obs + i * ORC_OBS_OUT : NULL,
                  out_dt ? out_dt + i * ORC_N_SUB : NULL,
                  out_force ? out_force + i * 3 : NULL,

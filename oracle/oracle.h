@@ -45,6 +45,9 @@ extern "C" {
 #define ORC_OCCLUSION  (1u << 6)
 #define ORC_FORCE      (1u << 7)
 #define ORC_PHYS       (1u << 8)
+/* SURVEY.md §8(f) rank 2 variants (off in the paper's FULL set) */
+#define ORC_SMOOTH     (1u << 9)   /* EMA action smoothing, 0.3 per 80 ms */
+#define ORC_SUBSTEP_BL (1u << 10)  /* backlash updated once per substep with dt_k */
 
 /* physical-parameter descriptor kinds (SPEC.md:126 schema; table itself missing) */
 #define ORC_PHYS_FIXED            0
@@ -80,6 +83,8 @@ typedef struct {
     /* physical parameters */
     int32_t n_phys, mass_index;
     orc_phys_desc phys[ORC_MAX_PHYS];
+    /* action smoothing coefficient per 80 ms step (PAPER.md:743 footnote: 0.3) */
+    double act_smooth_coef;
 } orc_params;
 
 /* One environment's episode record + mutable state, fp64. */
@@ -109,6 +114,7 @@ typedef struct {
     double   f_trig[3];
     uint32_t k_f;
     uint32_t _pad1;
+    double   ema[ORC_N_ACT];   /* smoothed action (ORC_SMOOTH) */
 } orc_env;
 
 typedef struct orc_ctx orc_ctx;
@@ -124,6 +130,10 @@ int  orc_reset(orc_ctx* c, const uint8_t* mask);          /* NULL = all envs */
 int  orc_step(orc_ctx* c, const float* actions, const float* raw_obs,
               double* out_actions, double* out_obs, double* out_dt, double* out_force,
               double* stats, double* bl_margin);
+/* Same step with the per-substep actions [n][10][20] of ORC_SUBSTEP_BL (may be NULL). */
+int  orc_step_sub(orc_ctx* c, const float* actions, const float* raw_obs,
+                  double* out_actions, double* out_actions_sub, double* out_obs, double* out_dt,
+                  double* out_force, double* stats, double* bl_margin);
 uint64_t orc_step_index(const orc_ctx* c);
 void     orc_set_step_index(orc_ctx* c, uint64_t t);
 int      orc_get_env(const orc_ctx* c, int64_t i, orc_env* dst);

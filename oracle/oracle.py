@@ -52,6 +52,7 @@ class OrcParams(C.Structure):
         ("force_decay_per_step", C.c_double),
         ("n_phys", C.c_int32), ("mass_index", C.c_int32),
         ("phys", PhysDesc * MAX_PHYS),
+        ("act_smooth_coef", C.c_double),
     ]
 
 
@@ -66,6 +67,7 @@ class OrcEnv(C.Structure):
         ("prev", C.c_double * N_ACT), ("slack", C.c_double * N_ACT), ("last", C.c_double * 15),
         ("has_last", C.c_int32), ("timer", C.c_int32 * N_TIPS),
         ("f_trig", C.c_double * 3), ("k_f", C.c_uint32), ("_pad1", C.c_uint32),
+        ("ema", C.c_double * N_ACT),
     ]
 
 
@@ -105,6 +107,8 @@ def lib():
         L.orc_reset.restype = C.c_int
         L.orc_step.argtypes = [C.c_void_p, fp, fp, dp, dp, dp, dp, dp, dp]
         L.orc_step.restype = C.c_int
+        L.orc_step_sub.argtypes = [C.c_void_p, fp, fp, dp, dp, dp, dp, dp, dp, dp]
+        L.orc_step_sub.restype = C.c_int
         L.orc_step_index.argtypes = [C.c_void_p]
         L.orc_step_index.restype = C.c_uint64
         L.orc_set_step_index.argtypes = [C.c_void_p, C.c_uint64]
@@ -277,7 +281,7 @@ class Oracle:
         rc = lib().orc_reset(self._h, _ptr(m, C.c_uint8))
         assert rc == 0
 
-    def step(self, actions, raw_obs, want_margin=False):
+    def step(self, actions, raw_obs, want_margin=False, want_sub=False):
         a = np.ascontiguousarray(actions, dtype=np.float32)
         o = np.ascontiguousarray(raw_obs, dtype=np.float32)
         assert a.shape == (self.n, N_ACT) and o.shape == (self.n, OBS_IN)
@@ -289,11 +293,14 @@ class Oracle:
             "stats": np.empty(N_STATS),
         }
         margin = np.empty((self.n, N_ACT)) if want_margin else None
+        sub = np.empty((self.n, N_SUB, N_ACT)) if want_sub else None
         dp = C.c_double
-        rc = lib().orc_step(self._h, _ptr(a, C.c_float), _ptr(o, C.c_float),
-                            _ptr(out["out_actions"], dp), _ptr(out["out_obs"], dp),
-                            _ptr(out["out_dt"], dp), _ptr(out["out_force"], dp),
-                            _ptr(out["stats"], dp), _ptr(margin, dp))
+        rc = lib().orc_step_sub(self._h, _ptr(a, C.c_float), _ptr(o, C.c_float),
+                                _ptr(out["out_actions"], dp), _ptr(sub, dp), _ptr(out["out_obs"], dp),
+                                _ptr(out["out_dt"], dp), _ptr(out["out_force"], dp),
+                                _ptr(out["stats"], dp), _ptr(margin, dp))
+        if want_sub:
+            out["out_actions_sub"] = sub
         assert rc == 0
         if want_margin:
             out["margin"] = margin

@@ -39,10 +39,15 @@ class DRContext:
         self.out_obs = torch.empty(self.n, dr.OBS_OUT, device=dev)
         self.out_dt = torch.empty(self.n, dr.N_SUB, device=dev)
         self.out_force = torch.empty(self.n, 3, device=dev)
+        self.substeps = bool(preset["layer_mask"] & dr.SUBSTEP_BACKLASH)
+        self.out_actions_sub = torch.empty(self.n, dr.N_SUB, dr.N_ACT, device=dev) if self.substeps else None
 
     def step(self, actions, raw_obs, outs=None):
         o = outs or (self.out_actions, self.out_obs, self.out_dt, self.out_force)
-        dr.dr_step(actions, raw_obs, *o)
+        if self.substeps:   # DR_SUBSTEP_BACKLASH: one gated action per substep as well
+            dr.dr_step_substeps(actions, raw_obs, o[0], self.out_actions_sub, *o[1:])
+        else:
+            dr.dr_step(actions, raw_obs, *o)
         return o
 
     def update_params(self, preset: dict, env_offset: int = None, n_env_global: int = None):

@@ -106,7 +106,10 @@ int validate(const dr_params* p, int64_t n_env) {
     if (!p) return fail(DR_EINVAL, "params: NULL");
     if (p->abi_version != DR_ABI_VERSION) return fail(DR_EINVAL, "abi_version: %u != %u", p->abi_version, DR_ABI_VERSION);
     if (p->struct_size != sizeof(dr_params)) return fail(DR_EINVAL, "struct_size: %u != %zu", p->struct_size, sizeof(dr_params));
-    if (p->layer_mask & ~DR_ALL) return fail(DR_EINVAL, "layer_mask: unknown bits 0x%x", p->layer_mask);
+    if (p->layer_mask & ~DR_ALL_EXT) return fail(DR_EINVAL, "layer_mask: unknown bits 0x%x", p->layer_mask);
+    if ((p->layer_mask & DR_SUBSTEP_BACKLASH) && !(p->layer_mask & DR_BACKLASH))
+        return fail(DR_EINVAL, "layer_mask: DR_SUBSTEP_BACKLASH needs DR_BACKLASH");
+    if (!(p->act_smooth_coef >= 0.0 && p->act_smooth_coef <= 1.0)) return fail(DR_EINVAL, "act_smooth_coef: outside [0, 1]");
     if (p->n_act != DR_N_ACT || p->n_tips != DR_N_TIPS || p->n_substeps != DR_N_SUBSTEPS)
         return fail(DR_EUNSUPPORTED, "n_act/n_tips/n_substeps: kernels specialise (20, 5, 10)");
     if (n_env < 1 || n_env > (int64_t(1) << 31)) return fail(DR_EINVAL, "n_env: %lld outside [1, 2^31]", (long long)n_env);
@@ -207,6 +210,8 @@ cudaError_t upload_params(Ctx* c, const dr_params& p, const char** what) {
     dc.occl_r2_hi = (float)(dc.occl_r2 * (1.0 + 1e-5));
     dc.occl_exact_only = (dc.occl_r2 < 1e-30 || dc.occl_r2 > 1e30) ? 1u : 0u;
     dc.accel_std = (float)p.force_accel_std;
+    dc.smooth_c = (float)p.act_smooth_coef;
+    dc.smooth_keep = (float)(1.0 - p.act_smooth_coef);
     dc.n_phys = p.n_phys;
     dc.mass_index = p.mass_index;
 
@@ -404,6 +409,7 @@ int dr_params_default(dr_params* p) {
     p->force_p_hi = 0.1;
     p->force_accel_std = 1.0;
     p->force_decay_per_step = 0.99;
+    p->act_smooth_coef = 0.3;              // PAPER.md:743 footnote (DR_SMOOTH, off by default)
     // physical parameters: the paper's table is missing; synthetic 256 slots, Q20
     p->n_phys = DR_MAX_PHYS;
     p->mass_index = 0;
@@ -547,24 +553,39 @@ int dr_reset(const uint8_t* env_mask) {
     return DR_OK;
 }
 
-int dr_step(const float* actions, const float* raw_obs, float* out_actions, float* out_obs, float* out_dt,
-            float* out_force) {
+static int step_common(const float* actions, const float* raw_obs, float* out_actions, float* out_sub, float* out_obs,
+                       float* out_dt, float* out_force) {
     Ctx* c = g_ctx;
     if (!c) return fail(DR_ENOTINIT, "dr_step: no context");
     if (g_sticky) return fail(DR_ECUDA, "sticky CUDA error: %s", g_err);
-    const void* ptrs[6] = {actions, raw_obs, out_actions, out_obs, out_dt, out_force};
-    const char* names[6] = {"actions", "raw_obs", "out_actions", "out_obs", "out_dt", "out_force"};
-    for (int i = 0; i < 6; ++i) {
+    const bool sub = (c->prm.layer_mask & DR_SUBSTEP_BACKLASH) != 0;
+    if (sub != (out_sub != nullptr))
+        return fail(DR_EINVAL, sub ? "DR_SUBSTEP_BACKLASH context: use dr_step_substeps"
+                                   : "dr_step_substeps: context has no DR_SUBSTEP_BACKLASH layer");
+    const void* ptrs[7] = {actions, raw_obs, out_actions, out_obs, out_dt, out_force, sub ? out_sub : actions};
+    const char* names[7] = {"actions", "raw_obs", "out_actions", "out_obs", "out_dt", "out_force", "out_actions_sub"};
+    for (int i = 0; i < 7; ++i) {
         if (!ptrs[i]) return fail(DR_EINVAL, "%s: NULL", names[i]);
         if (!aligned16(ptrs[i])) return fail(DR_EINVAL, "%s: not 16-byte aligned", names[i]);
     }
     cudaError_t e = launch_step(c->p, c->prm.layer_mask, actions, raw_obs, out_actions, out_obs, out_dt, out_force,
-                                (uint32_t)c->n_env, c->step_grid, c->stream);
+                                out_sub, (uint32_t)c->n_env, c->step_grid, c->stream);
     if (e != cudaSuccess) return cuda_fail(e, "step_kernel");
     c->t_host++;
     c->launches++;
     ++g_total_launches;
     return DR_OK;
+}
+
+int dr_step(const float* actions, const float* raw_obs, float* out_actions, float* out_obs, float* out_dt,
+            float* out_force) {
+    return step_common(actions, raw_obs, out_actions, nullptr, out_obs, out_dt, out_force);
+}
+
+int dr_step_substeps(const float* actions, const float* raw_obs, float* out_actions, float* out_actions_sub,
+                     float* out_obs, float* out_dt, float* out_force) {
+    if (!out_actions_sub) return fail(DR_EINVAL, "out_actions_sub: NULL");
+    return step_common(actions, raw_obs, out_actions, out_actions_sub, out_obs, out_dt, out_force);
 }
 
 int dr_step_host(const float* actions, const float* raw_obs, float* out_actions, float* out_obs, float* out_dt,
@@ -726,4 +747,4 @@ int dr_debug_philox(uint32_t domain, uint32_t channel, uint32_t block, uint32_t*
 
 }  // extern "C"
 
-static_assert(sizeof(dr_env_state) == 148 * 4, "dr_env_state must be 148 words");
+static_assert(sizeof(dr_env_state) == 168 * 4, "dr_env_state must be 168 words");

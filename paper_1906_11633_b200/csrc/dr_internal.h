@@ -46,7 +46,8 @@ enum : int {
     ST_FLAGS = 55,   // u32: tip i timer in bits 4i..4i+3, has_last in bit 20
     ST_FTRIG = 56,   // 3
     ST_KF = 59,      // u32
-    ST_PLANES = 60
+    ST_EMA = 60,     // 20: smoothed action (DR_SMOOTH)
+    ST_PLANES = 80
 };
 constexpr uint32_t HAS_LAST_BIT = 1u << 20;
 // Set by the reset kernel instead of zeroing the 60 state planes ("slack s initialized
@@ -92,6 +93,7 @@ struct DevConst {
     float occl_r2_lo, occl_r2_hi;      // r^2 (1 -+ 1e-5): fp32 fast-path decision band
     uint32_t occl_exact_only;          // r^2 outside the fp32 normal range: always exact fp64
     float accel_std;
+    float smooth_c, smooth_keep;       // EMA: a_s <- smooth_keep * a_s + smooth_c * a
     int32_t n_phys, mass_index;
     int32_t n_phys_u, n_phys_n;       // counts of uniform-kind / normal-kind params
     int32_t n_rs_philox, n_rs_pairs;  // reset task-table lengths (host-built, layer-dependent)
@@ -164,7 +166,7 @@ cudaError_t launch_reset(const DevPtrs& p, const uint8_t* mask, bool first, uint
                          int grid, cudaStream_t s);
 cudaError_t launch_step(const DevPtrs& p, uint32_t layer_mask, const float* actions,
                         const float* raw_obs, float* out_actions, float* out_obs, float* out_dt,
-                        float* out_force, uint32_t n_env, int grid, cudaStream_t s);
+                        float* out_force, float* out_sub, uint32_t n_env, int grid, cudaStream_t s);
 cudaError_t launch_export(const DevPtrs& p, void* dst, uint32_t lo, uint32_t hi, cudaStream_t s);
 cudaError_t launch_import(const DevPtrs& p, const void* src, uint32_t lo, uint32_t hi, cudaStream_t s);
 cudaError_t launch_debug_philox(uint32_t n_env, uint32_t dom, uint32_t ch, uint32_t blk, uint32_t* out,

@@ -21,19 +21,19 @@ __device__ __forceinline__ bool on(uint32_t bit) {
 enum : uint32_t {
     B_TIMING = 1u << 0, B_ACT_NOISE = 1u << 1, B_DELAY = 1u << 2, B_BACKLASH = 1u << 3,
     B_OBS_NOISE = 1u << 4, B_DROPOUT = 1u << 5, B_OCCLUSION = 1u << 6, B_FORCE = 1u << 7,
-    B_PHYS = 1u << 8
+    B_PHYS = 1u << 8, B_SMOOTH = 1u << 9, B_SUBSTEP = 1u << 10
 };
 // layers that own per-env state planes (their state is "fresh" = zero after a reset)
-constexpr uint32_t B_STATEFUL = B_DELAY | B_BACKLASH | B_DROPOUT | B_OCCLUSION | B_FORCE;
+constexpr uint32_t B_STATEFUL = B_DELAY | B_BACKLASH | B_DROPOUT | B_OCCLUSION | B_FORCE | B_SMOOTH;
 
 #include "dr_reset.cuh"
 #include "dr_step.cuh"
 
 // =====================================================================================
-// Export / import (dr_env_state, 148 words per env).  A FRESH env exports its logical state
+// Export / import (dr_env_state, 168 words per env).  A FRESH env exports its logical state
 // (all zero); import writes explicit state (clears FRESH).
 // =====================================================================================
-constexpr int EXP_WORDS = 148;
+constexpr int EXP_WORDS = 168;
 
 __global__ void export_kernel(DevPtrs p, uint32_t* __restrict__ dst, uint32_t lo, uint32_t hi) {
     const uint32_t e = lo + blockIdx.x * blockDim.x + threadIdx.x;
@@ -55,6 +55,7 @@ __global__ void export_kernel(DevPtrs p, uint32_t* __restrict__ dst, uint32_t lo
     for (int i = 0; i < REC_STEP_PLANES - REC_DNEG; ++i) o[8 + i] = R[(REC_DNEG + i) * P];   // 82 words
     for (int i = 0; i < ST_FLAGS; ++i) o[90 + i] = fresh ? 0u : S[i * P];                     // 55 words
     for (int i = 0; i < 3; ++i) o[145 + i] = fresh ? 0u : S[(ST_FTRIG + i) * P];
+    for (int i = 0; i < N_ACT; ++i) o[148 + i] = fresh ? 0u : S[(ST_EMA + i) * P];
 }
 
 __global__ void import_kernel(DevPtrs p, const uint32_t* __restrict__ src, uint32_t lo, uint32_t hi) {
@@ -77,6 +78,7 @@ __global__ void import_kernel(DevPtrs p, const uint32_t* __restrict__ src, uint3
     for (int i = 0; i < REC_STEP_PLANES - REC_DNEG; ++i) R[(REC_DNEG + i) * P] = o[8 + i];
     for (int i = 0; i < ST_FLAGS; ++i) S[i * P] = o[90 + i];
     for (int i = 0; i < 3; ++i) S[(ST_FTRIG + i) * P] = o[145 + i];
+    for (int i = 0; i < N_ACT; ++i) S[(ST_EMA + i) * P] = o[148 + i];
 }
 
 __global__ void debug_philox_kernel(uint32_t n_env, uint32_t dom, uint32_t ch, uint32_t blk, uint4* __restrict__ out) {
@@ -100,7 +102,7 @@ cudaError_t launch_reset(const DevPtrs& p, const uint8_t* mask, bool first, uint
 static constexpr uint32_t MASK_FULL = 0xFFu;  // PHYS does not affect the step
 static constexpr uint32_t MASK_CFG2 = B_TIMING | B_ACT_NOISE | B_BACKLASH | B_OBS_NOISE;
 
-typedef void (*StepFn)(const DevPtrs, const float*, const float*, float*, float*, float*, float*, uint32_t);
+typedef void (*StepFn)(const DevPtrs, const float*, const float*, float*, float*, float*, float*, float*, uint32_t);
 
 // Optional TMA bulk L2 prefetch policy of the step kernel (DR_PREFETCH=0/1/2; A/B experiments).
 // Measured on B200 at 1M envs with the v1 kernel: 0 = none 2.48e9 env-steps/s, 1 = current tile
@@ -141,7 +143,8 @@ static StepFn step_fn_tma(uint32_t m) {
 }
 
 static StepFn step_fn(uint32_t layer_mask) {
-    const uint32_t m = layer_mask & 0xFFu;
+    // PHYS does not affect the step; the variants (SMOOTH, SUBSTEP) run the runtime-mask kernel
+    const uint32_t m = layer_mask & 0x6FFu;
     if (g_pipe == 1) return step_fn_tma(m);
     if (g_pipe == 2) return step_fn_warp(m);
     if (g_prefetch == 0) return step_fn_pf<0>(m);
@@ -173,10 +176,10 @@ int reset_max_ctas_per_sm() {
 }
 
 cudaError_t launch_step(const DevPtrs& p, uint32_t layer_mask, const float* actions, const float* raw_obs,
-                        float* out_actions, float* out_obs, float* out_dt, float* out_force, uint32_t n_env,
-                        int grid, cudaStream_t s) {
+                        float* out_actions, float* out_obs, float* out_dt, float* out_force, float* out_sub,
+                        uint32_t n_env, int grid, cudaStream_t s) {
     step_fn(layer_mask)<<<grid, STEP_THREADS, step_dyn_smem(), s>>>(p, actions, raw_obs, out_actions, out_obs,
-                                                                    out_dt, out_force, n_env);
+                                                                    out_dt, out_force, out_sub, n_env);
     return cudaGetLastError();
 }
 

@@ -327,7 +327,7 @@ struct PipeTma {
 // same path (the ring protocol is warp-synchronous) but store nothing and count nothing.
 template <uint32_t L, class Pipe>
 __device__ __forceinline__ void env_step(const DevPtrs& p, uint32_t e, bool valid, uint32_t t, int tid, float* s_act,
-                                         float* s_obs, float* s_dt, Pipe& pipe, Acc& acc) {
+                                         float* s_obs, float* s_dt, float* out_sub, Pipe& pipe, Acc& acc) {
     constexpr size_t P = PLANE;
     uint32_t* S = p.st + st_index(e);
     const uint32_t g = c_dc.env_offset + e;
@@ -404,6 +404,11 @@ __device__ __forceinline__ void env_step(const DevPtrs& p, uint32_t e, bool vali
         }
         pipe.act_done(b);
 
+        float ema[4];   // DR_SMOOTH state: direct (coalesced) loads, issued before the normals
+        if (on<L>(B_SMOOTH)) {
+#pragma unroll
+            for (int q = 0; q < 4; ++q) ema[q] = fresh ? 0.f : __uint_as_float(S[(ST_EMA + 4 * b + q) * P]);
+        }
         float zu[4], zm[4];
         if (on<L>(B_ACT_NOISE)) {
             normals4_t<kSfuNormals>(philox(g, t, CH_ACT_UADD, b), zu);
@@ -411,11 +416,16 @@ __device__ __forceinline__ void env_step(const DevPtrs& p, uint32_t e, bool vali
         }
         const float4 a4 = a4p[b];
         const float av[4] = {a4.x, a4.y, a4.z, a4.w};
-        float ov[4];
+        float ov[4], anv[4];
 #pragma unroll
         for (int q = 0; q < 4; ++q) {
             const int j = 4 * b + q;
-            const float a = av[q];
+            float a = av[q];
+            if (on<L>(B_SMOOTH)) {
+                // EMA of the policy action before it is applied [Q25]
+                a = c_dc.smooth_keep * ema[q] + c_dc.smooth_c * a;
+                if (valid) S[(ST_EMA + j) * P] = __float_as_uint(a);
+            }
             float ad = a;
             if (on<L>(B_DELAY)) {
                 // one-step delay of flagged actuators [Q9]
@@ -436,7 +446,8 @@ __device__ __forceinline__ void env_step(const DevPtrs& p, uint32_t e, bool vali
             s_da += da;
             s_da2 += da * da;
             float out = an;
-            if (on<L>(B_BACKLASH)) {
+            anv[q] = an;
+            if (on<L>(B_BACKLASH) && !on<L>(B_SUBSTEP)) {
                 // backlash, verbatim [Q4], sgn(0) = 0 [Q3]:
                 // alpha = 1 - clamp(|sgn - s| / (|s' - s| + eps), 0, 1).  The ratio is >= 1 (alpha 0)
                 // unless s sits on the rail sgn already (num == 0: alpha 1) or s' lands on the rail
@@ -454,8 +465,41 @@ __device__ __forceinline__ void env_step(const DevPtrs& p, uint32_t e, bool vali
                 n_a1 += (al == 1.f) ? 1u : 0u;
                 if (valid) S[(ST_SLACK + j) * P] = __float_as_uint(sp);
             }
-            s_bl += fabsf(out - an);
+            s_bl += on<L>(B_SUBSTEP) ? 0.f : fabsf(out - an);
             ov[q] = out;
+        }
+        if (on<L>(B_BACKLASH) && on<L>(B_SUBSTEP)) {
+            // per-substep backlash [Q26]: the slack model of PAPER.md:102-109 once per substep k
+            // with dt_k, a_n held; out_sub[e][k][4b..4b+3] = alpha_k a_n, out_actions = substep 9
+            float sl[4], sg[4], dd[4];
+#pragma unroll
+            for (int q = 0; q < 4; ++q) {
+                sl[q] = slack[q];
+                sg[q] = (anv[q] > 0.f) ? 1.f : ((anv[q] < 0.f) ? -1.f : 0.f);
+                dd[q] = (anv[q] > 0.f) ? dpos[q] : ((anv[q] < 0.f) ? dneg[q] : 0.f);
+            }
+            float4* osub = reinterpret_cast<float4*>(out_sub + (size_t)e * (N_SUB * N_ACT) + 4 * b);
+#pragma unroll 1
+            for (int k = 0; k < N_SUB; ++k) {
+                const float dtk = s_dt[tid * N_SUB + k];
+#pragma unroll
+                for (int q = 0; q < 4; ++q) {
+                    const float s0 = sl[q];
+                    const float sp = fminf(fmaxf(s0 + anv[q] * dd[q] * dtk, -1.f), 1.f);
+                    const float num = fabsf(sg[q] - s0), den = fabsf(sp - s0) + c_dc.eps;
+                    const float al = (num == 0.f) ? 1.f : ((num < den) ? 1.f - __fdividef(num, den) : 0.f);
+                    ov[q] = al * anv[q];
+                    n_rail += (sg[q] != 0.f && fabsf(sp) == 1.f && sp != s0) ? 1u : 0u;
+                    n_a1 += (al == 1.f) ? 1u : 0u;
+                    sl[q] = sp;
+                }
+                if (valid) __stcs(osub + (size_t)k * (N_ACT / 4), make_float4(ov[0], ov[1], ov[2], ov[3]));
+            }
+#pragma unroll
+            for (int q = 0; q < 4; ++q) {
+                s_bl += fabsf(ov[q] - anv[q]);
+                if (valid) S[(ST_SLACK + 4 * b + q) * P] = __float_as_uint(sl[q]);
+            }
         }
         a4p[b] = make_float4(ov[0], ov[1], ov[2], ov[3]);
     }
@@ -732,7 +776,8 @@ __device__ __forceinline__ void reduce_stats(const DevPtrs& p, const Acc& acc, u
         red(6, (double)acc.n[K_TRIG]);
         red(7, (double)acc.n[K_RAIL]);
         red(8, (double)acc.n[K_ALPHA1]);
-        red(9, on<L>(B_BACKLASH) ? (double)my_envs * N_ACT - (double)acc.n[K_ALPHA1] : 0.0);
+        red(9, on<L>(B_BACKLASH) ? (double)my_envs * N_ACT * (on<L>(B_SUBSTEP) ? N_SUB : 1) - (double)acc.n[K_ALPHA1]
+                                 : 0.0);
         red(10, 0.0);
         red(11, (double)acc.n[K_CLAMPS]);
         red(12, 0.0); red(13, 0.0); red(14, 0.0); red(15, 0.0);
@@ -790,7 +835,7 @@ template <uint32_t L, int PF>
 __global__ void __launch_bounds__(STEP_THREADS, STEP_MIN_CTAS)
     step_kernel(const DevPtrs p, const float* __restrict__ actions, const float* __restrict__ raw_obs,
                 float* __restrict__ out_actions, float* __restrict__ out_obs, float* __restrict__ out_dt,
-                float* __restrict__ out_force, uint32_t n_env) {
+                float* __restrict__ out_force, float* __restrict__ out_sub, uint32_t n_env) {
     __shared__ __align__(16) float s_act[TILE * N_ACT];   // actions in, out_actions out (in place)
     __shared__ __align__(16) float s_obs[TILE * OBS_IN];  // raw_obs in, out_obs + out_force out (stride 26)
     __shared__ __align__(16) float s_dt[TILE * N_SUB];
@@ -837,7 +882,7 @@ __global__ void __launch_bounds__(STEP_THREADS, STEP_MIN_CTAS)
         __syncthreads();   // everyone's staging copies
         if (mine) {
             PipeThread<L> pipe{s_ring + tid, s_ring + RING_W * TILE + tid, R, S};
-            env_step<L>(p, e0 + tid, true, t, tid, s_act, s_obs, s_dt, pipe, acc);
+            env_step<L>(p, e0 + tid, true, t, tid, s_act, s_obs, s_dt, out_sub, pipe, acc);
             ++my_envs;
         }
         cp_wait<0>();
@@ -870,7 +915,7 @@ template <uint32_t L>
 __global__ void __launch_bounds__(STEP_THREADS, STEP_MIN_CTAS)
     step_kernel_tma(const DevPtrs p, const float* __restrict__ actions, const float* __restrict__ raw_obs,
                     float* __restrict__ out_actions, float* __restrict__ out_obs, float* __restrict__ out_dt,
-                    float* __restrict__ out_force, uint32_t n_env) {
+                    float* __restrict__ out_force, float* __restrict__ out_sub, uint32_t n_env) {
     __shared__ __align__(128) float s_act[TILE * N_ACT];   // TMA destination; out_actions in place
     __shared__ __align__(128) float s_obs[TILE * OBS_IN];  // TMA destination; out_obs + out_force in place
     __shared__ __align__(16) float s_dt[TILE * N_SUB];
@@ -913,7 +958,7 @@ __global__ void __launch_bounds__(STEP_THREADS, STEP_MIN_CTAS)
             *reinterpret_cast<float2*>(s_obs + cnt * OBS_IN - 2) = v;
         }
         PipeTma<L> pipe{&p, s_ring, &ts, it * N_PHASES, it, n_my, n_tiles, tid};
-        env_step<L>(p, e0 + tid, mine, t, tid, s_act, s_obs, s_dt, pipe, acc);
+        env_step<L>(p, e0 + tid, mine, t, tid, s_act, s_obs, s_dt, out_sub, pipe, acc);
         my_envs += mine ? 1u : 0u;
         __syncthreads();   // all output rows are in shared memory
         store_tile(e0, cnt, tid, s_act, s_obs, s_dt, out_actions, out_obs, out_dt, out_force);
@@ -935,7 +980,7 @@ template <uint32_t L>
 __global__ void __launch_bounds__(STEP_THREADS, STEP_MIN_CTAS)
     step_kernel_warp(const DevPtrs p, const float* __restrict__ actions, const float* __restrict__ raw_obs,
                      float* __restrict__ out_actions, float* __restrict__ out_obs, float* __restrict__ out_dt,
-                     float* __restrict__ out_force, uint32_t n_env) {
+                     float* __restrict__ out_force, float* __restrict__ out_sub, uint32_t n_env) {
     __shared__ __align__(16) float s_act[TILE * N_ACT];
     __shared__ __align__(16) float s_obs[TILE * OBS_IN];
     __shared__ __align__(16) float s_dt[TILE * N_SUB];
@@ -975,7 +1020,7 @@ __global__ void __launch_bounds__(STEP_THREADS, STEP_MIN_CTAS)
         cp_wait<1>();      // staging + S0
         __syncthreads();   // everyone's staging copies (and each warp's S0)
         const bool mine = (uint32_t)tid < cnt;
-        env_step<L>(p, e0 + tid, mine, t, tid, s_act, s_obs, s_dt, pipe, acc);
+        env_step<L>(p, e0 + tid, mine, t, tid, s_act, s_obs, s_dt, out_sub, pipe, acc);
         my_envs += mine ? 1u : 0u;
         cp_wait<0>();
         __syncthreads();

@@ -16,10 +16,11 @@ LIB_PATH = os.path.join(PKG, "libdr.so")
 # A/B experiments load an alternative in-tree build (e.g. variants/libdr_m6.so); never a fallback.
 _LIB_OVERRIDE = os.environ.get("DR_LIB")
 
-ABI_VERSION = 1
+ABI_VERSION = 2
 N_ACT, N_TIPS, N_SUB, MAX_PHYS, OBS_IN, OBS_OUT, N_STATS = 20, 5, 10, 256, 26, 22, 32
 TIMING, ACT_NOISE, DELAY, BACKLASH, OBS_NOISE = 1, 2, 4, 8, 16
 DROPOUT, OCCLUSION, FORCE, PHYS, ALL = 32, 64, 128, 256, 0x1FF
+SMOOTH, SUBSTEP_BACKLASH, ALL_EXT = 512, 1024, 0x7FF
 
 STATUS = {0: "DR_OK", -1: "DR_EINVAL", -2: "DR_ENOTINIT", -3: "DR_EALREADY", -4: "DR_ENOMEM",
           -5: "DR_ECUDA", -6: "DR_EUNSUPPORTED"}
@@ -57,6 +58,7 @@ class DrParams(C.Structure):
         ("dropout_rate_hz", C.c_double), ("occl_dist", C.c_double),
         ("force_p_lo", C.c_double), ("force_p_hi", C.c_double), ("force_accel_std", C.c_double),
         ("force_decay_per_step", C.c_double),
+        ("act_smooth_coef", C.c_double),
         ("n_phys", C.c_int32), ("mass_index", C.c_int32),
         ("phys", PhysDesc * MAX_PHYS),
         ("workspace", C.c_void_p), ("workspace_bytes", C.c_size_t), ("stream", C.c_void_p),
@@ -70,7 +72,7 @@ class DrEnvState(C.Structure):
         ("dneg", C.c_float * N_ACT), ("dpos", C.c_float * N_ACT), ("c_act", C.c_float * N_ACT),
         ("off_tip", C.c_float * 15), ("c_obj", C.c_float * 3), ("q_c", C.c_float * 4),
         ("prev", C.c_float * N_ACT), ("slack", C.c_float * N_ACT), ("last", C.c_float * 15),
-        ("f_trig", C.c_float * 3),
+        ("f_trig", C.c_float * 3), ("ema", C.c_float * N_ACT),
     ]
 
 
@@ -96,6 +98,7 @@ def load():
     L.dr_update_params.argtypes = [C.POINTER(DrParams)]
     L.dr_step.argtypes = [fp] * 6
     L.dr_step_host.argtypes = [fp] * 6
+    L.dr_step_substeps.argtypes = [fp] * 7
     L.dr_finalize.argtypes = []
     L.dr_workspace_bytes.argtypes = [C.POINTER(DrParams), C.c_int64]
     L.dr_workspace_bytes.restype = C.c_size_t
@@ -117,7 +120,7 @@ def load():
     L.dr_phys_export.argtypes = [vp, C.c_int64, C.c_int64]
     L.dr_debug_philox.argtypes = [C.c_uint32, C.c_uint32, C.c_uint32, vp]
     L.dr_debug_philox.restype = C.c_int
-    for f in ("dr_params_default", "dr_init", "dr_update_params", "dr_reset", "dr_step", "dr_step_host", "dr_finalize",
+    for f in ("dr_params_default", "dr_init", "dr_update_params", "dr_reset", "dr_step", "dr_step_substeps", "dr_step_host", "dr_finalize",
               "dr_set_stream", "dr_synchronize", "dr_set_stats_buffer", "dr_set_step_index",
               "dr_state_export", "dr_state_import", "dr_phys_export"):
         getattr(L, f).restype = C.c_int
@@ -209,6 +212,17 @@ def dr_step(actions, raw_obs, out_actions, out_obs, out_dt, out_force):
                                  _ptr(out_actions, (n, N_ACT), f, "out_actions"),
                                  _ptr(out_obs, (n, OBS_OUT), f, "out_obs"), _ptr(out_dt, (n, N_SUB), f, "out_dt"),
                                  _ptr(out_force, (n, 3), f, "out_force")))
+
+
+def dr_step_substeps(actions, raw_obs, out_actions, out_actions_sub, out_obs, out_dt, out_force):
+    import torch
+    n = actions.shape[0]
+    f = torch.float32
+    return _check(load().dr_step_substeps(
+        _ptr(actions, (n, N_ACT), f, "actions"), _ptr(raw_obs, (n, OBS_IN), f, "raw_obs"),
+        _ptr(out_actions, (n, N_ACT), f, "out_actions"), _ptr(out_actions_sub, (n, N_SUB, N_ACT), f, "out_actions_sub"),
+        _ptr(out_obs, (n, OBS_OUT), f, "out_obs"), _ptr(out_dt, (n, N_SUB), f, "out_dt"),
+        _ptr(out_force, (n, 3), f, "out_force")))
 
 
 def _host_ptr(t, shape, name):

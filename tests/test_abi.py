@@ -57,9 +57,9 @@ def test_default_params_are_the_paper_values(lib):
     assert (p.n_act, p.n_tips, p.n_substeps) == (20, 5, 10)
 
 
-def test_state_struct_is_148_words():
+def test_state_struct_is_168_words():
     from paper_1906_11633_b200 import dr
-    assert C.sizeof(dr.DrEnvState) == 148 * 4
+    assert C.sizeof(dr.DrEnvState) == 168 * 4
 
 
 @pytest.mark.parametrize("field,value,needle", [

@@ -6,7 +6,7 @@ import pytest
 from parity import (KnifeTracker, assert_close, compare_obs, compare_records, compare_stats)
 from workload import gen, presets
 from workload.presets import (ACT_NOISE, BACKLASH, CFG2, DELAY, DROPOUT, FORCE, FULL, OBS_NOISE,
-                              OCCLUSION, PHYS, TIMING)
+                              OCCLUSION, PHYS, SMOOTH, SUBSTEP_BACKLASH, TIMING)
 
 pytestmark = pytest.mark.gpu
 SEED = presets.SEED_DR
@@ -73,7 +73,8 @@ def run_pair(torch, mask, n_env, T, n_frames=8, resets=None, sample=None, state_
                 orc.reset(m[gids])
             f = t % n_frames
             ctx.step(A[f], O[f])
-            r = orc.step(acts[f][gids], obs[f][gids], want_margin=True)
+            sub = bool(mask & SUBSTEP_BACKLASH)
+            r = orc.step(acts[f][gids], obs[f][gids], want_margin=True, want_sub=sub)
             torch.cuda.synchronize()
             oa = ctx.out_actions.cpu().numpy()[gids]
             oo = ctx.out_obs.cpu().numpy()[gids]
@@ -81,6 +82,11 @@ def run_pair(torch, mask, n_env, T, n_frames=8, resets=None, sample=None, state_
             of = ctx.out_force.cpu().numpy()[gids]
             knife.update_before_compare(r["margin"])
             knife.compare_actions(oa, r["out_actions"], t)
+            if sub:
+                gs = ctx.out_actions_sub.cpu().numpy()[gids]
+                assert np.array_equal(gs[:, -1], oa), "out_actions == last substep"
+                assert_close(f"out_actions_sub t={t}", gs, r["out_actions_sub"], 1.0,
+                             mask=~np.broadcast_to(knife.excused[:, None, :], gs.shape))
             compare_obs(oo, r["out_obs"], t)
             assert_close(f"out_dt t={t}", od, r["out_dt"], 0.008)
             mass = np.array([orc.env(i)["mass"] for i in range(len(gids))]) if (mask & FORCE) else np.ones(len(gids))
@@ -159,6 +165,16 @@ def test_layer_subsets(torch_cuda, mask):
 def test_ragged_sizes(torch_cuda, n):
     """Tile tails (TILE = 128), single env, odd counts: scalar staging paths."""
     run_pair(torch_cuda, FULL, n, 12, n_frames=12, resets={6: (np.arange(n) % 2 == 0).astype(np.uint8)})
+
+
+@pytest.mark.parametrize("mask,n", [(FULL | SMOOTH, 200), (FULL | SMOOTH | SUBSTEP_BACKLASH, 200),
+                                    (CFG2 | SUBSTEP_BACKLASH, 131), (BACKLASH | SUBSTEP_BACKLASH, 70),
+                                    (SMOOTH | DELAY, 33)])
+def test_smoothing_and_substep_backlash(torch_cuda, mask, n):
+    """EMA action smoothing and the per-substep backlash
+    variant -- every output incl. the [n][10][20] substep actions, state incl.
+    the EMA, and stats, with resets mid-run."""
+    run_pair(torch_cuda, mask, n, 20, n_frames=20, resets={9: (np.arange(n) % 3 == 1).astype(np.uint8)})
 
 
 def test_update_params_mid_run(torch_cuda):

@@ -559,3 +559,79 @@ def test_update_params_force_and_dropout_thresholds():
         inits += o.step(acts[t], obs[t])["stats"][2]
     assert inits == 0
     o.close()
+
+
+# ---- §8(f) rank 2: EMA action smoothing and the per-substep backlash variant -------------------
+def test_smoothing_geometric_step_response():
+    """EMA with coefficient 0.3 per 80 ms step: a constant command a from a
+    zero state gives a (1 - 0.7^(t+1)) at step t -- the geometric closed form; a reset returns the
+    state to 0 [Q25]."""
+    from workload.presets import SMOOTH
+    n, T = 8, 12
+    o = _oracle(SMOOTH, n)
+    a = np.full((n, 20), 0.6, np.float32)
+    obs = gen.frames(n, 1)[1][0]
+    a64 = float(np.float32(0.6))
+    for t in range(T):
+        r = o.step(a, obs)
+        assert np.abs(r["out_actions"] - a64 * (1.0 - 0.7 ** (t + 1))).max() < 1e-12
+    o.reset((np.arange(n) < 4).astype(np.uint8))
+    r = o.step(a, obs)
+    assert np.abs(r["out_actions"][:4] - 0.3 * a64).max() < 1e-15
+    assert np.abs(r["out_actions"][4:] - a64 * (1.0 - 0.7 ** (T + 1))).max() < 1e-12
+    o.close()
+
+
+def test_substep_backlash_hand_computed_and_consistent():
+    """Per-substep backlash [Q26] with TIMING off (every dt_k = 8 ms), delta+1 = 4, a = 0.5 from
+    s = 0: the slack climbs 0.016 per substep (0.5 * 4 * 0.008), the gate stays closed (alpha = 0,
+    output 0) until the start-of-substep slack sits on the rail +1, then passes a exactly
+    (PAPER.md:102-109).  Without rail contact the 10 substep updates end where the one per-step
+    update with dt_env = sum dt_k ends (linearity), and out_actions = the last substep."""
+    from workload.presets import SUBSTEP_BACKLASH
+    n = 4
+    kw = dict(delta_cal_pos=[4.0] * 20, delta_cal_neg=[4.0] * 20, delta_jitter_std=0.0)
+    o = _oracle(BACKLASH | SUBSTEP_BACKLASH, n, **kw)
+    a = np.full((n, 20), 0.5, np.float32)
+    obs = gen.frames(n, 1)[1][0]
+    outs = []
+    for t in range(8):
+        r = o.step(a, obs, want_sub=True)
+        assert np.array_equal(r["out_actions"], r["out_actions_sub"][:, -1])
+        outs.append(r["out_actions_sub"][0, :, 0])
+    sub = np.concatenate(outs)     # 80 substeps of actuator 0
+    k_rail = int(np.ceil(1.0 / 0.016 - 1e-9))   # the update that reaches +1 (63rd)
+    assert (np.abs(sub[:k_rail]) < 1e-9).all()       # closed (alpha 0, or eps-sized on the rail hit)
+    assert (sub[k_rail:] == 0.5).all()               # open: s == sgn(a)
+    s_final = o.env(0)["slack"][0]
+    assert s_final == 1.0
+    # linearity: away from the rails, substep and per-step slack agree
+    p = _oracle(BACKLASH | SUBSTEP_BACKLASH | TIMING, n, **kw)
+    q = _oracle(BACKLASH | TIMING, n, **kw)
+    a2 = np.full((n, 20), 0.2, np.float32)
+    for t in range(3):
+        p.step(a2, obs)
+        q.step(a2, obs)
+        sp = np.array([p.env(i)["slack"] for i in range(n)])
+        sq = np.array([q.env(i)["slack"] for i in range(n)])
+        assert np.abs(sp - sq).max() < 1e-12 and np.abs(sq).max() < 1.0
+    o.close(), p.close(), q.close()
+
+
+def test_substep_backlash_invariants():
+    """Every substep keeps the slack in [-1, 1] and |out| <= |a_n| with out a_n >= 0, on the FULL
+    layer set with resets (PAPER.md:102-109 invariants)."""
+    from workload.presets import SMOOTH, SUBSTEP_BACKLASH
+    n, T = 64, 20
+    acts, obs = gen.frames(n, T)
+    o = _oracle(FULL | SMOOTH | SUBSTEP_BACKLASH, n)
+    for t in range(T):
+        r = o.step(acts[t], obs[t], want_sub=True)
+        s = np.array([o.env(i)["slack"] for i in range(n)])
+        assert np.abs(s).max() <= 1.0
+        sub = r["out_actions_sub"]
+        assert np.abs(sub).max() <= 1.0
+        assert np.array_equal(sub[:, -1], r["out_actions"])
+        if t == 10:
+            o.reset((np.arange(n) % 2).astype(np.uint8))
+    o.close()

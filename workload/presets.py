@@ -11,6 +11,8 @@ import copy
 TIMING, ACT_NOISE, DELAY, BACKLASH, OBS_NOISE = 1 << 0, 1 << 1, 1 << 2, 1 << 3, 1 << 4
 DROPOUT, OCCLUSION, FORCE, PHYS = 1 << 5, 1 << 6, 1 << 7, 1 << 8
 ALL = 0x1FF
+# SURVEY.md §8(f) rank 2 variants (not in the paper's randomization set, so not in FULL)
+SMOOTH, SUBSTEP_BACKLASH = 1 << 9, 1 << 10
 FULL = ALL
 # config 2: "backlash + action/obs noise"; TIMING is needed because backlash uses dt.
 CFG2 = TIMING | ACT_NOISE | BACKLASH | OBS_NOISE
@@ -70,6 +72,8 @@ PAPER = {
     "dropout_rate_hz": 0.2, "dropout_hold_steps": 13, "occl_dist": 0.015,
     # random forces
     "force_p_lo": 0.001, "force_p_hi": 0.1, "force_accel_std": 1.0, "force_decay_per_step": 0.99,
+    # action smoothing: "exponential moving average ... coefficient of 0.3 per 80ms" [Q25]
+    "act_smooth_coef": 0.3,
     # physical parameters [Q20]
     "n_phys": MAX_PHYS, "mass_index": 0, "phys": default_phys_table(),
     "layer_mask": FULL,
