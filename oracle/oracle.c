@@ -188,6 +188,7 @@ struct orc_ctx {
     double p_tab[P_TABLE_N];
     uint64_t t_tab[P_TABLE_N];
     orc_env* env;
+    const uint8_t* occl_mask;   /* simulator occlusion bits per env, or NULL (distance rule) */
 };
 
 /* 4 words of channel ch, block blk, for global env gid and domain index (t or k_e). */
@@ -457,7 +458,7 @@ int orc_reset(orc_ctx* c, const uint8_t* mask)
 /* One environment step of one env, PAPER.md:70-115 and 63-66 in the order of DESIGN.md
  * [Q1]: timing -> delay -> action noise (+clamp) -> backlash; occlusion -> dropout ->
  * fingertip noise + hold -> object position -> orientation -> force. */
-static void step_env(orc_ctx* c, orc_env* e, const float* act, const float* obs,
+static void step_env(orc_ctx* c, orc_env* e, const float* act, const float* obs, int occ_bits,
                      double* o_act, double* o_sub, double* o_obs, double* o_dt, double* o_force,
                      double* st, double* margin)
 {
@@ -577,9 +578,13 @@ static void step_env(orc_ctx* c, orc_env* e, const float* act, const float* obs,
         const float* tips = obs;        /* raw_obs[0..14] */
         const float* obj = obs + 15;    /* raw_obs[15..17] */
         int occ[ORC_N_TIPS], masked[ORC_N_TIPS];
-        /* 5. occlusion: distance rule on raw positions, exact fp64 [Q13]. */
+        /* 5. occlusion: distance rule on raw positions, exact fp64 [Q13]; or the
+         *    simulator's own per-marker occlusion bits when it provides them [Q27]. */
         for (i = 0; i < ORC_N_TIPS; ++i) {
-            occ[i] = ((L & ORC_OCCLUSION) && p->occl_dist > 0.0) ? orc_occluded(tips, obj, p->occl_dist, i) : 0;
+            if (occ_bits >= 0)
+                occ[i] = (L & ORC_OCCLUSION) ? ((occ_bits >> i) & 1) : 0;
+            else
+                occ[i] = ((L & ORC_OCCLUSION) && p->occl_dist > 0.0) ? orc_occluded(tips, obj, p->occl_dist, i) : 0;
             if (occ[i]) st[ORC_S_OCCLUDED] += 1.0;
         }
         /* 6. dropout: each fingertip marker starts a 1 s mask with probability
@@ -708,6 +713,7 @@ int orc_step_sub(orc_ctx* c, const float* actions, const float* raw_obs,
     memset(st, 0, sizeof(st));
     for (i = 0; i < c->n; ++i) {
         step_env(c, &c->env[i], actions + i * ORC_N_ACT, raw_obs + i * ORC_OBS_IN,
+                 c->occl_mask ? (int)(c->occl_mask[i] & 0x1Fu) : -1,
                  out_actions ? out_actions + i * ORC_N_ACT : NULL,
                  out_actions_sub ? out_actions_sub + i * ORC_N_SUB * ORC_N_ACT : NULL,
                  out_obs ? out_obs + i * ORC_OBS_OUT : NULL,
@@ -722,6 +728,8 @@ int orc_step_sub(orc_ctx* c, const float* actions, const float* raw_obs,
     c->t += 1;
     return 0;
 }
+
+void orc_set_occlusion_mask(orc_ctx* c, const uint8_t* mask) { if (c) c->occl_mask = mask; }
 
 uint64_t orc_step_index(const orc_ctx* c) { return c ? c->t : 0; }
 void orc_set_step_index(orc_ctx* c, uint64_t t) { if (c) c->t = t; }

@@ -134,6 +134,10 @@ int  orc_step(orc_ctx* c, const float* actions, const float* raw_obs,
 int  orc_step_sub(orc_ctx* c, const float* actions, const float* raw_obs,
                   double* out_actions, double* out_actions_sub, double* out_obs, double* out_dt,
                   double* out_force, double* stats, double* bl_margin);
+/* Simulator-provided occlusion: bit i of mask[e] = fingertip marker i of
+ * env e occluded this step (the simulator's collision-site rule) replaces the distance
+ * rule; NULL restores it.  The array (n bytes) is read at every later orc_step. */
+void     orc_set_occlusion_mask(orc_ctx* c, const uint8_t* mask);
 uint64_t orc_step_index(const orc_ctx* c);
 void     orc_set_step_index(orc_ctx* c, uint64_t t);
 int      orc_get_env(const orc_ctx* c, int64_t i, orc_env* dst);
@@ -185,6 +189,17 @@ int orc_scene_draw(const orc_vision_params* p, uint64_t seed, uint64_t batch, in
 int orc_image_augment(const orc_vision_params* p, uint64_t seed, uint64_t batch, int64_t image_offset,
                       const uint8_t* images, int64_t n, int32_t h, int32_t w, int32_t c, double* out,
                       double* img_stats);
+
+/* Vision-model training pose augmentation: per sample,
+ * keep the pose (p_keep = 20 %), rotate the object 90 deg about one of its body axes (p_rot90 =
+ * 40 %), or jitter position and rotation independently with Gaussian noise (the remaining 40 %).
+ * pose_in [n][7] = position xyz, unit quaternion wxyz; pose_out [n][7] fp64; branch [n] = 0/1/2. */
+typedef struct {
+    double p_keep, p_rot90;      /* 0.2, 0.4 */
+    double pos_std, rot_std;     /* jitter: 5 mm per axis, 0.05 rad about a uniform axis (values not in the paper) */
+} orc_pose_aug_params;
+int orc_pose_augment(const orc_pose_aug_params* p, uint64_t seed, uint64_t batch, int64_t offset,
+                     const float* pose_in, int64_t n, double* pose_out, uint8_t* branch);
 
 /* stats slot indices */
 enum {

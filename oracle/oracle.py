@@ -81,6 +81,10 @@ class OrcVisionParams(C.Structure):
         "noise_std_lo", "noise_std_hi", "std_floor")]
 
 
+class OrcPoseAugParams(C.Structure):
+    _fields_ = [("p_keep", C.c_double), ("p_rot90", C.c_double), ("pos_std", C.c_double), ("rot_std", C.c_double)]
+
+
 SCENE_WORDS = 64
 
 _lib = None
@@ -101,6 +105,9 @@ def lib():
         L.orc_image_augment.argtypes = [C.POINTER(OrcVisionParams), C.c_uint64, C.c_uint64, C.c_int64, u8p,
                                         C.c_int64, C.c_int32, C.c_int32, C.c_int32, dp, dp]
         L.orc_image_augment.restype = C.c_int
+        L.orc_pose_augment.argtypes = [C.POINTER(OrcPoseAugParams), C.c_uint64, C.c_uint64, C.c_int64, fp, C.c_int64,
+                                       dp, u8p]
+        L.orc_pose_augment.restype = C.c_int
         L.orc_update_params.argtypes = [C.c_void_p, C.POINTER(OrcParams)]
         L.orc_update_params.restype = C.c_int
         L.orc_reset.argtypes = [C.c_void_p, u8p]
@@ -109,6 +116,7 @@ def lib():
         L.orc_step.restype = C.c_int
         L.orc_step_sub.argtypes = [C.c_void_p, fp, fp, dp, dp, dp, dp, dp, dp, dp]
         L.orc_step_sub.restype = C.c_int
+        L.orc_set_occlusion_mask.argtypes = [C.c_void_p, u8p]
         L.orc_step_index.argtypes = [C.c_void_p]
         L.orc_step_index.restype = C.c_uint64
         L.orc_set_step_index.argtypes = [C.c_void_p, C.c_uint64]
@@ -238,6 +246,20 @@ def image_augment(preset: dict, seed: int, batch: int, images, image_offset: int
     return out, st
 
 
+def pose_augment(preset: dict, seed: int, batch: int, poses, offset: int = 0):
+    """poses float32 [n][7] (pos, quat wxyz) -> (fp64 [n][7], branch u8 [n])."""
+    x = np.ascontiguousarray(poses, dtype=np.float32)
+    n = x.shape[0]
+    p = OrcPoseAugParams(*(preset[k] for k in ("p_keep", "p_rot90", "pos_std", "rot_std")))
+    out = np.empty((n, 7))
+    br = np.empty(n, dtype=np.uint8)
+    rc = lib().orc_pose_augment(C.byref(p), C.c_uint64(seed), C.c_uint64(batch), offset, _ptr(x, C.c_float), n,
+                                _ptr(out, C.c_double), _ptr(br, C.c_uint8))
+    if rc != 0:
+        raise ValueError(f"orc_pose_augment failed: {rc}")
+    return out, br
+
+
 # ---- context -------------------------------------------------------------------------------
 class Oracle:
     """fp64 CPU oracle over a list of global env ids (any subset of a larger run)."""
@@ -266,6 +288,13 @@ class Oracle:
             self.close()
         except Exception:
             pass
+
+    def set_occlusion_mask(self, mask):
+        """Simulator occlusion bits [n] u8 (bit i = tip i), or None for the distance rule.  The
+        array is kept alive here and re-read at every step (update it in place)."""
+        self._occl = None if mask is None else np.ascontiguousarray(mask, dtype=np.uint8)
+        lib().orc_set_occlusion_mask(self._h, None if self._occl is None else _ptr(self._occl, C.c_uint8))
+        return self._occl
 
     def update_params(self, preset: dict):
         """Swap the parameter set mid-run: later draws use it."""

@@ -12,6 +12,7 @@
 #include "oracle.h"
 
 enum {
+    CH_POSE = 0x401,
     CH_IMG_PARAM = 0x201, CH_IMG_NOISE = 0x202,
     CH_SCENE_CAM = 0x301, CH_SCENE_MAT = 0x302, CH_SCENE_LIGHT = 0x303
 };
@@ -166,5 +167,59 @@ int orc_image_augment(const orc_vision_params* p, uint64_t seed, uint64_t batch,
     for (i = 0; i < n; ++i)
         augment_one(p, seed, batch, image_offset + i, images + i * E, E, out + i * E,
                     img_stats ? img_stats + 4 * i : NULL);
+    return 0;
+}
+
+/* Pose augmentation of one sample [Q28]:
+ *   x0 of block 0 picks the branch: x0 < floor(p_keep 2^32) keep; x0 < floor((p_keep + p_rot90)
+ *   2^32) rotate; else jitter (exact integer decisions);
+ *   rotate: k = floor(6 x1 / 2^32) -> body axis k / 2, sign (k odd ? -1 : +1); q_out = q (x) r with
+ *   r = (cos 45 deg, sign sin 45 deg e_axis): exactly 90 deg about the object's own axis;
+ *   jitter: position + pos_std z (normals 0..2 of block 1), q_out = q_j (x) q with q_j a rotation
+ *   of angle rot_std z about a uniform axis from block 2 (the obs-noise rotation convention). */
+static void pose_one(const orc_pose_aug_params* p, uint64_t seed, uint64_t batch, int64_t g, const float* in,
+                     double* out, uint8_t* br)
+{
+    uint32_t w[4], v[4];
+    double q[4], r[4];
+    int c, b;
+    uint64_t t1 = orc_bernoulli_threshold(p->p_keep);
+    uint64_t t2 = orc_bernoulli_threshold(p->p_keep + p->p_rot90);
+    for (c = 0; c < 3; ++c) out[c] = (double)in[c];
+    for (c = 0; c < 4; ++c) q[c] = (double)in[3 + c];
+    block(seed, g, batch, CH_POSE, 0, w);
+    b = ((uint64_t)w[0] < t1) ? 0 : (((uint64_t)w[0] < t2) ? 1 : 2);
+    if (b == 0) {
+        for (c = 0; c < 4; ++c) out[3 + c] = q[c];
+    } else if (b == 1) {
+        int k = (int)(((uint64_t)w[1] * 6u) >> 32);
+        double sh = (k & 1) ? -sqrt(0.5) : sqrt(0.5);
+        r[0] = sqrt(0.5);
+        r[1] = r[2] = r[3] = 0.0;
+        r[1 + k / 2] = sh;
+        orc_quat_mul(q, r, out + 3);
+    } else {
+        double z0, z1, z2, z3;
+        block(seed, g, batch, CH_POSE, 1, v);
+        orc_normal_pair(v[0], v[1], &z0, &z1);
+        orc_normal_pair(v[2], v[3], &z2, &z3);
+        (void)z3;
+        out[0] = out[0] + p->pos_std * z0;
+        out[1] = out[1] + p->pos_std * z1;
+        out[2] = out[2] + p->pos_std * z2;
+        block(seed, g, batch, CH_POSE, 2, v);
+        orc_rotation(p->rot_std, v, r);
+        orc_quat_mul(r, q, out + 3);
+    }
+    if (br) *br = (uint8_t)b;
+}
+
+int orc_pose_augment(const orc_pose_aug_params* p, uint64_t seed, uint64_t batch, int64_t offset,
+                     const float* pose_in, int64_t n, double* pose_out, uint8_t* branch)
+{
+    int64_t i;
+    if (!p || !pose_in || !pose_out || n < 0) return -1;
+    for (i = 0; i < n; ++i)
+        pose_one(p, seed, batch, offset + i, pose_in + 7 * i, pose_out + 7 * i, branch ? branch + i : NULL);
     return 0;
 }

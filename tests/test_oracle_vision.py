@@ -193,3 +193,74 @@ def test_scene_lights(scenes):
     r = I[:, 1] / I[:, 0]
     assert r.min() >= 0.2 - 1e-12 and r.max() <= 5 + 1e-12
     assert (S[:, 60:64] == 0).all()
+
+
+# ---- vision-model pose augmentation ----------------------
+def _qmul(a, b):
+    w1, x1, y1, z1 = a.T
+    w2, x2, y2, z2 = b.T
+    return np.stack([w1 * w2 - x1 * x2 - y1 * y2 - z1 * z2, w1 * x2 + x1 * w2 + y1 * z2 - z1 * y2,
+                     w1 * y2 - x1 * z2 + y1 * w2 + z1 * x2, w1 * z2 + x1 * y2 - y1 * x2 + z1 * w2], axis=1)
+
+
+def test_pose_augment_branches():
+    """Keep the pose 20 %, rotate 90 deg about a main (body) axis 40 %, jitter position and rotation
+    40 %: branch frequencies, exact identity, the relative rotation q_in^-1 q_out is
+    exactly 90 deg about +-e_x / e_y / e_z with the position unchanged, and the jitter's position
+    noise is N(0, pos_std^2) with a half-normal rotation angle."""
+    from oracle import oracle as O
+    P = presets.pose_preset()
+    n = 100000
+    x = presets.poses(n, seed=3)
+    out, br = O.pose_augment(P, SEED, 2, x)
+    f = np.bincount(br, minlength=3) / n
+    assert np.abs(f - np.array([0.2, 0.4, 0.4])).max() < 0.01
+    xin = x.astype(np.float64)
+    k0, k1, k2 = br == 0, br == 1, br == 2
+    assert np.array_equal(out[k0], xin[k0])
+    assert np.array_equal(out[k1, :3], xin[k1, :3])
+    conj = xin[k1, 3:] * np.array([1, -1, -1, -1])
+    rel = _qmul(conj, out[k1, 3:])
+    rel /= np.linalg.norm(rel, axis=1, keepdims=True)                       # inputs are unit to float32 only
+    assert np.abs(np.abs(rel[:, 0]) - math.sqrt(0.5)).max() < 1e-12        # angle exactly 90 deg
+    ax = np.abs(rel[:, 1:]) > 1e-9
+    assert (ax.sum(axis=1) == 1).all()                                      # about one body axis
+    cnt = ax.sum(axis=0) / ax.shape[0]
+    assert np.abs(cnt - 1 / 3).max() < 0.015
+    z = (out[k2, :3] - xin[k2, :3]) / P["pos_std"]
+    assert stats.kstest(z.reshape(-1), "norm").pvalue > 1e-3
+    qn = np.linalg.norm(out[:, 3:], axis=1)
+    assert np.abs(qn - 1).max() < 1e-6                                      # float32 inputs, unit to ~1e-7
+    rel2 = _qmul(out[k2, 3:], xin[k2, 3:] * np.array([1, -1, -1, -1]))     # q_j = q_out q_in^-1 (world frame)
+    ang = 2 * np.arccos(np.clip(np.abs(rel2[:, 0]) / np.linalg.norm(rel2, axis=1), -1, 1))
+    assert abs(ang.mean() - P["rot_std"] * math.sqrt(2 / math.pi)) < 4 * P["rot_std"] / math.sqrt(ang.size)
+
+
+# ---- simulator-provided occlusion bits (SURVEY.md §8(f) rank 4) ---------------------------------
+def test_simulator_occlusion_mask_drives_the_hold():
+    """With the simulator's occlusion bits installed, the occluded count is their popcount, and a
+    flagged tip returns exactly its previous reading (PAPER.md:66 "last available reading");
+    with the OCCLUSION layer off the bits are ignored."""
+    from oracle.oracle import Oracle
+    from workload.presets import DROPOUT, FULL, OCCLUSION
+    n, T = 32, 6
+    from workload import gen
+    acts, obs = gen.frames(n, T)
+    o = Oracle(presets.preset(FULL & ~DROPOUT), n, SEED)
+    rng = np.random.default_rng(0)
+    m = o.set_occlusion_mask(np.zeros(n, np.uint8))
+    prev = o.step(acts[0], obs[0])["out_obs"]
+    for t in range(1, T):
+        m[:] = rng.integers(0, 32, n)
+        r = o.step(acts[t], obs[t])
+        assert r["stats"][4] == sum(bin(int(v)).count("1") for v in m)
+        for i in range(5):
+            held = (m >> i) & 1 == 1
+            assert np.array_equal(r["out_obs"][held, 4 + 3 * i:7 + 3 * i], prev[held, 4 + 3 * i:7 + 3 * i])
+        prev = r["out_obs"]
+    o.close()
+    o = Oracle(presets.preset(FULL & ~DROPOUT & ~OCCLUSION), n, SEED)
+    o.set_occlusion_mask(np.full(n, 31, np.uint8))
+    o.step(acts[0], obs[0])
+    assert o.step(acts[1], obs[1])["stats"][4] == 0
+    o.close()

@@ -124,3 +124,29 @@ def vision_preset(**overrides) -> dict:
             raise KeyError(f"unknown vision parameter {k!r}")
         p[k] = v
     return p
+
+
+# vision-model training pose augmentation: keep 20 %, rotate 90 deg about a main axis
+# 40 %, jitter position + rotation 40 %.  Jitter stds are not given in the paper (SPEC.md:632's
+# 5 mm / 0.05 rad) -- parity unpinned workload choice.
+POSE_AUG = {"p_keep": 0.2, "p_rot90": 0.4, "pos_std": 5e-3, "rot_std": 0.05}
+
+
+def pose_preset(**overrides) -> dict:
+    p = dict(POSE_AUG)
+    for k, v in overrides.items():
+        if k not in p:
+            raise KeyError(f"unknown pose-augmentation parameter {k!r}")
+        p[k] = v
+    return p
+
+
+def poses(n: int, seed: int = SEED_WORKLOAD):
+    """Seeded object poses [n][7] float32: position around the palm + a uniform unit quaternion."""
+    import numpy as np
+    rng = np.random.default_rng(seed)
+    out = np.empty((n, 7))
+    out[:, 0:3] = np.array([0.0, 0.04, 0.03]) + 0.01 * rng.standard_normal((n, 3))
+    q = rng.standard_normal((n, 4))
+    out[:, 3:7] = q / np.linalg.norm(q, axis=1, keepdims=True)
+    return out.astype(np.float32)
