@@ -215,6 +215,12 @@ int dr_finalize(void);
 /* ---- auxiliaries ---- */
 size_t   dr_workspace_bytes(const dr_params* params, int64_t n_env); /* 0 on invalid input */
 int      dr_set_stream(void* cuda_stream);          /* later calls enqueue on this stream */
+/* Simulator-provided occlusion: occl_mask_dev is a device u8 [n_env]
+ * array whose bit i says fingertip marker i of env e is occluded this step (the simulator's
+ * collision-site rule); with DR_OCCLUSION on it replaces the 15 mm distance rule
+ * (Q13 / Q27).  Every later dr_step reads the array in stream order, so the caller
+ * refreshes its contents before each step.  NULL restores the distance rule. */
+int      dr_set_occlusion_input(const uint8_t* occl_mask_dev);
 int      dr_synchronize(void);                      /* blocking: wait for the library stream */
 const float*  dr_phys_params(void);   /* device [n_env][n_phys] fp32, row-major; valid in stream order */
 int      dr_n_phys(void);

@@ -90,6 +90,30 @@ int dr_image_augment(const dr_vision_params* p, uint64_t seed, uint64_t batch_in
                      const uint8_t* images, int64_t n_images, int32_t height, int32_t width, int32_t channels,
                      float* out, float* img_stats, void* stream);
 
+/* Vision-model training pose augmentation. */
+typedef struct {
+    uint32_t abi_version, struct_size;   /* DR_ABI_VERSION, sizeof(dr_pose_aug_params) */
+    double p_keep;     /* 0.2: "leave the object pose as is with 20% probability" */
+    double p_rot90;    /* 0.4: "rotate the object by 90 deg around its main axes with 40% probability" */
+    double pos_std;    /* 5e-3 m: position jitter per axis (not given in the paper)  [Q28] */
+    double rot_std;    /* 0.05 rad: rotation jitter angle about a uniform axis (not given) */
+} dr_pose_aug_params;
+
+int dr_pose_aug_params_default(dr_pose_aug_params* p);
+
+/* Per sample i (global id sample_offset + i) of batch batch_index, pose_in [n][7] = (position xyz,
+ * unit quaternion wxyz), device fp32:
+ *   branch 0 (p_keep):  pose unchanged;
+ *   branch 1 (p_rot90): q <- q (x) r, r = exactly 90 deg about one of the object's own axes (uniform
+ *                       axis and sign); position unchanged;
+ *   branch 2 (rest):    position + N(0, pos_std^2) per axis and q <- q_j (x) q with q_j an angle
+ *                       N(0, rot_std^2) about a uniform axis ("jitter ... both the position and
+ *                       rotation independently").
+ * The branch is an exact integer decision on one Philox word (channel 0x401).  pose_out [n][7]
+ * device fp32 (may alias pose_in); branch_out [n] device u8 or NULL.  Asynchronous on `stream`. */
+int dr_pose_augment(const dr_pose_aug_params* p, uint64_t seed, uint64_t batch_index, int64_t sample_offset,
+                    const float* pose_in, int64_t n, float* pose_out, uint8_t* branch_out, void* stream);
+
 #ifdef __cplusplus
 }
 #endif

@@ -633,6 +633,12 @@ int dr_finalize(void) {
     return DR_OK;
 }
 
+int dr_set_occlusion_input(const uint8_t* occl_mask_dev) {
+    if (!g_ctx) return fail(DR_ENOTINIT, "dr_set_occlusion_input: no context");
+    g_ctx->p.occl_in = occl_mask_dev;
+    return DR_OK;
+}
+
 int dr_set_stream(void* cuda_stream) {
     if (!g_ctx) return fail(DR_ENOTINIT, "dr_set_stream: no context");
     g_ctx->stream = static_cast<cudaStream_t>(cuda_stream);

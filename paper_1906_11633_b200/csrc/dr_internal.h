@@ -154,6 +154,7 @@ struct DevPtrs {
     double* partials;         // [max_ctas][N_STATS]
     double* stats;            // [2][N_STATS] (internal or caller-owned)
     unsigned long long* ctl;  // [0] = step t, [1] = CTAs done counter, [2] = resets pending
+    const uint8_t* occl_in;   // simulator occlusion bits per env (dr_set_occlusion_input) or NULL
 };
 
 // error / launch bookkeeping shared by every C-ABI entry point (dr_api.cu)

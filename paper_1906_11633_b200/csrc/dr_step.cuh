@@ -335,6 +335,9 @@ __device__ __forceinline__ void env_step(const DevPtrs& p, uint32_t e, bool vali
     constexpr bool kHold = (L == RUNTIME_MASK) || (L & (B_DROPOUT | B_OCCLUSION));
     const bool hold_layers = on<L>(B_DROPOUT) || on<L>(B_OCCLUSION);
 
+    // simulator occlusion bits: issued first so the byte load overlaps the action phases
+    const uint32_t occ_in = (on<L>(B_OCCLUSION) && p.occl_in && valid) ? (uint32_t)__ldg(p.occl_in + e) : 0u;
+
     // ---- S0: scalars ----
     const uint32_t* s0 = pipe.s0();
     const float il = on<L>(B_TIMING) ? ringf(s0, S0_INVLAM) : 0.f;
@@ -529,7 +532,11 @@ __device__ __forceinline__ void env_step(const DevPtrs& p, uint32_t e, bool vali
         }
     }
     uint32_t occ = 0;
-    if (on<L>(B_OCCLUSION) && c_dc.occl_on) {
+    if (on<L>(B_OCCLUSION) && p.occl_in) {
+        // the simulator's own occlusion bits (its collision-site rule) [Q27]
+        occ = occ_in & 0x1Fu;
+        acc.n[K_OCCLUDED] += __popc(occ) & vm;
+    } else if (on<L>(B_OCCLUSION) && c_dc.occl_on) {
         // occlusion: another tip or the object centre strictly closer than r [Q13].
         // The decision is the exactly rounded fp64 ((dx*dx + dy*dy) + dz*dz) < r^2 of the oracle.
         // Fast path: every fp32 op is correctly rounded, so the fp32 sum is within a few ulp

@@ -24,7 +24,7 @@
 
 namespace dr {
 
-enum : uint32_t { CH_IMG_PARAM = 0x201, CH_IMG_NOISE = 0x202, CH_SCENE_CAM = 0x301, CH_SCENE_MAT = 0x302,
+enum : uint32_t { CH_POSE = 0x401, CH_IMG_PARAM = 0x201, CH_IMG_NOISE = 0x202, CH_SCENE_CAM = 0x301, CH_SCENE_MAT = 0x302,
                   CH_SCENE_LIGHT = 0x303 };
 
 constexpr int IMG_THREADS = 256;
@@ -305,6 +305,50 @@ __global__ void scene_draw_kernel(const SceneArgs a, dr_scene_draw* __restrict__
     }
 }
 
+// ---- pose augmentation [Q28]: one thread per sample ----
+struct PoseArgs {
+    unsigned long long t_keep, t_rot;   // floor(p_keep 2^32), floor((p_keep + p_rot90) 2^32)
+    float pos_std, rot_std;
+    uint32_t batch, offset, n;
+    PhiloxKeys keys;
+};
+
+__global__ void pose_augment_kernel(const PoseArgs a, const float* in, float* out,   // may alias
+                                    uint8_t* __restrict__ branch) {
+    const uint32_t k = blockIdx.x * blockDim.x + threadIdx.x;
+    if (k >= a.n) return;
+    const uint32_t g = a.offset + k;
+    float v[7];
+#pragma unroll
+    for (int c = 0; c < 7; ++c) v[c] = in[(size_t)k * 7 + c];
+    const float q[4] = {v[3], v[4], v[5], v[6]};
+    const uint4 w = philox_k(g, a.batch, CH_POSE, 0, a.keys);
+    const int b = ((unsigned long long)w.x < a.t_keep) ? 0 : (((unsigned long long)w.x < a.t_rot) ? 1 : 2);
+    float o[7] = {v[0], v[1], v[2], q[0], q[1], q[2], q[3]};
+    if (b == 1) {
+        // exactly 90 deg about body axis kk / 2 with sign from kk's parity: q (x) r
+        const int kk = (int)(((unsigned long long)w.y * 6ull) >> 32);
+        const float h = 0.70710678118654752f;
+        float r[4] = {h, 0.f, 0.f, 0.f};
+        r[1 + kk / 2] = (kk & 1) ? -h : h;
+        qmul(q, r, o + 3);
+    } else if (b == 2) {
+        const uint4 u = philox_k(g, a.batch, CH_POSE, 1, a.keys);
+        float z0, z1, z2, z3;
+        box_muller(u.x, u.y, z0, z1);
+        box_muller(u.z, u.w, z2, z3);
+        o[0] = v[0] + a.pos_std * z0;
+        o[1] = v[1] + a.pos_std * z1;
+        o[2] = v[2] + a.pos_std * z2;
+        float qj[4];
+        rotation<false>(a.rot_std, philox_k(g, a.batch, CH_POSE, 2, a.keys), qj);
+        qmul(qj, q, o + 3);
+    }
+#pragma unroll
+    for (int c = 0; c < 7; ++c) out[(size_t)k * 7 + c] = o[c];
+    if (branch) branch[k] = (uint8_t)b;
+}
+
 static PhiloxKeys make_keys(uint64_t seed) {
     PhiloxKeys k;
     const uint32_t k0 = (uint32_t)(seed & 0xFFFFFFFFull), k1 = (uint32_t)(seed >> 32);
@@ -390,6 +434,53 @@ int dr_scene_draw_batch(const dr_vision_params* p, uint64_t seed, uint64_t batch
         a, out_dev);
     cudaError_t e = cudaGetLastError();
     if (e != cudaSuccess) return set_error(DR_ECUDA, "scene_draw_kernel: %s", cudaGetErrorString(e));
+    count_launch();
+    return DR_OK;
+}
+
+int dr_pose_aug_params_default(dr_pose_aug_params* p) {
+    if (!p) return set_error(DR_EINVAL, "params: NULL");
+    *p = dr_pose_aug_params{};
+    p->abi_version = DR_ABI_VERSION;
+    p->struct_size = sizeof(dr_pose_aug_params);
+    p->p_keep = 0.2;
+    p->p_rot90 = 0.4;
+    p->pos_std = 5e-3;   // not in the paper, Q28
+    p->rot_std = 0.05;
+    return DR_OK;
+}
+
+int dr_pose_augment(const dr_pose_aug_params* p, uint64_t seed, uint64_t batch_index, int64_t sample_offset,
+                    const float* pose_in, int64_t n, float* pose_out, uint8_t* branch_out, void* stream) {
+    if (!p) return set_error(DR_EINVAL, "pose params: NULL");
+    if (p->abi_version != DR_ABI_VERSION || p->struct_size != sizeof(dr_pose_aug_params))
+        return set_error(DR_EINVAL, "pose params: abi_version / struct_size mismatch");
+    if (!(p->p_keep >= 0.0 && p->p_rot90 >= 0.0 && p->p_keep + p->p_rot90 <= 1.0))
+        return set_error(DR_EINVAL, "p_keep/p_rot90: need p_keep, p_rot90 >= 0 and p_keep + p_rot90 <= 1");
+    if (!(p->pos_std >= 0.0) || !(p->rot_std >= 0.0) || !std::isfinite(p->pos_std) || !std::isfinite(p->rot_std))
+        return set_error(DR_EINVAL, "pos_std/rot_std: must be finite values >= 0");
+    if (n < 0 || sample_offset < 0 || sample_offset + n > (int64_t(1) << 32))
+        return set_error(DR_EINVAL, "n/sample_offset: outside [0, 2^32)");
+    if (n == 0) return DR_OK;
+    if (!pose_in || !pose_out) return set_error(DR_EINVAL, "pose_in/pose_out: NULL");
+    auto thr = [](double q) -> unsigned long long {
+        if (!(q > 0.0)) return 0ull;
+        if (q >= 1.0) return 1ull << 32;
+        return (unsigned long long)std::floor(q * 4294967296.0);
+    };
+    PoseArgs a{};
+    a.t_keep = thr(p->p_keep);
+    a.t_rot = thr(p->p_keep + p->p_rot90);
+    a.pos_std = (float)p->pos_std;
+    a.rot_std = (float)p->rot_std;
+    a.batch = (uint32_t)batch_index;
+    a.offset = (uint32_t)sample_offset;
+    a.n = (uint32_t)n;
+    a.keys = make_keys(seed);
+    pose_augment_kernel<<<(unsigned)((n + 127) / 128), 128, 0, static_cast<cudaStream_t>(stream)>>>(a, pose_in, pose_out,
+                                                                                                     branch_out);
+    cudaError_t e = cudaGetLastError();
+    if (e != cudaSuccess) return set_error(DR_ECUDA, "pose_augment_kernel: %s", cudaGetErrorString(e));
     count_launch();
     return DR_OK;
 }

@@ -103,6 +103,7 @@ def load():
     L.dr_workspace_bytes.argtypes = [C.POINTER(DrParams), C.c_int64]
     L.dr_workspace_bytes.restype = C.c_size_t
     L.dr_set_stream.argtypes = [vp]
+    L.dr_set_occlusion_input.argtypes = [vp]
     L.dr_synchronize.argtypes = []
     L.dr_phys_params.restype = C.c_void_p
     L.dr_n_phys.restype = C.c_int
@@ -121,7 +122,7 @@ def load():
     L.dr_debug_philox.argtypes = [C.c_uint32, C.c_uint32, C.c_uint32, vp]
     L.dr_debug_philox.restype = C.c_int
     for f in ("dr_params_default", "dr_init", "dr_update_params", "dr_reset", "dr_step", "dr_step_substeps", "dr_step_host", "dr_finalize",
-              "dr_set_stream", "dr_synchronize", "dr_set_stats_buffer", "dr_set_step_index",
+              "dr_set_stream", "dr_set_occlusion_input", "dr_synchronize", "dr_set_stats_buffer", "dr_set_step_index",
               "dr_state_export", "dr_state_import", "dr_phys_export"):
         getattr(L, f).restype = C.c_int
     if L.dr_abi_version() != ABI_VERSION:
@@ -252,6 +253,13 @@ def dr_workspace_bytes(params: DrParams, n_env: int) -> int:
 
 def dr_set_stream(stream_handle: int):
     return _check(load().dr_set_stream(C.c_void_p(stream_handle)))
+
+
+def dr_set_occlusion_input(mask=None, n_env=None):
+    """mask: CUDA uint8 [n_env] (bit i = tip i occluded), or None for the distance rule."""
+    import torch
+    m = None if mask is None else _ptr(mask, (n_env,) if n_env else None, torch.uint8, "occl_mask")
+    return _check(load().dr_set_occlusion_input(m))
 
 
 def dr_synchronize():

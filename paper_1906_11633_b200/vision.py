@@ -25,6 +25,11 @@ class DrVisionParams(C.Structure):
     _fields_ = [("abi_version", C.c_uint32), ("struct_size", C.c_uint32)] + _FIELDS
 
 
+class DrPoseAugParams(C.Structure):
+    _fields_ = [("abi_version", C.c_uint32), ("struct_size", C.c_uint32), ("p_keep", C.c_double),
+                ("p_rot90", C.c_double), ("pos_std", C.c_double), ("rot_std", C.c_double)]
+
+
 _ready = False
 
 
@@ -38,7 +43,11 @@ def _lib():
         L.dr_image_augment.argtypes = [C.POINTER(DrVisionParams), C.c_uint64, C.c_uint64, C.c_int64, vp, C.c_int64,
                                        C.c_int32, C.c_int32, C.c_int32, vp, vp, vp]
         L.dr_total_kernel_launches.restype = C.c_uint64
-        for f in ("dr_vision_params_default", "dr_scene_draw_batch", "dr_image_augment"):
+        L.dr_pose_aug_params_default.argtypes = [C.POINTER(DrPoseAugParams)]
+        L.dr_pose_augment.argtypes = [C.POINTER(DrPoseAugParams), C.c_uint64, C.c_uint64, C.c_int64, vp, C.c_int64,
+                                      vp, vp, vp]
+        for f in ("dr_vision_params_default", "dr_scene_draw_batch", "dr_image_augment", "dr_pose_aug_params_default",
+                  "dr_pose_augment"):
             getattr(L, f).restype = C.c_int
         _ready = True
     return L
@@ -99,3 +108,29 @@ def scene_fields(rec):
         "obj_metallic": r[:, 32], "obj_gloss": r[:, 33], "n_lights": r[:, 34].view(np.uint32),
         "light_dir": r[:, 35:53].reshape(-1, 6, 3), "light_intensity": r[:, 53:59], "total_intensity": r[:, 59],
     }
+
+
+def dr_pose_aug_params_default() -> DrPoseAugParams:
+    p = DrPoseAugParams()
+    dr._check(_lib().dr_pose_aug_params_default(C.byref(p)))
+    return p
+
+
+def pose_params_from_preset(preset: dict) -> DrPoseAugParams:
+    p = dr_pose_aug_params_default()
+    for k in ("p_keep", "p_rot90", "pos_std", "rot_std"):
+        if k in preset:
+            setattr(p, k, preset[k])
+    return p
+
+
+def dr_pose_augment(params: DrPoseAugParams, seed: int, batch_index: int, pose_in, pose_out, branch_out=None,
+                    sample_offset: int = 0, stream=None):
+    """pose_in / pose_out: CUDA float32 [n][7]; branch_out: CUDA uint8 [n] or None."""
+    import torch
+    n = pose_in.shape[0]
+    ip = dr._ptr(pose_in, (n, 7), torch.float32, "pose_in")
+    op = dr._ptr(pose_out, (n, 7), torch.float32, "pose_out")
+    bp = dr._ptr(branch_out, (n,), torch.uint8, "branch_out") if branch_out is not None else None
+    return dr._check(_lib().dr_pose_augment(C.byref(params), C.c_uint64(seed), C.c_uint64(batch_index), sample_offset,
+                                            ip, n, op, bp, _stream(stream)))

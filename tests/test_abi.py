@@ -18,8 +18,12 @@ def lib():
 
 
 def _declared_symbols():
-    with open(os.path.join(ROOT, "include", "dr.h")) as f:
-        src = f.read()
+    """Every function declared in include/*.h (dr.h and dr_vision.h)."""
+    import glob
+    src = ""
+    for h in sorted(glob.glob(os.path.join(ROOT, "include", "*.h"))):
+        with open(h) as f:
+            src += f.read()
     src = re.sub(r"/\*.*?\*/", "", src, flags=re.S)
     return sorted(set(re.findall(r"\b(dr_[a-z_]+)\s*\(", src)))
 

@@ -45,7 +45,7 @@ def _oracle(preset, gids, seed=SEED):
 
 
 def run_pair(torch, mask, n_env, T, n_frames=8, resets=None, sample=None, state_every=1,
-             stats=True, seed=SEED, frame_seed=presets.SEED_WORKLOAD, updates=None, **kw):
+             stats=True, seed=SEED, frame_seed=presets.SEED_WORKLOAD, updates=None, occl_masks=None, **kw):
     """Run the GPU on all n_env envs and the oracle on `sample` (default: all); compare every
     step.  `resets`: {t: uint8 mask [n_env]} applied before step t; `updates`: {t: parameter
     overrides} swapped in with dr_update_params / orc_update_params before step t."""
@@ -62,7 +62,16 @@ def run_pair(torch, mask, n_env, T, n_frames=8, resets=None, sample=None, state_
         G = ctx.export()
         compare_records({k: v[gids] for k, v in G.items()}, [orc.env(i) for i in range(len(gids))],
                         phys_g=ctx.phys()[gids], mask=mask)
+        occ_dev = occ_orc = None
+        if occl_masks is not None:   # simulator occlusion bits (dr_set_occlusion_input)
+            from paper_1906_11633_b200 import dr as _dr
+            occ_dev = torch.zeros(n_env, dtype=torch.uint8, device="cuda")
+            _dr.dr_set_occlusion_input(occ_dev, n_env)
+            occ_orc = orc.set_occlusion_mask(np.zeros(len(gids), np.uint8))
         for t in range(T):
+            if occl_masks is not None:
+                occ_dev.copy_(torch.from_numpy(occl_masks[t]))
+                occ_orc[:] = occl_masks[t][gids]
             if updates and t in updates:
                 P = presets.preset(mask, **{**kw, **updates[t]})
                 ctx.update_params(P)
@@ -175,6 +184,18 @@ def test_smoothing_and_substep_backlash(torch_cuda, mask, n):
     variant -- every output incl. the [n][10][20] substep actions, state incl.
     the EMA, and stats, with resets mid-run."""
     run_pair(torch_cuda, mask, n, 20, n_frames=20, resets={9: (np.arange(n) % 3 == 1).astype(np.uint8)})
+
+
+@pytest.mark.parametrize("mask", [FULL, FULL & ~DROPOUT, CFG2 | OCCLUSION, OCCLUSION])
+def test_simulator_occlusion_input(torch_cuda, mask):
+    """the simulator's per-marker occlusion bits replace the distance rule
+    (PAPER.md:66 collision sites) -- random bits every step, hold decisions bit-exact."""
+    n, T = 300, 16
+    rng = np.random.default_rng(7)
+    masks = [(rng.random((n, 5)) < 0.2).astype(np.uint8) @ (1 << np.arange(5, dtype=np.uint8)) for _ in range(T)]
+    masks = [m.astype(np.uint8) for m in masks]
+    run_pair(torch_cuda, mask, n, T, n_frames=T, occl_masks=masks,
+             resets={8: (np.arange(n) % 4 == 0).astype(np.uint8)})
 
 
 def test_update_params_mid_run(torch_cuda):

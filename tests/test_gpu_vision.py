@@ -135,3 +135,29 @@ def test_scene_draw_parity(torch_cuda):
     e = _rel(g[:, idx], o[:, idx], floor[idx])
     assert e.max() <= TOL, (e.max(), idx[np.unravel_index(e.argmax(), e.shape)[1]])
     assert (g[:, 60:64] == 0).all()
+
+
+def test_pose_augment_parity(torch_cuda):
+    """Vision-model pose augmentation for 20,000 samples (offset 5, batch 9): branch
+    bit-exact, poses within 1e-6 (floors 0.1 m, 1); in place (pose_out aliasing pose_in) gives the
+    same bits."""
+    from oracle import oracle as O
+    from paper_1906_11633_b200 import vision
+    torch = torch_cuda
+    P = presets.pose_preset()
+    n = 20000
+    x = presets.poses(n, seed=4)
+    xin = torch.from_numpy(x).cuda()
+    out = torch.empty_like(xin)
+    br = torch.empty(n, dtype=torch.uint8, device="cuda")
+    prm = vision.pose_params_from_preset(P)
+    vision.dr_pose_augment(prm, SEED, 9, xin, out, br, sample_offset=5)
+    torch.cuda.synchronize()
+    o, ob = O.pose_augment(P, SEED, 9, x, offset=5)
+    assert np.array_equal(br.cpu().numpy(), ob)
+    g = out.cpu().numpy()
+    e = _rel(g, o, np.array([0.1] * 3 + [1.0] * 4))
+    assert e.max() <= TOL, e.max()
+    vision.dr_pose_augment(prm, SEED, 9, xin, xin, None, sample_offset=5)
+    torch.cuda.synchronize()
+    assert np.array_equal(xin.cpu().numpy(), g)
