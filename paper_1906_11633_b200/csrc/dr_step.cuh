@@ -74,15 +74,16 @@ __device__ __forceinline__ void l2_prefetch(const void* ptr, uint32_t bytes) {
 }
 
 // Optional TMA bulk L2 prefetch of a tile's record/state blocks + input rows (DR_PREFETCH; A/B).
+// first_item = 2 prefetches only the row-major input rows.
 template <uint32_t L>
 __device__ __forceinline__ void prefetch_tile(const DevPtrs& p, const float* actions, const float* raw_obs,
-                                              uint32_t tile, uint32_t n_env) {
+                                              uint32_t tile, uint32_t n_env, int first_item = 0) {
     const uint32_t e0 = tile * TILE;
     if (e0 >= n_env) return;
     const uint32_t cnt = min((uint32_t)TILE, n_env - e0);
-    for (int item = threadIdx.x; item < 4; item += blockDim.x) {
+    for (int item = first_item + (int)threadIdx.x; item < 4; item += blockDim.x) {
         if (item == 0) l2_prefetch(p.rec + rec_index(e0), REC_STEP_PLANES * TILE * 4u);
-        else if (item == 1) l2_prefetch(p.st + st_index(e0), ST_PLANES * TILE * 4u);
+        else if (item == 1) l2_prefetch(p.st + st_index(e0), (on<L>(B_SMOOTH) ? ST_PLANES : ST_EMA) * TILE * 4u);
         else if (item == 2) l2_prefetch(actions + (size_t)e0 * N_ACT, cnt * N_ACT * 4u);
         else l2_prefetch(raw_obs + (size_t)e0 * OBS_IN, cnt * OBS_IN * 4u);   // rounded down: in bounds
     }
@@ -322,6 +323,21 @@ struct PipeTma {
     __device__ __forceinline__ void obs_done() { release(ph0 + N_PHASES - 1); }
 };
 
+// Backlash gate alpha = 1 - clamp(num / den, 0, 1) with num = |sgn - s|, den = |s' - s| + eps
+// (PAPER.md:107).  s' moves from s towards sgn and is clamped on the rail sgn, so |s' - s| <= num:
+// the ratio is >= 1 (alpha 0) unless num == 0 (s on the rail already: alpha 1) or s' lands on the
+// rail (num < den, den = num + eps): there alpha = 1 - num / (num + eps) = eps / den exactly, which
+// costs one MUFU.RCP instead of a full divide.  (fp32 values near +-1 are >= 6e-8 apart, so
+// 0 < num < eps, where the identity would not hold, cannot occur.)
+__device__ __forceinline__ float rcp_approx(float x) {
+    float r;
+    asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(r) : "f"(x));
+    return r;
+}
+__device__ __forceinline__ float backlash_alpha(float num, float den) {
+    return (num == 0.f) ? 1.f : ((num < den) ? c_dc.eps * rcp_approx(den) : 0.f);
+}
+
 // ---- the per-env transform -------------------------------------------------------------------
 // valid = false only for the lanes past n_env in the tail tile of the TMA kernel: they follow the
 // same path (the ring protocol is warp-synchronous) but store nothing and count nothing.
@@ -462,7 +478,7 @@ __device__ __forceinline__ void env_step(const DevPtrs& p, uint32_t e, bool vali
                 const float d = (an > 0.f) ? dpos[q] : ((an < 0.f) ? dneg[q] : 0.f);
                 const float sp = fminf(fmaxf(s + an * d * dt_env, -1.f), 1.f);
                 const float num = fabsf(sg - s), den = fabsf(sp - s) + c_dc.eps;
-                const float al = (num == 0.f) ? 1.f : ((num < den) ? 1.f - __fdividef(num, den) : 0.f);
+                const float al = backlash_alpha(num, den);
                 out = al * an;
                 n_rail += (sg != 0.f && fabsf(sp) == 1.f && sp != s) ? 1u : 0u;
                 n_a1 += (al == 1.f) ? 1u : 0u;
@@ -490,7 +506,7 @@ __device__ __forceinline__ void env_step(const DevPtrs& p, uint32_t e, bool vali
                     const float s0 = sl[q];
                     const float sp = fminf(fmaxf(s0 + anv[q] * dd[q] * dtk, -1.f), 1.f);
                     const float num = fabsf(sg[q] - s0), den = fabsf(sp - s0) + c_dc.eps;
-                    const float al = (num == 0.f) ? 1.f : ((num < den) ? 1.f - __fdividef(num, den) : 0.f);
+                    const float al = backlash_alpha(num, den);
                     ov[q] = al * anv[q];
                     n_rail += (sg[q] != 0.f && fabsf(sp) == 1.f && sp != s0) ? 1u : 0u;
                     n_a1 += (al == 1.f) ? 1u : 0u;
@@ -983,7 +999,7 @@ __global__ void __launch_bounds__(STEP_THREADS, STEP_MIN_CTAS)
 // ============================================================================================
 // Kernel C (PipeWarp, DR_PIPE=2): warp-cooperative 16-byte cp.async.cg ring.
 // ============================================================================================
-template <uint32_t L>
+template <uint32_t L, int WPF>
 __global__ void __launch_bounds__(STEP_THREADS, STEP_MIN_CTAS)
     step_kernel_warp(const DevPtrs p, const float* __restrict__ actions, const float* __restrict__ raw_obs,
                      float* __restrict__ out_actions, float* __restrict__ out_obs, float* __restrict__ out_dt,
@@ -1005,6 +1021,8 @@ __global__ void __launch_bounds__(STEP_THREADS, STEP_MIN_CTAS)
         const uint32_t e0 = tile * TILE;
         const uint32_t cnt = min((uint32_t)TILE, n_env - e0);
         const bool full = cnt == (uint32_t)TILE;
+        // WPF (A/B): TMA L2 prefetch of the next tile's input rows (1) or of everything it reads (2)
+        if (WPF) prefetch_tile<L>(p, actions, raw_obs, tile + gridDim.x, n_env, WPF == 1 ? 2 : 0);
         __syncthreads();   // previous tile's smem fully stored
         if (full) {
             const float* a = actions + (size_t)e0 * N_ACT;
