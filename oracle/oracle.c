@@ -169,7 +169,10 @@ int orc_occluded(const float* tips15, const float* obj3, double r, int i)
 /* Channels. Step-domain draws use counter word 1 = t,
  * reset-domain draws use counter word 1 = the env's episode index k_e. */
 enum {
-    CH_TIMING = 0x01, CH_ACT_UADD = 0x02, CH_ACT_MULT = 0x03, CH_DROPOUT = 0x04,
+    /* step-domain word channel: words 0-9 substep durations, 10-14 dropout of tips 0-4,
+     * 15 force trigger */
+    CH_STEP = 0x01, W_TIMING = 0, W_DROPOUT = 10, W_FORCE = 15,
+    CH_ACT_UADD = 0x02, CH_ACT_MULT = 0x03,
     CH_TIP_NOISE = 0x05, CH_OBJ_NOISE = 0x06, CH_ROT_NOISE = 0x07, CH_FORCE = 0x08,
     CH_PHYS_U = 0x101, CH_DELAY = 0x102, CH_BACKLASH = 0x103, CH_LAMBDA = 0x104,
     CH_FORCE_P = 0x105, CH_CORR_ACT = 0x106, CH_CORR_TIP = 0x107, CH_MARKER_TIP = 0x108,
@@ -475,7 +478,7 @@ static void step_env(orc_ctx* c, orc_env* e, const float* act, const float* obs,
      *    dt_env = left-to-right sum of the 10 substeps [Q2]. */
     for (j = 0; j < ORC_N_SUB; ++j) {
         if (L & ORC_TIMING)
-            dt[j] = p->dt_base + orc_exponential(draw_word(c, g, t, CH_TIMING, (uint32_t)j), e->lambda);
+            dt[j] = p->dt_base + orc_exponential(draw_word(c, g, t, CH_STEP, (uint32_t)(W_TIMING + j)), e->lambda);
         else
             dt[j] = p->dt_base;
     }
@@ -592,7 +595,7 @@ static void step_env(orc_ctx* c, orc_env* e, const float* act, const float* obs,
          *    a retrigger restarts it. */
         for (i = 0; i < ORC_N_TIPS; ++i) {
             if (L & ORC_DROPOUT) {
-                uint32_t x = draw_word(c, g, t, CH_DROPOUT, (uint32_t)i);
+                uint32_t x = draw_word(c, g, t, CH_STEP, (uint32_t)(W_DROPOUT + i));
                 if ((uint64_t)x < c->t_drop) {
                     e->timer[i] = p->dropout_hold_steps;
                     st[ORC_S_DROP_INIT] += 1.0;
@@ -667,7 +670,7 @@ static void step_env(orc_ctx* c, orc_env* e, const float* act, const float* obs,
     {
         double f[3] = {0.0, 0.0, 0.0};
         if (L & ORC_FORCE) {
-            uint32_t x = draw_word(c, g, t, CH_FORCE, 0);
+            uint32_t x = draw_word(c, g, t, CH_STEP, W_FORCE);
             if (x < e->t_force) {
                 double z0, z1, z2, z3;
                 uint32_t w[4];

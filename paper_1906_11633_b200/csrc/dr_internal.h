@@ -66,7 +66,8 @@ constexpr size_t PLANE = TILE;   // plane stride in words
 
 // Philox channels
 enum : uint32_t {
-    CH_TIMING = 0x01, CH_ACT_UADD = 0x02, CH_ACT_MULT = 0x03, CH_DROPOUT = 0x04,
+    CH_STEP = 0x01,   // 16 step words: substeps 0-9, dropout tips 10-14, force trigger 15
+    CH_ACT_UADD = 0x02, CH_ACT_MULT = 0x03,   // 0x04 retired (dropout words live in CH_STEP)
     CH_TIP_NOISE = 0x05, CH_OBJ_NOISE = 0x06, CH_ROT_NOISE = 0x07, CH_FORCE = 0x08,
     CH_PHYS_U = 0x101, CH_DELAY = 0x102, CH_BACKLASH = 0x103, CH_LAMBDA = 0x104,
     CH_FORCE_P = 0x105, CH_CORR_ACT = 0x106, CH_CORR_TIP = 0x107, CH_MARKER_TIP = 0x108,

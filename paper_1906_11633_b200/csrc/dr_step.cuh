@@ -377,13 +377,17 @@ __device__ __forceinline__ void env_step(const DevPtrs& p, uint32_t e, bool vali
     pipe.s0_done();
 
     // ---- 1. timing: 10 substeps of 8 ms + Exp(lambda); dt_env = sum [Q2] ----
+    // Step-word channel: words 0-9 substeps, 10-14 dropout, 15 force trigger.
+    // Block 2 (words 8-11) is shared by timing and dropout; block 3 by dropout and the force.
     float dt_env;
+    uint2 w_drop01 = make_uint2(0u, 0u);   // words 10, 11
     {
         float d[N_SUB];
         if (on<L>(B_TIMING)) {
 #pragma unroll
             for (int b = 0; b < 3; ++b) {
-                const uint4 w = philox(g, t, CH_TIMING, b);
+                const uint4 w = philox(g, t, CH_STEP, b);
+                if (b == 2) w_drop01 = make_uint2(w.z, w.w);
 #pragma unroll
                 for (int q = 0; q < 4; ++q)
                     if (4 * b + q < N_SUB)
@@ -589,16 +593,21 @@ __device__ __forceinline__ void env_step(const DevPtrs& p, uint32_t e, bool vali
         acc.n[K_OCCLUDED] += __popc(occ) & vm;
     }
     uint32_t masked = 0;
+    uint4 w_step3 = make_uint4(0u, 0u, 0u, 0u);   // step words 12-15 (dropout tips 2-4, force trigger)
     if (kHold && hold_layers) {
         uint32_t nflags = 0, n_init = 0;
         if (on<L>(B_DROPOUT)) {
             // dropout: a 13-step mask starts with probability 1 - exp(-0.2 * 0.08) per step;
             // a retrigger restarts it [Q11]
-            const uint4 w0 = philox(g, t, CH_DROPOUT, 0);
-            const uint32_t x4 = philox(g, t, CH_DROPOUT, 1).x;
+            if (!on<L>(B_TIMING)) {
+                const uint4 w2 = philox(g, t, CH_STEP, 2);
+                w_drop01 = make_uint2(w2.z, w2.w);
+            }
+            w_step3 = philox(g, t, CH_STEP, 3);
+            const uint32_t xs[N_TIPS] = {w_drop01.x, w_drop01.y, w_step3.x, w_step3.y, w_step3.z};
 #pragma unroll
             for (int i = 0; i < N_TIPS; ++i) {
-                const uint32_t x = (i < 4) ? word_of(w0, i) : x4;
+                const uint32_t x = xs[i];
                 uint32_t tm = (flags >> (4 * i)) & 0xFu;
                 if ((unsigned long long)x < c_dc.t_drop) { tm = c_dc.hold_steps; ++n_init; }
                 if (tm > 0u) { masked |= 1u << i; tm -= 1u; }
@@ -694,7 +703,7 @@ __device__ __forceinline__ void env_step(const DevPtrs& p, uint32_t e, bool vali
     //           [Q17, Q18] ----
     float f[3] = {0.f, 0.f, 0.f};
     if (on<L>(B_FORCE)) {
-        const uint32_t x = philox(g, t, CH_FORCE, 0).x;
+        const uint32_t x = on<L>(B_DROPOUT) ? w_step3.w : philox(g, t, CH_STEP, 3).w;   // step word 15
         if (x < tf) {
             const uint4 w = philox(g, t, CH_FORCE, 1);
             float z0, z1, z2, z3;
