@@ -22,6 +22,30 @@
 // register accumulators -> CTA shared-memory reduction -> last-CTA fixed-order fp64 reduction.
 #pragma once
 
+// State write-back policy (A/B): 0 = default write-back stores, 1 = streaming (st.global.cs).
+#ifndef DR_STATE_CS
+#define DR_STATE_CS 0
+#endif
+__device__ __forceinline__ void st_state(uint32_t* p, uint32_t v) {
+#if DR_STATE_CS
+    __stcs(p, v);
+#else
+    *p = v;
+#endif
+}
+// Output store policy (A/B): 1 = streaming (st.global.cs, default), 0 = default write-back.
+#ifndef DR_OUT_CS
+#define DR_OUT_CS 1
+#endif
+template <class T>
+__device__ __forceinline__ void st_out(T* p, T v) {
+#if DR_OUT_CS
+    __stcs(p, v);
+#else
+    *p = v;
+#endif
+}
+
 enum : int { K_DELAYED = 0, K_DROP_INIT, K_MASKED, K_OCCLUDED, K_HELD, K_TRIG, K_RAIL, K_ALPHA1, K_CLAMPS, K_COUNT };
 
 struct Acc {
@@ -447,13 +471,13 @@ __device__ __forceinline__ void env_step(const DevPtrs& p, uint32_t e, bool vali
             if (on<L>(B_SMOOTH)) {
                 // EMA of the policy action before it is applied [Q25]
                 a = c_dc.smooth_keep * ema[q] + c_dc.smooth_c * a;
-                if (valid) S[(ST_EMA + j) * P] = __float_as_uint(a);
+                if (valid) st_state(&S[(ST_EMA + j) * P], __float_as_uint(a));
             }
             float ad = a;
             if (on<L>(B_DELAY)) {
                 // one-step delay of flagged actuators [Q9]
                 if ((dbits >> j) & 1u) ad = prev[q];
-                if (valid) S[(ST_PREV + j) * P] = __float_as_uint(a);
+                if (valid) st_state(&S[(ST_PREV + j) * P], __float_as_uint(a));
             }
             float an = ad;
             if (on<L>(B_ACT_NOISE)) {
@@ -486,7 +510,7 @@ __device__ __forceinline__ void env_step(const DevPtrs& p, uint32_t e, bool vali
                 out = al * an;
                 n_rail += (sg != 0.f && fabsf(sp) == 1.f && sp != s) ? 1u : 0u;
                 n_a1 += (al == 1.f) ? 1u : 0u;
-                if (valid) S[(ST_SLACK + j) * P] = __float_as_uint(sp);
+                if (valid) st_state(&S[(ST_SLACK + j) * P], __float_as_uint(sp));
             }
             s_bl += on<L>(B_SUBSTEP) ? 0.f : fabsf(out - an);
             ov[q] = out;
@@ -521,7 +545,7 @@ __device__ __forceinline__ void env_step(const DevPtrs& p, uint32_t e, bool vali
 #pragma unroll
             for (int q = 0; q < 4; ++q) {
                 s_bl += fabsf(ov[q] - anv[q]);
-                if (valid) S[(ST_SLACK + 4 * b + q) * P] = __float_as_uint(sl[q]);
+                if (valid) st_state(&S[(ST_SLACK + 4 * b + q) * P], __float_as_uint(sl[q]));
             }
         }
         a4p[b] = make_float4(ov[0], ov[1], ov[2], ov[3]);
@@ -578,7 +602,9 @@ __device__ __forceinline__ void env_step(const DevPtrs& p, uint32_t e, bool vali
         }
         if (amb | c_dc.occl_exact_only) {
             const double r2 = c_dc.occl_r2;
+#pragma unroll
             for (int i = 0; i < N_TIPS; ++i) {
+#pragma unroll
                 for (int j = i + 1; j <= N_TIPS; ++j) {
                     if (!c_dc.occl_exact_only && !((amb >> (6 * i + (j - i - 1))) & 1u)) continue;
                     const float* o = (j < N_TIPS) ? &tip[3 * j] : obj;
@@ -616,9 +642,9 @@ __device__ __forceinline__ void env_step(const DevPtrs& p, uint32_t e, bool vali
             acc.n[K_MASKED] += __popc(masked) & vm;
             acc.n[K_DROP_INIT] += n_init & vm;
         }
-        if (valid) S[ST_FLAGS * P] = nflags | HAS_LAST_BIT;
+        if (valid) st_state(&S[ST_FLAGS * P], nflags | HAS_LAST_BIT);
     } else if (on<L>(B_STATEFUL) && fresh) {
-        if (valid) S[ST_FLAGS * P] = 0u;   // clear FRESH (no hold layers: timers / has_last unused)
+        if (valid) st_state(&S[ST_FLAGS * P], 0u);   // clear FRESH (no hold layers: timers / has_last unused)
     }
     const uint32_t hold = (flags & HAS_LAST_BIT) ? (masked | occ) : 0u;
     acc.n[K_HELD] += __popc(hold) & vm;
@@ -660,7 +686,7 @@ __device__ __forceinline__ void env_step(const DevPtrs& p, uint32_t e, bool vali
                 for (int c = 0; c < 3; ++c) tip[3 * i + c] = ro[3 * i + c];   // unchanged: no store
             } else if (valid) {
 #pragma unroll
-                for (int c = 0; c < 3; ++c) S[(ST_LAST + 3 * i + c) * P] = __float_as_uint(tip[3 * i + c]);
+                for (int c = 0; c < 3; ++c) st_state(&S[(ST_LAST + 3 * i + c) * P], __float_as_uint(tip[3 * i + c]));
             }
         }
     }
@@ -715,7 +741,7 @@ __device__ __forceinline__ void env_step(const DevPtrs& p, uint32_t e, bool vali
             ft[2] = ms * z2;
             if (valid) {
 #pragma unroll
-                for (int c = 0; c < 3; ++c) S[(ST_FTRIG + c) * P] = __float_as_uint(ft[c]);
+                for (int c = 0; c < 3; ++c) st_state(&S[(ST_FTRIG + c) * P], __float_as_uint(ft[c]));
             }
             kf = 0;
             acc.n[K_TRIG] += vm & 1u;
@@ -723,10 +749,10 @@ __device__ __forceinline__ void env_step(const DevPtrs& p, uint32_t e, bool vali
             kf = (kf < 65535u) ? kf + 1u : 65535u;
             if (fresh && valid) {   // materialise the zeroed force of a fresh episode
 #pragma unroll
-                for (int c = 0; c < 3; ++c) S[(ST_FTRIG + c) * P] = 0u;
+                for (int c = 0; c < 3; ++c) st_state(&S[(ST_FTRIG + c) * P], 0u);
             }
         }
-        if (valid) S[ST_KF * P] = kf;
+        if (valid) st_state(&S[ST_KF * P], kf);
         const double dec = __ldg(p.dec_tab + (kf & 255u)) * __ldg(p.dec_tab + 256u + (kf >> 8));   // L1-resident
 #pragma unroll
         for (int c = 0; c < 3; ++c) f[c] = (float)((double)ft[c] * dec);
@@ -755,21 +781,21 @@ __device__ __forceinline__ void store_tile(uint32_t e0, uint32_t cnt, int tid, c
         const float4* s4 = reinterpret_cast<const float4*>(s_act);
         float4* a4 = reinterpret_cast<float4*>(out_actions + (size_t)e0 * N_ACT);
 #pragma unroll
-        for (int i = tid; i < TILE * N_ACT / 4; i += STEP_THREADS) __stcs(a4 + i, s4[i]);
+        for (int i = tid; i < TILE * N_ACT / 4; i += STEP_THREADS) st_out(a4 + i, s4[i]);
         const float4* d4s = reinterpret_cast<const float4*>(s_dt);
         float4* d4 = reinterpret_cast<float4*>(out_dt + (size_t)e0 * N_SUB);
 #pragma unroll
-        for (int i = tid; i < TILE * N_SUB / 4; i += STEP_THREADS) __stcs(d4 + i, d4s[i]);
+        for (int i = tid; i < TILE * N_SUB / 4; i += STEP_THREADS) st_out(d4 + i, d4s[i]);
         // out_obs rows (22 floats = 11 float2) read from stride-26 smem rows
         float2* oo = reinterpret_cast<float2*>(out_obs + (size_t)e0 * OBS_OUT);
         for (int i = tid; i < TILE * 11; i += STEP_THREADS) {
             const int r = i / 11, k = i - r * 11;
-            __stcs(oo + i, reinterpret_cast<const float2*>(s_obs + r * OBS_IN)[k]);
+            st_out(oo + i, reinterpret_cast<const float2*>(s_obs + r * OBS_IN)[k]);
         }
         float* of = out_force + (size_t)e0 * 3;
         for (int i = tid; i < TILE * 3; i += STEP_THREADS) {
             const int r = i / 3, k = i - r * 3;
-            __stcs(of + i, s_obs[r * OBS_IN + 22 + k]);
+            st_out(of + i, s_obs[r * OBS_IN + 22 + k]);
         }
     } else {
         for (uint32_t i = tid; i < cnt * N_ACT; i += STEP_THREADS) out_actions[(size_t)e0 * N_ACT + i] = s_act[i];
