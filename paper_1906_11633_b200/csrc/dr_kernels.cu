@@ -126,10 +126,13 @@ void set_step_pipe(int mode) { g_pipe = (mode < 0 || mode > 2) ? 2 : mode; }
 #ifndef DR_WARP_PF
 #define DR_WARP_PF 0
 #endif
+#ifndef DR_WARP_XT
+#define DR_WARP_XT 1   // cross-tile pipelining of S0 / A0 (A/B)
+#endif
 static StepFn step_fn_warp(uint32_t m) {
-    if (m == MASK_FULL) return step_kernel_warp<MASK_FULL, DR_WARP_PF>;
-    if (m == MASK_CFG2) return step_kernel_warp<MASK_CFG2, DR_WARP_PF>;
-    return step_kernel_warp<RUNTIME_MASK, DR_WARP_PF>;
+    if (m == MASK_FULL) return step_kernel_warp<MASK_FULL, DR_WARP_PF, DR_WARP_XT != 0>;
+    if (m == MASK_CFG2) return step_kernel_warp<MASK_CFG2, DR_WARP_PF, DR_WARP_XT != 0>;
+    return step_kernel_warp<RUNTIME_MASK, DR_WARP_PF, DR_WARP_XT != 0>;
 }
 
 template <int PF>

@@ -234,13 +234,18 @@ struct PipeThread {
 // 32-env column segment of a slot with 16-byte cp.async.cg (L1 bypass): one instruction moves 4
 // planes x 128 B (lane l: plane l >> 3, bytes 16 (l & 7)), i.e. 4x fewer LDGSTS and no L1 lines.
 // Lanes read words other lanes copied, so every hand-over is a __syncwarp.
-template <uint32_t L>
+template <uint32_t L, bool XT = false>
 struct PipeWarp {
     uint32_t* slot0;   // s_ring (row 0, column 0)
     uint32_t* slot1;
     const uint32_t* Rw;   // record tile block + this warp's first column
     const uint32_t* Sw;   // state tile block + this warp's first column
     int tid, lane, wcol;  // wcol = 32 * warp
+    // XT (cross-tile pipelining): the next tile's A0 is issued into slot1 once A4 is consumed and its
+    // S0 into slot0 once OB is consumed, so a new tile starts with both phases already landed; the
+    // input rows are then waited for only after the timing section (io_wait).
+    const uint32_t* nRw;  // next tile of this CTA (nullptr: none)
+    const uint32_t* nSw;
     __device__ __forceinline__ void planes(uint32_t* slot, int row, const uint32_t* src, int n) {
         const int sub = 4 * (lane & 7);
         for (int i = 0; i < n; i += 4) {
@@ -248,20 +253,22 @@ struct PipeWarp {
             if (pi < n) cp_async16(slot + (row + pi) * TILE + wcol + sub, src + pi * TILE + sub);
         }
     }
-    __device__ __forceinline__ void issue_s0() {
-        if (on<L>(B_TIMING) || on<L>(B_DELAY) || on<L>(B_FORCE)) planes(slot0, 0, Rw, 4);   // record planes 0..3
-        if (on<L>(B_FORCE)) planes(slot0, S0_FLAGS, Sw + ST_FLAGS * TILE, 5);                // state planes 55..59
-        else if (on<L>(B_STATEFUL)) planes(slot0, S0_FLAGS, Sw + ST_FLAGS * TILE, 1);
+    __device__ __forceinline__ void issue_s0_of(const uint32_t* R, const uint32_t* S) {
+        if (on<L>(B_TIMING) || on<L>(B_DELAY) || on<L>(B_FORCE)) planes(slot0, 0, R, 4);   // record planes 0..3
+        if (on<L>(B_FORCE)) planes(slot0, S0_FLAGS, S + ST_FLAGS * TILE, 5);                // state planes 55..59
+        else if (on<L>(B_STATEFUL)) planes(slot0, S0_FLAGS, S + ST_FLAGS * TILE, 1);
     }
-    __device__ __forceinline__ void issue_act(uint32_t* sl, int b) {
-        if (on<L>(B_DELAY)) planes(sl, 0, Sw + (ST_PREV + 4 * b) * TILE, 4);
+    __device__ __forceinline__ void issue_act_of(uint32_t* sl, int b, const uint32_t* R, const uint32_t* S) {
+        if (on<L>(B_DELAY)) planes(sl, 0, S + (ST_PREV + 4 * b) * TILE, 4);
         if (on<L>(B_BACKLASH)) {
-            planes(sl, 4, Sw + (ST_SLACK + 4 * b) * TILE, 4);
-            planes(sl, 8, Rw + (REC_DNEG + 4 * b) * TILE, 4);
-            planes(sl, 12, Rw + (REC_DPOS + 4 * b) * TILE, 4);
+            planes(sl, 4, S + (ST_SLACK + 4 * b) * TILE, 4);
+            planes(sl, 8, R + (REC_DNEG + 4 * b) * TILE, 4);
+            planes(sl, 12, R + (REC_DPOS + 4 * b) * TILE, 4);
         }
-        if (on<L>(B_ACT_NOISE)) planes(sl, 16, Rw + (REC_CACT + 4 * b) * TILE, 4);
+        if (on<L>(B_ACT_NOISE)) planes(sl, 16, R + (REC_CACT + 4 * b) * TILE, 4);
     }
+    __device__ __forceinline__ void issue_s0() { issue_s0_of(Rw, Sw); }
+    __device__ __forceinline__ void issue_act(uint32_t* sl, int b) { issue_act_of(sl, b, Rw, Sw); }
     __device__ __forceinline__ void issue_obs(uint32_t* sl) {
         if (on<L>(B_OBS_NOISE)) planes(sl, 0, Rw + REC_OFFTIP * TILE, 22);
     }
@@ -271,7 +278,12 @@ struct PipeWarp {
         issue_act(slot0, 1);
         cp_commit();
     }
-    __device__ __forceinline__ void io_wait() {}
+    __device__ __forceinline__ void io_wait() {
+        if constexpr (XT) {   // the tile's input rows (all but the A1 group just committed)
+            cp_wait<1>();
+            __syncthreads();
+        }
+    }
     __device__ __forceinline__ const uint32_t* act(int b) {
         cp_wait<1>();
         __syncwarp();
@@ -282,14 +294,22 @@ struct PipeWarp {
         __syncwarp();
         if (b + 2 < 5) issue_act(sl, b + 2);
         else if (b + 2 == 5) issue_obs(sl);
+        else if (XT && nRw) issue_act_of(slot1, 0, nRw, nSw);   // b == 4: next tile's A0
         cp_commit();
     }
+    // called after the held-reading copies were committed: OB is older than (next A0, held)
     __device__ __forceinline__ const uint32_t* obs() {
-        cp_wait<1>();
+        cp_wait<XT ? 2 : 1>();
         __syncwarp();
         return slot0 + tid;
     }
-    __device__ __forceinline__ void obs_done() {}
+    __device__ __forceinline__ void obs_done() {
+        if constexpr (XT) {   // next tile's S0 into the slot OB just vacated
+            __syncwarp();
+            if (nRw) issue_s0_of(nRw, nSw);
+            cp_commit();
+        }
+    }
 };
 
 // CTA-wide TMA ring: phase ph (counted over this CTA's tiles) lives in slot ph % NS.
@@ -1034,7 +1054,7 @@ __global__ void __launch_bounds__(STEP_THREADS, STEP_MIN_CTAS)
 // ============================================================================================
 // Kernel C (PipeWarp, DR_PIPE=2): warp-cooperative 16-byte cp.async.cg ring.
 // ============================================================================================
-template <uint32_t L, int WPF>
+template <uint32_t L, int WPF, bool XT>
 __global__ void __launch_bounds__(STEP_THREADS, STEP_MIN_CTAS)
     step_kernel_warp(const DevPtrs p, const float* __restrict__ actions, const float* __restrict__ raw_obs,
                      float* __restrict__ out_actions, float* __restrict__ out_obs, float* __restrict__ out_dt,
@@ -1059,30 +1079,52 @@ __global__ void __launch_bounds__(STEP_THREADS, STEP_MIN_CTAS)
         // WPF (A/B): TMA L2 prefetch of the next tile's input rows (1) or of everything it reads (2)
         if (WPF) prefetch_tile<L>(p, actions, raw_obs, tile + gridDim.x, n_env, WPF == 1 ? 2 : 0);
         __syncthreads();   // previous tile's smem fully stored
-        if (full) {
-            const float* a = actions + (size_t)e0 * N_ACT;
-            const float* o = raw_obs + (size_t)e0 * OBS_IN;
+        auto stage = [&]() {   // the row-major input tile -> shared memory (16-byte cp.async)
+            if (full) {
+                const float* a = actions + (size_t)e0 * N_ACT;
+                const float* o = raw_obs + (size_t)e0 * OBS_IN;
 #pragma unroll
-            for (int i = tid; i < TILE * N_ACT / 4; i += STEP_THREADS) cp_async16(s_act + 4 * i, a + 4 * i);
+                for (int i = tid; i < TILE * N_ACT / 4; i += STEP_THREADS) cp_async16(s_act + 4 * i, a + 4 * i);
 #pragma unroll
-            for (int i = tid; i < TILE * OBS_IN / 4; i += STEP_THREADS) cp_async16(s_obs + 4 * i, o + 4 * i);
+                for (int i = tid; i < TILE * OBS_IN / 4; i += STEP_THREADS) cp_async16(s_obs + 4 * i, o + 4 * i);
+            } else {
+                for (uint32_t i = tid; i < cnt * N_ACT; i += STEP_THREADS)
+                    cp_async4(s_act + i, actions + (size_t)e0 * N_ACT + i);
+                for (uint32_t i = tid; i < cnt * OBS_IN; i += STEP_THREADS)
+                    cp_async4(s_obs + i, raw_obs + (size_t)e0 * OBS_IN + i);
+            }
+            cp_commit();
+        };
+        const uint32_t ntile = tile + gridDim.x;
+        const uint32_t en = ntile * TILE;
+        PipeWarp<L, XT> pipe{s_ring, s_ring + RING_W * TILE, p.rec + rec_index(e0) + wcol, p.st + st_index(e0) + wcol,
+                             tid, lane, wcol, (XT && ntile < n_tiles) ? p.rec + rec_index(en) + wcol : nullptr,
+                             (XT && ntile < n_tiles) ? p.st + st_index(en) + wcol : nullptr};
+        if (XT) {
+            // S0 / A0 of this tile were issued by the previous tile (on the first tile: here, ahead
+            // of the staging group); the staging group is waited for in io_wait(), after timing
+            if (tile == blockIdx.x) {
+                pipe.issue_s0();
+                cp_commit();
+                pipe.issue_act(pipe.slot1, 0);
+                cp_commit();
+            }
+            stage();
+            cp_wait<1>();   // S0 and A0 landed; the staging group may still fly
+            __syncwarp();
         } else {
-            for (uint32_t i = tid; i < cnt * N_ACT; i += STEP_THREADS) cp_async4(s_act + i, actions + (size_t)e0 * N_ACT + i);
-            for (uint32_t i = tid; i < cnt * OBS_IN; i += STEP_THREADS) cp_async4(s_obs + i, raw_obs + (size_t)e0 * OBS_IN + i);
+            stage();
+            pipe.issue_s0();                   // S0 -> slot0 (this warp's columns)
+            cp_commit();
+            pipe.issue_act(pipe.slot1, 0);     // A0 -> slot1
+            cp_commit();
+            cp_wait<1>();      // staging + S0
+            __syncthreads();   // everyone's staging copies (and each warp's S0)
         }
-        cp_commit();
-        PipeWarp<L> pipe{s_ring, s_ring + RING_W * TILE, p.rec + rec_index(e0) + wcol, p.st + st_index(e0) + wcol, tid,
-                         lane, wcol};
-        pipe.issue_s0();                   // S0 -> slot0 (this warp's columns)
-        cp_commit();
-        pipe.issue_act(pipe.slot1, 0);     // A0 -> slot1
-        cp_commit();
-        cp_wait<1>();      // staging + S0
-        __syncthreads();   // everyone's staging copies (and each warp's S0)
         const bool mine = (uint32_t)tid < cnt;
         env_step<L>(p, e0 + tid, mine, t, tid, s_act, s_obs, s_dt, out_sub, pipe, acc);
         my_envs += mine ? 1u : 0u;
-        cp_wait<0>();
+        cp_wait<XT ? 1 : 0>();   // XT: the next tile's S0 keeps flying through the store
         __syncthreads();
         store_tile(e0, cnt, tid, s_act, s_obs, s_dt, out_actions, out_obs, out_dt, out_force);
     }
