@@ -203,9 +203,13 @@ int dr_step_substeps(const float* actions, const float* raw_obs, float* out_acti
                      float* out_obs, float* out_dt, float* out_force);
 
 /* End-to-end variant on HOST buffers (same layouts): copies inputs host->device, runs dr_step,
- * copies outputs device->host, all on the library stream through library-owned device buffers.
- * Asynchronous if the host buffers are pinned (cudaHostAlloc / torch pin_memory); the outputs
- * are valid after dr_synchronize(). */
+ * copies outputs device->host through two library-owned device buffer sets.  Pipelined over
+ * consecutive calls: the H2D of call t runs on a library copy stream, the step on the library
+ * stream, the D2H on a second copy stream, ordered by events, so call t+1's upload overlaps call
+ * t's download and compute.  Asynchronous if the host buffers are pinned (cudaHostAlloc / torch
+ * pin_memory): the caller must not modify an input buffer or read an output buffer of a call
+ * until dr_synchronize(), which waits for all three streams.  DR_EINVAL for
+ * DR_SUBSTEP_BACKLASH contexts. */
 int dr_step_host(const float* actions, const float* raw_obs, float* out_actions, float* out_obs,
                  float* out_dt, float* out_force);
 

@@ -74,9 +74,12 @@ struct Ctx {
     int step_grid = 1, reset_grid = 1;
     uint64_t t_host = 0;
     uint64_t launches = 0;
-    // dr_step_host buffers
+    // dr_step_host: double-buffered device I/O, H2D / D2H streams and their events
     float* io = nullptr;
     size_t io_bytes = 0;
+    cudaStream_t s_h2d = nullptr, s_d2h = nullptr;
+    cudaEvent_t ev_h[2] = {nullptr, nullptr}, ev_k[2] = {nullptr, nullptr}, ev_d[2] = {nullptr, nullptr};
+    uint64_t host_calls = 0;
 };
 
 Ctx* g_ctx = nullptr;
@@ -588,6 +591,11 @@ int dr_step_substeps(const float* actions, const float* raw_obs, float* out_acti
     return step_common(actions, raw_obs, out_actions, out_actions_sub, out_obs, out_dt, out_force);
 }
 
+// End-to-end step on host buffers, pipelined over consecutive calls: the H2D copy of call t runs on
+// its own stream into device buffer set t % 2 (after kernel t-2 released it), the kernel waits for
+// that copy and for the D2H of call t-2 (which frees output set t % 2), and the D2H of call t runs
+// on a third stream -- so with back-to-back calls, inputs of t+1 go up while outputs of t come
+// down (PCIe is full duplex) and kernel t+1 computes.
 int dr_step_host(const float* actions, const float* raw_obs, float* out_actions, float* out_obs, float* out_dt,
                  float* out_force) {
     Ctx* c = g_ctx;
@@ -595,29 +603,51 @@ int dr_step_host(const float* actions, const float* raw_obs, float* out_actions,
     if (g_sticky) return fail(DR_ECUDA, "sticky CUDA error: %s", g_err);
     if (!actions || !raw_obs || !out_actions || !out_obs || !out_dt || !out_force)
         return fail(DR_EINVAL, "dr_step_host: NULL buffer");
+    if (c->prm.layer_mask & DR_SUBSTEP_BACKLASH)
+        return fail(DR_EINVAL, "dr_step_host: DR_SUBSTEP_BACKLASH contexts need dr_step_substeps on device buffers");
     const size_t n = (size_t)c->n_env;
     const size_t fa = n * N_ACT, fo = n * OBS_IN, foa = n * N_ACT, foo = n * OBS_OUT, fdt = n * N_SUB, ff = n * 3;
     auto up16 = [](size_t f) { return (f + 3) / 4 * 4; };
-    const size_t total = (up16(fa) + up16(fo) + up16(foa) + up16(foo) + up16(fdt) + up16(ff)) * 4;
+    const size_t set_floats = up16(fa) + up16(fo) + up16(foa) + up16(foo) + up16(fdt) + up16(ff);
     if (!c->io) {
-        CK(cudaMalloc(&c->io, total));
-        c->io_bytes = total;
+        CK(cudaMalloc(&c->io, 2 * set_floats * 4));
+        c->io_bytes = 2 * set_floats * 4;
+        CK(cudaStreamCreateWithFlags(&c->s_h2d, cudaStreamNonBlocking));
+        CK(cudaStreamCreateWithFlags(&c->s_d2h, cudaStreamNonBlocking));
+        for (int i = 0; i < 2; ++i) {
+            CK(cudaEventCreateWithFlags(&c->ev_h[i], cudaEventDisableTiming));
+            CK(cudaEventCreateWithFlags(&c->ev_k[i], cudaEventDisableTiming));
+            CK(cudaEventCreateWithFlags(&c->ev_d[i], cudaEventDisableTiming));
+        }
+        c->host_calls = 0;
     }
-    float* d_a = c->io;
+    const uint64_t t = c->host_calls;
+    const int b = (int)(t & 1u);
+    float* d_a = c->io + (size_t)b * set_floats;
     float* d_o = d_a + up16(fa);
     float* d_oa = d_o + up16(fo);
     float* d_oo = d_oa + up16(foa);
     float* d_dt = d_oo + up16(foo);
     float* d_f = d_dt + up16(fdt);
-    cudaStream_t s = c->stream;
-    CK(cudaMemcpyAsync(d_a, actions, fa * 4, cudaMemcpyHostToDevice, s));
-    CK(cudaMemcpyAsync(d_o, raw_obs, fo * 4, cudaMemcpyHostToDevice, s));
+    // inputs of call t: after kernel t-2 is done reading this set
+    if (t >= 2) CK(cudaStreamWaitEvent(c->s_h2d, c->ev_k[b], 0));
+    CK(cudaMemcpyAsync(d_a, actions, fa * 4, cudaMemcpyHostToDevice, c->s_h2d));
+    CK(cudaMemcpyAsync(d_o, raw_obs, fo * 4, cudaMemcpyHostToDevice, c->s_h2d));
+    CK(cudaEventRecord(c->ev_h[b], c->s_h2d));
+    // the step: after its inputs landed and the outputs of call t-2 left this set
+    CK(cudaStreamWaitEvent(c->stream, c->ev_h[b], 0));
+    if (t >= 2) CK(cudaStreamWaitEvent(c->stream, c->ev_d[b], 0));
     int rc = dr_step(d_a, d_o, d_oa, d_oo, d_dt, d_f);
     if (rc != DR_OK) return rc;
-    CK(cudaMemcpyAsync(out_actions, d_oa, foa * 4, cudaMemcpyDeviceToHost, s));
-    CK(cudaMemcpyAsync(out_obs, d_oo, foo * 4, cudaMemcpyDeviceToHost, s));
-    CK(cudaMemcpyAsync(out_dt, d_dt, fdt * 4, cudaMemcpyDeviceToHost, s));
-    CK(cudaMemcpyAsync(out_force, d_f, ff * 4, cudaMemcpyDeviceToHost, s));
+    CK(cudaEventRecord(c->ev_k[b], c->stream));
+    // outputs of call t
+    CK(cudaStreamWaitEvent(c->s_d2h, c->ev_k[b], 0));
+    CK(cudaMemcpyAsync(out_actions, d_oa, foa * 4, cudaMemcpyDeviceToHost, c->s_d2h));
+    CK(cudaMemcpyAsync(out_obs, d_oo, foo * 4, cudaMemcpyDeviceToHost, c->s_d2h));
+    CK(cudaMemcpyAsync(out_dt, d_dt, fdt * 4, cudaMemcpyDeviceToHost, c->s_d2h));
+    CK(cudaMemcpyAsync(out_force, d_f, ff * 4, cudaMemcpyDeviceToHost, c->s_d2h));
+    CK(cudaEventRecord(c->ev_d[b], c->s_d2h));
+    c->host_calls = t + 1;
     return DR_OK;
 }
 
@@ -625,8 +655,17 @@ int dr_finalize(void) {
     Ctx* c = g_ctx;
     if (!c) return fail(DR_ENOTINIT, "dr_finalize: no context");
     cudaStreamSynchronize(c->stream);
+    if (c->s_h2d) cudaStreamSynchronize(c->s_h2d);
+    if (c->s_d2h) cudaStreamSynchronize(c->s_d2h);
     if (c->owns_ws) cudaFree(c->ws);
     if (c->io) cudaFree(c->io);
+    for (int i = 0; i < 2; ++i) {
+        if (c->ev_h[i]) cudaEventDestroy(c->ev_h[i]);
+        if (c->ev_k[i]) cudaEventDestroy(c->ev_k[i]);
+        if (c->ev_d[i]) cudaEventDestroy(c->ev_d[i]);
+    }
+    if (c->s_h2d) cudaStreamDestroy(c->s_h2d);
+    if (c->s_d2h) cudaStreamDestroy(c->s_d2h);
     delete c;
     g_ctx = nullptr;
     g_sticky = false;
@@ -648,6 +687,8 @@ int dr_set_stream(void* cuda_stream) {
 int dr_synchronize(void) {
     if (!g_ctx) return fail(DR_ENOTINIT, "dr_synchronize: no context");
     CK(cudaStreamSynchronize(g_ctx->stream));
+    if (g_ctx->s_d2h) CK(cudaStreamSynchronize(g_ctx->s_d2h));
+    if (g_ctx->s_h2d) CK(cudaStreamSynchronize(g_ctx->s_h2d));
     return DR_OK;
 }
 

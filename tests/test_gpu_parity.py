@@ -395,6 +395,16 @@ def test_workspace_adoption_and_host_path(torch_cuda):
         for u, v in zip(outs, ref[t]):
             assert np.array_equal(u.numpy(), v)
     ctx.close()
+    # pipelined: three back-to-back calls (copy streams overlapping), one sync at the end
+    ctx = _ctx(P, n)
+    outs3 = [[torch.empty(n, c).pin_memory() for c in (20, 22, 10, 3)] for _ in range(3)]
+    for t in range(3):
+        dr.dr_step_host(ha[t], ho[t], *outs3[t])
+    dr.dr_synchronize()
+    for t in range(3):
+        for u, v in zip(outs3[t], ref[t]):
+            assert np.array_equal(u.numpy(), v), t
+    ctx.close()
 
 
 def test_value_view_isolation_and_invariants_1M(torch_cuda):
