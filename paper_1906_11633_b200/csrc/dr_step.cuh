@@ -880,12 +880,29 @@ __device__ __forceinline__ void reduce_stats(const DevPtrs& p, const Acc& acc, u
     if (*s_last) {
         __threadfence();
         const uint32_t slot = t & 1u;
-        for (int s = wid; s < N_STATS; s += NW) {
-            double sum = 0.0;
-            for (uint32_t b = lane; b < gridDim.x; b += 32) sum += __ldcg(p.partials + (size_t)b * N_STATS + s);
+        // thread (q = warp, s = lane) sums slot s over CTAs b = q, q + NW, ... with 8 independent
+        // accumulators (8 loads in flight per thread: ~G / 256 L2 round trips instead of G / 32),
+        // then the NW warp sums are combined in warp order -- a fixed association, deterministic
+        {
+            double a8[8];
 #pragma unroll
-            for (int o = 16; o > 0; o >>= 1) sum += __shfl_xor_sync(0xFFFFFFFFu, sum, o);
-            if (lane == 0) p.stats[slot * N_STATS + s] = sum;
+            for (int i = 0; i < 8; ++i) a8[i] = 0.0;
+            const uint32_t G = gridDim.x;
+            uint32_t b = (uint32_t)wid;
+            for (; b + 7u * NW < G; b += 8u * NW) {
+#pragma unroll
+                for (int i = 0; i < 8; ++i) a8[i] += __ldcg(p.partials + (size_t)(b + (uint32_t)i * NW) * N_STATS + lane);
+            }
+            for (int i = 0; b < G; b += NW, ++i) a8[i & 7] += __ldcg(p.partials + (size_t)b * N_STATS + lane);
+            const double w = ((a8[0] + a8[1]) + (a8[2] + a8[3])) + ((a8[4] + a8[5]) + (a8[6] + a8[7]));
+            s_red[wid * N_STATS + lane] = w;   // s_red: >= NW * 32 doubles (the CTA scratch)
+        }
+        __syncthreads();
+        if (tid < N_STATS) {
+            double sum = 0.0;
+#pragma unroll
+            for (int q = 0; q < NW; ++q) sum += s_red[q * N_STATS + tid];
+            p.stats[slot * N_STATS + tid] = sum;
         }
         __syncthreads();
         if (tid == 0) {
