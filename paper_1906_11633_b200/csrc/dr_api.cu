@@ -270,7 +270,7 @@ cudaError_t upload_params(Ctx* c, const dr_params& p, const char** what) {
     }
     dc.n_rs_philox = (int)rph.size();
     dc.n_rs_pairs = (int)rpr.size();
-    // physics: v = C0 + C1 * f(A + B x) (dr_internal.h), from the descriptor schema
+    // physics: v = C0 + C1 * f(A + B x) (dr_internal.h), f = 2^(.) for the exp kinds (A, B in log2 units)
     std::vector<float> rphys(MAX_PHYS * 4, 0.f);
     std::vector<uint32_t> rsrc(MAX_PHYS, 0u);
     {
@@ -285,9 +285,9 @@ cudaError_t upload_params(Ctx* c, const dr_params& p, const char** what) {
                 if (on_phys) { A = (float)d.a; B = (float)(d.b - d.a); C0 = 0.f; C1 = (float)d.base; src = SL_PHYS_U * 4 + u; }
                 ++u;
                 break;
-            case DR_PHYS_LOGUNIFORM_SCALE:   // base * exp(ln a + (ln b - ln a) U)
+            case DR_PHYS_LOGUNIFORM_SCALE:   // base * exp(ln a + (ln b - ln a) U) = base * 2^(log2 a + log2(b/a) U)
                 if (on_phys) {
-                    A = (float)std::log(d.a); B = (float)(std::log(d.b) - std::log(d.a)); C0 = 0.f; C1 = (float)d.base;
+                    A = (float)std::log2(d.a); B = (float)(std::log2(d.b) - std::log2(d.a)); C0 = 0.f; C1 = (float)d.base;
                     src = (SL_PHYS_U * 4 + u) | RS_SRC_EXP;
                 }
                 ++u;
@@ -296,8 +296,11 @@ cudaError_t upload_params(Ctx* c, const dr_params& p, const char** what) {
                 if (on_phys) { B = (float)d.a; C0 = (float)d.base; C1 = 1.f; src = (ZB_PHYS + n) | RS_SRC_NORMAL; }
                 ++n;
                 break;
-            case DR_PHYS_MUL_LOGNORMAL:   // base * exp(sigma z)
-                if (on_phys) { B = (float)d.a; C0 = 0.f; C1 = (float)d.base; src = (ZB_PHYS + n) | RS_SRC_NORMAL | RS_SRC_EXP; }
+            case DR_PHYS_MUL_LOGNORMAL:   // base * exp(sigma z) = base * 2^(sigma log2(e) z)
+                if (on_phys) {
+                    B = (float)(d.a * 1.4426950408889634074); C0 = 0.f; C1 = (float)d.base;
+                    src = (ZB_PHYS + n) | RS_SRC_NORMAL | RS_SRC_EXP;
+                }
                 ++n;
                 break;
             default:   // FIXED
@@ -307,7 +310,7 @@ cudaError_t upload_params(Ctx* c, const dr_params& p, const char** what) {
             rphys[4 * i + 1] = B;
             rphys[4 * i + 2] = C0;
             rphys[4 * i + 3] = C1;
-            rsrc[i] = src;
+            rsrc[i] = src | ((on_phys && d.kind != DR_PHYS_FIXED) ? RS_SRC_DRAW : 0u);
         }
     }
     // loguniform force probability quantised to 65,536 midpoints of ln p (Q19)
@@ -506,10 +509,9 @@ int dr_init(const dr_params* params, int64_t n_env, uint64_t seed) {
     const uint32_t n_tiles = (uint32_t)((n_env + TILE - 1) / TILE);
     c->step_grid = (int)std::min<long long>((long long)n_tiles, (long long)c->sm_count * occ_step);
     if (c->step_grid > c->max_ctas) c->step_grid = c->max_ctas;
-    const uint32_t n_chunks = (uint32_t)((n_env + 31) / 32);
-    const int occ_reset = reset_max_ctas_per_sm();
-    c->reset_grid = (int)std::min<long long>((long long)(n_chunks + 7) / 8, (long long)c->sm_count * occ_reset);
-    if (c->reset_grid < 1) c->reset_grid = 1;
+    const char* rv = std::getenv("DR_RESET");
+    set_reset_version(rv ? std::atoi(rv) : 3);
+    c->reset_grid = reset_grid_for((uint32_t)n_env, c->sm_count);
 
     // episode 0 for every env (sampled at the beginning of every episode)
     if ((e = launch_reset(P, nullptr, true, (uint32_t)n_env, c->reset_grid, s)) != cudaSuccess) return bail(e, "reset_kernel");

@@ -103,7 +103,7 @@ struct DevConst {
 // Reset task tables (built on the host at dr_init, staged in shared memory by the reset kernel):
 //   philox task : slot | blk << 8 | channel << 16        (one Philox block per entry)
 //   pair task   : slot | pair << 8 | zbuf_base << 16     (one Box-Muller pair per entry)
-//   phys entry  : float4 (A, B, C0, C1) + src word: v = C0 + C1 * f, f = (exp?) (A + B x), where
+//   phys entry  : float4 (A, B, C0, C1) + src word: v = C0 + C1 * f, f = (exp?) 2^(A + B x) : A + B x, where
 //                 x = U(word src) for uniform kinds or z[src] for normal kinds
 //                 (src bit 31: normal kind, bit 30: exp, bits 0..29: index)
 constexpr int RS_MAX_PHILOX = 161, RS_MAX_PAIRS = 128 + 50;
@@ -134,7 +134,7 @@ enum : int {
     ZB_CO = 352,    // 4 (3 used)
     ZB_COUNT = 356
 };
-constexpr uint32_t RS_SRC_NORMAL = 1u << 31, RS_SRC_EXP = 1u << 30, RS_SRC_IDX = (1u << 30) - 1u;
+constexpr uint32_t RS_SRC_NORMAL = 1u << 31, RS_SRC_EXP = 1u << 30, RS_SRC_DRAW = 1u << 29, RS_SRC_IDX = (1u << 29) - 1u;
 
 // Pointers of the device workspace.
 struct DevPtrs {
@@ -177,6 +177,8 @@ int step_max_ctas_per_sm(uint32_t layer_mask);
 void set_step_prefetch(int mode);
 void set_step_pipe(int mode);
 int reset_max_ctas_per_sm();
+void set_reset_version(int v);
+int reset_grid_for(uint32_t n_env, int sm_count);
 constexpr int RESET_THREADS = 256;
 constexpr int STEP_THREADS = TILE;
 #ifndef DR_STEP_MIN_CTAS

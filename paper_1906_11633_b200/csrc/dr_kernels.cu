@@ -5,6 +5,7 @@
 //   below        : checkpoint export/import, the Philox test hook, and the host launchers.
 #include <cuda_runtime.h>
 
+#include <algorithm>
 #include <cstdint>
 
 #include "dr_device.cuh"
@@ -93,10 +94,28 @@ cudaError_t upload_const(const DevConst& c, cudaStream_t s) {
     return cudaMemcpyToSymbolAsync(c_dc, &c, sizeof(DevConst), 0, cudaMemcpyHostToDevice, s);
 }
 
+// Reset kernel (DR_RESET at dr_init, A/B): 3 = thread per resetting env over a compacted list
+// (reset_kernel_t, default), 2 = warp per resetting env in four lane-parallel phases (reset_kernel).
+static int g_reset_v = 3;
+void set_reset_version(int v) { g_reset_v = (v == 2) ? 2 : 3; }
+
 cudaError_t launch_reset(const DevPtrs& p, const uint8_t* mask, bool first, uint32_t n_env, int grid,
                          cudaStream_t s) {
-    reset_kernel<<<grid, RESET_THREADS, 0, s>>>(p, mask, first ? 1 : 0, n_env);
+    if (g_reset_v == 2) reset_kernel<<<grid, RESET_THREADS, 0, s>>>(p, mask, first ? 1 : 0, n_env);
+    else reset_kernel_t<<<grid, RT_THREADS, 0, s>>>(p, mask, first ? 1 : 0, n_env);
     return cudaGetLastError();
+}
+
+int reset_grid_for(uint32_t n_env, int sm_count) {
+    int n = 0;
+    if (g_reset_v == 2) {
+        if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, reset_kernel, RESET_THREADS, 0) != cudaSuccess || n < 1) n = 1;
+        const long long chunks = (n_env + 31) / 32;
+        return (int)std::max<long long>(1, std::min<long long>((chunks + 7) / 8, (long long)sm_count * n));
+    }
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, reset_kernel_t, RT_THREADS, 0) != cudaSuccess || n < 1) n = 1;
+    const long long ranges = (n_env + RT_RANGE - 1) / RT_RANGE;
+    return (int)std::max<long long>(1, std::min<long long>(ranges, (long long)sm_count * n));
 }
 
 static constexpr uint32_t MASK_FULL = 0xFFu;  // PHYS does not affect the step

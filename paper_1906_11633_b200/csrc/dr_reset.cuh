@@ -11,6 +11,9 @@
 //      x a uniform or a normal and f = exp or identity by descriptor -- written as coalesced
 //      128-byte lines of the row phys[e][*];
 //   D. the episode record fields (cheap arithmetic on the staged draws), one lane per field.
+// reset_kernel_t (the default) instead compacts the resetting envs of a 2,048-env
+// range into a shared-memory list and runs one thread per resetting env over that list: every
+// lane does useful work whatever the mask density, with the same draws and arithmetic.
 // The 60 state planes are not zeroed here: one word (FRESH_BIT in the flags plane) marks the env
 // and the step kernel reads a fresh env's state as zero (dr_internal.h).
 #pragma once
@@ -54,8 +57,10 @@ __device__ __forceinline__ void reset_one(const DevPtrs& p, uint32_t e, uint32_t
         // (with PHYS off, or a FIXED descriptor, the host table is A = B = C1 = 0, C0 = base)
         const uint32_t idx = src & RS_SRC_IDX;
         const float x = (src & RS_SRC_NORMAL) ? zb[idx] : uni(w32[idx]);
+        // exp kinds carry log2(e) in A and B (host table), so the exponential is one MUFU.EX2
+        // (relative error ~2^-22, inside the 1e-6 budget of the |base| floor)
         const float tv = fmaf(d.y, x, d.x);
-        const float v = fmaf(d.w, (src & RS_SRC_EXP) ? expf(tv) : tv, d.z);
+        const float v = fmaf(d.w, (src & RS_SRC_EXP) ? ex2_approx(tv) : tv, d.z);
         prow[q] = v;
         if (q == c_dc.mass_index) R[REC_MASS * P] = __float_as_uint(v);   // the object mass [Q18]
     }
@@ -166,4 +171,218 @@ __global__ void __launch_bounds__(RESET_THREADS) reset_kernel(DevPtrs p, const u
         ep_cur = ep_nxt;
     }
     if (!first && lane == 0 && applied) atomicAdd(&p.ctl[2], (unsigned long long)applied);
+}
+
+// =====================================================================================
+// Thread-per-resetting-env reset (default): per-CTA compaction of the mask, then one thread per
+// env runs the whole episode draw -- physics parameters streamed in descriptor order (a Philox
+// block is drawn when the first parameter of its 4-word group comes up; all lanes are at the same
+// parameter, so the branches are warp-uniform), then the record fields.  Same channels, words and
+// transforms as reset_one / the oracle.
+// =====================================================================================
+constexpr int RT_THREADS = 256;
+constexpr uint32_t RT_RANGE = 2048;   // envs scanned per CTA pass (~205 resetting at 10 %)
+
+__device__ __forceinline__ float sel4(const float z[4], uint32_t r) {
+    return r == 0u ? z[0] : (r == 1u ? z[1] : (r == 2u ? z[2] : z[3]));
+}
+__device__ __forceinline__ uint32_t selw(const uint4 w, uint32_t r) {
+    return r == 0u ? w.x : (r == 1u ? w.y : (r == 2u ? w.z : w.w));
+}
+
+__device__ void reset_env_thread(const DevPtrs& p, uint32_t e, uint32_t k, const float4* s_pd,
+                                 const uint32_t* s_src) {
+    const uint32_t lm = c_dc.layer_mask;
+    constexpr size_t P = PLANE;
+    uint32_t* R = p.rec + rec_index(e);
+    uint32_t* S = p.st + st_index(e);
+    const uint32_t g = c_dc.env_offset + e;
+    // ---- physics [Q20]: v = C0 + C1 f(A + B x) ----
+    {
+        const int np = c_dc.n_phys;
+        float* prow = p.phys + (size_t)e * np;
+        const bool vec = (np & 3) == 0;   // rows are 16-byte aligned: float4 stores
+        uint4 wu = make_uint4(0u, 0u, 0u, 0u);
+        float zn[4] = {0.f, 0.f, 0.f, 0.f};
+        for (int q0 = 0; q0 < np; q0 += 4) {
+            float v4[4];
+#pragma unroll
+            for (int r = 0; r < 4; ++r) {
+                const int q = q0 + r;
+                float v = 0.f;
+                if (q < np) {
+                    const float4 d = s_pd[q];
+                    const uint32_t src = s_src[q];
+                    float x = 0.f;
+                    if (src & RS_SRC_DRAW) {   // warp-uniform: every lane is at parameter q
+                        if (src & RS_SRC_NORMAL) {
+                            const uint32_t n = (src & RS_SRC_IDX) - ZB_PHYS;
+                            if ((n & 3u) == 0u) {
+                                const uint4 w = philox(g, k, CH_PHYS_N, n >> 2);
+                                box_muller(w.x, w.y, zn[0], zn[1]);
+                                box_muller(w.z, w.w, zn[2], zn[3]);
+                            }
+                            x = sel4(zn, n & 3u);
+                        } else {
+                            const uint32_t u = (src & RS_SRC_IDX) - SL_PHYS_U * 4;
+                            if ((u & 3u) == 0u) wu = philox(g, k, CH_PHYS_U, u >> 2);
+                            x = uni(selw(wu, u & 3u));
+                        }
+                    }
+                    const float tv = fmaf(d.y, x, d.x);
+                    v = fmaf(d.w, (src & RS_SRC_EXP) ? ex2_approx(tv) : tv, d.z);
+                    if (q == c_dc.mass_index) R[REC_MASS * P] = __float_as_uint(v);   // the object mass [Q18]
+                    if (!vec) prow[q] = v;
+                }
+                v4[r] = v;
+            }
+            if (vec) reinterpret_cast<float4*>(prow)[q0 >> 2] = make_float4(v4[0], v4[1], v4[2], v4[3]);
+        }
+    }
+    // ---- delay flags ----
+    uint32_t bits = 0u;
+    if (lm & B_DELAY) {
+#pragma unroll
+        for (int b = 0; b < 5; ++b) {
+            const uint4 w = philox(g, k, CH_DELAY, b);
+            const uint32_t ws[4] = {w.x, w.y, w.z, w.w};
+#pragma unroll
+            for (int q = 0; q < 4; ++q) bits |= ((unsigned long long)ws[q] < c_dc.t_delay ? 1u : 0u) << (4 * b + q);
+        }
+    }
+    R[REC_DELAY * P] = bits;
+    // ---- backlash widths [Q7]: normal j -> delta-1_j, 20 + j -> delta+1_j ----
+#pragma unroll 1
+    for (int b = 0; b < 10; ++b) {
+        float z[4] = {0.f, 0.f, 0.f, 0.f};
+        if (lm & B_BACKLASH) {
+            const uint4 w = philox(g, k, CH_BACKLASH, b);
+            box_muller(w.x, w.y, z[0], z[1]);
+            box_muller(w.z, w.w, z[2], z[3]);
+        }
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+            const int n = 4 * b + q;
+            const int j = n < N_ACT ? n : n - N_ACT;
+            const float cal = n < N_ACT ? c_dc.dcal_neg[j] : c_dc.dcal_pos[j];
+            const float dv = (lm & B_BACKLASH) ? fmaxf(0.f, cal + c_dc.jitter * z[q]) : 0.f;
+            R[((n < N_ACT ? REC_DNEG : REC_DPOS) + j) * P] = __float_as_uint(dv);
+        }
+    }
+    // ---- correlated action offset (Table action-noise) ----
+#pragma unroll 1
+    for (int b = 0; b < 5; ++b) {
+        float z[4] = {0.f, 0.f, 0.f, 0.f};
+        if (lm & B_ACT_NOISE) {
+            const uint4 w = philox(g, k, CH_CORR_ACT, b);
+            box_muller(w.x, w.y, z[0], z[1]);
+            box_muller(w.z, w.w, z[2], z[3]);
+        }
+#pragma unroll
+        for (int q = 0; q < 4; ++q) R[(REC_CACT + 4 * b + q) * P] = __float_as_uint(c_dc.sc * z[q]);
+    }
+    // ---- observation offsets [Q14, Q15] ----
+    if (lm & B_OBS_NOISE) {
+        float mb[4];
+        {
+            const uint4 w = philox(g, k, CH_MARKER_BASE, 0);
+            box_muller(w.x, w.y, mb[0], mb[1]);
+            box_muller(w.z, w.w, mb[2], mb[3]);
+        }
+#pragma unroll 1
+        for (int b = 0; b < 4; ++b) {
+            float zc[4], zm[4];
+            const uint4 wc = philox(g, k, CH_CORR_TIP, b);
+            const uint4 wm = philox(g, k, CH_MARKER_TIP, b);
+            box_muller(wc.x, wc.y, zc[0], zc[1]);
+            box_muller(wc.z, wc.w, zc[2], zc[3]);
+            box_muller(wm.x, wm.y, zm[0], zm[1]);
+            box_muller(wm.z, wm.w, zm[2], zm[3]);
+#pragma unroll
+            for (int q = 0; q < 4; ++q) {
+                const int n = 4 * b + q;
+                if (n < 15) {
+                    float v = c_dc.tip_corr * zc[q] + c_dc.tip_marker * zm[q];
+                    if (c_dc.base_to_tips) v = v - c_dc.base_marker * sel4(mb, (uint32_t)(n % 3));
+                    R[(REC_OFFTIP + n) * P] = __float_as_uint(v);
+                }
+            }
+        }
+        float zo[4];
+        const uint4 wo = philox(g, k, CH_CORR_OBJ, 0);
+        box_muller(wo.x, wo.y, zo[0], zo[1]);
+        box_muller(wo.z, wo.w, zo[2], zo[3]);
+#pragma unroll
+        for (int c = 0; c < 3; ++c) R[(REC_COBJ + c) * P] = __float_as_uint(c_dc.obj_corr * zo[c]);
+        float q[4];
+        rotation(c_dc.rot_corr, philox(g, k, CH_CORR_ROT, 0), q);
+#pragma unroll
+        for (int c = 0; c < 4; ++c) R[(REC_QC + c) * P] = __float_as_uint(q[c]);
+    } else {
+#pragma unroll
+        for (int n = 0; n < 18; ++n) R[(REC_OFFTIP + n) * P] = 0u;   // tips 15 + object 3
+        const float q[4] = {1.f, 0.f, 0.f, 0.f};
+#pragma unroll
+        for (int c = 0; c < 4; ++c) R[(REC_QC + c) * P] = __float_as_uint(q[c]);
+    }
+    // ---- timing coefficient lambda ~ U[1250, 10000] ----
+    {
+        float lam = 0.f, il = 0.f;
+        if (lm & B_TIMING) {
+            lam = c_dc.lam_lo + c_dc.lam_range * uni(philox(g, k, CH_LAMBDA, 0).x);
+            il = 1.0f / lam;
+        }
+        R[REC_LAMBDA * P] = __float_as_uint(lam);
+        R[REC_INVLAM * P] = __float_as_uint(il);
+    }
+    // ---- loguniform force probability [Q19]: index + exact integer threshold ----
+    {
+        const uint32_t j = (lm & B_FORCE) ? (philox(g, k, CH_FORCE_P, 0).x >> 16) : 0u;
+        R[REC_PINDEX * P] = j;
+        R[REC_TFORCE * P] = (lm & B_FORCE) ? __ldg(p.t_tab + j) : 0u;
+    }
+    R[REC_EPISODE * P] = k;
+    S[ST_FLAGS * P] = FRESH_BIT;   // state reads as zero at the next step [Q6, Q9]
+}
+
+__global__ void __launch_bounds__(RT_THREADS) reset_kernel_t(DevPtrs p, const uint8_t* __restrict__ mask, int first,
+                                                             uint32_t n_env) {
+    __shared__ float4 s_pd[MAX_PHYS];
+    __shared__ uint32_t s_src[MAX_PHYS];
+    __shared__ uint32_t s_env[RT_RANGE];
+    __shared__ uint32_t s_kk[RT_RANGE];
+    __shared__ uint32_t s_n;
+    const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
+    constexpr int NWR = RT_THREADS / 32;
+    for (int i = tid; i < c_dc.n_phys; i += RT_THREADS) {
+        s_pd[i] = p.rs_phys[i];
+        s_src[i] = p.rs_src[i];
+    }
+    uint32_t applied = 0;
+    for (uint32_t base = blockIdx.x * RT_RANGE; base < n_env; base += gridDim.x * RT_RANGE) {
+        if (tid == 0) s_n = 0u;
+        __syncthreads();
+        // compaction: one coalesced load of 32 mask bytes (and, for the masked lanes, episode
+        // counters) per chunk; warp-aggregated append to the CTA list
+        for (uint32_t c = wid; c < RT_RANGE / 32; c += NWR) {
+            const uint32_t e = base + c * 32u + lane;
+            const bool m = e < n_env && (mask == nullptr || mask[e] != 0);
+            const uint32_t bal = __ballot_sync(0xFFFFFFFFu, m);
+            if (!bal) continue;
+            uint32_t pos0 = 0;
+            if (lane == 0) pos0 = atomicAdd(&s_n, (uint32_t)__popc(bal));
+            pos0 = __shfl_sync(0xFFFFFFFFu, pos0, 0);
+            if (m) {
+                const uint32_t idx = pos0 + __popc(bal & ((1u << lane) - 1u));
+                s_env[idx] = e;
+                s_kk[idx] = first ? 0u : p.rec[rec_index(e) + REC_EPISODE * PLANE] + 1u;
+            }
+            applied += (lane == 0) ? (uint32_t)__popc(bal) : 0u;
+        }
+        __syncthreads();
+        const uint32_t n = s_n;
+        for (uint32_t i = tid; i < n; i += RT_THREADS) reset_env_thread(p, s_env[i], s_kk[i], s_pd, s_src);
+        __syncthreads();
+    }
+    if (!first && applied) atomicAdd(&p.ctl[2], (unsigned long long)applied);
 }
