@@ -198,6 +198,26 @@ def test_simulator_occlusion_input(torch_cuda, mask):
              resets={8: (np.arange(n) % 4 == 0).astype(np.uint8)})
 
 
+@pytest.mark.parametrize("over", [
+    # saturated probabilities, maximal hold, every marker occluded, exact-threshold force
+    dict(delay_prob=1.0, dropout_rate_hz=1e4, dropout_hold_steps=15, occl_dist=0.2, force_p_lo=1.0, force_p_hi=1.0),
+    # nothing fires: zero probabilities / radii, zero hold
+    dict(delay_prob=0.0, dropout_rate_hz=0.0, dropout_hold_steps=0, occl_dist=0.0, force_p_lo=1e-9, force_p_hi=1e-9),
+    # backlash widths near 0 (the jitter clamps ~31 % of them at 0, Q7), heavy action noise (clamps),
+    # a point lambda, zero obs noise
+    dict(delta_cal_neg=[0.05] * 20, delta_cal_pos=[0.05] * 20, act_sigma_uadd=2.0, act_sigma_mult=1.0,
+         act_sigma_cadd=0.5, lambda_lo=3000.0, lambda_hi=3000.0, tip_uncorr=0.0, obj_uncorr=0.0, rot_uncorr=0.0,
+         tip_corr=0.0, obj_corr=0.0, rot_corr=0.0, tip_marker=0.0, base_marker=0.0),
+    # huge backlash widths (every step hits a rail), decay 1 (force never decays), mass-free physics off
+    dict(delta_cal_neg=[50.0] * 20, delta_cal_pos=[80.0] * 20, force_decay_per_step=1.0, force_accel_std=3.0),
+])
+def test_extreme_parameters(torch_cuda, over):
+    """Degenerate and saturated parameter settings of every randomizer (SPEC.md:127 ranges' ends):
+    same parity contract, with resets mid-run."""
+    n = 160
+    run_pair(torch_cuda, FULL, n, 18, n_frames=18, resets={9: (np.arange(n) % 3 == 0).astype(np.uint8)}, **over)
+
+
 def test_update_params_mid_run(torch_cuda):
     """On-the-fly parameter updates: step-draw parameters change from the next
     step, episode-draw parameters at each env's next reset -- identically on both sides."""
@@ -449,3 +469,56 @@ def test_tma_pipeline_variant(torch_cuda, monkeypatch, n, mask):
     including odd tail tiles (hand-loaded raw_obs remainder) and invalid tail lanes."""
     monkeypatch.setenv("DR_PIPE", "1")
     run_pair(torch_cuda, mask, n, 12, n_frames=12, resets={6: (np.arange(n) % 3 == 0).astype(np.uint8)})
+
+
+def test_large_8M_envs_sampled(torch_cuda):
+    """Size edge: 8,388,608 envs (8x config 4, ~20 GB of state + I/O, grid-stride over 65,536 tiles)
+    -- inputs generated on the device, 48 sampled envs (incl. the first and last tiles) compared
+    with the oracle every step, a masked reset of every 7th env in between."""
+    torch = torch_cuda
+    from oracle.oracle import Oracle
+    from paper_1906_11633_b200 import dr
+    P = presets.preset(FULL)
+    n = 1 << 23
+    rng = np.random.default_rng(8)
+    sample = np.sort(np.concatenate([[0, 1, 127, 128, n - 129, n - 2, n - 1], rng.choice(n, 41, replace=False)]))
+    gen_t = torch.Generator(device="cuda").manual_seed(presets.SEED_WORKLOAD)
+    ctx = _ctx(P, n)
+    orc = Oracle(P, len(sample), SEED, gids=sample)
+    idx = torch.from_numpy(sample).cuda()
+    try:
+        for t in range(4):
+            if t == 2:
+                m = (torch.arange(n, device="cuda") % 7 == 3).to(torch.uint8)
+                ctx.reset(m)
+                orc.reset(m[idx].cpu().numpy())
+            k = torch.randint(0, 11, (n, 20), device="cuda", generator=gen_t)
+            A = (-1.0 + (2.0 * k + 1.0) / 11.0).float().contiguous()
+            del k
+            O = torch.empty(n, 26, device="cuda")
+            O[:, 0:15] = torch.tensor(gen.TIP_NOMINAL.reshape(-1), device="cuda", dtype=torch.float32) + \
+                gen.TIP_JITTER * torch.randn(n, 15, device="cuda", generator=gen_t)
+            O[:, 15:18] = torch.tensor(gen.OBJ_NOMINAL, device="cuda", dtype=torch.float32) + \
+                gen.OBJ_JITTER * torch.randn(n, 3, device="cuda", generator=gen_t)
+            q = torch.randn(n, 8, device="cuda", generator=gen_t)
+            O[:, 18:22] = q[:, 0:4] / q[:, 0:4].norm(dim=-1, keepdim=True)
+            O[:, 22:26] = q[:, 4:8] / q[:, 4:8].norm(dim=-1, keepdim=True)
+            del q
+            ctx.step(A, O)
+            r = orc.step(A[idx].cpu().numpy(), O[idx].cpu().numpy(), want_margin=True)
+            torch.cuda.synchronize()
+            knife = KnifeTracker(len(sample))
+            knife.update_before_compare(r["margin"])
+            knife.compare_actions(ctx.out_actions[idx].cpu().numpy(), r["out_actions"], t)
+            compare_obs(ctx.out_obs[idx].cpu().numpy(), r["out_obs"], t)
+            assert_close(f"out_dt t={t}", ctx.out_dt[idx].cpu().numpy(), r["out_dt"], 0.008)
+            mass = np.array([orc.env(i)["mass"] for i in range(len(sample))])
+            assert_close(f"out_force t={t}", ctx.out_force[idx].cpu().numpy(), r["out_force"], mass[:, None])
+            assert ctx.last_stats()[0] == n
+            del A, O
+        for i, gid in enumerate(sample[:: 6]):
+            st = dr.states_to_numpy(dr.dr_state_export(int(gid), int(gid) + 1))
+            assert st["episode"][0] == orc.env(6 * i)["episode"] and st["t_force"][0] == orc.env(6 * i)["t_force"]
+    finally:
+        ctx.close()
+        orc.close()
