@@ -72,6 +72,7 @@ struct Ctx {
     int sm_count = 148;
     int max_ctas = 0;
     int step_grid = 1, reset_grid = 1;
+    int step_mode = 0;
     uint64_t t_host = 0;
     uint64_t launches = 0;
     // dr_step_host: double-buffered device I/O, H2D / D2H streams and their events
@@ -505,9 +506,18 @@ int dr_init(const dr_params* params, int64_t n_env, uint64_t seed) {
     const char* pp = std::getenv("DR_PIPE");
     set_step_prefetch(pf ? std::atoi(pf) : 0);
     set_step_pipe(pp ? std::atoi(pp) : 2);
+    // step mode by the job size (n_env_global, so every shard of a job runs the same kernel and
+    // per-env results stay bit-identical across GPU counts); DR_STEP_MODE=throughput|latency forces
+    const char* sm = std::getenv("DR_STEP_MODE");
+    int mode = (c->prm.n_env_global <= LAT_MAX_ENVS) ? 1 : 0;
+    if (sm && std::strcmp(sm, "throughput") == 0) mode = 0;
+    if (sm && std::strcmp(sm, "latency") == 0) mode = 1;
+    set_step_mode(mode);
+    c->step_mode = mode;
     const int occ_step = step_max_ctas_per_sm(c->prm.layer_mask);
-    const uint32_t n_tiles = (uint32_t)((n_env + TILE - 1) / TILE);
-    c->step_grid = (int)std::min<long long>((long long)n_tiles, (long long)c->sm_count * occ_step);
+    const uint32_t units = mode ? (uint32_t)((n_env + LAT_ENVS_PER_CTA - 1) / LAT_ENVS_PER_CTA)
+                                : (uint32_t)((n_env + TILE - 1) / TILE);
+    c->step_grid = (int)std::min<long long>((long long)units, (long long)c->sm_count * occ_step);
     if (c->step_grid > c->max_ctas) c->step_grid = c->max_ctas;
     const char* rv = std::getenv("DR_RESET");
     set_reset_version(rv ? std::atoi(rv) : 3);
@@ -573,6 +583,7 @@ static int step_common(const float* actions, const float* raw_obs, float* out_ac
         if (!ptrs[i]) return fail(DR_EINVAL, "%s: NULL", names[i]);
         if (!aligned16(ptrs[i])) return fail(DR_EINVAL, "%s: not 16-byte aligned", names[i]);
     }
+    set_step_mode(c->step_mode);
     cudaError_t e = launch_step(c->p, c->prm.layer_mask, actions, raw_obs, out_actions, out_obs, out_dt, out_force,
                                 out_sub, (uint32_t)c->n_env, c->step_grid, c->stream);
     if (e != cudaSuccess) return cuda_fail(e, "step_kernel");

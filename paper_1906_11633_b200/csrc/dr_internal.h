@@ -176,6 +176,10 @@ cudaError_t launch_debug_philox(uint32_t n_env, uint32_t dom, uint32_t ch, uint3
 int step_max_ctas_per_sm(uint32_t layer_mask);
 void set_step_prefetch(int mode);
 void set_step_pipe(int mode);
+void set_step_mode(int mode);   // 0 throughput, 1 latency
+int step_mode();
+constexpr int64_t LAT_MAX_ENVS = 131072;   // latency mode up to this many envs per job (n_env_global)
+constexpr int LAT_ENVS_PER_CTA = 32;
 int reset_max_ctas_per_sm();
 void set_reset_version(int v);
 int reset_grid_for(uint32_t n_env, int sm_count);

@@ -29,6 +29,7 @@ constexpr uint32_t B_STATEFUL = B_DELAY | B_BACKLASH | B_DROPOUT | B_OCCLUSION |
 
 #include "dr_reset.cuh"
 #include "dr_step.cuh"
+#include "dr_step_lat.cuh"
 
 // =====================================================================================
 // Export / import (dr_env_state, 168 words per env).  A FRESH env exports its logical state
@@ -167,9 +168,22 @@ static StepFn step_fn_tma(uint32_t m) {
     return step_kernel_tma<RUNTIME_MASK>;
 }
 
+// Step mode (chosen at dr_init from n_env_global): 0 = throughput (one thread per
+// env, persistent tiles), 1 = latency (8 warps split one 32-env group's transform).
+static int g_step_mode = 0;
+void set_step_mode(int mode) { g_step_mode = mode ? 1 : 0; }
+int step_mode() { return g_step_mode; }
+
+static StepFn step_fn_lat(uint32_t m) {
+    if (m == MASK_FULL) return step_kernel_lat<MASK_FULL>;
+    if (m == MASK_CFG2) return step_kernel_lat<MASK_CFG2>;
+    return step_kernel_lat<RUNTIME_MASK>;
+}
+
 static StepFn step_fn(uint32_t layer_mask) {
     // PHYS does not affect the step; the variants (SMOOTH, SUBSTEP) run the runtime-mask kernel
     const uint32_t m = layer_mask & 0x6FFu;
+    if (g_step_mode == 1) return step_fn_lat(m);
     if (g_pipe == 1) return step_fn_tma(m);
     if (g_pipe == 2) return step_fn_warp(m);
     if (g_prefetch == 0) return step_fn_pf<0>(m);
@@ -177,7 +191,8 @@ static StepFn step_fn(uint32_t layer_mask) {
     return step_fn_pf<1>(m);
 }
 
-static size_t step_dyn_smem() { return g_pipe == 1 ? STEP_TMA_DYN_SMEM : STEP_DYN_SMEM; }
+static size_t step_dyn_smem() { return g_step_mode == 1 ? 0 : (g_pipe == 1 ? STEP_TMA_DYN_SMEM : STEP_DYN_SMEM); }
+static int step_threads() { return g_step_mode == 1 ? LAT_THREADS : STEP_THREADS; }
 
 // the phase ring is dynamic shared memory (static + dynamic > 48 KB needs the opt-in attribute)
 static StepFn step_fn_ready(uint32_t layer_mask) {
@@ -188,7 +203,7 @@ static StepFn step_fn_ready(uint32_t layer_mask) {
 
 int step_max_ctas_per_sm(uint32_t layer_mask) {
     int n = 0;
-    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, step_fn_ready(layer_mask), STEP_THREADS, step_dyn_smem()) !=
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, step_fn_ready(layer_mask), step_threads(), step_dyn_smem()) !=
         cudaSuccess)
         return 1;
     return n > 0 ? n : 1;
@@ -203,7 +218,7 @@ int reset_max_ctas_per_sm() {
 cudaError_t launch_step(const DevPtrs& p, uint32_t layer_mask, const float* actions, const float* raw_obs,
                         float* out_actions, float* out_obs, float* out_dt, float* out_force, float* out_sub,
                         uint32_t n_env, int grid, cudaStream_t s) {
-    step_fn(layer_mask)<<<grid, STEP_THREADS, step_dyn_smem(), s>>>(p, actions, raw_obs, out_actions, out_obs,
+    step_fn(layer_mask)<<<grid, step_threads(), step_dyn_smem(), s>>>(p, actions, raw_obs, out_actions, out_obs,
                                                                     out_dt, out_force, out_sub, n_env);
     return cudaGetLastError();
 }

@@ -832,12 +832,12 @@ __device__ __forceinline__ void store_tile(uint32_t e0, uint32_t cnt, int tid, c
 }
 
 // ---- stats: register accumulators -> CTA reduction -> last-CTA fixed-order reduction ----
-template <uint32_t L>
+template <uint32_t L, int NT = STEP_THREADS>
 __device__ __forceinline__ void reduce_stats(const DevPtrs& p, const Acc& acc, uint32_t my_envs, uint32_t t,
                                              double* s_red, int* s_last) {
     const int tid = threadIdx.x;
     const int lane = tid & 31, wid = tid >> 5;
-    constexpr int NW = STEP_THREADS / 32;
+    constexpr int NW = NT / 32;
     __syncthreads();
     {
         auto red = [&](int i, double x) {
