@@ -178,7 +178,9 @@ void set_step_prefetch(int mode);
 void set_step_pipe(int mode);
 void set_step_mode(int mode);   // 0 throughput, 1 latency
 int step_mode();
-constexpr int64_t LAT_MAX_ENVS = 131072;   // latency mode up to this many envs per job (n_env_global)
+// latency mode up to this many envs per job (n_env_global).  Measured (profiles/round1_notes.md):
+// 4,096 envs 7.3 us vs 9.6 us per step; 65,536 envs 26 us vs 21 us -- so only small jobs
+constexpr int64_t LAT_MAX_ENVS = 16384;
 constexpr int LAT_ENVS_PER_CTA = 32;
 int reset_max_ctas_per_sm();
 void set_reset_version(int v);

@@ -17,9 +17,12 @@
 
 constexpr int LAT_THREADS = 256;
 constexpr int LAT_ENVS = 32;
+#ifndef DR_LAT_MIN_CTAS
+#define DR_LAT_MIN_CTAS 2   // __launch_bounds__ occupancy target (A/B: 3 or 4 spill and run slower)
+#endif
 
 template <uint32_t L>
-__global__ void __launch_bounds__(LAT_THREADS) step_kernel_lat(const DevPtrs p, const float* __restrict__ actions,
+__global__ void __launch_bounds__(LAT_THREADS, DR_LAT_MIN_CTAS) step_kernel_lat(const DevPtrs p, const float* __restrict__ actions,
                                                                const float* __restrict__ raw_obs,
                                                                float* __restrict__ out_actions,
                                                                float* __restrict__ out_obs, float* __restrict__ out_dt,

@@ -20,6 +20,14 @@ def torch_cuda():
     return torch
 
 
+@pytest.fixture(params=["throughput", "latency"], autouse=True)
+def step_mode(request, monkeypatch):
+    """Every parity test runs on both step kernels (DR_STEP_MODE, read at dr_init): the throughput
+    kernel (persistent tiles, one thread per env) and the latency kernel (8 warps per 32 envs)."""
+    monkeypatch.setenv("DR_STEP_MODE", request.param)
+    return request.param
+
+
 @pytest.fixture(autouse=True)
 def _finalize_leaked_context():
     """A failing test must not leave its context behind (dr_init would return DR_EALREADY)."""
