@@ -53,6 +53,8 @@ def parse():
     ap.add_argument("--cpu-sample-envs", type=int, default=65536)
     ap.add_argument("--cpu-sample-steps", type=int, default=24)
     ap.add_argument("--profile", action="store_true", help="short run for ncu (no e2e/cpu legs)")
+    ap.add_argument("--backend", default="nccl", choices=["nccl", "gloo"],
+                    help="process-group backend for N > 1 (gloo: tests that run several ranks on one GPU)")
     ap.add_argument("--graph", type=int, default=-1,
                     help="steps per CUDA graph in the timed region (0 = eager launches; default: 100 for the "
                          "launch-bound small configs at N=1, else 0)")
@@ -229,9 +231,13 @@ def run_vision(args):
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
+    local = local % torch.cuda.device_count()
     torch.cuda.set_device(local)
     if world > 1:
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        if args.backend == "nccl":
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        else:
+            dist.init_process_group("gloo")
     S, NI, H, W, Cc = presets.VISION_BATCH_SAMPLES, presets.VISION_BATCH_SAMPLES * presets.VISION_CAMERAS, \
         presets.VISION_H, presets.VISION_W, presets.VISION_C
     E = H * W * Cc
@@ -359,9 +365,13 @@ def main():
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
+    local = local % torch.cuda.device_count()   # several ranks may share a GPU in tests (gloo)
     torch.cuda.set_device(local)
     if world > 1:
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        if args.backend == "nccl":
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        else:
+            dist.init_process_group("gloo")
     cfg = config_of(args.config, args.n_env)
     cfg["scaling"] = args.scaling
     n_glob = cfg["n"] * world if args.scaling == "weak" else cfg["n"]
