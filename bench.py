@@ -407,13 +407,13 @@ def main():
 
     def one_step(t):
         if reducer is not None:
-            reducer.before_step(t)   # slot t % 2's previous all-reduce is done before it is rewritten
+            reducer.before_step(t)   # the all-reduce of step t-3 is done before step t clears its slot
         if masks is not None:
             ctx.reset(masks[t % 10])
         ctx.step(A[t % F], O[t % F])
         if reducer is not None:
             # the path's one collective: sum of the 32 x fp64 stats of step t over ranks,
-            # on its own stream so it overlaps step t+1 (slot t % 2 is double-buffered)
+            # on its own stream so it overlaps the next steps (stats slots form a ring of 4)
             reducer.after_step(t)
 
     with torch.cuda.stream(lib_stream):

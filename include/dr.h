@@ -228,13 +228,19 @@ int      dr_set_occlusion_input(const uint8_t* occl_mask_dev);
 int      dr_synchronize(void);                      /* blocking: wait for the library stream */
 const float*  dr_phys_params(void);   /* device [n_env][n_phys] fp32, row-major; valid in stream order */
 int      dr_n_phys(void);
-/* Per-step stats (see DR_S_*) of the step with index t land in slot t % 2: device [32] fp64.
- * dr_set_stats_buffer lets the caller own the [2][32] fp64 device buffer (e.g. a torch tensor
- * it all-reduces with NCCL); NULL restores the internal one. */
+/* Per-step stats (see DR_S_*) of the step with index t land in slot t % DR_STAT_SLOTS (a ring of
+ * 4): device [32] fp64, complete when step t's kernel is.  Step t's kernel also clears slot
+ * (t + 1) % 4 for the next step, so a caller all-reducing slot t % 4 (NCCL, overlapped with later
+ * steps) must have finished before step t + 3 is enqueued.  Counts are exact; the moment slots
+ * are sums of per-CTA partials rounded to a power-of-two quantum chosen from n_env_global (so the
+ * order-free fp64 atomic sum is exact and deterministic; ~1e-12 relative).  dr_set_stats_buffer
+ * lets the caller own the [4][32] fp64 device buffer (e.g. a torch tensor it all-reduces with
+ * NCCL); NULL restores the internal one. */
+#define DR_STAT_SLOTS 4
 const double* dr_stats(int slot);
 int      dr_set_stats_buffer(double* dev_buf);
 uint64_t dr_step_index(void);               /* host count of enqueued steps (== device t unless graph-replayed) */
-int      dr_set_step_index(uint64_t t);     /* blocking; for resume */
+int      dr_set_step_index(uint64_t t);     /* blocking; for resume (also clears the stats ring) */
 size_t   dr_state_bytes(void);              /* sizeof(dr_env_state) * n_env */
 /* Blocking copies of per-env state for envs [env_lo, env_hi) (local indices); lo = hi = 0
  * means all envs.  host_dst / host_src hold (hi - lo) dr_env_state records. */

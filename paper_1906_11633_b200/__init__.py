@@ -9,7 +9,7 @@ from . import dr  # noqa: F401
 class DRContext:
     """One libdr context on the current CUDA device (one per process).
 
-    Allocates the output tensors and a caller-owned [2][32] fp64 stats buffer (so NCCL can
+    Allocates the output tensors and a caller-owned [4][32] fp64 stats ring (so NCCL can
     all-reduce it), and passes torch's current stream to the library.  Marshalling only."""
 
     def __init__(self, preset: dict, n_env: int, seed: int, env_offset: int = 0, n_env_global: int = 0,
@@ -33,7 +33,7 @@ class DRContext:
         dr.dr_init(params, self.n, seed)
         self._open = True
         dev = "cuda"
-        self.stats = torch.zeros(2, dr.N_STATS, dtype=torch.float64, device=dev)
+        self.stats = torch.zeros(dr.N_STAT_SLOTS, dr.N_STATS, dtype=torch.float64, device=dev)
         dr.dr_set_stats_buffer(self.stats)
         self.out_actions = torch.empty(self.n, dr.N_ACT, device=dev)
         self.out_obs = torch.empty(self.n, dr.OBS_OUT, device=dev)
@@ -65,7 +65,7 @@ class DRContext:
         """fp64 stats of the most recent step (synchronises)."""
         t = dr.dr_step_index()
         self.stream.synchronize()
-        return self.stats[(t - 1) % 2].cpu().numpy()
+        return self.stats[(t - 1) % dr.N_STAT_SLOTS].cpu().numpy()
 
     def export(self, lo: int = 0, hi: int = 0) -> dict:
         return dr.states_to_numpy(dr.dr_state_export(lo, hi))

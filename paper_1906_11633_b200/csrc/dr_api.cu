@@ -5,6 +5,7 @@
 // There is no CPU fallback: every step of the path runs in the kernels of dr_kernels.cu.
 #include <cuda_runtime.h>
 
+#include <algorithm>
 #include <cmath>
 #include <cstdarg>
 #include <cstdio>
@@ -52,7 +53,7 @@ Layout make_layout(int64_t n_env, int n_phys, int max_ctas) {
     L.rs_src = take(MAX_PHYS * 4);
     L.dec = take(512 * 8);
     L.partials = take((size_t)max_ctas * N_STATS * 8);
-    L.stats = take(2 * N_STATS * 8);
+    L.stats = take(N_STAT_SLOTS * N_STATS * 8);
     L.ctl = take(4 * 8);
     L.total = off;
     return L;
@@ -216,6 +217,33 @@ cudaError_t upload_params(Ctx* c, const dr_params& p, const char** what) {
     dc.accel_std = (float)p.force_accel_std;
     dc.smooth_c = (float)p.act_smooth_coef;
     dc.smooth_keep = (float)(1.0 - p.act_smooth_coef);
+    {
+        // moment slots 16..23: bound each job total (n_env_global x a per-env-step bound x 4) and
+        // round CTA sums to 2^-k with bound * 2^k < 2^52, so fp64 atomic sums are exact
+        double mass_max = 0.0;
+        {
+            const dr_phys_desc& d = p.phys[p.mass_index];
+            const bool on = (p.layer_mask & DR_PHYS) != 0;
+            switch (on ? d.kind : (uint32_t)DR_PHYS_FIXED) {
+            case DR_PHYS_UNIFORM_SCALE: mass_max = d.base * std::max(std::fabs(d.a), std::fabs(d.b)); break;
+            case DR_PHYS_LOGUNIFORM_SCALE: mass_max = d.base * d.b; break;
+            case DR_PHYS_ADD_GAUSS: mass_max = std::fabs(d.base) + 6.0 * d.a; break;
+            case DR_PHYS_MUL_LOGNORMAL: mass_max = d.base * std::exp(6.0 * d.a); break;
+            default: mass_max = std::fabs(d.base); break;
+            }
+        }
+        const double z2 = 36.0;   // |z| <= sqrt(-2 ln 2^-24) < 6
+        const double dtmax = 10.0 * (p.dt_base + 17.0 / p.lambda_lo);
+        const double fmax = mass_max * p.force_accel_std * 6.0;
+        const double per_env[8] = {dtmax, dtmax * dtmax, 40.0, 80.0, 20.0, 20.0 * z2, 15.0 * z2, 3.0 * fmax * fmax};
+        const double ng = (double)(p.n_env_global ? p.n_env_global : c->n_env);
+        for (int i = 0; i < 8; ++i) {
+            const double bound = std::max(ng * per_env[i] * 4.0, 1.0);
+            const int k = 52 - (int)std::ceil(std::log2(bound));
+            dc.mq_scale[i] = std::ldexp(1.0, k);
+            dc.mq_inv[i] = std::ldexp(1.0, -k);
+        }
+    }
     dc.n_phys = p.n_phys;
     dc.mass_index = p.mass_index;
 
@@ -495,7 +523,7 @@ int dr_init(const dr_params* params, int64_t n_env, uint64_t seed) {
     };
     const char* what = "";
     if ((e = upload_params(c, c->prm, &what)) != cudaSuccess) return bail(e, what);
-    if ((e = cudaMemsetAsync(P.stats, 0, 2 * N_STATS * 8, s)) != cudaSuccess) return bail(e, "memset stats");
+    if ((e = cudaMemsetAsync(P.stats, 0, N_STAT_SLOTS * N_STATS * 8, s)) != cudaSuccess) return bail(e, "memset stats");
     if ((e = cudaMemsetAsync(P.ctl, 0, 4 * 8, s)) != cudaSuccess) return bail(e, "memset ctl");
     // state planes start zeroed so that never-reset lanes of a partial tile stay defined
     if ((e = cudaMemsetAsync(P.st, 0, (size_t)ST_PLANES * L.pitch * 4, s)) != cudaSuccess) return bail(e, "memset st");
@@ -709,7 +737,7 @@ const float* dr_phys_params(void) { return g_ctx ? g_ctx->p.phys : nullptr; }
 int dr_n_phys(void) { return g_ctx ? g_ctx->prm.n_phys : 0; }
 
 const double* dr_stats(int slot) {
-    if (!g_ctx || slot < 0 || slot > 1) return nullptr;
+    if (!g_ctx || slot < 0 || slot >= N_STAT_SLOTS) return nullptr;
     return g_ctx->p.stats + slot * N_STATS;
 }
 
@@ -717,6 +745,8 @@ int dr_set_stats_buffer(double* dev_buf) {
     if (!g_ctx) return fail(DR_ENOTINIT, "dr_set_stats_buffer: no context");
     if (dev_buf && ((uintptr_t)dev_buf & 7u)) return fail(DR_EINVAL, "stats buffer: not 8-byte aligned");
     g_ctx->p.stats = dev_buf ? dev_buf : g_ctx->internal_stats;
+    // the ring must start cleared: step t accumulates into slot t % 4 (cleared by step t - 1)
+    CK(cudaMemsetAsync(g_ctx->p.stats, 0, N_STAT_SLOTS * N_STATS * 8, g_ctx->stream));
     return DR_OK;
 }
 
@@ -727,6 +757,7 @@ int dr_set_step_index(uint64_t t) {
     if (!c) return fail(DR_ENOTINIT, "dr_set_step_index: no context");
     unsigned long long v = t;
     CK(cudaMemcpyAsync(c->p.ctl, &v, 8, cudaMemcpyHostToDevice, c->stream));
+    CK(cudaMemsetAsync(c->p.stats, 0, N_STAT_SLOTS * N_STATS * 8, c->stream));   // restart the stats ring
     CK(cudaStreamSynchronize(c->stream));
     c->t_host = t;
     return DR_OK;

@@ -16,6 +16,7 @@ namespace dr {
 
 constexpr int N_ACT = 20, N_TIPS = 5, N_SUB = 10, MAX_PHYS = 256, OBS_IN = 26, OBS_OUT = 22;
 constexpr int N_STATS = 32;
+constexpr int N_STAT_SLOTS = 4;     // stats ring: step t accumulates into slot t % 4 (DESIGN.md §8 "Stats")
 constexpr int TILE = 128;           // envs per CTA tile (one thread per env)
 constexpr uint32_t RUNTIME_MASK = 0xFFFFFFFFu;
 
@@ -95,6 +96,8 @@ struct DevConst {
     uint32_t occl_exact_only;          // r^2 outside the fp32 normal range: always exact fp64
     float accel_std;
     float smooth_c, smooth_keep;       // EMA: a_s <- smooth_keep * a_s + smooth_c * a
+    double mq_scale[8], mq_inv[8];     // moment slots 16..23: CTA sums are rounded to multiples of
+                                       // mq_inv (a power of 2) so the fp64 atomic totals are exact
     int32_t n_phys, mass_index;
     int32_t n_phys_u, n_phys_n;       // counts of uniform-kind / normal-kind params
     int32_t n_rs_philox, n_rs_pairs;  // reset task-table lengths (host-built, layer-dependent)
@@ -153,8 +156,8 @@ struct DevPtrs {
     uint32_t* rs_src;         // [256] physics draw source
     double* dec_tab;          // [512]: 0.99^j (j < 256), then 0.99^(256 i)
     double* partials;         // [max_ctas][N_STATS]
-    double* stats;            // [2][N_STATS] (internal or caller-owned)
-    unsigned long long* ctl;  // [0] = step t, [1] = CTAs done counter, [2] = resets pending
+    double* stats;            // [N_STAT_SLOTS][N_STATS] (internal or caller-owned)
+    unsigned long long* ctl;  // [0] = step t, [1] = CTAs started counter, [2] = resets pending
     const uint8_t* occl_in;   // simulator occlusion bits per env (dr_set_occlusion_input) or NULL
 };
 

@@ -831,10 +831,39 @@ __device__ __forceinline__ void store_tile(uint32_t e0, uint32_t cnt, int tid, c
     }
 }
 
-// ---- stats: register accumulators -> CTA reduction -> last-CTA fixed-order reduction ----
+// ---- step index + stats protocol (no grid-wide tail) ----------------------------------------
+// step_begin: thread 0 reads the step index t and counts its CTA in with an acq_rel atomic; the
+// last CTA to start advances ctl[0] to t + 1 (every CTA read t before counting in) and re-arms the
+// counter.  CTA 0 also clears stats slot (t + 1) % 4 for the next step (its all-reduce, from step
+// t - 3, finished before this step was enqueued: parallel.StatsReducer) and moves the pending reset
+// count into slot t % 4.  At the end every CTA adds its reduced partials into slot t % 4 with fp64
+// atomics -- counts are small integers and the moment sums are rounded per CTA to multiples of a
+// host-chosen power of two, so every partial total is exact and the slot does not depend on the
+// order the atomics land in (deterministic, and identical to a fixed-order sum of the rounded CTA
+// sums).  No fence, no last-CTA pass: the kernel ends when its last tile is stored.
+__device__ __forceinline__ uint32_t step_begin(const DevPtrs& p, uint32_t* s_t) {
+    if (threadIdx.x == 0) {
+        const uint32_t t = (uint32_t)*(volatile unsigned long long*)&p.ctl[0];
+        unsigned long long prev;
+        asm volatile("atom.acq_rel.gpu.global.add.u64 %0, [%1], 1;" : "=l"(prev) : "l"(&p.ctl[1]) : "memory");
+        if (prev == (unsigned long long)gridDim.x - 1ull) {
+            p.ctl[1] = 0ull;
+            *(volatile unsigned long long*)&p.ctl[0] = (unsigned long long)t + 1ull;
+        }
+        if (blockIdx.x == 0) {
+            double* nxt = p.stats + ((t + 1u) % N_STAT_SLOTS) * N_STATS;
+            for (int i = 0; i < N_STATS; ++i) nxt[i] = 0.0;
+            p.stats[(t % N_STAT_SLOTS) * N_STATS + 10] = (double)atomicExch(&p.ctl[2], 0ull);   // resets
+        }
+        *s_t = t;
+    }
+    __syncthreads();
+    return *s_t;
+}
+
 template <uint32_t L, int NT = STEP_THREADS>
 __device__ __forceinline__ void reduce_stats(const DevPtrs& p, const Acc& acc, uint32_t my_envs, uint32_t t,
-                                             double* s_red, int* s_last) {
+                                             double* s_red) {
     const int tid = threadIdx.x;
     const int lane = tid & 31, wid = tid >> 5;
     constexpr int NW = NT / 32;
@@ -856,62 +885,17 @@ __device__ __forceinline__ void reduce_stats(const DevPtrs& p, const Acc& acc, u
         red(8, (double)acc.n[K_ALPHA1]);
         red(9, on<L>(B_BACKLASH) ? (double)my_envs * N_ACT * (on<L>(B_SUBSTEP) ? N_SUB : 1) - (double)acc.n[K_ALPHA1]
                                  : 0.0);
-        red(10, 0.0);
         red(11, (double)acc.n[K_CLAMPS]);
-        red(12, 0.0); red(13, 0.0); red(14, 0.0); red(15, 0.0);
 #pragma unroll
         for (int i = 0; i < 8; ++i) red(16 + i, (double)acc.m[i]);
     }
     __syncthreads();
-    if (tid < N_STATS) {
+    if (tid < 24 && tid != 10 && (tid < 12 || tid >= 16)) {
         double sum = 0.0;
-        if (tid < N_STATS - 8)
 #pragma unroll
-            for (int w = 0; w < NW; ++w) sum += s_red[tid * NW + w];
-        p.partials[(size_t)blockIdx.x * N_STATS + tid] = sum;
-    }
-    __threadfence();
-    __syncthreads();
-    if (tid == 0) {
-        const unsigned long long prev = atomicAdd(&p.ctl[1], 1ull);
-        *s_last = (prev == (unsigned long long)gridDim.x - 1ull);
-    }
-    __syncthreads();
-    if (*s_last) {
-        __threadfence();
-        const uint32_t slot = t & 1u;
-        // thread (q = warp, s = lane) sums slot s over CTAs b = q, q + NW, ... with 8 independent
-        // accumulators (8 loads in flight per thread: ~G / 256 L2 round trips instead of G / 32),
-        // then the NW warp sums are combined in warp order -- a fixed association, deterministic
-        {
-            double a8[8];
-#pragma unroll
-            for (int i = 0; i < 8; ++i) a8[i] = 0.0;
-            const uint32_t G = gridDim.x;
-            uint32_t b = (uint32_t)wid;
-            for (; b + 7u * NW < G; b += 8u * NW) {
-#pragma unroll
-                for (int i = 0; i < 8; ++i) a8[i] += __ldcg(p.partials + (size_t)(b + (uint32_t)i * NW) * N_STATS + lane);
-            }
-            for (int i = 0; b < G; b += NW, ++i) a8[i & 7] += __ldcg(p.partials + (size_t)b * N_STATS + lane);
-            const double w = ((a8[0] + a8[1]) + (a8[2] + a8[3])) + ((a8[4] + a8[5]) + (a8[6] + a8[7]));
-            s_red[wid * N_STATS + lane] = w;   // s_red: >= NW * 32 doubles (the CTA scratch)
-        }
-        __syncthreads();
-        if (tid < N_STATS) {
-            double sum = 0.0;
-#pragma unroll
-            for (int q = 0; q < NW; ++q) sum += s_red[q * N_STATS + tid];
-            p.stats[slot * N_STATS + tid] = sum;
-        }
-        __syncthreads();
-        if (tid == 0) {
-            const unsigned long long res = atomicExch(&p.ctl[2], 0ull);
-            p.stats[slot * N_STATS + 10] = (double)res;
-            p.ctl[1] = 0ull;
-            p.ctl[0] = (unsigned long long)t + 1ull;
-            __threadfence();
-        }
+        for (int w = 0; w < NW; ++w) sum += s_red[tid * NW + w];
+        if (tid >= 16) sum = rint(sum * c_dc.mq_scale[tid - 16]) * c_dc.mq_inv[tid - 16];
+        if (sum != 0.0) atomicAdd(p.stats + (t % N_STAT_SLOTS) * N_STATS + tid, sum);
     }
 }
 
@@ -935,10 +919,10 @@ __global__ void __launch_bounds__(STEP_THREADS, STEP_MIN_CTAS)
     __shared__ __align__(16) float s_obs[TILE * OBS_IN];  // raw_obs in, out_obs + out_force out (stride 26)
     __shared__ __align__(16) float s_dt[TILE * N_SUB];
     extern __shared__ __align__(128) uint32_t s_ring[];   // [2][RING_W][TILE] (dynamic: > 48 KB total)
-    __shared__ int s_last;
 
     const int tid = threadIdx.x;
-    const uint32_t t = (uint32_t)p.ctl[0];
+    __shared__ uint32_t s_tstep;
+    const uint32_t t = step_begin(p, &s_tstep);
     const uint32_t n_tiles = (n_env + TILE - 1) / TILE;
     constexpr size_t P = PLANE;
     if (PF == 2) prefetch_tile<L>(p, actions, raw_obs, blockIdx.x, n_env);
@@ -984,7 +968,7 @@ __global__ void __launch_bounds__(STEP_THREADS, STEP_MIN_CTAS)
         __syncthreads();
         store_tile(e0, cnt, tid, s_act, s_obs, s_dt, out_actions, out_obs, out_dt, out_force);
     }
-    reduce_stats<L>(p, acc, my_envs, t, reinterpret_cast<double*>(s_obs), &s_last);
+    reduce_stats<L>(p, acc, my_envs, t, reinterpret_cast<double*>(s_obs));
 }
 
 // ============================================================================================
@@ -1015,11 +999,11 @@ __global__ void __launch_bounds__(STEP_THREADS, STEP_MIN_CTAS)
     __shared__ __align__(128) float s_obs[TILE * OBS_IN];  // TMA destination; out_obs + out_force in place
     __shared__ __align__(16) float s_dt[TILE * N_SUB];
     __shared__ TmaShared ts;
-    __shared__ int s_last;
     extern __shared__ __align__(128) uint32_t s_ring[];    // [TMA_SLOTS][RING_W][TILE]
 
     const int tid = threadIdx.x;
-    const uint32_t t = (uint32_t)p.ctl[0];
+    __shared__ uint32_t s_tstep;
+    const uint32_t t = step_begin(p, &s_tstep);
     const uint32_t n_tiles = (n_env + TILE - 1) / TILE;
     const uint32_t n_my = (blockIdx.x < n_tiles) ? (n_tiles - blockIdx.x + gridDim.x - 1) / gridDim.x : 0u;
     if (tid == 0) {
@@ -1065,7 +1049,7 @@ __global__ void __launch_bounds__(STEP_THREADS, STEP_MIN_CTAS)
             tma_issue_io<L>(actions, raw_obs, s_act, s_obs, &ts, it + 1, n_my, n_env);
         }
     }
-    reduce_stats<L>(p, acc, my_envs, t, reinterpret_cast<double*>(s_dt), &s_last);
+    reduce_stats<L>(p, acc, my_envs, t, reinterpret_cast<double*>(s_dt));
 }
 
 // ============================================================================================
@@ -1080,10 +1064,10 @@ __global__ void __launch_bounds__(STEP_THREADS, STEP_MIN_CTAS)
     __shared__ __align__(16) float s_obs[TILE * OBS_IN];
     __shared__ __align__(16) float s_dt[TILE * N_SUB];
     extern __shared__ __align__(128) uint32_t s_ring[];   // [2][RING_W][TILE]
-    __shared__ int s_last;
 
     const int tid = threadIdx.x, lane = tid & 31, wcol = tid & ~31;
-    const uint32_t t = (uint32_t)p.ctl[0];
+    __shared__ uint32_t s_tstep;
+    const uint32_t t = step_begin(p, &s_tstep);
     const uint32_t n_tiles = (n_env + TILE - 1) / TILE;
     Acc acc;
     acc_zero(acc);
@@ -1145,5 +1129,5 @@ __global__ void __launch_bounds__(STEP_THREADS, STEP_MIN_CTAS)
         __syncthreads();
         store_tile(e0, cnt, tid, s_act, s_obs, s_dt, out_actions, out_obs, out_dt, out_force);
     }
-    reduce_stats<L>(p, acc, my_envs, t, reinterpret_cast<double*>(s_obs), &s_last);
+    reduce_stats<L>(p, acc, my_envs, t, reinterpret_cast<double*>(s_obs));
 }

@@ -32,10 +32,10 @@ __global__ void __launch_bounds__(LAT_THREADS, DR_LAT_MIN_CTAS) step_kernel_lat(
     __shared__ float s_dtk[N_SUB][LAT_ENVS];
     __shared__ uint32_t s_wd[6][LAT_ENVS];   // step words 10-15
     __shared__ double s_red[N_STATS * (LAT_THREADS / 32)];
-    __shared__ int s_last;
 
     const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
-    const uint32_t t = (uint32_t)p.ctl[0];
+    __shared__ uint32_t s_tstep;
+    const uint32_t t = step_begin(p, &s_tstep);
     constexpr size_t P = PLANE;
     constexpr bool kHold = (L == RUNTIME_MASK) || (L & (B_DROPOUT | B_OCCLUSION));
     const bool hold_layers = on<L>(B_DROPOUT) || on<L>(B_OCCLUSION);
@@ -437,5 +437,5 @@ __global__ void __launch_bounds__(LAT_THREADS, DR_LAT_MIN_CTAS) step_kernel_lat(
             }
         }
     }
-    reduce_stats<L, LAT_THREADS>(p, acc, my_envs, t, s_red, &s_last);
+    reduce_stats<L, LAT_THREADS>(p, acc, my_envs, t, s_red);
 }

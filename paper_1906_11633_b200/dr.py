@@ -17,6 +17,7 @@ LIB_PATH = os.path.join(PKG, "libdr.so")
 _LIB_OVERRIDE = os.environ.get("DR_LIB")
 
 ABI_VERSION = 2
+N_STAT_SLOTS = 4
 N_ACT, N_TIPS, N_SUB, MAX_PHYS, OBS_IN, OBS_OUT, N_STATS = 20, 5, 10, 256, 26, 22, 32
 TIMING, ACT_NOISE, DELAY, BACKLASH, OBS_NOISE = 1, 2, 4, 8, 16
 DROPOUT, OCCLUSION, FORCE, PHYS, ALL = 32, 64, 128, 256, 0x1FF
@@ -280,7 +281,8 @@ def dr_stats(slot: int) -> int:
 
 def dr_set_stats_buffer(buf=None):
     import torch
-    return _check(load().dr_set_stats_buffer(None if buf is None else _ptr(buf, (2, N_STATS), torch.float64, "stats")))
+    return _check(load().dr_set_stats_buffer(None if buf is None else _ptr(buf, (N_STAT_SLOTS, N_STATS), torch.float64,
+                                                                           "stats")))
 
 
 def dr_step_index() -> int:

@@ -5,7 +5,7 @@ global ids [offset_r, offset_r + n_r) and runs its own libdr context with env_of
 offset_r and n_env_global = N (same seed).  Philox counters use global ids, so every env's
 outputs are bit-identical for any W.  The only exchange is the per-step statistics vector
 (32 x fp64 = 256 B), summed over ranks with one all-reduce on a dedicated comm stream so it
-overlaps the next step (slot t % 2 is double-buffered).  Plumbing only: no arithmetic of the
+overlaps the next steps (a ring of 4 stats slots).  Plumbing only: no arithmetic of the
 method lives here.
 """
 from __future__ import annotations
@@ -30,10 +30,12 @@ def stats_all_reduce(stats_slot, group=None, async_op: bool = False):
 class StatsReducer:
     """The overlapped per-step stats all-reduce on a dedicated comm stream.
 
-    Step t's kernel writes slot t % 2; the all-reduce of slot t % 2 runs on the comm stream after
-    an event recorded behind step t, so it overlaps step t+1.  Before step t+2 overwrites that
-    slot, the library stream waits for the all-reduce's completion event (``before_step``), so
-    the double buffer is never raced."""
+    Step t's kernel accumulates into stats slot t % 4 and clears slot (t + 1) % 4 (include/dr.h).
+    The all-reduce of slot t % 4 runs on the comm stream after an event recorded behind step t,
+    so it overlaps the following steps; before step t is enqueued, the library stream waits for
+    the all-reduce of step t - 3 (whose slot step t clears), so the ring is never raced."""
+
+    SLOTS = 4
 
     def __init__(self, stats, lib_stream, group=None):
         import torch
@@ -41,10 +43,10 @@ class StatsReducer:
         self.lib_stream = lib_stream
         self.comm_stream = torch.cuda.Stream()
         self.group = group
-        self.done = [None, None]
+        self.done = [None] * self.SLOTS
 
     def before_step(self, t: int):
-        ev = self.done[t % 2]
+        ev = self.done[(t + 1) % self.SLOTS]   # the all-reduce of step t - 3
         if ev is not None:
             self.lib_stream.wait_event(ev)
 
@@ -54,10 +56,10 @@ class StatsReducer:
         ev.record(self.lib_stream)
         self.comm_stream.wait_event(ev)
         with torch.cuda.stream(self.comm_stream):
-            stats_all_reduce(self.stats[t % 2], group=self.group)
+            stats_all_reduce(self.stats[t % self.SLOTS], group=self.group)
         done = torch.cuda.Event()
         done.record(self.comm_stream)
-        self.done[t % 2] = done
+        self.done[t % self.SLOTS] = done
 
     def sync(self):
         self.lib_stream.wait_stream(self.comm_stream)

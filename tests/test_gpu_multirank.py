@@ -49,7 +49,7 @@ def _run(torch, ctx_factory, off, n, reducer_factory=None):
         if red:
             red.sync()
         torch.cuda.synchronize()
-        stats.append(ctx.stats[t % 2].cpu().numpy().copy())
+        stats.append(ctx.stats[t % 4].cpu().numpy().copy())
     ctx.close()
     return np.stack(outs), np.stack(stats)
 
