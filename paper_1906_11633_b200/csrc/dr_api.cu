@@ -21,7 +21,7 @@ using namespace dr;
 namespace {
 
 struct Layout {
-    size_t rec, st, phys, pd_kr, pd_a, pd_b, pd_base, t_tab, rs_philox, rs_pairs, rs_phys, rs_src, dec, partials,
+    size_t rec, st, phys, pd_kr, pd_a, pd_b, pd_base, t_tab, rs_philox, rs_pairs, rs_phys, rs_src, dec,
         stats, ctl, total;
     uint64_t pitch;
 };
@@ -52,7 +52,6 @@ Layout make_layout(int64_t n_env, int n_phys, int max_ctas) {
     L.rs_phys = take(MAX_PHYS * 16);
     L.rs_src = take(MAX_PHYS * 4);
     L.dec = take(512 * 8);
-    L.partials = take((size_t)max_ctas * N_STATS * 8);
     L.stats = take(N_STAT_SLOTS * N_STATS * 8);
     L.ctl = take(4 * 8);
     L.total = off;
@@ -510,7 +509,6 @@ int dr_init(const dr_params* params, int64_t n_env, uint64_t seed) {
     P.rs_phys = reinterpret_cast<float4*>(c->ws + L.rs_phys);
     P.rs_src = reinterpret_cast<uint32_t*>(c->ws + L.rs_src);
     P.dec_tab = reinterpret_cast<double*>(c->ws + L.dec);
-    P.partials = reinterpret_cast<double*>(c->ws + L.partials);
     P.stats = reinterpret_cast<double*>(c->ws + L.stats);
     P.ctl = reinterpret_cast<unsigned long long*>(c->ws + L.ctl);
     c->internal_stats = P.stats;

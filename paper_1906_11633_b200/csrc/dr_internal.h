@@ -155,7 +155,6 @@ struct DevPtrs {
     float4* rs_phys;          // [256] physics coefficients
     uint32_t* rs_src;         // [256] physics draw source
     double* dec_tab;          // [512]: 0.99^j (j < 256), then 0.99^(256 i)
-    double* partials;         // [max_ctas][N_STATS]
     double* stats;            // [N_STAT_SLOTS][N_STATS] (internal or caller-owned)
     unsigned long long* ctl;  // [0] = step t, [1] = CTAs started counter, [2] = resets pending
     const uint8_t* occl_in;   // simulator occlusion bits per env (dr_set_occlusion_input) or NULL
