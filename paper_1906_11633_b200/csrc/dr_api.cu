@@ -21,7 +21,7 @@ using namespace dr;
 namespace {
 
 struct Layout {
-    size_t rec, st, phys, rlist, pd_kr, pd_a, pd_b, pd_base, t_tab, rs_philox, rs_pairs, rs_phys, rs_src, dec,
+    size_t rec, st, phys, pd_kr, pd_a, pd_b, pd_base, t_tab, rs_philox, rs_pairs, rs_phys, rs_src, dec,
         stats, ctl, total;
     uint64_t pitch;
 };
@@ -42,7 +42,6 @@ Layout make_layout(int64_t n_env, int n_phys, int max_ctas) {
     L.rec = take((size_t)REC_PLANES * L.pitch * 4);   // [n_tiles][REC_PLANES][TILE]
     L.st = take((size_t)ST_PLANES * L.pitch * 4);     // [n_tiles][ST_PLANES][TILE]
     L.phys = take((size_t)n_env * n_phys * 4);
-    L.rlist = take((size_t)n_env * 8);                 // reset list (env, episode) pairs
     L.pd_kr = take(MAX_PHYS * 4);
     L.pd_a = take(MAX_PHYS * 4);
     L.pd_b = take(MAX_PHYS * 4);
@@ -54,7 +53,7 @@ Layout make_layout(int64_t n_env, int n_phys, int max_ctas) {
     L.rs_src = take(MAX_PHYS * 4);
     L.dec = take(512 * 8);
     L.stats = take(N_STAT_SLOTS * N_STATS * 8);
-    L.ctl = take(8 * 8);
+    L.ctl = take(4 * 8);
     L.total = off;
     return L;
 }
@@ -372,11 +371,7 @@ cudaError_t upload_params(Ctx* c, const dr_params& p, const char** what) {
     if (!rpr.empty() && (e = cudaMemcpyAsync(P.rs_pairs, rpr.data(), rpr.size() * 4, cudaMemcpyHostToDevice, s)) != cudaSuccess)
         { *what = "memcpy rs_pairs"; return e; };
     if ((e = cudaMemcpyAsync(P.rs_phys, rphys.data(), MAX_PHYS * 16, cudaMemcpyHostToDevice, s)) != cudaSuccess) { *what = "memcpy rs_phys"; return e; };
-    if ((e = cudaMemcpyAsync(P.rs_src, rsrc.data(), MAX_PHYS * 4, cudaMemcpyHostToDevice, s)) != cudaSuccess) { *what = "memcpy rs_src"; return e; }
-    if ((e = upload_reset_tables(reinterpret_cast<const float4*>(rphys.data()), rsrc.data(), s)) != cudaSuccess) {
-        *what = "upload_reset_tables";
-        return e;
-    };
+    if ((e = cudaMemcpyAsync(P.rs_src, rsrc.data(), MAX_PHYS * 4, cudaMemcpyHostToDevice, s)) != cudaSuccess) { *what = "memcpy rs_src"; return e; };
     if ((e = cudaMemcpyAsync(P.dec_tab, dec.data(), 512 * 8, cudaMemcpyHostToDevice, s)) != cudaSuccess) { *what = "memcpy dec"; return e; };
     return cudaSuccess;
 }
@@ -504,7 +499,6 @@ int dr_init(const dr_params* params, int64_t n_env, uint64_t seed) {
     P.rec = reinterpret_cast<uint32_t*>(c->ws + L.rec);
     P.st = reinterpret_cast<uint32_t*>(c->ws + L.st);
     P.phys = reinterpret_cast<float*>(c->ws + L.phys);
-    P.rlist = reinterpret_cast<uint2*>(c->ws + L.rlist);
     P.pd_kind_rank = reinterpret_cast<uint32_t*>(c->ws + L.pd_kr);
     P.pd_a = reinterpret_cast<float*>(c->ws + L.pd_a);
     P.pd_b = reinterpret_cast<float*>(c->ws + L.pd_b);
@@ -528,7 +522,7 @@ int dr_init(const dr_params* params, int64_t n_env, uint64_t seed) {
     const char* what = "";
     if ((e = upload_params(c, c->prm, &what)) != cudaSuccess) return bail(e, what);
     if ((e = cudaMemsetAsync(P.stats, 0, N_STAT_SLOTS * N_STATS * 8, s)) != cudaSuccess) return bail(e, "memset stats");
-    if ((e = cudaMemsetAsync(P.ctl, 0, 8 * 8, s)) != cudaSuccess) return bail(e, "memset ctl");
+    if ((e = cudaMemsetAsync(P.ctl, 0, 4 * 8, s)) != cudaSuccess) return bail(e, "memset ctl");
     // state planes start zeroed so that never-reset lanes of a partial tile stay defined
     if ((e = cudaMemsetAsync(P.st, 0, (size_t)ST_PLANES * L.pitch * 4, s)) != cudaSuccess) return bail(e, "memset st");
     if ((e = cudaStreamSynchronize(s)) != cudaSuccess) return bail(e, "sync init");
@@ -552,13 +546,12 @@ int dr_init(const dr_params* params, int64_t n_env, uint64_t seed) {
     c->step_grid = (int)std::min<long long>((long long)units, (long long)c->sm_count * occ_step);
     if (c->step_grid > c->max_ctas) c->step_grid = c->max_ctas;
     const char* rv = std::getenv("DR_RESET");
-    set_reset_version(rv ? std::atoi(rv) : 4);
+    set_reset_version(rv ? std::atoi(rv) : 3);
     c->reset_grid = reset_grid_for((uint32_t)n_env, c->sm_count);
 
     // episode 0 for every env (sampled at the beginning of every episode)
-    int nl = 1;
-    if ((e = launch_reset(P, nullptr, true, (uint32_t)n_env, c->reset_grid, s, &nl)) != cudaSuccess) return bail(e, "reset_kernel");
-    c->launches = nl;
+    if ((e = launch_reset(P, nullptr, true, (uint32_t)n_env, c->reset_grid, s)) != cudaSuccess) return bail(e, "reset_kernel");
+    c->launches = 1;
     ++g_total_launches;
     g_ctx = c;
     g_err[0] = 0;
@@ -594,11 +587,10 @@ int dr_reset(const uint8_t* env_mask) {
     Ctx* c = g_ctx;
     if (!c) return fail(DR_ENOTINIT, "dr_reset: no context");
     if (g_sticky) return fail(DR_ECUDA, "sticky CUDA error: %s", g_err);
-    int nl = 1;
-    cudaError_t e = launch_reset(c->p, env_mask, false, (uint32_t)c->n_env, c->reset_grid, c->stream, &nl);
+    cudaError_t e = launch_reset(c->p, env_mask, false, (uint32_t)c->n_env, c->reset_grid, c->stream);
     if (e != cudaSuccess) return cuda_fail(e, "reset_kernel");
-    c->launches += (uint64_t)nl;
-    g_total_launches += (uint64_t)nl;
+    c->launches++;
+    ++g_total_launches;
     return DR_OK;
 }
 

@@ -156,10 +156,8 @@ struct DevPtrs {
     uint32_t* rs_src;         // [256] physics draw source
     double* dec_tab;          // [512]: 0.99^j (j < 256), then 0.99^(256 i)
     double* stats;            // [N_STAT_SLOTS][N_STATS] (internal or caller-owned)
-    unsigned long long* ctl;  // [0] step t, [1] CTAs started (step), [2] resets pending,
-                              // [3] reset list length, [4] CTAs started (reset work)
+    unsigned long long* ctl;  // [0] = step t, [1] = CTAs started counter, [2] = resets pending
     const uint8_t* occl_in;   // simulator occlusion bits per env (dr_set_occlusion_input) or NULL
-    uint2* rlist;             // [n_env] (env, new episode index) of the resetting envs (reset v4)
 };
 
 // error / launch bookkeeping shared by every C-ABI entry point (dr_api.cu)
@@ -169,8 +167,7 @@ void count_launch();                              // one library kernel enqueued
 // launchers (dr_kernels.cu)
 cudaError_t upload_const(const DevConst& c, cudaStream_t s);
 cudaError_t launch_reset(const DevPtrs& p, const uint8_t* mask, bool first, uint32_t n_env,
-                         int grid, cudaStream_t s, int* n_launched);
-cudaError_t upload_reset_tables(const float4* phys, const uint32_t* src, cudaStream_t s);
+                         int grid, cudaStream_t s);
 cudaError_t launch_step(const DevPtrs& p, uint32_t layer_mask, const float* actions,
                         const float* raw_obs, float* out_actions, float* out_obs, float* out_dt,
                         float* out_force, float* out_sub, uint32_t n_env, int grid, cudaStream_t s);

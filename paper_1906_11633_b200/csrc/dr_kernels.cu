@@ -95,33 +95,15 @@ cudaError_t upload_const(const DevConst& c, cudaStream_t s) {
     return cudaMemcpyToSymbolAsync(c_dc, &c, sizeof(DevConst), 0, cudaMemcpyHostToDevice, s);
 }
 
-// Reset kernel (DR_RESET at dr_init, A/B): 4 = global compaction + balanced thread-per-env work
-// kernel (default), 3 = per-CTA compaction + thread per env (reset_kernel_t), 2 = warp per
-// resetting env in four lane-parallel phases (reset_kernel).
-static int g_reset_v = 4;
-void set_reset_version(int v) { g_reset_v = (v == 2 || v == 3) ? v : 4; }
-
-cudaError_t upload_reset_tables(const float4* phys, const uint32_t* src, cudaStream_t s) {
-    cudaError_t e = cudaMemcpyToSymbolAsync(c_rs_phys, phys, sizeof(float4) * MAX_PHYS, 0, cudaMemcpyHostToDevice, s);
-    if (e != cudaSuccess) return e;
-    return cudaMemcpyToSymbolAsync(c_rs_src, src, sizeof(uint32_t) * MAX_PHYS, 0, cudaMemcpyHostToDevice, s);
-}
+// Reset kernel (DR_RESET at dr_init, A/B): 3 = thread per resetting env over a compacted list
+// (reset_kernel_t, default), 2 = warp per resetting env in four lane-parallel phases (reset_kernel).
+static int g_reset_v = 3;
+void set_reset_version(int v) { g_reset_v = (v == 2) ? 2 : 3; }
 
 cudaError_t launch_reset(const DevPtrs& p, const uint8_t* mask, bool first, uint32_t n_env, int grid,
-                         cudaStream_t s, int* n_launched) {
-    *n_launched = 1;
-    if (g_reset_v == 2) {
-        reset_kernel<<<grid, RESET_THREADS, 0, s>>>(p, mask, first ? 1 : 0, n_env);
-    } else if (g_reset_v == 3) {
-        reset_kernel_t<<<grid, RT_THREADS, 0, s>>>(p, mask, first ? 1 : 0, n_env);
-    } else if (first) {
-        reset_work_kernel<<<grid, RT_THREADS, 0, s>>>(p, 1, n_env);
-    } else {
-        const int cgrid = (int)std::min<long long>(((long long)n_env + 1023) / 1024, (long long)grid * 4);
-        reset_compact_kernel<<<std::max(cgrid, 1), RT_THREADS, 0, s>>>(p, mask, n_env);
-        reset_work_kernel<<<grid, RT_THREADS, 0, s>>>(p, 0, n_env);
-        *n_launched = 2;
-    }
+                         cudaStream_t s) {
+    if (g_reset_v == 2) reset_kernel<<<grid, RESET_THREADS, 0, s>>>(p, mask, first ? 1 : 0, n_env);
+    else reset_kernel_t<<<grid, RT_THREADS, 0, s>>>(p, mask, first ? 1 : 0, n_env);
     return cudaGetLastError();
 }
 
@@ -132,15 +114,9 @@ int reset_grid_for(uint32_t n_env, int sm_count) {
         const long long chunks = (n_env + 31) / 32;
         return (int)std::max<long long>(1, std::min<long long>((chunks + 7) / 8, (long long)sm_count * n));
     }
-    if (g_reset_v == 3) {
-        if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, reset_kernel_t, RT_THREADS, 0) != cudaSuccess || n < 1) n = 1;
-        const long long ranges = (n_env + RT_RANGE - 1) / RT_RANGE;
-        return (int)std::max<long long>(1, std::min<long long>(ranges, (long long)sm_count * n));
-    }
-    // v4 work kernel: persistent, one wave of resident CTAs (capped by the env count)
-    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, reset_work_kernel, RT_THREADS, 0) != cudaSuccess || n < 1) n = 1;
-    const long long need = (n_env + RT_THREADS - 1) / RT_THREADS;
-    return (int)std::max<long long>(1, std::min<long long>(need, (long long)sm_count * n));
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, reset_kernel_t, RT_THREADS, 0) != cudaSuccess || n < 1) n = 1;
+    const long long ranges = (n_env + RT_RANGE - 1) / RT_RANGE;
+    return (int)std::max<long long>(1, std::min<long long>(ranges, (long long)sm_count * n));
 }
 
 static constexpr uint32_t MASK_FULL = 0xFFu;  // PHYS does not affect the step

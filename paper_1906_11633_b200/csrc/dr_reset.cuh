@@ -190,7 +190,6 @@ __device__ __forceinline__ uint32_t selw(const uint4 w, uint32_t r) {
     return r == 0u ? w.x : (r == 1u ? w.y : (r == 2u ? w.z : w.w));
 }
 
-template <bool kConstTables>
 __device__ void reset_env_thread(const DevPtrs& p, uint32_t e, uint32_t k, const float4* s_pd,
                                  const uint32_t* s_src) {
     const uint32_t lm = c_dc.layer_mask;
@@ -212,8 +211,8 @@ __device__ void reset_env_thread(const DevPtrs& p, uint32_t e, uint32_t k, const
                 const int q = q0 + r;
                 float v = 0.f;
                 if (q < np) {
-                    const float4 d = kConstTables ? c_rs_phys[q] : s_pd[q];
-                    const uint32_t src = kConstTables ? c_rs_src[q] : s_src[q];
+                    const float4 d = s_pd[q];
+                    const uint32_t src = s_src[q];
                     float x = 0.f;
                     if (src & RS_SRC_DRAW) {   // warp-uniform: every lane is at parameter q
                         if (src & RS_SRC_NORMAL) {
@@ -382,54 +381,8 @@ __global__ void __launch_bounds__(RT_THREADS) reset_kernel_t(DevPtrs p, const ui
         }
         __syncthreads();
         const uint32_t n = s_n;
-        for (uint32_t i = tid; i < n; i += RT_THREADS) reset_env_thread<false>(p, s_env[i], s_kk[i], s_pd, s_src);
+        for (uint32_t i = tid; i < n; i += RT_THREADS) reset_env_thread(p, s_env[i], s_kk[i], s_pd, s_src);
         __syncthreads();
     }
     if (!first && applied) atomicAdd(&p.ctl[2], (unsigned long long)applied);
-}
-
-// =====================================================================================
-// v4 (default): the resetting envs of the whole mask are compacted into one global list
-// (reset_compact_kernel: ballot + one atomic per warp), then reset_work_kernel runs a balanced
-// persistent grid-stride loop of one thread per list entry -- no per-range barriers, no idle
-// lanes beyond the last partial warp -- with the physics descriptors read from the constant bank.
-// =====================================================================================
-__global__ void __launch_bounds__(RT_THREADS) reset_compact_kernel(DevPtrs p, const uint8_t* __restrict__ mask,
-                                                                   uint32_t n_env) {
-    const int lane = threadIdx.x & 31;
-    const uint32_t n_chunks = (n_env + 31u) >> 5;
-    uint32_t applied = 0;
-    for (uint32_t c = (blockIdx.x * RT_THREADS + threadIdx.x) >> 5; c < n_chunks; c += (gridDim.x * RT_THREADS) >> 5) {
-        const uint32_t e = (c << 5) + lane;
-        const bool m = e < n_env && (mask == nullptr || mask[e] != 0);
-        const uint32_t bal = __ballot_sync(0xFFFFFFFFu, m);
-        if (!bal) continue;
-        uint32_t pos0 = 0;
-        if (lane == 0) pos0 = (uint32_t)atomicAdd(&p.ctl[3], (unsigned long long)__popc(bal));
-        pos0 = __shfl_sync(0xFFFFFFFFu, pos0, 0);
-        if (m) p.rlist[pos0 + __popc(bal & ((1u << lane) - 1u))] = make_uint2(e, p.rec[rec_index(e) + REC_EPISODE * PLANE] + 1u);
-        applied += (lane == 0) ? (uint32_t)__popc(bal) : 0u;
-    }
-    if (lane == 0 && applied) atomicAdd(&p.ctl[2], (unsigned long long)applied);
-}
-
-// all_envs: the dr_init reset (every env, episode 0) without a list
-__global__ void __launch_bounds__(RT_THREADS) reset_work_kernel(DevPtrs p, int all_envs, uint32_t n_env) {
-    __shared__ uint32_t s_count;
-    if (threadIdx.x == 0) {
-        s_count = all_envs ? n_env : (uint32_t)*(volatile unsigned long long*)&p.ctl[3];
-        // the last CTA to read the list length re-arms it for the next dr_reset
-        unsigned long long prev;
-        asm volatile("atom.acq_rel.gpu.global.add.u64 %0, [%1], 1;" : "=l"(prev) : "l"(&p.ctl[4]) : "memory");
-        if (prev == (unsigned long long)gridDim.x - 1ull) {
-            p.ctl[4] = 0ull;
-            if (!all_envs) p.ctl[3] = 0ull;
-        }
-    }
-    __syncthreads();
-    const uint32_t n = s_count;
-    for (uint32_t i = blockIdx.x * RT_THREADS + threadIdx.x; i < n; i += gridDim.x * RT_THREADS) {
-        const uint2 ek = all_envs ? make_uint2(i, 0u) : p.rlist[i];
-        reset_env_thread<true>(p, ek.x, ek.y, nullptr, nullptr);
-    }
 }
