@@ -188,7 +188,11 @@ int dr_reset(const uint8_t* env_mask);
  *   out_dt      [n][10] out  substep durations, s
  *   out_force   [n][3]  out  force on the object, N
  * The global step counter t advances by one in stream order (device-resident, so a CUDA graph
- * of dr_step calls advances it on every replay).  Asynchronous. */
+ * of dr_step calls advances it on every replay).  Jobs of up to 16,384 envs (n_env_global) run a
+ * latency-mode kernel (8 warps split a 32-env group's transform), larger jobs the throughput
+ * kernel (one thread per env, persistent tiles); the environment variable DR_STEP_MODE =
+ * throughput | latency, read at dr_init, forces either.  Both give the same results within the
+ * parity contract, and every shard of a job runs the same one.  Asynchronous. */
 int dr_step(const float* actions, const float* raw_obs, float* out_actions, float* out_obs,
             float* out_dt, float* out_force);
 
