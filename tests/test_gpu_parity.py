@@ -1,5 +1,7 @@
 """GPU parity: the CUDA path (through the C-ABI, libdr.so) against the fp64 oracle on the same
 seeded inputs, element by element (tests/parity.py states the contract)."""
+import math
+
 import numpy as np
 import pytest
 
@@ -530,3 +532,54 @@ def test_large_8M_envs_sampled(torch_cuda):
     finally:
         ctx.close()
         orc.close()
+
+
+def test_full_size_statistics_1M(torch_cuda):
+    """Full-size parity via properties that hold at any size (1M envs, full pipeline, 24 steps),
+    against closed forms fixed by the paper's tables: E[dt_env] = 10 (8 ms + ln 8 / 8750 s)
+    (PAPER.md:84-88); the force trigger rate E[p] = 0.099 / ln 100 (loguniform 0.1 %-10 %,
+    PAPER.md:113); the dropout initiation rate 1 - exp(-0.2 * 0.08) per tip-step and the
+    steady-state masked fraction 1 - (1 - p)^13; half of all actuators delayed
+    (PAPER.md:77-78); unit-variance uncorrelated action and fingertip normals."""
+    torch = torch_cuda
+    P = presets.preset(FULL)
+    n = 1 << 20
+    g = torch.Generator(device="cuda").manual_seed(5)
+    k = torch.randint(0, 11, (n, 20), device="cuda", generator=g)
+    A = (-1.0 + (2.0 * k + 1.0) / 11.0).float().contiguous()
+    O = torch.empty(n, 26, device="cuda")
+    O[:, 0:15] = torch.tensor(gen.TIP_NOMINAL.reshape(-1), device="cuda", dtype=torch.float32) + \
+        gen.TIP_JITTER * torch.randn(n, 15, device="cuda", generator=g)
+    O[:, 15:18] = torch.tensor(gen.OBJ_NOMINAL, device="cuda", dtype=torch.float32) + \
+        gen.OBJ_JITTER * torch.randn(n, 3, device="cuda", generator=g)
+    q = torch.randn(n, 8, device="cuda", generator=g)
+    O[:, 18:22] = q[:, :4] / q[:, :4].norm(dim=1, keepdim=True)
+    O[:, 22:26] = q[:, 4:] / q[:, 4:].norm(dim=1, keepdim=True)
+    ctx = _ctx(P, n)
+    T = 24
+    acc = np.zeros(32)
+    try:
+        for t in range(T):
+            ctx.step(A, O)
+            s = ctx.last_stats()
+            assert s[0] == n
+            acc += s
+            if t == T - 1:
+                masked_last = s[3] / (5.0 * n)
+    finally:
+        ctx.close()
+    steps = T * n
+    # substep timing: E[dt_env] over lambda ~ U[1250, 10000]
+    e_dt = 10 * (0.008 + math.log(8.0) / 8750.0)
+    assert abs(acc[16] / steps - e_dt) < 5e-6
+    # force trigger rate (2.4e7 env-steps; binomial sd ~3e-5)
+    assert abs(acc[6] / steps - 0.099 / math.log(100.0)) < 2e-4
+    # dropout: initiation rate per tip-step and the steady-state masked fraction (after 13+ steps)
+    p_d = 1.0 - math.exp(-0.2 * 0.08)
+    assert abs(acc[2] / (5 * steps) - p_d) < 2e-4
+    assert abs(masked_last - (1.0 - (1.0 - p_d) ** 13)) < 2e-3
+    # delay flags: half of all actuators (each env's 20 flags drawn once per episode)
+    assert abs(acc[1] / (20 * steps) - 0.5) < 2e-3
+    # unit-variance normals: sum z_u^2 over actions, sum z^2 over fingertip coordinates
+    assert abs(acc[21] / (20 * steps) - 1.0) < 2e-3
+    assert abs(acc[22] / (15 * steps) - 1.0) < 2e-3
