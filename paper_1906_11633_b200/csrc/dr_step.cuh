@@ -521,15 +521,17 @@ __device__ __forceinline__ void env_step(const DevPtrs& p, uint32_t e, bool vali
                 // within eps of it (num < den, only when num < ~1.7e-5 in fp32): there alpha is a
                 // cancellation whose absolute error (<= 2 ulp of 1 with the fast divide) is far
                 // inside the 1e-6 budget of alpha * a_n -- so no branch.
+                // (an == 0: the product an d dt is 0 whatever d is, so d needs no third case; alpha is 1
+                //  exactly when num == 0; a rail hit needs s' != s, which an == 0 cannot give)
                 const float s = slack[q];
                 const float sg = (an > 0.f) ? 1.f : ((an < 0.f) ? -1.f : 0.f);
-                const float d = (an > 0.f) ? dpos[q] : ((an < 0.f) ? dneg[q] : 0.f);
+                const float d = (an > 0.f) ? dpos[q] : dneg[q];
                 const float sp = fminf(fmaxf(s + an * d * dt_env, -1.f), 1.f);
                 const float num = fabsf(sg - s), den = fabsf(sp - s) + c_dc.eps;
                 const float al = backlash_alpha(num, den);
                 out = al * an;
-                n_rail += (sg != 0.f && fabsf(sp) == 1.f && sp != s) ? 1u : 0u;
-                n_a1 += (al == 1.f) ? 1u : 0u;
+                n_rail += (fabsf(sp) == 1.f && sp != s) ? 1u : 0u;
+                n_a1 += (num == 0.f) ? 1u : 0u;
                 if (valid) st_state(&S[(ST_SLACK + j) * P], __float_as_uint(sp));
             }
             s_bl += on<L>(B_SUBSTEP) ? 0.f : fabsf(out - an);
@@ -543,7 +545,7 @@ __device__ __forceinline__ void env_step(const DevPtrs& p, uint32_t e, bool vali
             for (int q = 0; q < 4; ++q) {
                 sl[q] = slack[q];
                 sg[q] = (anv[q] > 0.f) ? 1.f : ((anv[q] < 0.f) ? -1.f : 0.f);
-                dd[q] = (anv[q] > 0.f) ? dpos[q] : ((anv[q] < 0.f) ? dneg[q] : 0.f);
+                dd[q] = (anv[q] > 0.f) ? dpos[q] : dneg[q];
             }
             float4* osub = reinterpret_cast<float4*>(out_sub + (size_t)e * (N_SUB * N_ACT) + 4 * b);
 #pragma unroll 1
@@ -556,8 +558,8 @@ __device__ __forceinline__ void env_step(const DevPtrs& p, uint32_t e, bool vali
                     const float num = fabsf(sg[q] - s0), den = fabsf(sp - s0) + c_dc.eps;
                     const float al = backlash_alpha(num, den);
                     ov[q] = al * anv[q];
-                    n_rail += (sg[q] != 0.f && fabsf(sp) == 1.f && sp != s0) ? 1u : 0u;
-                    n_a1 += (al == 1.f) ? 1u : 0u;
+                    n_rail += (fabsf(sp) == 1.f && sp != s0) ? 1u : 0u;
+                    n_a1 += (num == 0.f) ? 1u : 0u;
                     sl[q] = sp;
                 }
                 if (valid) __stcs(osub + (size_t)k * (N_ACT / 4), make_float4(ov[0], ov[1], ov[2], ov[3]));

@@ -118,13 +118,13 @@ __global__ void __launch_bounds__(LAT_THREADS, DR_LAT_MIN_CTAS) step_kernel_lat(
                 for (int q = 0; q < 4; ++q) {                            // [Q3, Q4]
                     const float an = anv[q], s = slack[q];
                     const float sg = (an > 0.f) ? 1.f : ((an < 0.f) ? -1.f : 0.f);
-                    const float d = (an > 0.f) ? dpos[q] : ((an < 0.f) ? dneg[q] : 0.f);
+                    const float d = (an > 0.f) ? dpos[q] : dneg[q];
                     const float sp = fminf(fmaxf(s + an * d * dt_env, -1.f), 1.f);
                     const float num = fabsf(sg - s), den = fabsf(sp - s) + c_dc.eps;
                     const float al = backlash_alpha(num, den);
                     ov[q] = al * an;
-                    n_rail += (sg != 0.f && fabsf(sp) == 1.f && sp != s) ? 1u : 0u;
-                    n_a1 += (al == 1.f) ? 1u : 0u;
+                    n_rail += (fabsf(sp) == 1.f && sp != s) ? 1u : 0u;
+                    n_a1 += (num == 0.f) ? 1u : 0u;
                     s_bl += fabsf(ov[q] - an);
                     if (valid) st_state(&S[(ST_SLACK + 4 * b + q) * P], __float_as_uint(sp));
                 }
@@ -134,7 +134,7 @@ __global__ void __launch_bounds__(LAT_THREADS, DR_LAT_MIN_CTAS) step_kernel_lat(
                 for (int q = 0; q < 4; ++q) {
                     sl[q] = slack[q];
                     sg[q] = (anv[q] > 0.f) ? 1.f : ((anv[q] < 0.f) ? -1.f : 0.f);
-                    dd[q] = (anv[q] > 0.f) ? dpos[q] : ((anv[q] < 0.f) ? dneg[q] : 0.f);
+                    dd[q] = (anv[q] > 0.f) ? dpos[q] : dneg[q];
                     ov[q] = anv[q];
                 }
                 float4* osub = reinterpret_cast<float4*>(out_sub + (size_t)ec * (N_SUB * N_ACT) + 4 * b);
@@ -148,8 +148,8 @@ __global__ void __launch_bounds__(LAT_THREADS, DR_LAT_MIN_CTAS) step_kernel_lat(
                         const float num = fabsf(sg[q] - s0), den = fabsf(sp - s0) + c_dc.eps;
                         const float al = backlash_alpha(num, den);
                         ov[q] = al * anv[q];
-                        n_rail += (sg[q] != 0.f && fabsf(sp) == 1.f && sp != s0) ? 1u : 0u;
-                        n_a1 += (al == 1.f) ? 1u : 0u;
+                        n_rail += (fabsf(sp) == 1.f && sp != s0) ? 1u : 0u;
+                        n_a1 += (num == 0.f) ? 1u : 0u;
                         sl[q] = sp;
                     }
                     if (valid) __stcs(osub + (size_t)k * (N_ACT / 4), make_float4(ov[0], ov[1], ov[2], ov[3]));
