@@ -96,13 +96,20 @@ cudaError_t upload_const(const DevConst& c, cudaStream_t s) {
 }
 
 // Reset kernel (DR_RESET at dr_init, A/B): 3 = thread per resetting env over a compacted list
-// (reset_kernel_t, default), 2 = warp per resetting env in four lane-parallel phases (reset_kernel).
+// (reset_kernel_t, default), 5 = task-split over (task, env) items (reset_kernel_v5; measured 3 %
+// slower), 2 = warp per resetting env in four lane-parallel phases (reset_kernel).
 static int g_reset_v = 3;
-void set_reset_version(int v) { g_reset_v = (v == 2) ? 2 : 3; }
+void set_reset_version(int v) { g_reset_v = (v == 2 || v == 5) ? v : 3; }
 
 cudaError_t launch_reset(const DevPtrs& p, const uint8_t* mask, bool first, uint32_t n_env, int grid,
                          cudaStream_t s) {
     if (g_reset_v == 2) reset_kernel<<<grid, RESET_THREADS, 0, s>>>(p, mask, first ? 1 : 0, n_env);
+    else if (g_reset_v == 5) {
+        // per-CTA range: the envs split evenly over the grid, in whole 32-env chunks, <= R5_RANGE
+        const uint32_t per = (uint32_t)(((unsigned long long)n_env + grid - 1) / grid);
+        const uint32_t range = std::min<uint32_t>(R5_RANGE, std::max<uint32_t>(32u, (per + 31u) & ~31u));
+        reset_kernel_v5<<<grid, R5_THREADS, 0, s>>>(p, mask, first ? 1 : 0, n_env, range);
+    }
     else reset_kernel_t<<<grid, RT_THREADS, 0, s>>>(p, mask, first ? 1 : 0, n_env);
     return cudaGetLastError();
 }
@@ -113,6 +120,12 @@ int reset_grid_for(uint32_t n_env, int sm_count) {
         if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, reset_kernel, RESET_THREADS, 0) != cudaSuccess || n < 1) n = 1;
         const long long chunks = (n_env + 31) / 32;
         return (int)std::max<long long>(1, std::min<long long>((chunks + 7) / 8, (long long)sm_count * n));
+    }
+    if (g_reset_v == 5) {
+        // one resident wave: as many CTAs as fit (6 per SM), fewer for small jobs (>= 32 envs each)
+        if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, reset_kernel_v5, R5_THREADS, 0) != cudaSuccess || n < 1) n = 1;
+        const long long ranges = (n_env + 31) / 32;
+        return (int)std::max<long long>(1, std::min<long long>(ranges, (long long)sm_count * n));
     }
     if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, reset_kernel_t, RT_THREADS, 0) != cudaSuccess || n < 1) n = 1;
     const long long ranges = (n_env + RT_RANGE - 1) / RT_RANGE;

@@ -386,3 +386,232 @@ __global__ void __launch_bounds__(RT_THREADS) reset_kernel_t(DevPtrs p, const ui
     }
     if (!first && applied) atomicAdd(&p.ctl[2], (unsigned long long)applied);
 }
+
+// =====================================================================================
+// Task-split reset (v5, A/B variant DR_RESET=5; v3 stays the default): the v3 thread-per-env chain (~11k dependent instructions) left
+// the SMs latency-bound with ~22 resident warps of work per SM.  Here each resetting env's work
+// is cut into independent tasks -- ceil(n_phys / 32) physics chunks of 32 parameters plus four
+// record tasks of 7-10 Philox blocks each -- and a CTA's threads walk (task, env) items with the
+// env index fastest, so a warp runs one task kind over 32 envs (warp-uniform descriptor walk).
+// Capped at 40 registers (6 CTAs per SM); the host sizes the per-CTA env range so the grid is one
+// resident wave (1M envs: 888 CTAs of 1,184 envs).
+// Same channels, words and transforms as reset_env_thread / the oracle.
+// Measured (B200, 1M envs, 10 % resets): 0.470 ms per reset+step vs v3's 0.458; ncu: 68 % warps
+// active (v3 ~24 %) but 98 M warp-instructions and the stalls move to the scattered stores
+// (mio / lg throttle, long scoreboard on store operands) -- more resident chains do not pay.
+// =====================================================================================
+constexpr int R5_THREADS = 256;
+constexpr uint32_t R5_RANGE = 2048;   // max envs per CTA pass (shared-memory list size)
+constexpr int R5_REC_TASKS = 4;
+
+__device__ __forceinline__ void r5_phys_chunk(const DevPtrs& p, uint32_t e, uint32_t k, uint32_t g, int c,
+                                              const float4* s_pd, const uint32_t* s_src) {
+    const int np = c_dc.n_phys;
+    const int q_lo = c * 32, q_hi = min(np, q_lo + 32);
+    float* prow = p.phys + (size_t)e * np;
+    const bool vec = (np & 3) == 0;
+    uint32_t cur_n = 0xFFFFFFFFu, cur_u = 0xFFFFFFFFu;
+    uint4 wu = make_uint4(0u, 0u, 0u, 0u);
+    float zn[4] = {0.f, 0.f, 0.f, 0.f};
+#pragma unroll 1
+    for (int q0 = q_lo; q0 < q_hi; q0 += 4) {
+        float v4[4];
+#pragma unroll
+        for (int r = 0; r < 4; ++r) {
+            const int q = q0 + r;
+            float v = 0.f;
+            if (q < q_hi) {
+                const float4 d = s_pd[q];
+                const uint32_t src = s_src[q];
+                float x = 0.f;
+                if (src & RS_SRC_DRAW) {
+                    if (src & RS_SRC_NORMAL) {
+                        const uint32_t n = (src & RS_SRC_IDX) - ZB_PHYS;
+                        if ((n >> 2) != cur_n) {
+                            cur_n = n >> 2;
+                            const uint4 w = philox(g, k, CH_PHYS_N, cur_n);
+                            box_muller(w.x, w.y, zn[0], zn[1]);
+                            box_muller(w.z, w.w, zn[2], zn[3]);
+                        }
+                        x = sel4(zn, n & 3u);
+                    } else {
+                        const uint32_t u = (src & RS_SRC_IDX) - SL_PHYS_U * 4;
+                        if ((u >> 2) != cur_u) {
+                            cur_u = u >> 2;
+                            wu = philox(g, k, CH_PHYS_U, cur_u);
+                        }
+                        x = uni(selw(wu, u & 3u));
+                    }
+                }
+                const float tv = fmaf(d.y, x, d.x);
+                v = fmaf(d.w, (src & RS_SRC_EXP) ? ex2_approx(tv) : tv, d.z);
+                if (q == c_dc.mass_index) p.rec[rec_index(e) + REC_MASS * PLANE] = __float_as_uint(v);   // [Q18]
+                if (!vec) prow[q] = v;
+            }
+            v4[r] = v;
+        }
+        if (vec) reinterpret_cast<float4*>(prow)[q0 >> 2] = make_float4(v4[0], v4[1], v4[2], v4[3]);
+    }
+}
+
+__device__ __forceinline__ void r5_record_task(const DevPtrs& p, uint32_t e, uint32_t k, uint32_t g, int t) {
+    const uint32_t lm = c_dc.layer_mask;
+    constexpr size_t P = PLANE;
+    uint32_t* R = p.rec + rec_index(e);
+    if (t == 0) {
+        // delay flags, timing lambda, force probability [Q19]
+        uint32_t bits = 0u;
+        if (lm & B_DELAY) {
+#pragma unroll
+            for (int b = 0; b < 5; ++b) {
+                const uint4 w = philox(g, k, CH_DELAY, b);
+                const uint32_t ws[4] = {w.x, w.y, w.z, w.w};
+#pragma unroll
+                for (int q = 0; q < 4; ++q)
+                    bits |= ((unsigned long long)ws[q] < c_dc.t_delay ? 1u : 0u) << (4 * b + q);
+            }
+        }
+        R[REC_DELAY * P] = bits;
+        float lam = 0.f, il = 0.f;
+        if (lm & B_TIMING) {
+            lam = c_dc.lam_lo + c_dc.lam_range * uni(philox(g, k, CH_LAMBDA, 0).x);
+            il = 1.0f / lam;
+        }
+        R[REC_LAMBDA * P] = __float_as_uint(lam);
+        R[REC_INVLAM * P] = __float_as_uint(il);
+        const uint32_t j = (lm & B_FORCE) ? (philox(g, k, CH_FORCE_P, 0).x >> 16) : 0u;
+        R[REC_PINDEX * P] = j;
+        R[REC_TFORCE * P] = (lm & B_FORCE) ? __ldg(p.t_tab + j) : 0u;
+        R[REC_EPISODE * P] = k;
+        p.st[st_index(e) + ST_FLAGS * P] = FRESH_BIT;   // state reads as zero next step [Q6, Q9]
+    } else if (t == 1) {
+        // backlash widths [Q7]: normal j -> delta-1_j, 20 + j -> delta+1_j
+#pragma unroll 1
+        for (int b = 0; b < 10; ++b) {
+            float z[4] = {0.f, 0.f, 0.f, 0.f};
+            if (lm & B_BACKLASH) {
+                const uint4 w = philox(g, k, CH_BACKLASH, b);
+                box_muller(w.x, w.y, z[0], z[1]);
+                box_muller(w.z, w.w, z[2], z[3]);
+            }
+#pragma unroll
+            for (int q = 0; q < 4; ++q) {
+                const int n = 4 * b + q;
+                const int j = n < N_ACT ? n : n - N_ACT;
+                const float cal = n < N_ACT ? c_dc.dcal_neg[j] : c_dc.dcal_pos[j];
+                const float dv = (lm & B_BACKLASH) ? fmaxf(0.f, cal + c_dc.jitter * z[q]) : 0.f;
+                R[((n < N_ACT ? REC_DNEG : REC_DPOS) + j) * P] = __float_as_uint(dv);
+            }
+        }
+    } else if (t == 2) {
+        // correlated action offset (Table action-noise); object offset and rotation
+#pragma unroll 1
+        for (int b = 0; b < 5; ++b) {
+            float z[4] = {0.f, 0.f, 0.f, 0.f};
+            if (lm & B_ACT_NOISE) {
+                const uint4 w = philox(g, k, CH_CORR_ACT, b);
+                box_muller(w.x, w.y, z[0], z[1]);
+                box_muller(w.z, w.w, z[2], z[3]);
+            }
+#pragma unroll
+            for (int q = 0; q < 4; ++q) R[(REC_CACT + 4 * b + q) * P] = __float_as_uint(c_dc.sc * z[q]);
+        }
+        float zo[4] = {0.f, 0.f, 0.f, 0.f};
+        float q[4] = {1.f, 0.f, 0.f, 0.f};
+        if (lm & B_OBS_NOISE) {
+            const uint4 wo = philox(g, k, CH_CORR_OBJ, 0);
+            box_muller(wo.x, wo.y, zo[0], zo[1]);
+            box_muller(wo.z, wo.w, zo[2], zo[3]);
+            rotation(c_dc.rot_corr, philox(g, k, CH_CORR_ROT, 0), q);
+        }
+#pragma unroll
+        for (int c = 0; c < 3; ++c) R[(REC_COBJ + c) * P] = __float_as_uint(c_dc.obj_corr * zo[c]);
+#pragma unroll
+        for (int c = 0; c < 4; ++c) R[(REC_QC + c) * P] = __float_as_uint(q[c]);
+    } else {
+        // fingertip offsets [Q14, Q15]
+        if (lm & B_OBS_NOISE) {
+            float mb[4];
+            {
+                const uint4 w = philox(g, k, CH_MARKER_BASE, 0);
+                box_muller(w.x, w.y, mb[0], mb[1]);
+                box_muller(w.z, w.w, mb[2], mb[3]);
+            }
+#pragma unroll 1
+            for (int b = 0; b < 4; ++b) {
+                float zc[4], zm[4];
+                const uint4 wc = philox(g, k, CH_CORR_TIP, b);
+                const uint4 wm = philox(g, k, CH_MARKER_TIP, b);
+                box_muller(wc.x, wc.y, zc[0], zc[1]);
+                box_muller(wc.z, wc.w, zc[2], zc[3]);
+                box_muller(wm.x, wm.y, zm[0], zm[1]);
+                box_muller(wm.z, wm.w, zm[2], zm[3]);
+#pragma unroll
+                for (int q = 0; q < 4; ++q) {
+                    const int n = 4 * b + q;
+                    if (n < 15) {
+                        float v = c_dc.tip_corr * zc[q] + c_dc.tip_marker * zm[q];
+                        if (c_dc.base_to_tips) v = v - c_dc.base_marker * sel4(mb, (uint32_t)(n % 3));
+                        R[(REC_OFFTIP + n) * P] = __float_as_uint(v);
+                    }
+                }
+            }
+        } else {
+#pragma unroll
+            for (int n = 0; n < 15; ++n) R[(REC_OFFTIP + n) * P] = 0u;
+        }
+    }
+}
+
+__global__ void __launch_bounds__(R5_THREADS, 6) reset_kernel_v5(DevPtrs p, const uint8_t* __restrict__ mask,
+                                                                 int first, uint32_t n_env, uint32_t range) {
+    __shared__ float4 s_pd[MAX_PHYS];
+    __shared__ uint32_t s_src[MAX_PHYS];
+    __shared__ uint32_t s_env[R5_RANGE];
+    __shared__ uint32_t s_kk[R5_RANGE];
+    __shared__ uint32_t s_n;
+    const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
+    constexpr int NWR = R5_THREADS / 32;
+    const int np = c_dc.n_phys;
+    for (int i = tid; i < np; i += R5_THREADS) {
+        s_pd[i] = p.rs_phys[i];
+        s_src[i] = p.rs_src[i];
+    }
+    const int n_pt = (np + 31) >> 5;   // physics chunks
+    const uint32_t n_tasks = (uint32_t)(n_pt + R5_REC_TASKS);
+    uint32_t applied = 0;
+    for (uint32_t base = blockIdx.x * range; base < n_env; base += gridDim.x * range) {
+        if (tid == 0) s_n = 0u;
+        __syncthreads();
+        for (uint32_t c = wid; c < range / 32; c += NWR) {
+            const uint32_t e = base + c * 32u + lane;
+            const bool m = e < n_env && (mask == nullptr || mask[e] != 0);
+            const uint32_t bal = __ballot_sync(0xFFFFFFFFu, m);
+            if (!bal) continue;
+            uint32_t pos0 = 0;
+            if (lane == 0) pos0 = atomicAdd(&s_n, (uint32_t)__popc(bal));
+            pos0 = __shfl_sync(0xFFFFFFFFu, pos0, 0);
+            if (m) {
+                const uint32_t idx = pos0 + __popc(bal & ((1u << lane) - 1u));
+                s_env[idx] = e;
+                s_kk[idx] = first ? 0u : p.rec[rec_index(e) + REC_EPISODE * PLANE] + 1u;
+            }
+            applied += (lane == 0) ? (uint32_t)__popc(bal) : 0u;
+        }
+        __syncthreads();
+        const uint32_t n = s_n;
+        const uint32_t n32 = (n + 31u) & ~31u;   // each task's segment padded to whole warps: no warp
+        const uint32_t total = n32 * n_tasks;    // straddles two task kinds (no divergent task code)
+        // the record tasks (longer) first, so the tail is made of short physics chunks
+        for (uint32_t j = tid; j < total; j += R5_THREADS) {
+            const uint32_t t = j / n32, i = j - t * n32;
+            if (i >= n) continue;
+            const uint32_t e = s_env[i], k = s_kk[i];
+            const uint32_t g = c_dc.env_offset + e;
+            if (t < (uint32_t)R5_REC_TASKS) r5_record_task(p, e, k, g, (int)t);
+            else r5_phys_chunk(p, e, k, g, (int)t - R5_REC_TASKS, s_pd, s_src);
+        }
+        __syncthreads();
+    }
+    if (!first && applied) atomicAdd(&p.ctl[2], (unsigned long long)applied);
+}

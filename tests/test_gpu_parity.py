@@ -165,6 +165,29 @@ def test_reset_records_and_phys(torch_cuda):
         ctx.close()
 
 
+@pytest.mark.parametrize("version", ["2", "3", "5"])
+@pytest.mark.parametrize("n", [1, 200, 2049])
+def test_reset_kernel_versions(torch_cuda, monkeypatch, version, n):
+    """Every reset kernel (DR_RESET, read at dr_init: 2 warp per env, 3 thread per env (default),
+    5 task-split) gives the oracle's episode records and physics rows -- full init, then masked
+    resets at two densities (a lone env, every 3rd env) -- and the steps after them agree."""
+    monkeypatch.setenv("DR_RESET", version)
+    torch = torch_cuda
+    P = presets.preset(FULL)
+    ctx = _ctx(P, n)
+    orc = _oracle(P, np.arange(n))
+    try:
+        compare_records(ctx.export(), [orc.env(i) for i in range(n)], phys_g=ctx.phys())
+        for m in [(np.arange(n) == n - 1).astype(np.uint8), (np.arange(n) % 3 == 0).astype(np.uint8)]:
+            ctx.reset(torch.from_numpy(m).cuda())
+            orc.reset(m)
+            torch.cuda.synchronize()
+            compare_records(ctx.export(), [orc.env(i) for i in range(n)], phys_g=ctx.phys())
+    finally:
+        ctx.close()
+    run_pair(torch_cuda, FULL, n, 6, n_frames=6, resets={3: (np.arange(n) % 4 == 1).astype(np.uint8)})
+
+
 def test_config1_free_running(torch_cuda):
     """BASELINE config 1: 4 envs x 50 steps, all layers, fixed seed; every output, state and
     stats slot each step (M1 free-running), with resets mid-run."""
