@@ -34,7 +34,6 @@ N_GLOBAL_1M = 1 << 20
 # + state read/write, for the layer sets the configs use
 BYTES_FULL = 184 + 220 + 344 + 480
 BYTES_CFG2 = 184 + 220 + 332 + 160 + 4   # + the flags word (FRESH marker) read per step
-RESET_BYTES = 1024 + 356 + 240 + 1      # phys row + record planes + state planes + mask byte
 
 
 def parse():
@@ -59,6 +58,9 @@ def parse():
                     help="steps per CUDA graph in the timed region (0 = eager launches; default: 100 for the "
                          "launch-bound small configs at N=1, else 0)")
     return ap.parse_args()
+
+
+RESET_BYTES = 1024 + 356 + 4   # per resetting env: phys row, 89-plane episode record, FRESH flag
 
 
 def config_of(name, n_override):
@@ -405,11 +407,13 @@ def main():
             masks = [((e + t) % 10 == 0).to(torch.uint8) for t in range(10)]
         torch.cuda.synchronize()
 
-    def one_step(t):
+    def one_step(t, mid=None):
         if reducer is not None:
             reducer.before_step(t)   # the all-reduce of step t-3 is done before step t clears its slot
         if masks is not None:
             ctx.reset(masks[t % 10])
+            if mid is not None:
+                mid.record(lib_stream)   # between dr_reset and dr_step: the two kernels' shares
         ctx.step(A[t % F], O[t % F])
         if reducer is not None:
             # the path's one collective: sum of the 32 x fp64 stats of step t over ranks,
@@ -451,9 +455,10 @@ def main():
                 evs[i + 1].record(lib_stream)
         else:
             evs = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps + 1)]
+            mids = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)] if cfg["resets"] else None
             evs[0].record(lib_stream)
             for i in range(args.steps):
-                one_step(t_base + i)
+                one_step(t_base + i, mids[i] if mids else None)
                 evs[i + 1].record(lib_stream)
         if reducer is not None:
             reducer.sync()
@@ -473,14 +478,26 @@ def main():
         stats = ctx.last_stats()
 
     value = n_glob * args.steps / (elapsed_ms / 1e3)
+    split = None
+    if cfg["resets"] and G == 0:
+        # dr_reset and dr_step launch times from the events around each (library stream)
+        r_ms = [evs[i].elapsed_time(mids[i]) for i in range(args.steps)]
+        s_ms = [mids[i].elapsed_time(evs[i + 1]) for i in range(args.steps)]
+        split = {"reset_ms_avg": sum(r_ms) / len(r_ms), "step_ms_avg": sum(s_ms) / len(s_ms),
+                 "resets_per_step": n // 10, "reset_bytes_per_env": RESET_BYTES}
     per.sort()
     kern_ms = sum(per) / len(per)
     peak, peak_kind = measured_peak()
-    achieved = cfg["bytes"] * n / (kern_ms / 1e3) / 1e9
+    # algorithmic bytes per step: the step's 1228 B per env, plus (reset config) 1,384 B per
+    # resetting env (phys row 1024 + record 356 + FRESH flag 4) and the 1-byte mask per env
+    bytes_step = cfg["bytes"] * n + ((n // 10) * RESET_BYTES + n if cfg["resets"] else 0)
+    achieved = bytes_step / (kern_ms / 1e3) / 1e9
     roofline = {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
-                "traffic": ncu_traffic(cfg["workload"]), "peak_kind": peak_kind,
-                "bytes_per_env_step": cfg["bytes"], "kernel": "dr::step_kernel_warp" + (" (+ dr::reset_kernel)" if cfg["resets"] else ""),
+                "traffic": None if cfg["resets"] else ncu_traffic(cfg["workload"]), "peak_kind": peak_kind,
+                "bytes_per_env_step": cfg["bytes"], "kernel": "dr::step_kernel_warp" + (" + dr::reset_kernel (one step = dr_reset + dr_step)" if cfg["resets"] else ""),
                 "kernel_ms_avg": kern_ms, "kernel_ms_median": per[len(per) // 2]}
+    if split:
+        roofline["split"] = split
 
     # ---- e2e: through dr_step_host with pinned host buffers (copies inside the timed region) ----
     e2e = None

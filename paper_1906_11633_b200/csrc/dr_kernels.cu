@@ -95,11 +95,13 @@ cudaError_t upload_const(const DevConst& c, cudaStream_t s) {
     return cudaMemcpyToSymbolAsync(c_dc, &c, sizeof(DevConst), 0, cudaMemcpyHostToDevice, s);
 }
 
-// Reset kernel (DR_RESET at dr_init, A/B): 3 = thread per resetting env over a compacted list
-// (reset_kernel_t, default), 5 = task-split over (task, env) items (reset_kernel_v5; measured 3 %
-// slower), 2 = warp per resetting env in four lane-parallel phases (reset_kernel).
-static int g_reset_v = 3;
-void set_reset_version(int v) { g_reset_v = (v == 2 || v == 5) ? v : 3; }
+// Reset kernel (DR_RESET at dr_init, A/B): 6 = thread-per-env record chain + warp-per-env physics
+// rows (reset_kernel_h, default; config 5 reset + step 0.418-0.425 ms vs v3's 0.458-0.460),
+// 3 = thread per resetting env over a compacted list (reset_kernel_t), 5 = task-split over
+// (task, env) items (reset_kernel_v5), 2 = warp per resetting env in four lane-parallel phases
+// (reset_kernel).
+static int g_reset_v = 6;
+void set_reset_version(int v) { g_reset_v = (v == 2 || v == 3 || v == 5) ? v : 6; }
 
 cudaError_t launch_reset(const DevPtrs& p, const uint8_t* mask, bool first, uint32_t n_env, int grid,
                          cudaStream_t s) {
@@ -110,6 +112,7 @@ cudaError_t launch_reset(const DevPtrs& p, const uint8_t* mask, bool first, uint
         const uint32_t range = std::min<uint32_t>(R5_RANGE, std::max<uint32_t>(32u, (per + 31u) & ~31u));
         reset_kernel_v5<<<grid, R5_THREADS, 0, s>>>(p, mask, first ? 1 : 0, n_env, range);
     }
+    else if (g_reset_v == 6) reset_kernel_h<<<grid, RT_THREADS, 0, s>>>(p, mask, first ? 1 : 0, n_env);
     else reset_kernel_t<<<grid, RT_THREADS, 0, s>>>(p, mask, first ? 1 : 0, n_env);
     return cudaGetLastError();
 }
@@ -127,7 +130,7 @@ int reset_grid_for(uint32_t n_env, int sm_count) {
         const long long ranges = (n_env + 31) / 32;
         return (int)std::max<long long>(1, std::min<long long>(ranges, (long long)sm_count * n));
     }
-    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, reset_kernel_t, RT_THREADS, 0) != cudaSuccess || n < 1) n = 1;
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, g_reset_v == 6 ? reset_kernel_h : reset_kernel_t, RT_THREADS, 0) != cudaSuccess || n < 1) n = 1;
     const long long ranges = (n_env + RT_RANGE - 1) / RT_RANGE;
     return (int)std::max<long long>(1, std::min<long long>(ranges, (long long)sm_count * n));
 }

@@ -190,6 +190,8 @@ __device__ __forceinline__ uint32_t selw(const uint4 w, uint32_t r) {
     return r == 0u ? w.x : (r == 1u ? w.y : (r == 2u ? w.z : w.w));
 }
 
+// kPhys = false: the record part only (reset_kernel_h writes the physics rows warp-cooperatively).
+template <bool kPhys = true>
 __device__ void reset_env_thread(const DevPtrs& p, uint32_t e, uint32_t k, const float4* s_pd,
                                  const uint32_t* s_src) {
     const uint32_t lm = c_dc.layer_mask;
@@ -198,7 +200,7 @@ __device__ void reset_env_thread(const DevPtrs& p, uint32_t e, uint32_t k, const
     uint32_t* S = p.st + st_index(e);
     const uint32_t g = c_dc.env_offset + e;
     // ---- physics [Q20]: v = C0 + C1 f(A + B x) ----
-    {
+    if constexpr (kPhys) {
         const int np = c_dc.n_phys;
         float* prow = p.phys + (size_t)e * np;
         const bool vec = (np & 3) == 0;   // rows are 16-byte aligned: float4 stores
@@ -382,6 +384,96 @@ __global__ void __launch_bounds__(RT_THREADS) reset_kernel_t(DevPtrs p, const ui
         __syncthreads();
         const uint32_t n = s_n;
         for (uint32_t i = tid; i < n; i += RT_THREADS) reset_env_thread(p, s_env[i], s_kk[i], s_pd, s_src);
+        __syncthreads();
+    }
+    if (!first && applied) atomicAdd(&p.ctl[2], (unsigned long long)applied);
+}
+
+// =====================================================================================
+// Hybrid reset (v6, DR_RESET=6): v3's compaction and thread-per-env record chain, but the physics
+// rows -- two thirds of v3's per-thread chain (64 of ~97 Philox blocks, 64 of ~114 Box-Muller
+// pairs, a 256-step descriptor walk with data-dependent block draws) -- are written by a warp per
+// env: lanes draw the env's physics blocks (uniform blocks -> 4 uniforms, normal blocks -> 4
+// normals) into a per-warp shared-memory buffer, then lanes walk the parameters (lane q, q + 32,
+// ...), so every store is one coalesced 128-byte line of phys[e][*] and the work has lane- and
+// parameter-level parallelism instead of one serial chain.  Same channels, words, transforms and
+// operation order as reset_env_thread (bit-identical results).
+// =====================================================================================
+constexpr int RH_DRAW = 2 * MAX_PHYS;   // per-warp draw buffer: uniforms at [0, 256), normals at [256, 512)
+
+__device__ __forceinline__ void reset_phys_warp(const DevPtrs& p, uint32_t e, uint32_t k, int lane, float* dr,
+                                                const float4* s_pd, const uint32_t* s_src, int nub, int nnb) {
+    const uint32_t g = c_dc.env_offset + e;
+    __syncwarp();
+    for (int b = lane; b < nub + nnb; b += 32) {
+        if (b < nub) {   // uniform-kind parameter u uses word u % 4 of block u / 4 (channel PHYS_U)
+            const uint4 w = philox(g, k, CH_PHYS_U, (uint32_t)b);
+            reinterpret_cast<float4*>(dr)[b] = make_float4(uni(w.x), uni(w.y), uni(w.z), uni(w.w));
+        } else {         // normal-kind parameter n uses normal n % 4 of block n / 4 (channel PHYS_N)
+            const int bn = b - nub;
+            const uint4 w = philox(g, k, CH_PHYS_N, (uint32_t)bn);
+            float4 z;
+            box_muller(w.x, w.y, z.x, z.y);
+            box_muller(w.z, w.w, z.z, z.w);
+            reinterpret_cast<float4*>(dr + MAX_PHYS)[bn] = z;
+        }
+    }
+    __syncwarp();
+    const int np = c_dc.n_phys;
+    float* prow = p.phys + (size_t)e * np;
+    for (int q = lane; q < np; q += 32) {
+        const float4 d = s_pd[q];   // (A, B, C0, C1)
+        const uint32_t src = s_src[q];
+        float x = 0.f;
+        if (src & RS_SRC_DRAW) x = dr[(src & RS_SRC_IDX) + ((src & RS_SRC_NORMAL) ? MAX_PHYS : 0)];
+        const float tv = fmaf(d.y, x, d.x);
+        const float v = fmaf(d.w, (src & RS_SRC_EXP) ? ex2_approx(tv) : tv, d.z);
+        prow[q] = v;
+        if (q == c_dc.mass_index) p.rec[rec_index(e) + REC_MASS * PLANE] = __float_as_uint(v);   // [Q18]
+    }
+}
+
+__global__ void __launch_bounds__(RT_THREADS) reset_kernel_h(DevPtrs p, const uint8_t* __restrict__ mask, int first,
+                                                             uint32_t n_env) {
+    __shared__ float4 s_pd[MAX_PHYS];
+    __shared__ uint32_t s_src[MAX_PHYS];
+    __shared__ uint32_t s_env[RT_RANGE];
+    __shared__ uint32_t s_kk[RT_RANGE];
+    __shared__ __align__(16) float s_dr[RT_THREADS / 32][RH_DRAW];
+    __shared__ uint32_t s_n;
+    const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
+    constexpr int NWR = RT_THREADS / 32;
+    for (int i = tid; i < c_dc.n_phys; i += RT_THREADS) {
+        s_pd[i] = p.rs_phys[i];
+        s_src[i] = p.rs_src[i];
+    }
+    const bool phys_on = (c_dc.layer_mask & B_PHYS) != 0;
+    const int nub = phys_on ? (c_dc.n_phys_u + 3) / 4 : 0;
+    const int nnb = phys_on ? (c_dc.n_phys_n + 3) / 4 : 0;
+    uint32_t applied = 0;
+    for (uint32_t base = blockIdx.x * RT_RANGE; base < n_env; base += gridDim.x * RT_RANGE) {
+        if (tid == 0) s_n = 0u;
+        __syncthreads();
+        for (uint32_t c = wid; c < RT_RANGE / 32; c += NWR) {
+            const uint32_t e = base + c * 32u + lane;
+            const bool m = e < n_env && (mask == nullptr || mask[e] != 0);
+            const uint32_t bal = __ballot_sync(0xFFFFFFFFu, m);
+            if (!bal) continue;
+            uint32_t pos0 = 0;
+            if (lane == 0) pos0 = atomicAdd(&s_n, (uint32_t)__popc(bal));
+            pos0 = __shfl_sync(0xFFFFFFFFu, pos0, 0);
+            if (m) {
+                const uint32_t idx = pos0 + __popc(bal & ((1u << lane) - 1u));
+                s_env[idx] = e;
+                s_kk[idx] = first ? 0u : p.rec[rec_index(e) + REC_EPISODE * PLANE] + 1u;
+            }
+            applied += (lane == 0) ? (uint32_t)__popc(bal) : 0u;
+        }
+        __syncthreads();
+        const uint32_t n = s_n;
+        // the record chains first (latency-bound), then the lane-parallel physics rows fill the issue slots
+        for (uint32_t i = tid; i < n; i += RT_THREADS) reset_env_thread<false>(p, s_env[i], s_kk[i], s_pd, s_src);
+        for (uint32_t i = wid; i < n; i += NWR) reset_phys_warp(p, s_env[i], s_kk[i], lane, s_dr[wid], s_pd, s_src, nub, nnb);
         __syncthreads();
     }
     if (!first && applied) atomicAdd(&p.ctl[2], (unsigned long long)applied);

@@ -108,13 +108,9 @@ __device__ __forceinline__ void img_bm(uint32_t x, uint32_t y, float& z0, float&
 }
 // the same pair times sf, folded into the radius (one multiply per pair instead of per element)
 __device__ __forceinline__ void img_bm_scaled(uint32_t x, uint32_t y, float sf, float& z0, float& z1) {
-    const float u = uni(x);
-    const float v = 1.0f - u;
-    const float series = fmaf(fmaf(v, 0.333333343f, 0.5f), v * v, v);
-    const float lg = lg2_approx(u) * -0.69314718055994530942f;
-    const float nr = -sqrt_approx(2.0f * ((v < 0.015625f) ? series : lg)) * sf;
+    const float nr = -sqrt_approx(m2ln_fast(x)) * sf;
     float sn, cs;
-    __sincosf(6.28318530717958647692f * (uni(y) - 0.5f), &sn, &cs);
+    __sincosf(sfu_angle(y), &sn, &cs);
     z0 = nr * cs;
     z1 = nr * sn;
 }

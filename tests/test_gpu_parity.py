@@ -165,11 +165,11 @@ def test_reset_records_and_phys(torch_cuda):
         ctx.close()
 
 
-@pytest.mark.parametrize("version", ["2", "3", "5"])
+@pytest.mark.parametrize("version", ["2", "3", "5", "6"])
 @pytest.mark.parametrize("n", [1, 200, 2049])
 def test_reset_kernel_versions(torch_cuda, monkeypatch, version, n):
-    """Every reset kernel (DR_RESET, read at dr_init: 2 warp per env, 3 thread per env (default),
-    5 task-split) gives the oracle's episode records and physics rows -- full init, then masked
+    """Every reset kernel (DR_RESET, read at dr_init: 2 warp per env, 3 thread per env,
+    5 task-split, 6 hybrid (default): thread-per-env record + warp-per-env physics rows) gives the oracle's episode records and physics rows -- full init, then masked
     resets at two densities (a lone env, every 3rd env) -- and the steps after them agree."""
     monkeypatch.setenv("DR_RESET", version)
     torch = torch_cuda
@@ -186,6 +186,28 @@ def test_reset_kernel_versions(torch_cuda, monkeypatch, version, n):
     finally:
         ctx.close()
     run_pair(torch_cuda, FULL, n, 6, n_frames=6, resets={3: (np.arange(n) % 4 == 1).astype(np.uint8)})
+
+
+@pytest.mark.parametrize("version", ["3", "6"])
+@pytest.mark.parametrize("mask", [CFG2, PHYS, 0])
+def test_reset_kernel_layer_sets(torch_cuda, monkeypatch, version, mask):
+    """The reset kernels with PHYS off (physics rows = the descriptor bases, no draws) or alone:
+    records and physics rows equal the oracle's after init and after a masked reset."""
+    monkeypatch.setenv("DR_RESET", version)
+    torch = torch_cuda
+    n = 300
+    P = presets.preset(mask)
+    ctx = _ctx(P, n)
+    orc = _oracle(P, np.arange(n))
+    try:
+        compare_records(ctx.export(), [orc.env(i) for i in range(n)], phys_g=ctx.phys())
+        m = (np.arange(n) % 7 == 2).astype(np.uint8)
+        ctx.reset(torch.from_numpy(m).cuda())
+        orc.reset(m)
+        torch.cuda.synchronize()
+        compare_records(ctx.export(), [orc.env(i) for i in range(n)], phys_g=ctx.phys())
+    finally:
+        ctx.close()
 
 
 def test_config1_free_running(torch_cuda):
