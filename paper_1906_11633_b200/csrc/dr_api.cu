@@ -547,6 +547,8 @@ int dr_init(const dr_params* params, int64_t n_env, uint64_t seed) {
     if (c->step_grid > c->max_ctas) c->step_grid = c->max_ctas;
     const char* rv = std::getenv("DR_RESET");
     set_reset_version(rv ? std::atoi(rv) : 6);
+    const char* pdl = std::getenv("DR_PDL");
+    set_pdl(!(pdl && std::atoi(pdl) == 0));
     c->reset_grid = reset_grid_for((uint32_t)n_env, c->sm_count);
 
     // episode 0 for every env (sampled at the beginning of every episode)

@@ -186,6 +186,7 @@ constexpr int64_t LAT_MAX_ENVS = 16384;
 constexpr int LAT_ENVS_PER_CTA = 32;
 int reset_max_ctas_per_sm();
 void set_reset_version(int v);
+void set_pdl(bool on);            // programmatic dependent launch of the step / reset kernels (DR_PDL, default on)
 int reset_grid_for(uint32_t n_env, int sm_count);
 constexpr int RESET_THREADS = 256;
 constexpr int STEP_THREADS = TILE;

@@ -100,21 +100,42 @@ cudaError_t upload_const(const DevConst& c, cudaStream_t s) {
 // 3 = thread per resetting env over a compacted list (reset_kernel_t), 5 = task-split over
 // (task, env) items (reset_kernel_v5), 2 = warp per resetting env in four lane-parallel phases
 // (reset_kernel).
+// Step and reset kernels go out with cudaLaunchAttributeProgrammaticStreamSerialization: each waits
+// (griddepcontrol.wait) for the previous kernel before its first global access, so consecutive
+// steps overlap launch latency with the previous grid's tail (dr_device.cuh).  DR_PDL=0: plain launches.
+static bool g_pdl = true;
+void set_pdl(bool on) { g_pdl = on; }
+
+template <typename... KArgs, typename... Args>
+static cudaError_t launch_k(void (*kernel)(KArgs...), int grid, int block, size_t smem, cudaStream_t s, Args... args) {
+    cudaLaunchConfig_t cfg{};
+    cfg.gridDim = dim3((unsigned)grid, 1, 1);
+    cfg.blockDim = dim3((unsigned)block, 1, 1);
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = s;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    at[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = at;
+    cfg.numAttrs = g_pdl ? 1 : 0;
+    return cudaLaunchKernelEx(&cfg, kernel, args...);
+}
+
 static int g_reset_v = 6;
 void set_reset_version(int v) { g_reset_v = (v == 2 || v == 3 || v == 5) ? v : 6; }
 
 cudaError_t launch_reset(const DevPtrs& p, const uint8_t* mask, bool first, uint32_t n_env, int grid,
                          cudaStream_t s) {
-    if (g_reset_v == 2) reset_kernel<<<grid, RESET_THREADS, 0, s>>>(p, mask, first ? 1 : 0, n_env);
-    else if (g_reset_v == 5) {
+    const int f = first ? 1 : 0;
+    if (g_reset_v == 2) return launch_k(reset_kernel, grid, RESET_THREADS, 0, s, p, mask, f, n_env);
+    if (g_reset_v == 5) {
         // per-CTA range: the envs split evenly over the grid, in whole 32-env chunks, <= R5_RANGE
         const uint32_t per = (uint32_t)(((unsigned long long)n_env + grid - 1) / grid);
         const uint32_t range = std::min<uint32_t>(R5_RANGE, std::max<uint32_t>(32u, (per + 31u) & ~31u));
-        reset_kernel_v5<<<grid, R5_THREADS, 0, s>>>(p, mask, first ? 1 : 0, n_env, range);
+        return launch_k(reset_kernel_v5, grid, R5_THREADS, 0, s, p, mask, f, n_env, range);
     }
-    else if (g_reset_v == 6) reset_kernel_h<<<grid, RT_THREADS, 0, s>>>(p, mask, first ? 1 : 0, n_env);
-    else reset_kernel_t<<<grid, RT_THREADS, 0, s>>>(p, mask, first ? 1 : 0, n_env);
-    return cudaGetLastError();
+    if (g_reset_v == 6) return launch_k(reset_kernel_h, grid, RT_THREADS, 0, s, p, mask, f, n_env);
+    return launch_k(reset_kernel_t, grid, RT_THREADS, 0, s, p, mask, f, n_env);
 }
 
 int reset_grid_for(uint32_t n_env, int sm_count) {
@@ -234,9 +255,8 @@ int reset_max_ctas_per_sm() {
 cudaError_t launch_step(const DevPtrs& p, uint32_t layer_mask, const float* actions, const float* raw_obs,
                         float* out_actions, float* out_obs, float* out_dt, float* out_force, float* out_sub,
                         uint32_t n_env, int grid, cudaStream_t s) {
-    step_fn(layer_mask)<<<grid, step_threads(), step_dyn_smem(), s>>>(p, actions, raw_obs, out_actions, out_obs,
-                                                                    out_dt, out_force, out_sub, n_env);
-    return cudaGetLastError();
+    return launch_k(step_fn(layer_mask), grid, step_threads(), step_dyn_smem(), s, p, actions, raw_obs, out_actions,
+                    out_obs, out_dt, out_force, out_sub, n_env);
 }
 
 cudaError_t launch_debug_philox(uint32_t n_env, uint32_t dom, uint32_t ch, uint32_t blk, uint32_t* out, cudaStream_t s) {

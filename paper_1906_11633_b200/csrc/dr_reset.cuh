@@ -133,6 +133,7 @@ __global__ void __launch_bounds__(RESET_THREADS) reset_kernel(DevPtrs p, const u
     __shared__ uint32_t s_ph[RS_MAX_PHILOX];
     __shared__ uint32_t s_pr[RS_MAX_PAIRS];
     const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
+    pdl_wait();   // before any global access (dr_device.cuh)
     for (int i = threadIdx.x; i < c_dc.n_phys; i += RESET_THREADS) {
         s_pd[i] = p.rs_phys[i];
         s_src[i] = p.rs_src[i];
@@ -170,6 +171,7 @@ __global__ void __launch_bounds__(RESET_THREADS) reset_kernel(DevPtrs p, const u
         m_cur = m_nxt;
         ep_cur = ep_nxt;
     }
+    pdl_trigger();
     if (!first && lane == 0 && applied) atomicAdd(&p.ctl[2], (unsigned long long)applied);
 }
 
@@ -355,6 +357,7 @@ __global__ void __launch_bounds__(RT_THREADS) reset_kernel_t(DevPtrs p, const ui
     __shared__ uint32_t s_kk[RT_RANGE];
     __shared__ uint32_t s_n;
     const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
+    pdl_wait();   // before any global access (dr_device.cuh)
     constexpr int NWR = RT_THREADS / 32;
     for (int i = tid; i < c_dc.n_phys; i += RT_THREADS) {
         s_pd[i] = p.rs_phys[i];
@@ -386,6 +389,7 @@ __global__ void __launch_bounds__(RT_THREADS) reset_kernel_t(DevPtrs p, const ui
         for (uint32_t i = tid; i < n; i += RT_THREADS) reset_env_thread(p, s_env[i], s_kk[i], s_pd, s_src);
         __syncthreads();
     }
+    pdl_trigger();
     if (!first && applied) atomicAdd(&p.ctl[2], (unsigned long long)applied);
 }
 
@@ -442,6 +446,7 @@ __global__ void __launch_bounds__(RT_THREADS) reset_kernel_h(DevPtrs p, const ui
     __shared__ __align__(16) float s_dr[RT_THREADS / 32][RH_DRAW];
     __shared__ uint32_t s_n;
     const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
+    pdl_wait();   // before any global access (dr_device.cuh)
     constexpr int NWR = RT_THREADS / 32;
     for (int i = tid; i < c_dc.n_phys; i += RT_THREADS) {
         s_pd[i] = p.rs_phys[i];
@@ -476,6 +481,7 @@ __global__ void __launch_bounds__(RT_THREADS) reset_kernel_h(DevPtrs p, const ui
         for (uint32_t i = wid; i < n; i += NWR) reset_phys_warp(p, s_env[i], s_kk[i], lane, s_dr[wid], s_pd, s_src, nub, nnb);
         __syncthreads();
     }
+    pdl_trigger();
     if (!first && applied) atomicAdd(&p.ctl[2], (unsigned long long)applied);
 }
 
@@ -663,6 +669,7 @@ __global__ void __launch_bounds__(R5_THREADS, 6) reset_kernel_v5(DevPtrs p, cons
     __shared__ uint32_t s_kk[R5_RANGE];
     __shared__ uint32_t s_n;
     const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
+    pdl_wait();   // before any global access (dr_device.cuh)
     constexpr int NWR = R5_THREADS / 32;
     const int np = c_dc.n_phys;
     for (int i = tid; i < np; i += R5_THREADS) {
@@ -705,5 +712,6 @@ __global__ void __launch_bounds__(R5_THREADS, 6) reset_kernel_v5(DevPtrs p, cons
         }
         __syncthreads();
     }
+    pdl_trigger();
     if (!first && applied) atomicAdd(&p.ctl[2], (unsigned long long)applied);
 }

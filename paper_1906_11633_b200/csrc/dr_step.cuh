@@ -844,6 +844,7 @@ __device__ __forceinline__ void store_tile(uint32_t e0, uint32_t cnt, int tid, c
 // order the atomics land in (deterministic, and identical to a fixed-order sum of the rounded CTA
 // sums).  No fence, no last-CTA pass: the kernel ends when its last tile is stored.
 __device__ __forceinline__ uint32_t step_begin(const DevPtrs& p, uint32_t* s_t) {
+    pdl_wait();   // before any global access (dr_device.cuh)
     if (threadIdx.x == 0) {
         const uint32_t t = (uint32_t)*(volatile unsigned long long*)&p.ctl[0];
         unsigned long long prev;
@@ -866,6 +867,7 @@ __device__ __forceinline__ uint32_t step_begin(const DevPtrs& p, uint32_t* s_t) 
 template <uint32_t L, int NT = STEP_THREADS>
 __device__ __forceinline__ void reduce_stats(const DevPtrs& p, const Acc& acc, uint32_t my_envs, uint32_t t,
                                              double* s_red) {
+    pdl_trigger();   // this CTA's tiles are issued: the next step may launch (dr_device.cuh)
     const int tid = threadIdx.x;
     const int lane = tid & 31, wid = tid >> 5;
     constexpr int NW = NT / 32;
