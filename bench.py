@@ -47,7 +47,7 @@ def parse():
     ap.add_argument("--scaling", default="weak", choices=["weak", "strong"],
                     help="weak: every rank owns the config's env count (global = N x that); "
                          "strong: the config's env count is split over the ranks")
-    ap.add_argument("--e2e-steps", type=int, default=10)
+    ap.add_argument("--e2e-steps", type=int, default=30)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-sample-envs", type=int, default=65536)
     ap.add_argument("--cpu-sample-steps", type=int, default=24)

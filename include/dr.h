@@ -192,7 +192,10 @@ int dr_reset(const uint8_t* env_mask);
  * latency-mode kernel (8 warps split a 32-env group's transform), larger jobs the throughput
  * kernel (one thread per env, persistent tiles); the environment variable DR_STEP_MODE =
  * throughput | latency, read at dr_init, forces either.  Both give the same results within the
- * parity contract, and every shard of a job runs the same one.  Asynchronous. */
+ * parity contract, and every shard of a job runs the same one.  The step (and reset) kernels are
+ * launched with programmatic dependent launch: they wait for the previous kernel in the stream
+ * before touching memory, so ordering is unchanged (DR_PDL=0 at dr_init: plain launches).
+ * Asynchronous. */
 int dr_step(const float* actions, const float* raw_obs, float* out_actions, float* out_obs,
             float* out_dt, float* out_force);
 
