@@ -378,8 +378,11 @@ __device__ __forceinline__ float rcp_approx(float x) {
     asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(r) : "f"(x));
     return r;
 }
+// Branch-free (the MUFU.RCP is issued unconditionally; selects instead of divergent branches).
 __device__ __forceinline__ float backlash_alpha(float num, float den) {
-    return (num == 0.f) ? 1.f : ((num < den) ? c_dc.eps * rcp_approx(den) : 0.f);
+    const float rail = c_dc.eps * rcp_approx(den);
+    const float a = (num < den) ? rail : 0.f;
+    return (num == 0.f) ? 1.f : a;
 }
 
 // ---- the per-env transform -------------------------------------------------------------------
@@ -618,8 +621,8 @@ __device__ __forceinline__ void env_step(const DevPtrs& p, uint32_t e, bool vali
                 const float dx = tip[3 * i] - o[0], dy = tip[3 * i + 1] - o[1], dz = tip[3 * i + 2] - o[2];
                 const float d2 = fmaf(dz, dz, fmaf(dy, dy, dx * dx));
                 const uint32_t pair = (1u << i) | ((j < N_TIPS) ? (1u << j) : 0u);
-                if (d2 < lo) occ |= pair;
-                else if (!(d2 > hi)) amb |= 1u << (6 * i + (j - i - 1));
+                occ |= (d2 < lo) ? pair : 0u;   // selects, no divergent branches
+                amb |= (d2 < lo || d2 > hi) ? 0u : 1u << (6 * i + (j - i - 1));
             }
         }
         if (amb | c_dc.occl_exact_only) {
