@@ -508,7 +508,7 @@ __device__ __forceinline__ void env_step(const DevPtrs& p, uint32_t e, bool vali
                 an = ad + ad * (c_dc.sm * zm[q]);
                 an = an + c_dc.su * zu[q];
                 an = an + cact[q];
-                n_clamp += (an > 1.f || an < -1.f) ? 1u : 0u;
+                n_clamp += (fabsf(an) > 1.f) ? 1u : 0u;
                 an = fminf(fmaxf(an, -1.f), 1.f);
                 s_zu2 += zu[q] * zu[q];
             }
@@ -527,7 +527,7 @@ __device__ __forceinline__ void env_step(const DevPtrs& p, uint32_t e, bool vali
                 // (an == 0: the product an d dt is 0 whatever d is, so d needs no third case; alpha is 1
                 //  exactly when num == 0; a rail hit needs s' != s, which an == 0 cannot give)
                 const float s = slack[q];
-                const float sg = (an > 0.f) ? 1.f : ((an < 0.f) ? -1.f : 0.f);
+                const float sg = (an != 0.f) ? copysignf(1.f, an) : 0.f;   // sgn, sgn(0) = 0
                 const float d = (an > 0.f) ? dpos[q] : dneg[q];
                 const float sp = fminf(fmaxf(s + an * d * dt_env, -1.f), 1.f);
                 const float num = fabsf(sg - s), den = fabsf(sp - s) + c_dc.eps;
@@ -812,10 +812,13 @@ __device__ __forceinline__ void store_tile(uint32_t e0, uint32_t cnt, int tid, c
 #pragma unroll
         for (int i = tid; i < TILE * N_SUB / 4; i += STEP_THREADS) st_out(d4 + i, d4s[i]);
         // out_obs rows (22 floats = 11 float2) read from stride-26 smem rows
+        // thread (r0, k) = divmod(tid, 11), tid < 121: each pass stores 11 whole rows (121 float2,
+        // contiguous), so the row/column indices only advance -- no division per element
         float2* oo = reinterpret_cast<float2*>(out_obs + (size_t)e0 * OBS_OUT);
-        for (int i = tid; i < TILE * 11; i += STEP_THREADS) {
-            const int r = i / 11, k = i - r * 11;
-            st_out(oo + i, reinterpret_cast<const float2*>(s_obs + r * OBS_IN)[k]);
+        if (tid < 121) {
+            const int r0 = tid / 11, k = tid - r0 * 11;
+            for (int r = r0; r < TILE; r += 11)
+                st_out(oo + r * 11 + k, reinterpret_cast<const float2*>(s_obs + r * OBS_IN)[k]);
         }
         float* of = out_force + (size_t)e0 * 3;
         for (int i = tid; i < TILE * 3; i += STEP_THREADS) {

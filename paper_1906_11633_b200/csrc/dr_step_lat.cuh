@@ -101,7 +101,7 @@ __global__ void __launch_bounds__(LAT_THREADS, DR_LAT_MIN_CTAS) step_kernel_lat(
                     an = ad + ad * (c_dc.sm * zm[q]);
                     an = an + c_dc.su * zu[q];
                     an = an + cact[q];
-                    n_clamp += (an > 1.f || an < -1.f) ? 1u : 0u;
+                    n_clamp += (fabsf(an) > 1.f) ? 1u : 0u;
                     an = fminf(fmaxf(an, -1.f), 1.f);
                     s_zu2 += zu[q] * zu[q];
                 }
@@ -117,7 +117,7 @@ __global__ void __launch_bounds__(LAT_THREADS, DR_LAT_MIN_CTAS) step_kernel_lat(
 #pragma unroll
                 for (int q = 0; q < 4; ++q) {                            // [Q3, Q4]
                     const float an = anv[q], s = slack[q];
-                    const float sg = (an > 0.f) ? 1.f : ((an < 0.f) ? -1.f : 0.f);
+                    const float sg = (an != 0.f) ? copysignf(1.f, an) : 0.f;   // sgn, sgn(0) = 0
                     const float d = (an > 0.f) ? dpos[q] : dneg[q];
                     const float sp = fminf(fmaxf(s + an * d * dt_env, -1.f), 1.f);
                     const float num = fabsf(sg - s), den = fabsf(sp - s) + c_dc.eps;
