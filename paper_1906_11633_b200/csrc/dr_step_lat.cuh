@@ -11,7 +11,7 @@
 //   warp  7    object position, orientation -> relative goal, random force
 // Each warp loads its own planes straight from HBM/L2 (coalesced 128-byte lines: one env per lane)
 // and the one cross-warp dependency -- dt_env and the step words of warp 5 -- goes through shared
-// memory behind a single __syncthreads.  The arithmetic of every output is the same expression,
+// memory behind a single CTA barrier (role_barrier).  The arithmetic of every output is the same expression,
 // in the same order, as env_step's (so the same oracle parity contract holds).
 #pragma once
 
@@ -20,6 +20,12 @@ constexpr int LAT_ENVS = 32;
 #ifndef DR_LAT_MIN_CTAS
 #define DR_LAT_MIN_CTAS 2   // __launch_bounds__ occupancy target (A/B: 3 or 4 spill and run slower)
 #endif
+
+// The warp roles meet at one CTA barrier per group, reached from a different call site in each
+// role: the non-.aligned barrier.sync (all threads of a warp take the same site; sites differ across
+// warps), not __syncthreads (barrier.sync.aligned requires every thread of the CTA at the same
+// instruction -- compute-sanitizer synccheck flags it).
+__device__ __forceinline__ void role_barrier() { asm volatile("barrier.sync 0;" ::: "memory"); }
 
 template <uint32_t L>
 __global__ void __launch_bounds__(LAT_THREADS, DR_LAT_MIN_CTAS) step_kernel_lat(const DevPtrs p, const float* __restrict__ actions,
@@ -110,7 +116,7 @@ __global__ void __launch_bounds__(LAT_THREADS, DR_LAT_MIN_CTAS) step_kernel_lat(
                 s_da2 += da * da;
                 anv[q] = an;
             }
-            __syncthreads();   // dt_env / dt_k of warp 5
+            role_barrier();   // dt_env / dt_k of warp 5
             float ov[4];
             if (on<L>(B_BACKLASH) && !on<L>(B_SUBSTEP)) {
                 const float dt_env = s_dtenv[lane];
@@ -216,7 +222,7 @@ __global__ void __launch_bounds__(LAT_THREADS, DR_LAT_MIN_CTAS) step_kernel_lat(
             acc.m[0] += valid ? dt_env : 0.f;
             acc.m[1] += valid ? dt_env * dt_env : 0.f;
             my_envs += valid ? 1u : 0u;
-            __syncthreads();
+            role_barrier();
         } else if (wid == 6) {
             // ================= fingertips =================
             const float* ro = raw_obs + (size_t)ec * OBS_IN;
@@ -295,7 +301,7 @@ __global__ void __launch_bounds__(LAT_THREADS, DR_LAT_MIN_CTAS) step_kernel_lat(
                 }
             }
             acc.m[6] += valid ? s_zt : 0.f;
-            __syncthreads();   // the dropout words of warp 5
+            role_barrier();   // the dropout words of warp 5
             uint32_t masked = 0;
             if (kHold && hold_layers) {
                 uint32_t nflags = 0, n_init = 0;
@@ -398,7 +404,7 @@ __global__ void __launch_bounds__(LAT_THREADS, DR_LAT_MIN_CTAS) step_kernel_lat(
                 st_out(oo + 19, obj[0]);
                 st_out(o2 + 10, make_float2(obj[1], obj[2]));
             }
-            __syncthreads();   // the force trigger word of warp 5
+            role_barrier();   // the force trigger word of warp 5
             float f[3] = {0.f, 0.f, 0.f};
             if (on<L>(B_FORCE)) {                                        // [Q17, Q18]
                 const uint32_t x = s_wd[5][lane];                        // step word 15
