@@ -879,23 +879,30 @@ __device__ __forceinline__ void reduce_stats(const DevPtrs& p, const Acc& acc, u
     constexpr int NW = NT / 32;
     __syncthreads();
     {
+        // counts: one REDUX.SUM per slot (32-bit integer warp sums, exact); moments: fp64 butterflies
+        auto redc = [&](int i, uint32_t x) {
+            const uint32_t v = __reduce_add_sync(0xFFFFFFFFu, x);
+            if (lane == 0) s_red[i * NW + wid] = (double)v;
+            return v;
+        };
         auto red = [&](int i, double x) {
 #pragma unroll
             for (int o = 16; o > 0; o >>= 1) x += __shfl_xor_sync(0xFFFFFFFFu, x, o);
             if (lane == 0) s_red[i * NW + wid] = x;
         };
-        red(0, (double)my_envs);
-        red(1, (double)acc.n[K_DELAYED]);
-        red(2, (double)acc.n[K_DROP_INIT]);
-        red(3, (double)acc.n[K_MASKED]);
-        red(4, (double)acc.n[K_OCCLUDED]);
-        red(5, (double)acc.n[K_HELD]);
-        red(6, (double)acc.n[K_TRIG]);
-        red(7, (double)acc.n[K_RAIL]);
-        red(8, (double)acc.n[K_ALPHA1]);
-        red(9, on<L>(B_BACKLASH) ? (double)my_envs * N_ACT * (on<L>(B_SUBSTEP) ? N_SUB : 1) - (double)acc.n[K_ALPHA1]
-                                 : 0.0);
-        red(11, (double)acc.n[K_CLAMPS]);
+        const uint32_t envs = redc(0, my_envs);
+        redc(1, acc.n[K_DELAYED]);
+        redc(2, acc.n[K_DROP_INIT]);
+        redc(3, acc.n[K_MASKED]);
+        redc(4, acc.n[K_OCCLUDED]);
+        redc(5, acc.n[K_HELD]);
+        redc(6, acc.n[K_TRIG]);
+        redc(7, acc.n[K_RAIL]);
+        const uint32_t a1 = redc(8, acc.n[K_ALPHA1]);
+        if (lane == 0)   // gated actuator-steps (alpha < 1) = actuator-steps - alpha-1 count
+            s_red[9 * NW + wid] = on<L>(B_BACKLASH)
+                                      ? (double)envs * N_ACT * (on<L>(B_SUBSTEP) ? N_SUB : 1) - (double)a1 : 0.0;
+        redc(11, acc.n[K_CLAMPS]);
 #pragma unroll
         for (int i = 0; i < 8; ++i) red(16 + i, (double)acc.m[i]);
     }
