@@ -403,7 +403,10 @@ __global__ void __launch_bounds__(RT_THREADS) reset_kernel_t(DevPtrs p, const ui
 // parameter-level parallelism instead of one serial chain.  Same channels, words, transforms and
 // operation order as reset_env_thread (bit-identical results).
 // =====================================================================================
-constexpr int RH_DRAW = 2 * MAX_PHYS;   // per-warp draw buffer: uniforms at [0, 256), normals at [256, 512)
+// per-warp draw buffer: uniforms at [0, 256), normals at [256, 512), a constant 0 at 512 (the x of
+// draw-free descriptors).  s_src holds, per parameter, the buffer offset of its x | RH_EXP.
+constexpr int RH_DRAW = 2 * MAX_PHYS + 4;
+constexpr uint32_t RH_EXP = 1u << 31;
 
 __device__ __forceinline__ void reset_phys_warp(const DevPtrs& p, uint32_t e, uint32_t k, int lane, float* dr,
                                                 const float4* s_pd, const uint32_t* s_src, int nub, int nnb) {
@@ -423,18 +426,23 @@ __device__ __forceinline__ void reset_phys_warp(const DevPtrs& p, uint32_t e, ui
         }
     }
     __syncwarp();
-    const int np = c_dc.n_phys;
+    const int np = c_dc.n_phys, mi = c_dc.mass_index;
     float* prow = p.phys + (size_t)e * np;
-    for (int q = lane; q < np; q += 32) {
-        const float4 d = s_pd[q];   // (A, B, C0, C1)
-        const uint32_t src = s_src[q];
-        float x = 0.f;
-        if (src & RS_SRC_DRAW) x = dr[(src & RS_SRC_IDX) + ((src & RS_SRC_NORMAL) ? MAX_PHYS : 0)];
-        const float tv = fmaf(d.y, x, d.x);
-        const float v = fmaf(d.w, (src & RS_SRC_EXP) ? ex2_approx(tv) : tv, d.z);
-        prow[q] = v;
-        if (q == c_dc.mass_index) p.rec[rec_index(e) + REC_MASS * PLANE] = __float_as_uint(v);   // [Q18]
+    float vm = 0.f;
+#pragma unroll
+    for (int i = 0; i < MAX_PHYS / 32; ++i) {
+        const int q = lane + 32 * i;
+        if (q < np) {
+            const float4 d = s_pd[q];   // (A, B, C0, C1)
+            const uint32_t o = s_src[q];
+            const float x = dr[o & ~RH_EXP];
+            const float tv = fmaf(d.y, x, d.x);
+            const float v = fmaf(d.w, (o & RH_EXP) ? ex2_approx(tv) : tv, d.z);
+            prow[q] = v;
+            if (i == (mi >> 5)) vm = v;
+        }
     }
+    if (lane == (mi & 31)) p.rec[rec_index(e) + REC_MASS * PLANE] = __float_as_uint(vm);   // the object mass [Q18]
 }
 
 __global__ void __launch_bounds__(RT_THREADS) reset_kernel_h(DevPtrs p, const uint8_t* __restrict__ mask, int first,
@@ -450,8 +458,11 @@ __global__ void __launch_bounds__(RT_THREADS) reset_kernel_h(DevPtrs p, const ui
     constexpr int NWR = RT_THREADS / 32;
     for (int i = tid; i < c_dc.n_phys; i += RT_THREADS) {
         s_pd[i] = p.rs_phys[i];
-        s_src[i] = p.rs_src[i];
+        const uint32_t src = p.rs_src[i];   // -> draw-buffer offset of x | RH_EXP (the record part does not read it)
+        const uint32_t off = (src & RS_SRC_DRAW) ? (src & RS_SRC_IDX) + ((src & RS_SRC_NORMAL) ? MAX_PHYS : 0) : 2 * MAX_PHYS;
+        s_src[i] = off | ((src & RS_SRC_EXP) ? RH_EXP : 0u);
     }
+    if (lane == 0) s_dr[wid][2 * MAX_PHYS] = 0.f;
     const bool phys_on = (c_dc.layer_mask & B_PHYS) != 0;
     const int nub = phys_on ? (c_dc.n_phys_u + 3) / 4 : 0;
     const int nnb = phys_on ? (c_dc.n_phys_n + 3) / 4 : 0;
