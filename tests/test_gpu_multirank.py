@@ -106,3 +106,36 @@ def test_bench_torchrun_two_ranks_gloo():
     assert d["config"]["n_env_global"] == 2 * 32768
     assert d["stats_check"]["envs_last_step"] == 2 * 32768   # the all-reduced stats cover both ranks
     assert d["gpu_launches"] == 20
+
+
+def _nccl_worker(rank, world, port, out_dir):
+    import torch
+    import torch.distributed as dist
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port), RANK=str(rank), WORLD_SIZE=str(world))
+    torch.cuda.set_device(0)
+    dist.init_process_group("nccl", rank=rank, world_size=world, device_id=torch.device("cuda", 0))
+    from paper_1906_11633_b200 import DRContext
+    from paper_1906_11633_b200.parallel import StatsReducer
+    outs, stats = _run(torch, lambda s: DRContext(presets.preset(presets.FULL), N_GLOBAL, SEED, stream=s), 0,
+                       N_GLOBAL, lambda ctx, s: StatsReducer(ctx.stats, s))
+    np.save(os.path.join(out_dir, "outs.npy"), outs)
+    np.save(os.path.join(out_dir, "stats.npy"), stats)
+    dist.barrier()
+    dist.destroy_process_group()
+
+
+def test_nccl_stats_reducer_single_rank(tmp_path):
+    """The NCCL backend path of the StatsReducer (all-reduce on the comm stream, event ordering,
+    the ring of 4 slots) with one rank -- the only NCCL configuration one GPU allows: the reduced
+    stats equal the local ones and the outputs equal a run without the reducer."""
+    import torch
+    import torch.multiprocessing as mp
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    mp.spawn(_nccl_worker, args=(1, _free_port(), str(tmp_path)), nprocs=1, join=True)
+    from paper_1906_11633_b200 import DRContext
+    torch.cuda.set_device(0)
+    ref_out, ref_st = _run(torch, lambda s: DRContext(presets.preset(presets.FULL), N_GLOBAL, SEED, stream=s),
+                           0, N_GLOBAL)
+    assert np.array_equal(np.load(tmp_path / "outs.npy"), ref_out)
+    assert np.array_equal(np.load(tmp_path / "stats.npy"), ref_st)
