@@ -31,7 +31,7 @@ enum : uint32_t { CH_POSE = 0x401, CH_IMG_PARAM = 0x201, CH_IMG_NOISE = 0x202, C
 
 constexpr int IMG_THREADS = 256;
 #ifndef DR_IMG_ILP
-#define DR_IMG_ILP 2   // A/B
+#define DR_IMG_ILP 4   // A/B: 4 measured 40.55 vs 40.97 us per 192-image batch for 2 (three alternating runs)
 #endif
 constexpr int IMG_ILP = DR_IMG_ILP;
 constexpr uint32_t IMG_SLICE_MAX = 200 * 1024;
