@@ -134,7 +134,7 @@ cudaError_t launch_reset(const DevPtrs& p, const uint8_t* mask, bool first, uint
         const uint32_t range = std::min<uint32_t>(R5_RANGE, std::max<uint32_t>(32u, (per + 31u) & ~31u));
         return launch_k(reset_kernel_v5, grid, R5_THREADS, 0, s, p, mask, f, n_env, range);
     }
-    if (g_reset_v == 6) return launch_k(reset_kernel_h, grid, RT_THREADS, 0, s, p, mask, f, n_env);
+    if (g_reset_v == 6) return launch_k(reset_kernel_h, grid, RH_THREADS, 0, s, p, mask, f, n_env);
     return launch_k(reset_kernel_t, grid, RT_THREADS, 0, s, p, mask, f, n_env);
 }
 
@@ -151,7 +151,12 @@ int reset_grid_for(uint32_t n_env, int sm_count) {
         const long long ranges = (n_env + 31) / 32;
         return (int)std::max<long long>(1, std::min<long long>(ranges, (long long)sm_count * n));
     }
-    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, g_reset_v == 6 ? reset_kernel_h : reset_kernel_t, RT_THREADS, 0) != cudaSuccess || n < 1) n = 1;
+    if (g_reset_v == 6) {
+        if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, reset_kernel_h, RH_THREADS, 0) != cudaSuccess || n < 1) n = 1;
+        const long long ranges = (n_env + RH_RANGE - 1) / RH_RANGE;
+        return (int)std::max<long long>(1, std::min<long long>(ranges, (long long)sm_count * n));
+    }
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, reset_kernel_t, RT_THREADS, 0) != cudaSuccess || n < 1) n = 1;
     const long long ranges = (n_env + RT_RANGE - 1) / RT_RANGE;
     return (int)std::max<long long>(1, std::min<long long>(ranges, (long long)sm_count * n));
 }

@@ -406,6 +406,20 @@ __global__ void __launch_bounds__(RT_THREADS) reset_kernel_t(DevPtrs p, const ui
 // per-warp draw buffer: uniforms at [0, 256), normals at [256, 512), a constant 0 at 512 (the x of
 // draw-free descriptors).  s_src holds, per parameter, the buffer offset of its x | RH_EXP.
 constexpr int RH_DRAW = 2 * MAX_PHYS + 4;
+// CTA shape of reset_kernel_h (A/B: DR_RH_THREADS / DR_RH_RANGE): threads, envs scanned per pass.
+// Config 5 (1M envs, 10 % resets), reset ms per launch, three runs each: 256/2048 0.202,
+// 256/1024 0.168, 128/1024 0.193, 128/512 0.165-0.170, 512/1024 0.158, 512/512 0.167,
+// 256/512 0.151-0.152, 128/256 0.151, 256/256 0.163, 128/128 0.153, 64/256 0.169, 64/128 0.188.
+// Small ranges (~51 resetting envs per CTA at 10 %) give thousands of short CTAs whose record
+// chains and physics warps from different CTAs overlap on each SM, with a small tail.
+#ifndef DR_RH_THREADS
+#define DR_RH_THREADS 256
+#endif
+#ifndef DR_RH_RANGE
+#define DR_RH_RANGE 512
+#endif
+constexpr int RH_THREADS = DR_RH_THREADS;
+constexpr uint32_t RH_RANGE = DR_RH_RANGE;
 constexpr uint32_t RH_EXP = 1u << 31;
 
 __device__ __forceinline__ void reset_phys_warp(const DevPtrs& p, uint32_t e, uint32_t k, int lane, float* dr,
@@ -445,18 +459,18 @@ __device__ __forceinline__ void reset_phys_warp(const DevPtrs& p, uint32_t e, ui
     if (lane == (mi & 31)) p.rec[rec_index(e) + REC_MASS * PLANE] = __float_as_uint(vm);   // the object mass [Q18]
 }
 
-__global__ void __launch_bounds__(RT_THREADS) reset_kernel_h(DevPtrs p, const uint8_t* __restrict__ mask, int first,
+__global__ void __launch_bounds__(RH_THREADS) reset_kernel_h(DevPtrs p, const uint8_t* __restrict__ mask, int first,
                                                              uint32_t n_env) {
     __shared__ float4 s_pd[MAX_PHYS];
     __shared__ uint32_t s_src[MAX_PHYS];
-    __shared__ uint32_t s_env[RT_RANGE];
-    __shared__ uint32_t s_kk[RT_RANGE];
-    __shared__ __align__(16) float s_dr[RT_THREADS / 32][RH_DRAW];
+    __shared__ uint32_t s_env[RH_RANGE];
+    __shared__ uint32_t s_kk[RH_RANGE];
+    __shared__ __align__(16) float s_dr[RH_THREADS / 32][RH_DRAW];
     __shared__ uint32_t s_n;
     const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
     pdl_wait();   // before any global access (dr_device.cuh)
-    constexpr int NWR = RT_THREADS / 32;
-    for (int i = tid; i < c_dc.n_phys; i += RT_THREADS) {
+    constexpr int NWR = RH_THREADS / 32;
+    for (int i = tid; i < c_dc.n_phys; i += RH_THREADS) {
         s_pd[i] = p.rs_phys[i];
         const uint32_t src = p.rs_src[i];   // -> draw-buffer offset of x | RH_EXP (the record part does not read it)
         const uint32_t off = (src & RS_SRC_DRAW) ? (src & RS_SRC_IDX) + ((src & RS_SRC_NORMAL) ? MAX_PHYS : 0) : 2 * MAX_PHYS;
@@ -467,10 +481,10 @@ __global__ void __launch_bounds__(RT_THREADS) reset_kernel_h(DevPtrs p, const ui
     const int nub = phys_on ? (c_dc.n_phys_u + 3) / 4 : 0;
     const int nnb = phys_on ? (c_dc.n_phys_n + 3) / 4 : 0;
     uint32_t applied = 0;
-    for (uint32_t base = blockIdx.x * RT_RANGE; base < n_env; base += gridDim.x * RT_RANGE) {
+    for (uint32_t base = blockIdx.x * RH_RANGE; base < n_env; base += gridDim.x * RH_RANGE) {
         if (tid == 0) s_n = 0u;
         __syncthreads();
-        for (uint32_t c = wid; c < RT_RANGE / 32; c += NWR) {
+        for (uint32_t c = wid; c < RH_RANGE / 32; c += NWR) {
             const uint32_t e = base + c * 32u + lane;
             const bool m = e < n_env && (mask == nullptr || mask[e] != 0);
             const uint32_t bal = __ballot_sync(0xFFFFFFFFu, m);
@@ -488,7 +502,7 @@ __global__ void __launch_bounds__(RT_THREADS) reset_kernel_h(DevPtrs p, const ui
         __syncthreads();
         const uint32_t n = s_n;
         // the record chains first (latency-bound), then the lane-parallel physics rows fill the issue slots
-        for (uint32_t i = tid; i < n; i += RT_THREADS) reset_env_thread<false>(p, s_env[i], s_kk[i], s_pd, s_src);
+        for (uint32_t i = tid; i < n; i += RH_THREADS) reset_env_thread<false>(p, s_env[i], s_kk[i], s_pd, s_src);
         for (uint32_t i = wid; i < n; i += NWR) reset_phys_warp(p, s_env[i], s_kk[i], lane, s_dr[wid], s_pd, s_src, nub, nnb);
         __syncthreads();
     }
