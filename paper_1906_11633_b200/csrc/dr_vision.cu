@@ -29,7 +29,10 @@ namespace dr {
 enum : uint32_t { CH_POSE = 0x401, CH_IMG_PARAM = 0x201, CH_IMG_NOISE = 0x202, CH_SCENE_CAM = 0x301, CH_SCENE_MAT = 0x302,
                   CH_SCENE_LIGHT = 0x303 };
 
-constexpr int IMG_THREADS = 256;
+#ifndef DR_IMG_THREADS
+#define DR_IMG_THREADS 256   // A/B (us per 192-image batch): 128 41.1, 256 40.2, 512 43.3
+#endif
+constexpr int IMG_THREADS = DR_IMG_THREADS;
 #ifndef DR_IMG_ILP
 #define DR_IMG_ILP 4   // A/B: 4 measured 40.55 vs 40.97 us per 192-image batch for 2 (three alternating runs)
 #endif
