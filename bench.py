@@ -522,9 +522,17 @@ def main():
     e2e = None
     if not args.profile and args.e2e_steps > 0:
         with torch.cuda.stream(lib_stream):
-            ha = A[0].cpu().pin_memory()
-            ho = O[0].cpu().pin_memory()
-            outs = [torch.empty(n, c).pin_memory() for c in (20, 22, 10, 3)]
+            # one pinned allocation each way (inputs [n*20 | n*26], outputs [n*20 | n*22 | n*10 | n*3]),
+            # so dr_step_host moves each direction in one copy (include/dr.h)
+            hin = torch.empty(n * (20 + 26)).pin_memory()
+            ha, ho = hin[:n * 20].view(n, 20), hin[n * 20:].view(n, 26)
+            ha.copy_(A[0].cpu())
+            ho.copy_(O[0].cpu())
+            hout = torch.empty(n * (20 + 22 + 10 + 3)).pin_memory()
+            outs, o = [], 0
+            for c in (20, 22, 10, 3):
+                outs.append(hout[o:o + n * c].view(n, c))
+                o += n * c
             dr.dr_step_host(ha, ho, *outs)
             dr.dr_synchronize()
             if world > 1:

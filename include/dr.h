@@ -215,7 +215,10 @@ int dr_step_substeps(const float* actions, const float* raw_obs, float* out_acti
  * stream, the D2H on a second copy stream, ordered by events, so call t+1's upload overlaps call
  * t's download and compute.  Asynchronous if the host buffers are pinned (cudaHostAlloc / torch
  * pin_memory): the caller must not modify an input buffer or read an output buffer of a call
- * until dr_synchronize(), which waits for all three streams.  DR_EINVAL for
+ * until dr_synchronize(), which waits for all three streams.  If raw_obs directly follows
+ * actions in host memory (one [n][20 + 26] allocation), the upload is one copy; if out_obs,
+ * out_dt and out_force directly follow out_actions (one [n][20 + 22 + 10 + 3] allocation, n even),
+ * the download is one copy -- fewer per-copy latencies for small n.  DR_EINVAL for
  * DR_SUBSTEP_BACKLASH contexts. */
 int dr_step_host(const float* actions, const float* raw_obs, float* out_actions, float* out_obs,
                  float* out_dt, float* out_force);

@@ -672,8 +672,16 @@ int dr_step_host(const float* actions, const float* raw_obs, float* out_actions,
     float* d_f = d_dt + up16(fdt);
     // inputs of call t: after kernel t-2 is done reading this set
     if (t >= 2) CK(cudaStreamWaitEvent(c->s_h2d, c->ev_k[b], 0));
-    CK(cudaMemcpyAsync(d_a, actions, fa * 4, cudaMemcpyHostToDevice, c->s_h2d));
-    CK(cudaMemcpyAsync(d_o, raw_obs, fo * 4, cudaMemcpyHostToDevice, c->s_h2d));
+    // host buffers laid out back to back (one allocation, as the device set is): one copy each way
+    const bool in_one = raw_obs == actions + fa && d_o == d_a + fa;
+    const bool out_one = out_obs == out_actions + foa && out_dt == out_obs + foo && out_force == out_dt + fdt &&
+                         d_oo == d_oa + foa && d_dt == d_oo + foo && d_f == d_dt + fdt;
+    if (in_one) {
+        CK(cudaMemcpyAsync(d_a, actions, (fa + fo) * 4, cudaMemcpyHostToDevice, c->s_h2d));
+    } else {
+        CK(cudaMemcpyAsync(d_a, actions, fa * 4, cudaMemcpyHostToDevice, c->s_h2d));
+        CK(cudaMemcpyAsync(d_o, raw_obs, fo * 4, cudaMemcpyHostToDevice, c->s_h2d));
+    }
     CK(cudaEventRecord(c->ev_h[b], c->s_h2d));
     // the step: after its inputs landed and the outputs of call t-2 left this set
     CK(cudaStreamWaitEvent(c->stream, c->ev_h[b], 0));
@@ -683,10 +691,14 @@ int dr_step_host(const float* actions, const float* raw_obs, float* out_actions,
     CK(cudaEventRecord(c->ev_k[b], c->stream));
     // outputs of call t
     CK(cudaStreamWaitEvent(c->s_d2h, c->ev_k[b], 0));
-    CK(cudaMemcpyAsync(out_actions, d_oa, foa * 4, cudaMemcpyDeviceToHost, c->s_d2h));
-    CK(cudaMemcpyAsync(out_obs, d_oo, foo * 4, cudaMemcpyDeviceToHost, c->s_d2h));
-    CK(cudaMemcpyAsync(out_dt, d_dt, fdt * 4, cudaMemcpyDeviceToHost, c->s_d2h));
-    CK(cudaMemcpyAsync(out_force, d_f, ff * 4, cudaMemcpyDeviceToHost, c->s_d2h));
+    if (out_one) {
+        CK(cudaMemcpyAsync(out_actions, d_oa, (foa + foo + fdt + ff) * 4, cudaMemcpyDeviceToHost, c->s_d2h));
+    } else {
+        CK(cudaMemcpyAsync(out_actions, d_oa, foa * 4, cudaMemcpyDeviceToHost, c->s_d2h));
+        CK(cudaMemcpyAsync(out_obs, d_oo, foo * 4, cudaMemcpyDeviceToHost, c->s_d2h));
+        CK(cudaMemcpyAsync(out_dt, d_dt, fdt * 4, cudaMemcpyDeviceToHost, c->s_d2h));
+        CK(cudaMemcpyAsync(out_force, d_f, ff * 4, cudaMemcpyDeviceToHost, c->s_d2h));
+    }
     CK(cudaEventRecord(c->ev_d[b], c->s_d2h));
     c->host_calls = t + 1;
     return DR_OK;

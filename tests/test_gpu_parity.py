@@ -482,6 +482,43 @@ def test_workspace_adoption_and_host_path(torch_cuda):
     ctx.close()
 
 
+@pytest.mark.parametrize("n", [777, 778])
+def test_host_path_contiguous_buffers(torch_cuda, n):
+    """dr_step_host with the inputs and the outputs each in one host allocation (the one-copy
+    paths: inputs always merge; outputs merge for even n, where the device set has no padding)
+    gives the device path's bits, pipelined over three calls."""
+    torch = torch_cuda
+    from paper_1906_11633_b200 import dr
+    P = presets.preset(FULL)
+    acts, obs = gen.frames(n, 3)
+    A, O = _frames_cuda(torch, acts), _frames_cuda(torch, obs)
+    ctx = _ctx(P, n)
+    ref = []
+    for t in range(3):
+        ctx.step(A[t], O[t])
+        ref.append([x.cpu().numpy() for x in (ctx.out_actions, ctx.out_obs, ctx.out_dt, ctx.out_force)])
+    ctx.close()
+    ctx = _ctx(P, n)
+    hins, houts = [], []
+    for t in range(3):
+        hin = torch.empty(n * 46).pin_memory()
+        hin[:n * 20].copy_(torch.from_numpy(acts[t]).reshape(-1))
+        hin[n * 20:].copy_(torch.from_numpy(obs[t]).reshape(-1))
+        hout = torch.full((n * 55,), float("nan")).pin_memory()
+        views, o = [], 0
+        for c in (20, 22, 10, 3):
+            views.append(hout[o:o + n * c].view(n, c))
+            o += n * c
+        hins.append((hin[:n * 20].view(n, 20), hin[n * 20:].view(n, 26)))
+        houts.append(views)
+        dr.dr_step_host(*hins[t], *houts[t])
+    dr.dr_synchronize()
+    for t in range(3):
+        for u, v in zip(houts[t], ref[t]):
+            assert np.array_equal(u.numpy(), v), t
+    ctx.close()
+
+
 def test_value_view_isolation_and_invariants_1M(torch_cuda):
     """Inputs are never written; GPU-only invariants over every env of a 1M-env
     full-pipeline run: |a_out| <= 1, dt_k >= 8 ms, relative-goal w >= 0 and unit norm, slack in
