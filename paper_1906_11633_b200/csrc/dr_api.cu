@@ -545,6 +545,12 @@ int dr_init(const dr_params* params, int64_t n_env, uint64_t seed) {
                                 : (uint32_t)((n_env + TILE - 1) / TILE);
     c->step_grid = (int)std::min<long long>((long long)units, (long long)c->sm_count * occ_step);
     if (c->step_grid > c->max_ctas) c->step_grid = c->max_ctas;
+    // A/B: persistent grid size (clamped to the default). 1M envs: 592 (default) 4.90e9, 586 4.89e9,
+    // 546 4.75e9, 512 4.60e9, 444 4.73e9 env-steps/s
+    if (const char* sg = std::getenv("DR_STEP_GRID")) {
+        const int v = std::atoi(sg);
+        if (v >= 1 && v < c->step_grid) c->step_grid = v;
+    }
     const char* rv = std::getenv("DR_RESET");
     set_reset_version(rv ? std::atoi(rv) : 6);
     const char* pdl = std::getenv("DR_PDL");
