@@ -418,6 +418,9 @@ constexpr int RH_DRAW = 2 * MAX_PHYS + 4;
 #ifndef DR_RH_RANGE
 #define DR_RH_RANGE 512
 #endif
+#ifndef DR_RH_MINB
+#define DR_RH_MINB 1   // __launch_bounds__ min CTAs per SM (A/B, reset ms: 1 (56 regs) 0.156, 5 0.165, 6 0.165, 8 0.169)
+#endif
 constexpr int RH_THREADS = DR_RH_THREADS;
 constexpr uint32_t RH_RANGE = DR_RH_RANGE;
 constexpr uint32_t RH_EXP = 1u << 31;
@@ -459,7 +462,7 @@ __device__ __forceinline__ void reset_phys_warp(const DevPtrs& p, uint32_t e, ui
     if (lane == (mi & 31)) p.rec[rec_index(e) + REC_MASS * PLANE] = __float_as_uint(vm);   // the object mass [Q18]
 }
 
-__global__ void __launch_bounds__(RH_THREADS) reset_kernel_h(DevPtrs p, const uint8_t* __restrict__ mask, int first,
+__global__ void __launch_bounds__(RH_THREADS, DR_RH_MINB) reset_kernel_h(DevPtrs p, const uint8_t* __restrict__ mask, int first,
                                                              uint32_t n_env) {
     __shared__ float4 s_pd[MAX_PHYS];
     __shared__ uint32_t s_src[MAX_PHYS];
