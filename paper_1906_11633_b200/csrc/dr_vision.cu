@@ -741,20 +741,63 @@ bool g_img_attr_set = false;
 
 uint32_t img_slice_of(uint64_t E, uint32_t K) { return (uint32_t)(((E + K - 1) / K + 15) / 16 * 16); }
 
-// Cluster size: the smallest K in {1, 2, 4, 8} whose slice fits 32 KB, else the smallest whose
-// slice fits 200 KB.  A/B (B200, 192 images of 200 x 200 x 3, us per batch): K = 3 44.1, K = 4 41.0,
-// K = 6 45.2 (only 187 clusters of 6 co-resident: a second wave), K = 8 45-51 -- the per-SM
-// balance of slices is not what bounds the kernel, so the simple rule stays.
-// DR_IMG_K=1..8 forces K.
-uint32_t img_cluster_size(uint64_t E, uint64_t /*n*/) {
+// Cluster size K (1..8, DR_IMG_K=1..8 forces it).  Images whose slice fits 32 KB at some K <= 8:
+// among the K with slice <= 32 KB (and >= 8 KB, or K = 1), the one minimising waves x slice bytes,
+// with waves = ceil(n_images / co-resident clusters of K) from cudaOccupancyMaxActiveClusters --
+// the per-CTA time scales with its slice and a partial second wave doubles it.  Measured (B200,
+// 192 images of 200 x 200 x 3, us per batch): K = 3 43.2, 4 40.0, 5 39.2 (chosen), 6 44.5
+// (187 co-resident clusters < 192: two waves), 7 44.0, 8 44.2.  Larger images: the smallest
+// power of two whose slice fits 200 KB.
+uint32_t img_cluster_size(uint64_t E, uint64_t n) {
     static const int forced = [] {
         const char* v = std::getenv("DR_IMG_K");
         return v ? std::atoi(v) : 0;
     }();
     if (forced >= 1 && forced <= 8 && img_slice_of(E, (uint32_t)forced) <= IMG_SLICE_MAX) return (uint32_t)forced;
-    uint32_t K = 1;
-    while (K < 8 && img_slice_of(E, K) > 32u * 1024u) K *= 2;
-    return K;
+    if (img_slice_of(E, 8) > 32u * 1024u) {   // large images: the smallest power of two that fits
+        uint32_t K = 1;
+        while (K < 8 && img_slice_of(E, K) > 32u * 1024u) K *= 2;
+        return K;
+    }
+    thread_local uint64_t c_E = 0, c_n = 0;
+    thread_local uint32_t c_K = 0;
+    if (c_E == E && c_n == n && c_K) return c_K;
+    uint32_t best = 0;
+    double best_cost = 0.0;
+    for (uint32_t K = 1; K <= 8; ++K) {
+        const uint32_t sl = img_slice_of(E, K);
+        if (sl > 32u * 1024u || (K > 1 && sl < 8u * 1024u)) continue;
+        cudaLaunchConfig_t cfg{};
+        cfg.gridDim = dim3(K, 1, 1);
+        cfg.blockDim = dim3(IMG_THREADS, 1, 1);
+        cfg.dynamicSmemBytes = sl;
+        cudaLaunchAttribute attr[1];
+        attr[0].id = cudaLaunchAttributeClusterDimension;
+        attr[0].val.clusterDim.x = K;
+        attr[0].val.clusterDim.y = 1;
+        attr[0].val.clusterDim.z = 1;
+        cfg.attrs = attr;
+        cfg.numAttrs = 1;
+        int clusters = 0;
+        if (cudaOccupancyMaxActiveClusters(&clusters, dr::image_augment_kernel, &cfg) != cudaSuccess || clusters < 1) {
+            cudaGetLastError();
+            continue;
+        }
+        const double waves = (double)((n + (uint64_t)clusters - 1) / (uint64_t)clusters);
+        const double cost = waves * (double)sl;
+        if (!best || cost < best_cost) {
+            best = K;
+            best_cost = cost;
+        }
+    }
+    if (!best) {   // no occupancy answer: the smallest power of two whose slice fits 32 KB
+        best = 1;
+        while (best < 8 && img_slice_of(E, best) > 32u * 1024u) best *= 2;
+    }
+    c_E = E;
+    c_n = n;
+    c_K = best;
+    return best;
 }
 
 // The two-pass augmentation (image_moments_kernel, image_noise_kernel).  The per-image constants
@@ -844,6 +887,12 @@ int dr_image_augment(const dr_vision_params* p, uint64_t seed, uint64_t batch_in
     if (mode && std::strcmp(mode, "two_pass") == 0)
         return image_augment_two_pass(p, seed, batch_index, image_offset, images, n_images, E, out, img_stats,
                                       static_cast<cudaStream_t>(stream));
+    if (!g_img_attr_set) {   // once per process (the attribute is per function, not per launch)
+        const cudaError_t ea = cudaFuncSetAttribute(image_augment_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                                    (int)IMG_SLICE_MAX);
+        if (ea != cudaSuccess) return set_error(DR_ECUDA, "cudaFuncSetAttribute: %s", cudaGetErrorString(ea));
+        g_img_attr_set = true;
+    }
     const uint32_t K = img_cluster_size(E, (uint64_t)n_images);
     const uint32_t slice = img_slice_of(E, K);
     if (slice > IMG_SLICE_MAX) return set_error(DR_EUNSUPPORTED, "image slice of %u bytes too large", slice);
@@ -863,11 +912,6 @@ int dr_image_augment(const dr_vision_params* p, uint64_t seed, uint64_t batch_in
     a.std_floor = p->std_floor;
     a.keys = make_keys(seed);
     cudaError_t e = cudaSuccess;
-    if (!g_img_attr_set) {   // once per process (the attribute is per function, not per launch)
-        e = cudaFuncSetAttribute(image_augment_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)IMG_SLICE_MAX);
-        if (e != cudaSuccess) return set_error(DR_ECUDA, "cudaFuncSetAttribute: %s", cudaGetErrorString(e));
-        g_img_attr_set = true;
-    }
     cudaLaunchConfig_t cfg{};
     cfg.gridDim = dim3((unsigned)(n_images * K), 1, 1);
     cfg.blockDim = dim3(IMG_THREADS, 1, 1);
