@@ -104,7 +104,7 @@ typedef struct dr_params {
     /* backlash */
     double delta_cal_neg[DR_N_ACT], delta_cal_pos[DR_N_ACT]; /* calibrated widths (>= 0) */
     double delta_jitter_std;     /* 0.1 */
-    double backlash_eps;         /* 1e-12 */
+    double backlash_eps;         /* 1e-12; must be in [0, 1e-8] (DR_EINVAL otherwise) */
     /* observation noise std, metres / radians (Table obs-noise) */
     double tip_corr, tip_uncorr, obj_corr, obj_uncorr, rot_corr, rot_uncorr, tip_marker, base_marker;
     int32_t base_marker_to_tips; /* 1: hand-base marker error shifts all tips (Q14) */
@@ -250,6 +250,10 @@ int      dr_n_phys(void);
 const double* dr_stats(int slot);
 int      dr_set_stats_buffer(double* dev_buf);
 uint64_t dr_step_index(void);               /* host count of enqueued steps (== device t unless graph-replayed) */
+/* Blocking: waits for the library stream and returns the device step counter t (the index of the
+ * next step; CUDA-graph replays of dr_step advance it too), and resets the host count to it.  The
+ * stats of the last completed step are then in slot (t - 1) % DR_STAT_SLOTS. */
+uint64_t dr_step_index_sync(void);
 int      dr_set_step_index(uint64_t t);     /* blocking; for resume (also clears the stats ring) */
 size_t   dr_state_bytes(void);              /* sizeof(dr_env_state) * n_env */
 /* Blocking copies of per-env state for envs [env_lo, env_hi) (local indices); lo = hi = 0

@@ -191,6 +191,7 @@ struct orc_ctx {
     double p_tab[P_TABLE_N];
     uint64_t t_tab[P_TABLE_N];
     orc_env* env;
+    double* st_env;             /* [n][ORC_N_STATS] per-env stats contributions of the current step */
     const uint8_t* occl_mask;   /* simulator occlusion bits per env, or NULL (distance rule) */
 };
 
@@ -256,6 +257,8 @@ int orc_init(const orc_params* p, int64_t n_env, const int64_t* gids, uint64_t s
     if (!c) return -4;
     c->env = (orc_env*)calloc((size_t)n_env, sizeof(orc_env));
     if (!c->env) { free(c); return -4; }
+    c->st_env = (double*)calloc((size_t)n_env * ORC_N_STATS, sizeof(double));
+    if (!c->st_env) { free(c->env); free(c); return -4; }
     c->n = n_env;
     c->key[0] = (uint32_t)(seed & 0xFFFFFFFFu);
     c->key[1] = (uint32_t)(seed >> 32);
@@ -297,6 +300,7 @@ int orc_update_params(orc_ctx* c, const orc_params* p)
 void orc_free(orc_ctx* c)
 {
     if (!c) return;
+    free(c->st_env);
     free(c->env);
     free(c);
 }
@@ -446,15 +450,20 @@ static void reset_env(orc_ctx* c, orc_env* e)
     e->k_f = 0;
 }
 
+/* Envs are independent (each draws from its own counters), so the all-core build (-fopenmp,
+ * oracle.py "omp") runs the per-env loops of orc_reset / orc_step_sub in parallel; the result is
+ * bit-identical to the single-thread build (tests/test_oracle_pipeline.py). */
 int orc_reset(orc_ctx* c, const uint8_t* mask)
 {
     int64_t i;
     if (!c) return -2;
+#pragma omp parallel for schedule(static)
     for (i = 0; i < c->n; ++i) {
         if (mask && !mask[i]) continue;
         reset_env(c, &c->env[i]);
-        c->resets_pending += 1;
     }
+    for (i = 0; i < c->n; ++i)
+        if (!mask || mask[i]) c->resets_pending += 1;
     return 0;
 }
 
@@ -538,6 +547,7 @@ static void step_env(orc_ctx* c, orc_env* e, const float* act, const float* obs,
                     double d = (sg > 0.0) ? e->dpos[j] : e->dneg[j];
                     double m = fabs((s + an * d * dt[k]) - sg);
                     if (m < mg) mg = m;
+                    if (sn == sg && s != sg && fabs(sg - s) < mg) mg = fabs(sg - s);   /* eps-gate point */
                 }
                 if (sg != 0.0 && fabs(sn) == 1.0 && sn != s) st[ORC_S_RAIL_HITS] += 1.0;
                 if (al == 1.0) st[ORC_S_ALPHA_ONE] += 1.0; else st[ORC_S_ALPHA_LT1] += 1.0;
@@ -557,6 +567,10 @@ static void step_env(orc_ctx* c, orc_env* e, const float* act, const float* obs,
                 if (sg != 0.0) {
                     double d = (sg > 0.0) ? e->dpos[j] : e->dneg[j];
                     margin[j] = fabs((s + an * d * dt_env) - sg);
+                    /* a rail hit from s != sgn gives alpha = eps / (|sgn - s| + eps): for |sgn - s|
+                     * near or below sqrt(eps) that value moves with the last bits of s, so the
+                     * distance |sgn - s| is the second knife-edge margin of the gate */
+                    if (sn == sg && s != sg && fabs(sg - s) < margin[j]) margin[j] = fabs(sg - s);
                 } else {
                     margin[j] = INFINITY;
                 }
@@ -712,8 +726,10 @@ int orc_step_sub(orc_ctx* c, const float* actions, const float* raw_obs,
 {
     double st[ORC_N_STATS];
     int64_t i;
+    int k;
     if (!c || !actions || !raw_obs) return -1;
-    memset(st, 0, sizeof(st));
+    memset(c->st_env, 0, (size_t)c->n * ORC_N_STATS * sizeof(double));
+#pragma omp parallel for schedule(static)
     for (i = 0; i < c->n; ++i) {
         step_env(c, &c->env[i], actions + i * ORC_N_ACT, raw_obs + i * ORC_OBS_IN,
                  c->occl_mask ? (int)(c->occl_mask[i] & 0x1Fu) : -1,
@@ -722,9 +738,13 @@ int orc_step_sub(orc_ctx* c, const float* actions, const float* raw_obs,
                  out_obs ? out_obs + i * ORC_OBS_OUT : NULL,
                  out_dt ? out_dt + i * ORC_N_SUB : NULL,
                  out_force ? out_force + i * 3 : NULL,
-                 st,
+                 c->st_env + i * ORC_N_STATS,
                  bl_margin ? bl_margin + i * ORC_N_ACT : NULL);
     }
+    /* the step's stats: per-env contributions summed in env order */
+    memset(st, 0, sizeof(st));
+    for (i = 0; i < c->n; ++i)
+        for (k = 0; k < ORC_N_STATS; ++k) st[k] += c->st_env[i * ORC_N_STATS + k];
     st[ORC_S_RESETS] = (double)c->resets_pending;
     c->resets_pending = 0;
     if (stats) memcpy(stats, st, sizeof(st));
@@ -742,6 +762,22 @@ int orc_get_env(const orc_ctx* c, int64_t i, orc_env* dst)
 {
     if (!c || !dst || i < 0 || i >= c->n) return -1;
     *dst = c->env[i];
+    return 0;
+}
+
+/* State import: a plain field copy of *src into env i (its global id is kept: the Philox counter
+ * of env i stays the context's).  The reproducibility principle of the paper (ORRB's seeded,
+ * deterministic randomization) makes a run resumable from any exported state: the
+ * next draws depend only on (seed, global id, t, k_e), so import -> continue equals the
+ * uninterrupted run.  The test suite also uses it to start the oracle from a crafted state
+ * (boundary cases) or from the GPU's exported state (windowed re-sync). */
+int orc_set_env(orc_ctx* c, int64_t i, const orc_env* src)
+{
+    int64_t gid;
+    if (!c || !src || i < 0 || i >= c->n) return -1;
+    gid = c->env[i].gid;
+    c->env[i] = *src;
+    c->env[i].gid = gid;
     return 0;
 }
 

@@ -125,8 +125,10 @@ void orc_free(orc_ctx* c);
 int  orc_update_params(orc_ctx* c, const orc_params* p); /* mid-run parameter swap */
 int  orc_reset(orc_ctx* c, const uint8_t* mask);          /* NULL = all envs */
 /* One env step for all envs of the context.  Outputs may be NULL.
- * bl_margin [n][20]: fp64 |(s + a_n*d*dt_env) - sgn(a_n)| (the backlash rail margin), +inf when
- * sgn(a_n) = 0 or BACKLASH off -- used by tests to classify knife-edge rail hits. */
+ * bl_margin [n][20]: fp64 |(s + a_n*d*dt_env) - sgn(a_n)| (the backlash rail margin: where fp32 and
+ * fp64 may clamp differently), or on a rail hit from s != sgn(a_n) the smaller |sgn(a_n) - s| (where
+ * alpha = eps / (|sgn - s| + eps) is ill-conditioned in s); +inf when sgn(a_n) = 0 or BACKLASH off --
+ * used by tests to classify knife-edge gate decisions (diagnostic only: no output depends on it). */
 int  orc_step(orc_ctx* c, const float* actions, const float* raw_obs,
               double* out_actions, double* out_obs, double* out_dt, double* out_force,
               double* stats, double* bl_margin);
@@ -141,6 +143,7 @@ void     orc_set_occlusion_mask(orc_ctx* c, const uint8_t* mask);
 uint64_t orc_step_index(const orc_ctx* c);
 void     orc_set_step_index(orc_ctx* c, uint64_t t);
 int      orc_get_env(const orc_ctx* c, int64_t i, orc_env* dst);
+int      orc_set_env(orc_ctx* c, int64_t i, const orc_env* src);   /* state import (gid kept) */
 int64_t  orc_n_env(const orc_ctx* c);
 uint64_t orc_force_threshold(const orc_ctx* c, uint32_t j); /* T_j of the 65,536-entry table */
 double   orc_force_p(const orc_ctx* c, uint32_t j);

@@ -14,6 +14,7 @@ import numpy as np
 
 HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.path.join(HERE, "liboracle.so")
+LIB_OMP_PATH = os.path.join(HERE, "liboracle_omp.so")   # same source, -fopenmp: per-env loops over all cores
 SOURCES = [os.path.join(HERE, "oracle.c"), os.path.join(HERE, "oracle_vision.c")]
 HEADERS = [os.path.join(HERE, "oracle.h")]
 
@@ -21,12 +22,14 @@ N_ACT, N_TIPS, N_SUB, MAX_PHYS, OBS_IN, OBS_OUT, N_STATS = 20, 5, 10, 256, 26, 2
 
 
 def build(force: bool = False) -> str:
-    """gcc -O2 -ffp-contract=off: plain scalar fp64, no FMA contraction."""
+    """gcc -O2 -ffp-contract=off: plain scalar fp64, no FMA contraction.  Built twice: single-thread
+    (liboracle.so) and with -fopenmp (liboracle_omp.so, the all-core CPU baseline)."""
     newest = max(os.path.getmtime(p) for p in SOURCES + HEADERS)
-    if force or not os.path.exists(LIB_PATH) or os.path.getmtime(LIB_PATH) < newest:
-        cmd = ["gcc", "-O2", "-std=c99", "-D_DEFAULT_SOURCE", "-ffp-contract=off", "-fno-fast-math",
-               "-fPIC", "-shared", "-Wall", "-o", LIB_PATH] + SOURCES + ["-lm"]
-        subprocess.check_call(cmd)
+    for path, extra in ((LIB_PATH, []), (LIB_OMP_PATH, ["-fopenmp"])):
+        if force or not os.path.exists(path) or os.path.getmtime(path) < newest:
+            cmd = ["gcc", "-O2", "-std=c99", "-D_DEFAULT_SOURCE", "-ffp-contract=off", "-fno-fast-math",
+                   "-fPIC", "-shared", "-Wall", "-Wno-unknown-pragmas"] + extra + ["-o", path] + SOURCES + ["-lm"]
+            subprocess.check_call(cmd)
     return LIB_PATH
 
 
@@ -87,14 +90,14 @@ class OrcPoseAugParams(C.Structure):
 
 SCENE_WORDS = 64
 
-_lib = None
+_libs = {}
 
 
-def lib():
-    global _lib
-    if _lib is None:
+def lib(omp: bool = False):
+    """The single-thread oracle library, or (omp=True) the -fopenmp build of the same source."""
+    if omp not in _libs:
         build()
-        L = C.CDLL(LIB_PATH)
+        L = C.CDLL(LIB_OMP_PATH if omp else LIB_PATH)
         dp, fp, u8p = C.POINTER(C.c_double), C.POINTER(C.c_float), C.POINTER(C.c_uint8)
         L.orc_init.argtypes = [C.POINTER(OrcParams), C.c_int64, C.POINTER(C.c_int64), C.c_uint64,
                                C.POINTER(C.c_void_p)]
@@ -122,6 +125,8 @@ def lib():
         L.orc_set_step_index.argtypes = [C.c_void_p, C.c_uint64]
         L.orc_get_env.argtypes = [C.c_void_p, C.c_int64, C.POINTER(OrcEnv)]
         L.orc_get_env.restype = C.c_int
+        L.orc_set_env.argtypes = [C.c_void_p, C.c_int64, C.POINTER(OrcEnv)]
+        L.orc_set_env.restype = C.c_int
         L.orc_force_threshold.argtypes = [C.c_void_p, C.c_uint32]
         L.orc_force_threshold.restype = C.c_uint64
         L.orc_force_p.argtypes = [C.c_void_p, C.c_uint32]
@@ -139,8 +144,8 @@ def lib():
         L.orc_occluded.restype = C.c_int
         L.orc_bernoulli_threshold.argtypes = [C.c_double]
         L.orc_bernoulli_threshold.restype = C.c_uint64
-        _lib = L
-    return _lib
+        _libs[omp] = L
+    return _libs[omp]
 
 
 def make_params(preset: dict) -> OrcParams:
@@ -264,8 +269,9 @@ def pose_augment(preset: dict, seed: int, batch: int, poses, offset: int = 0):
 class Oracle:
     """fp64 CPU oracle over a list of global env ids (any subset of a larger run)."""
 
-    def __init__(self, preset: dict, n_env: int, seed: int, gids=None):
-        L = lib()
+    def __init__(self, preset: dict, n_env: int, seed: int, gids=None, omp: bool = False):
+        """omp=True: the all-core (-fopenmp) build of the same oracle (bit-identical results)."""
+        L = self._L = lib(omp)
         self._params = make_params(preset)
         self.n = int(n_env)
         if gids is None:
@@ -280,7 +286,7 @@ class Oracle:
 
     def close(self):
         if getattr(self, "_h", None):
-            lib().orc_free(self._h)
+            self._L.orc_free(self._h)
             self._h = None
 
     def __del__(self):
@@ -293,13 +299,13 @@ class Oracle:
         """Simulator occlusion bits [n] u8 (bit i = tip i), or None for the distance rule.  The
         array is kept alive here and re-read at every step (update it in place)."""
         self._occl = None if mask is None else np.ascontiguousarray(mask, dtype=np.uint8)
-        lib().orc_set_occlusion_mask(self._h, None if self._occl is None else _ptr(self._occl, C.c_uint8))
+        self._L.orc_set_occlusion_mask(self._h, None if self._occl is None else _ptr(self._occl, C.c_uint8))
         return self._occl
 
     def update_params(self, preset: dict):
         """Swap the parameter set mid-run: later draws use it."""
         self._params = make_params(preset)
-        rc = lib().orc_update_params(self._h, C.byref(self._params))
+        rc = self._L.orc_update_params(self._h, C.byref(self._params))
         if rc != 0:
             raise ValueError(f"orc_update_params failed: {rc}")
 
@@ -307,7 +313,7 @@ class Oracle:
         m = None if mask is None else np.ascontiguousarray(mask, dtype=np.uint8)
         if m is not None:
             assert m.shape == (self.n,)
-        rc = lib().orc_reset(self._h, _ptr(m, C.c_uint8))
+        rc = self._L.orc_reset(self._h, _ptr(m, C.c_uint8))
         assert rc == 0
 
     def step(self, actions, raw_obs, want_margin=False, want_sub=False):
@@ -324,7 +330,7 @@ class Oracle:
         margin = np.empty((self.n, N_ACT)) if want_margin else None
         sub = np.empty((self.n, N_SUB, N_ACT)) if want_sub else None
         dp = C.c_double
-        rc = lib().orc_step_sub(self._h, _ptr(a, C.c_float), _ptr(o, C.c_float),
+        rc = self._L.orc_step_sub(self._h, _ptr(a, C.c_float), _ptr(o, C.c_float),
                                 _ptr(out["out_actions"], dp), _ptr(sub, dp), _ptr(out["out_obs"], dp),
                                 _ptr(out["out_dt"], dp), _ptr(out["out_force"], dp),
                                 _ptr(out["stats"], dp), _ptr(margin, dp))
@@ -337,15 +343,15 @@ class Oracle:
 
     @property
     def step_index(self):
-        return lib().orc_step_index(self._h)
+        return self._L.orc_step_index(self._h)
 
     @step_index.setter
     def step_index(self, t):
-        lib().orc_set_step_index(self._h, t)
+        self._L.orc_set_step_index(self._h, t)
 
     def env(self, i) -> dict:
         e = OrcEnv()
-        assert lib().orc_get_env(self._h, i, C.byref(e)) == 0
+        assert self._L.orc_get_env(self._h, i, C.byref(e)) == 0
         d = {}
         for name, ty in OrcEnv._fields_:
             if name.startswith("_pad"):
@@ -356,8 +362,27 @@ class Oracle:
             d["lambda" if name == "lambda_" else name] = v
         return d
 
+    def set_env(self, i, d: dict):
+        """State import of env i from a dict shaped like env(i) (missing keys keep their value)."""
+        e = OrcEnv()
+        assert self._L.orc_get_env(self._h, i, C.byref(e)) == 0
+        for name, _ in OrcEnv._fields_:
+            key = "lambda" if name == "lambda_" else name
+            if name.startswith("_pad") or key not in d:
+                continue
+            v = d[key]
+            cur = getattr(e, name)
+            if hasattr(cur, "_length_"):
+                vals = np.asarray(v).ravel()
+                assert len(vals) == cur._length_, name
+                for k in range(cur._length_):
+                    cur[k] = vals[k].item()
+            else:
+                setattr(e, name, v.item() if hasattr(v, "item") else v)
+        assert self._L.orc_set_env(self._h, i, C.byref(e)) == 0
+
     def force_threshold(self, j):
-        return lib().orc_force_threshold(self._h, j)
+        return self._L.orc_force_threshold(self._h, j)
 
     def force_p(self, j):
-        return lib().orc_force_p(self._h, j)
+        return self._L.orc_force_p(self._h, j)

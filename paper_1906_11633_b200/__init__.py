@@ -62,9 +62,9 @@ class DRContext:
         dr.dr_reset(mask, self.n if mask is not None else None)
 
     def last_stats(self):
-        """fp64 stats of the most recent step (synchronises)."""
-        t = dr.dr_step_index()
-        self.stream.synchronize()
+        """fp64 stats of the most recent step (synchronises; the slot comes from the device step
+        counter, which CUDA-graph replays advance too)."""
+        t = dr.dr_step_index_sync()
         return self.stats[(t - 1) % dr.N_STAT_SLOTS].cpu().numpy()
 
     def export(self, lo: int = 0, hi: int = 0) -> dict:

@@ -12,7 +12,13 @@ CSRC = os.path.join(PKG, "csrc")
 INCLUDE = os.path.join(ROOT, "include")
 LIB = os.path.join(PKG, "libdr.so")
 SOURCES = [os.path.join(CSRC, f) for f in ("dr_kernels.cu", "dr_api.cu", "dr_vision.cu")]
-DEPS = SOURCES + [os.path.join(CSRC, f) for f in ("dr_internal.h", "dr_device.cuh", "dr_math.cuh", "dr_step.cuh", "dr_reset.cuh")] + [os.path.join(INCLUDE, f) for f in ("dr.h", "dr_vision.h")]
+import glob  # noqa: E402
+
+
+def deps():
+    """Every source and header the library is built from (an edit to any of them rebuilds)."""
+    return sorted(glob.glob(os.path.join(CSRC, "*.cu")) + glob.glob(os.path.join(CSRC, "*.cuh")) +
+                  glob.glob(os.path.join(CSRC, "*.h")) + glob.glob(os.path.join(INCLUDE, "*.h")))
 
 NVCC = os.environ.get("NVCC", "nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
@@ -24,7 +30,7 @@ def needs_build() -> bool:
     if not os.path.exists(LIB):
         return True
     t = os.path.getmtime(LIB)
-    return any(os.path.getmtime(d) > t for d in DEPS)
+    return any(os.path.getmtime(d) > t for d in deps())
 
 
 def build(force: bool = False, verbose: bool = False) -> str:

@@ -21,7 +21,7 @@ using namespace dr;
 namespace {
 
 struct Layout {
-    size_t rec, st, phys, pd_kr, pd_a, pd_b, pd_base, t_tab, rs_philox, rs_pairs, rs_phys, rs_src, dec,
+    size_t rec, st, phys, t_tab, rs_phys, rs_src, dec,
         stats, ctl, total;
     uint64_t pitch;
 };
@@ -39,16 +39,10 @@ Layout make_layout(int64_t n_env, int n_phys, int max_ctas) {
     L.pitch = align_up((size_t)n_env, TILE);   // envs rounded up to whole tiles
     size_t off = 0;
     auto take = [&](size_t bytes) { size_t o = off; off = align_up(off + bytes, 256); return o; };
-    L.rec = take((size_t)REC_PLANES * L.pitch * 4);   // [n_tiles][REC_PLANES][TILE]
+    L.rec = take((size_t)REC_WORDS * L.pitch * 4);    // [n_tiles][REC_GROUPS][TILE][8]
     L.st = take((size_t)ST_PLANES * L.pitch * 4);     // [n_tiles][ST_PLANES][TILE]
     L.phys = take((size_t)n_env * n_phys * 4);
-    L.pd_kr = take(MAX_PHYS * 4);
-    L.pd_a = take(MAX_PHYS * 4);
-    L.pd_b = take(MAX_PHYS * 4);
-    L.pd_base = take(MAX_PHYS * 4);
     L.t_tab = take(65536 * 4);
-    L.rs_philox = take(RS_MAX_PHILOX * 4);
-    L.rs_pairs = take(RS_MAX_PAIRS * 4);
     L.rs_phys = take(MAX_PHYS * 16);
     L.rs_src = take(MAX_PHYS * 4);
     L.dec = take(512 * 8);
@@ -131,6 +125,11 @@ int validate(const dr_params* p, int64_t n_env) {
         {"dropout_rate_hz", p->dropout_rate_hz}, {"occl_dist", p->occl_dist}};
     for (auto& s : stds)
         if (!(s.v >= 0.0) || !std::isfinite(s.v)) return fail(DR_EINVAL, "%s: must be a finite value >= 0", s.n);
+    // The kernels evaluate the backlash gate as alpha = eps / (|s' - s| + eps) whenever num < den
+    // (dr_step.cuh backlash_alpha): exact only while s' can sit within eps of a rail by landing on
+    // it, i.e. for eps below the fp32 spacing just inside +-1 (2^-24 ~ 6e-8).  The paper's eps is
+    // 1e-12.
+    if (!(p->backlash_eps <= 1e-8)) return fail(DR_EINVAL, "backlash_eps: must be <= 1e-8 (the paper's is 1e-12)");
     if (!(p->delay_prob >= 0.0 && p->delay_prob <= 1.0)) return fail(DR_EINVAL, "delay_prob: outside [0, 1]");
     if (!(p->dt_base > 0.0)) return fail(DR_EINVAL, "dt_base: must be > 0");
     if (!(p->step_nominal > 0.0)) return fail(DR_EINVAL, "step_nominal: must be > 0");
@@ -246,58 +245,16 @@ cudaError_t upload_params(Ctx* c, const dr_params& p, const char** what) {
     dc.n_phys = p.n_phys;
     dc.mass_index = p.mass_index;
 
-    std::vector<uint32_t> kr(MAX_PHYS, 0);
-    std::vector<float> pa(MAX_PHYS, 0.f), pb(MAX_PHYS, 0.f), pbase(MAX_PHYS, 0.f);
-    int nu = 0, nn = 0;
+    int nu = 0, nn = 0;   // uniform-kind / normal-kind parameter counts (draw ranks)
     for (int i = 0; i < p.n_phys; ++i) {
-        const dr_phys_desc& d = p.phys[i];
-        uint32_t rank = 0;
-        switch (d.kind) {
-        case DR_PHYS_UNIFORM_SCALE: rank = nu++; pa[i] = (float)d.a; pb[i] = (float)(d.b - d.a); break;
-        case DR_PHYS_LOGUNIFORM_SCALE:
-            rank = nu++; pa[i] = (float)std::log(d.a); pb[i] = (float)(std::log(d.b) - std::log(d.a)); break;
-        case DR_PHYS_ADD_GAUSS:
-        case DR_PHYS_MUL_LOGNORMAL: rank = nn++; pa[i] = (float)d.a; break;
-        default: break;
-        }
-        kr[i] = d.kind | (rank << 8);
-        pbase[i] = (float)d.base;
+        const uint32_t kd = p.phys[i].kind;
+        if (kd == DR_PHYS_UNIFORM_SCALE || kd == DR_PHYS_LOGUNIFORM_SCALE) ++nu;
+        else if (kd == DR_PHYS_ADD_GAUSS || kd == DR_PHYS_MUL_LOGNORMAL) ++nn;
     }
     dc.n_phys_u = nu;
     dc.n_phys_n = nn;
 
-    // ---- reset task tables (dr_internal.h): only the blocks / pairs the enabled layers draw ----
     const uint32_t lm = p.layer_mask;
-    std::vector<uint32_t> rph, rpr;
-    auto ph = [&](int slot, uint32_t ch, int nblk) {
-        for (int b = 0; b < nblk; ++b) rph.push_back((uint32_t)(slot + b) | ((uint32_t)b << 8) | (ch << 16));
-    };
-    auto pr = [&](int slot, int npairs, int zbase) {
-        for (int q = 0; q < npairs; ++q) rpr.push_back((uint32_t)slot | ((uint32_t)q << 8) | ((uint32_t)zbase << 16));
-    };
-    if (lm & DR_PHYS) {
-        ph(SL_PHYS_U, CH_PHYS_U, (nu + 3) / 4);
-        ph(SL_PHYS_N, CH_PHYS_N, (nn + 3) / 4);
-        pr(SL_PHYS_N, (nn + 1) / 2, ZB_PHYS);
-    }
-    if (lm & DR_DELAY) ph(SL_DELAY, CH_DELAY, 5);
-    if (lm & DR_BACKLASH) { ph(SL_BACKLASH, CH_BACKLASH, 10); pr(SL_BACKLASH, 20, ZB_BL); }
-    if (lm & DR_TIMING) ph(SL_LAMBDA, CH_LAMBDA, 1);
-    if (lm & DR_FORCE) ph(SL_FORCE_P, CH_FORCE_P, 1);
-    if (lm & DR_ACT_NOISE) { ph(SL_CORR_ACT, CH_CORR_ACT, 5); pr(SL_CORR_ACT, 10, ZB_CA); }
-    if (lm & DR_OBS_NOISE) {
-        ph(SL_CORR_TIP, CH_CORR_TIP, 4);
-        ph(SL_MARKER_TIP, CH_MARKER_TIP, 4);
-        ph(SL_MARKER_BASE, CH_MARKER_BASE, 1);
-        ph(SL_CORR_OBJ, CH_CORR_OBJ, 1);
-        ph(SL_CORR_ROT, CH_CORR_ROT, 1);
-        pr(SL_CORR_TIP, 8, ZB_CT);
-        pr(SL_MARKER_TIP, 8, ZB_MT);
-        pr(SL_MARKER_BASE, 2, ZB_MB);
-        pr(SL_CORR_OBJ, 2, ZB_CO);
-    }
-    dc.n_rs_philox = (int)rph.size();
-    dc.n_rs_pairs = (int)rpr.size();
     // physics: v = C0 + C1 * f(A + B x) (dr_internal.h), f = 2^(.) for the exp kinds (A, B in log2 units)
     std::vector<float> rphys(MAX_PHYS * 4, 0.f);
     std::vector<uint32_t> rsrc(MAX_PHYS, 0u);
@@ -306,28 +263,28 @@ cudaError_t upload_params(Ctx* c, const dr_params& p, const char** what) {
         for (int i = 0; i < p.n_phys; ++i) {
             const dr_phys_desc& d = p.phys[i];
             float A = 0.f, B = 0.f, C0 = (float)d.base, C1 = 0.f;
-            uint32_t src = 0u;
+            uint32_t src = RS_OFF_ZERO;
             const bool on_phys = (lm & DR_PHYS) != 0;
             switch (d.kind) {
             case DR_PHYS_UNIFORM_SCALE:   // base * (a + (b - a) U)
-                if (on_phys) { A = (float)d.a; B = (float)(d.b - d.a); C0 = 0.f; C1 = (float)d.base; src = SL_PHYS_U * 4 + u; }
+                if (on_phys) { A = (float)d.a; B = (float)(d.b - d.a); C0 = 0.f; C1 = (float)d.base; src = (uint32_t)u; }
                 ++u;
                 break;
             case DR_PHYS_LOGUNIFORM_SCALE:   // base * exp(ln a + (ln b - ln a) U) = base * 2^(log2 a + log2(b/a) U)
                 if (on_phys) {
                     A = (float)std::log2(d.a); B = (float)(std::log2(d.b) - std::log2(d.a)); C0 = 0.f; C1 = (float)d.base;
-                    src = (SL_PHYS_U * 4 + u) | RS_SRC_EXP;
+                    src = (uint32_t)u | RS_EXP;
                 }
                 ++u;
                 break;
             case DR_PHYS_ADD_GAUSS:   // base + sigma z
-                if (on_phys) { B = (float)d.a; C0 = (float)d.base; C1 = 1.f; src = (ZB_PHYS + n) | RS_SRC_NORMAL; }
+                if (on_phys) { B = (float)d.a; C0 = (float)d.base; C1 = 1.f; src = RS_OFF_NORMAL + (uint32_t)n; }
                 ++n;
                 break;
             case DR_PHYS_MUL_LOGNORMAL:   // base * exp(sigma z) = base * 2^(sigma log2(e) z)
                 if (on_phys) {
                     B = (float)(d.a * 1.4426950408889634074); C0 = 0.f; C1 = (float)d.base;
-                    src = (ZB_PHYS + n) | RS_SRC_NORMAL | RS_SRC_EXP;
+                    src = (RS_OFF_NORMAL + (uint32_t)n) | RS_EXP;
                 }
                 ++n;
                 break;
@@ -338,7 +295,7 @@ cudaError_t upload_params(Ctx* c, const dr_params& p, const char** what) {
             rphys[4 * i + 1] = B;
             rphys[4 * i + 2] = C0;
             rphys[4 * i + 3] = C1;
-            rsrc[i] = src | ((on_phys && d.kind != DR_PHYS_FIXED) ? RS_SRC_DRAW : 0u);
+            rsrc[i] = src;
         }
     }
     // loguniform force probability quantised to 65,536 midpoints of ln p (Q19)
@@ -361,15 +318,7 @@ cudaError_t upload_params(Ctx* c, const dr_params& p, const char** what) {
     cudaError_t e;
     const DevPtrs& P = c->p;
     if ((e = upload_const(dc, s)) != cudaSuccess) { *what = "upload_const"; return e; };
-    if ((e = cudaMemcpyAsync(P.pd_kind_rank, kr.data(), MAX_PHYS * 4, cudaMemcpyHostToDevice, s)) != cudaSuccess) { *what = "memcpy pd"; return e; };
-    if ((e = cudaMemcpyAsync(P.pd_a, pa.data(), MAX_PHYS * 4, cudaMemcpyHostToDevice, s)) != cudaSuccess) { *what = "memcpy pd"; return e; };
-    if ((e = cudaMemcpyAsync(P.pd_b, pb.data(), MAX_PHYS * 4, cudaMemcpyHostToDevice, s)) != cudaSuccess) { *what = "memcpy pd"; return e; };
-    if ((e = cudaMemcpyAsync(P.pd_base, pbase.data(), MAX_PHYS * 4, cudaMemcpyHostToDevice, s)) != cudaSuccess) { *what = "memcpy pd"; return e; };
     if ((e = cudaMemcpyAsync(P.t_tab, ttab.data(), 65536 * 4, cudaMemcpyHostToDevice, s)) != cudaSuccess) { *what = "memcpy t_tab"; return e; };
-    if (!rph.empty() && (e = cudaMemcpyAsync(P.rs_philox, rph.data(), rph.size() * 4, cudaMemcpyHostToDevice, s)) != cudaSuccess)
-        { *what = "memcpy rs_philox"; return e; };
-    if (!rpr.empty() && (e = cudaMemcpyAsync(P.rs_pairs, rpr.data(), rpr.size() * 4, cudaMemcpyHostToDevice, s)) != cudaSuccess)
-        { *what = "memcpy rs_pairs"; return e; };
     if ((e = cudaMemcpyAsync(P.rs_phys, rphys.data(), MAX_PHYS * 16, cudaMemcpyHostToDevice, s)) != cudaSuccess) { *what = "memcpy rs_phys"; return e; };
     if ((e = cudaMemcpyAsync(P.rs_src, rsrc.data(), MAX_PHYS * 4, cudaMemcpyHostToDevice, s)) != cudaSuccess) { *what = "memcpy rs_src"; return e; };
     if ((e = cudaMemcpyAsync(P.dec_tab, dec.data(), 512 * 8, cudaMemcpyHostToDevice, s)) != cudaSuccess) { *what = "memcpy dec"; return e; };
@@ -499,13 +448,7 @@ int dr_init(const dr_params* params, int64_t n_env, uint64_t seed) {
     P.rec = reinterpret_cast<uint32_t*>(c->ws + L.rec);
     P.st = reinterpret_cast<uint32_t*>(c->ws + L.st);
     P.phys = reinterpret_cast<float*>(c->ws + L.phys);
-    P.pd_kind_rank = reinterpret_cast<uint32_t*>(c->ws + L.pd_kr);
-    P.pd_a = reinterpret_cast<float*>(c->ws + L.pd_a);
-    P.pd_b = reinterpret_cast<float*>(c->ws + L.pd_b);
-    P.pd_base = reinterpret_cast<float*>(c->ws + L.pd_base);
     P.t_tab = reinterpret_cast<uint32_t*>(c->ws + L.t_tab);
-    P.rs_philox = reinterpret_cast<uint32_t*>(c->ws + L.rs_philox);
-    P.rs_pairs = reinterpret_cast<uint32_t*>(c->ws + L.rs_pairs);
     P.rs_phys = reinterpret_cast<float4*>(c->ws + L.rs_phys);
     P.rs_src = reinterpret_cast<uint32_t*>(c->ws + L.rs_src);
     P.dec_tab = reinterpret_cast<double*>(c->ws + L.dec);
@@ -528,10 +471,6 @@ int dr_init(const dr_params* params, int64_t n_env, uint64_t seed) {
     if ((e = cudaStreamSynchronize(s)) != cudaSuccess) return bail(e, "sync init");
 
     // A/B knobs, read at every dr_init (unset = the defaults)
-    const char* pf = std::getenv("DR_PREFETCH");
-    const char* pp = std::getenv("DR_PIPE");
-    set_step_prefetch(pf ? std::atoi(pf) : 0);
-    set_step_pipe(pp ? std::atoi(pp) : 2);
     // step mode by the job size (n_env_global, so every shard of a job runs the same kernel and
     // per-env results stay bit-identical across GPU counts); DR_STEP_MODE=throughput|latency forces
     const char* sm = std::getenv("DR_STEP_MODE");
@@ -551,8 +490,6 @@ int dr_init(const dr_params* params, int64_t n_env, uint64_t seed) {
         const int v = std::atoi(sg);
         if (v >= 1 && v < c->step_grid) c->step_grid = v;
     }
-    const char* rv = std::getenv("DR_RESET");
-    set_reset_version(rv ? std::atoi(rv) : 6);
     const char* pdl = std::getenv("DR_PDL");
     set_pdl(!(pdl && std::atoi(pdl) == 0));
     c->reset_grid = reset_grid_for((uint32_t)n_env, c->sm_count);
@@ -770,6 +707,17 @@ int dr_set_stats_buffer(double* dev_buf) {
 
 uint64_t dr_step_index(void) { return g_ctx ? g_ctx->t_host : 0; }
 
+uint64_t dr_step_index_sync(void) {
+    Ctx* c = g_ctx;
+    if (!c) return 0;
+    unsigned long long v = 0;
+    if (cudaMemcpyAsync(&v, c->p.ctl, 8, cudaMemcpyDeviceToHost, c->stream) != cudaSuccess ||
+        cudaStreamSynchronize(c->stream) != cudaSuccess)
+        return c->t_host;
+    c->t_host = v;   // graph replays advanced the device counter
+    return v;
+}
+
 int dr_set_step_index(uint64_t t) {
     Ctx* c = g_ctx;
     if (!c) return fail(DR_ENOTINIT, "dr_set_step_index: no context");
@@ -820,8 +768,8 @@ int dr_state_import(const void* host_src, int64_t env_lo, int64_t env_hi) {
     CK(cudaMemcpyAsync(d, host_src, bytes, cudaMemcpyHostToDevice, c->stream));
     cudaError_t e = launch_import(c->p, d, (uint32_t)env_lo, (uint32_t)env_hi, c->stream);
     if (e != cudaSuccess) return cuda_fail(e, "import_kernel");
-    c->launches++;
-    ++g_total_launches;
+    c->launches += 2;   // import_kernel + import_phys_kernel
+    g_total_launches += 2;
     CK(cudaFreeAsync(d, c->stream));
     CK(cudaStreamSynchronize(c->stream));
     return DR_OK;

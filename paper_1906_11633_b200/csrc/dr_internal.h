@@ -1,12 +1,14 @@
 // dr_internal.h -- shared between the host library (dr_api.cu) and the kernels (dr_kernels.cu).
-// Device data layout: tiled structure-of-arrays ("AoSoA").
-//   rec  : episode record, [n_tiles][REC_PLANES][TILE] 4-byte words
-//   st   : mutable per-env state, [n_tiles][ST_PLANES][TILE]
+// Device data layout:
+//   rec  : episode record, [n_tiles][REC_GROUPS][TILE][8] 4-byte words: record word w of env e is
+//          word w % 8 of the 32-byte group w / 8 of that env, so the eight words of a group are one
+//          DRAM sector of ONE env.  A reset rewrites whole sectors (no L2 read-fill of partially
+//          written sectors), and the step reads a group of its 32 consecutive envs as 1 KB of
+//          contiguous memory (16-byte cp.async per half group, coalesced).
+//   st   : mutable per-env state, [n_tiles][ST_PLANES][TILE] (plane k of env e at k * TILE + e % TILE:
+//          a warp's 32 consecutive envs read and write one 128-byte line per plane)
 //   phys : [n_env][n_phys] fp32, row-major (the simulator reads rows)
-// Within a tile, plane k of env e sits at k * TILE + (e % TILE): a warp's 32 consecutive envs
-// read one 128-byte line per plane (coalesced), every plane offset from an env's base is a
-// compile-time immediate (no per-access address arithmetic), and a tile's whole record /
-// state is one contiguous block (one bulk copy / L2 prefetch).
+// A tile's whole record / state is one contiguous block.
 #pragma once
 #include <cstddef>
 #include <cstdint>
@@ -20,25 +22,31 @@ constexpr int N_STAT_SLOTS = 4;     // stats ring: step t accumulates into slot 
 constexpr int TILE = 128;           // envs per CTA tile (one thread per env)
 constexpr uint32_t RUNTIME_MASK = 0xFFFFFFFFu;
 
-// ---- record planes (read by the step kernel: 86 of them) ----
+// ---- record words (REC_WORDS per env, 12 sector groups of 8).  Grouped by the step kernel's phases
+// (dr_step.cuh): group 0 = the S0 scalars + c_act 0..3, groups 1..5 = (delta-1, delta+1) of actuators
+// 4b..4b+3, groups 6..7 = c_act 4..19, groups 8..10 = the observation offsets (+ lambda, p-index),
+// group 11 = the episode counter (the step never reads it).
 enum : int {
     REC_DELAY = 0,   // u32 delay bits
     REC_INVLAM = 1,  // 1/lambda (the step only needs the reciprocal rate)
     REC_TFORCE = 2,  // u32 force threshold
     REC_MASS = 3,
-    REC_DNEG = 4,    // 20
-    REC_DPOS = 24,   // 20
-    REC_CACT = 44,   // 20
+    REC_G_BL = 1,    // groups 1..5: words 8 + 8b + q = delta-1 of actuator 4b + q, 12 + 8b + q = delta+1
     REC_OFFTIP = 64, // 15
     REC_COBJ = 79,   // 3
     REC_QC = 82,     // 4
-    REC_STEP_PLANES = 86,
-    // not read by the step kernel
     REC_LAMBDA = 86,
     REC_PINDEX = 87, // u32
     REC_EPISODE = 88,// u32
-    REC_PLANES = 89
+    REC_STEP_GROUPS = 11,   // groups 0..10 are read by the step kernel
+    REC_GROUPS = 12,
+    REC_WORDS = 8 * REC_GROUPS
 };
+__host__ __device__ constexpr int rec_dneg(int j) { return 8 + 8 * (j >> 2) + (j & 3); }
+__host__ __device__ constexpr int rec_dpos(int j) { return 12 + 8 * (j >> 2) + (j & 3); }
+__host__ __device__ constexpr int rec_cact(int j) { return j < 4 ? 4 + j : 44 + j; }
+// word offset of record word w from an env's base (rec_index): group w / 8, word w % 8
+__host__ __device__ constexpr size_t rec_off(int w) { return (size_t)(w >> 3) * (TILE * 8) + (w & 7); }
 // ---- state planes (read + written by the step kernel) ----
 enum : int {
     ST_PREV = 0,     // 20
@@ -56,10 +64,11 @@ constexpr uint32_t HAS_LAST_BIT = 1u << 20;
 // back, so a reset costs one scattered state word instead of sixty.
 constexpr uint32_t FRESH_BIT = 1u << 21;
 
-// AoSoA addressing: word offset of env e's plane 0; plane k is at + k * TILE.
+// word offset of env e's record word 0 (record word w at + rec_off(w))
 __host__ __device__ __forceinline__ size_t rec_index(uint32_t e) {
-    return (size_t)(e / TILE) * (REC_PLANES * TILE) + (e % TILE);
+    return (size_t)(e / TILE) * (REC_WORDS * TILE) + (size_t)(e % TILE) * 8;
 }
+// AoSoA state addressing: word offset of env e's plane 0; plane k is at + k * TILE.
 __host__ __device__ __forceinline__ size_t st_index(uint32_t e) {
     return (size_t)(e / TILE) * (ST_PLANES * TILE) + (e % TILE);
 }
@@ -100,60 +109,23 @@ struct DevConst {
                                        // mq_inv (a power of 2) so the fp64 atomic totals are exact
     int32_t n_phys, mass_index;
     int32_t n_phys_u, n_phys_n;       // counts of uniform-kind / normal-kind params
-    int32_t n_rs_philox, n_rs_pairs;  // reset task-table lengths (host-built, layer-dependent)
 };
 
-// Reset task tables (built on the host at dr_init, staged in shared memory by the reset kernel):
-//   philox task : slot | blk << 8 | channel << 16        (one Philox block per entry)
-//   pair task   : slot | pair << 8 | zbuf_base << 16     (one Box-Muller pair per entry)
-//   phys entry  : float4 (A, B, C0, C1) + src word: v = C0 + C1 * f, f = (exp?) 2^(A + B x) : A + B x, where
-//                 x = U(word src) for uniform kinds or z[src] for normal kinds
-//                 (src bit 31: normal kind, bit 30: exp, bits 0..29: index)
-constexpr int RS_MAX_PHILOX = 161, RS_MAX_PAIRS = 128 + 50;
-// Philox block slots of one reset env (shared-memory layout; the task table says which are live)
-enum : int {
-    SL_PHYS_U = 0,        // up to 64 blocks (256 uniform-kind params)
-    SL_PHYS_N = 64,       // up to 64 blocks (256 normal-kind params)
-    SL_DELAY = 128,       // 5
-    SL_BACKLASH = 133,    // 10 (40 normals)
-    SL_LAMBDA = 143,      // 1
-    SL_FORCE_P = 144,     // 1
-    SL_CORR_ACT = 145,    // 5
-    SL_CORR_TIP = 150,    // 4
-    SL_MARKER_TIP = 154,  // 4
-    SL_MARKER_BASE = 158, // 1
-    SL_CORR_OBJ = 159,    // 1
-    SL_CORR_ROT = 160,    // 1
-    SL_COUNT = 161
-};
-// z buffer of one reset env: normal n of a channel at its base + n
-enum : int {
-    ZB_PHYS = 0,    // by normal rank, up to 256
-    ZB_BL = 256,    // 40: delta_-1 normals 0..19, delta_+1 normals 20..39
-    ZB_CA = 296,    // 20
-    ZB_CT = 316,    // 16 (15 used)
-    ZB_MT = 332,    // 16 (15 used)
-    ZB_MB = 348,    // 4 (3 used)
-    ZB_CO = 352,    // 4 (3 used)
-    ZB_COUNT = 356
-};
-constexpr uint32_t RS_SRC_NORMAL = 1u << 31, RS_SRC_EXP = 1u << 30, RS_SRC_DRAW = 1u << 29, RS_SRC_IDX = (1u << 29) - 1u;
+// Physics table of the reset kernel (built on the host at dr_init): per parameter q, rs_phys[q] =
+// (A, B, C0, C1) and rs_src[q] = draw-buffer offset of its x | exp flag (bit 31), with
+// v = C0 + C1 * f(A + B x), f = 2^(.) for the exp kinds (A, B in log2 units), x = the u-th uniform
+// (offset u), the n-th normal (offset 256 + n) or the constant 0 (offset 512, draw-free kinds).
+constexpr uint32_t RS_EXP = 1u << 31;
+constexpr uint32_t RS_OFF_NORMAL = MAX_PHYS, RS_OFF_ZERO = 2 * MAX_PHYS;
 
 // Pointers of the device workspace.
 struct DevPtrs {
-    uint32_t* rec;            // [n_tiles][REC_PLANES][TILE]
+    uint32_t* rec;            // [n_tiles][REC_GROUPS][TILE][8]
     uint32_t* st;             // [n_tiles][ST_PLANES][TILE]
     float* phys;              // [n_env][n_phys]
-    // physics descriptor table (global, lane-indexed in the reset kernel)
-    uint32_t* pd_kind_rank;   // [256]: kind | (rank << 8)
-    float* pd_a;              // [256]  a (or ln a for loguniform)
-    float* pd_b;              // [256]  b (or ln b - ln a for loguniform)
-    float* pd_base;           // [256]
     uint32_t* t_tab;          // [65536] force thresholds
-    uint32_t* rs_philox;      // [RS_MAX_PHILOX] reset Philox tasks
-    uint32_t* rs_pairs;       // [RS_MAX_PAIRS] reset Box-Muller pair tasks
-    float4* rs_phys;          // [256] physics coefficients
-    uint32_t* rs_src;         // [256] physics draw source
+    float4* rs_phys;          // [256] physics coefficients (A, B, C0, C1)
+    uint32_t* rs_src;         // [256] physics draw-buffer offset | RS_EXP
     double* dec_tab;          // [512]: 0.99^j (j < 256), then 0.99^(256 i)
     double* stats;            // [N_STAT_SLOTS][N_STATS] (internal or caller-owned)
     unsigned long long* ctl;  // [0] = step t, [1] = CTAs started counter, [2] = resets pending
@@ -176,19 +148,14 @@ cudaError_t launch_import(const DevPtrs& p, const void* src, uint32_t lo, uint32
 cudaError_t launch_debug_philox(uint32_t n_env, uint32_t dom, uint32_t ch, uint32_t blk, uint32_t* out,
                                 cudaStream_t s);
 int step_max_ctas_per_sm(uint32_t layer_mask);
-void set_step_prefetch(int mode);
-void set_step_pipe(int mode);
 void set_step_mode(int mode);   // 0 throughput, 1 latency
 int step_mode();
 // latency mode up to this many envs per job (n_env_global).  Measured (profiles/round1_notes.md):
 // 4,096 envs 7.3 us vs 9.6 us per step; 65,536 envs 26 us vs 21 us -- so only small jobs
 constexpr int64_t LAT_MAX_ENVS = 16384;
 constexpr int LAT_ENVS_PER_CTA = 32;
-int reset_max_ctas_per_sm();
-void set_reset_version(int v);
 void set_pdl(bool on);            // programmatic dependent launch of the step / reset kernels (DR_PDL, default on)
 int reset_grid_for(uint32_t n_env, int sm_count);
-constexpr int RESET_THREADS = 256;
 constexpr int STEP_THREADS = TILE;
 #ifndef DR_STEP_MIN_CTAS
 #define DR_STEP_MIN_CTAS 4

@@ -1,7 +1,8 @@
 // dr_kernels.cu -- sm_100a kernels of the domain-randomization pipeline.
 // One translation unit (the __constant__ parameters are shared by every kernel):
-//   dr_reset.cuh : reset_kernel -- episode-reset sampling, warp-cooperative
-//   dr_step.cuh  : step_kernel<LayerMask, Prefetch> -- the fused per-env-step transform
+//   dr_reset.cuh    : reset_kernel -- episode-reset sampling
+//   dr_step.cuh     : step_kernel_warp<LayerMask> -- the fused per-env-step transform (throughput mode)
+//   dr_step_lat.cuh : step_kernel_lat<LayerMask> -- the same transform, 8 warps per 32 envs (latency mode)
 //   below        : checkpoint export/import, the Philox test hook, and the host launchers.
 #include <cuda_runtime.h>
 
@@ -32,8 +33,14 @@ constexpr uint32_t B_STATEFUL = B_DELAY | B_BACKLASH | B_DROPOUT | B_OCCLUSION |
 #include "dr_step_lat.cuh"
 
 // =====================================================================================
-// Export / import (dr_env_state, 168 words per env).  A FRESH env exports its logical state
-// (all zero); import writes explicit state (clears FRESH).
+// Export / import (dr_env_state, 168 words per env, include/dr.h).  A FRESH env exports its logical
+// state (all zero); import writes explicit state (clears FRESH), then import_phys_kernel re-derives
+// the imported envs' physics rows from (seed, global id, imported episode index): the rows are a
+// pure function of those (PAPER.md:7-8 draws, keyed like every reset draw), so a resumed context
+// holds the same rows as the one that was exported (under the same parameters).
+// dr_env_state words: 0 episode, 1 delay, 2 p-index, 3 t_force, 4 flags, 5 k_f, 6 lambda, 7 mass,
+// 8 dneg[20], 28 dpos[20], 48 c_act[20], 68 off_tip[15], 83 c_obj[3], 86 q_c[4], 90 prev[20],
+// 110 slack[20], 130 last[15], 145 f_trig[3], 148 ema[20].
 // =====================================================================================
 constexpr int EXP_WORDS = 168;
 
@@ -46,16 +53,21 @@ __global__ void export_kernel(DevPtrs p, uint32_t* __restrict__ dst, uint32_t lo
     uint32_t* o = dst + (size_t)(e - lo) * EXP_WORDS;
     const uint32_t flags = S[ST_FLAGS * P];
     const bool fresh = flags & FRESH_BIT;
-    o[0] = R[REC_EPISODE * P];
-    o[1] = R[REC_DELAY * P];
-    o[2] = R[REC_PINDEX * P];
-    o[3] = R[REC_TFORCE * P];
+    o[0] = R[rec_off(REC_EPISODE)];
+    o[1] = R[rec_off(REC_DELAY)];
+    o[2] = R[rec_off(REC_PINDEX)];
+    o[3] = R[rec_off(REC_TFORCE)];
     o[4] = fresh ? 0u : flags;
     o[5] = fresh ? 0u : S[ST_KF * P];
-    o[6] = R[REC_LAMBDA * P];
-    o[7] = R[REC_MASS * P];
-    for (int i = 0; i < REC_STEP_PLANES - REC_DNEG; ++i) o[8 + i] = R[(REC_DNEG + i) * P];   // 82 words
-    for (int i = 0; i < ST_FLAGS; ++i) o[90 + i] = fresh ? 0u : S[i * P];                     // 55 words
+    o[6] = R[rec_off(REC_LAMBDA)];
+    o[7] = R[rec_off(REC_MASS)];
+    for (int j = 0; j < N_ACT; ++j) {
+        o[8 + j] = R[rec_off(rec_dneg(j))];
+        o[28 + j] = R[rec_off(rec_dpos(j))];
+        o[48 + j] = R[rec_off(rec_cact(j))];
+    }
+    for (int i = 0; i < 22; ++i) o[68 + i] = R[rec_off(REC_OFFTIP + i)];                        // off_tip, c_obj, q_c
+    for (int i = 0; i < ST_FLAGS; ++i) o[90 + i] = fresh ? 0u : S[i * P];                     // prev, slack, last
     for (int i = 0; i < 3; ++i) o[145 + i] = fresh ? 0u : S[(ST_FTRIG + i) * P];
     for (int i = 0; i < N_ACT; ++i) o[148 + i] = fresh ? 0u : S[(ST_EMA + i) * P];
 }
@@ -67,20 +79,46 @@ __global__ void import_kernel(DevPtrs p, const uint32_t* __restrict__ src, uint3
     uint32_t* R = p.rec + rec_index(e);
     uint32_t* S = p.st + st_index(e);
     const uint32_t* o = src + (size_t)(e - lo) * EXP_WORDS;
-    R[REC_EPISODE * P] = o[0];
-    R[REC_DELAY * P] = o[1];
-    R[REC_PINDEX * P] = o[2];
-    R[REC_TFORCE * P] = o[3];
+    R[rec_off(REC_EPISODE)] = o[0];
+    R[rec_off(REC_DELAY)] = o[1];
+    R[rec_off(REC_PINDEX)] = o[2];
+    R[rec_off(REC_TFORCE)] = o[3];
     S[ST_FLAGS * P] = o[4] & ~FRESH_BIT;
     S[ST_KF * P] = o[5];
-    R[REC_LAMBDA * P] = o[6];
+    R[rec_off(REC_LAMBDA)] = o[6];
     const float lam = __uint_as_float(o[6]);
-    R[REC_INVLAM * P] = __float_as_uint(lam > 0.f ? 1.0f / lam : 0.f);
-    R[REC_MASS * P] = o[7];
-    for (int i = 0; i < REC_STEP_PLANES - REC_DNEG; ++i) R[(REC_DNEG + i) * P] = o[8 + i];
+    R[rec_off(REC_INVLAM)] = __float_as_uint(lam > 0.f ? 1.0f / lam : 0.f);
+    R[rec_off(REC_MASS)] = o[7];
+    for (int j = 0; j < N_ACT; ++j) {
+        R[rec_off(rec_dneg(j))] = o[8 + j];
+        R[rec_off(rec_dpos(j))] = o[28 + j];
+        R[rec_off(rec_cact(j))] = o[48 + j];
+    }
+    for (int i = 0; i < 22; ++i) R[rec_off(REC_OFFTIP + i)] = o[68 + i];
     for (int i = 0; i < ST_FLAGS; ++i) S[i * P] = o[90 + i];
     for (int i = 0; i < 3; ++i) S[(ST_FTRIG + i) * P] = o[145 + i];
     for (int i = 0; i < N_ACT; ++i) S[(ST_EMA + i) * P] = o[148 + i];
+}
+
+// Physics rows of envs [lo, hi) from their (imported) episode index: a warp per env, as in the reset.
+constexpr int IMPORT_PHYS_THREADS = 256;
+__global__ void __launch_bounds__(IMPORT_PHYS_THREADS) import_phys_kernel(DevPtrs p, uint32_t lo, uint32_t hi) {
+    __shared__ float4 s_pd[MAX_PHYS];
+    __shared__ uint32_t s_src[MAX_PHYS];
+    __shared__ __align__(16) float s_dr[IMPORT_PHYS_THREADS / 32][RH_DRAW];
+    const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
+    for (int i = tid; i < c_dc.n_phys; i += IMPORT_PHYS_THREADS) {
+        s_pd[i] = p.rs_phys[i];
+        s_src[i] = p.rs_src[i];
+    }
+    if (lane == 0) s_dr[wid][RS_OFF_ZERO] = 0.f;
+    __syncthreads();
+    const bool phys_on = (c_dc.layer_mask & B_PHYS) != 0;
+    const int nub = phys_on ? (c_dc.n_phys_u + 3) / 4 : 0;
+    const int nnb = phys_on ? (c_dc.n_phys_n + 3) / 4 : 0;
+    const uint32_t e = lo + blockIdx.x * (IMPORT_PHYS_THREADS / 32) + wid;
+    if (e >= hi) return;
+    reset_phys_warp(p, e, p.rec[rec_index(e) + rec_off(REC_EPISODE)], lane, s_dr[wid], s_pd, s_src, nub, nnb);
 }
 
 __global__ void debug_philox_kernel(uint32_t n_env, uint32_t dom, uint32_t ch, uint32_t blk, uint4* __restrict__ out) {
@@ -95,11 +133,6 @@ cudaError_t upload_const(const DevConst& c, cudaStream_t s) {
     return cudaMemcpyToSymbolAsync(c_dc, &c, sizeof(DevConst), 0, cudaMemcpyHostToDevice, s);
 }
 
-// Reset kernel (DR_RESET at dr_init, A/B): 6 = thread-per-env record chain + warp-per-env physics
-// rows (reset_kernel_h, default; config 5 reset + step 0.418-0.425 ms vs v3's 0.458-0.460),
-// 3 = thread per resetting env over a compacted list (reset_kernel_t), 5 = task-split over
-// (task, env) items (reset_kernel_v5), 2 = warp per resetting env in four lane-parallel phases
-// (reset_kernel).
 // Step and reset kernels go out with cudaLaunchAttributeProgrammaticStreamSerialization: each waits
 // (griddepcontrol.wait) for the previous kernel before its first global access, so consecutive
 // steps overlap launch latency with the previous grid's tail (dr_device.cuh).  DR_PDL=0: plain launches.
@@ -121,43 +154,15 @@ static cudaError_t launch_k(void (*kernel)(KArgs...), int grid, int block, size_
     return cudaLaunchKernelEx(&cfg, kernel, args...);
 }
 
-static int g_reset_v = 6;
-void set_reset_version(int v) { g_reset_v = (v == 2 || v == 3 || v == 5) ? v : 6; }
-
 cudaError_t launch_reset(const DevPtrs& p, const uint8_t* mask, bool first, uint32_t n_env, int grid,
                          cudaStream_t s) {
-    const int f = first ? 1 : 0;
-    if (g_reset_v == 2) return launch_k(reset_kernel, grid, RESET_THREADS, 0, s, p, mask, f, n_env);
-    if (g_reset_v == 5) {
-        // per-CTA range: the envs split evenly over the grid, in whole 32-env chunks, <= R5_RANGE
-        const uint32_t per = (uint32_t)(((unsigned long long)n_env + grid - 1) / grid);
-        const uint32_t range = std::min<uint32_t>(R5_RANGE, std::max<uint32_t>(32u, (per + 31u) & ~31u));
-        return launch_k(reset_kernel_v5, grid, R5_THREADS, 0, s, p, mask, f, n_env, range);
-    }
-    if (g_reset_v == 6) return launch_k(reset_kernel_h, grid, RH_THREADS, 0, s, p, mask, f, n_env);
-    return launch_k(reset_kernel_t, grid, RT_THREADS, 0, s, p, mask, f, n_env);
+    return launch_k(reset_kernel, grid, RH_THREADS, 0, s, p, mask, first ? 1 : 0, n_env);
 }
 
 int reset_grid_for(uint32_t n_env, int sm_count) {
     int n = 0;
-    if (g_reset_v == 2) {
-        if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, reset_kernel, RESET_THREADS, 0) != cudaSuccess || n < 1) n = 1;
-        const long long chunks = (n_env + 31) / 32;
-        return (int)std::max<long long>(1, std::min<long long>((chunks + 7) / 8, (long long)sm_count * n));
-    }
-    if (g_reset_v == 5) {
-        // one resident wave: as many CTAs as fit (6 per SM), fewer for small jobs (>= 32 envs each)
-        if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, reset_kernel_v5, R5_THREADS, 0) != cudaSuccess || n < 1) n = 1;
-        const long long ranges = (n_env + 31) / 32;
-        return (int)std::max<long long>(1, std::min<long long>(ranges, (long long)sm_count * n));
-    }
-    if (g_reset_v == 6) {
-        if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, reset_kernel_h, RH_THREADS, 0) != cudaSuccess || n < 1) n = 1;
-        const long long ranges = (n_env + RH_RANGE - 1) / RH_RANGE;
-        return (int)std::max<long long>(1, std::min<long long>(ranges, (long long)sm_count * n));
-    }
-    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, reset_kernel_t, RT_THREADS, 0) != cudaSuccess || n < 1) n = 1;
-    const long long ranges = (n_env + RT_RANGE - 1) / RT_RANGE;
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, reset_kernel, RH_THREADS, 0) != cudaSuccess || n < 1) n = 1;
+    const long long ranges = (n_env + RH_RANGE - 1) / RH_RANGE;
     return (int)std::max<long long>(1, std::min<long long>(ranges, (long long)sm_count * n));
 }
 
@@ -166,48 +171,10 @@ static constexpr uint32_t MASK_CFG2 = B_TIMING | B_ACT_NOISE | B_BACKLASH | B_OB
 
 typedef void (*StepFn)(const DevPtrs, const float*, const float*, float*, float*, float*, float*, float*, uint32_t);
 
-// Optional TMA bulk L2 prefetch policy of the step kernel (DR_PREFETCH=0/1/2; A/B experiments).
-// Measured on B200 at 1M envs with the v1 kernel: 0 = none 2.48e9 env-steps/s, 1 = current tile
-// 2.10e9, 2 = next tile 1.92e9; the cp.async phase ring (v3+) makes it moot.
-static int g_prefetch = 0;
-
-void set_step_prefetch(int mode) { g_prefetch = (mode < 0 || mode > 2) ? 0 : mode; }
-
-// Ring pipeline of the step kernel (DR_PIPE at dr_init): 2 = warp-cooperative 16-byte cp.async.cg
-// ring (step_kernel_warp, default), 0 = per-thread 4-byte cp.async ring (step_kernel), 1 = CTA-wide
-// TMA bulk-copy ring (step_kernel_tma).  Measured on B200, 1M envs, full pipeline
-// (profiles/round1_notes.md), env-steps/s at 3 / 4 CTAs per SM:
-//   pipe 2: 4.04e9 / 4.10e9   pipe 0: 3.65e9 / 3.47e9   pipe 1: - / 3.27e9
-// Pipe 2 issues 4x fewer LDGSTS and bypasses L1 (the 4-byte .ca copies of pipe 0 allocate L1 lines,
-// which thrash once 4 CTAs leave ~24 KB of L1); pipe 1 couples the CTA's warps (a slot is refilled
-// only after the slowest warp releases it).
-static int g_pipe = 2;
-
-void set_step_pipe(int mode) { g_pipe = (mode < 0 || mode > 2) ? 2 : mode; }
-
-#ifndef DR_WARP_PF
-#define DR_WARP_PF 0
-#endif
-#ifndef DR_WARP_XT
-#define DR_WARP_XT 1   // cross-tile pipelining of S0 / A0 (A/B)
-#endif
 static StepFn step_fn_warp(uint32_t m) {
-    if (m == MASK_FULL) return step_kernel_warp<MASK_FULL, DR_WARP_PF, DR_WARP_XT != 0>;
-    if (m == MASK_CFG2) return step_kernel_warp<MASK_CFG2, DR_WARP_PF, DR_WARP_XT != 0>;
-    return step_kernel_warp<RUNTIME_MASK, DR_WARP_PF, DR_WARP_XT != 0>;
-}
-
-template <int PF>
-static StepFn step_fn_pf(uint32_t m) {
-    if (m == MASK_FULL) return step_kernel<MASK_FULL, PF>;
-    if (m == MASK_CFG2) return step_kernel<MASK_CFG2, PF>;
-    return step_kernel<RUNTIME_MASK, PF>;
-}
-
-static StepFn step_fn_tma(uint32_t m) {
-    if (m == MASK_FULL) return step_kernel_tma<MASK_FULL>;
-    if (m == MASK_CFG2) return step_kernel_tma<MASK_CFG2>;
-    return step_kernel_tma<RUNTIME_MASK>;
+    if (m == MASK_FULL) return step_kernel_warp<MASK_FULL>;
+    if (m == MASK_CFG2) return step_kernel_warp<MASK_CFG2>;
+    return step_kernel_warp<RUNTIME_MASK>;
 }
 
 // Step mode (chosen at dr_init from n_env_global): 0 = throughput (one thread per
@@ -225,15 +192,10 @@ static StepFn step_fn_lat(uint32_t m) {
 static StepFn step_fn(uint32_t layer_mask) {
     // PHYS does not affect the step; the variants (SMOOTH, SUBSTEP) run the runtime-mask kernel
     const uint32_t m = layer_mask & 0x6FFu;
-    if (g_step_mode == 1) return step_fn_lat(m);
-    if (g_pipe == 1) return step_fn_tma(m);
-    if (g_pipe == 2) return step_fn_warp(m);
-    if (g_prefetch == 0) return step_fn_pf<0>(m);
-    if (g_prefetch == 2) return step_fn_pf<2>(m);
-    return step_fn_pf<1>(m);
+    return g_step_mode == 1 ? step_fn_lat(m) : step_fn_warp(m);
 }
 
-static size_t step_dyn_smem() { return g_step_mode == 1 ? 0 : (g_pipe == 1 ? STEP_TMA_DYN_SMEM : STEP_DYN_SMEM); }
+static size_t step_dyn_smem() { return g_step_mode == 1 ? 0 : STEP_DYN_SMEM; }
 static int step_threads() { return g_step_mode == 1 ? LAT_THREADS : STEP_THREADS; }
 
 // the phase ring is dynamic shared memory (static + dynamic > 48 KB needs the opt-in attribute)
@@ -248,12 +210,6 @@ int step_max_ctas_per_sm(uint32_t layer_mask) {
     if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, step_fn_ready(layer_mask), step_threads(), step_dyn_smem()) !=
         cudaSuccess)
         return 1;
-    return n > 0 ? n : 1;
-}
-
-int reset_max_ctas_per_sm() {
-    int n = 0;
-    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, reset_kernel, RESET_THREADS, 0) != cudaSuccess) return 1;
     return n > 0 ? n : 1;
 }
 
@@ -278,6 +234,10 @@ cudaError_t launch_export(const DevPtrs& p, void* dst, uint32_t lo, uint32_t hi,
 cudaError_t launch_import(const DevPtrs& p, const void* src, uint32_t lo, uint32_t hi, cudaStream_t s) {
     const uint32_t n = hi - lo;
     import_kernel<<<(n + 127) / 128, 128, 0, s>>>(p, static_cast<const uint32_t*>(src), lo, hi);
+    cudaError_t e = cudaGetLastError();
+    if (e != cudaSuccess) return e;
+    constexpr uint32_t W = IMPORT_PHYS_THREADS / 32;
+    import_phys_kernel<<<(n + W - 1) / W, IMPORT_PHYS_THREADS, 0, s>>>(p, lo, hi);
     return cudaGetLastError();
 }
 

@@ -4,22 +4,15 @@
 // Mapping: persistent CTAs of TILE (= 128) threads, one thread per env, static round-robin tiles
 // of 128 envs.  Every byte of state makes one HBM round trip per step.
 //
-// The per-env record/state planes (AoSoA: a tile's plane is one contiguous 512-B chunk) are
-// consumed in seven phases -- S0 (scalars), A0..A4 (4 actuators each), OB (observation offsets)
-// -- streamed through a shared-memory ring so that in-flight bytes live in shared memory, not in
-// registers.  Two interchangeable pipelines feed the ring:
-//   * PipeThread (step_kernel, default): a per-thread 2-slot ring filled with 4-byte cp.async
-//     (LDGSTS) -- each thread's pipeline is independent of the other warps'.
-//   * PipeTma (step_kernel_tma, DR_PIPE=1): a 3-slot CTA-wide ring filled by TMA bulk copies
-//     (cp.async.bulk + mbarrier complete_tx); a slot is refilled two phases ahead by the last
-//     warp to release it (smem atomic), so no thread ever blocks to produce; the row-major input
-//     tile is also a TMA bulk copy, and the next tile's inputs are issued as soon as the current
-//     tile's outputs are stored.  Measured slower (the ring couples the CTA's warps); kept as an
-//     A/B alternative and parity-tested.
-// Outputs are written in place over the input rows in shared memory (out_actions over actions,
-// out_obs + out_force over raw_obs) and stored with coalesced 128/64-bit stores.  Held fingertip
-// readings are fetched with per-thread cp.async while the fingertip noise is computed.  Stats:
-// register accumulators -> CTA shared-memory reduction -> last-CTA fixed-order fp64 reduction.
+// The per-env record (sector groups, dr_internal.h) and state planes are consumed in seven phases
+// -- S0 (scalars), A0..A4 (4 actuators each), OB (observation offsets) -- streamed through a
+// two-slot shared-memory ring so that in-flight bytes live in shared memory, not in registers.  A
+// warp fills its own 32-env column segment of a slot with 16-byte cp.async.cg (L1 bypass) and
+// hands over with __syncwarp, so the four warps of a CTA run their pipelines independently
+// (DESIGN.md §8).  Outputs are written in place over the input rows in shared memory (out_actions
+// over actions, out_obs + out_force over raw_obs) and stored with coalesced 128/64-bit stores.  Held
+// fingertip readings are fetched with per-thread cp.async while the fingertip noise is computed.
+// Stats: register accumulators -> CTA shared-memory reduction -> order-free exact fp64 atomics.
 #pragma once
 
 // State write-back policy (A/B): 0 = default write-back stores, 1 = streaming (st.global.cs).
@@ -65,186 +58,57 @@ __device__ __forceinline__ void cp_commit() { asm volatile("cp.async.commit_grou
 template <int N>
 __device__ __forceinline__ void cp_wait() { asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory"); }
 
-// ---- mbarrier + TMA bulk-copy helpers (sm_90+ PTX; SASS: SYNCS.* and UBLKCP) --------------
-__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
-    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count) : "memory");
-}
-__device__ __forceinline__ void mbar_arrive_expect_tx(uint64_t* bar, uint32_t bytes) {
-    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes) : "memory");
-}
-__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
-    asm volatile(
-        "{\n\t.reg .pred p;\n"
-        "WAIT_%=:\n\t"
-        "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t"
-        "@!p bra WAIT_%=;\n}" ::"r"(smem_u32(bar)),
-        "r"(parity)
-        : "memory");
-}
-__device__ __forceinline__ void tma_load(void* sdst, const void* gsrc, uint32_t bytes, uint64_t* bar) {
-    asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
-                     smem_u32(sdst)),
-                 "l"(gsrc), "r"(bytes), "r"(smem_u32(bar))
-                 : "memory");
-}
-// order this thread's generic-proxy shared-memory accesses before subsequent async-proxy (TMA)
-// writes to the same buffers (ring / I/O slot reuse)
-__device__ __forceinline__ void fence_proxy_async() { asm volatile("fence.proxy.async.shared::cta;" ::: "memory"); }
-__device__ __forceinline__ void fence_mbar_init() { asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory"); }
-
-__device__ __forceinline__ void l2_prefetch(const void* ptr, uint32_t bytes) {
-    if (bytes >= 16u)
-        asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(ptr), "r"(bytes & ~15u) : "memory");
-}
-
-// Optional TMA bulk L2 prefetch of a tile's record/state blocks + input rows (DR_PREFETCH; A/B).
-// first_item = 2 prefetches only the row-major input rows.
-template <uint32_t L>
-__device__ __forceinline__ void prefetch_tile(const DevPtrs& p, const float* actions, const float* raw_obs,
-                                              uint32_t tile, uint32_t n_env, int first_item = 0) {
-    const uint32_t e0 = tile * TILE;
-    if (e0 >= n_env) return;
-    const uint32_t cnt = min((uint32_t)TILE, n_env - e0);
-    for (int item = first_item + (int)threadIdx.x; item < 4; item += blockDim.x) {
-        if (item == 0) l2_prefetch(p.rec + rec_index(e0), REC_STEP_PLANES * TILE * 4u);
-        else if (item == 1) l2_prefetch(p.st + st_index(e0), (on<L>(B_SMOOTH) ? ST_PLANES : ST_EMA) * TILE * 4u);
-        else if (item == 2) l2_prefetch(actions + (size_t)e0 * N_ACT, cnt * N_ACT * 4u);
-        else l2_prefetch(raw_obs + (size_t)e0 * OBS_IN, cnt * OBS_IN * 4u);   // rounded down: in bounds
-    }
-}
-
 // ---- phase ring layout ---------------------------------------------------------------------
-// slot row w of thread tid lives at slot[w * TILE + tid]: a warp reads 32 consecutive words
-// (conflict-free LDS), and a tile's plane chunk (512 B) maps onto one row.
-constexpr int RING_W = 22;
+// A slot is RING_W rows of TILE words, and warp w owns columns 32 w .. 32 w + 31 of every row (the
+// four warps of a CTA run their pipelines independently, so no row segment is shared).  A state
+// plane takes one row (thread tid's word at row * TILE + tid: a warp reads 32 consecutive words,
+// conflict-free).  A record quad -- 4 consecutive record words of one env, half a sector group --
+// takes 4 rows: lane l's float4 sits in row + l / 8 at column 32 w + 4 (l % 8) (quad_off), so each
+// quarter-warp of an LDS.128 reads 128 contiguous bytes (conflict-free).
+// Record groups are always fetched whole (two 16-byte cp.async per lane pair, 512 contiguous bytes
+// per instruction): a half-group fetch would touch each sector twice and scatter its shared-memory
+// writes (measured: 8x the LDGSTS wavefronts, 1.8x the L2 sectors, 17 % slower).  A group whose two
+// halves feed different phases lands in two places: half 0 in its phase's rows, half 1 in rows a
+// later phase reads (the c_act quads: see cact()).
+constexpr int RING_W = 24;
 constexpr int N_PHASES = 7;   // S0, A0..A4, OB
-constexpr size_t STEP_DYN_SMEM = 2 * RING_W * TILE * sizeof(uint32_t);   // PipeThread: 2 slots
-// S0 rows: record planes 0..3 then state planes 55..59 (both contiguous ranges)
-enum : int { S0_DELAY = 0, S0_INVLAM = 1, S0_TFORCE = 2, S0_MASS = 3, S0_FLAGS = 4, S0_FTRIG = 5, S0_KF = 8 };
-// A_b rows: prev 0..3 | slack 4..7 | dneg 8..11 | dpos 12..15 | cact 16..19 ; OB rows: offtip 0..14 |
-// c_obj 15..17 | q_c 18..21 (record planes 64..85)
+constexpr size_t STEP_DYN_SMEM = 2 * RING_W * TILE * sizeof(uint32_t);   // 2 slots
+// S0 (slot 0): rows 0..3 the quad (delay bits, 1/lambda, force threshold, mass) = record words 0..3,
+// then the state planes flags (row 4), f_trig (5..7), k_f (8).
+enum : int { S0_FLAGS = 4, S0_FTRIG = 5, S0_KF = 8 };
+// A_b (slot 1 for even b, slot 0 for odd b): rows 0..3 prev (planes), 4..7 slack (planes), 8 the
+// delta-1 quad, 12 the delta+1 quad (record group 1 + b).  The c_act quad of A_b (record words
+// rec_cact(4b)..+3) sits at cact(b): A0 slot 1 rows 16.. (second half of group 0, fetched with S0),
+// A1 / A3 slot 0 rows 16.. and A2 slot 0 rows 20.. / A4 slot 1 rows 20.. (groups 6 / 7, fetched with
+// A1 / A3).  OB (slot 0): rows 4h.. = quad h of record words 64..87 (off_tip 0..14, c_obj 0..2,
+// q_c 0..3; the last two words, lambda and p-index, ride along in their sector).
+enum : int { A_PREV = 0, A_SLACK = 4, A_DNEG = 8, A_DPOS = 12, A_CACT = 16, A_CACT2 = 20 };
 
-// -- per-thread 4-byte copies (PipeThread) --
-template <uint32_t L>
-__device__ __forceinline__ void issue_s0(uint32_t* slot, const uint32_t* R, const uint32_t* S, size_t P) {
-    if (on<L>(B_TIMING)) cp_async4(slot + S0_INVLAM * TILE, R + REC_INVLAM * P);
-    if (on<L>(B_DELAY)) cp_async4(slot + S0_DELAY * TILE, R + REC_DELAY * P);
-    if (on<L>(B_STATEFUL)) cp_async4(slot + S0_FLAGS * TILE, S + ST_FLAGS * P);   // timers, has_last, FRESH
-    if (on<L>(B_FORCE)) {
-        cp_async4(slot + S0_TFORCE * TILE, R + REC_TFORCE * P);
-        cp_async4(slot + S0_MASS * TILE, R + REC_MASS * P);
-        cp_async4(slot + S0_KF * TILE, S + ST_KF * P);
-#pragma unroll
-        for (int c = 0; c < 3; ++c) cp_async4(slot + (S0_FTRIG + c) * TILE, S + (ST_FTRIG + c) * P);
-    }
+__device__ __forceinline__ float ringf(const uint32_t* slot, int row, int tid) {
+    return __uint_as_float(slot[row * TILE + tid]);
 }
-template <uint32_t L>
-__device__ __forceinline__ void issue_act(uint32_t* slot, const uint32_t* R, const uint32_t* S, size_t P, int b) {
-#pragma unroll
-    for (int q = 0; q < 4; ++q) {
-        const int j = 4 * b + q;
-        if (on<L>(B_DELAY)) cp_async4(slot + (0 + q) * TILE, S + (ST_PREV + j) * P);
-        if (on<L>(B_BACKLASH)) {
-            cp_async4(slot + (4 + q) * TILE, S + (ST_SLACK + j) * P);
-            cp_async4(slot + (8 + q) * TILE, R + (REC_DNEG + j) * P);
-            cp_async4(slot + (12 + q) * TILE, R + (REC_DPOS + j) * P);
-        }
-        if (on<L>(B_ACT_NOISE)) cp_async4(slot + (16 + q) * TILE, R + (REC_CACT + j) * P);
-    }
+// word offset of env-lane tid's quad inside a 4-row quad block (see above)
+__device__ __forceinline__ int quad_off(int tid) { return ((tid & 31) >> 3) * TILE + (tid & ~31) + 4 * (tid & 7); }
+__device__ __forceinline__ float4 ringq(const uint32_t* slot, int row, int tid) {
+    return *reinterpret_cast<const float4*>(slot + row * TILE + quad_off(tid));
 }
-template <uint32_t L>
-__device__ __forceinline__ void issue_obs(uint32_t* slot, const uint32_t* R, size_t P) {
-    if (on<L>(B_OBS_NOISE)) {
-#pragma unroll
-        for (int w = 0; w < 22; ++w) cp_async4(slot + w * TILE, R + (REC_OFFTIP + w) * P);
-    }
-}
+__device__ __forceinline__ float q4(const float4 v, int c) { return c == 0 ? v.x : (c == 1 ? v.y : (c == 2 ? v.z : v.w)); }
 
-// -- CTA-wide TMA bulk copies of phase k of a tile (PipeTma): contiguous plane ranges --
+// Warp-cooperative ring: a warp fills its 32-env column segment of a slot with 16-byte cp.async.cg
+// (L1 bypass).  State planes: one instruction moves 4 planes x 128 B (lane l: plane l >> 3, bytes
+// 16 (l & 7)).  Record groups: two instructions, each moving the 32-byte groups of 16 envs (512
+// contiguous bytes; lane l: env 16 i + l / 2, half l & 1).  Lanes read words other lanes copied, so
+// every hand-over is a __syncwarp.  Cross-tile pipelining: the next tile's A0 is issued into slot 1
+// once A4 is consumed and its S0 into slot 0 once OB is consumed, so a new tile starts with both
+// phases already landed; the input rows are waited for only after the timing section (io_wait).
 template <uint32_t L>
-__device__ __forceinline__ uint32_t phase_bytes(int k) {
-    constexpr uint32_t C = TILE * 4u;   // one plane chunk
-    if (k == 0) {
-        uint32_t b = (on<L>(B_TIMING) || on<L>(B_DELAY) || on<L>(B_FORCE)) ? 4 * C : 0u;
-        if (on<L>(B_FORCE)) b += 5 * C;
-        else if (on<L>(B_STATEFUL)) b += C;
-        return b;
-    }
-    if (k == N_PHASES - 1) return on<L>(B_OBS_NOISE) ? 22 * C : 0u;
-    return (on<L>(B_DELAY) ? 4 * C : 0u) + (on<L>(B_BACKLASH) ? 12 * C : 0u) + (on<L>(B_ACT_NOISE) ? 4 * C : 0u);
-}
-template <uint32_t L>
-__device__ __forceinline__ void issue_phase_tma(uint32_t* slot, const uint32_t* Rt, const uint32_t* St, int k,
-                                                uint64_t* bar) {
-    constexpr uint32_t C = TILE * 4u;
-    mbar_arrive_expect_tx(bar, phase_bytes<L>(k));
-    if (k == 0) {
-        if (on<L>(B_TIMING) || on<L>(B_DELAY) || on<L>(B_FORCE)) tma_load(slot, Rt, 4 * C, bar);   // planes 0..3
-        if (on<L>(B_FORCE)) tma_load(slot + S0_FLAGS * TILE, St + ST_FLAGS * TILE, 5 * C, bar);    // 55..59
-        else if (on<L>(B_STATEFUL)) tma_load(slot + S0_FLAGS * TILE, St + ST_FLAGS * TILE, C, bar);
-    } else if (k == N_PHASES - 1) {
-        if (on<L>(B_OBS_NOISE)) tma_load(slot, Rt + REC_OFFTIP * TILE, 22 * C, bar);
-    } else {
-        const int b = k - 1;
-        if (on<L>(B_DELAY)) tma_load(slot, St + (ST_PREV + 4 * b) * TILE, 4 * C, bar);
-        if (on<L>(B_BACKLASH)) {
-            tma_load(slot + 4 * TILE, St + (ST_SLACK + 4 * b) * TILE, 4 * C, bar);
-            tma_load(slot + 8 * TILE, Rt + (REC_DNEG + 4 * b) * TILE, 4 * C, bar);
-            tma_load(slot + 12 * TILE, Rt + (REC_DPOS + 4 * b) * TILE, 4 * C, bar);
-        }
-        if (on<L>(B_ACT_NOISE)) tma_load(slot + 16 * TILE, Rt + (REC_CACT + 4 * b) * TILE, 4 * C, bar);
-    }
-}
-
-__device__ __forceinline__ float ringf(const uint32_t* slot, int w) { return __uint_as_float(slot[w * TILE]); }
-
-// ---- pipeline policies -----------------------------------------------------------------------
-// Per-thread ring (v3-v5): slot0 holds S0, A1, A3, OB; slot1 holds A0, A2, A4.
-template <uint32_t L>
-struct PipeThread {
-    uint32_t* slot0;
-    uint32_t* slot1;
-    const uint32_t* R;
-    const uint32_t* S;
-    __device__ __forceinline__ const uint32_t* s0() { return slot0; }   // the tile loop waited for it
-    __device__ __forceinline__ void s0_done() {
-        issue_act<L>(slot0, R, S, PLANE, 1);
-        cp_commit();
-    }
-    __device__ __forceinline__ void io_wait() {}
-    __device__ __forceinline__ const uint32_t* act(int b) {
-        cp_wait<1>();
-        return (b & 1) ? slot0 : slot1;
-    }
-    __device__ __forceinline__ void act_done(int b) {
-        uint32_t* sl = (b & 1) ? slot0 : slot1;
-        if (b + 2 < 5) issue_act<L>(sl, R, S, PLANE, b + 2);
-        else if (b + 2 == 5) issue_obs<L>(sl, R, PLANE);
-        cp_commit();
-    }
-    // called after the held-reading copies were committed: wait for everything but them
-    __device__ __forceinline__ const uint32_t* obs() {
-        cp_wait<1>();
-        return slot0;
-    }
-    __device__ __forceinline__ void obs_done() {}
-};
-
-// Warp-cooperative ring (DR_PIPE=2): the same 2-slot layout as PipeThread, but a warp fills its
-// 32-env column segment of a slot with 16-byte cp.async.cg (L1 bypass): one instruction moves 4
-// planes x 128 B (lane l: plane l >> 3, bytes 16 (l & 7)), i.e. 4x fewer LDGSTS and no L1 lines.
-// Lanes read words other lanes copied, so every hand-over is a __syncwarp.
-template <uint32_t L, bool XT = false>
 struct PipeWarp {
     uint32_t* slot0;   // s_ring (row 0, column 0)
     uint32_t* slot1;
-    const uint32_t* Rw;   // record tile block + this warp's first column
+    const uint32_t* Rt;   // record tile block
     const uint32_t* Sw;   // state tile block + this warp's first column
     int tid, lane, wcol;  // wcol = 32 * warp
-    // XT (cross-tile pipelining): the next tile's A0 is issued into slot1 once A4 is consumed and its
-    // S0 into slot0 once OB is consumed, so a new tile starts with both phases already landed; the
-    // input rows are then waited for only after the timing section (io_wait).
-    const uint32_t* nRw;  // next tile of this CTA (nullptr: none)
+    const uint32_t* nRt;  // next tile of this CTA (nullptr: none)
     const uint32_t* nSw;
     __device__ __forceinline__ void planes(uint32_t* slot, int row, const uint32_t* src, int n) {
         const int sub = 4 * (lane & 7);
@@ -253,118 +117,78 @@ struct PipeWarp {
             if (pi < n) cp_async16(slot + (row + pi) * TILE + wcol + sub, src + pi * TILE + sub);
         }
     }
+    // record sector group grp of the warp's 32 envs: half 0 -> d0 (a quad row block), half 1 -> d1
+    __device__ __forceinline__ void group(uint32_t* d0, uint32_t* d1, const uint32_t* R, int grp) {
+        const int h = lane & 1;
+#pragma unroll
+        for (int i = 0; i < 2; ++i) {
+            const int el = wcol + 16 * i + (lane >> 1);
+            cp_async16((h ? d1 : d0) + quad_off(el), R + (size_t)grp * (TILE * 8) + (size_t)el * 8 + 4 * h);
+        }
+    }
+    __device__ __forceinline__ uint32_t* row(uint32_t* slot, int r) { return slot + r * TILE; }
+    __device__ __forceinline__ const uint32_t* cact(int b) const {
+        return (b == 0 || b == 4 ? slot1 : slot0) + (b == 2 || b == 4 ? A_CACT2 : A_CACT) * TILE;
+    }
     __device__ __forceinline__ void issue_s0_of(const uint32_t* R, const uint32_t* S) {
-        if (on<L>(B_TIMING) || on<L>(B_DELAY) || on<L>(B_FORCE)) planes(slot0, 0, R, 4);   // record planes 0..3
-        if (on<L>(B_FORCE)) planes(slot0, S0_FLAGS, S + ST_FLAGS * TILE, 5);                // state planes 55..59
+        if (on<L>(B_TIMING) || on<L>(B_DELAY) || on<L>(B_FORCE) || on<L>(B_ACT_NOISE))
+            group(slot0, row(slot1, A_CACT), R, 0);                                   // S0 quad | c_act 0..3
+        if (on<L>(B_FORCE)) planes(slot0, S0_FLAGS, S + ST_FLAGS * TILE, 5);         // state planes 55..59
         else if (on<L>(B_STATEFUL)) planes(slot0, S0_FLAGS, S + ST_FLAGS * TILE, 1);
     }
     __device__ __forceinline__ void issue_act_of(uint32_t* sl, int b, const uint32_t* R, const uint32_t* S) {
-        if (on<L>(B_DELAY)) planes(sl, 0, S + (ST_PREV + 4 * b) * TILE, 4);
+        if (on<L>(B_DELAY)) planes(sl, A_PREV, S + (ST_PREV + 4 * b) * TILE, 4);
         if (on<L>(B_BACKLASH)) {
-            planes(sl, 4, S + (ST_SLACK + 4 * b) * TILE, 4);
-            planes(sl, 8, R + (REC_DNEG + 4 * b) * TILE, 4);
-            planes(sl, 12, R + (REC_DPOS + 4 * b) * TILE, 4);
+            planes(sl, A_SLACK, S + (ST_SLACK + 4 * b) * TILE, 4);
+            group(row(sl, A_DNEG), row(sl, A_DPOS), R, REC_G_BL + b);
         }
-        if (on<L>(B_ACT_NOISE)) planes(sl, 16, R + (REC_CACT + 4 * b) * TILE, 4);
+        if (on<L>(B_ACT_NOISE)) {
+            if (b == 1) group(row(slot0, A_CACT), row(slot0, A_CACT2), R, 6);   // c_act 4..7 | 8..11
+            if (b == 3) group(row(slot0, A_CACT), row(slot1, A_CACT2), R, 7);   // c_act 12..15 | 16..19
+        }
     }
-    __device__ __forceinline__ void issue_s0() { issue_s0_of(Rw, Sw); }
-    __device__ __forceinline__ void issue_act(uint32_t* sl, int b) { issue_act_of(sl, b, Rw, Sw); }
+    __device__ __forceinline__ void issue_s0() { issue_s0_of(Rt, Sw); }
+    __device__ __forceinline__ void issue_act(uint32_t* sl, int b) { issue_act_of(sl, b, Rt, Sw); }
     __device__ __forceinline__ void issue_obs(uint32_t* sl) {
-        if (on<L>(B_OBS_NOISE)) planes(sl, 0, Rw + REC_OFFTIP * TILE, 22);
+        if (on<L>(B_OBS_NOISE)) {
+#pragma unroll
+            for (int gi = 0; gi < 3; ++gi) group(row(sl, 8 * gi), row(sl, 8 * gi + 4), Rt, REC_OFFTIP / 8 + gi);
+        }
     }
-    __device__ __forceinline__ const uint32_t* s0() { return slot0 + tid; }   // the tile loop waited
+    __device__ __forceinline__ const uint32_t* s0() { return slot0; }   // the tile loop waited
     __device__ __forceinline__ void s0_done() {
         __syncwarp();
         issue_act(slot0, 1);
         cp_commit();
     }
-    __device__ __forceinline__ void io_wait() {
-        if constexpr (XT) {   // the tile's input rows (all but the A1 group just committed)
-            cp_wait<1>();
-            __syncthreads();
-        }
+    __device__ __forceinline__ void io_wait() {   // the tile's input rows (all but the A1 group just committed)
+        cp_wait<1>();
+        __syncthreads();
     }
     __device__ __forceinline__ const uint32_t* act(int b) {
         cp_wait<1>();
         __syncwarp();
-        return ((b & 1) ? slot0 : slot1) + tid;
+        return (b & 1) ? slot0 : slot1;
     }
     __device__ __forceinline__ void act_done(int b) {
         uint32_t* sl = (b & 1) ? slot0 : slot1;
         __syncwarp();
         if (b + 2 < 5) issue_act(sl, b + 2);
         else if (b + 2 == 5) issue_obs(sl);
-        else if (XT && nRw) issue_act_of(slot1, 0, nRw, nSw);   // b == 4: next tile's A0
+        else if (nRt) issue_act_of(slot1, 0, nRt, nSw);   // b == 4: next tile's A0
         cp_commit();
     }
     // called after the held-reading copies were committed: OB is older than (next A0, held)
     __device__ __forceinline__ const uint32_t* obs() {
-        cp_wait<XT ? 2 : 1>();
+        cp_wait<2>();
         __syncwarp();
-        return slot0 + tid;
+        return slot0;
     }
-    __device__ __forceinline__ void obs_done() {
-        if constexpr (XT) {   // next tile's S0 into the slot OB just vacated
-            __syncwarp();
-            if (nRw) issue_s0_of(nRw, nSw);
-            cp_commit();
-        }
-    }
-};
-
-// CTA-wide TMA ring: phase ph (counted over this CTA's tiles) lives in slot ph % NS.
-constexpr int TMA_SLOTS = 3;
-struct TmaShared {
-    uint64_t full[TMA_SLOTS];
-    uint64_t io_full;
-    uint32_t rel[TMA_SLOTS];   // warps that released the slot's current phase
-    uint32_t io_rel;
-};
-
-template <uint32_t L>
-__device__ __forceinline__ void tma_issue_phase(const DevPtrs& p, uint32_t* ring, TmaShared* ts, uint32_t ph,
-                                                uint32_t n_my, uint32_t n_tiles) {
-    const uint32_t it = ph / N_PHASES, k = ph % N_PHASES;
-    if (it >= n_my) return;
-    const uint32_t tile = blockIdx.x + it * gridDim.x;
-    if (tile >= n_tiles) return;
-    const uint32_t e0 = tile * TILE;
-    issue_phase_tma<L>(ring + (ph % TMA_SLOTS) * (RING_W * TILE), p.rec + rec_index(e0), p.st + st_index(e0), (int)k,
-                       &ts->full[ph % TMA_SLOTS]);
-}
-
-template <uint32_t L>
-struct PipeTma {
-    const DevPtrs* p;
-    uint32_t* ring;
-    TmaShared* ts;
-    uint32_t ph0;   // global phase index of this tile's S0
-    uint32_t it;    // tile iteration (I/O parity)
-    uint32_t n_my, n_tiles;
-    int tid;
-    __device__ __forceinline__ const uint32_t* wait(uint32_t ph) {
-        mbar_wait(&ts->full[ph % TMA_SLOTS], (ph / TMA_SLOTS) & 1u);
-        return ring + (ph % TMA_SLOTS) * (RING_W * TILE) + tid;
-    }
-    // the last of the 4 warps to release phase ph refills its slot with phase ph + NS
-    __device__ __forceinline__ void release(uint32_t ph) {
+    __device__ __forceinline__ void obs_done() {   // next tile's S0 into the slot OB just vacated
         __syncwarp();
-        if ((tid & 31) == 0) {
-            const uint32_t s = ph % TMA_SLOTS;
-            if (atomicAdd(&ts->rel[s], 1u) == (uint32_t)(TILE / 32) - 1u) {
-                ts->rel[s] = 0u;
-                fence_proxy_async();
-                tma_issue_phase<L>(*p, ring, ts, ph + TMA_SLOTS, n_my, n_tiles);
-            }
-        }
+        if (nRt) issue_s0_of(nRt, nSw);
+        cp_commit();
     }
-    __device__ __forceinline__ const uint32_t* s0() { return wait(ph0); }
-    __device__ __forceinline__ void s0_done() { release(ph0); }
-    __device__ __forceinline__ void io_wait() { mbar_wait(&ts->io_full, it & 1u); }
-    __device__ __forceinline__ const uint32_t* act(int b) { return wait(ph0 + 1 + b); }
-    __device__ __forceinline__ void act_done(int b) { release(ph0 + 1 + b); }
-    __device__ __forceinline__ const uint32_t* obs() { return wait(ph0 + N_PHASES - 1); }
-    __device__ __forceinline__ void obs_done() { release(ph0 + N_PHASES - 1); }
 };
 
 // Backlash gate alpha = 1 - clamp(num / den, 0, 1) with num = |sgn - s|, den = |s' - s| + eps
@@ -386,8 +210,8 @@ __device__ __forceinline__ float backlash_alpha(float num, float den) {
 }
 
 // ---- the per-env transform -------------------------------------------------------------------
-// valid = false only for the lanes past n_env in the tail tile of the TMA kernel: they follow the
-// same path (the ring protocol is warp-synchronous) but store nothing and count nothing.
+// valid = false: a lane past n_env in a tail tile (it computes on garbage, stores nothing and
+// counts nothing).
 template <uint32_t L, class Pipe>
 __device__ __forceinline__ void env_step(const DevPtrs& p, uint32_t e, bool valid, uint32_t t, int tid, float* s_act,
                                          float* s_obs, float* s_dt, float* out_sub, Pipe& pipe, Acc& acc) {
@@ -403,22 +227,24 @@ __device__ __forceinline__ void env_step(const DevPtrs& p, uint32_t e, bool vali
 
     // ---- S0: scalars ----
     const uint32_t* s0 = pipe.s0();
-    const float il = on<L>(B_TIMING) ? ringf(s0, S0_INVLAM) : 0.f;
-    const uint32_t dbits = on<L>(B_DELAY) ? s0[S0_DELAY * TILE] : 0u;
+    const float4 sq = (on<L>(B_TIMING) || on<L>(B_DELAY) || on<L>(B_FORCE)) ? ringq(s0, 0, tid)
+                                                                             : make_float4(0.f, 0.f, 0.f, 0.f);
+    const float il = on<L>(B_TIMING) ? sq.y : 0.f;
+    const uint32_t dbits = on<L>(B_DELAY) ? __float_as_uint(sq.x) : 0u;
     // a FRESH env (reset since its last step) has all-zero state: slack 0, prev 0, no reading,
     // timers 0, force 0 -- the reset kernel does not write the state planes
-    const uint32_t flags_raw = on<L>(B_STATEFUL) ? s0[S0_FLAGS * TILE] : 0u;
+    const uint32_t flags_raw = on<L>(B_STATEFUL) ? s0[S0_FLAGS * TILE + tid] : 0u;
     const bool fresh = (flags_raw & FRESH_BIT) != 0u;
     const uint32_t flags = (kHold && hold_layers && !fresh) ? flags_raw : 0u;
     uint32_t tf = 0, kf = 0;
     float mass = 0.f, ft[3] = {0.f, 0.f, 0.f};
     if (on<L>(B_FORCE)) {
-        tf = s0[S0_TFORCE * TILE];
-        mass = ringf(s0, S0_MASS);
+        tf = __float_as_uint(sq.z);
+        mass = sq.w;
         if (!fresh) {
-            kf = s0[S0_KF * TILE];
+            kf = s0[S0_KF * TILE + tid];
 #pragma unroll
-            for (int c = 0; c < 3; ++c) ft[c] = ringf(s0, S0_FTRIG + c);
+            for (int c = 0; c < 3; ++c) ft[c] = ringf(s0, S0_FTRIG + c, tid);
         }
     }
     pipe.s0_done();
@@ -464,13 +290,17 @@ __device__ __forceinline__ void env_step(const DevPtrs& p, uint32_t e, bool vali
     for (int b = 0; b < 5; ++b) {   // rolled: keeps the kernel inside the instruction cache
         const uint32_t* sl = pipe.act(b);
         float prev[4], slack[4], dneg[4], dpos[4], cact[4];
+        const float4 z4 = make_float4(0.f, 0.f, 0.f, 0.f);
+        const float4 dn4 = on<L>(B_BACKLASH) ? ringq(sl, A_DNEG, tid) : z4;
+        const float4 dp4 = on<L>(B_BACKLASH) ? ringq(sl, A_DPOS, tid) : z4;
+        const float4 ca4 = on<L>(B_ACT_NOISE) ? ringq(pipe.cact(b), 0, tid) : z4;
 #pragma unroll
         for (int q = 0; q < 4; ++q) {
-            prev[q] = (on<L>(B_DELAY) && !fresh) ? ringf(sl, q) : 0.f;
-            slack[q] = (on<L>(B_BACKLASH) && !fresh) ? ringf(sl, 4 + q) : 0.f;
-            dneg[q] = on<L>(B_BACKLASH) ? ringf(sl, 8 + q) : 0.f;
-            dpos[q] = on<L>(B_BACKLASH) ? ringf(sl, 12 + q) : 0.f;
-            cact[q] = on<L>(B_ACT_NOISE) ? ringf(sl, 16 + q) : 0.f;
+            prev[q] = (on<L>(B_DELAY) && !fresh) ? ringf(sl, A_PREV + q, tid) : 0.f;
+            slack[q] = (on<L>(B_BACKLASH) && !fresh) ? ringf(sl, A_SLACK + q, tid) : 0.f;
+            dneg[q] = q4(dn4, q);
+            dpos[q] = q4(dp4, q);
+            cact[q] = q4(ca4, q);
         }
         pipe.act_done(b);
 
@@ -691,11 +521,12 @@ __device__ __forceinline__ void env_step(const DevPtrs& p, uint32_t e, bool vali
         for (int b = 0; b < 4; ++b) {
             float z[4];
             normals4_t<kSfuNormals>(philox(g, t, CH_TIP_NOISE, b), z);
+            const float4 off4 = ringq(ob, 4 * b, tid);   // off_tip 4b..4b+3 (quad 3: 12..14, c_obj 0)
 #pragma unroll
             for (int q = 0; q < 4; ++q) {
                 const int n = 4 * b + q;
                 if (n < 15) {
-                    tip[n] = (tip[n] + ringf(ob, n)) + c_dc.tip_uncorr * z[q];
+                    tip[n] = (tip[n] + q4(off4, q)) + c_dc.tip_uncorr * z[q];
                     s_zt += z[q] * z[q];
                 }
             }
@@ -719,8 +550,9 @@ __device__ __forceinline__ void env_step(const DevPtrs& p, uint32_t e, bool vali
     if (on<L>(B_OBS_NOISE)) {
         float z[4];
         normals4_t<kSfuNormals>(philox(g, t, CH_OBJ_NOISE, 0), z);
+        const float co[3] = {q4(ringq(ob, 12, tid), 3), q4(ringq(ob, 16, tid), 0), q4(ringq(ob, 16, tid), 1)};
 #pragma unroll
-        for (int c = 0; c < 3; ++c) obj[c] = (obj[c] + ringf(ob, 15 + c)) + c_dc.obj_uncorr * z[c];
+        for (int c = 0; c < 3; ++c) obj[c] = (obj[c] + co[c]) + c_dc.obj_uncorr * z[c];
     }
 
     // ---- 9. orientation noise -> noisy relative goal [Q15, Q16] ----
@@ -734,7 +566,8 @@ __device__ __forceinline__ void env_step(const DevPtrs& p, uint32_t e, bool vali
         float qn[4];
         if (on<L>(B_OBS_NOISE)) {
             float qu[4], tmp[4];
-            const float qc[4] = {ringf(ob, 18), ringf(ob, 19), ringf(ob, 20), ringf(ob, 21)};
+            const float4 qa4 = ringq(ob, 16, tid), qb4 = ringq(ob, 20, tid);   // q_c = record words 82..85
+            const float qc[4] = {qa4.z, qa4.w, qb4.x, qb4.y};
             rotation<kSfuNormals>(c_dc.rot_uncorr, philox(g, t, CH_ROT_NOISE, 0), qu);
             qmul(qc, qo, tmp);
             qmul(qu, tmp, qn);
@@ -924,155 +757,9 @@ __device__ __forceinline__ void acc_zero(Acc& acc) {
 }
 
 // ============================================================================================
-// Kernel A (PipeThread): per-thread cp.async ring.  Prefetch policy (DR_PREFETCH): 0 = none,
-// 1 = TMA L2 prefetch of the current tile, 2 = of the next tile (A/B experiments).
+// step_kernel_warp: persistent CTAs, the warp-cooperative phase ring, cross-tile pipelining.
 // ============================================================================================
-template <uint32_t L, int PF>
-__global__ void __launch_bounds__(STEP_THREADS, STEP_MIN_CTAS)
-    step_kernel(const DevPtrs p, const float* __restrict__ actions, const float* __restrict__ raw_obs,
-                float* __restrict__ out_actions, float* __restrict__ out_obs, float* __restrict__ out_dt,
-                float* __restrict__ out_force, float* __restrict__ out_sub, uint32_t n_env) {
-    __shared__ __align__(16) float s_act[TILE * N_ACT];   // actions in, out_actions out (in place)
-    __shared__ __align__(16) float s_obs[TILE * OBS_IN];  // raw_obs in, out_obs + out_force out (stride 26)
-    __shared__ __align__(16) float s_dt[TILE * N_SUB];
-    extern __shared__ __align__(128) uint32_t s_ring[];   // [2][RING_W][TILE] (dynamic: > 48 KB total)
-
-    const int tid = threadIdx.x;
-    __shared__ uint32_t s_tstep;
-    const uint32_t t = step_begin(p, &s_tstep);
-    const uint32_t n_tiles = (n_env + TILE - 1) / TILE;
-    constexpr size_t P = PLANE;
-    if (PF == 2) prefetch_tile<L>(p, actions, raw_obs, blockIdx.x, n_env);
-    Acc acc;
-    acc_zero(acc);
-    uint32_t my_envs = 0;
-
-    for (uint32_t tile = blockIdx.x; tile < n_tiles; tile += gridDim.x) {
-        const uint32_t e0 = tile * TILE;
-        const uint32_t cnt = min((uint32_t)TILE, n_env - e0);
-        const bool full = cnt == (uint32_t)TILE;
-        if (PF == 1) prefetch_tile<L>(p, actions, raw_obs, tile, n_env);
-        if (PF == 2) prefetch_tile<L>(p, actions, raw_obs, tile + gridDim.x, n_env);
-        __syncthreads();   // previous tile's smem fully stored
-        // stage the row-major input tiles (LDGSTS, 16 B per copy for full tiles)
-        if (full) {
-            const float* a = actions + (size_t)e0 * N_ACT;
-            const float* o = raw_obs + (size_t)e0 * OBS_IN;
-#pragma unroll
-            for (int i = tid; i < TILE * N_ACT / 4; i += STEP_THREADS) cp_async16(s_act + 4 * i, a + 4 * i);
-#pragma unroll
-            for (int i = tid; i < TILE * OBS_IN / 4; i += STEP_THREADS) cp_async16(s_obs + 4 * i, o + 4 * i);
-        } else {
-            for (uint32_t i = tid; i < cnt * N_ACT; i += STEP_THREADS) cp_async4(s_act + i, actions + (size_t)e0 * N_ACT + i);
-            for (uint32_t i = tid; i < cnt * OBS_IN; i += STEP_THREADS) cp_async4(s_obs + i, raw_obs + (size_t)e0 * OBS_IN + i);
-        }
-        cp_commit();
-        const bool mine = (uint32_t)tid < cnt;
-        const uint32_t* R = p.rec + rec_index(e0 + tid);
-        const uint32_t* S = p.st + st_index(e0 + tid);
-        if (mine) issue_s0<L>(s_ring + tid, R, S, P);                          // S0 -> slot0
-        cp_commit();
-        if (mine) issue_act<L>(s_ring + RING_W * TILE + tid, R, S, P, 0);      // A0 -> slot1
-        cp_commit();
-        cp_wait<1>();      // staging + S0 of this thread
-        __syncthreads();   // everyone's staging copies
-        if (mine) {
-            PipeThread<L> pipe{s_ring + tid, s_ring + RING_W * TILE + tid, R, S};
-            env_step<L>(p, e0 + tid, true, t, tid, s_act, s_obs, s_dt, out_sub, pipe, acc);
-            ++my_envs;
-        }
-        cp_wait<0>();
-        __syncthreads();
-        store_tile(e0, cnt, tid, s_act, s_obs, s_dt, out_actions, out_obs, out_dt, out_force);
-    }
-    reduce_stats<L>(p, acc, my_envs, t, reinterpret_cast<double*>(s_obs));
-}
-
-// ============================================================================================
-// Kernel B (PipeTma, default): CTA-wide TMA ring of TMA_SLOTS phase slots + TMA input tiles.
-// ============================================================================================
-constexpr size_t STEP_TMA_DYN_SMEM = (size_t)TMA_SLOTS * RING_W * TILE * sizeof(uint32_t);
-
 template <uint32_t L>
-__device__ __forceinline__ void tma_issue_io(const float* actions, const float* raw_obs, float* s_act, float* s_obs,
-                                             TmaShared* ts, uint32_t it, uint32_t n_my, uint32_t n_env) {
-    if (it >= n_my) return;
-    const uint32_t tile = blockIdx.x + it * gridDim.x;
-    const uint32_t e0 = tile * TILE;
-    const uint32_t cnt = min((uint32_t)TILE, n_env - e0);
-    const uint32_t ba = cnt * N_ACT * 4u;             // multiple of 16
-    const uint32_t bo = (cnt * OBS_IN * 4u) & ~15u;   // odd tail: the last 8 bytes are loaded by hand
-    mbar_arrive_expect_tx(&ts->io_full, ba + bo);
-    tma_load(s_act, actions + (size_t)e0 * N_ACT, ba, &ts->io_full);
-    tma_load(s_obs, raw_obs + (size_t)e0 * OBS_IN, bo, &ts->io_full);
-}
-
-template <uint32_t L>
-__global__ void __launch_bounds__(STEP_THREADS, STEP_MIN_CTAS)
-    step_kernel_tma(const DevPtrs p, const float* __restrict__ actions, const float* __restrict__ raw_obs,
-                    float* __restrict__ out_actions, float* __restrict__ out_obs, float* __restrict__ out_dt,
-                    float* __restrict__ out_force, float* __restrict__ out_sub, uint32_t n_env) {
-    __shared__ __align__(128) float s_act[TILE * N_ACT];   // TMA destination; out_actions in place
-    __shared__ __align__(128) float s_obs[TILE * OBS_IN];  // TMA destination; out_obs + out_force in place
-    __shared__ __align__(16) float s_dt[TILE * N_SUB];
-    __shared__ TmaShared ts;
-    extern __shared__ __align__(128) uint32_t s_ring[];    // [TMA_SLOTS][RING_W][TILE]
-
-    const int tid = threadIdx.x;
-    __shared__ uint32_t s_tstep;
-    const uint32_t t = step_begin(p, &s_tstep);
-    const uint32_t n_tiles = (n_env + TILE - 1) / TILE;
-    const uint32_t n_my = (blockIdx.x < n_tiles) ? (n_tiles - blockIdx.x + gridDim.x - 1) / gridDim.x : 0u;
-    if (tid == 0) {
-#pragma unroll
-        for (int s = 0; s < TMA_SLOTS; ++s) {
-            mbar_init(&ts.full[s], 1);
-            ts.rel[s] = 0u;
-        }
-        mbar_init(&ts.io_full, 1);
-        ts.io_rel = 0u;
-        fence_mbar_init();
-    }
-    __syncthreads();
-    if (tid == 0) {
-        for (uint32_t ph = 0; ph < (uint32_t)TMA_SLOTS; ++ph) tma_issue_phase<L>(p, s_ring, &ts, ph, n_my, n_tiles);
-        tma_issue_io<L>(actions, raw_obs, s_act, s_obs, &ts, 0, n_my, n_env);
-    }
-    Acc acc;
-    acc_zero(acc);
-    uint32_t my_envs = 0;
-
-    for (uint32_t it = 0; it < n_my; ++it) {
-        const uint32_t tile = blockIdx.x + it * gridDim.x;
-        const uint32_t e0 = tile * TILE;
-        const uint32_t cnt = min((uint32_t)TILE, n_env - e0);
-        const bool mine = (uint32_t)tid < cnt;
-        if ((cnt & 1u) && tid == (int)cnt - 1) {
-            // odd tail tile: the TMA copy was rounded down to 16 B; this env's last 2 words by hand
-            mbar_wait(&ts.io_full, it & 1u);
-            const float2 v = *reinterpret_cast<const float2*>(raw_obs + (size_t)(e0 + cnt) * OBS_IN - 2);
-            *reinterpret_cast<float2*>(s_obs + cnt * OBS_IN - 2) = v;
-        }
-        PipeTma<L> pipe{&p, s_ring, &ts, it * N_PHASES, it, n_my, n_tiles, tid};
-        env_step<L>(p, e0 + tid, mine, t, tid, s_act, s_obs, s_dt, out_sub, pipe, acc);
-        my_envs += mine ? 1u : 0u;
-        __syncthreads();   // all output rows are in shared memory
-        store_tile(e0, cnt, tid, s_act, s_obs, s_dt, out_actions, out_obs, out_dt, out_force);
-        // the last warp done storing issues the next tile's input rows into the same buffers
-        __syncwarp();
-        if ((tid & 31) == 0 && atomicAdd(&ts.io_rel, 1u) == (uint32_t)(STEP_THREADS / 32) - 1u) {
-            ts.io_rel = 0u;
-            fence_proxy_async();
-            tma_issue_io<L>(actions, raw_obs, s_act, s_obs, &ts, it + 1, n_my, n_env);
-        }
-    }
-    reduce_stats<L>(p, acc, my_envs, t, reinterpret_cast<double*>(s_dt));
-}
-
-// ============================================================================================
-// Kernel C (PipeWarp, DR_PIPE=2): warp-cooperative 16-byte cp.async.cg ring.
-// ============================================================================================
-template <uint32_t L, int WPF, bool XT>
 __global__ void __launch_bounds__(STEP_THREADS, STEP_MIN_CTAS)
     step_kernel_warp(const DevPtrs p, const float* __restrict__ actions, const float* __restrict__ raw_obs,
                      float* __restrict__ out_actions, float* __restrict__ out_obs, float* __restrict__ out_dt,
@@ -1094,55 +781,39 @@ __global__ void __launch_bounds__(STEP_THREADS, STEP_MIN_CTAS)
         const uint32_t e0 = tile * TILE;
         const uint32_t cnt = min((uint32_t)TILE, n_env - e0);
         const bool full = cnt == (uint32_t)TILE;
-        // WPF (A/B): TMA L2 prefetch of the next tile's input rows (1) or of everything it reads (2)
-        if (WPF) prefetch_tile<L>(p, actions, raw_obs, tile + gridDim.x, n_env, WPF == 1 ? 2 : 0);
         __syncthreads();   // previous tile's smem fully stored
-        auto stage = [&]() {   // the row-major input tile -> shared memory (16-byte cp.async)
-            if (full) {
-                const float* a = actions + (size_t)e0 * N_ACT;
-                const float* o = raw_obs + (size_t)e0 * OBS_IN;
-#pragma unroll
-                for (int i = tid; i < TILE * N_ACT / 4; i += STEP_THREADS) cp_async16(s_act + 4 * i, a + 4 * i);
-#pragma unroll
-                for (int i = tid; i < TILE * OBS_IN / 4; i += STEP_THREADS) cp_async16(s_obs + 4 * i, o + 4 * i);
-            } else {
-                for (uint32_t i = tid; i < cnt * N_ACT; i += STEP_THREADS)
-                    cp_async4(s_act + i, actions + (size_t)e0 * N_ACT + i);
-                for (uint32_t i = tid; i < cnt * OBS_IN; i += STEP_THREADS)
-                    cp_async4(s_obs + i, raw_obs + (size_t)e0 * OBS_IN + i);
-            }
-            cp_commit();
-        };
         const uint32_t ntile = tile + gridDim.x;
         const uint32_t en = ntile * TILE;
-        PipeWarp<L, XT> pipe{s_ring, s_ring + RING_W * TILE, p.rec + rec_index(e0) + wcol, p.st + st_index(e0) + wcol,
-                             tid, lane, wcol, (XT && ntile < n_tiles) ? p.rec + rec_index(en) + wcol : nullptr,
-                             (XT && ntile < n_tiles) ? p.st + st_index(en) + wcol : nullptr};
-        if (XT) {
-            // S0 / A0 of this tile were issued by the previous tile (on the first tile: here, ahead
-            // of the staging group); the staging group is waited for in io_wait(), after timing
-            if (tile == blockIdx.x) {
-                pipe.issue_s0();
-                cp_commit();
-                pipe.issue_act(pipe.slot1, 0);
-                cp_commit();
-            }
-            stage();
-            cp_wait<1>();   // S0 and A0 landed; the staging group may still fly
-            __syncwarp();
-        } else {
-            stage();
-            pipe.issue_s0();                   // S0 -> slot0 (this warp's columns)
+        PipeWarp<L> pipe{s_ring, s_ring + RING_W * TILE, p.rec + rec_index(e0), p.st + st_index(e0) + wcol,
+                         tid, lane, wcol, ntile < n_tiles ? p.rec + rec_index(en) : nullptr,
+                         ntile < n_tiles ? p.st + st_index(en) + wcol : nullptr};
+        // S0 / A0 of this tile were issued by the previous tile (on the first tile: here, ahead of
+        // the staging group); the staging group is waited for in io_wait(), after timing
+        if (tile == blockIdx.x) {
+            pipe.issue_s0();
             cp_commit();
-            pipe.issue_act(pipe.slot1, 0);     // A0 -> slot1
+            pipe.issue_act(pipe.slot1, 0);
             cp_commit();
-            cp_wait<1>();      // staging + S0
-            __syncthreads();   // everyone's staging copies (and each warp's S0)
         }
+        // the row-major input tile -> shared memory (16-byte cp.async)
+        if (full) {
+            const float* a = actions + (size_t)e0 * N_ACT;
+            const float* o = raw_obs + (size_t)e0 * OBS_IN;
+#pragma unroll
+            for (int i = tid; i < TILE * N_ACT / 4; i += STEP_THREADS) cp_async16(s_act + 4 * i, a + 4 * i);
+#pragma unroll
+            for (int i = tid; i < TILE * OBS_IN / 4; i += STEP_THREADS) cp_async16(s_obs + 4 * i, o + 4 * i);
+        } else {
+            for (uint32_t i = tid; i < cnt * N_ACT; i += STEP_THREADS) cp_async4(s_act + i, actions + (size_t)e0 * N_ACT + i);
+            for (uint32_t i = tid; i < cnt * OBS_IN; i += STEP_THREADS) cp_async4(s_obs + i, raw_obs + (size_t)e0 * OBS_IN + i);
+        }
+        cp_commit();
+        cp_wait<1>();   // S0 and A0 landed; the staging group may still fly
+        __syncwarp();
         const bool mine = (uint32_t)tid < cnt;
         env_step<L>(p, e0 + tid, mine, t, tid, s_act, s_obs, s_dt, out_sub, pipe, acc);
         my_envs += mine ? 1u : 0u;
-        cp_wait<XT ? 1 : 0>();   // XT: the next tile's S0 keeps flying through the store
+        cp_wait<1>();   // the next tile's S0 keeps flying through the store
         __syncthreads();
         store_tile(e0, cnt, tid, s_act, s_obs, s_dt, out_actions, out_obs, out_dt, out_force);
     }

@@ -9,7 +9,8 @@
 //   warp  5    substep timing and the remaining step words (dropout tips, force trigger)
 //   warp  6    fingertips (occlusion, dropout timers, noise, hold-last-reading)
 //   warp  7    object position, orientation -> relative goal, random force
-// Each warp loads its own planes straight from HBM/L2 (coalesced 128-byte lines: one env per lane)
+// Each warp loads its own state planes straight from HBM/L2 (coalesced 128-byte lines: one env per
+// lane) and its record words as 16/32-byte vectors of its env's sector groups (dr_internal.h)
 // and the one cross-warp dependency -- dt_env and the step words of warp 5 -- goes through shared
 // memory behind a single CTA barrier (role_barrier).  The arithmetic of every output is the same expression,
 // in the same order, as env_step's (so the same oracle parity contract holds).
@@ -66,16 +67,21 @@ __global__ void __launch_bounds__(LAT_THREADS, DR_LAT_MIN_CTAS) step_kernel_lat(
         if (wid < 5) {
             // ================= actuators 4b .. 4b+3 [Q1] =================
             const int b = wid;
-            const uint32_t dbits = on<L>(B_DELAY) ? R[REC_DELAY * P] : 0u;
+            const uint32_t dbits = on<L>(B_DELAY) ? R[rec_off(REC_DELAY)] : 0u;
             float prev[4], slack[4], dneg[4], dpos[4], cact[4], ema[4];
+            const float4 z4 = make_float4(0.f, 0.f, 0.f, 0.f);
+            const float4* Rq = reinterpret_cast<const float4*>(R);
+            const float4 dn4 = on<L>(B_BACKLASH) ? Rq[rec_off(rec_dneg(4 * b)) / 4] : z4;   // record group 1 + b
+            const float4 dp4 = on<L>(B_BACKLASH) ? Rq[rec_off(rec_dpos(4 * b)) / 4] : z4;
+            const float4 ca4 = on<L>(B_ACT_NOISE) ? Rq[rec_off(rec_cact(4 * b)) / 4] : z4;
 #pragma unroll
             for (int q = 0; q < 4; ++q) {
                 const int j = 4 * b + q;
                 prev[q] = (on<L>(B_DELAY) && !fresh) ? __uint_as_float(S[(ST_PREV + j) * P]) : 0.f;
                 slack[q] = (on<L>(B_BACKLASH) && !fresh) ? __uint_as_float(S[(ST_SLACK + j) * P]) : 0.f;
-                dneg[q] = on<L>(B_BACKLASH) ? __uint_as_float(R[(REC_DNEG + j) * P]) : 0.f;
-                dpos[q] = on<L>(B_BACKLASH) ? __uint_as_float(R[(REC_DPOS + j) * P]) : 0.f;
-                cact[q] = on<L>(B_ACT_NOISE) ? __uint_as_float(R[(REC_CACT + j) * P]) : 0.f;
+                dneg[q] = q4(dn4, q);
+                dpos[q] = q4(dp4, q);
+                cact[q] = q4(ca4, q);
                 ema[q] = (on<L>(B_SMOOTH) && !fresh) ? __uint_as_float(S[(ST_EMA + j) * P]) : 0.f;
             }
             const float4 a4 = __ldg(reinterpret_cast<const float4*>(actions + (size_t)ec * N_ACT) + b);
@@ -180,7 +186,7 @@ __global__ void __launch_bounds__(LAT_THREADS, DR_LAT_MIN_CTAS) step_kernel_lat(
             acc.m[5] += valid ? s_zu2 : 0.f;
         } else if (wid == 5) {
             // ================= timing + step words [Q2] =================
-            const float il = on<L>(B_TIMING) ? __uint_as_float(R[REC_INVLAM * P]) : 0.f;
+            const float il = on<L>(B_TIMING) ? __uint_as_float(R[rec_off(REC_INVLAM)]) : 0.f;
             float d[N_SUB];
             uint2 w01 = make_uint2(0u, 0u);
             if (on<L>(B_TIMING)) {
@@ -241,11 +247,21 @@ __global__ void __launch_bounds__(LAT_THREADS, DR_LAT_MIN_CTAS) step_kernel_lat(
                     }
                 }
             }
+            if (on<L>(B_OBS_NOISE)) {   // off_tip = record words 64..78 (groups 8, 9)
+                const float4* Rq = reinterpret_cast<const float4*>(R);
 #pragma unroll
-            for (int n = 0; n < 15; ++n) {
-                off[n] = on<L>(B_OBS_NOISE) ? __uint_as_float(R[(REC_OFFTIP + n) * P]) : 0.f;
-                last[n] = (kHold && hold_layers && !fresh) ? __uint_as_float(S[(ST_LAST + n) * P]) : 0.f;
+                for (int h = 0; h < 4; ++h) {
+                    const float4 v = Rq[rec_off(REC_OFFTIP + 4 * h) / 4];
+#pragma unroll
+                    for (int c = 0; c < 4; ++c)
+                        if (4 * h + c < 15) off[4 * h + c] = q4(v, c);
+                }
+            } else {
+#pragma unroll
+                for (int n = 0; n < 15; ++n) off[n] = 0.f;
             }
+#pragma unroll
+            for (int n = 0; n < 15; ++n) last[n] = (kHold && hold_layers && !fresh) ? __uint_as_float(S[(ST_LAST + n) * P]) : 0.f;
             const uint32_t occ_in = (on<L>(B_OCCLUSION) && p.occl_in) ? (uint32_t)__ldg(p.occl_in + ec) : 0u;
             uint32_t occ = 0;
             if (on<L>(B_OCCLUSION) && p.occl_in) {                       // [Q27]
@@ -354,16 +370,18 @@ __global__ void __launch_bounds__(LAT_THREADS, DR_LAT_MIN_CTAS) step_kernel_lat(
             }
             const float2 qa = __ldg(reinterpret_cast<const float2*>(ro + 18)), qb = __ldg(reinterpret_cast<const float2*>(ro + 20));
             const float2 ga = __ldg(reinterpret_cast<const float2*>(ro + 22)), gb = __ldg(reinterpret_cast<const float2*>(ro + 24));
-            float cobj[3], qc[4];
-#pragma unroll
-            for (int c = 0; c < 3; ++c) cobj[c] = on<L>(B_OBS_NOISE) ? __uint_as_float(R[(REC_COBJ + c) * P]) : 0.f;
-#pragma unroll
-            for (int c = 0; c < 4; ++c) qc[c] = on<L>(B_OBS_NOISE) ? __uint_as_float(R[(REC_QC + c) * P]) : 0.f;
+            float cobj[3] = {0.f, 0.f, 0.f}, qc[4] = {0.f, 0.f, 0.f, 0.f};
+            if (on<L>(B_OBS_NOISE)) {   // c_obj, q_c = record words 79..85 (groups 9, 10)
+                const float4* Rq = reinterpret_cast<const float4*>(R);
+                const float4 v0 = Rq[rec_off(76) / 4], v1 = Rq[rec_off(80) / 4], v2 = Rq[rec_off(84) / 4];
+                cobj[0] = v0.w; cobj[1] = v1.x; cobj[2] = v1.y;
+                qc[0] = v1.z; qc[1] = v1.w; qc[2] = v2.x; qc[3] = v2.y;
+            }
             uint32_t tf = 0, kf = 0;
             float mass = 0.f, ft[3] = {0.f, 0.f, 0.f};
             if (on<L>(B_FORCE)) {
-                tf = R[REC_TFORCE * P];
-                mass = __uint_as_float(R[REC_MASS * P]);
+                tf = R[rec_off(REC_TFORCE)];
+                mass = __uint_as_float(R[rec_off(REC_MASS)]);
                 if (!fresh) {
                     kf = S[ST_KF * P];
 #pragma unroll

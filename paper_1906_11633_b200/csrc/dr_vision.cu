@@ -272,199 +272,6 @@ __global__ void __launch_bounds__(IMG_THREADS) image_augment_kernel(const ImgArg
     cluster_wait();   // no CTA leaves while another may still read its s_part
 }
 
-// ---- two-pass augmentation (A/B variant, DR_IMG_MODE=two_pass; the cluster kernel above is the default)
-// Pass 1 (image_moments_kernel): one cluster of P <= 8 CTAs per image; CTA p reduces chunk p of
-// the image to exact integer partials (sum, sum of squares; DP4A on 16-byte loads, four in flight
-// per thread), the cluster's rank 0 gathers the P partials through distributed shared memory in
-// rank order and writes the image's constants (mu_hi, scale, k, s) -- a pure streaming read of the
-// u8 batch that leaves it in L2.
-// Pass 2 (image_noise_kernel): one thread per 4-element Philox block, out = (x - mu_hi) * scale +
-// (s z + k) with float4 streaming stores; each thread loads its image's constants itself (one
-// broadcast 16-byte load, issued before the Philox chain), so there is no shared memory, no
-// barrier and no per-CTA prologue: full occupancy over thousands of equal CTAs, where the cluster
-// kernel ran one image per cluster with its load, reduction and barrier phases serialised.
-// Same per-element expression, draws and per-image constants as the cluster kernel's main loop.
-// Measured (B200, 192 images of 200 x 200 x 3 per step): 45.7-46.6 us vs the cluster kernel's
-// 41.0 us.  ncu: moments 12 us (cold L2), noise 30 us at 69 % issue with 19.8 M warp-instructions
-// (stalls: not_selected, math-pipe throttle) -- the noise is issue-bound either way, and the
-// second pass over the batch costs more than the cluster kernel's serialised phases.
-constexpr int MOM_THREADS = 256, NOISE_THREADS = 256, NOISE_ILP = 2;
-constexpr uint32_t NOISE_BLOCKS_PER_CTA = NOISE_THREADS * NOISE_ILP * 2;   // 1,024 blocks = 4,096 elements
-
-struct MomArgs {
-    const uint8_t* images;
-    float4* par;        // [n_images] (mu_hi, scale, k, s)
-    float* img_stats;
-    uint64_t E;
-    uint32_t chunk;     // bytes per CTA (multiple of 16)
-    uint32_t aligned;
-    uint32_t batch;
-    uint32_t image_offset;
-    double contrast_lo, contrast_range, noise_lo, noise_range;
-    double std_floor;
-    PhiloxKeys keys;
-};
-
-__global__ void __launch_bounds__(MOM_THREADS) image_moments_kernel(const MomArgs a) {
-    __shared__ unsigned long long s_w[2][MOM_THREADS / 32];
-    __shared__ unsigned long long s_part[2];
-    const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
-    const uint32_t P = cluster_size(), r = cluster_rank();
-    const uint64_t img = blockIdx.x / P;
-    const uint64_t lo0 = (uint64_t)r * a.chunk;
-    const uint64_t lo = lo0 < a.E ? lo0 : a.E;
-    const uint64_t hi = (lo + a.chunk) < a.E ? (lo + a.chunk) : a.E;
-    const uint8_t* src = a.images + img * a.E;
-    uint32_t sum = 0, sq = 0;   // <= chunk / MOM_THREADS bytes per thread: no u32 overflow (host caps chunk)
-    if (a.aligned) {
-        const uint4* s16 = reinterpret_cast<const uint4*>(src);
-        const uint64_t i1 = hi / 16;
-        for (uint64_t i = lo / 16 + tid; i < i1; i += 4 * MOM_THREADS) {
-            uint4 v[4];
-#pragma unroll
-            for (int u = 0; u < 4; ++u) {
-                const uint64_t j = i + (uint64_t)u * MOM_THREADS;
-                v[u] = j < i1 ? __ldg(s16 + j) : make_uint4(0u, 0u, 0u, 0u);
-            }
-#pragma unroll
-            for (int u = 0; u < 4; ++u) {
-                sum = __dp4a(v[u].x, 0x01010101u, sum);
-                sq = __dp4a(v[u].x, v[u].x, sq);
-                sum = __dp4a(v[u].y, 0x01010101u, sum);
-                sq = __dp4a(v[u].y, v[u].y, sq);
-                sum = __dp4a(v[u].z, 0x01010101u, sum);
-                sq = __dp4a(v[u].z, v[u].z, sq);
-                sum = __dp4a(v[u].w, 0x01010101u, sum);
-                sq = __dp4a(v[u].w, v[u].w, sq);
-            }
-        }
-    } else {
-        for (uint64_t i = lo + tid; i < hi; i += MOM_THREADS) {
-            const uint32_t x = __ldg(src + i);
-            sum += x;
-            sq += x * x;
-        }
-    }
-    unsigned long long S = sum, Q = sq;
-#pragma unroll
-    for (int o = 16; o > 0; o >>= 1) {
-        S += __shfl_xor_sync(0xFFFFFFFFu, S, o);
-        Q += __shfl_xor_sync(0xFFFFFFFFu, Q, o);
-    }
-    if (lane == 0) {
-        s_w[0][wid] = S;
-        s_w[1][wid] = Q;
-    }
-    __syncthreads();
-    if (tid == 0) {
-        S = 0;
-        Q = 0;
-#pragma unroll
-        for (int k = 0; k < MOM_THREADS / 32; ++k) {
-            S += s_w[0][k];
-            Q += s_w[1][k];
-        }
-        s_part[0] = S;
-        s_part[1] = Q;
-    }
-    cluster_arrive();   // publishes s_part to the cluster
-    cluster_wait();
-    if (r == 0 && tid == 0) {
-        S = 0;
-        Q = 0;
-        for (uint32_t q = 0; q < P; ++q) {   // fixed rank order (integer sums: exact in any order)
-            S += ld_dsmem_u64(smem_addr(&s_part[0]), q);
-            Q += ld_dsmem_u64(smem_addr(&s_part[1]), q);
-        }
-        const uint64_t E = a.E;
-        const uint32_t g = a.image_offset + (uint32_t)img;
-        const double mean = (double)S / (double)E;
-        const unsigned long long vnum = Q * E - S * S;   // E^2 var, exact
-        const double sd = sqrt((double)vnum / ((double)E * (double)E));
-        const uint4 pw = philox_k(g, a.batch, CH_IMG_PARAM, 0, a.keys);
-        const double f = a.contrast_lo + a.contrast_range * (double)uni(pw.x);
-        const double s = a.noise_lo + a.noise_range * (double)uni(pw.y);
-        const float scale = (float)(f / (sd > a.std_floor ? sd : a.std_floor));
-        const float mu_hi = (float)mean, mu_lo = (float)(mean - (double)mu_hi);
-        // k = -mu_lo * scale: see the cluster kernel's epilogue
-        a.par[img] = make_float4(mu_hi, scale, (float)(-(double)mu_lo * (double)scale), (float)s);
-        if (a.img_stats) reinterpret_cast<float4*>(a.img_stats)[img] = make_float4((float)mean, (float)sd, (float)f, (float)s);
-    }
-    cluster_arrive();   // rank 0 is done reading the other CTAs' shared memory
-    cluster_wait();
-}
-
-struct NoiseArgs {
-    const uint8_t* images;
-    float* out;
-    const float4* par;
-    uint64_t E;
-    uint32_t nblk;       // Philox blocks (4 elements each) per image
-    uint32_t aligned;
-    uint32_t batch;
-    uint32_t image_offset;
-    PhiloxKeys keys;
-};
-
-__global__ void __launch_bounds__(NOISE_THREADS) image_noise_kernel(const NoiseArgs a) {
-    const int tid = threadIdx.x;
-    const uint64_t img = blockIdx.x;
-    const uint32_t g = a.image_offset + (uint32_t)img;
-    const float4 pp = __ldg(a.par + img);
-    const float mu_hi = pp.x, scale = pp.y, kq = pp.z, sf = pp.w;
-    const uint32_t b0 = blockIdx.y * NOISE_BLOCKS_PER_CTA;
-    const uint32_t b1 = min(a.nblk, b0 + NOISE_BLOCKS_PER_CTA);
-    if (a.aligned) {
-        const uint32_t* x4 = reinterpret_cast<const uint32_t*>(a.images + img * a.E);
-        float4* o4 = reinterpret_cast<float4*>(a.out + img * a.E);
-        uint32_t b = b0 + tid;
-        for (; b + (NOISE_ILP - 1) * NOISE_THREADS < b1; b += NOISE_ILP * NOISE_THREADS) {
-            uint4 w[NOISE_ILP];
-            uint32_t x[NOISE_ILP];
-#pragma unroll
-            for (int u = 0; u < NOISE_ILP; ++u) {
-                x[u] = __ldg(x4 + b + u * NOISE_THREADS);
-                w[u] = philox_k(g, a.batch, CH_IMG_NOISE, b + u * NOISE_THREADS, a.keys);
-            }
-#pragma unroll
-            for (int u = 0; u < NOISE_ILP; ++u) {
-                float z[4];
-                img_bm_scaled(w[u].x, w[u].y, sf, z[0], z[1]);   // z = s * normal
-                img_bm_scaled(w[u].z, w[u].w, sf, z[2], z[3]);
-                float v[4];
-#pragma unroll
-                for (int k = 0; k < 4; ++k) v[k] = fmaf((float)((x[u] >> (8 * k)) & 0xFFu) - mu_hi, scale, z[k] + kq);
-                __stcs(o4 + b + u * NOISE_THREADS, make_float4(v[0], v[1], v[2], v[3]));
-            }
-        }
-        for (; b < b1; b += NOISE_THREADS) {
-            const uint32_t xx = __ldg(x4 + b);
-            const uint4 w = philox_k(g, a.batch, CH_IMG_NOISE, b, a.keys);
-            float z[4];
-            img_bm_scaled(w.x, w.y, sf, z[0], z[1]);
-            img_bm_scaled(w.z, w.w, sf, z[2], z[3]);
-            float v[4];
-#pragma unroll
-            for (int k = 0; k < 4; ++k) v[k] = fmaf((float)((xx >> (8 * k)) & 0xFFu) - mu_hi, scale, z[k] + kq);
-            __stcs(o4 + b, make_float4(v[0], v[1], v[2], v[3]));
-        }
-    } else {
-        const uint8_t* src = a.images + img * a.E;
-        float* out = a.out + img * a.E;
-        for (uint32_t b = b0 + tid; b < b1; b += NOISE_THREADS) {
-            const uint4 w = philox_k(g, a.batch, CH_IMG_NOISE, b, a.keys);
-            float z[4];
-            img_bm_scaled(w.x, w.y, sf, z[0], z[1]);
-            img_bm_scaled(w.z, w.w, sf, z[2], z[3]);
-#pragma unroll
-            for (int k = 0; k < 4; ++k) {
-                const uint64_t e = 4ull * b + k;
-                if (e < a.E) out[e] = fmaf((float)__ldg(src + e) - mu_hi, scale, z[k] + kq);
-            }
-        }
-    }
-}
-
 // ---- appearance draws: one thread per sample, fp64 (no contraction in the decision chain) ----
 struct SceneArgs {
     dr_vision_params p;
@@ -800,70 +607,6 @@ uint32_t img_cluster_size(uint64_t E, uint64_t n) {
     return best;
 }
 
-// The two-pass augmentation (image_moments_kernel, image_noise_kernel).  The per-image constants
-// (16 B per image) live in a stream-ordered scratch (cudaMallocAsync / cudaFreeAsync from the
-// device's default pool), so concurrent calls on different streams never share it.
-int image_augment_two_pass(const dr_vision_params* p, uint64_t seed, uint64_t batch_index, int64_t image_offset,
-                           const uint8_t* images, int64_t n_images, uint64_t E, float* out, float* img_stats,
-                           cudaStream_t st) {
-    constexpr uint64_t MOM_CHUNK_TARGET = 16384;   // bytes per moments CTA (64 per thread), P <= 8
-    const uint32_t aligned = (E % 16 == 0 && ((uintptr_t)images & 15u) == 0 && ((uintptr_t)out & 15u) == 0) ? 1u : 0u;
-    uint32_t P = (uint32_t)((E + MOM_CHUNK_TARGET - 1) / MOM_CHUNK_TARGET);
-    if (P > 8) P = 8;
-    const uint32_t chunk = (uint32_t)(((E + P - 1) / P + 15) / 16 * 16);   // <= 200 KB: <= 800 B per thread
-    const uint64_t nblk = (E + 3) / 4;
-    const uint64_t Q = (nblk + NOISE_BLOCKS_PER_CTA - 1) / NOISE_BLOCKS_PER_CTA;
-    if (n_images * (int64_t)P > 0x7FFFFFFF || Q > 65535) return set_error(DR_EUNSUPPORTED, "image batch too large for one launch");
-    float4* par = nullptr;
-    cudaError_t e = cudaMallocAsync(reinterpret_cast<void**>(&par), (size_t)n_images * sizeof(float4), st);
-    if (e != cudaSuccess) return set_error(DR_ECUDA, "cudaMallocAsync: %s", cudaGetErrorString(e));
-    MomArgs m{};
-    m.images = images;
-    m.par = par;
-    m.img_stats = img_stats;
-    m.E = E;
-    m.chunk = chunk;
-    m.aligned = aligned;
-    m.batch = (uint32_t)batch_index;
-    m.image_offset = (uint32_t)image_offset;
-    m.contrast_lo = p->contrast_lo;
-    m.contrast_range = p->contrast_hi - p->contrast_lo;
-    m.noise_lo = p->noise_std_lo;
-    m.noise_range = p->noise_std_hi - p->noise_std_lo;
-    m.std_floor = p->std_floor;
-    m.keys = make_keys(seed);
-    cudaLaunchConfig_t cfg{};
-    cfg.gridDim = dim3((unsigned)(n_images * P), 1, 1);
-    cfg.blockDim = dim3(MOM_THREADS, 1, 1);
-    cfg.stream = st;
-    cudaLaunchAttribute attr[1];
-    attr[0].id = cudaLaunchAttributeClusterDimension;
-    attr[0].val.clusterDim.x = P;
-    attr[0].val.clusterDim.y = 1;
-    attr[0].val.clusterDim.z = 1;
-    cfg.attrs = attr;
-    cfg.numAttrs = 1;
-    e = cudaLaunchKernelEx(&cfg, image_moments_kernel, m);
-    if (e != cudaSuccess) return set_error(DR_ECUDA, "image_moments_kernel: %s", cudaGetErrorString(e));
-    count_launch();
-    NoiseArgs a{};
-    a.images = images;
-    a.out = out;
-    a.par = par;
-    a.E = E;
-    a.nblk = (uint32_t)nblk;
-    a.aligned = aligned;
-    a.batch = (uint32_t)batch_index;
-    a.image_offset = (uint32_t)image_offset;
-    a.keys = m.keys;
-    image_noise_kernel<<<dim3((unsigned)n_images, (unsigned)Q), NOISE_THREADS, 0, st>>>(a);
-    e = cudaGetLastError();
-    if (e != cudaSuccess) return set_error(DR_ECUDA, "image_noise_kernel: %s", cudaGetErrorString(e));
-    count_launch();
-    e = cudaFreeAsync(par, st);
-    if (e != cudaSuccess) return set_error(DR_ECUDA, "cudaFreeAsync: %s", cudaGetErrorString(e));
-    return DR_OK;
-}
 }  // namespace
 
 extern "C" {
@@ -883,10 +626,6 @@ int dr_image_augment(const dr_vision_params* p, uint64_t seed, uint64_t batch_in
     if (!images || !out) return set_error(DR_EINVAL, "images/out: NULL");
     if (img_stats && ((uintptr_t)img_stats & 15u)) return set_error(DR_EINVAL, "img_stats: not 16-byte aligned");
     if (n_images * (int64_t)2 > (int64_t)0x7FFFFFFF / 8) return set_error(DR_EINVAL, "n_images: too many for one launch");
-    const char* mode = std::getenv("DR_IMG_MODE");   // A/B: "two_pass" = moments kernel + noise kernel
-    if (mode && std::strcmp(mode, "two_pass") == 0)
-        return image_augment_two_pass(p, seed, batch_index, image_offset, images, n_images, E, out, img_stats,
-                                      static_cast<cudaStream_t>(stream));
     if (!g_img_attr_set) {   // once per process (the attribute is per function, not per launch)
         const cudaError_t ea = cudaFuncSetAttribute(image_augment_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                                     (int)IMG_SLICE_MAX);

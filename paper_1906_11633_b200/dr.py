@@ -112,6 +112,7 @@ def load():
     L.dr_stats.restype = C.c_void_p
     L.dr_set_stats_buffer.argtypes = [vp]
     L.dr_step_index.restype = C.c_uint64
+    L.dr_step_index_sync.restype = C.c_uint64
     L.dr_set_step_index.argtypes = [C.c_uint64]
     L.dr_state_bytes.restype = C.c_size_t
     L.dr_state_export.argtypes = [vp, C.c_int64, C.c_int64]
@@ -287,6 +288,10 @@ def dr_set_stats_buffer(buf=None):
 
 def dr_step_index() -> int:
     return load().dr_step_index()
+
+
+def dr_step_index_sync() -> int:
+    return load().dr_step_index_sync()
 
 
 def dr_set_step_index(t: int):

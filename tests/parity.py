@@ -52,13 +52,14 @@ def compare_obs(g_obs, o_obs, t=None):
 class KnifeTracker:
     """Per-(env, actuator) excusal of backlash rail knife-edges."""
 
-    def __init__(self, n):
+    def __init__(self, n, tau=None):
+        self.tau = KNIFE_TAU if tau is None else tau
         self.excused = np.zeros((n, 20), dtype=bool)
         self.events = 0
         self.excused_mismatches = 0
 
     def update_before_compare(self, margin):
-        k = margin < KNIFE_TAU
+        k = margin < self.tau
         self.events += int(k.sum())
         self.excused |= k
 
@@ -135,15 +136,46 @@ STAT_INT = list(range(0, 12))
 STAT_MOM = list(range(16, 24))
 
 
-def compare_stats(g, o, n_envs, knife_events=0):
+def compare_stats(g, o, n_envs, knife_events=0, t=None):
     """Integer slots exact; fp64 moment slots to 1e-6 of a magnitude bound (they sum fp32 vs fp64
     per-env values).  Backlash-gate counts may differ by the knife-edge count."""
     for s in STAT_INT:
         if s in (7, 8, 9) and knife_events:
-            assert abs(g[s] - o[s]) <= 2 * knife_events, (s, g[s], o[s])
+            assert abs(g[s] - o[s]) <= 2 * knife_events, (t, s, g[s], o[s])
         else:
-            assert g[s] == o[s], (s, g[s], o[s])
+            assert g[s] == o[s], (t, s, g[s], o[s])
     scale = {16: 0.09 * n_envs, 17: 0.01 * n_envs, 18: 2.0 * 20 * n_envs, 19: 20 * n_envs,
              20: 20 * n_envs, 21: 20 * n_envs, 22: 15 * n_envs, 23: 10 * n_envs}
     for s in STAT_MOM:
-        assert abs(g[s] - o[s]) <= 1e-6 * max(abs(o[s]), scale[s]) * (1 + knife_events), (s, g[s], o[s])
+        assert abs(g[s] - o[s]) <= 1e-6 * max(abs(o[s]), scale[s]) * (1 + knife_events), (t, s, g[s], o[s])
+
+
+# ---- state transfer between the two sides (test infrastructure: marshalling, no method arithmetic) ----
+GPU_TO_ORACLE_FIELDS = ("episode", "delay_bits", "p_index", "t_force", "k_f", "lambda", "mass", "dneg", "dpos",
+                        "c_act", "off_tip", "c_obj", "q_c", "prev", "slack", "last", "f_trig", "ema")
+
+
+def oracle_env_from_gpu(G: dict, i: int, orc) -> dict:
+    """The oracle env dict of GPU-exported env i (dr_env_state, fp32 -> fp64 exactly): record and
+    state fields copied, the flags word split into the dropout timers and has_last, and the episode's
+    force probability looked up from its p-index in the oracle's own table."""
+    d = {k: np.asarray(G[k][i]).astype(np.float64) if np.asarray(G[k][i]).dtype.kind == "f" else G[k][i]
+         for k in GPU_TO_ORACLE_FIELDS}
+    flags = int(G["flags"][i])
+    d["timer"] = np.array([(flags >> (4 * t)) & 15 for t in range(5)], dtype=np.int64)
+    d["has_last"] = (flags >> 20) & 1
+    d["p_force"] = orc.force_p(int(G["p_index"][i]))
+    return d
+
+
+def state_array_from_numpy(states, G: dict):
+    """Write the dict-of-arrays G (states_to_numpy shape) back into a ctypes dr_env_state array."""
+    raw = np.frombuffer(states, dtype=np.uint32).reshape(len(states), -1)
+    off = 0
+    for name, ty in type(states[0])._fields_:
+        key = "lambda" if name == "lambda_" else name
+        n = ty._length_ if hasattr(ty, "_length_") else 1
+        col = np.asarray(G[key]).reshape(len(states), n)
+        raw[:, off:off + n] = col.view(np.uint32) if col.dtype == np.float32 else col.astype(np.uint32)
+        off += n
+    return states

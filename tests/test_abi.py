@@ -78,6 +78,7 @@ def test_state_struct_is_168_words():
     ("abi_version", 99, "abi_version"),
     ("struct_size", 8, "struct_size"),
     ("layer_mask", 0x400, "layer_mask"),
+    ("backlash_eps", 1e-3, "backlash_eps"),   # the kernels' gate identity needs eps < 2^-24
 ])
 def test_validation_errors_name_the_field(lib, field, value, needle):
     from paper_1906_11633_b200 import dr

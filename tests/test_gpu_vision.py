@@ -20,17 +20,6 @@ def torch_cuda():
     return torch
 
 
-@pytest.fixture(params=["cluster", "two_pass"])
-def img_mode(request, monkeypatch):
-    """Both augmentation paths of dr_image_augment: the one-pass cluster kernel (default) and the
-    two-pass A/B variant (moments kernel + noise kernel, DR_IMG_MODE=two_pass)."""
-    if request.param == "two_pass":
-        monkeypatch.setenv("DR_IMG_MODE", "two_pass")
-    else:
-        monkeypatch.delenv("DR_IMG_MODE", raising=False)
-    return request.param
-
-
 def _rel(g, o, floor):
     return np.abs(np.asarray(g, np.float64) - o) / np.maximum(np.abs(o), floor)
 
@@ -58,14 +47,14 @@ def _check_augment(torch, P, imgs, batch=0, image_offset=0):
 
 @pytest.mark.parametrize("shape", [(1, 1, 1, 1), (3, 17, 13, 3), (5, 7, 5, 1), (4, 32, 32, 3), (2, 64, 48, 4),
                                    (2, 200, 200, 3), (3, 100, 130, 3)])
-def test_image_augment_small_shapes(torch_cuda, img_mode, shape):
+def test_image_augment_small_shapes(torch_cuda, shape):
     """Element-by-element parity at ragged shapes (unaligned byte path), cluster sizes 1-4 and the
     paper's 200 x 200 x 3 image."""
     imgs = gen.images(*shape, seed=sum(shape))
     _check_augment(torch_cuda, presets.vision_preset(), imgs, batch=3)
 
 
-def test_image_augment_degenerate_and_pinned(torch_cuda, img_mode):
+def test_image_augment_degenerate_and_pinned(torch_cuda):
     """Constant images (std floored: noise only), a two-level image, contrast / noise pinned."""
     imgs = np.zeros((4, 16, 16, 3), np.uint8)
     imgs[1] = 255
@@ -77,13 +66,13 @@ def test_image_augment_degenerate_and_pinned(torch_cuda, img_mode):
     _check_augment(torch_cuda, presets.vision_preset(noise_std_lo=0.0, noise_std_hi=0.3), imgs, batch=2)
 
 
-def test_image_augment_large_image_cluster8(torch_cuda, img_mode):
+def test_image_augment_large_image_cluster8(torch_cuda):
     """640 x 480 x 3 (921,600 bytes): a cluster of 8 CTAs with 115 KB slices each."""
     imgs = gen.images(1, 480, 640, 3, seed=5)
     _check_augment(torch_cuda, presets.vision_preset(), imgs, batch=0)
 
 
-def test_image_augment_paper_batch_sampled(torch_cuda, img_mode):
+def test_image_augment_paper_batch_sampled(torch_cuda):
     """The paper's batch: 64 samples x 3 cameras = 192 images of 200 x 200 x 3 in one
     call; 8 sampled images compared element by element with the oracle (image_offset selects the
     global id), and every image has mean ~0 and std ~sqrt(f^2 + s^2)."""
@@ -102,7 +91,7 @@ def test_image_augment_paper_batch_sampled(torch_cuda, img_mode):
     assert np.abs(s - np.sqrt(gs[:, 2] ** 2 + gs[:, 3] ** 2)).max() < 5e-3
 
 
-def test_image_augment_partition_invariance(torch_cuda, img_mode):
+def test_image_augment_partition_invariance(torch_cuda):
     """One call over 6 images equals two calls over [0, 2) and [2, 6) with image_offset 2, bitwise."""
     imgs = gen.images(6, 40, 40, 3, seed=3)
     P = presets.vision_preset()

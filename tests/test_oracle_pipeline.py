@@ -478,6 +478,96 @@ def test_reproducibility_and_partition_invariance():
     assert not np.array_equal(other.step(acts[0], obs[0])["out_obs"], Oracle(P, n, SEED).step(acts[0], obs[0])["out_obs"])
 
 
+def test_openmp_build_is_bit_identical():
+    """The all-core oracle (-fopenmp build of the same source, the bench's all-core CPU baseline) gives
+    the single-thread oracle's results bit for bit: envs are independent and the step's stats are
+    summed in env order after the parallel loop."""
+    from oracle.oracle import Oracle
+    n, T = 257, 6
+    acts, obs = gen.frames(n, T, seed=9)
+    P = presets.preset(FULL | presets.SMOOTH)
+    one, omp = Oracle(P, n, SEED), Oracle(P, n, SEED, omp=True)
+    for t in range(T):
+        if t == 3:
+            m = (np.arange(n) % 3 == 1).astype(np.uint8)
+            one.reset(m)
+            omp.reset(m)
+        a = one.step(acts[t], obs[t], want_margin=True)
+        b = omp.step(acts[t], obs[t], want_margin=True)
+        for k in a:
+            assert np.array_equal(a[k], b[k]), (t, k)
+    for i in (0, 100, 256):
+        ea, eb = one.env(i), omp.env(i)
+        for k in ea:
+            assert np.array_equal(ea[k], eb[k]), (i, k)
+
+
+def test_state_import_resume_equals_uninterrupted():
+    """State import (orc_set_env) pinned by the reproducibility principle (seeded
+    deterministic randomization; SPEC.md:499 bit-exact resume): a second oracle that imports every env's
+    state and the step index after 7 steps (one reset in between) continues exactly like the
+    uninterrupted run, resets included -- so the env state holds everything the future depends on."""
+    from oracle.oracle import Oracle
+    n, T = 9, 14
+    acts, obs = gen.frames(n, T, seed=5)
+    P = presets.preset(FULL | presets.SMOOTH)
+    a = Oracle(P, n, SEED)
+    b = Oracle(P, n, SEED)
+    for t in range(T):
+        if t in (3, 10):
+            m = (np.arange(n) % 2 == t % 2).astype(np.uint8)
+            a.reset(m)
+            if t > 7:
+                b.reset(m)
+        if t == 7:
+            for i in range(n):
+                b.set_env(i, a.env(i))
+            b.step_index = a.step_index
+        ra = a.step(acts[t], obs[t])
+        if t >= 7:
+            rb = b.step(acts[t], obs[t])
+            for k in ra:
+                assert np.array_equal(ra[k], rb[k]), (t, k)
+    for i in range(n):
+        ea, eb = a.env(i), b.env(i)
+        for k in ea:
+            assert np.array_equal(ea[k], eb[k]), (i, k)
+
+
+def test_state_import_backlash_golden_rows_through_step():
+    """The golden backlash rows (PAPER.md:102-109 hand evaluations, tests/golden/backlash_hand.txt)
+    through the whole step from an imported state: with BACKLASH the only layer the action reaches
+    the gate unchanged and dt_env = 10 dt_base, so the step's out_actions and slack are the row's
+    values (to the fp32 rounding of the inputs and the fp64 sum of the ten substeps)."""
+    from oracle.oracle import Oracle
+    rows = []
+    with open(os.path.join(GOLDEN, "backlash_hand.txt")) as f:
+        for line in f:
+            if line.strip() and not line.startswith("#"):
+                lhs, rhs, tol, note = [x.strip() for x in line.split("|", 3)]
+                rows.append(([float(x) for x in lhs.split()], [float(x) for x in rhs.split()], float(tol), note))
+    for dt in sorted({r[0][4] for r in rows}):
+        sel = [r for r in rows if r[0][4] == dt]
+        n = len(sel)
+        orc = Oracle(presets.preset(BACKLASH, dt_base=dt / 10), n, SEED)
+        acts = np.zeros((n, 20), np.float32)
+        for i, ((s, a, dn, dp, _), _, _, _) in enumerate(sel):
+            e = orc.env(i)
+            e["slack"][0], e["dneg"][0], e["dpos"][0] = s, dn, dp
+            orc.set_env(i, e)
+            acts[i, 0] = a
+        obs = np.zeros((n, 26), np.float32)
+        obs[:, 18] = obs[:, 22] = 1.0
+        r = orc.step(acts, obs)
+        for i, ((s, a, dn, dp, _), (s_new, alpha, out), tol, note) in enumerate(sel):
+            got_out, got_s = r["out_actions"][i, 0], orc.env(i)["slack"][0]
+            a32 = float(np.float32(a))
+            assert abs(got_s - s_new) <= 1e-9 + 1e-7 * abs(s_new), (note, got_s, s_new)
+            assert abs(got_out - out) <= max(tol, 1e-7 * abs(out)) + 1e-7 * abs(a32 - a), (note, got_out, out)
+            if out == 0.0 and tol == 0.0:   # exact zero rows: the sign of zero is alpha * a's [Q3]
+                assert got_out == 0.0 and math.copysign(1.0, got_out) == math.copysign(1.0, out), note
+
+
 def test_reset_mask_semantics():
     n = 10
     acts, obs = gen.frames(n, 3, seed=8)
