@@ -1,8 +1,8 @@
 // dr_internal.h -- shared between the host library (dr_api.cu) and the kernels (dr_kernels.cu).
 // Device data layout:
 //   rec  : episode record, [n_tiles][REC_GROUPS][TILE][8] 4-byte words: record word w of env e is
-//          word w % 8 of the 32-byte group w / 8 of that env, so the eight words of a group are one
-//          DRAM sector of ONE env.  A reset rewrites whole sectors (no L2 read-fill of partially
+//          word w % 8 of the 32-byte group w / 8 of that env (halves swapped when bit 2 of e is set,
+//          rec_off), so the eight words of a group are one DRAM sector of ONE env.  A reset rewrites whole sectors (no L2 read-fill of partially
 //          written sectors), and the step reads a group of its 32 consecutive envs as 1 KB of
 //          contiguous memory (16-byte cp.async per half group, coalesced).
 //   st   : mutable per-env state, [n_tiles][ST_PLANES][TILE] (plane k of env e at k * TILE + e % TILE:
@@ -45,8 +45,15 @@ enum : int {
 __host__ __device__ constexpr int rec_dneg(int j) { return 8 + 8 * (j >> 2) + (j & 3); }
 __host__ __device__ constexpr int rec_dpos(int j) { return 12 + 8 * (j >> 2) + (j & 3); }
 __host__ __device__ constexpr int rec_cact(int j) { return j < 4 ? 4 + j : 44 + j; }
-// word offset of record word w from an env's base (rec_index): group w / 8, word w % 8
-__host__ __device__ constexpr size_t rec_off(int w) { return (size_t)(w >> 3) * (TILE * 8) + (w & 7); }
+// Word offset of record word w of env e from the env's base (rec_index): group w / 8, word w % 8 --
+// with the two 16-byte halves of every group swapped for envs with bit 2 of e set.  The step kernel
+// copies groups into shared memory sector by sector (a sector must land contiguously) and thread e
+// reads its half h at chunk h ^ swz: within a quarter-warp, envs 0-3 and 4-7 of each 8 then hit
+// different 16-byte bank groups (an LDS.128 of the same logical half is conflict-free).
+__host__ __device__ constexpr uint32_t rec_swz(uint32_t e) { return ((e >> 2) & 1u) << 2; }
+__host__ __device__ constexpr size_t rec_off(uint32_t e, int w) {
+    return (size_t)(w >> 3) * (TILE * 8) + ((uint32_t)(w & 7) ^ rec_swz(e));
+}
 // ---- state planes (read + written by the step kernel) ----
 enum : int {
     ST_PREV = 0,     // 20

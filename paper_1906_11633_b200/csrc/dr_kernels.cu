@@ -53,20 +53,20 @@ __global__ void export_kernel(DevPtrs p, uint32_t* __restrict__ dst, uint32_t lo
     uint32_t* o = dst + (size_t)(e - lo) * EXP_WORDS;
     const uint32_t flags = S[ST_FLAGS * P];
     const bool fresh = flags & FRESH_BIT;
-    o[0] = R[rec_off(REC_EPISODE)];
-    o[1] = R[rec_off(REC_DELAY)];
-    o[2] = R[rec_off(REC_PINDEX)];
-    o[3] = R[rec_off(REC_TFORCE)];
+    o[0] = R[rec_off(e, REC_EPISODE)];
+    o[1] = R[rec_off(e, REC_DELAY)];
+    o[2] = R[rec_off(e, REC_PINDEX)];
+    o[3] = R[rec_off(e, REC_TFORCE)];
     o[4] = fresh ? 0u : flags;
     o[5] = fresh ? 0u : S[ST_KF * P];
-    o[6] = R[rec_off(REC_LAMBDA)];
-    o[7] = R[rec_off(REC_MASS)];
+    o[6] = R[rec_off(e, REC_LAMBDA)];
+    o[7] = R[rec_off(e, REC_MASS)];
     for (int j = 0; j < N_ACT; ++j) {
-        o[8 + j] = R[rec_off(rec_dneg(j))];
-        o[28 + j] = R[rec_off(rec_dpos(j))];
-        o[48 + j] = R[rec_off(rec_cact(j))];
+        o[8 + j] = R[rec_off(e, rec_dneg(j))];
+        o[28 + j] = R[rec_off(e, rec_dpos(j))];
+        o[48 + j] = R[rec_off(e, rec_cact(j))];
     }
-    for (int i = 0; i < 22; ++i) o[68 + i] = R[rec_off(REC_OFFTIP + i)];                        // off_tip, c_obj, q_c
+    for (int i = 0; i < 22; ++i) o[68 + i] = R[rec_off(e, REC_OFFTIP + i)];                        // off_tip, c_obj, q_c
     for (int i = 0; i < ST_FLAGS; ++i) o[90 + i] = fresh ? 0u : S[i * P];                     // prev, slack, last
     for (int i = 0; i < 3; ++i) o[145 + i] = fresh ? 0u : S[(ST_FTRIG + i) * P];
     for (int i = 0; i < N_ACT; ++i) o[148 + i] = fresh ? 0u : S[(ST_EMA + i) * P];
@@ -79,22 +79,22 @@ __global__ void import_kernel(DevPtrs p, const uint32_t* __restrict__ src, uint3
     uint32_t* R = p.rec + rec_index(e);
     uint32_t* S = p.st + st_index(e);
     const uint32_t* o = src + (size_t)(e - lo) * EXP_WORDS;
-    R[rec_off(REC_EPISODE)] = o[0];
-    R[rec_off(REC_DELAY)] = o[1];
-    R[rec_off(REC_PINDEX)] = o[2];
-    R[rec_off(REC_TFORCE)] = o[3];
+    R[rec_off(e, REC_EPISODE)] = o[0];
+    R[rec_off(e, REC_DELAY)] = o[1];
+    R[rec_off(e, REC_PINDEX)] = o[2];
+    R[rec_off(e, REC_TFORCE)] = o[3];
     S[ST_FLAGS * P] = o[4] & ~FRESH_BIT;
     S[ST_KF * P] = o[5];
-    R[rec_off(REC_LAMBDA)] = o[6];
+    R[rec_off(e, REC_LAMBDA)] = o[6];
     const float lam = __uint_as_float(o[6]);
-    R[rec_off(REC_INVLAM)] = __float_as_uint(lam > 0.f ? 1.0f / lam : 0.f);
-    R[rec_off(REC_MASS)] = o[7];
+    R[rec_off(e, REC_INVLAM)] = __float_as_uint(lam > 0.f ? 1.0f / lam : 0.f);
+    R[rec_off(e, REC_MASS)] = o[7];
     for (int j = 0; j < N_ACT; ++j) {
-        R[rec_off(rec_dneg(j))] = o[8 + j];
-        R[rec_off(rec_dpos(j))] = o[28 + j];
-        R[rec_off(rec_cact(j))] = o[48 + j];
+        R[rec_off(e, rec_dneg(j))] = o[8 + j];
+        R[rec_off(e, rec_dpos(j))] = o[28 + j];
+        R[rec_off(e, rec_cact(j))] = o[48 + j];
     }
-    for (int i = 0; i < 22; ++i) R[rec_off(REC_OFFTIP + i)] = o[68 + i];
+    for (int i = 0; i < 22; ++i) R[rec_off(e, REC_OFFTIP + i)] = o[68 + i];
     for (int i = 0; i < ST_FLAGS; ++i) S[i * P] = o[90 + i];
     for (int i = 0; i < 3; ++i) S[(ST_FTRIG + i) * P] = o[145 + i];
     for (int i = 0; i < N_ACT; ++i) S[(ST_EMA + i) * P] = o[148 + i];
@@ -118,7 +118,7 @@ __global__ void __launch_bounds__(IMPORT_PHYS_THREADS) import_phys_kernel(DevPtr
     const int nnb = phys_on ? (c_dc.n_phys_n + 3) / 4 : 0;
     const uint32_t e = lo + blockIdx.x * (IMPORT_PHYS_THREADS / 32) + wid;
     if (e >= hi) return;
-    reset_phys_warp(p, e, p.rec[rec_index(e) + rec_off(REC_EPISODE)], lane, s_dr[wid], s_pd, s_src, nub, nnb);
+    reset_phys_warp(p, e, p.rec[rec_index(e) + rec_off(e, REC_EPISODE)], lane, s_dr[wid], s_pd, s_src, nub, nnb);
 }
 
 __global__ void debug_philox_kernel(uint32_t n_env, uint32_t dom, uint32_t ch, uint32_t blk, uint4* __restrict__ out) {

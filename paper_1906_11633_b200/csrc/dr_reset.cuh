@@ -43,13 +43,20 @@ __device__ __forceinline__ uint32_t selw(const uint4 w, uint32_t r) {
     return r == 0u ? w.x : (r == 1u ? w.y : (r == 2u ? w.z : w.w));
 }
 
-// One record group (8 words = one DRAM sector of one env) in one 256-bit store.
-__device__ __forceinline__ void st_group(uint32_t* R, int grp, uint32_t a0, uint32_t a1, uint32_t a2, uint32_t a3,
-                                         uint32_t a4, uint32_t a5, uint32_t a6, uint32_t a7) {
+// One record group (8 words = one DRAM sector of one env) in one 256-bit store, its halves swapped
+// for the envs rec_swz says.
+__device__ __forceinline__ void st_group(uint32_t* R, uint32_t e, int grp, uint32_t a0, uint32_t a1, uint32_t a2,
+                                         uint32_t a3, uint32_t a4, uint32_t a5, uint32_t a6, uint32_t a7) {
     uint32_t* q = R + (size_t)grp * (TILE * 8);
-    asm volatile("st.global.v8.b32 [%0], {%1, %2, %3, %4, %5, %6, %7, %8};" ::"l"(q), "r"(a0), "r"(a1), "r"(a2),
-                 "r"(a3), "r"(a4), "r"(a5), "r"(a6), "r"(a7)
-                 : "memory");
+    if (rec_swz(e)) {
+        asm volatile("st.global.v8.b32 [%0], {%1, %2, %3, %4, %5, %6, %7, %8};" ::"l"(q), "r"(a4), "r"(a5), "r"(a6),
+                     "r"(a7), "r"(a0), "r"(a1), "r"(a2), "r"(a3)
+                     : "memory");
+    } else {
+        asm volatile("st.global.v8.b32 [%0], {%1, %2, %3, %4, %5, %6, %7, %8};" ::"l"(q), "r"(a0), "r"(a1), "r"(a2),
+                     "r"(a3), "r"(a4), "r"(a5), "r"(a6), "r"(a7)
+                     : "memory");
+    }
 }
 __device__ __forceinline__ uint32_t fu(float x) { return __float_as_uint(x); }
 
@@ -114,7 +121,7 @@ __device__ void reset_record_thread(const DevPtrs& p, uint32_t e, uint32_t k, co
     {
         float z[4];
         reset_normals4(lm & B_ACT_NOISE, g, k, CH_CORR_ACT, 0, z);
-        st_group(R, 0, bits, fu(il), tf, fu(mass), fu(sc * z[0]), fu(sc * z[1]), fu(sc * z[2]), fu(sc * z[3]));
+        st_group(R, e, 0, bits, fu(il), tf, fu(mass), fu(sc * z[0]), fu(sc * z[1]), fu(sc * z[2]), fu(sc * z[3]));
     }
     // ---- groups 1..5: backlash widths of actuators 4b..4b+3 [Q7]:
     //      normal j -> delta-1_j (block j / 4), normal 20 + j -> delta+1_j (block 5 + j / 4) ----
@@ -129,7 +136,7 @@ __device__ void reset_record_thread(const DevPtrs& p, uint32_t e, uint32_t k, co
             dn[q] = (lm & B_BACKLASH) ? fmaxf(0.f, c_dc.dcal_neg[j] + c_dc.jitter * zn[q]) : 0.f;
             dp[q] = (lm & B_BACKLASH) ? fmaxf(0.f, c_dc.dcal_pos[j] + c_dc.jitter * zp[q]) : 0.f;
         }
-        st_group(R, REC_G_BL + b, fu(dn[0]), fu(dn[1]), fu(dn[2]), fu(dn[3]), fu(dp[0]), fu(dp[1]), fu(dp[2]), fu(dp[3]));
+        st_group(R, e, REC_G_BL + b, fu(dn[0]), fu(dn[1]), fu(dn[2]), fu(dn[3]), fu(dp[0]), fu(dp[1]), fu(dp[2]), fu(dp[3]));
     }
     // ---- groups 6..7: c_act 4..11, 12..19 ----
 #pragma unroll 1
@@ -137,7 +144,7 @@ __device__ void reset_record_thread(const DevPtrs& p, uint32_t e, uint32_t k, co
         float z0[4], z1[4];
         reset_normals4(lm & B_ACT_NOISE, g, k, CH_CORR_ACT, b, z0);
         reset_normals4(lm & B_ACT_NOISE, g, k, CH_CORR_ACT, b + 1, z1);
-        st_group(R, 6 + (b >> 1), fu(sc * z0[0]), fu(sc * z0[1]), fu(sc * z0[2]), fu(sc * z0[3]), fu(sc * z1[0]),
+        st_group(R, e, 6 + (b >> 1), fu(sc * z0[0]), fu(sc * z0[1]), fu(sc * z0[2]), fu(sc * z0[3]), fu(sc * z1[0]),
                  fu(sc * z1[1]), fu(sc * z1[2]), fu(sc * z1[3]));
     }
     // ---- groups 8..10: observation offsets [Q14, Q15], lambda, p-index ----
@@ -164,11 +171,11 @@ __device__ void reset_record_thread(const DevPtrs& p, uint32_t e, uint32_t k, co
         for (int c = 0; c < 3; ++c) co[c] = obs ? c_dc.obj_corr * co[c] : 0.f;
         if (obs) rotation(c_dc.rot_corr, philox(g, k, CH_CORR_ROT, 0), qc);
     }
-    st_group(R, 8, fu(off[0]), fu(off[1]), fu(off[2]), fu(off[3]), fu(off[4]), fu(off[5]), fu(off[6]), fu(off[7]));
-    st_group(R, 9, fu(off[8]), fu(off[9]), fu(off[10]), fu(off[11]), fu(off[12]), fu(off[13]), fu(off[14]), fu(co[0]));
-    st_group(R, 10, fu(co[1]), fu(co[2]), fu(qc[0]), fu(qc[1]), fu(qc[2]), fu(qc[3]), fu(lam), jp);
+    st_group(R, e, 8, fu(off[0]), fu(off[1]), fu(off[2]), fu(off[3]), fu(off[4]), fu(off[5]), fu(off[6]), fu(off[7]));
+    st_group(R, e, 9, fu(off[8]), fu(off[9]), fu(off[10]), fu(off[11]), fu(off[12]), fu(off[13]), fu(off[14]), fu(co[0]));
+    st_group(R, e, 10, fu(co[1]), fu(co[2]), fu(qc[0]), fu(qc[1]), fu(qc[2]), fu(qc[3]), fu(lam), jp);
     // ---- group 11: the episode counter ----
-    st_group(R, 11, k, 0u, 0u, 0u, 0u, 0u, 0u, 0u);
+    st_group(R, e, 11, k, 0u, 0u, 0u, 0u, 0u, 0u, 0u);
     p.st[st_index(e) + ST_FLAGS * PLANE] = FRESH_BIT;   // state reads as zero at the next step [Q6, Q9]
 }
 
@@ -241,7 +248,7 @@ __global__ void __launch_bounds__(RH_THREADS, DR_RH_MINB) reset_kernel(DevPtrs p
             if (m) {
                 const uint32_t idx = pos0 + __popc(bal & ((1u << lane) - 1u));
                 s_env[idx] = e;
-                s_kk[idx] = first ? 0u : p.rec[rec_index(e) + rec_off(REC_EPISODE)] + 1u;
+                s_kk[idx] = first ? 0u : p.rec[rec_index(e) + rec_off(e, REC_EPISODE)] + 1u;
             }
             applied += (lane == 0) ? (uint32_t)__popc(bal) : 0u;
         }

@@ -60,37 +60,39 @@ __device__ __forceinline__ void cp_wait() { asm volatile("cp.async.wait_group %0
 
 // ---- phase ring layout ---------------------------------------------------------------------
 // A slot is RING_W rows of TILE words, and warp w owns columns 32 w .. 32 w + 31 of every row (the
-// four warps of a CTA run their pipelines independently, so no row segment is shared).  A state
-// plane takes one row (thread tid's word at row * TILE + tid: a warp reads 32 consecutive words,
-// conflict-free).  A record quad -- 4 consecutive record words of one env, half a sector group --
-// takes 4 rows: lane l's float4 sits in row + l / 8 at column 32 w + 4 (l % 8) (quad_off), so each
-// quarter-warp of an LDS.128 reads 128 contiguous bytes (conflict-free).
-// Record groups are always fetched whole (two 16-byte cp.async per lane pair, 512 contiguous bytes
-// per instruction): a half-group fetch would touch each sector twice and scatter its shared-memory
-// writes (measured: 8x the LDGSTS wavefronts, 1.8x the L2 sectors, 17 % slower).  A group whose two
-// halves feed different phases lands in two places: half 0 in its phase's rows, half 1 in rows a
-// later phase reads (the c_act quads: see cact()).
+// four warps of a CTA run their pipelines independently, so no row segment is shared).
+//  * A state plane takes one row: thread tid's word at row * TILE + tid (a warp reads 32
+//    consecutive words, conflict-free).
+//  * A record group (one 32-byte sector per env) takes an 8-row block: env lane l's 8 words sit in
+//    row l / 4 of the block at columns 32 w + 8 (l % 4) .. + 7 (group_off), in the order they are
+//    stored in HBM, so a sector lands contiguously (one L2 request per sector: a split sector costs
+//    a request per half -- measured 4x the L2 read requests and 20 % more step time).  Thread tid
+//    reads logical half h with one LDS.128 at chunk h ^ rec_swz (dr_internal.h): within each
+//    quarter-warp the eight lanes then hit eight different 16-byte bank groups.
+// Record groups are fetched whole (two 16-byte cp.async per env, 512 contiguous bytes per
+// instruction); a group whose two halves feed different phases lands in a block that outlives both.
 constexpr int RING_W = 24;
 constexpr int N_PHASES = 7;   // S0, A0..A4, OB
 constexpr size_t STEP_DYN_SMEM = 2 * RING_W * TILE * sizeof(uint32_t);   // 2 slots
-// S0 (slot 0): rows 0..3 the quad (delay bits, 1/lambda, force threshold, mass) = record words 0..3,
-// then the state planes flags (row 4), f_trig (5..7), k_f (8).
-enum : int { S0_FLAGS = 4, S0_FTRIG = 5, S0_KF = 8 };
-// A_b (slot 1 for even b, slot 0 for odd b): rows 0..3 prev (planes), 4..7 slack (planes), 8 the
-// delta-1 quad, 12 the delta+1 quad (record group 1 + b).  The c_act quad of A_b (record words
-// rec_cact(4b)..+3) sits at cact(b): A0 slot 1 rows 16.. (second half of group 0, fetched with S0),
-// A1 / A3 slot 0 rows 16.. and A2 slot 0 rows 20.. / A4 slot 1 rows 20.. (groups 6 / 7, fetched with
-// A1 / A3).  OB (slot 0): rows 4h.. = quad h of record words 64..87 (off_tip 0..14, c_obj 0..2,
-// q_c 0..3; the last two words, lambda and p-index, ride along in their sector).
-enum : int { A_PREV = 0, A_SLACK = 4, A_DNEG = 8, A_DPOS = 12, A_CACT = 16, A_CACT2 = 20 };
+// S0 (slot 0): state planes flags (row 0), f_trig (1..3), k_f (4).  Its record words 0..3 (delay
+// bits, 1/lambda, force threshold, mass) are half 0 of group 0, which lands in slot 1 block 16 with
+// c_act 0..3 (half 1, read by A0).
+enum : int { S0_FLAGS = 0, S0_FTRIG = 1, S0_KF = 4 };
+// A_b (slot 1 for even b, slot 0 for odd b): rows 0..3 prev, 4..7 slack (state planes), block 8 =
+// record group 1 + b (half 0 delta-1, half 1 delta+1 of actuators 4b..4b+3).  c_act quads: A0 slot 1
+// block 16 half 1 (group 0); A1 / A2 slot 0 block 16 halves 0 / 1 (group 6, fetched with A1); A3 / A4
+// slot 1 block 16 halves 0 / 1 (group 7, fetched with A3).  OB (slot 0): blocks 0, 8, 16 = record
+// groups 8, 9, 10 (off_tip 0..14, c_obj 0..2, q_c 0..3, lambda, p-index).
+enum : int { A_PREV = 0, A_SLACK = 4, A_BL = 8, BLK16 = 16 };
 
 __device__ __forceinline__ float ringf(const uint32_t* slot, int row, int tid) {
     return __uint_as_float(slot[row * TILE + tid]);
 }
-// word offset of env-lane tid's quad inside a 4-row quad block (see above)
-__device__ __forceinline__ int quad_off(int tid) { return ((tid & 31) >> 3) * TILE + (tid & ~31) + 4 * (tid & 7); }
-__device__ __forceinline__ float4 ringq(const uint32_t* slot, int row, int tid) {
-    return *reinterpret_cast<const float4*>(slot + row * TILE + quad_off(tid));
+// word offset of env lane el's 8-word block inside an 8-row group block (see above)
+__device__ __forceinline__ int group_off(int el) { return ((el & 31) >> 2) * TILE + (el & ~31) + 8 * (el & 3); }
+// logical half h (0: record words 8g..8g+3, 1: 8g+4..8g+7) of thread tid's env in the group block
+__device__ __forceinline__ float4 ringh(const uint32_t* blk, int tid, int h) {
+    return *reinterpret_cast<const float4*>(blk + group_off(tid) + 4 * (h ^ (int)(rec_swz((uint32_t)tid) >> 2)));
 }
 __device__ __forceinline__ float q4(const float4 v, int c) { return c == 0 ? v.x : (c == 1 ? v.y : (c == 2 ? v.z : v.w)); }
 
@@ -99,8 +101,8 @@ __device__ __forceinline__ float q4(const float4 v, int c) { return c == 0 ? v.x
 // 16 (l & 7)).  Record groups: two instructions, each moving the 32-byte groups of 16 envs (512
 // contiguous bytes; lane l: env 16 i + l / 2, half l & 1).  Lanes read words other lanes copied, so
 // every hand-over is a __syncwarp.  Cross-tile pipelining: the next tile's A0 is issued into slot 1
-// once A4 is consumed and its S0 into slot 0 once OB is consumed, so a new tile starts with both
-// phases already landed; the input rows are waited for only after the timing section (io_wait).
+// once A4 is consumed and its S0 once OB is consumed, so a new tile starts with both phases already
+// landed; the input rows are waited for only after the timing section (io_wait).
 template <uint32_t L>
 struct PipeWarp {
     uint32_t* slot0;   // s_ring (row 0, column 0)
@@ -117,34 +119,38 @@ struct PipeWarp {
             if (pi < n) cp_async16(slot + (row + pi) * TILE + wcol + sub, src + pi * TILE + sub);
         }
     }
-    // record sector group grp of the warp's 32 envs: half 0 -> d0 (a quad row block), half 1 -> d1
-    __device__ __forceinline__ void group(uint32_t* d0, uint32_t* d1, const uint32_t* R, int grp) {
+    // record sector group grp of the warp's 32 envs -> the 8-row block at blk
+    __device__ __forceinline__ void group(uint32_t* blk, const uint32_t* R, int grp) {
         const int h = lane & 1;
 #pragma unroll
         for (int i = 0; i < 2; ++i) {
             const int el = wcol + 16 * i + (lane >> 1);
-            cp_async16((h ? d1 : d0) + quad_off(el), R + (size_t)grp * (TILE * 8) + (size_t)el * 8 + 4 * h);
+            cp_async16(blk + group_off(el) + 4 * h, R + (size_t)grp * (TILE * 8) + (size_t)el * 8 + 4 * h);
         }
     }
-    __device__ __forceinline__ uint32_t* row(uint32_t* slot, int r) { return slot + r * TILE; }
-    __device__ __forceinline__ const uint32_t* cact(int b) const {
-        return (b == 0 || b == 4 ? slot1 : slot0) + (b == 2 || b == 4 ? A_CACT2 : A_CACT) * TILE;
+    __device__ __forceinline__ static uint32_t* row(uint32_t* slot, int r) { return slot + r * TILE; }
+    // the group-0 block: S0's record words (half 0) and A0's c_act (half 1)
+    __device__ __forceinline__ const uint32_t* g0() const { return slot1 + BLK16 * TILE; }
+    // c_act quad of phase b: (block, logical half)
+    __device__ __forceinline__ float4 cact(int b) const {
+        const uint32_t* blk = (b == 1 || b == 2 ? slot0 : slot1) + BLK16 * TILE;
+        return ringh(blk, tid, (b == 1 || b == 3) ? 0 : 1);
     }
     __device__ __forceinline__ void issue_s0_of(const uint32_t* R, const uint32_t* S) {
         if (on<L>(B_TIMING) || on<L>(B_DELAY) || on<L>(B_FORCE) || on<L>(B_ACT_NOISE))
-            group(slot0, row(slot1, A_CACT), R, 0);                                   // S0 quad | c_act 0..3
-        if (on<L>(B_FORCE)) planes(slot0, S0_FLAGS, S + ST_FLAGS * TILE, 5);         // state planes 55..59
+            group(row(slot1, BLK16), R, 0);                                            // S0 quad | c_act 0..3
+        if (on<L>(B_FORCE)) planes(slot0, S0_FLAGS, S + ST_FLAGS * TILE, 5);           // state planes 55..59
         else if (on<L>(B_STATEFUL)) planes(slot0, S0_FLAGS, S + ST_FLAGS * TILE, 1);
     }
     __device__ __forceinline__ void issue_act_of(uint32_t* sl, int b, const uint32_t* R, const uint32_t* S) {
         if (on<L>(B_DELAY)) planes(sl, A_PREV, S + (ST_PREV + 4 * b) * TILE, 4);
         if (on<L>(B_BACKLASH)) {
             planes(sl, A_SLACK, S + (ST_SLACK + 4 * b) * TILE, 4);
-            group(row(sl, A_DNEG), row(sl, A_DPOS), R, REC_G_BL + b);
+            group(row(sl, A_BL), R, REC_G_BL + b);
         }
         if (on<L>(B_ACT_NOISE)) {
-            if (b == 1) group(row(slot0, A_CACT), row(slot0, A_CACT2), R, 6);   // c_act 4..7 | 8..11
-            if (b == 3) group(row(slot0, A_CACT), row(slot1, A_CACT2), R, 7);   // c_act 12..15 | 16..19
+            if (b == 1) group(row(slot0, BLK16), R, 6);   // c_act 4..7 | 8..11 (A1 | A2)
+            if (b == 3) group(row(slot1, BLK16), R, 7);   // c_act 12..15 | 16..19 (A3 | A4)
         }
     }
     __device__ __forceinline__ void issue_s0() { issue_s0_of(Rt, Sw); }
@@ -152,7 +158,7 @@ struct PipeWarp {
     __device__ __forceinline__ void issue_obs(uint32_t* sl) {
         if (on<L>(B_OBS_NOISE)) {
 #pragma unroll
-            for (int gi = 0; gi < 3; ++gi) group(row(sl, 8 * gi), row(sl, 8 * gi + 4), Rt, REC_OFFTIP / 8 + gi);
+            for (int gi = 0; gi < 3; ++gi) group(row(sl, 8 * gi), Rt, REC_OFFTIP / 8 + gi);
         }
     }
     __device__ __forceinline__ const uint32_t* s0() { return slot0; }   // the tile loop waited
@@ -227,7 +233,7 @@ __device__ __forceinline__ void env_step(const DevPtrs& p, uint32_t e, bool vali
 
     // ---- S0: scalars ----
     const uint32_t* s0 = pipe.s0();
-    const float4 sq = (on<L>(B_TIMING) || on<L>(B_DELAY) || on<L>(B_FORCE)) ? ringq(s0, 0, tid)
+    const float4 sq = (on<L>(B_TIMING) || on<L>(B_DELAY) || on<L>(B_FORCE)) ? ringh(pipe.g0(), tid, 0)
                                                                              : make_float4(0.f, 0.f, 0.f, 0.f);
     const float il = on<L>(B_TIMING) ? sq.y : 0.f;
     const uint32_t dbits = on<L>(B_DELAY) ? __float_as_uint(sq.x) : 0u;
@@ -291,9 +297,9 @@ __device__ __forceinline__ void env_step(const DevPtrs& p, uint32_t e, bool vali
         const uint32_t* sl = pipe.act(b);
         float prev[4], slack[4], dneg[4], dpos[4], cact[4];
         const float4 z4 = make_float4(0.f, 0.f, 0.f, 0.f);
-        const float4 dn4 = on<L>(B_BACKLASH) ? ringq(sl, A_DNEG, tid) : z4;
-        const float4 dp4 = on<L>(B_BACKLASH) ? ringq(sl, A_DPOS, tid) : z4;
-        const float4 ca4 = on<L>(B_ACT_NOISE) ? ringq(pipe.cact(b), 0, tid) : z4;
+        const float4 dn4 = on<L>(B_BACKLASH) ? ringh(sl + A_BL * TILE, tid, 0) : z4;
+        const float4 dp4 = on<L>(B_BACKLASH) ? ringh(sl + A_BL * TILE, tid, 1) : z4;
+        const float4 ca4 = on<L>(B_ACT_NOISE) ? pipe.cact(b) : z4;
 #pragma unroll
         for (int q = 0; q < 4; ++q) {
             prev[q] = (on<L>(B_DELAY) && !fresh) ? ringf(sl, A_PREV + q, tid) : 0.f;
@@ -521,7 +527,7 @@ __device__ __forceinline__ void env_step(const DevPtrs& p, uint32_t e, bool vali
         for (int b = 0; b < 4; ++b) {
             float z[4];
             normals4_t<kSfuNormals>(philox(g, t, CH_TIP_NOISE, b), z);
-            const float4 off4 = ringq(ob, 4 * b, tid);   // off_tip 4b..4b+3 (quad 3: 12..14, c_obj 0)
+            const float4 off4 = ringh(ob + 8 * (b >> 1) * TILE, tid, b & 1);   // off_tip 4b..4b+3 (b = 3: 12..14, c_obj 0)
 #pragma unroll
             for (int q = 0; q < 4; ++q) {
                 const int n = 4 * b + q;
@@ -550,7 +556,8 @@ __device__ __forceinline__ void env_step(const DevPtrs& p, uint32_t e, bool vali
     if (on<L>(B_OBS_NOISE)) {
         float z[4];
         normals4_t<kSfuNormals>(philox(g, t, CH_OBJ_NOISE, 0), z);
-        const float co[3] = {q4(ringq(ob, 12, tid), 3), q4(ringq(ob, 16, tid), 0), q4(ringq(ob, 16, tid), 1)};
+        const float4 c0 = ringh(ob + 8 * TILE, tid, 1), c1 = ringh(ob + 16 * TILE, tid, 0);
+        const float co[3] = {c0.w, c1.x, c1.y};
 #pragma unroll
         for (int c = 0; c < 3; ++c) obj[c] = (obj[c] + co[c]) + c_dc.obj_uncorr * z[c];
     }
@@ -566,7 +573,7 @@ __device__ __forceinline__ void env_step(const DevPtrs& p, uint32_t e, bool vali
         float qn[4];
         if (on<L>(B_OBS_NOISE)) {
             float qu[4], tmp[4];
-            const float4 qa4 = ringq(ob, 16, tid), qb4 = ringq(ob, 20, tid);   // q_c = record words 82..85
+            const float4 qa4 = ringh(ob + 16 * TILE, tid, 0), qb4 = ringh(ob + 16 * TILE, tid, 1);   // q_c = words 82..85
             const float qc[4] = {qa4.z, qa4.w, qb4.x, qb4.y};
             rotation<kSfuNormals>(c_dc.rot_uncorr, philox(g, t, CH_ROT_NOISE, 0), qu);
             qmul(qc, qo, tmp);

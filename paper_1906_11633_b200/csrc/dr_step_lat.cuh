@@ -67,13 +67,13 @@ __global__ void __launch_bounds__(LAT_THREADS, DR_LAT_MIN_CTAS) step_kernel_lat(
         if (wid < 5) {
             // ================= actuators 4b .. 4b+3 [Q1] =================
             const int b = wid;
-            const uint32_t dbits = on<L>(B_DELAY) ? R[rec_off(REC_DELAY)] : 0u;
+            const uint32_t dbits = on<L>(B_DELAY) ? R[rec_off(ec, REC_DELAY)] : 0u;
             float prev[4], slack[4], dneg[4], dpos[4], cact[4], ema[4];
             const float4 z4 = make_float4(0.f, 0.f, 0.f, 0.f);
             const float4* Rq = reinterpret_cast<const float4*>(R);
-            const float4 dn4 = on<L>(B_BACKLASH) ? Rq[rec_off(rec_dneg(4 * b)) / 4] : z4;   // record group 1 + b
-            const float4 dp4 = on<L>(B_BACKLASH) ? Rq[rec_off(rec_dpos(4 * b)) / 4] : z4;
-            const float4 ca4 = on<L>(B_ACT_NOISE) ? Rq[rec_off(rec_cact(4 * b)) / 4] : z4;
+            const float4 dn4 = on<L>(B_BACKLASH) ? Rq[rec_off(ec, rec_dneg(4 * b)) / 4] : z4;   // record group 1 + b
+            const float4 dp4 = on<L>(B_BACKLASH) ? Rq[rec_off(ec, rec_dpos(4 * b)) / 4] : z4;
+            const float4 ca4 = on<L>(B_ACT_NOISE) ? Rq[rec_off(ec, rec_cact(4 * b)) / 4] : z4;
 #pragma unroll
             for (int q = 0; q < 4; ++q) {
                 const int j = 4 * b + q;
@@ -186,7 +186,7 @@ __global__ void __launch_bounds__(LAT_THREADS, DR_LAT_MIN_CTAS) step_kernel_lat(
             acc.m[5] += valid ? s_zu2 : 0.f;
         } else if (wid == 5) {
             // ================= timing + step words [Q2] =================
-            const float il = on<L>(B_TIMING) ? __uint_as_float(R[rec_off(REC_INVLAM)]) : 0.f;
+            const float il = on<L>(B_TIMING) ? __uint_as_float(R[rec_off(ec, REC_INVLAM)]) : 0.f;
             float d[N_SUB];
             uint2 w01 = make_uint2(0u, 0u);
             if (on<L>(B_TIMING)) {
@@ -251,7 +251,7 @@ __global__ void __launch_bounds__(LAT_THREADS, DR_LAT_MIN_CTAS) step_kernel_lat(
                 const float4* Rq = reinterpret_cast<const float4*>(R);
 #pragma unroll
                 for (int h = 0; h < 4; ++h) {
-                    const float4 v = Rq[rec_off(REC_OFFTIP + 4 * h) / 4];
+                    const float4 v = Rq[rec_off(ec, REC_OFFTIP + 4 * h) / 4];
 #pragma unroll
                     for (int c = 0; c < 4; ++c)
                         if (4 * h + c < 15) off[4 * h + c] = q4(v, c);
@@ -373,15 +373,15 @@ __global__ void __launch_bounds__(LAT_THREADS, DR_LAT_MIN_CTAS) step_kernel_lat(
             float cobj[3] = {0.f, 0.f, 0.f}, qc[4] = {0.f, 0.f, 0.f, 0.f};
             if (on<L>(B_OBS_NOISE)) {   // c_obj, q_c = record words 79..85 (groups 9, 10)
                 const float4* Rq = reinterpret_cast<const float4*>(R);
-                const float4 v0 = Rq[rec_off(76) / 4], v1 = Rq[rec_off(80) / 4], v2 = Rq[rec_off(84) / 4];
+                const float4 v0 = Rq[rec_off(ec, 76) / 4], v1 = Rq[rec_off(ec, 80) / 4], v2 = Rq[rec_off(ec, 84) / 4];
                 cobj[0] = v0.w; cobj[1] = v1.x; cobj[2] = v1.y;
                 qc[0] = v1.z; qc[1] = v1.w; qc[2] = v2.x; qc[3] = v2.y;
             }
             uint32_t tf = 0, kf = 0;
             float mass = 0.f, ft[3] = {0.f, 0.f, 0.f};
             if (on<L>(B_FORCE)) {
-                tf = R[rec_off(REC_TFORCE)];
-                mass = __uint_as_float(R[rec_off(REC_MASS)]);
+                tf = R[rec_off(ec, REC_TFORCE)];
+                mass = __uint_as_float(R[rec_off(ec, REC_MASS)]);
                 if (!fresh) {
                     kf = S[ST_KF * P];
 #pragma unroll
