@@ -3,10 +3,11 @@
 
 Default workload (N=1): BASELINE config 4's single-GPU reference -- 1,048,576 envs, full
 pipeline (all 9 layers), Shadow-hand shapes.  Under torchrun the envs are sharded by global id
-(env_offset = rank * n_local, same seed): by default every rank owns 1M envs ("weak", per-GPU
-work fixed); --scaling strong splits the 1M envs of config 4 over the N ranks.  The per-step
-NCCL all-reduce of the 32 x fp64 stats vector runs on a comm stream -- the path's one
-collective (DESIGN.md "Multi-GPU").
+(env_offset = offset of the rank's shard, same seed): by default the 1M envs of config 4 are split
+over the N ranks ("strong", config 4's "1M envs sharded 2/4/8"); --scaling weak gives every rank
+1M envs.  The per-step NCCL all-reduce of the 32 x fp64 stats vector runs on a comm stream -- the
+path's one collective -- and for N > 1 the steps and their all-reduces are
+captured in CUDA graphs of 100 steps.
 
   python bench.py [--gpus N] [--steps K] [--warmup W] [--config full1m|cfg2|cfg3|reset]
   python bench.py --impl reference ...   # the fp64 CPU oracle on the box's host cores
@@ -44,9 +45,9 @@ def parse():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--config", default="full1m", choices=["full1m", "cfg2", "cfg3", "reset", "vision"])
     ap.add_argument("--n-env", type=int, default=0, help="override the env count (per GPU if weak, global if strong)")
-    ap.add_argument("--scaling", default="weak", choices=["weak", "strong"],
-                    help="weak: every rank owns the config's env count (global = N x that); "
-                         "strong: the config's env count is split over the ranks")
+    ap.add_argument("--scaling", default="strong", choices=["weak", "strong"],
+                    help="strong (default): the config's env count is split over the ranks (BASELINE config 4: "
+                         "1M envs sharded over 2 / 4 / 8 GPUs); weak: every rank owns the config's env count")
     ap.add_argument("--e2e-steps", type=int, default=30)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-sample-envs", type=int, default=65536)
@@ -56,7 +57,7 @@ def parse():
                     help="process-group backend for N > 1 (gloo: tests that run several ranks on one GPU)")
     ap.add_argument("--graph", type=int, default=-1,
                     help="steps per CUDA graph in the timed region (0 = eager launches; default: 100 for the "
-                         "launch-bound small configs at N=1, else 0)")
+                         "launch-bound small configs at N=1 and for every N > 1 run over NCCL, else 0)")
     return ap.parse_args()
 
 
@@ -79,12 +80,16 @@ def config_of(name, n_override):
 
 
 class ClockSampler:
-    """nvidia-smi clocks + throttle reasons sampled every 100 ms during the timed region."""
+    """nvidia-smi clocks + throttle reasons every 20 ms, each sample stamped with the host clock.
+    The bench runs a >= 1 s pre-roll at the timed load with the sampler on (short timed regions,
+    e.g. --steps 20 at 0.2 ms, are shorter than any sampling interval) and keeps it on through the
+    timed region; the report says how many samples fell inside the timed window itself."""
 
     def __init__(self, index):
         self.index = index
         self.proc = None
         self.lines = []
+        self.window = None
 
     def start(self):
         q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
@@ -92,7 +97,7 @@ class ClockSampler:
              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
         try:
             self.proc = subprocess.Popen(["nvidia-smi", "-i", str(self.index), f"--query-gpu={q}",
-                                          "--format=csv,noheader,nounits", "-lms", "100"],
+                                          "--format=csv,noheader,nounits", "-lms", "20"],
                                          stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
             self.t = threading.Thread(target=self._read, daemon=True)
             self.t.start()
@@ -101,20 +106,24 @@ class ClockSampler:
 
     def _read(self):
         for line in self.proc.stdout:
-            self.lines.append(line.strip())
+            self.lines.append((time.monotonic(), line.strip()))
+
+    def mark_timed(self, t0, t1):
+        self.window = (t0, t1)
 
     def stop(self):
         if not self.proc:
             return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        time.sleep(0.05)
         self.proc.terminate()
         try:
             self.proc.wait(timeout=2)
         except Exception:
             self.proc.kill()
         time.sleep(0.05)
-        sm, mx, reasons = [], None, set()
+        sm, mx, reasons, in_timed = [], None, set(), 0
         names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
-        for ln in self.lines:
+        for ts, ln in self.lines:
             parts = [x.strip() for x in ln.split(",")]
             if len(parts) < 9:
                 continue
@@ -123,12 +132,30 @@ class ClockSampler:
                 mx = float(parts[2])
             except ValueError:
                 continue
+            if self.window and self.window[0] <= ts <= self.window[1] + 0.025:
+                in_timed += 1
             for nm, v in zip(names, parts[5:9]):
                 if v.lower() == "active":
                     reasons.add(nm)
         sm.sort()
         med = sm[len(sm) // 2] if sm else None
-        return {"sm_mhz": med, "sm_max_mhz": mx, "reasons": sorted(reasons), "samples": len(sm)}
+        return {"sm_mhz": med, "sm_max_mhz": mx, "reasons": sorted(reasons), "samples": len(sm),
+                "samples_in_timed_window": in_timed, "interval_ms": 20,
+                "coverage": ">= 1 s pre-roll at the timed load + the timed region"}
+
+
+def host_cpu():
+    """(logical cores, CPU model) of this host."""
+    model = None
+    try:
+        with open("/proc/cpuinfo") as f:
+            for ln in f:
+                if ln.startswith("model name"):
+                    model = ln.split(":", 1)[1].strip()
+                    break
+    except OSError:
+        pass
+    return os.cpu_count(), model
 
 
 def measured_peak():
@@ -176,10 +203,13 @@ def run_reference(args):
         return
     cfg = config_of(args.config, args.n_env)
     cfg["scaling"] = args.scaling
+    cores, model = host_cpu()
+    # the oracle as it stands, all host cores (the -fopenmp build: OpenMP over envs), a bounded
+    # sample of the workload per step so the whole --steps K --warmup W run takes a few minutes
     n = min(cfg["n"], args.cpu_sample_envs)
     P = presets.preset(cfg["mask"])
     acts, obs = gen.frames(n, 4)
-    orc = Oracle(P, n, presets.SEED_DR)
+    orc = Oracle(P, n, presets.SEED_DR, omp=True)
     for t in range(args.warmup):
         orc.step(acts[t % 4], obs[t % 4])
     steps = max(1, min(args.steps, args.cpu_sample_steps))
@@ -194,21 +224,20 @@ def run_reference(args):
             "n_gpus": args.gpus, "steps": steps, "warmup": args.warmup, "ms_per_step": dt / steps * 1e3,
             "higher_is_better": True, "scaling": cfg["scaling"], "vs_baseline": None, "dtype": "f64",
             "data": "synthetic", "config": {"workload": cfg["workload"], "n_env_sample": n, "layers": hex(cfg["mask"])},
-            "cpu_baseline": {"value": v, "unit": "env-steps/s", "cores": 1, "kind": "oracle",
-                             "sample": f"{n} envs x {steps} steps of {cfg['workload']} (single thread, fp64)"},
+            "cpu_baseline": {"value": v, "unit": "env-steps/s", "cores": cores, "kind": "oracle", "cpu_model": model,
+                             "sample": f"{n} envs x {steps} steps of {cfg['workload']} (fp64 oracle, OpenMP over envs)"},
             "e2e": {"value": v, "unit": "env-steps/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
 
 
-def cpu_baseline(cfg, args):
-    import numpy as np  # noqa: F401
+def _oracle_rate(cfg, n, steps, omp):
+    """env-steps/s of the fp64 oracle (single-thread or -fopenmp build) on n envs x steps."""
     from oracle.oracle import Oracle
     from workload import gen, presets
-    n = min(cfg["n"], args.cpu_sample_envs)
     P = presets.preset(cfg["mask"])
     acts, obs = gen.frames(n, 4)
-    orc = Oracle(P, n, presets.SEED_DR)
-    steps = args.cpu_sample_steps
+    orc = Oracle(P, n, presets.SEED_DR, omp=omp)
+    orc.step(acts[0], obs[0])   # first touch
     t0 = time.perf_counter()
     for t in range(steps):
         if cfg["resets"]:
@@ -216,8 +245,25 @@ def cpu_baseline(cfg, args):
         orc.step(acts[t % 4], obs[t % 4])
     dt = time.perf_counter() - t0
     orc.close()
-    return {"value": n * steps / dt, "unit": "env-steps/s", "cores": 1, "kind": "oracle",
-            "sample": f"{n} envs x {steps} steps of {cfg['workload']} (fp64 oracle, single thread)"}
+    return n * steps / dt, dt
+
+
+def cpu_baseline(cfg, args):
+    """The oracle as it stands on this host: single thread (liboracle.so) and all cores (the same
+    source built with -fopenmp, parallel over envs; bit-identical results).  Bounded samples:
+    ~10 s single-thread, ~10 s all-core.  `value` is the all-core rate (the paper's DR ran on CPU
+    workers, so all cores is the honest CPU comparison)."""
+    cores, model = host_cpu()
+    n = min(cfg["n"], args.cpu_sample_envs)
+    v1, _ = _oracle_rate(cfg, n, args.cpu_sample_steps, omp=False)
+    na = n
+    probe, dtp = _oracle_rate(cfg, na, 2, omp=True)
+    steps_all = max(2, min(200, int(10.0 / max(dtp / 2, 1e-6))))
+    va, _ = _oracle_rate(cfg, na, steps_all, omp=True)
+    return {"value": va, "unit": "env-steps/s", "cores": cores, "kind": "oracle", "cpu_model": model,
+            "sample": f"all cores: {na} envs x {steps_all} steps of {cfg['workload']} (fp64 oracle, OpenMP over envs); "
+                      f"single thread: {n} envs x {args.cpu_sample_steps} steps",
+            "single_thread": {"value": v1, "unit": "env-steps/s", "cores": 1}}
 
 
 def run_vision(args):
@@ -276,19 +322,27 @@ def run_vision(args):
         torch.cuda.synchronize()
         sampler = ClockSampler(local)
         sampler.start()
-        for t in range(args.warmup, args.warmup + min(args.warmup, 50)):
-            one_step(t)
-        t_base = args.warmup + min(args.warmup, 50)
+        w0 = time.perf_counter()   # >= 1 s pre-roll at the timed load (clock coverage, see ClockSampler)
+        t_base = args.warmup
+        while True:
+            for _ in range(20):
+                one_step(t_base)
+                t_base += 1
+            torch.cuda.synchronize()
+            if time.perf_counter() - w0 >= 1.0:
+                break
         if world > 1:
             dist.barrier()
         torch.cuda.synchronize()
         l0 = vision.dr_total_kernel_launches()
         evs = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps + 1)]
+        h0 = time.monotonic()
         evs[0].record(stream)
         for i in range(args.steps):
             one_step(t_base + i)
             evs[i + 1].record(stream)
         torch.cuda.synchronize()
+        sampler.mark_timed(h0, time.monotonic())
         if world > 1:
             dist.barrier()
         launches = vision.dr_total_kernel_launches() - l0
@@ -443,31 +497,52 @@ def main():
         for t in range(args.warmup):
             one_step(t)
         torch.cuda.synchronize()
+        # pre-roll at the timed load for >= 1 s with the clock sampler on (the timed region of a
+        # short --steps run is shorter than nvidia-smi's sampling interval)
         sampler = ClockSampler(local)
         sampler.start()
-        # keep the GPU busy briefly so the sampler sees load clocks even for short K
-        for t in range(args.warmup, args.warmup + min(args.warmup, 50)):
-            one_step(t)
-        t_base = args.warmup + min(args.warmup, 50)
+        w0 = time.perf_counter()
+        t_next = args.warmup
+        while True:
+            for _ in range(10):
+                one_step(t_next)
+                t_next += 1
+            torch.cuda.synchronize()
+            if time.perf_counter() - w0 >= 1.0:
+                break
+        t_base = t_next
         if world > 1:
             dist.barrier()
         torch.cuda.synchronize()
         launches0 = dr.dr_kernel_launches()
-        G = args.graph if args.graph >= 0 else (100 if (world == 1 and n * cfg["bytes"] < 2e8) else 0)
-        if G > 0 and (world > 1 or args.steps % G or (cfg["resets"] and G % 10)):
-            G = 0   # graphs need K % G == 0 (and whole 10-step reset-mask cycles); multi-rank runs eager
+        # CUDA graphs of G steps: the launch-bound small configs at N = 1, and every N > 1 run over NCCL
+        # (the step kernels and the per-step stats all-reduce of the comm stream captured together, so
+        # no rank's host issues a launch or a collective per step)
+        graphable = world == 1 or args.backend == "nccl"
+        G = args.graph if args.graph >= 0 else (100 if (graphable and (world > 1 or n * cfg["bytes"] < 2e8)) else 0)
+        if G > 0 and (not graphable or args.steps % G or (cfg["resets"] and G % 10)):
+            G = 0   # graphs need K % G == 0 (and whole 10-step reset-mask cycles); gloo cannot be captured
         if G > 0:
             # launch-bound configs: one CUDA graph of G steps (the step index is device-resident, so
-            # every replay advances it); events around each replay, per-step time = replay / G
+            # every replay advances it); events around each replay, per-step time = replay / G.
+            # Inside the capture the reducer only waits for all-reduces of the same graph: the graph
+            # ends by joining the comm stream, so the previous replay's all-reduces are complete.
             graph = torch.cuda.CUDAGraph()
             with torch.cuda.graph(graph, stream=lib_stream):
+                if reducer is not None:
+                    reducer.reset_ring()
                 for i in range(G):
                     one_step(t_base + i)
+                if reducer is not None:
+                    reducer.sync()
             per_graph_launches = dr.dr_kernel_launches() - launches0
             graph.replay()   # warm replay
             torch.cuda.synchronize()
+            if world > 1:
+                dist.barrier()
             reps = args.steps // G
             evs = [torch.cuda.Event(enable_timing=True) for _ in range(reps + 1)]
+            h0 = time.monotonic()
             evs[0].record(lib_stream)
             for i in range(reps):
                 graph.replay()
@@ -475,6 +550,7 @@ def main():
         else:
             evs = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps + 1)]
             mids = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)] if cfg["resets"] else None
+            h0 = time.monotonic()
             evs[0].record(lib_stream)
             for i in range(args.steps):
                 one_step(t_base + i, mids[i] if mids else None)
@@ -484,6 +560,7 @@ def main():
         end = torch.cuda.Event(enable_timing=True)
         end.record(lib_stream)
         torch.cuda.synchronize()
+        sampler.mark_timed(h0, time.monotonic())
         if world > 1:
             dist.barrier()
         launches = per_graph_launches * reps if G > 0 else dr.dr_kernel_launches() - launches0

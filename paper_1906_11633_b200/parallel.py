@@ -45,6 +45,11 @@ class StatsReducer:
         self.group = group
         self.done = [None] * self.SLOTS
 
+    def reset_ring(self):
+        """Forget the pending all-reduce events (e.g. at the start of a CUDA-graph capture whose
+        predecessor work was joined by sync())."""
+        self.done = [None] * self.SLOTS
+
     def before_step(self, t: int):
         ev = self.done[(t + 1) % self.SLOTS]   # the all-reduce of step t - 3
         if ev is not None:
