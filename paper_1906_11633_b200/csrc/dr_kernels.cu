@@ -104,13 +104,10 @@ __global__ void import_kernel(DevPtrs p, const uint32_t* __restrict__ src, uint3
 constexpr int IMPORT_PHYS_THREADS = 256;
 __global__ void __launch_bounds__(IMPORT_PHYS_THREADS) import_phys_kernel(DevPtrs p, uint32_t lo, uint32_t hi) {
     __shared__ float4 s_pd[MAX_PHYS];
-    __shared__ uint32_t s_src[MAX_PHYS];
+    __shared__ __align__(16) uint32_t s_src[MAX_PHYS];
     __shared__ __align__(16) float s_dr[IMPORT_PHYS_THREADS / 32][RH_DRAW];
     const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
-    for (int i = tid; i < c_dc.n_phys; i += IMPORT_PHYS_THREADS) {
-        s_pd[i] = p.rs_phys[i];
-        s_src[i] = p.rs_src[i];
-    }
+    stage_phys_tables(p, s_pd, s_src, tid, IMPORT_PHYS_THREADS);
     if (lane == 0) s_dr[wid][RS_OFF_ZERO] = 0.f;
     __syncthreads();
     const bool phys_on = (c_dc.layer_mask & B_PHYS) != 0;

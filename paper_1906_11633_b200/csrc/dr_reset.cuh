@@ -70,16 +70,28 @@ __device__ __forceinline__ void reset_normals4(bool on, uint32_t g, uint32_t k, 
     }
 }
 
+// Physics tables in shared memory, transposed for the row evaluation: lane l writes parameters
+// 8 l .. 8 l + 7 of a row (one 256-bit store), so parameter q lives at [q % 8][q / 8] (s_pd) and the
+// draw sources of lane l's quad h at [h][l] (s_src4): every LDS.128 of a warp is conflict-free.
+__device__ __forceinline__ int pd_slot(int q) { return (q & 7) * 32 + (q >> 3); }
+__device__ __forceinline__ void stage_phys_tables(const DevPtrs& p, float4* s_pd, uint32_t* s_src, int tid, int nthr) {
+    for (int q = tid; q < MAX_PHYS; q += nthr) {   // padded: draw-free zero entries past n_phys
+        const bool live = q < c_dc.n_phys;
+        s_pd[pd_slot(q)] = live ? p.rs_phys[q] : make_float4(0.f, 0.f, 0.f, 0.f);
+        s_src[(((q & 7) >> 2) * 32 + (q >> 3)) * 4 + (q & 3)] = live ? p.rs_src[q] : RS_OFF_ZERO;
+    }
+}
+
 // The object mass phys[mass_index] [Q18], recomputed by the record thread so that record group 0
 // is written whole (same draw, coefficients and operations as reset_phys_warp: bit-identical).
 __device__ __forceinline__ float reset_mass(uint32_t g, uint32_t k, const float4* s_pd, const uint32_t* s_src) {
     const int mi = c_dc.mass_index;
-    const float4 d = s_pd[mi];
-    const uint32_t o = s_src[mi], off = o & ~RS_EXP;
+    const float4 d = s_pd[pd_slot(mi)];
+    const uint32_t o = s_src[(((mi & 7) >> 2) * 32 + (mi >> 3)) * 4 + (mi & 3)], off = o & ~RS_EXP;
     float x = 0.f;
-    if (off < RS_OFF_NORMAL) {                  // uniform-kind parameter u: word u % 4 of block u / 4
+    if (off < RS_OFF_NORMAL) {                       // uniform-kind parameter u: word u % 4 of block u / 4
         x = uni(selw(philox(g, k, CH_PHYS_U, off >> 2), off & 3u));
-    } else if (off < RS_OFF_ZERO) {                      // normal-kind parameter n: normal n % 4 of block n / 4
+    } else if (off < RS_OFF_ZERO) {                  // normal-kind parameter n: normal n % 4 of block n / 4
         const uint32_t n = off - RS_OFF_NORMAL;
         const uint4 w = philox(g, k, CH_PHYS_N, n >> 2);
         float z0, z1;
@@ -91,66 +103,77 @@ __device__ __forceinline__ float reset_mass(uint32_t g, uint32_t k, const float4
     return fmaf(d.w, (o & RS_EXP) ? ex2_approx(tv) : tv, d.z);
 }
 
-// The episode record of env e for episode k (oracle: reset_env, steps 2-9), written group by group.
-__device__ void reset_record_thread(const DevPtrs& p, uint32_t e, uint32_t k, const float4* s_pd,
-                                    const uint32_t* s_src) {
+// The episode record of env e for episode k (oracle: reset_env, steps 2-9), in three independent
+// parts so three threads share one env's serial chain (each ~a third of the Philox blocks and
+// Box-Muller pairs); every part writes whole record groups:
+//   part 0: group 0 (delay flags, 1/lambda, force threshold, mass, c_act 0..3), groups 6-7 (c_act
+//           4..19), group 11 (episode counter) and the FRESH flag;
+//   part 1: groups 1-5 (backlash widths);
+//   part 2: groups 8-10 (observation offsets; lambda and p-index, drawn again, ride in group 10).
+__device__ void reset_record_part(const DevPtrs& p, uint32_t e, uint32_t k, int part, const float4* s_pd,
+                                  const uint32_t* s_src) {
     const uint32_t lm = c_dc.layer_mask;
     uint32_t* R = p.rec + rec_index(e);
     const uint32_t g = c_dc.env_offset + e;
-    // ---- group 0: delay flags, 1/lambda, force threshold, mass, c_act 0..3 ----
-    uint32_t bits = 0u;   // per-actuator delay flags, Bernoulli(0.5) per episode
-    if (lm & B_DELAY) {
-#pragma unroll
-        for (int b = 0; b < 5; ++b) {
-            const uint4 w = philox(g, k, CH_DELAY, b);
-            const uint32_t ws[4] = {w.x, w.y, w.z, w.w};
-#pragma unroll
-            for (int q = 0; q < 4; ++q) bits |= ((unsigned long long)ws[q] < c_dc.t_delay ? 1u : 0u) << (4 * b + q);
-        }
-    }
-    float lam = 0.f, il = 0.f;   // timing coefficient lambda ~ U[1250, 10000] (PAPER.md:87-88)
-    if (lm & B_TIMING) {
-        lam = c_dc.lam_lo + c_dc.lam_range * uni(philox(g, k, CH_LAMBDA, 0).x);
-        il = 1.0f / lam;
-    }
-    // loguniform force probability [Q19]: index + exact integer threshold
-    const uint32_t jp = (lm & B_FORCE) ? (philox(g, k, CH_FORCE_P, 0).x >> 16) : 0u;
-    const uint32_t tf = (lm & B_FORCE) ? __ldg(p.t_tab + jp) : 0u;
-    const float mass = reset_mass(g, k, s_pd, s_src);
     const float sc = c_dc.sc;   // correlated action noise, Table action-noise
-    {
-        float z[4];
-        reset_normals4(lm & B_ACT_NOISE, g, k, CH_CORR_ACT, 0, z);
-        st_group(R, e, 0, bits, fu(il), tf, fu(mass), fu(sc * z[0]), fu(sc * z[1]), fu(sc * z[2]), fu(sc * z[3]));
-    }
-    // ---- groups 1..5: backlash widths of actuators 4b..4b+3 [Q7]:
-    //      normal j -> delta-1_j (block j / 4), normal 20 + j -> delta+1_j (block 5 + j / 4) ----
-#pragma unroll 1
-    for (int b = 0; b < 5; ++b) {
-        float zn[4], zp[4], dn[4], dp[4];
-        reset_normals4(lm & B_BACKLASH, g, k, CH_BACKLASH, b, zn);
-        reset_normals4(lm & B_BACKLASH, g, k, CH_BACKLASH, 5 + b, zp);
-#pragma unroll
-        for (int q = 0; q < 4; ++q) {
-            const int j = 4 * b + q;
-            dn[q] = (lm & B_BACKLASH) ? fmaxf(0.f, c_dc.dcal_neg[j] + c_dc.jitter * zn[q]) : 0.f;
-            dp[q] = (lm & B_BACKLASH) ? fmaxf(0.f, c_dc.dcal_pos[j] + c_dc.jitter * zp[q]) : 0.f;
+    float lam = 0.f, il = 0.f;   // timing coefficient lambda ~ U[1250, 10000] (PAPER.md:87-88)
+    uint32_t jp = 0u;            // loguniform force probability [Q19]: index
+    if (part != 1) {
+        if (lm & B_TIMING) {
+            lam = c_dc.lam_lo + c_dc.lam_range * uni(philox(g, k, CH_LAMBDA, 0).x);
+            il = 1.0f / lam;
         }
-        st_group(R, e, REC_G_BL + b, fu(dn[0]), fu(dn[1]), fu(dn[2]), fu(dn[3]), fu(dp[0]), fu(dp[1]), fu(dp[2]), fu(dp[3]));
+        jp = (lm & B_FORCE) ? (philox(g, k, CH_FORCE_P, 0).x >> 16) : 0u;
     }
-    // ---- groups 6..7: c_act 4..11, 12..19 ----
+    if (part == 0) {
+        uint32_t bits = 0u;   // per-actuator delay flags, Bernoulli(0.5) per episode
+        if (lm & B_DELAY) {
+#pragma unroll
+            for (int b = 0; b < 5; ++b) {
+                const uint4 w = philox(g, k, CH_DELAY, b);
+                const uint32_t ws[4] = {w.x, w.y, w.z, w.w};
+#pragma unroll
+                for (int q = 0; q < 4; ++q) bits |= ((unsigned long long)ws[q] < c_dc.t_delay ? 1u : 0u) << (4 * b + q);
+            }
+        }
+        const uint32_t tf = (lm & B_FORCE) ? __ldg(p.t_tab + jp) : 0u;   // exact integer threshold
+        const float mass = reset_mass(g, k, s_pd, s_src);
+        {
+            float z[4];
+            reset_normals4(lm & B_ACT_NOISE, g, k, CH_CORR_ACT, 0, z);
+            st_group(R, e, 0, bits, fu(il), tf, fu(mass), fu(sc * z[0]), fu(sc * z[1]), fu(sc * z[2]), fu(sc * z[3]));
+        }
 #pragma unroll 1
-    for (int b = 1; b < 5; b += 2) {
-        float z0[4], z1[4];
-        reset_normals4(lm & B_ACT_NOISE, g, k, CH_CORR_ACT, b, z0);
-        reset_normals4(lm & B_ACT_NOISE, g, k, CH_CORR_ACT, b + 1, z1);
-        st_group(R, e, 6 + (b >> 1), fu(sc * z0[0]), fu(sc * z0[1]), fu(sc * z0[2]), fu(sc * z0[3]), fu(sc * z1[0]),
-                 fu(sc * z1[1]), fu(sc * z1[2]), fu(sc * z1[3]));
-    }
-    // ---- groups 8..10: observation offsets [Q14, Q15], lambda, p-index ----
-    float off[16], co[4], qc[4] = {1.f, 0.f, 0.f, 0.f};
-    const bool obs = (lm & B_OBS_NOISE) != 0;
-    {
+        for (int b = 1; b < 5; b += 2) {   // groups 6..7: c_act 4..11, 12..19
+            float z0[4], z1[4];
+            reset_normals4(lm & B_ACT_NOISE, g, k, CH_CORR_ACT, b, z0);
+            reset_normals4(lm & B_ACT_NOISE, g, k, CH_CORR_ACT, b + 1, z1);
+            st_group(R, e, 6 + (b >> 1), fu(sc * z0[0]), fu(sc * z0[1]), fu(sc * z0[2]), fu(sc * z0[3]), fu(sc * z1[0]),
+                     fu(sc * z1[1]), fu(sc * z1[2]), fu(sc * z1[3]));
+        }
+        st_group(R, e, 11, k, 0u, 0u, 0u, 0u, 0u, 0u, 0u);
+        p.st[st_index(e) + ST_FLAGS * PLANE] = FRESH_BIT;   // state reads as zero at the next step [Q6, Q9]
+    } else if (part == 1) {
+        // backlash widths of actuators 4b..4b+3 [Q7]: normal j -> delta-1_j
+        // (block j / 4), normal 20 + j -> delta+1_j (block 5 + j / 4)
+#pragma unroll 1
+        for (int b = 0; b < 5; ++b) {
+            float zn[4], zp[4], dn[4], dp[4];
+            reset_normals4(lm & B_BACKLASH, g, k, CH_BACKLASH, b, zn);
+            reset_normals4(lm & B_BACKLASH, g, k, CH_BACKLASH, 5 + b, zp);
+#pragma unroll
+            for (int q = 0; q < 4; ++q) {
+                const int j = 4 * b + q;
+                dn[q] = (lm & B_BACKLASH) ? fmaxf(0.f, c_dc.dcal_neg[j] + c_dc.jitter * zn[q]) : 0.f;
+                dp[q] = (lm & B_BACKLASH) ? fmaxf(0.f, c_dc.dcal_pos[j] + c_dc.jitter * zp[q]) : 0.f;
+            }
+            st_group(R, e, REC_G_BL + b, fu(dn[0]), fu(dn[1]), fu(dn[2]), fu(dn[3]), fu(dp[0]), fu(dp[1]), fu(dp[2]),
+                     fu(dp[3]));
+        }
+    } else {
+        // observation offsets [Q14, Q15]
+        float off[16], co[4], qc[4] = {1.f, 0.f, 0.f, 0.f};
+        const bool obs = (lm & B_OBS_NOISE) != 0;
         float mb[4];
         reset_normals4(obs, g, k, CH_MARKER_BASE, 0, mb);
 #pragma unroll
@@ -170,17 +193,16 @@ __device__ void reset_record_thread(const DevPtrs& p, uint32_t e, uint32_t k, co
 #pragma unroll
         for (int c = 0; c < 3; ++c) co[c] = obs ? c_dc.obj_corr * co[c] : 0.f;
         if (obs) rotation(c_dc.rot_corr, philox(g, k, CH_CORR_ROT, 0), qc);
+        st_group(R, e, 8, fu(off[0]), fu(off[1]), fu(off[2]), fu(off[3]), fu(off[4]), fu(off[5]), fu(off[6]), fu(off[7]));
+        st_group(R, e, 9, fu(off[8]), fu(off[9]), fu(off[10]), fu(off[11]), fu(off[12]), fu(off[13]), fu(off[14]), fu(co[0]));
+        st_group(R, e, 10, fu(co[1]), fu(co[2]), fu(qc[0]), fu(qc[1]), fu(qc[2]), fu(qc[3]), fu(lam), jp);
     }
-    st_group(R, e, 8, fu(off[0]), fu(off[1]), fu(off[2]), fu(off[3]), fu(off[4]), fu(off[5]), fu(off[6]), fu(off[7]));
-    st_group(R, e, 9, fu(off[8]), fu(off[9]), fu(off[10]), fu(off[11]), fu(off[12]), fu(off[13]), fu(off[14]), fu(co[0]));
-    st_group(R, e, 10, fu(co[1]), fu(co[2]), fu(qc[0]), fu(qc[1]), fu(qc[2]), fu(qc[3]), fu(lam), jp);
-    // ---- group 11: the episode counter ----
-    st_group(R, e, 11, k, 0u, 0u, 0u, 0u, 0u, 0u, 0u);
-    p.st[st_index(e) + ST_FLAGS * PLANE] = FRESH_BIT;   // state reads as zero at the next step [Q6, Q9]
 }
 
 // The physics row of env e for episode k [Q20]: v = C0 + C1 f(A + B x),
-// f = 2^(.) for the exp kinds (the host folds log2(e) into A and B: one MUFU.EX2).
+// f = 2^(.) for the exp kinds (the host folds log2(e) into A and B: one MUFU.EX2).  Lanes draw the
+// env's Philox blocks into the warp's draw buffer, then lane l evaluates parameters 8 l .. 8 l + 7
+// (tables padded to 256 with draw-free zero entries) and writes them with one 256-bit store.
 __device__ __forceinline__ void reset_phys_warp(const DevPtrs& p, uint32_t e, uint32_t k, int lane, float* dr,
                                                 const float4* s_pd, const uint32_t* s_src, int nub, int nnb) {
     const uint32_t g = c_dc.env_offset + e;
@@ -200,42 +222,55 @@ __device__ __forceinline__ void reset_phys_warp(const DevPtrs& p, uint32_t e, ui
     }
     __syncwarp();
     const int np = c_dc.n_phys;
-    float* prow = p.phys + (size_t)e * np;
+    if (8 * lane >= np) return;
+    const uint4* src4 = reinterpret_cast<const uint4*>(s_src);
+    float v[8];
 #pragma unroll
-    for (int i = 0; i < MAX_PHYS / 32; ++i) {
-        const int q = lane + 32 * i;
-        if (q < np) {
-            const float4 d = s_pd[q];   // (A, B, C0, C1)
-            const uint32_t o = s_src[q];
-            const float x = dr[o & ~RS_EXP];
+    for (int h = 0; h < 2; ++h) {
+        const uint4 o4 = src4[h * 32 + lane];
+        const uint32_t os[4] = {o4.x, o4.y, o4.z, o4.w};
+#pragma unroll
+        for (int c = 0; c < 4; ++c) {
+            const float4 d = s_pd[(4 * h + c) * 32 + lane];   // (A, B, C0, C1)
+            const float x = dr[os[c] & ~RS_EXP];
             const float tv = fmaf(d.y, x, d.x);
-            prow[q] = fmaf(d.w, (o & RS_EXP) ? ex2_approx(tv) : tv, d.z);
+            v[4 * h + c] = fmaf(d.w, (os[c] & RS_EXP) ? ex2_approx(tv) : tv, d.z);
         }
+    }
+    float* prow = p.phys + (size_t)e * np + 8 * lane;
+    if ((np & 7) == 0) {   // rows 32-byte aligned (np % 8 == 0): one 256-bit store per lane
+        asm volatile("st.global.v8.f32 [%0], {%1, %2, %3, %4, %5, %6, %7, %8};" ::"l"(prow), "f"(v[0]), "f"(v[1]),
+                     "f"(v[2]), "f"(v[3]), "f"(v[4]), "f"(v[5]), "f"(v[6]), "f"(v[7])
+                     : "memory");
+    } else {
+#pragma unroll
+        for (int c = 0; c < 8; ++c)
+            if (8 * lane + c < np) prow[c] = v[c];
     }
 }
 
 __global__ void __launch_bounds__(RH_THREADS, DR_RH_MINB) reset_kernel(DevPtrs p, const uint8_t* __restrict__ mask, int first,
                                                               uint32_t n_env) {
-    __shared__ float4 s_pd[MAX_PHYS];
-    __shared__ uint32_t s_src[MAX_PHYS];
+    __shared__ float4 s_pd[MAX_PHYS];           // transposed: parameter q at pd_slot(q)
+    __shared__ __align__(16) uint32_t s_src[MAX_PHYS];   // transposed: lane l's quad h at [(h * 32 + l) * 4]
     __shared__ uint32_t s_env[RH_RANGE];
     __shared__ uint32_t s_kk[RH_RANGE];
     __shared__ __align__(16) float s_dr[RH_THREADS / 32][RH_DRAW];
-    __shared__ uint32_t s_n;
+    __shared__ uint32_t s_n, s_next;
     const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
     pdl_wait();   // before any global access (dr_device.cuh)
     constexpr int NWR = RH_THREADS / 32;
-    for (int i = tid; i < c_dc.n_phys; i += RH_THREADS) {
-        s_pd[i] = p.rs_phys[i];
-        s_src[i] = p.rs_src[i];
-    }
+    stage_phys_tables(p, s_pd, s_src, tid, RH_THREADS);
     if (lane == 0) s_dr[wid][RS_OFF_ZERO] = 0.f;
     const bool phys_on = (c_dc.layer_mask & B_PHYS) != 0;
     const int nub = phys_on ? (c_dc.n_phys_u + 3) / 4 : 0;
     const int nnb = phys_on ? (c_dc.n_phys_n + 3) / 4 : 0;
     uint32_t applied = 0;
     for (uint32_t base = blockIdx.x * RH_RANGE; base < n_env; base += gridDim.x * RH_RANGE) {
-        if (tid == 0) s_n = 0u;
+        if (tid == 0) {
+            s_n = 0u;
+            s_next = 0u;
+        }
         __syncthreads();
         for (uint32_t c = wid; c < RH_RANGE / 32; c += NWR) {
             const uint32_t e = base + c * 32u + lane;
@@ -254,9 +289,21 @@ __global__ void __launch_bounds__(RH_THREADS, DR_RH_MINB) reset_kernel(DevPtrs p
         }
         __syncthreads();
         const uint32_t n = s_n;
-        // the record chains first (latency-bound), then the lane-parallel physics rows fill the issue slots
-        for (uint32_t i = tid; i < n; i += RH_THREADS) reset_record_thread(p, s_env[i], s_kk[i], s_pd, s_src);
-        for (uint32_t i = wid; i < n; i += NWR) reset_phys_warp(p, s_env[i], s_kk[i], lane, s_dr[wid], s_pd, s_src, nub, nnb);
+        // the record chains first: part p of env i on thread p * npad + i (whole warps per part, so no
+        // warp mixes code paths); then every warp pulls physics rows from a shared counter, so the
+        // warps without a record chunk start on them at once and the rows spread over all warps
+        const uint32_t npad = (n + 31u) & ~31u;
+        for (uint32_t ti = tid; ti < 3u * npad; ti += RH_THREADS) {
+            const uint32_t part = ti / npad, i = ti - part * npad;
+            if (i < n) reset_record_part(p, s_env[i], s_kk[i], (int)part, s_pd, s_src);
+        }
+        for (;;) {
+            uint32_t i = 0;
+            if (lane == 0) i = atomicAdd(&s_next, 1u);
+            i = __shfl_sync(0xFFFFFFFFu, i, 0);
+            if (i >= n) break;
+            reset_phys_warp(p, s_env[i], s_kk[i], lane, s_dr[wid], s_pd, s_src, nub, nnb);
+        }
         __syncthreads();
     }
     pdl_trigger();
