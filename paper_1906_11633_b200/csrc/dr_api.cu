@@ -482,14 +482,18 @@ int dr_init(const dr_params* params, int64_t n_env, uint64_t seed) {
     const int occ_step = step_max_ctas_per_sm(c->prm.layer_mask);
     const uint32_t units = mode ? (uint32_t)((n_env + LAT_ENVS_PER_CTA - 1) / LAT_ENVS_PER_CTA)
                                 : (uint32_t)((n_env + TILE - 1) / TILE);
-    // Persistent grid, balanced: the tiles (or latency groups) go round-robin over the CTAs, so a
-    // grid of min(units, resident slots) leaves a partial last wave whenever units is not a multiple
-    // of it (131,072 envs = 1,024 tiles on 592 slots: the slowest CTAs run 2 tiles against an average
-    // of 1.73).  Instead take the fewest waves w the resident slots allow and spread the units evenly:
-    // grid = ceil(units / w), every CTA runs w or w - 1 units.
+    // Persistent grid of min(units, resident slots) CTAs, the slots a multiple of the SM count: unit i
+    // runs on CTA i % grid, i.e. on SM i % 148, so every SM gets the same number of units (+-1) even
+    // when the CTAs do not (DR_STEP_BALANCE=1, A/B: the fewest waves, grid = ceil(units / waves) --
+    // equal units per CTA but 3 or 4 CTAs per SM).
     const long long slots = std::min<long long>((long long)c->sm_count * occ_step, (long long)c->max_ctas);
-    const long long waves = ((long long)units + slots - 1) / slots;
-    c->step_grid = (int)(((long long)units + waves - 1) / waves);
+    c->step_grid = (int)std::min<long long>((long long)units, slots);
+    if (const char* bal = std::getenv("DR_STEP_BALANCE")) {
+        if (std::atoi(bal) == 1) {
+            const long long waves = ((long long)units + slots - 1) / slots;
+            c->step_grid = (int)(((long long)units + waves - 1) / waves);
+        }
+    }
     // A/B: persistent grid size (clamped to the default). 1M envs: 592 (default) 4.90e9, 586 4.89e9,
     // 546 4.75e9, 512 4.60e9, 444 4.73e9 env-steps/s
     if (const char* sg = std::getenv("DR_STEP_GRID")) {
