@@ -21,7 +21,7 @@ using namespace dr;
 namespace {
 
 struct Layout {
-    size_t rec, st, phys, t_tab, rs_phys, rs_src, dec,
+    size_t rec, st, phys, t_tab, rs_phys, rs_src, dec, sync,
         stats, ctl, total;
     uint64_t pitch;
 };
@@ -47,7 +47,8 @@ Layout make_layout(int64_t n_env, int n_phys, int max_ctas) {
     L.rs_src = take(MAX_PHYS * 4);
     L.dec = take(512 * 8);
     L.stats = take(N_STAT_SLOTS * N_STATS * 8);
-    L.ctl = take(4 * 8);
+    L.ctl = take(8 * 8);
+    L.sync = take((N_STAT_SLOTS + (size_t)max_ctas) * 4);   // done | cta_done
     L.total = off;
     return L;
 }
@@ -69,6 +70,8 @@ struct Ctx {
     int step_mode = 0;
     uint64_t t_host = 0;
     uint64_t launches = 0;
+    bool chain_enabled = true;   // DR_CHAIN
+    bool chain_next = false;     // the last library launch on the stream was a step kernel
     // dr_step_host: double-buffered device I/O, H2D / D2H streams and their events
     float* io = nullptr;
     size_t io_bytes = 0;
@@ -454,6 +457,8 @@ int dr_init(const dr_params* params, int64_t n_env, uint64_t seed) {
     P.dec_tab = reinterpret_cast<double*>(c->ws + L.dec);
     P.stats = reinterpret_cast<double*>(c->ws + L.stats);
     P.ctl = reinterpret_cast<unsigned long long*>(c->ws + L.ctl);
+    P.done = reinterpret_cast<uint32_t*>(c->ws + L.sync);
+    P.cta_done = P.done + N_STAT_SLOTS;
     c->internal_stats = P.stats;
 
     cudaStream_t s = c->stream;
@@ -465,7 +470,7 @@ int dr_init(const dr_params* params, int64_t n_env, uint64_t seed) {
     const char* what = "";
     if ((e = upload_params(c, c->prm, &what)) != cudaSuccess) return bail(e, what);
     if ((e = cudaMemsetAsync(P.stats, 0, N_STAT_SLOTS * N_STATS * 8, s)) != cudaSuccess) return bail(e, "memset stats");
-    if ((e = cudaMemsetAsync(P.ctl, 0, 4 * 8, s)) != cudaSuccess) return bail(e, "memset ctl");
+    if ((e = cudaMemsetAsync(P.ctl, 0, 8 * 8, s)) != cudaSuccess) return bail(e, "memset ctl");
     // state planes start zeroed so that never-reset lanes of a partial tile stay defined
     if ((e = cudaMemsetAsync(P.st, 0, (size_t)ST_PLANES * L.pitch * 4, s)) != cudaSuccess) return bail(e, "memset st");
     if ((e = cudaStreamSynchronize(s)) != cudaSuccess) return bail(e, "sync init");
@@ -503,11 +508,19 @@ int dr_init(const dr_params* params, int64_t n_env, uint64_t seed) {
     const char* pdl = std::getenv("DR_PDL");
     set_pdl(!(pdl && std::atoi(pdl) == 0));
     c->reset_grid = reset_grid_for((uint32_t)n_env, c->sm_count);
+    // chained steps (dr_step.cuh): back-to-back dr_step calls overlap at their boundary; DR_CHAIN=0
+    // (A/B) makes every step wait for its predecessor to complete
+    const char* ch = std::getenv("DR_CHAIN");
+    c->chain_enabled = !(ch && std::atoi(ch) == 0);
+    c->chain_next = false;
 
-    // episode 0 for every env (sampled at the beginning of every episode)
+    // the step protocol at t = 0, then episode 0 for every env (sampled at the
+    // beginning of every episode)
+    if ((e = launch_sync_init(P, 0, c->step_grid, c->max_ctas, s)) != cudaSuccess)
+        return bail(e, "sync_init_kernel");
     if ((e = launch_reset(P, nullptr, true, (uint32_t)n_env, c->reset_grid, s)) != cudaSuccess) return bail(e, "reset_kernel");
-    c->launches = 1;
-    ++g_total_launches;
+    c->launches = 2;
+    g_total_launches += 2;
     g_ctx = c;
     g_err[0] = 0;
     return DR_OK;
@@ -544,6 +557,7 @@ int dr_reset(const uint8_t* env_mask) {
     if (g_sticky) return fail(DR_ECUDA, "sticky CUDA error: %s", g_err);
     cudaError_t e = launch_reset(c->p, env_mask, false, (uint32_t)c->n_env, c->reset_grid, c->stream);
     if (e != cudaSuccess) return cuda_fail(e, "reset_kernel");
+    c->chain_next = false;   // the next step must wait for the reset to complete
     c->launches++;
     ++g_total_launches;
     return DR_OK;
@@ -565,9 +579,11 @@ static int step_common(const float* actions, const float* raw_obs, float* out_ac
         if (!aligned16(ptrs[i])) return fail(DR_EINVAL, "%s: not 16-byte aligned", names[i]);
     }
     set_step_mode(c->step_mode);
+    const int chain = (c->chain_enabled && c->chain_next) ? 1 : 0;
     cudaError_t e = launch_step(c->p, c->prm.layer_mask, actions, raw_obs, out_actions, out_obs, out_dt, out_force,
-                                out_sub, (uint32_t)c->n_env, c->step_grid, c->stream);
+                                out_sub, (uint32_t)c->n_env, c->step_grid, chain, c->stream);
     if (e != cudaSuccess) return cuda_fail(e, "step_kernel");
+    c->chain_next = true;
     c->t_host++;
     c->launches++;
     ++g_total_launches;
@@ -731,11 +747,14 @@ uint64_t dr_step_index_sync(void) {
 int dr_set_step_index(uint64_t t) {
     Ctx* c = g_ctx;
     if (!c) return fail(DR_ENOTINIT, "dr_set_step_index: no context");
-    unsigned long long v = t;
-    CK(cudaMemcpyAsync(c->p.ctl, &v, 8, cudaMemcpyHostToDevice, c->stream));
     CK(cudaMemsetAsync(c->p.stats, 0, N_STAT_SLOTS * N_STATS * 8, c->stream));   // restart the stats ring
+    cudaError_t e = launch_sync_init(c->p, t, c->step_grid, c->max_ctas, c->stream);
+    if (e != cudaSuccess) return cuda_fail(e, "sync_init_kernel");
+    c->launches++;
+    ++g_total_launches;
     CK(cudaStreamSynchronize(c->stream));
     c->t_host = t;
+    c->chain_next = false;
     return DR_OK;
 }
 

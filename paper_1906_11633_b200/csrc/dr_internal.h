@@ -135,7 +135,9 @@ struct DevPtrs {
     uint32_t* rs_src;         // [256] physics draw-buffer offset | RS_EXP
     double* dec_tab;          // [512]: 0.99^j (j < 256), then 0.99^(256 i)
     double* stats;            // [N_STAT_SLOTS][N_STATS] (internal or caller-owned)
-    unsigned long long* ctl;  // [0] = step t, [1] = CTAs started counter, [2] = resets pending
+    unsigned long long* ctl;  // [0] = step t (host-visible), [2] = resets pending, [4] = CTA-start tickets
+    uint32_t* done;           // [N_STAT_SLOTS]: CTAs of the step that owns stats slot i that finished their atomics
+    uint32_t* cta_done;       // [max CTAs]: steps whose CTA of this index has finished (dr_step.cuh)
     const uint8_t* occl_in;   // simulator occlusion bits per env (dr_set_occlusion_input) or NULL
 };
 
@@ -149,7 +151,9 @@ cudaError_t launch_reset(const DevPtrs& p, const uint8_t* mask, bool first, uint
                          int grid, cudaStream_t s);
 cudaError_t launch_step(const DevPtrs& p, uint32_t layer_mask, const float* actions,
                         const float* raw_obs, float* out_actions, float* out_obs, float* out_dt,
-                        float* out_force, float* out_sub, uint32_t n_env, int grid, cudaStream_t s);
+                        float* out_force, float* out_sub, uint32_t n_env, int grid, int chain, cudaStream_t s);
+// (re)arm the step protocol at step index t for a step grid of `grid` CTAs (dr_init, dr_set_step_index)
+cudaError_t launch_sync_init(const DevPtrs& p, uint64_t t, int grid, int max_ctas, cudaStream_t s);
 cudaError_t launch_export(const DevPtrs& p, void* dst, uint32_t lo, uint32_t hi, cudaStream_t s);
 cudaError_t launch_import(const DevPtrs& p, const void* src, uint32_t lo, uint32_t hi, cudaStream_t s);
 cudaError_t launch_debug_philox(uint32_t n_env, uint32_t dom, uint32_t ch, uint32_t blk, uint32_t* out,

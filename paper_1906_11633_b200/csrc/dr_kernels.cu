@@ -166,7 +166,7 @@ int reset_grid_for(uint32_t n_env, int sm_count) {
 static constexpr uint32_t MASK_FULL = 0xFFu;  // PHYS does not affect the step
 static constexpr uint32_t MASK_CFG2 = B_TIMING | B_ACT_NOISE | B_BACKLASH | B_OBS_NOISE;
 
-typedef void (*StepFn)(const DevPtrs, const float*, const float*, float*, float*, float*, float*, float*, uint32_t);
+typedef void (*StepFn)(const DevPtrs, const float*, const float*, float*, float*, float*, float*, float*, uint32_t, int);
 
 static StepFn step_fn_warp(uint32_t m) {
     if (m == MASK_FULL) return step_kernel_warp<MASK_FULL>;
@@ -212,9 +212,27 @@ int step_max_ctas_per_sm(uint32_t layer_mask) {
 
 cudaError_t launch_step(const DevPtrs& p, uint32_t layer_mask, const float* actions, const float* raw_obs,
                         float* out_actions, float* out_obs, float* out_dt, float* out_force, float* out_sub,
-                        uint32_t n_env, int grid, cudaStream_t s) {
+                        uint32_t n_env, int grid, int chain, cudaStream_t s) {
     return launch_k(step_fn(layer_mask), grid, step_threads(), step_dyn_smem(), s, p, actions, raw_obs, out_actions,
-                    out_obs, out_dt, out_force, out_sub, n_env);
+                    out_obs, out_dt, out_force, out_sub, n_env, chain);
+}
+
+__global__ void sync_init_kernel(DevPtrs p, unsigned long long t, uint32_t grid, uint32_t max_ctas) {
+    const uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
+    // the slot of step t starts cleared and empty (as if step t - 1 had prepared it); every other
+    // slot's previous owner counts as done
+    if (i < N_STAT_SLOTS) p.done[i] = (i == (uint32_t)(t % N_STAT_SLOTS)) ? 0u : grid;
+    if (i < max_ctas) p.cta_done[i] = (uint32_t)t;     // steps < t finished
+    if (i == 0) {
+        p.ctl[0] = t;
+        p.ctl[4] = t * grid;   // the first ticket of step t
+    }
+}
+
+cudaError_t launch_sync_init(const DevPtrs& p, uint64_t t, int grid, int max_ctas, cudaStream_t s) {
+    const uint32_t n = std::max<uint32_t>((uint32_t)max_ctas, (uint32_t)N_STAT_SLOTS);
+    sync_init_kernel<<<(n + 255) / 256, 256, 0, s>>>(p, (unsigned long long)t, (uint32_t)grid, (uint32_t)max_ctas);
+    return cudaGetLastError();
 }
 
 cudaError_t launch_debug_philox(uint32_t n_env, uint32_t dom, uint32_t ch, uint32_t blk, uint32_t* out, cudaStream_t s) {

@@ -96,6 +96,14 @@ __device__ __forceinline__ float4 ringh(const uint32_t* blk, int tid, int h) {
 }
 __device__ __forceinline__ float q4(const float4 v, int c) { return c == 0 ? v.x : (c == 1 ? v.y : (c == 2 ? v.z : v.w)); }
 
+__device__ __forceinline__ unsigned ld_acquire_u32(const uint32_t* q) {
+    unsigned v;
+    asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(q) : "memory");
+    return v;
+}
+__device__ __forceinline__ void st_release_u32(uint32_t* q, unsigned v) {
+    asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(q), "r"(v) : "memory");
+}
 // Warp-cooperative ring: a warp fills its 32-env column segment of a slot with 16-byte cp.async.cg
 // (L1 bypass).  State planes: one instruction moves 4 planes x 128 B (lane l: plane l >> 3, bytes
 // 16 (l & 7)).  Record groups: two instructions, each moving the 32-byte groups of 16 envs (512
@@ -679,41 +687,58 @@ __device__ __forceinline__ void store_tile(uint32_t e0, uint32_t cnt, int tid, c
     }
 }
 
-// ---- step index + stats protocol (no grid-wide tail) ----------------------------------------
-// step_begin: thread 0 reads the step index t and counts its CTA in with an acq_rel atomic; the
-// last CTA to start advances ctl[0] to t + 1 (every CTA read t before counting in) and re-arms the
-// counter.  CTA 0 also clears stats slot (t + 1) % 4 for the next step (its all-reduce, from step
-// t - 3, finished before this step was enqueued: parallel.StatsReducer) and moves the pending reset
-// count into slot t % 4.  At the end every CTA adds its reduced partials into slot t % 4 with fp64
-// atomics -- counts are small integers and the moment sums are rounded per CTA to multiples of a
-// host-chosen power of two, so every partial total is exact and the slot does not depend on the
-// order the atomics land in (deterministic, and identical to a fixed-order sum of the rounded CTA
-// sums).  No fence, no last-CTA pass: the kernel ends when its last tile is stored.
-__device__ __forceinline__ uint32_t step_begin(const DevPtrs& p, uint32_t* s_t) {
-    pdl_wait();   // before any global access (dr_device.cuh)
+// ---- step index + stats protocol ---------------------------------------------------------
+// Every CTA of every step kernel takes a ticket (one atomic on ctl[4]); step t owns the tickets
+// [t G, (t + 1) G), G the context's fixed grid, so t = ticket / G.  A CTA takes its ticket before
+// it lets the next step launch (griddepcontrol.launch_dependents), and the ticket atomic's result
+// is consumed first, so every ticket of step t precedes every ticket of step t + 1 in the atomic's
+// coherence order -- no grid-wide barrier and no wait on the previous grid are needed to know t.
+// The last CTA of step t publishes t + 1 in ctl[0] (dr_step_index_sync).
+// Stats: step t accumulates into slot t % 4.  Its first CTA prepares slot (t + 1) % 4 for step
+// t + 1: it waits until every CTA of step t - 3 (the slot's previous owner) has counted itself in
+// done[(t + 1) % 4] after its atomics, clears the slot and re-arms the counter, moves the pending
+// reset count into slot t % 4, and only then lets the next step launch.  At the end every CTA adds
+// its reduced partials into slot t % 4 with fp64 atomics -- counts are small integers and the moment
+// sums are rounded per CTA to multiples of a host-chosen power of two, so every partial total is
+// exact and the slot does not depend on the order the atomics land in -- then counts itself done.
+// chain = 1 (the previous launch on the stream was a step kernel of this context): no
+// griddepcontrol.wait -- CTA c works on tiles c, c + G, ... like CTA c of the previous step, so it
+// starts as soon as that CTA has finished and published its stores (cta_done[c]), while the
+// previous step's other CTAs may still run: consecutive steps overlap at their boundary (a CTA
+// that starts early spins in a slot a finished CTA freed); chain = 0 (after a reset, dr_init or
+// dr_set_step_index): wait for the previous grid to complete.  Both step kernels chain (the latency
+// kernel's CTA c works on 32-env groups c, c + G, ... every step).
+__device__ __forceinline__ uint32_t step_begin(const DevPtrs& p, uint32_t* s_t, int chain) {
+    if (!chain) pdl_wait();   // before any global access (dr_device.cuh)
     if (threadIdx.x == 0) {
-        const uint32_t t = (uint32_t)*(volatile unsigned long long*)&p.ctl[0];
-        unsigned long long prev;
-        asm volatile("atom.acq_rel.gpu.global.add.u64 %0, [%1], 1;" : "=l"(prev) : "l"(&p.ctl[1]) : "memory");
-        if (prev == (unsigned long long)gridDim.x - 1ull) {
-            p.ctl[1] = 0ull;
-            *(volatile unsigned long long*)&p.ctl[0] = (unsigned long long)t + 1ull;
-        }
-        if (blockIdx.x == 0) {
-            double* nxt = p.stats + ((t + 1u) % N_STAT_SLOTS) * N_STATS;
+        const unsigned long long ticket = atomicAdd(&p.ctl[4], 1ull);
+        const uint32_t t = (uint32_t)(ticket / gridDim.x);
+        const uint32_t k = (uint32_t)(ticket - (unsigned long long)t * gridDim.x);
+        if (k == 0) {
+            const uint32_t nslot = (t + 1u) % N_STAT_SLOTS;
+            while (ld_acquire_u32(p.done + nslot) != gridDim.x) __nanosleep(128);   // step t - 3 is done with it
+            double* nxt = p.stats + nslot * N_STATS;
             for (int i = 0; i < N_STATS; ++i) nxt[i] = 0.0;
+            p.done[nslot] = 0u;
             p.stats[(t % N_STAT_SLOTS) * N_STATS + 10] = (double)atomicExch(&p.ctl[2], 0ull);   // resets
+            __threadfence();
         }
+        if (k == gridDim.x - 1u)
+            asm volatile("st.release.gpu.global.u64 [%0], %1;" ::"l"(&p.ctl[0]), "l"((unsigned long long)t + 1ull) : "memory");
+        // chained: this CTA works on the same tiles as the same-index CTA of step t - 1 (fixed grid,
+        // tile i on CTA i % G); start once that CTA has finished (its state stores published)
+        if (chain)
+            while (ld_acquire_u32(p.cta_done + blockIdx.x) != t) __nanosleep(64);
         *s_t = t;
     }
     __syncthreads();
+    if (chain) pdl_trigger();   // ticket taken (and, for the first CTA, the next slot prepared)
     return *s_t;
 }
-
 template <uint32_t L, int NT = STEP_THREADS>
 __device__ __forceinline__ void reduce_stats(const DevPtrs& p, const Acc& acc, uint32_t my_envs, uint32_t t,
                                              double* s_red) {
-    pdl_trigger();   // this CTA's tiles are issued: the next step may launch (dr_device.cuh)
+    pdl_trigger();   // (unchained launches) this CTA's tiles are issued: the next step may launch
     const int tid = threadIdx.x;
     const int lane = tid & 31, wid = tid >> 5;
     constexpr int NW = NT / 32;
@@ -754,6 +779,14 @@ __device__ __forceinline__ void reduce_stats(const DevPtrs& p, const Acc& acc, u
         if (tid >= 16) sum = rint(sum * c_dc.mq_scale[tid - 16]) * c_dc.mq_inv[tid - 16];
         if (sum != 0.0) atomicAdd(p.stats + (t % N_STAT_SLOTS) * N_STATS + tid, sum);
     }
+    __syncthreads();
+    if (tid == 0) {
+        __threadfence();
+        atomicAdd(p.done + (t % N_STAT_SLOTS), 1u);   // this CTA's atomics into slot t % 4 are in
+        // publish: the same-index CTA of step t + 1 (same tiles) may start; since it waited for this
+        // one, a step never completes before its predecessor, so stream order still means "all done"
+        st_release_u32(p.cta_done + blockIdx.x, t + 1u);
+    }
 }
 
 __device__ __forceinline__ void acc_zero(Acc& acc) {
@@ -770,7 +803,7 @@ template <uint32_t L>
 __global__ void __launch_bounds__(STEP_THREADS, STEP_MIN_CTAS)
     step_kernel_warp(const DevPtrs p, const float* __restrict__ actions, const float* __restrict__ raw_obs,
                      float* __restrict__ out_actions, float* __restrict__ out_obs, float* __restrict__ out_dt,
-                     float* __restrict__ out_force, float* __restrict__ out_sub, uint32_t n_env) {
+                     float* __restrict__ out_force, float* __restrict__ out_sub, uint32_t n_env, int chain) {
     __shared__ __align__(16) float s_act[TILE * N_ACT];
     __shared__ __align__(16) float s_obs[TILE * OBS_IN];
     __shared__ __align__(16) float s_dt[TILE * N_SUB];
@@ -778,7 +811,7 @@ __global__ void __launch_bounds__(STEP_THREADS, STEP_MIN_CTAS)
 
     const int tid = threadIdx.x, lane = tid & 31, wcol = tid & ~31;
     __shared__ uint32_t s_tstep;
-    const uint32_t t = step_begin(p, &s_tstep);
+    const uint32_t t = step_begin(p, &s_tstep, chain);
     const uint32_t n_tiles = (n_env + TILE - 1) / TILE;
     Acc acc;
     acc_zero(acc);

@@ -34,7 +34,7 @@ __global__ void __launch_bounds__(LAT_THREADS, DR_LAT_MIN_CTAS) step_kernel_lat(
                                                                float* __restrict__ out_actions,
                                                                float* __restrict__ out_obs, float* __restrict__ out_dt,
                                                                float* __restrict__ out_force, float* __restrict__ out_sub,
-                                                               uint32_t n_env) {
+                                                               uint32_t n_env, int chain) {
     __shared__ float s_dtenv[LAT_ENVS];
     __shared__ float s_dtk[N_SUB][LAT_ENVS];
     __shared__ uint32_t s_wd[6][LAT_ENVS];   // step words 10-15
@@ -42,7 +42,7 @@ __global__ void __launch_bounds__(LAT_THREADS, DR_LAT_MIN_CTAS) step_kernel_lat(
 
     const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
     __shared__ uint32_t s_tstep;
-    const uint32_t t = step_begin(p, &s_tstep);
+    const uint32_t t = step_begin(p, &s_tstep, chain);   // CTA g works on groups g, g + G, ... every step
     constexpr size_t P = PLANE;
     constexpr bool kHold = (L == RUNTIME_MASK) || (L & (B_DROPOUT | B_OCCLUSION));
     const bool hold_layers = on<L>(B_DROPOUT) || on<L>(B_OCCLUSION);
