@@ -125,7 +125,19 @@ int orc_scene_draw(const orc_vision_params* p, uint64_t seed, uint64_t batch, in
  *      (contrast about the normalized mean, which is 0) [V6];
  *   3. "per-pixel Gaussian noise is added" (Table: +-10 %): + s z, z ~ N(0, 1) i.i.d. per pixel
  *      and channel, s ~ U[noise lo, noise hi] per image (default 0.1, 10 % of the unit std) [V6].
- * Element e (row-major H, W, C) takes normal e % 4 of Philox block e / 4 of channel IMG_NOISE. */
+ * Noise draws (vision RNG map v2, DESIGN.md "Vision readings" V7): one 32-bit word gives one Box-Muller
+ * pair -- the radius from its top 20 bits, U20 = ((x >> 12) + 1/2) 2^-20, the angle from its low 12
+ * bits, A12 = ((x & 0xFFF) + 1/2) 2^-12 -- so element e (row-major H, W, C) takes normal e % 2
+ * (cos, sin) of the pair of word (e % 8) / 2 of Philox block e / 8 of channel IMG_NOISE. */
+static void noise_pair(uint32_t x, double* z0, double* z1)
+{
+    double u = ((double)(x >> 12) + 0.5) * (1.0 / 1048576.0);
+    double a = ((double)(x & 0xFFFu) + 0.5) * (1.0 / 4096.0);
+    double r = sqrt(-2.0 * log(u));
+    double th = 2.0 * M_PI * a;
+    *z0 = r * cos(th);
+    *z1 = r * sin(th);
+}
 static void augment_one(const orc_vision_params* p, uint64_t seed, uint64_t batch, int64_t g, const uint8_t* x,
                         int64_t E, double* out, double* st)
 {
@@ -143,9 +155,8 @@ static void augment_one(const orc_vision_params* p, uint64_t seed, uint64_t batc
         double xh = ((double)x[e] - mu) / (sd > p->std_floor ? sd : p->std_floor);   /* 1 */
         double z0, z1, z;
         xh = f * xh;                                                                 /* 2 */
-        block(seed, g, batch, CH_IMG_NOISE, (uint32_t)(e / 4), w);
-        if ((e % 4) < 2) orc_normal_pair(w[0], w[1], &z0, &z1);
-        else orc_normal_pair(w[2], w[3], &z0, &z1);
+        block(seed, g, batch, CH_IMG_NOISE, (uint32_t)(e / 8), w);
+        noise_pair(w[(e % 8) / 2], &z0, &z1);
         z = (e % 2 == 0) ? z0 : z1;
         out[e] = xh + s * z;                                                         /* 3 */
     }

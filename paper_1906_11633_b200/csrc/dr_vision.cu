@@ -30,11 +30,14 @@ enum : uint32_t { CH_POSE = 0x401, CH_IMG_PARAM = 0x201, CH_IMG_NOISE = 0x202, C
                   CH_SCENE_LIGHT = 0x303 };
 
 #ifndef DR_IMG_THREADS
-#define DR_IMG_THREADS 256   // A/B (us per 192-image batch): 128 41.1, 256 40.2, 512 43.3
+#define DR_IMG_THREADS 128   // A/B (us per 192-image batch, map v2): 128 35.9, 256 36.7, 512 49.5 (map v1: 41.1, 40.2, 43.3)
 #endif
 constexpr int IMG_THREADS = DR_IMG_THREADS;
 #ifndef DR_IMG_ILP
-#define DR_IMG_ILP 4   // A/B: 4 measured 40.55 vs 40.97 us per 192-image batch for 2 (three alternating runs)
+#ifndef DR_IMG_PROBE
+#define DR_IMG_PROBE 0   // roofline probes (A/B builds only): 1 = no noise draws, 2 = no output stores
+#endif
+#define DR_IMG_ILP 1   // A/B (8-element groups per iteration): 1 36.7, 2 40.6 us per 192-image batch
 #endif
 constexpr int IMG_ILP = DR_IMG_ILP;
 constexpr uint32_t IMG_SLICE_MAX = 200 * 1024;
@@ -98,32 +101,48 @@ __device__ __forceinline__ void tma_bulk(void* dst, const void* src, uint32_t by
                  : "memory");
 }
 
-// image-noise Box-Muller (A/B): 0 = MUFU sin/cos (default), 1 = polynomial angle (MUFU only for lg2 /
-// sqrt) -- measured 41.9 vs 49.9 us per 192-image batch: the kernel is issue-bound, not MUFU-bound
-#ifndef DR_IMG_POLY
-#define DR_IMG_POLY 0
+// Image-noise normals (vision RNG map v2, V7): one Philox block gives 8 normals -- word w
+// is one Box-Muller pair with the radius from its top 20 bits and the angle from its low 12 bits --
+// so element e takes normal e % 2 of the pair of word (e % 8) / 2 of block e / 8 (map v1 drew one
+// block per 4 elements: Philox was ~40 % of the kernel's instructions).
+// nz_pair returns s z0 + k, s z1 + k (the noise std s and the per-image constant k folded in):
+//   -2 ln U (s^2 folded into the constants): MUFU.LG2 except for 1 - U < 2^-6, where the series
+//   v (2 + v (1 + 2v/3)) keeps the tiny radius accurate (the fast pair of dr_math.cuh); U and 1 - U
+//   are exact, built from the word's bits; r s from MUFU.SQRT;
+//   the angle 2 pi (A - 1/2) in one FFMA from the 12-bit integer, then MUFU.SIN / MUFU.COS
+//   (cos(t - pi) = -cos t and sin(t - pi) = -sin t: the sign goes into the FFMA with k).
+//   A/B: a quarter-wave (cos, sin) table in shared memory instead of MUFU.SIN / COS measured slower
+//   (41.4 vs 35.9 us per 192-image batch: the random table reads conflict).
+struct NzConst {
+    float s2_lg;    // -2 ln(2) s^2
+    float s2_c2, s2_c1, s2_c0;   // s^2 (2/3), s^2, 2 s^2
+    float kq;
+};
+#ifndef DR_IMG_SINCOS
+#define DR_IMG_SINCOS 0   // A/B: 0 = MUFU.SIN / COS, 1 = FMA-pipe polynomial, 2 = polynomial for pairs 2, 3 only
 #endif
-__device__ __forceinline__ void img_bm(uint32_t x, uint32_t y, float& z0, float& z1) {
-#if DR_IMG_POLY
-    box_muller_fast_poly(x, y, z0, z1);
-#else
-    box_muller_fast(x, y, z0, z1);
-#endif
-}
-// the same pair times sf, folded into the radius (one multiply per pair instead of per element)
-__device__ __forceinline__ void img_bm_scaled(uint32_t x, uint32_t y, float sf, float& z0, float& z1) {
-    const float nr = -sqrt_approx(m2ln_fast(x)) * sf;
+template <bool kPoly>
+__device__ __forceinline__ void nz_pair(uint32_t x, const NzConst& c, float& z0, float& z1) {
+    const float u = __uint_as_float(0x3F800004u | ((x >> 12) << 3)) - 1.0f;           // (k + 1/2) 2^-20, exact
+    const float v = __uint_as_float(0x3F800004u | ((~x >> 12) << 3)) - 1.0f;          // 1 - u, exact
+    const float series = v * fmaf(fmaf(v, c.s2_c2, c.s2_c1), v, c.s2_c0);
+    const float lg = lg2_approx(u) * c.s2_lg;
+    const float rs = sqrt_approx((v < 0.015625f) ? series : lg);                     // s sqrt(-2 ln u)
     float sn, cs;
-    __sincosf(sfu_angle(y), &sn, &cs);
-    z0 = nr * cs;
-    z1 = nr * sn;
+    if constexpr (kPoly) {   // (sin, cos)(2 pi A) on the FMA pipe, A = (k + 1/2) 2^-12 exact
+        sincos_2pi(fmaf((float)(x & 0xFFFu), 2.44140625e-04f, 1.220703125e-04f), sn, cs);
+        z0 = fmaf(rs, cs, c.kq);
+        z1 = fmaf(rs, sn, c.kq);
+    } else {                 // MUFU: the angle 2 pi (A - 1/2) in one FFMA from the 12-bit integer
+        const float ang = fmaf((float)(x & 0xFFFu), 1.53398078788564122e-03f, -3.14082566319585e+00f);
+        __sincosf(ang, &sn, &cs);
+        z0 = fmaf(-rs, cs, c.kq);
+        z1 = fmaf(-rs, sn, c.kq);
+    }
 }
-
-// the 4 normals of noise block b of image g: element 4b + k takes normal k
-__device__ __forceinline__ void noise4(const ImgArgs& a, uint32_t g, uint32_t b, float z[4]) {
-    const uint4 w = philox_k(g, a.batch, CH_IMG_NOISE, b, a.keys);
-    img_bm(w.x, w.y, z[0], z[1]);   // s = 0.1 scales its <= ~1e-6 normal error
-    img_bm(w.z, w.w, z[2], z[3]);
+template <int Q>
+__device__ __forceinline__ void nz_pair_q(uint32_t x, const NzConst& c, float& z0, float& z1) {
+    nz_pair<(DR_IMG_SINCOS == 1) || (DR_IMG_SINCOS == 2 && Q >= 2)>(x, c, z0, z1);
 }
 
 __global__ void __launch_bounds__(IMG_THREADS) image_augment_kernel(const ImgArgs a) {
@@ -209,63 +228,81 @@ __global__ void __launch_bounds__(IMG_THREADS) image_augment_kernel(const ImgArg
     const double s = a.noise_lo + a.noise_range * (double)uni(pw.y);
     const float scale = (float)(f / (sd > a.std_floor ? sd : a.std_floor));
     const float mu_hi = (float)mean, mu_lo = (float)(mean - (double)mu_hi);   // x - mu_hi is exact
-    const float sf = (float)s;
     // out = (x - mu_hi) * scale + (s z - mu_lo scale): the remainder term k = -mu_lo * scale is one
     // per-image constant (|mu_lo| <= 2^-24 * 128 and scale <= ~2e5 for a non-constant u8 image, so
-    // |k| < 1.5; a constant image has mu_lo = 0), and s is folded into the Box-Muller radius
-    const float kq = (float)(-(double)mu_lo * (double)scale);
+    // |k| < 1.5; a constant image has mu_lo = 0); s and k are folded into the noise pair (nz_pair).
+    // Every element of every image takes the same expression, whatever the slice / cluster size.
+    NzConst nc;
+    {
+        const double s2 = s * s;
+        nc.s2_lg = (float)(-1.38629436111989061883 * s2);
+        nc.s2_c2 = (float)(0.666666666666666667 * s2);
+        nc.s2_c1 = (float)s2;
+        nc.s2_c0 = (float)(2.0 * s2);
+        nc.kq = (float)(-(double)mu_lo * (double)scale);
+    }
     if (r == 0 && tid == 0 && a.img_stats)
-        reinterpret_cast<float4*>(a.img_stats)[img] = make_float4((float)mean, (float)sd, (float)f, sf);
+        reinterpret_cast<float4*>(a.img_stats)[img] = make_float4((float)mean, (float)sd, (float)f, (float)s);
 
     float* out = a.out + img * E + lo;
-    const uint32_t b0 = (uint32_t)(lo >> 2);   // lo is a multiple of 16
+    const uint32_t b0 = (uint32_t)(lo >> 3);   // lo is a multiple of 16: 8-element noise blocks
     if (a.aligned) {
-        // IMG_ILP independent 4-element groups per iteration: their Philox chains and Box-Muller
-        // pairs interleave, so each warp has IMG_ILP times the independent instructions in flight
+        // whole 8-element groups: one Philox block, four independent Box-Muller pairs, two float4
+        // streaming stores (IMG_ILP groups per iteration, A/B)
+        const uint2* w8 = reinterpret_cast<const uint2*>(s_img);
         float4* o4 = reinterpret_cast<float4*>(out);
+        const uint32_t n8 = n >> 3;   // n is a multiple of 16 on this path
+        auto group = [&](uint32_t i) {
+#if DR_IMG_PROBE == 1
+            const uint4 w = make_uint4(i, i, i, i);
+#else
+            const uint4 w = philox_k(g, a.batch, CH_IMG_NOISE, b0 + i, a.keys);
+#endif
+            const uint2 x = w8[i];
+            const uint32_t ws[4] = {w.x, w.y, w.z, w.w};
+            float z[8];
+#if DR_IMG_PROBE == 1   // roofline probe (A/B only): no noise draws
+            for (int q = 0; q < 8; ++q) z[q] = nc.kq + (float)(ws[q & 3] & 1u);
+#else
+            nz_pair_q<0>(ws[0], nc, z[0], z[1]);
+            nz_pair_q<1>(ws[1], nc, z[2], z[3]);
+            nz_pair_q<2>(ws[2], nc, z[4], z[5]);
+            nz_pair_q<3>(ws[3], nc, z[6], z[7]);
+#endif
+            float v[8];
+#pragma unroll
+            for (int k = 0; k < 8; ++k) {
+                const uint32_t xb = (k < 4 ? x.x : x.y) >> (8 * (k & 3));
+                v[k] = fmaf((float)(xb & 0xFFu) - mu_hi, scale, z[k]);   // x - mu_hi exact
+            }
+#if DR_IMG_PROBE == 2   // roofline probe (A/B only): no output stores
+            if (v[0] + v[1] + v[2] + v[3] + v[4] + v[5] + v[6] + v[7] == 12345.f) out[0] = 0.f;
+#else
+            // one 256-bit streaming store per group: a warp writes 32 whole sectors (1 KB contiguous)
+            asm volatile("st.global.cs.v8.f32 [%0], {%1, %2, %3, %4, %5, %6, %7, %8};" ::"l"(o4 + 2 * i), "f"(v[0]),
+                         "f"(v[1]), "f"(v[2]), "f"(v[3]), "f"(v[4]), "f"(v[5]), "f"(v[6]), "f"(v[7])
+                         : "memory");
+#endif
+        };
         uint32_t i = tid;
-        for (; i + (IMG_ILP - 1) * IMG_THREADS < n4; i += IMG_ILP * IMG_THREADS) {
-            uint4 w[IMG_ILP];
+        for (; i + (IMG_ILP - 1) * IMG_THREADS < n8; i += IMG_ILP * IMG_THREADS) {
 #pragma unroll
-            for (int u = 0; u < IMG_ILP; ++u) w[u] = philox_k(g, a.batch, CH_IMG_NOISE, b0 + i + u * IMG_THREADS, a.keys);
-#pragma unroll
-            for (int u = 0; u < IMG_ILP; ++u) {
-                const uint32_t x = w4[i + u * IMG_THREADS];
-                float z[4];
-                img_bm_scaled(w[u].x, w[u].y, sf, z[0], z[1]);   // z = s * normal
-                img_bm_scaled(w[u].z, w[u].w, sf, z[2], z[3]);
-                float v[4];
-#pragma unroll
-                for (int k = 0; k < 4; ++k) {
-                    const float d = (float)((x >> (8 * k)) & 0xFFu) - mu_hi;   // exact
-                    v[k] = fmaf(d, scale, z[k] + kq);
-                }
-                __stcs(o4 + i + u * IMG_THREADS, make_float4(v[0], v[1], v[2], v[3]));
-            }
+            for (int u = 0; u < IMG_ILP; ++u) group(i + u * IMG_THREADS);
         }
-        for (; i < n4; i += IMG_THREADS) {
-            const uint32_t x = w4[i];
-            float z[4];
-            noise4(a, g, b0 + i, z);
-            float v[4];
-#pragma unroll
-            for (int k = 0; k < 4; ++k) {
-                const float d = ((float)((x >> (8 * k)) & 0xFFu) - mu_hi) - mu_lo;
-                v[k] = fmaf(d, scale, sf * z[k]);
-            }
-            __stcs(o4 + i, make_float4(v[0], v[1], v[2], v[3]));
-        }
+        for (; i < n8; i += IMG_THREADS) group(i);
     } else {
-        for (uint32_t i = tid; i < (n + 3) / 4; i += IMG_THREADS) {
-            float z[4];
-            noise4(a, g, b0 + i, z);
+        for (uint32_t i = tid; i < (n + 7) / 8; i += IMG_THREADS) {
+            const uint4 w = philox_k(g, a.batch, CH_IMG_NOISE, b0 + i, a.keys);
+            const uint32_t ws[4] = {w.x, w.y, w.z, w.w};
+            float z[8];
+            nz_pair_q<0>(ws[0], nc, z[0], z[1]);
+            nz_pair_q<1>(ws[1], nc, z[2], z[3]);
+            nz_pair_q<2>(ws[2], nc, z[4], z[5]);
+            nz_pair_q<3>(ws[3], nc, z[6], z[7]);
 #pragma unroll
-            for (int k = 0; k < 4; ++k) {
-                const uint32_t e = 4 * i + k;
-                if (e < n) {
-                    const float d = ((float)s_img[e] - mu_hi) - mu_lo;
-                    out[e] = fmaf(d, scale, sf * z[k]);
-                }
+            for (int k = 0; k < 8; ++k) {
+                const uint32_t e = 8 * i + k;
+                if (e < n) out[e] = fmaf((float)s_img[e] - mu_hi, scale, z[k]);
             }
         }
     }

@@ -101,6 +101,19 @@ def test_image_augment_partition_invariance(torch_cuda):
     assert np.array_equal(a, np.concatenate([b1, b2])) and np.array_equal(sa, np.concatenate([s1, s2]))
 
 
+def test_image_augment_batch_size_invariance_paper_shape(torch_cuda):
+    """The paper's batch of 192 images of 200 x 200 x 3 in one call equals three calls of 64 images
+    (image_offset 0, 64, 128) bit for bit: the cluster size K the kernel picks depends on the batch
+    (occupancy), so every element -- also of each slice's last partial group -- takes the same
+    expression whatever K is."""
+    imgs = gen.images(192, 200, 200, 3, seed=11)
+    P = presets.vision_preset()
+    a, sa = _augment_gpu(torch_cuda, P, imgs, 9)
+    parts = [_augment_gpu(torch_cuda, P, imgs[k:k + 64], 9, image_offset=k) for k in (0, 64, 128)]
+    assert np.array_equal(a, np.concatenate([p[0] for p in parts]))
+    assert np.array_equal(sa, np.concatenate([p[1] for p in parts]))
+
+
 def test_image_augment_rejects(torch_cuda):
     from paper_1906_11633_b200 import dr, vision
     torch = torch_cuda
