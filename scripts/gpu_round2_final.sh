@@ -1,0 +1,33 @@
+#!/bin/bash
+# Round-2 evidence in one call: smoke, GPU tests, every bench line (default with cpu_baseline and
+# e2e; cfg2/cfg3/reset/vision; the reference arm), the PCIe probe, the ncu launch list of the
+# default bench and ncu --set full captures of the step, reset and image kernels.  gpurun_out/final_*.
+cd "${GRAFT_REPO_ROOT:-/root/repo}"
+mkdir -p gpurun_out
+O=gpurun_out/r2
+nvidia-smi > ${O}_nvidia-smi.txt 2>&1
+lscpu > ${O}_lscpu.txt 2>&1
+timeout 300 python -c "import __graft_entry__ as g; g.smoke()" > ${O}_smoke.log 2>&1; echo "smoke rc=$?" >> ${O}_smoke.log
+timeout 1500 python -m pytest tests -m gpu -q -rA > ${O}_pytest_gpu.log 2>&1; echo "pytest rc=$?" >> ${O}_pytest_gpu.log
+timeout 900 python bench.py > ${O}_bench_default.log 2>&1
+timeout 600 python bench.py --config cfg2 --steps 5000 --warmup 20 --no-cpu-baseline > ${O}_bench_cfg2.log 2>&1
+timeout 600 python bench.py --config cfg3 --steps 2000 --warmup 20 --no-cpu-baseline > ${O}_bench_cfg3.log 2>&1
+timeout 600 python bench.py --config reset --steps 300 --warmup 10 --no-cpu-baseline > ${O}_bench_reset.log 2>&1
+timeout 600 python bench.py --config vision --steps 500 --warmup 20 --no-cpu-baseline > ${O}_bench_vision.log 2>&1
+timeout 600 python bench.py --impl reference --steps 3 --warmup 1 > ${O}_bench_reference.log 2>&1
+for n in 524288 262144 131072; do
+  timeout 600 python bench.py --n-env $n --steps 4000 --warmup 20 --no-cpu-baseline > ${O}_bench_n$n.log 2>&1
+done
+timeout 300 python scripts/pcie_probe.py > ${O}_pcie.log 2>&1
+timeout 600 ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum --clock-control none \
+    -k regex:"step_kernel|reset_kernel|augment|scene|pose|image_" -c 40 --csv --log-file ${O}_launches.csv \
+    python bench.py --profile --steps 30 --warmup 5 --no-cpu-baseline > ${O}_ncu_launch.log 2>&1
+timeout 900 ncu --set full --clock-control none --import-source on -k regex:step_kernel -s 3 -c 1 -o ${O}_prof_step -f \
+    python bench.py --profile --steps 6 --warmup 3 --no-cpu-baseline > ${O}_ncu_step.log 2>&1
+timeout 900 ncu --set full --clock-control none --import-source on -k regex:reset_kernel -s 3 -c 1 -o ${O}_prof_reset -f \
+    python bench.py --config reset --profile --steps 6 --warmup 3 --no-cpu-baseline > ${O}_ncu_reset.log 2>&1
+timeout 900 ncu --set full --clock-control none --import-source on -k regex:image_augment -s 3 -c 1 -o ${O}_prof_vision -f \
+    python bench.py --config vision --profile --steps 6 --warmup 3 --no-cpu-baseline > ${O}_ncu_vision.log 2>&1
+bash scripts/gpu_sanitize.sh > ${O}_sanitize.log 2>&1
+for t in memcheck racecheck synccheck initcheck; do cp gpurun_out/sanitize_$t.log ${O}_sanitize_$t.log 2>/dev/null; done
+echo done
