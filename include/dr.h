@@ -271,6 +271,14 @@ uint64_t dr_total_kernel_launches(void);
  * (global id of env e, domain, channel, block) under the context's seed.  out_dev: device
  * uint32 [n_env][4].  Asynchronous.  Lets tests check the RNG words bit-exactly. */
 int      dr_debug_philox(uint32_t domain, uint32_t channel, uint32_t block, uint32_t* out_dev);
+/* Test hook (no context needed): out_dev[i] = Philox4x32-10(counter ctr_dev[i][0..3], key
+ * key_dev[i][0..1]) computed by the same device round function every kernel uses (Salmon et al.,
+ * SC'11; the RNG of DESIGN.md "RNG conventions"), round keys built from the key in registers.
+ * ctr_dev / out_dev: device uint32 [n][4], 16-byte aligned; key_dev: device uint32 [n][2], 8-byte
+ * aligned; n <= 2^32.  Asynchronous on `stream` (cudaStream_t, NULL = legacy default stream).
+ * Lets tests check the device RNG against cuRAND's curand_Philox4x32_10 on arbitrary pairs. */
+int      dr_debug_philox_keyed(const uint32_t* ctr_dev, const uint32_t* key_dev, uint32_t* out_dev, uint64_t n,
+                               void* stream);
 uint32_t dr_abi_version(void);
 
 #ifdef __cplusplus

@@ -831,6 +831,20 @@ int dr_debug_philox(uint32_t domain, uint32_t channel, uint32_t block, uint32_t*
     return DR_OK;
 }
 
+int dr_debug_philox_keyed(const uint32_t* ctr_dev, const uint32_t* key_dev, uint32_t* out_dev, uint64_t n,
+                          void* stream) {
+    if (n == 0) return DR_OK;
+    if (!ctr_dev || !key_dev || !out_dev) return fail(DR_EINVAL, "dr_debug_philox_keyed: NULL pointer");
+    if (!aligned16(ctr_dev) || !aligned16(out_dev) || ((uintptr_t)key_dev & 7u))
+        return fail(DR_EINVAL, "dr_debug_philox_keyed: ctr/out need 16-byte, key 8-byte alignment");
+    if (n > (1ull << 32)) return fail(DR_EINVAL, "dr_debug_philox_keyed: n > 2^32");
+    cudaError_t e = launch_debug_philox_keyed(ctr_dev, key_dev, out_dev, (unsigned long long)n,
+                                              static_cast<cudaStream_t>(stream));
+    if (e != cudaSuccess) return cuda_fail(e, "debug_philox_keyed_kernel");
+    ++g_total_launches;
+    return DR_OK;
+}
+
 }  // extern "C"
 
 static_assert(sizeof(dr_env_state) == 168 * 4, "dr_env_state must be 168 words");

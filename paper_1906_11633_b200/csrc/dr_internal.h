@@ -158,6 +158,8 @@ cudaError_t launch_export(const DevPtrs& p, void* dst, uint32_t lo, uint32_t hi,
 cudaError_t launch_import(const DevPtrs& p, const void* src, uint32_t lo, uint32_t hi, cudaStream_t s);
 cudaError_t launch_debug_philox(uint32_t n_env, uint32_t dom, uint32_t ch, uint32_t blk, uint32_t* out,
                                 cudaStream_t s);
+cudaError_t launch_debug_philox_keyed(const uint32_t* ctr, const uint32_t* key, uint32_t* out, unsigned long long n,
+                                      cudaStream_t s);
 int step_max_ctas_per_sm(uint32_t layer_mask);
 void set_step_mode(int mode);   // 0 throughput, 1 latency
 int step_mode();

@@ -123,6 +123,23 @@ __global__ void debug_philox_kernel(uint32_t n_env, uint32_t dom, uint32_t ch, u
     if (e < n_env) out[e] = philox(c_dc.env_offset + e, dom, ch, blk);
 }
 
+// Keyed test hook: the same round function on arbitrary (counter, key) pairs, round keys built in
+// registers from the key (the key schedule dr_api.cu precomputes for a context).
+__global__ void debug_philox_keyed_kernel(const uint4* __restrict__ ctr, const uint2* __restrict__ key,
+                                          uint4* __restrict__ out, unsigned long long n) {
+    const unsigned long long i = (unsigned long long)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    const uint4 c = ctr[i];
+    const uint2 k = key[i];
+    PhiloxKeys rk;
+#pragma unroll
+    for (int r = 0; r < 10; ++r) {
+        rk.rk0[r] = k.x + (uint32_t)r * 0x9E3779B9u;
+        rk.rk1[r] = k.y + (uint32_t)r * 0xBB67AE85u;
+    }
+    out[i] = philox_rounds(c.x, c.y, c.z, c.w, rk);
+}
+
 // =====================================================================================
 // launchers
 // =====================================================================================
@@ -237,6 +254,14 @@ cudaError_t launch_sync_init(const DevPtrs& p, uint64_t t, int grid, int max_cta
 
 cudaError_t launch_debug_philox(uint32_t n_env, uint32_t dom, uint32_t ch, uint32_t blk, uint32_t* out, cudaStream_t s) {
     debug_philox_kernel<<<(n_env + 127) / 128, 128, 0, s>>>(n_env, dom, ch, blk, reinterpret_cast<uint4*>(out));
+    return cudaGetLastError();
+}
+
+cudaError_t launch_debug_philox_keyed(const uint32_t* ctr, const uint32_t* key, uint32_t* out, unsigned long long n,
+                                      cudaStream_t s) {
+    if (n == 0) return cudaSuccess;
+    debug_philox_keyed_kernel<<<(unsigned)((n + 255) / 256), 256, 0, s>>>(
+        reinterpret_cast<const uint4*>(ctr), reinterpret_cast<const uint2*>(key), reinterpret_cast<uint4*>(out), n);
     return cudaGetLastError();
 }
 

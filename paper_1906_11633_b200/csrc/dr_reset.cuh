@@ -267,6 +267,7 @@ __global__ void __launch_bounds__(RH_THREADS, DR_RH_MINB) reset_kernel(DevPtrs p
     const int nnb = phys_on ? (c_dc.n_phys_n + 3) / 4 : 0;
     uint32_t applied = 0;
     for (uint32_t base = blockIdx.x * RH_RANGE; base < n_env; base += gridDim.x * RH_RANGE) {
+        const uint32_t end = min(n_env, base + RH_RANGE);
         if (tid == 0) {
             s_n = 0u;
             s_next = 0u;
@@ -274,7 +275,7 @@ __global__ void __launch_bounds__(RH_THREADS, DR_RH_MINB) reset_kernel(DevPtrs p
         __syncthreads();
         for (uint32_t c = wid; c < RH_RANGE / 32; c += NWR) {
             const uint32_t e = base + c * 32u + lane;
-            const bool m = e < n_env && (mask == nullptr || mask[e] != 0);
+            const bool m = e < end && (mask == nullptr || mask[e] != 0);
             const uint32_t bal = __ballot_sync(0xFFFFFFFFu, m);
             if (!bal) continue;
             uint32_t pos0 = 0;

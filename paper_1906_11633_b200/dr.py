@@ -123,6 +123,8 @@ def load():
     L.dr_phys_export.argtypes = [vp, C.c_int64, C.c_int64]
     L.dr_debug_philox.argtypes = [C.c_uint32, C.c_uint32, C.c_uint32, vp]
     L.dr_debug_philox.restype = C.c_int
+    L.dr_debug_philox_keyed.argtypes = [vp, vp, vp, C.c_uint64, vp]
+    L.dr_debug_philox_keyed.restype = C.c_int
     for f in ("dr_params_default", "dr_init", "dr_update_params", "dr_reset", "dr_step", "dr_step_substeps", "dr_step_host", "dr_finalize",
               "dr_set_stream", "dr_set_occlusion_input", "dr_synchronize", "dr_set_stats_buffer", "dr_set_step_index",
               "dr_state_export", "dr_state_import", "dr_phys_export"):
@@ -343,6 +345,15 @@ def states_to_numpy(states) -> dict:
 def dr_debug_philox(domain: int, channel: int, block: int, out):
     import torch
     return _check(load().dr_debug_philox(domain, channel, block, _ptr(out, None, torch.int32, "out")))
+
+
+def dr_debug_philox_keyed(ctr, key, out, stream=None):
+    """ctr, out: CUDA int32 [n][4]; key: CUDA int32 [n][2] (uint32 bit patterns)."""
+    import torch
+    n = ctr.shape[0]
+    s = stream if stream is not None else torch.cuda.current_stream()
+    return _check(load().dr_debug_philox_keyed(_ptr(ctr, (n, 4), torch.int32, "ctr"), _ptr(key, (n, 2), torch.int32, "key"),
+                                               _ptr(out, (n, 4), torch.int32, "out"), n, C.c_void_p(s.cuda_stream)))
 
 
 def dr_phys_export(env_lo: int = 0, env_hi: int = 0):
