@@ -61,7 +61,9 @@ def parse():
     return ap.parse_args()
 
 
-RESET_BYTES = 1024 + 356 + 4   # per resetting env: phys row, 89-plane episode record, FRESH flag
+# per resetting env: phys row, the 89 record words (written as 12 whole 32-byte groups = 384 B), the
+# FRESH flag and the episode-counter read
+RESET_BYTES = 1024 + 356 + 4 + 4
 
 
 def config_of(name, n_override):
@@ -167,7 +169,8 @@ def measured_peak():
 
 
 def ncu_traffic(workload):
-    """Per-launch dram bytes of the step kernel from the committed ncu summary, if any."""
+    """Per-launch dram bytes of a kernel from the committed ncu summary (profiles/ncu_step_summary.json:
+    the step kernel per workload, the reset kernel under "cfg5-reset-kernel"), if any."""
     try:
         with open(os.path.join(ROOT, "profiles", "ncu_step_summary.json")) as f:
             d = json.load(f)
@@ -579,8 +582,17 @@ def main():
         # dr_reset and dr_step launch times from the events around each (library stream)
         r_ms = [evs[i].elapsed_time(mids[i]) for i in range(args.steps)]
         s_ms = [mids[i].elapsed_time(evs[i + 1]) for i in range(args.steps)]
-        split = {"reset_ms_avg": sum(r_ms) / len(r_ms), "step_ms_avg": sum(s_ms) / len(s_ms),
-                 "resets_per_step": n // 10, "reset_bytes_per_env": RESET_BYTES}
+        r_avg = sum(r_ms) / len(r_ms)
+        # the reset kernel on its own: algorithmic bytes (1,392 B per resetting env + the 1-byte mask of
+        # every env) over its own launch time, and ncu's DRAM bytes per launch against them
+        r_bytes = (n // 10) * RESET_BYTES + n
+        r_traffic = ncu_traffic("cfg5-reset-kernel")
+        r_gbs = r_bytes / (r_avg / 1e3) / 1e9
+        split = {"reset_ms_avg": r_avg, "step_ms_avg": sum(s_ms) / len(s_ms),
+                 "resets_per_step": n // 10, "reset_bytes_per_env": RESET_BYTES,
+                 "reset": {"bound": "issue", "achieved": r_gbs, "unit": "GB/s", "frac_of_hbm": r_gbs / measured_peak()[0],
+                           "algorithmic_bytes": r_bytes, "traffic": r_traffic,
+                           "traffic_over_algorithmic": (r_traffic / r_bytes) if r_traffic else None}}
     per.sort()
     kern_ms = sum(per) / len(per)
     peak, peak_kind = measured_peak()
@@ -590,7 +602,7 @@ def main():
     achieved = bytes_step / (kern_ms / 1e3) / 1e9
     roofline = {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
                 "traffic": None if cfg["resets"] else ncu_traffic(cfg["workload"]), "peak_kind": peak_kind,
-                "bytes_per_env_step": cfg["bytes"], "kernel": "dr::step_kernel_warp" + (" + dr::reset_kernel (one step = dr_reset + dr_step)" if cfg["resets"] else ""),
+                "bytes_per_env_step": bytes_step / n, "kernel": "dr::step_kernel_warp" + (" + dr::reset_kernel (one step = dr_reset + dr_step)" if cfg["resets"] else ""),
                 "kernel_ms_avg": kern_ms, "kernel_ms_median": per[len(per) // 2]}
     if split:
         roofline["split"] = split

@@ -46,6 +46,16 @@ def main(run, tag):
     for k in ("reset", "vision"):
         if os.path.exists(g + f"_prof_{k}.ncu-rep"):
             open(P + f"_{k}_ncu.txt", "w").write(kernel_summary(g + f"_prof_{k}.ncu-rep"))
+    if os.path.exists(g + "_prof_reset.ncu-rep"):   # the reset kernel's DRAM bytes per launch (config 5)
+        full = ncu_summary.raw(g + "_prof_reset.ncu-rep")[0]
+        scale = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9}
+        rb = float(full["dram__bytes_read.sum"][0]) * scale.get(full["dram__bytes_read.sum"][1], 1)
+        wb = float(full["dram__bytes_write.sum"][0]) * scale.get(full["dram__bytes_write.sum"][1], 1)
+        js_path = os.path.join(ROOT, "profiles", "ncu_step_summary.json")
+        js = json.load(open(js_path)) if os.path.exists(js_path) else {}
+        js["cfg5-reset-kernel"] = {"tag": tag, "dram_bytes_per_launch": rb + wb, "dram_read": rb, "dram_write": wb,
+                                   "resets_per_launch": 104857}
+        json.dump(js, open(js_path, "w"), indent=1)
     out = []
     for t in ("memcheck", "racecheck", "synccheck", "initcheck"):
         f = g + f"_sanitize_{t}.log"
@@ -54,6 +64,8 @@ def main(run, tag):
             keep = [ln for ln in txt.splitlines() if re.search(r"SUMMARY|sanitize paths OK|Invalid|Race|Barrier", ln)]
             out.append(f"== {t}\n" + "\n".join(keep))
     if out:
+        out.append("memcheck 'errors', if any, are leak reports: check their allocation frames (torch's caching "
+                   "allocators vs libdr) in gpurun_out/" + run + "_sanitize_memcheck.log.")
         open(P + "_sanitizer.txt", "w").write("\n".join(out) + "\n")
 
 
