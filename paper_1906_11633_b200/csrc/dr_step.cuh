@@ -46,18 +46,6 @@ struct Acc {
     float m[8];   // a thread sums only its ~n/(grid*TILE) envs in fp32; CTA and grid sums are fp64
 };
 
-// ---- cp.async (LDGSTS) helpers ------------------------------------------------------------
-__device__ __forceinline__ uint32_t smem_u32(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
-__device__ __forceinline__ void cp_async4(void* sdst, const void* gsrc) {
-    asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"(smem_u32(sdst)), "l"(gsrc) : "memory");
-}
-__device__ __forceinline__ void cp_async16(void* sdst, const void* gsrc) {
-    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(smem_u32(sdst)), "l"(gsrc) : "memory");
-}
-__device__ __forceinline__ void cp_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
-template <int N>
-__device__ __forceinline__ void cp_wait() { asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory"); }
-
 // ---- phase ring layout ---------------------------------------------------------------------
 // A slot is RING_W rows of TILE words, and warp w owns columns 32 w .. 32 w + 31 of every row (the
 // four warps of a CTA run their pipelines independently, so no row segment is shared).
