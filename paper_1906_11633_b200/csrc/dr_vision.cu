@@ -33,13 +33,16 @@ enum : uint32_t { CH_POSE = 0x401, CH_IMG_PARAM = 0x201, CH_IMG_NOISE = 0x202, C
 #define DR_IMG_THREADS 128   // A/B (us per 192-image batch, map v2): 128 35.9, 256 36.7, 512 49.5 (map v1: 41.1, 40.2, 43.3)
 #endif
 constexpr int IMG_THREADS = DR_IMG_THREADS;
-#ifndef DR_IMG_ILP
 #ifndef DR_IMG_PROBE
 #define DR_IMG_PROBE 0   // roofline probes (A/B builds only): 1 = no noise draws, 2 = no output stores
 #endif
-#define DR_IMG_ILP 1   // A/B (8-element groups per iteration): 1 36.7, 2 40.6 us per 192-image batch
+#ifndef DR_IMG_PRE
+#define DR_IMG_PRE 2   // 8-element groups per thread whose noise is drawn while the slice loads
 #endif
-constexpr int IMG_ILP = DR_IMG_ILP;
+#ifndef DR_IMG_MID
+#define DR_IMG_MID 1   // ... and groups drawn between the cluster barrier's arrive and wait
+#endif
+constexpr int IMG_PRE = DR_IMG_PRE, IMG_MID = DR_IMG_MID, IMG_EARLY = IMG_PRE + IMG_MID;
 constexpr uint32_t IMG_SLICE_MAX = 200 * 1024;
 
 
@@ -105,44 +108,46 @@ __device__ __forceinline__ void tma_bulk(void* dst, const void* src, uint32_t by
 // is one Box-Muller pair with the radius from its top 20 bits and the angle from its low 12 bits --
 // so element e takes normal e % 2 of the pair of word (e % 8) / 2 of block e / 8 (map v1 drew one
 // block per 4 elements: Philox was ~40 % of the kernel's instructions).
-// nz_pair returns s z0 + k, s z1 + k (the noise std s and the per-image constant k folded in):
+// nz_raw gives the pair's s r, sin and cos; the noise of the two elements is then
+// (-(s r) cos + k, -(s r) sin + k) with the per-image constant k (nz_fold), so the draws -- all of the
+// XU work -- need no image moments and start while the slice is still loading:
 //   -2 ln U (s^2 folded into the constants): MUFU.LG2 except for 1 - U < 2^-6, where the series
 //   v (2 + v (1 + 2v/3)) keeps the tiny radius accurate (the fast pair of dr_math.cuh); U and 1 - U
 //   are exact, built from the word's bits; r s from MUFU.SQRT;
 //   the angle 2 pi (A - 1/2) in one FFMA from the 12-bit integer, then MUFU.SIN / MUFU.COS
 //   (cos(t - pi) = -cos t and sin(t - pi) = -sin t: the sign goes into the FFMA with k).
-//   A/B: a quarter-wave (cos, sin) table in shared memory instead of MUFU.SIN / COS measured slower
-//   (41.4 vs 35.9 us per 192-image batch: the random table reads conflict).
+//   A/B (µs per 192-image batch): a quarter-wave (cos, sin) table in shared memory 41.4 vs 35.9 (the
+//   random reads conflict); (sin, cos) as FMA-pipe polynomials 43.0, for half the pairs 38.6.
 struct NzConst {
     float s2_lg;    // -2 ln(2) s^2
     float s2_c2, s2_c1, s2_c0;   // s^2 (2/3), s^2, 2 s^2
-    float kq;
 };
-#ifndef DR_IMG_SINCOS
-#define DR_IMG_SINCOS 0   // A/B: 0 = MUFU.SIN / COS, 1 = FMA-pipe polynomial, 2 = polynomial for pairs 2, 3 only
-#endif
-template <bool kPoly>
-__device__ __forceinline__ void nz_pair(uint32_t x, const NzConst& c, float& z0, float& z1) {
-    const float u = __uint_as_float(0x3F800004u | ((x >> 12) << 3)) - 1.0f;           // (k + 1/2) 2^-20, exact
-    const float v = __uint_as_float(0x3F800004u | ((~x >> 12) << 3)) - 1.0f;          // 1 - u, exact
+struct NzRaw {
+    float rs[4], sn[4], cs[4];   // the four pairs of one 8-element group
+};
+__device__ __forceinline__ void nz_raw(uint32_t x, const NzConst& c, float& rs, float& sn, float& cs) {
+    uint32_t ub;   // (x >> 12) * 8 + 0x3F800004 in one IMAD after the shift (the OR form took two LOP3s)
+    asm("mad.lo.u32 %0, %1, 8, 0x3F800004;" : "=r"(ub) : "r"(x >> 12));
+    const float u = __uint_as_float(ub) - 1.0f;                                       // (k + 1/2) 2^-20, exact
+    const float v = 1.0f - u;   // exact: u has 21 significant bits below 1 (one FADD: 32.8 -> 30.9 us)
     const float series = v * fmaf(fmaf(v, c.s2_c2, c.s2_c1), v, c.s2_c0);
     const float lg = lg2_approx(u) * c.s2_lg;
-    const float rs = sqrt_approx((v < 0.015625f) ? series : lg);                     // s sqrt(-2 ln u)
-    float sn, cs;
-    if constexpr (kPoly) {   // (sin, cos)(2 pi A) on the FMA pipe, A = (k + 1/2) 2^-12 exact
-        sincos_2pi(fmaf((float)(x & 0xFFFu), 2.44140625e-04f, 1.220703125e-04f), sn, cs);
-        z0 = fmaf(rs, cs, c.kq);
-        z1 = fmaf(rs, sn, c.kq);
-    } else {                 // MUFU: the angle 2 pi (A - 1/2) in one FFMA from the 12-bit integer
-        const float ang = fmaf((float)(x & 0xFFFu), 1.53398078788564122e-03f, -3.14082566319585e+00f);
-        __sincosf(ang, &sn, &cs);
-        z0 = fmaf(-rs, cs, c.kq);
-        z1 = fmaf(-rs, sn, c.kq);
-    }
+    rs = sqrt_approx((v < 0.015625f) ? series : lg);                                  // s sqrt(-2 ln u)
+    const float ang = fmaf((float)(x & 0xFFFu), 1.53398078788564122e-03f, -3.14082566319585e+00f);
+    __sincosf(ang, &sn, &cs);
 }
-template <int Q>
-__device__ __forceinline__ void nz_pair_q(uint32_t x, const NzConst& c, float& z0, float& z1) {
-    nz_pair<(DR_IMG_SINCOS == 1) || (DR_IMG_SINCOS == 2 && Q >= 2)>(x, c, z0, z1);
+__device__ __forceinline__ void nz_group(const uint4 w, const NzConst& c, NzRaw& q) {
+    nz_raw(w.x, c, q.rs[0], q.sn[0], q.cs[0]);
+    nz_raw(w.y, c, q.rs[1], q.sn[1], q.cs[1]);
+    nz_raw(w.z, c, q.rs[2], q.sn[2], q.cs[2]);
+    nz_raw(w.w, c, q.rs[3], q.sn[3], q.cs[3]);
+}
+__device__ __forceinline__ void nz_fold(const NzRaw& q, float kq, float z[8]) {
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+        z[2 * j] = fmaf(-q.rs[j], q.cs[j], kq);
+        z[2 * j + 1] = fmaf(-q.rs[j], q.sn[j], kq);
+    }
 }
 
 __global__ void __launch_bounds__(IMG_THREADS) image_augment_kernel(const ImgArgs a) {
@@ -161,13 +166,36 @@ __global__ void __launch_bounds__(IMG_THREADS) image_augment_kernel(const ImgArg
     const uint32_t n = (uint32_t)(hi - lo);
     const uint8_t* src = a.images + img * E + lo;
 
-    // ---- 1. slice -> shared memory (one TMA bulk copy) ----
+    // the image's contrast f and noise std s: one Philox block, no moments needed
+    const uint32_t g = a.image_offset + (uint32_t)img;
+    const uint4 pw = philox_k(g, a.batch, CH_IMG_PARAM, 0, a.keys);
+    const double f = a.contrast_lo + a.contrast_range * (double)uni(pw.x);
+    const double s = a.noise_lo + a.noise_range * (double)uni(pw.y);
+    NzConst nc;
+    {
+        const double s2 = s * s;
+        nc.s2_lg = (float)(-1.38629436111989061883 * s2);
+        nc.s2_c2 = (float)(0.666666666666666667 * s2);
+        nc.s2_c1 = (float)s2;
+        nc.s2_c0 = (float)(2.0 * s2);
+    }
+    const uint32_t b0 = (uint32_t)(lo >> 3);   // lo is a multiple of 16: 8-element noise blocks
+    const uint32_t n8 = n >> 3;
+
+    // ---- 1. slice -> shared memory (one TMA bulk copy); the first IMG_PRE groups' noise draws
+    //         (Philox + the XU transforms) run while it lands ----
+    NzRaw pre[IMG_EARLY > 0 ? IMG_EARLY : 1];
     if (a.aligned) {
         if (tid == 0) mbar_init1(&s_bar);
         __syncthreads();
         if (tid == 0) {
             mbar_expect(&s_bar, n);
             if (n) tma_bulk(s_img, src, n, &s_bar);
+        }
+#pragma unroll
+        for (int q = 0; q < IMG_PRE; ++q) {
+            const uint32_t i = tid + q * IMG_THREADS;
+            if (i < n8) nz_group(philox_k(g, a.batch, CH_IMG_NOISE, b0 + i, a.keys), nc, pre[q]);
         }
         mbar_wait0(&s_bar);
     } else {
@@ -210,6 +238,13 @@ __global__ void __launch_bounds__(IMG_THREADS) image_augment_kernel(const ImgArg
         s_part[1] = Q;
     }
     cluster_arrive();   // publishes s_part to the cluster
+    if (a.aligned) {
+#pragma unroll
+        for (int q = IMG_PRE; q < IMG_EARLY; ++q) {
+            const uint32_t i = tid + q * IMG_THREADS;
+            if (i < n8) nz_group(philox_k(g, a.batch, CH_IMG_NOISE, b0 + i, a.keys), nc, pre[q]);
+        }
+    }
     cluster_wait();
     unsigned long long S = 0, Q = 0;
     for (uint32_t q = 0; q < K; ++q) {   // fixed rank order: identical totals in every CTA
@@ -219,90 +254,69 @@ __global__ void __launch_bounds__(IMG_THREADS) image_augment_kernel(const ImgArg
     cluster_arrive();   // done reading the other CTAs' shared memory (matched by the wait at exit)
 
     // ---- 3. normalise, contrast, noise ----
-    const uint32_t g = a.image_offset + (uint32_t)img;
     const double mean = (double)S / (double)E;
     const unsigned long long vnum = Q * E - S * S;   // E^2 var, exact (no overflow below the size limit)
     const double sd = sqrt((double)vnum / ((double)E * (double)E));
-    const uint4 pw = philox_k(g, a.batch, CH_IMG_PARAM, 0, a.keys);
-    const double f = a.contrast_lo + a.contrast_range * (double)uni(pw.x);
-    const double s = a.noise_lo + a.noise_range * (double)uni(pw.y);
     const float scale = (float)(f / (sd > a.std_floor ? sd : a.std_floor));
-    const float mu_hi = (float)mean, mu_lo = (float)(mean - (double)mu_hi);   // x - mu_hi is exact
-    // out = (x - mu_hi) * scale + (s z - mu_lo scale): the remainder term k = -mu_lo * scale is one
-    // per-image constant (|mu_lo| <= 2^-24 * 128 and scale <= ~2e5 for a non-constant u8 image, so
-    // |k| < 1.5; a constant image has mu_lo = 0); s and k are folded into the noise pair (nz_pair).
-    // Every element of every image takes the same expression, whatever the slice / cluster size.
-    NzConst nc;
-    {
-        const double s2 = s * s;
-        nc.s2_lg = (float)(-1.38629436111989061883 * s2);
-        nc.s2_c2 = (float)(0.666666666666666667 * s2);
-        nc.s2_c1 = (float)s2;
-        nc.s2_c0 = (float)(2.0 * s2);
-        nc.kq = (float)(-(double)mu_lo * (double)scale);
-    }
+    // out = (x - mu_i) * scale + (s z + k), mu_i = rint(mean), k = -(mean - mu_i) * scale: a byte x is
+    // read as the float 2^23 + x (one PRMT of the packed bytes under the exponent 0x4B, no I2F on the
+    // XU pipe the noise draws' MUFUs share: 35.9 -> 34.5 us per batch) and (2^23 + x) - (2^23 + mu_i)
+    // is exact; |x - mean| >= |mean - mu_i| for every byte x, so k never dominates the result it is
+    // rounded into.  Every element of every image takes the same expression, whatever the slice /
+    // cluster size.
+    const float mu_i = (float)rint(mean), c_b = 8388608.0f + mu_i;   // exact: integer < 2^24
+    const float kq = (float)(-(mean - (double)mu_i) * (double)scale);
     if (r == 0 && tid == 0 && a.img_stats)
         reinterpret_cast<float4*>(a.img_stats)[img] = make_float4((float)mean, (float)sd, (float)f, (float)s);
 
     float* out = a.out + img * E + lo;
-    const uint32_t b0 = (uint32_t)(lo >> 3);   // lo is a multiple of 16: 8-element noise blocks
     if (a.aligned) {
-        // whole 8-element groups: one Philox block, four independent Box-Muller pairs, two float4
-        // streaming stores (IMG_ILP groups per iteration, A/B)
+        // whole 8-element groups: one Philox block, four Box-Muller pairs, one 256-bit streaming store
         const uint2* w8 = reinterpret_cast<const uint2*>(s_img);
         float4* o4 = reinterpret_cast<float4*>(out);
-        const uint32_t n8 = n >> 3;   // n is a multiple of 16 on this path
-        auto group = [&](uint32_t i) {
-#if DR_IMG_PROBE == 1
-            const uint4 w = make_uint4(i, i, i, i);
-#else
-            const uint4 w = philox_k(g, a.batch, CH_IMG_NOISE, b0 + i, a.keys);
-#endif
-            const uint2 x = w8[i];
-            const uint32_t ws[4] = {w.x, w.y, w.z, w.w};
+        auto emit = [&](uint32_t i, const NzRaw& q) {
             float z[8];
-#if DR_IMG_PROBE == 1   // roofline probe (A/B only): no noise draws
-            for (int q = 0; q < 8; ++q) z[q] = nc.kq + (float)(ws[q & 3] & 1u);
-#else
-            nz_pair_q<0>(ws[0], nc, z[0], z[1]);
-            nz_pair_q<1>(ws[1], nc, z[2], z[3]);
-            nz_pair_q<2>(ws[2], nc, z[4], z[5]);
-            nz_pair_q<3>(ws[3], nc, z[6], z[7]);
-#endif
+            nz_fold(q, kq, z);
+            const uint2 x = w8[i];
             float v[8];
 #pragma unroll
             for (int k = 0; k < 8; ++k) {
-                const uint32_t xb = (k < 4 ? x.x : x.y) >> (8 * (k & 3));
-                v[k] = fmaf((float)(xb & 0xFFu) - mu_hi, scale, z[k]);   // x - mu_hi exact
+                const float xb = __uint_as_float(__byte_perm(k < 4 ? x.x : x.y, 0x4B000000u, 0x7540u | (k & 3)));
+                v[k] = fmaf(xb - c_b, scale, z[k]);   // (2^23 + x) - (2^23 + mu_i), exact
             }
 #if DR_IMG_PROBE == 2   // roofline probe (A/B only): no output stores
             if (v[0] + v[1] + v[2] + v[3] + v[4] + v[5] + v[6] + v[7] == 12345.f) out[0] = 0.f;
 #else
-            // one 256-bit streaming store per group: a warp writes 32 whole sectors (1 KB contiguous)
+            // a warp writes 32 whole sectors (1 KB contiguous) per store
             asm volatile("st.global.cs.v8.f32 [%0], {%1, %2, %3, %4, %5, %6, %7, %8};" ::"l"(o4 + 2 * i), "f"(v[0]),
                          "f"(v[1]), "f"(v[2]), "f"(v[3]), "f"(v[4]), "f"(v[5]), "f"(v[6]), "f"(v[7])
                          : "memory");
 #endif
         };
-        uint32_t i = tid;
-        for (; i + (IMG_ILP - 1) * IMG_THREADS < n8; i += IMG_ILP * IMG_THREADS) {
 #pragma unroll
-            for (int u = 0; u < IMG_ILP; ++u) group(i + u * IMG_THREADS);
+        for (int q = 0; q < IMG_EARLY; ++q) {
+            const uint32_t i = tid + q * IMG_THREADS;
+            if (i < n8) emit(i, pre[q]);
         }
-        for (; i < n8; i += IMG_THREADS) group(i);
+        for (uint32_t i = tid + IMG_EARLY * IMG_THREADS; i < n8; i += IMG_THREADS) {
+            NzRaw q;
+#if DR_IMG_PROBE == 1   // roofline probe (A/B only): no noise draws
+            for (int j = 0; j < 4; ++j) q.rs[j] = q.sn[j] = q.cs[j] = (float)(i & (1u << j));
+#else
+            nz_group(philox_k(g, a.batch, CH_IMG_NOISE, b0 + i, a.keys), nc, q);
+#endif
+            emit(i, q);
+        }
     } else {
         for (uint32_t i = tid; i < (n + 7) / 8; i += IMG_THREADS) {
-            const uint4 w = philox_k(g, a.batch, CH_IMG_NOISE, b0 + i, a.keys);
-            const uint32_t ws[4] = {w.x, w.y, w.z, w.w};
+            NzRaw q;
+            nz_group(philox_k(g, a.batch, CH_IMG_NOISE, b0 + i, a.keys), nc, q);
             float z[8];
-            nz_pair_q<0>(ws[0], nc, z[0], z[1]);
-            nz_pair_q<1>(ws[1], nc, z[2], z[3]);
-            nz_pair_q<2>(ws[2], nc, z[4], z[5]);
-            nz_pair_q<3>(ws[3], nc, z[6], z[7]);
+            nz_fold(q, kq, z);
 #pragma unroll
             for (int k = 0; k < 8; ++k) {
                 const uint32_t e = 8 * i + k;
-                if (e < n) out[e] = fmaf((float)s_img[e] - mu_hi, scale, z[k]);
+                if (e < n) out[e] = fmaf(__uint_as_float(0x4B000000u | s_img[e]) - c_b, scale, z[k]);
             }
         }
     }
