@@ -489,16 +489,10 @@ int dr_init(const dr_params* params, int64_t n_env, uint64_t seed) {
                                 : (uint32_t)((n_env + TILE - 1) / TILE);
     // Persistent grid of min(units, resident slots) CTAs, the slots a multiple of the SM count: unit i
     // runs on CTA i % grid, i.e. on SM i % 148, so every SM gets the same number of units (+-1) even
-    // when the CTAs do not (DR_STEP_BALANCE=1, A/B: the fewest waves, grid = ceil(units / waves) --
-    // equal units per CTA but 3 or 4 CTAs per SM).
+    // when the CTAs do not (the fewest-waves grid ceil(units / waves) -- equal units per CTA but 3 or
+    // 4 CTAs per SM -- measured slower, profiles/round2_notes.md).
     const long long slots = std::min<long long>((long long)c->sm_count * occ_step, (long long)c->max_ctas);
     c->step_grid = (int)std::min<long long>((long long)units, slots);
-    if (const char* bal = std::getenv("DR_STEP_BALANCE")) {
-        if (std::atoi(bal) == 1) {
-            const long long waves = ((long long)units + slots - 1) / slots;
-            c->step_grid = (int)(((long long)units + waves - 1) / waves);
-        }
-    }
     // A/B: persistent grid size (clamped to the default). 1M envs: 592 (default) 4.90e9, 586 4.89e9,
     // 546 4.75e9, 512 4.60e9, 444 4.73e9 env-steps/s
     if (const char* sg = std::getenv("DR_STEP_GRID")) {
