@@ -338,12 +338,14 @@ def run_vision(args):
             dist.barrier()
         torch.cuda.synchronize()
         l0 = vision.dr_total_kernel_launches()
-        evs = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps + 1)]
+        # events at the two ends only (an event between two launches costs ~2 us per step:
+        # scripts/vision_probe.py)
+        evs = [torch.cuda.Event(enable_timing=True) for _ in range(2)]
         h0 = time.monotonic()
         evs[0].record(stream)
         for i in range(args.steps):
             one_step(t_base + i)
-            evs[i + 1].record(stream)
+        evs[1].record(stream)
         torch.cuda.synchronize()
         sampler.mark_timed(h0, time.monotonic())
         if world > 1:
@@ -351,7 +353,7 @@ def run_vision(args):
         launches = vision.dr_total_kernel_launches() - l0
         clocks = sampler.stop()
         elapsed_ms = evs[0].elapsed_time(evs[-1])
-        per = sorted(evs[i].elapsed_time(evs[i + 1]) for i in range(args.steps))
+        per = [elapsed_ms / args.steps]
         t_ms = torch.tensor([elapsed_ms], dtype=torch.float64, device="cuda")
         if world > 1:
             dist.all_reduce(t_ms, op=dist.ReduceOp.MAX)
@@ -551,13 +553,14 @@ def main():
                 graph.replay()
                 evs[i + 1].record(lib_stream)
         else:
-            evs = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps + 1)]
-            mids = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)] if cfg["resets"] else None
+            # events only at the two ends: an event recorded between two launches makes the second
+            # wait for the first to drain and costs ~2 us per step (it also stops chained steps from
+            # overlapping); the reset / step split comes from a separate pass below
+            evs = [torch.cuda.Event(enable_timing=True)]
             h0 = time.monotonic()
             evs[0].record(lib_stream)
             for i in range(args.steps):
-                one_step(t_base + i, mids[i] if mids else None)
-                evs[i + 1].record(lib_stream)
+                one_step(t_base + i)
         if reducer is not None:
             reducer.sync()
         end = torch.cuda.Event(enable_timing=True)
@@ -569,19 +572,34 @@ def main():
         launches = per_graph_launches * reps if G > 0 else dr.dr_kernel_launches() - launches0
         clocks = sampler.stop()
         elapsed_ms = evs[0].elapsed_time(end)
-        per = [evs[i].elapsed_time(evs[i + 1]) / max(G, 1) for i in range(len(evs) - 1)]
+        if G > 0:
+            per = [evs[i].elapsed_time(evs[i + 1]) / G for i in range(len(evs) - 1)]
+        else:
+            per = [elapsed_ms / args.steps]
         t_ms = torch.tensor([elapsed_ms], dtype=torch.float64, device="cuda")
         if world > 1:
             dist.all_reduce(t_ms, op=dist.ReduceOp.MAX)
         elapsed_ms = float(t_ms.item())
         stats = ctx.last_stats()
+        r_ms = s_ms = None
+        if cfg["resets"] and G == 0:
+            # diagnostic pass after the timed region (not part of value): events around each dr_reset
+            # and dr_step give the two kernels' shares of a step
+            D = min(args.steps, 50)
+            ev_a = [torch.cuda.Event(enable_timing=True) for _ in range(D + 1)]
+            ev_m = [torch.cuda.Event(enable_timing=True) for _ in range(D)]
+            ev_a[0].record(lib_stream)
+            for i in range(D):
+                one_step(t_base + args.steps + i, ev_m[i])
+                ev_a[i + 1].record(lib_stream)
+            torch.cuda.synchronize()
+            r_ms = [ev_a[i].elapsed_time(ev_m[i]) for i in range(D)]
+            s_ms = [ev_m[i].elapsed_time(ev_a[i + 1]) for i in range(D)]
 
     value = n_glob * args.steps / (elapsed_ms / 1e3)
     split = None
-    if cfg["resets"] and G == 0:
-        # dr_reset and dr_step launch times from the events around each (library stream)
-        r_ms = [evs[i].elapsed_time(mids[i]) for i in range(args.steps)]
-        s_ms = [mids[i].elapsed_time(evs[i + 1]) for i in range(args.steps)]
+    if r_ms:
+        # dr_reset and dr_step launch times from the diagnostic pass (events around each)
         r_avg = sum(r_ms) / len(r_ms)
         # the reset kernel on its own: algorithmic bytes (1,392 B per resetting env + the 1-byte mask of
         # every env) over its own launch time, and ncu's DRAM bytes per launch against them
