@@ -330,6 +330,20 @@ def test_config5_reset_stress_sampled(torch_cuda):
     run_pair(torch_cuda, FULL, n, 6, n_frames=4, sample=sample, resets=resets, state_every=1)
 
 
+def test_config4_config5_full_size_sampled_1M(torch_cuda):
+    """BASELINE configs 4 and 5 at their full size (1,048,576 envs, all layers) in bench.py's launch
+    configuration (persistent grid of 592 CTAs, chained steps, a 4-frame input ring): 10 steps with
+    config 5's resets before every step ((e + t) mod 10 == 0, so every env resets once), then 2
+    more without; 96 sampled envs (incl. the first and last tiles) compared with the oracle every
+    step, records and state every 4 steps."""
+    n = 1 << 20
+    rng = np.random.default_rng(45)
+    sample = np.sort(np.unique(np.concatenate([[0, 1, 127, 128, n - 129, n - 2, n - 1],
+                                                rng.choice(n, 89, replace=False)])))
+    resets = {t: gen.reset_mask_ring(n, t) for t in range(10)}
+    run_pair(torch_cuda, FULL, n, 12, n_frames=4, sample=sample, resets=resets, state_every=4, stats=False)
+
+
 def _run_outputs(torch, P, n, T, seed=SEED, env_offset=0, n_env_global=0, rows=None, resets=None, graph=False):
     acts, obs = gen.frames(n_env_global or n, 6)
     lo = env_offset
