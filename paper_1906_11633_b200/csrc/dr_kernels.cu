@@ -176,7 +176,7 @@ cudaError_t launch_reset(const DevPtrs& p, const uint8_t* mask, bool first, uint
 int reset_grid_for(uint32_t n_env, int sm_count) {
     int n = 0;
     if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, reset_kernel, RH_THREADS, 0) != cudaSuccess || n < 1) n = 1;
-    const long long ranges = (n_env + RH_RANGE - 1) / RH_RANGE;
+    const long long ranges = (n_env + 31) / 32;   // 32-env mask chunks
     return (int)std::max<long long>(1, std::min<long long>(ranges, (long long)sm_count * n));
 }
 

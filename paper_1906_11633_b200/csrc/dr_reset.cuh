@@ -1,9 +1,9 @@
 // dr_reset.cuh -- episode-reset sampling (PAPER.md:7-8, 13, 15-18, 36-41, 77-78, 87-88, 100-101,
 // 113), included by dr_kernels.cu inside namespace dr.
 //
-// reset_kernel: each CTA scans a RH_RANGE-env range of the mask (one coalesced 32-byte load and a
-// ballot per warp), appends the resetting envs (and their next episode index) to a shared-memory
-// list, then
+// reset_kernel: each CTA scans its interleaved 32-env chunks of the mask (one coalesced 32-byte
+// load and a ballot per warp and chunk), appends the resetting envs (and their next episode index)
+// to a shared-memory list, then
 //   * one thread per resetting env draws the episode record and writes it as 12 whole 32-byte
 //     sectors (one 256-bit store per record group, dr_internal.h): the record of an env is written
 //     in full, so L2 never read-fills a partially written sector from DRAM (the AoSoA record of
@@ -20,21 +20,23 @@
 // per-warp draw buffer: uniforms at [0, 256), normals at [256, 512), a constant 0 at 512 (the x of
 // draw-free descriptors); rs_src holds, per parameter, the buffer offset of its x | RS_EXP.
 constexpr int RH_DRAW = 2 * MAX_PHYS + 4;
-// CTA shape (threads, envs scanned per pass).  Round-1 sweep with the AoSoA record (config 5, reset
-// ms per launch): 256/2048 0.202, 256/1024 0.168, 128/512 0.165-0.170, 512/1024 0.158, 256/512
-// 0.151, 128/256 0.151, 128/128 0.153: small ranges (~51 resetting envs per CTA at 10 %) give
-// thousands of short CTAs whose record chains and physics warps overlap on each SM.
+// CTA shape: 256 threads, <= 64 registers (4 CTAs per SM).  Scan schedule: CTA c owns the 32-env
+// mask chunks c, c + G, c + 2 G, ... (G = the grid) and scans up to RH_PASS envs of them into one
+// shared-memory list per pass -- at 1M envs one pass of ~1,771 envs per CTA.  Measured against the
+// round-1/2 schedule of 512-env ranges handed out grid-stride (3.46 ranges per CTA: four barrier
+// rounds and a 4-vs-3.46 tail), config 5 reset ms per launch (three alternating runs): ranges
+// 0.0952, passes of 512 / 1,024 / 2,048 envs 0.0949 / 0.0920 / 0.0887 (kept).
 #ifndef DR_RH_THREADS
 #define DR_RH_THREADS 256
-#endif
-#ifndef DR_RH_RANGE
-#define DR_RH_RANGE 512
 #endif
 #ifndef DR_RH_MINB
 #define DR_RH_MINB 4   // __launch_bounds__ min CTAs per SM (<= 64 registers)
 #endif
 constexpr int RH_THREADS = DR_RH_THREADS;
-constexpr uint32_t RH_RANGE = DR_RH_RANGE;
+#ifndef DR_RH_PASS
+#define DR_RH_PASS 2048
+#endif
+constexpr uint32_t RH_PASS = DR_RH_PASS;   // envs scanned per pass (the shared-memory list's capacity)
 
 __device__ __forceinline__ float sel4(const float z[4], uint32_t r) {
     return r == 0u ? z[0] : (r == 1u ? z[1] : (r == 2u ? z[2] : z[3]));
@@ -261,50 +263,20 @@ __global__ void __launch_bounds__(RH_THREADS, DR_RH_MINB) reset_kernel(DevPtrs p
                                                               uint32_t n_env) {
     __shared__ float4 s_pd[MAX_PHYS];           // transposed: parameter q at pd_slot(q)
     __shared__ __align__(16) uint32_t s_src[MAX_PHYS];   // transposed: lane l's quad h at [(h * 32 + l) * 4]
-    __shared__ uint32_t s_env[1][RH_RANGE];
-    __shared__ uint32_t s_kk[1][RH_RANGE];    // episode counter k - 1 (0xFFFFFFFF on the first reset)
+    __shared__ uint32_t s_env[1][RH_PASS];
+    __shared__ uint32_t s_kk[1][RH_PASS];    // episode counter k - 1 (0xFFFFFFFF on the first reset)
     __shared__ __align__(16) float s_dr[RH_THREADS / 32][RH_DRAW];
     __shared__ uint32_t s_n[1], s_next[1];
     const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
     pdl_wait();   // before any global access (dr_device.cuh)
     constexpr int NWR = RH_THREADS / 32;
-    constexpr int NCH = RH_RANGE / 32 / NWR;   // mask chunks of 32 envs per warp and range
-    static_assert(RH_RANGE % (32 * NWR) == 0, "range = whole chunks per warp");
+    static_assert(RH_PASS % (32 * NWR) == 0, "pass = whole chunks per warp");
     stage_phys_tables(p, s_pd, s_src, tid, RH_THREADS);
     if (lane == 0) s_dr[wid][RS_OFF_ZERO] = 0.f;
     const bool phys_on = (c_dc.layer_mask & B_PHYS) != 0;
     const int nub = phys_on ? (c_dc.n_phys_u + 3) / 4 : 0;
     const int nnb = phys_on ? (c_dc.n_phys_n + 3) / 4 : 0;
-    const uint32_t stride = gridDim.x * RH_RANGE;
     uint32_t applied = 0;
-    // mask bytes of one range: chunk j of warp w is envs base + (w + NWR j) * 32 + lane
-    auto load_mask = [&](uint32_t base, uint32_t mk[NCH]) {
-#pragma unroll
-        for (int j = 0; j < NCH; ++j) {
-            const uint32_t e = base + (uint32_t)(wid + NWR * j) * 32u + lane;
-            mk[j] = (e < n_env) ? (mask == nullptr ? 1u : (uint32_t)mask[e]) : 0u;
-        }
-    };
-    // append the range's resetting envs to slot sl; their episode counters follow by cp.async
-    auto compact = [&](uint32_t base, const uint32_t mk[NCH], int sl, uint32_t* cnt) {
-#pragma unroll
-        for (int j = 0; j < NCH; ++j) {
-            const uint32_t e = base + (uint32_t)(wid + NWR * j) * 32u + lane;
-            const bool m = mk[j] != 0u;
-            const uint32_t bal = __ballot_sync(0xFFFFFFFFu, m);
-            if (!bal) continue;
-            uint32_t pos0 = 0;
-            if (lane == 0) pos0 = atomicAdd(cnt, (uint32_t)__popc(bal));
-            pos0 = __shfl_sync(0xFFFFFFFFu, pos0, 0);
-            if (m) {
-                const uint32_t idx = pos0 + __popc(bal & ((1u << lane) - 1u));
-                s_env[sl][idx] = e;
-                if (first) s_kk[sl][idx] = 0xFFFFFFFFu;
-                else cp_async4(&s_kk[sl][idx], p.rec + rec_index(e) + rec_off(e, REC_EPISODE));
-            }
-            applied += (lane == 0) ? (uint32_t)__popc(bal) : 0u;
-        }
-    };
     // the record chains first: part p of env i on thread p * npad + i (whole warps per part, so no
     // warp mixes code paths); then every warp pulls physics rows from a shared counter, so the
     // warps without a record chunk start on them at once and the rows spread over all warps
@@ -322,20 +294,50 @@ __global__ void __launch_bounds__(RH_THREADS, DR_RH_MINB) reset_kernel(DevPtrs p
             reset_phys_warp(p, s_env[sl][i], s_kk[sl][i] + 1u, lane, s_dr[wid], s_pd, s_src, nub, nnb);
         }
     };
-    uint32_t mk[NCH];
-    for (uint32_t base = blockIdx.x * RH_RANGE; base < n_env; base += stride) {
-        if (tid == 0) {
-            s_n[0] = 0u;
-            s_next[0] = 0u;
+    // interleaved 32-env chunks: CTA c owns chunks c, c + G, c + 2 G, ... (G = gridDim.x), scanned
+    // RH_PASS / 32 at a time into one shared-memory list: one barrier round per pass and, for any
+    // mask that is uniform at the scale of G chunks, the same number of resets in every CTA
+    {
+        constexpr uint32_t PASS_CH = RH_PASS / 32;
+        constexpr int NCH1 = PASS_CH / NWR;
+        const uint32_t nch = (n_env + 31u) / 32u, G = gridDim.x;
+        const uint32_t my = (nch > blockIdx.x) ? (nch - blockIdx.x + G - 1u) / G : 0u;
+        for (uint32_t j0 = 0; j0 < my; j0 += PASS_CH) {
+            if (tid == 0) {
+                s_n[0] = 0u;
+                s_next[0] = 0u;
+            }
+            __syncthreads();
+            uint32_t mk1[NCH1], ee[NCH1];
+#pragma unroll
+            for (int jj = 0; jj < NCH1; ++jj) {
+                const uint32_t j = j0 + (uint32_t)(wid + NWR * jj);
+                ee[jj] = (blockIdx.x + G * j) * 32u + lane;
+                mk1[jj] = (j < my && ee[jj] < n_env) ? (mask == nullptr ? 1u : (uint32_t)mask[ee[jj]]) : 0u;
+            }
+#pragma unroll
+            for (int jj = 0; jj < NCH1; ++jj) {
+                const bool m = mk1[jj] != 0u;
+                const uint32_t bal = __ballot_sync(0xFFFFFFFFu, m);
+                if (!bal) continue;
+                uint32_t pos0 = 0;
+                if (lane == 0) pos0 = atomicAdd(&s_n[0], (uint32_t)__popc(bal));
+                pos0 = __shfl_sync(0xFFFFFFFFu, pos0, 0);
+                if (m) {
+                    const uint32_t idx = pos0 + __popc(bal & ((1u << lane) - 1u));
+                    const uint32_t e = ee[jj];
+                    s_env[0][idx] = e;
+                    if (first) s_kk[0][idx] = 0xFFFFFFFFu;
+                    else cp_async4(&s_kk[0][idx], p.rec + rec_index(e) + rec_off(e, REC_EPISODE));
+                }
+                applied += (lane == 0) ? (uint32_t)__popc(bal) : 0u;
+            }
+            cp_commit();
+            cp_wait<0>();
+            __syncthreads();
+            work(0, s_n[0], &s_next[0]);
+            __syncthreads();
         }
-        __syncthreads();
-        load_mask(base, mk);
-        compact(base, mk, 0, &s_n[0]);
-        cp_commit();
-        cp_wait<0>();
-        __syncthreads();
-        work(0, s_n[0], &s_next[0]);
-        __syncthreads();
     }
     pdl_trigger();
     if (!first && applied) atomicAdd(&p.ctl[2], (unsigned long long)applied);
