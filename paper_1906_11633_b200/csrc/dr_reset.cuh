@@ -72,6 +72,42 @@ __device__ __noinline__ float4 normals4_block(uint32_t g, uint32_t k, uint32_t c
     box_muller(w.z, w.w, z.z, z.w);
     return z;
 }
+// Eight normals of two blocks (block b1 of channel ch1, block b2 of channel ch2): the two Philox
+// chains are independent, so their rounds interleave (twice the ILP of two normals4_block calls).
+struct Normals8 {
+    float4 a, b;
+};
+__device__ __noinline__ Normals8 normals8_block(uint32_t g, uint32_t k, uint32_t ch1, uint32_t b1, uint32_t ch2,
+                                                uint32_t b2) {
+    const uint4 w1 = philox(g, k, ch1, b1);
+    const uint4 w2 = philox(g, k, ch2, b2);
+    Normals8 z;
+    box_muller(w1.x, w1.y, z.a.x, z.a.y);
+    box_muller(w1.z, w1.w, z.a.z, z.a.w);
+    box_muller(w2.x, w2.y, z.b.x, z.b.y);
+    box_muller(w2.z, w2.w, z.b.z, z.b.w);
+    return z;
+}
+// Physics draws of block b: 4 uniforms of PHYS_U block b (a) and 4 normals of PHYS_N block b (b).
+__device__ __noinline__ Normals8 phys_pair_block(uint32_t g, uint32_t k, uint32_t b) {
+    const uint4 wu = philox(g, k, CH_PHYS_U, b);
+    const uint4 wn = philox(g, k, CH_PHYS_N, b);
+    Normals8 z;
+    z.a = make_float4(uni(wu.x), uni(wu.y), uni(wu.z), uni(wu.w));
+    box_muller(wn.x, wn.y, z.b.x, z.b.y);
+    box_muller(wn.z, wn.w, z.b.z, z.b.w);
+    return z;
+}
+__device__ __forceinline__ void reset_normals8(bool on, uint32_t g, uint32_t k, uint32_t ch1, uint32_t b1, uint32_t ch2,
+                                               uint32_t b2, float z1[4], float z2[4]) {
+#pragma unroll
+    for (int q = 0; q < 4; ++q) z1[q] = z2[q] = 0.f;
+    if (on) {
+        const Normals8 v = normals8_block(g, k, ch1, b1, ch2, b2);
+        z1[0] = v.a.x; z1[1] = v.a.y; z1[2] = v.a.z; z1[3] = v.a.w;
+        z2[0] = v.b.x; z2[1] = v.b.y; z2[2] = v.b.z; z2[3] = v.b.w;
+    }
+}
 // ... zero when the layer is off.
 __device__ __forceinline__ void reset_normals4(bool on, uint32_t g, uint32_t k, uint32_t ch, uint32_t b, float z[4]) {
     z[0] = z[1] = z[2] = z[3] = 0.f;
@@ -160,8 +196,7 @@ __device__ void reset_record_part(const DevPtrs& p, uint32_t e, uint32_t k, int 
 #pragma unroll 1
         for (int b = 1; b < 5; b += 2) {   // groups 6..7: c_act 4..11, 12..19
             float z0[4], z1[4];
-            reset_normals4(lm & B_ACT_NOISE, g, k, CH_CORR_ACT, b, z0);
-            reset_normals4(lm & B_ACT_NOISE, g, k, CH_CORR_ACT, b + 1, z1);
+            reset_normals8(lm & B_ACT_NOISE, g, k, CH_CORR_ACT, b, CH_CORR_ACT, b + 1, z0, z1);
             st_group(R, e, 6 + (b >> 1), fu(sc * z0[0]), fu(sc * z0[1]), fu(sc * z0[2]), fu(sc * z0[3]), fu(sc * z1[0]),
                      fu(sc * z1[1]), fu(sc * z1[2]), fu(sc * z1[3]));
         }
@@ -173,8 +208,7 @@ __device__ void reset_record_part(const DevPtrs& p, uint32_t e, uint32_t k, int 
 #pragma unroll 1
         for (int b = 0; b < 5; ++b) {
             float zn[4], zp[4], dn[4], dp[4];
-            reset_normals4(lm & B_BACKLASH, g, k, CH_BACKLASH, b, zn);
-            reset_normals4(lm & B_BACKLASH, g, k, CH_BACKLASH, 5 + b, zp);
+            reset_normals8(lm & B_BACKLASH, g, k, CH_BACKLASH, b, CH_BACKLASH, 5 + b, zn, zp);
 #pragma unroll
             for (int q = 0; q < 4; ++q) {
                 const int j = 4 * b + q;
@@ -189,12 +223,11 @@ __device__ void reset_record_part(const DevPtrs& p, uint32_t e, uint32_t k, int 
         float off[16], co[4], qc[4] = {1.f, 0.f, 0.f, 0.f};
         const bool obs = (lm & B_OBS_NOISE) != 0;
         float mb[4];
-        reset_normals4(obs, g, k, CH_MARKER_BASE, 0, mb);
+        reset_normals8(obs, g, k, CH_MARKER_BASE, 0, CH_CORR_OBJ, 0, mb, co);
 #pragma unroll
         for (int b = 0; b < 4; ++b) {
             float zc[4], zm[4];
-            reset_normals4(obs, g, k, CH_CORR_TIP, b, zc);
-            reset_normals4(obs, g, k, CH_MARKER_TIP, b, zm);
+            reset_normals8(obs, g, k, CH_CORR_TIP, b, CH_MARKER_TIP, b, zc, zm);
 #pragma unroll
             for (int q = 0; q < 4; ++q) {
                 const int n = 4 * b + q;
@@ -203,7 +236,6 @@ __device__ void reset_record_part(const DevPtrs& p, uint32_t e, uint32_t k, int 
                 off[n] = obs ? v : 0.f;
             }
         }
-        reset_normals4(obs, g, k, CH_CORR_OBJ, 0, co);
 #pragma unroll
         for (int c = 0; c < 3; ++c) co[c] = obs ? c_dc.obj_corr * co[c] : 0.f;
         if (obs) rotation(c_dc.rot_corr, philox(g, k, CH_CORR_ROT, 0), qc);
@@ -221,13 +253,20 @@ __device__ __forceinline__ void reset_phys_warp(const DevPtrs& p, uint32_t e, ui
                                                 const float4* s_pd, const uint32_t* s_src, int nub, int nnb) {
     const uint32_t g = c_dc.env_offset + e;
     __syncwarp();
-    for (int b = lane; b < nub + nnb; b += 32) {
-        if (b < nub) {   // uniform-kind parameter u uses word u % 4 of block u / 4 (channel PHYS_U)
+    // uniform-kind parameter u uses word u % 4 of block u / 4 (channel PHYS_U); normal-kind
+    // parameter n uses normal n % 4 of block n / 4 (channel PHYS_N).  Lane l draws uniform block b and
+    // normal block b (b = l, l + 32) together: two independent Philox chains interleave.
+    const int nb = max(nub, nnb);
+    for (int b = lane; b < nb; b += 32) {
+        if (b < nub && b < nnb) {
+            const Normals8 v = phys_pair_block(g, k, (uint32_t)b);
+            reinterpret_cast<float4*>(dr)[b] = v.a;
+            reinterpret_cast<float4*>(dr + MAX_PHYS)[b] = v.b;
+        } else if (b < nub) {
             const uint4 w = philox(g, k, CH_PHYS_U, (uint32_t)b);
             reinterpret_cast<float4*>(dr)[b] = make_float4(uni(w.x), uni(w.y), uni(w.z), uni(w.w));
-        } else {         // normal-kind parameter n uses normal n % 4 of block n / 4 (channel PHYS_N)
-            const int bn = b - nub;
-            reinterpret_cast<float4*>(dr + MAX_PHYS)[bn] = normals4_block(g, k, CH_PHYS_N, (uint32_t)bn);
+        } else {
+            reinterpret_cast<float4*>(dr + MAX_PHYS)[b] = normals4_block(g, k, CH_PHYS_N, (uint32_t)b);
         }
     }
     __syncwarp();
