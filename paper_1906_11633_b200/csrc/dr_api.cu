@@ -48,7 +48,7 @@ Layout make_layout(int64_t n_env, int n_phys, int max_ctas) {
     L.dec = take(512 * 8);
     L.stats = take(N_STAT_SLOTS * N_STATS * 8);
     L.ctl = take(8 * 8);
-    L.sync = take((N_STAT_SLOTS + (size_t)max_ctas) * 4);   // done | cta_done
+    L.sync = take((N_STAT_SLOTS + 2 * (size_t)max_ctas) * 4);   // done | cta_done | cta_ready
     L.total = off;
     return L;
 }
@@ -459,6 +459,7 @@ int dr_init(const dr_params* params, int64_t n_env, uint64_t seed) {
     P.ctl = reinterpret_cast<unsigned long long*>(c->ws + L.ctl);
     P.done = reinterpret_cast<uint32_t*>(c->ws + L.sync);
     P.cta_done = P.done + N_STAT_SLOTS;
+    P.cta_ready = P.cta_done + c->max_ctas;
     c->internal_stats = P.stats;
 
     cudaStream_t s = c->stream;

@@ -138,6 +138,7 @@ struct DevPtrs {
     unsigned long long* ctl;  // [0] = step t (host-visible), [2] = resets pending, [4] = CTA-start tickets
     uint32_t* done;           // [N_STAT_SLOTS]: CTAs of the step that owns stats slot i that finished their atomics
     uint32_t* cta_done;       // [max CTAs]: steps whose CTA of this index has finished (dr_step.cuh)
+    uint32_t* cta_ready;      // [max CTAs]: steps whose CTA of this index has published its state stores
     const uint8_t* occl_in;   // simulator occlusion bits per env (dr_set_occlusion_input) or NULL
 };
 

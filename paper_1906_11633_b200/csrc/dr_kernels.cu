@@ -239,7 +239,7 @@ __global__ void sync_init_kernel(DevPtrs p, unsigned long long t, uint32_t grid,
     // the slot of step t starts cleared and empty (as if step t - 1 had prepared it); every other
     // slot's previous owner counts as done
     if (i < N_STAT_SLOTS) p.done[i] = (i == (uint32_t)(t % N_STAT_SLOTS)) ? 0u : grid;
-    if (i < max_ctas) p.cta_done[i] = (uint32_t)t;     // steps < t finished
+    if (i < max_ctas) p.cta_done[i] = p.cta_ready[i] = (uint32_t)t;     // steps < t finished
     if (i == 0) {
         p.ctl[0] = t;
         p.ctl[4] = t * grid;   // the first ticket of step t

@@ -714,9 +714,10 @@ __device__ __forceinline__ uint32_t step_begin(const DevPtrs& p, uint32_t* s_t, 
         if (k == gridDim.x - 1u)
             asm volatile("st.release.gpu.global.u64 [%0], %1;" ::"l"(&p.ctl[0]), "l"((unsigned long long)t + 1ull) : "memory");
         // chained: this CTA works on the same tiles as the same-index CTA of step t - 1 (fixed grid,
-        // tile i on CTA i % G); start once that CTA has finished (its state stores published)
+        // tile i on CTA i % G); start once that CTA has published its state stores (cta_ready: before
+        // its stats atomics, which are not on this step's path)
         if (chain)
-            while (ld_acquire_u32(p.cta_done + blockIdx.x) != t) __nanosleep(64);
+            while (ld_acquire_u32(p.cta_ready + blockIdx.x) != t) __nanosleep(64);
         *s_t = t;
     }
     __syncthreads();
@@ -731,6 +732,13 @@ __device__ __forceinline__ void reduce_stats(const DevPtrs& p, const Acc& acc, u
     const int lane = tid & 31, wid = tid >> 5;
     constexpr int NW = NT / 32;
     __syncthreads();
+    // every state and output store of this CTA is issued: the same-index CTA of step t + 1 (same
+    // tiles) may start now -- the stats atomics below are off its path (their round trip and the
+    // fence behind them were ~0.7 us of config 2's 3.9 us step)
+    if (tid == 0) {
+        __threadfence();
+        st_release_u32(p.cta_ready + blockIdx.x, t + 1u);
+    }
     {
         // counts: one REDUX.SUM per slot (32-bit integer warp sums, exact); moments: fp64 butterflies
         auto redc = [&](int i, uint32_t x) {
@@ -771,8 +779,9 @@ __device__ __forceinline__ void reduce_stats(const DevPtrs& p, const Acc& acc, u
     if (tid == 0) {
         __threadfence();
         atomicAdd(p.done + (t % N_STAT_SLOTS), 1u);   // this CTA's atomics into slot t % 4 are in
-        // publish: the same-index CTA of step t + 1 (same tiles) may start; since it waited for this
-        // one, a step never completes before its predecessor, so stream order still means "all done"
+        // a step never completes before its predecessor (so stream order still means "all done"):
+        // this CTA ends only after the same-index CTA of step t - 1 has ended (long since, in practice)
+        while (ld_acquire_u32(p.cta_done + blockIdx.x) != t) __nanosleep(64);
         st_release_u32(p.cta_done + blockIdx.x, t + 1u);
     }
 }
