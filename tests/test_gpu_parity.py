@@ -206,6 +206,36 @@ def test_reset_kernel_layer_sets(torch_cuda, mask):
         ctx.close()
 
 
+def test_reset_mask_patterns(torch_cuda):
+    """The reset's scan schedule (CTA c owns the interleaved 32-env mask chunks c, c + G, ...): at
+    20,011 envs (626 chunks over the 592-CTA grid: some CTAs own two chunks, the last one a ragged
+    tail) a contiguous block, the first env alone, every other env and an explicit all-ones mask
+    each give the oracle's records and physics rows for every env, and the next step's stats slot
+    10 counts exactly the resets."""
+    torch = torch_cuda
+    P = presets.preset(FULL)
+    n = 20011
+    ctx = _ctx(P, n)
+    orc = _oracle(P, np.arange(n))
+    acts, obs = gen.frames(n, 1)
+    A, O = torch.from_numpy(acts[0]).cuda(), torch.from_numpy(obs[0]).cuda()
+    e = np.arange(n)
+    masks = [((e >= 9000) & (e < 17011)), e == 0, e % 2 == 1, np.ones(n, dtype=bool)]
+    try:
+        for m in masks:
+            m = m.astype(np.uint8)
+            ctx.reset(torch.from_numpy(m).cuda())
+            orc.reset(m)
+            torch.cuda.synchronize()
+            compare_records(ctx.export(), [orc.env(i) for i in range(n)], phys_g=ctx.phys(), strict_state=False)
+            ctx.step(A, O)
+            orc.step(acts[0], obs[0])
+            assert ctx.last_stats()[10] == int(m.sum())
+    finally:
+        ctx.close()
+        orc.close()
+
+
 def test_config1_free_running(torch_cuda):
     """BASELINE config 1: 4 envs x 50 steps, all layers, fixed seed; every output, state and
     stats slot each step (M1 free-running), with resets mid-run."""
