@@ -696,10 +696,29 @@ __device__ __forceinline__ void store_tile(uint32_t e0, uint32_t cnt, int tid, c
 // that starts early spins in a slot a finished CTA freed); chain = 0 (after a reset, dr_init or
 // dr_set_step_index): wait for the previous grid to complete.  Both step kernels chain (the latency
 // kernel's CTA c works on 32-env groups c, c + G, ... every step).
+#ifdef DR_PROBE_TIMING   // A/B probe only (scripts/probe_timing.py): per-CTA globaltimer stamps over the physics rows
+__device__ __forceinline__ unsigned long long gtime() {
+    unsigned long long v;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(v));
+    return v;
+}
+__device__ __forceinline__ unsigned long long* probe_slot(const DevPtrs& p, uint32_t t) {
+    return reinterpret_cast<unsigned long long*>(p.phys) + ((size_t)(t % 8u) * gridDim.x + blockIdx.x) * 8;
+}
+#define DR_PROBE(t, k) probe_slot(p, t)[k] = gtime()
+#else
+#define DR_PROBE(t, k) (void)0
+#endif
 __device__ __forceinline__ uint32_t step_begin(const DevPtrs& p, uint32_t* s_t, int chain) {
+#ifdef DR_PROBE_TIMING
+    const unsigned long long ts0 = gtime();
+#endif
     if (!chain) pdl_wait();   // before any global access (dr_device.cuh)
     if (threadIdx.x == 0) {
         const unsigned long long ticket = atomicAdd(&p.ctl[4], 1ull);
+#ifdef DR_PROBE_TIMING
+        const unsigned long long ts1 = gtime() + (ticket & 0ull);
+#endif
         const uint32_t t = (uint32_t)(ticket / gridDim.x);
         const uint32_t k = (uint32_t)(ticket - (unsigned long long)t * gridDim.x);
         if (k == 0) {
@@ -719,6 +738,11 @@ __device__ __forceinline__ uint32_t step_begin(const DevPtrs& p, uint32_t* s_t, 
         if (chain)
             while (ld_acquire_u32(p.cta_ready + blockIdx.x) != t) __nanosleep(64);
         *s_t = t;
+#ifdef DR_PROBE_TIMING
+        probe_slot(p, t)[0] = ts0;
+        probe_slot(p, t)[1] = ts1;
+        DR_PROBE(t, 2);
+#endif
     }
     __syncthreads();
     if (chain) pdl_trigger();   // ticket taken (and, for the first CTA, the next slot prepared)
@@ -728,6 +752,7 @@ template <uint32_t L, int NT = STEP_THREADS>
 __device__ __forceinline__ void reduce_stats(const DevPtrs& p, const Acc& acc, uint32_t my_envs, uint32_t t,
                                              double* s_red) {
     pdl_trigger();   // (unchained launches) this CTA's tiles are issued: the next step may launch
+    if (threadIdx.x == 0) DR_PROBE(t, 3);
     const int tid = threadIdx.x;
     const int lane = tid & 31, wid = tid >> 5;
     constexpr int NW = NT / 32;
@@ -738,7 +763,11 @@ __device__ __forceinline__ void reduce_stats(const DevPtrs& p, const Acc& acc, u
     // (st.release.gpu after the CTA barrier: the release is cumulative over the CTA's stores that
     // precede the barrier (PTX memory model), so no extra fence.sc -- measured: the MEMBAR.SC +
     // L1 invalidate it compiled to cost config 2 0.17 us per step)
-    if (tid == 0) st_release_u32(p.cta_ready + blockIdx.x, t + 1u);
+    if (tid == 0) {
+        DR_PROBE(t, 4);
+        st_release_u32(p.cta_ready + blockIdx.x, t + 1u);
+        DR_PROBE(t, 5);
+    }
     {
         // counts: one REDUX.SUM per slot (32-bit integer warp sums, exact); moments: fp64 butterflies
         auto redc = [&](int i, uint32_t x) {
@@ -783,6 +812,7 @@ __device__ __forceinline__ void reduce_stats(const DevPtrs& p, const Acc& acc, u
         // this CTA ends only after the same-index CTA of step t - 1 has ended (long since, in practice)
         while (ld_acquire_u32(p.cta_done + blockIdx.x) != t) __nanosleep(64);
         st_release_u32(p.cta_done + blockIdx.x, t + 1u);
+        DR_PROBE(t, 6);
     }
 }
 
