@@ -703,7 +703,7 @@ __device__ __forceinline__ unsigned long long gtime() {
     return v;
 }
 __device__ __forceinline__ unsigned long long* probe_slot(const DevPtrs& p, uint32_t t) {
-    return reinterpret_cast<unsigned long long*>(p.phys) + ((size_t)(t % 8u) * gridDim.x + blockIdx.x) * 8;
+    return reinterpret_cast<unsigned long long*>(p.phys) + ((size_t)(t % 8u) * gridDim.x + blockIdx.x) * 16;
 }
 #define DR_PROBE(t, k) probe_slot(p, t)[k] = gtime()
 #else

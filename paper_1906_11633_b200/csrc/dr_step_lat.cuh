@@ -461,5 +461,8 @@ __global__ void __launch_bounds__(LAT_THREADS, DR_LAT_MIN_CTAS) step_kernel_lat(
             }
         }
     }
+#ifdef DR_PROBE_TIMING
+    if (lane == 0) probe_slot(p, t)[8 + wid] = gtime();   // this warp's role done
+#endif
     reduce_stats<L, LAT_THREADS>(p, acc, my_envs, t, s_red);
 }

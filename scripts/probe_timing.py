@@ -37,7 +37,7 @@ def main():
     ph = np.ascontiguousarray(ctx.phys()).view(np.uint64).reshape(-1)
     ctx.close()
     G = int(os.environ.get("GRID", (n + 31) // 32 if n <= 16384 else min((n + 127) // 128, 592)))
-    a = ph[: 8 * G * 8].reshape(8, G, 8).astype(np.int64)
+    a = ph[: 8 * G * 16].reshape(8, G, 16).astype(np.int64)
     print(f"n_env {n} grid {G} last step {t_end - 1}")
     names = ["ticket", "ready-wait", "work", "reduce", "fence+release", "stats+done"]
     steps = [(t_end - 8 + i) for i in range(8)]
@@ -51,6 +51,9 @@ def main():
     print(f"  step period (first CTA starts) median {np.median(per):.0f} ns")
     print(f"  CTA c: next step's start - this step's ready: median {np.median(start):.0f} ns (negative = started before)")
     print(f"  CTA c: next step's wait done - this step's ready: median {np.median(hand):.0f} ns")
+    if n <= 16384:   # latency kernel: each warp role's finish, relative to the readiness wait
+        w = np.concatenate([a[t % 8, :, 8:16] - a[t % 8, :, 2:3] for t in steps[1:]])
+        print("  per-warp role done after the wait (median ns, warps 0-7):", [int(x) for x in np.median(w, axis=0)])
     span = [a[t % 8, :, 6].max() - a[t % 8, :, 0].min() for t in steps[1:]]
     print(f"  one step's span (first start -> last end) median {np.median(span):.0f} ns")
 
