@@ -299,7 +299,7 @@ def run_vision(args):
         host = [gen.images(NI, H, W, Cc, seed=presets.SEED_WORKLOAD + 101 * rank + k) for k in range(R)]
         X = [torch.from_numpy(h).cuda() for h in host]
         Y = [torch.empty(NI, H, W, Cc, dtype=torch.float32, device="cuda") for _ in range(R)]
-        ST = torch.empty(NI, 4, dtype=torch.float32, device="cuda")
+        ST = [torch.empty(NI, 4, dtype=torch.float32, device="cuda") for _ in range(R)]   # per-batch image stats
         SC = torch.empty(S, 64, dtype=torch.float32, device="cuda")
         torch.cuda.synchronize()
 
@@ -307,30 +307,41 @@ def run_vision(args):
 
         def one_step(t):
             # batch index b = t: fresh draws every step; images of rank r have global ids r * NI + i.
-            # The 64 scene draws (latency-bound, independent of the images) run on a side stream
-            # forked from and joined back into the step's stream, overlapping the augmentation.
+            # The 64 scene draws (latency-bound, independent of the images) run on a side stream,
+            # forked from the step stream and joined back into it once per run of steps (fork() /
+            # join()), so consecutive augmentations stay adjacent on their stream: a batch's
+            # clusters read their images while the previous batch is still writing (programmatic
+            # dependent launch; an event between two launches breaks that overlap).
             b = t
-            fork = torch.cuda.Event()
-            fork.record(stream)
-            side.wait_event(fork)
             vision.dr_scene_draw_batch(P, presets.SEED_DR, b, SC, sample_offset=rank * S, stream=side)
-            vision.dr_image_augment(P, presets.SEED_DR, b, X[t % R], Y[t % R], ST, image_offset=rank * NI,
+            vision.dr_image_augment(P, presets.SEED_DR, b, X[t % R], Y[t % R], ST[t % R], image_offset=rank * NI,
                                     stream=stream)
-            join = torch.cuda.Event()
-            join.record(side)
-            stream.wait_event(join)
 
+        def fork():
+            ev = torch.cuda.Event()
+            ev.record(stream)
+            side.wait_event(ev)
+
+        def join():
+            ev = torch.cuda.Event()
+            ev.record(side)
+            stream.wait_event(ev)
+
+        fork()
         for t in range(args.warmup):
             one_step(t)
+        join()
         torch.cuda.synchronize()
         sampler = ClockSampler(local)
         sampler.start()
         w0 = time.perf_counter()   # >= 1 s pre-roll at the timed load (clock coverage, see ClockSampler)
         t_base = args.warmup
         while True:
+            fork()
             for _ in range(20):
                 one_step(t_base)
                 t_base += 1
+            join()
             torch.cuda.synchronize()
             if time.perf_counter() - w0 >= 1.0:
                 break
@@ -343,8 +354,10 @@ def run_vision(args):
         evs = [torch.cuda.Event(enable_timing=True) for _ in range(2)]
         h0 = time.monotonic()
         evs[0].record(stream)
+        fork()
         for i in range(args.steps):
             one_step(t_base + i)
+        join()
         evs[1].record(stream)
         torch.cuda.synchronize()
         sampler.mark_timed(h0, time.monotonic())
@@ -382,7 +395,7 @@ def run_vision(args):
                 if i >= 2:
                     stream.wait_event(ev_down[b])   # step i-2's download has read Y[b]
                 vision.dr_scene_draw_batch(P, presets.SEED_DR, i, SC, sample_offset=rank * S, stream=stream)
-                vision.dr_image_augment(P, presets.SEED_DR, i, X[b], Y[b], ST, image_offset=rank * NI, stream=stream)
+                vision.dr_image_augment(P, presets.SEED_DR, i, X[b], Y[b], ST[b], image_offset=rank * NI, stream=stream)
                 ev_aug[b].record(stream)
                 s_down.wait_event(ev_aug[b])
                 with torch.cuda.stream(s_down):

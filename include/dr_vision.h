@@ -85,7 +85,10 @@ int dr_scene_draw_batch(const dr_vision_params* p, uint64_t seed, uint64_t batch
  * img_stats: device fp32 [n_images][4] = (mean, std, f, s), or NULL.
  * One thread-block cluster per image: the image is read from HBM once (TMA bulk copies into the
  * cluster's shared memory), reduced through distributed shared memory, and written once.
- * DR_EUNSUPPORTED if height * width * channels > DR_VIS_MAX_IMAGE_BYTES.  Asynchronous. */
+ * DR_EUNSUPPORTED if height * width * channels > DR_VIS_MAX_IMAGE_BYTES.  Asynchronous.
+ * Launched with programmatic dependent launch: a call directly behind another dr_image_augment
+ * on the same stream reads its images while that call is still writing (and writes early too
+ * when neither call's buffers overlap the other's); the results are those of stream order. */
 int dr_image_augment(const dr_vision_params* p, uint64_t seed, uint64_t batch_index, int64_t image_offset,
                      const uint8_t* images, int64_t n_images, int32_t height, int32_t width, int32_t channels,
                      float* out, float* img_stats, void* stream);

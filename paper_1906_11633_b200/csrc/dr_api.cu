@@ -346,6 +346,43 @@ void count_launch() {
     ++g_total_launches;
     if (g_ctx) g_ctx->launches++;
 }
+// Per-stream record of the last libdr launch (a small table; a stream missing from it reads as
+// "not an augmentation", the conservative answer).  Every libdr launch goes through here.
+namespace {
+struct StreamLast {
+    bool used = false;
+    void* stream = nullptr;
+    bool aug = false;
+    AugRec rec{};
+};
+StreamLast g_stream_last[8];
+int g_stream_next = 0;
+StreamLast* stream_slot(void* stream) {
+    for (auto& sl : g_stream_last)
+        if (sl.used && sl.stream == stream) return &sl;
+    return nullptr;
+}
+}  // namespace
+void note_stream_launch(void* stream, const AugRec* aug) {
+    StreamLast* sl = stream_slot(stream);
+    if (!sl) {
+        sl = &g_stream_last[g_stream_next];
+        g_stream_next = (g_stream_next + 1) % 8;
+    }
+    sl->used = true;
+    sl->stream = stream;
+    sl->aug = aug != nullptr;
+    if (aug) sl->rec = *aug;
+    // a chained step (no griddepcontrol.wait) may only follow a step of its context directly: the
+    // augmentation triggers its dependents at once, so a step behind it must wait for the grid
+    if (aug && g_ctx && static_cast<void*>(g_ctx->stream) == stream) g_ctx->chain_next = false;
+}
+bool last_launch_is_augment(void* stream, AugRec* prev) {
+    const StreamLast* sl = stream_slot(stream);
+    if (!sl || !sl->aug) return false;
+    *prev = sl->rec;
+    return true;
+}
 }  // namespace dr
 
 extern "C" {
@@ -516,6 +553,7 @@ int dr_init(const dr_params* params, int64_t n_env, uint64_t seed) {
     if ((e = launch_reset(P, nullptr, true, (uint32_t)n_env, c->reset_grid, s)) != cudaSuccess) return bail(e, "reset_kernel");
     c->launches = 2;
     g_total_launches += 2;
+    note_stream_launch(s, nullptr);
     g_ctx = c;
     g_err[0] = 0;
     return DR_OK;
@@ -555,6 +593,7 @@ int dr_reset(const uint8_t* env_mask) {
     c->chain_next = false;   // the next step must wait for the reset to complete
     c->launches++;
     ++g_total_launches;
+    note_stream_launch(c->stream, nullptr);
     return DR_OK;
 }
 
@@ -582,6 +621,7 @@ static int step_common(const float* actions, const float* raw_obs, float* out_ac
     c->t_host++;
     c->launches++;
     ++g_total_launches;
+    note_stream_launch(c->stream, nullptr);
     return DR_OK;
 }
 
@@ -747,6 +787,7 @@ int dr_set_step_index(uint64_t t) {
     if (e != cudaSuccess) return cuda_fail(e, "sync_init_kernel");
     c->launches++;
     ++g_total_launches;
+    note_stream_launch(c->stream, nullptr);
     CK(cudaStreamSynchronize(c->stream));
     c->t_host = t;
     c->chain_next = false;
@@ -774,6 +815,7 @@ int dr_state_export(void* host_dst, int64_t env_lo, int64_t env_hi) {
     if (e != cudaSuccess) return cuda_fail(e, "export_kernel");
     c->launches++;
     ++g_total_launches;
+    note_stream_launch(c->stream, nullptr);
     CK(cudaMemcpyAsync(host_dst, d, bytes, cudaMemcpyDeviceToHost, c->stream));
     CK(cudaFreeAsync(d, c->stream));
     CK(cudaStreamSynchronize(c->stream));
@@ -794,6 +836,7 @@ int dr_state_import(const void* host_src, int64_t env_lo, int64_t env_hi) {
     if (e != cudaSuccess) return cuda_fail(e, "import_kernel");
     c->launches += 2;   // import_kernel + import_phys_kernel
     g_total_launches += 2;
+    note_stream_launch(c->stream, nullptr);
     CK(cudaFreeAsync(d, c->stream));
     CK(cudaStreamSynchronize(c->stream));
     return DR_OK;
@@ -823,6 +866,7 @@ int dr_debug_philox(uint32_t domain, uint32_t channel, uint32_t block, uint32_t*
     if (e != cudaSuccess) return cuda_fail(e, "debug_philox_kernel");
     c->launches++;
     ++g_total_launches;
+    note_stream_launch(c->stream, nullptr);
     return DR_OK;
 }
 
@@ -837,6 +881,7 @@ int dr_debug_philox_keyed(const uint32_t* ctr_dev, const uint32_t* key_dev, uint
                                               static_cast<cudaStream_t>(stream));
     if (e != cudaSuccess) return cuda_fail(e, "debug_philox_keyed_kernel");
     ++g_total_launches;
+    note_stream_launch(stream, nullptr);
     return DR_OK;
 }
 

@@ -145,6 +145,19 @@ struct DevPtrs {
 // error / launch bookkeeping shared by every C-ABI entry point (dr_api.cu)
 int set_error(int code, const char* fmt, ...);   // records the message for dr_last_error(), returns code
 void count_launch();                              // one library kernel enqueued
+// The last libdr kernel enqueued on each stream (dr_api.cu), for programmatic-dependent-launch
+// decisions: an image augmentation may write early only behind the previous augmentation of its
+// stream (dr_vision.cu), and a chained step only directly behind a step of its context.
+struct AugRec {
+    const void* images;
+    size_t img_bytes;
+    const void* out;
+    size_t out_bytes;
+    const void* st;
+    size_t st_bytes;
+};
+void note_stream_launch(void* stream, const AugRec* aug);   // aug: the augmentation's buffers, or NULL (any other kernel)
+bool last_launch_is_augment(void* stream, AugRec* prev);    // and, if so, its buffers
 
 // launchers (dr_kernels.cu)
 cudaError_t upload_const(const DevConst& c, cudaStream_t s);

@@ -55,6 +55,8 @@ struct ImgArgs {
     uint32_t aligned;    // TMA + float4 path (E % 16 == 0, pointers 16-byte aligned)
     uint32_t batch;
     uint32_t image_offset;
+    uint32_t early_read;    // 1: this call may read its images before the previous kernel of the stream completed
+    uint32_t early_write;   // 1: ... and write its outputs
     double contrast_lo, contrast_range, noise_lo, noise_range;   // lo + (hi - lo) U, as the oracle
     double std_floor;
     PhiloxKeys keys;
@@ -150,7 +152,24 @@ __device__ __forceinline__ void nz_fold(const NzRaw& q, float kq, float z[8]) {
     }
 }
 
+// Programmatic dependent launch (the augment kernel goes out with
+// cudaLaunchAttributeProgrammaticStreamSerialization): every CTA lets the next kernel of the stream
+// launch at once, so the next batch's clusters take the SM slots this batch's clusters free and
+// read their images, reduce their moments and draw their first noise groups while this batch is
+// still writing (one batch is one wave of clusters that read all images, then write all outputs).
+// A call reads its images before the previous kernel of the stream has completed only when the
+// host saw that kernel is the previous augmentation of the same stream and its outputs do not
+// overlap these images (a.early_read), and writes (img_stats, out) early only when in addition
+// neither call's outputs overlap the other's images or outputs (a.early_write, dr_image_augment);
+// otherwise every CTA waits (griddepcontrol.wait) at its start, or before its first write.  Every
+// CTA waits before it exits, so no call completes before its predecessor.  Back-to-back batches of 192 images (A/B): 28.7 us per batch
+// without PDL, 27.3 with every write behind the wait, 21.5 with early writes.
+__device__ __forceinline__ void img_pdl_trigger() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
+__device__ __forceinline__ void img_pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+
 __global__ void __launch_bounds__(IMG_THREADS) image_augment_kernel(const ImgArgs a) {
+    img_pdl_trigger();
+    if (!a.early_read) img_pdl_wait();   // the previous kernel of the stream may have written the images
     extern __shared__ __align__(128) uint8_t s_img[];
     __shared__ __align__(8) uint64_t s_bar;
     __shared__ unsigned long long s_part[2];
@@ -252,6 +271,7 @@ __global__ void __launch_bounds__(IMG_THREADS) image_augment_kernel(const ImgArg
         Q += ld_dsmem_u64(smem_addr(&s_part[1]), q);
     }
     cluster_arrive();   // done reading the other CTAs' shared memory (matched by the wait at exit)
+    if (!a.early_write) img_pdl_wait();   // the previous kernel of the stream has completed: this CTA may write
 
     // ---- 3. normalise, contrast, noise ----
     const double mean = (double)S / (double)E;
@@ -321,6 +341,7 @@ __global__ void __launch_bounds__(IMG_THREADS) image_augment_kernel(const ImgArg
         }
     }
     cluster_wait();   // no CTA leaves while another may still read its s_part
+    img_pdl_wait();   // ... nor before the previous kernel of the stream has completed
 }
 
 // ---- appearance draws: one thread per sample, fp64 (no contraction in the decision chain) ----
@@ -542,6 +563,7 @@ int dr_scene_draw_batch(const dr_vision_params* p, uint64_t seed, uint64_t batch
     cudaError_t e = cudaGetLastError();
     if (e != cudaSuccess) return set_error(DR_ECUDA, "scene_draw_kernel: %s", cudaGetErrorString(e));
     count_launch();
+    note_stream_launch(stream, nullptr);
     return DR_OK;
 }
 
@@ -589,6 +611,7 @@ int dr_pose_augment(const dr_pose_aug_params* p, uint64_t seed, uint64_t batch_i
     cudaError_t e = cudaGetLastError();
     if (e != cudaSuccess) return set_error(DR_ECUDA, "pose_augment_kernel: %s", cudaGetErrorString(e));
     count_launch();
+    note_stream_launch(stream, nullptr);
     return DR_OK;
 }
 
@@ -701,22 +724,49 @@ int dr_image_augment(const dr_vision_params* p, uint64_t seed, uint64_t batch_in
     a.noise_range = p->noise_std_hi - p->noise_std_lo;
     a.std_floor = p->std_floor;
     a.keys = make_keys(seed);
+    // early reads / writes only directly behind the previous augmentation of this stream (the last
+    // libdr launch on it): reads when its outputs do not overlap these images (RAW), writes when in
+    // addition this call's outputs overlap neither its outputs (WAW) nor its images (WAR); a user
+    // kernel in between completes before this call starts (it does not trigger its dependents
+    // early), so it needs no check
+    const size_t out_bytes = (size_t)n_images * E * 4, st_bytes = img_stats ? (size_t)n_images * 16 : 0;
+    const auto disjoint = [](const void* a0, size_t na, const void* b0, size_t nb) {
+        const uintptr_t a1 = (uintptr_t)a0, b1 = (uintptr_t)b0;
+        return na == 0 || nb == 0 || a1 + na <= b1 || b1 + nb <= a1;
+    };
+    AugRec prev{};
+    const AugRec cur{images, (size_t)n_images * E, out, out_bytes, img_stats, st_bytes};
+    const bool early_read = last_launch_is_augment(stream, &prev) &&
+                            disjoint(cur.images, cur.img_bytes, prev.out, prev.out_bytes) &&
+                            disjoint(cur.images, cur.img_bytes, prev.st, prev.st_bytes);
+    const bool early = early_read &&
+                       disjoint(cur.out, cur.out_bytes, prev.out, prev.out_bytes) &&
+                       disjoint(cur.out, cur.out_bytes, prev.st, prev.st_bytes) &&
+                       disjoint(cur.out, cur.out_bytes, prev.images, prev.img_bytes) &&
+                       disjoint(cur.st, cur.st_bytes, prev.out, prev.out_bytes) &&
+                       disjoint(cur.st, cur.st_bytes, prev.st, prev.st_bytes) &&
+                       disjoint(cur.st, cur.st_bytes, prev.images, prev.img_bytes);
+    a.early_read = early_read ? 1u : 0u;
+    a.early_write = early ? 1u : 0u;
     cudaError_t e = cudaSuccess;
     cudaLaunchConfig_t cfg{};
     cfg.gridDim = dim3((unsigned)(n_images * K), 1, 1);
     cfg.blockDim = dim3(IMG_THREADS, 1, 1);
     cfg.dynamicSmemBytes = slice;
     cfg.stream = static_cast<cudaStream_t>(stream);
-    cudaLaunchAttribute attr[1];
+    cudaLaunchAttribute attr[2];
     attr[0].id = cudaLaunchAttributeClusterDimension;
     attr[0].val.clusterDim.x = K;
     attr[0].val.clusterDim.y = 1;
     attr[0].val.clusterDim.z = 1;
+    attr[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;   // see image_augment_kernel
+    attr[1].val.programmaticStreamSerializationAllowed = 1;
     cfg.attrs = attr;
-    cfg.numAttrs = 1;
+    cfg.numAttrs = 2;
     e = cudaLaunchKernelEx(&cfg, image_augment_kernel, a);
     if (e != cudaSuccess) return set_error(DR_ECUDA, "image_augment_kernel: %s", cudaGetErrorString(e));
     count_launch();
+    note_stream_launch(stream, &cur);
     return DR_OK;
 }
 

@@ -114,6 +114,65 @@ def test_image_augment_batch_size_invariance_paper_shape(torch_cuda):
     assert np.array_equal(sa, np.concatenate([p[1] for p in parts]))
 
 
+def test_image_augment_back_to_back_stream_order(torch_cuda):
+    """Consecutive dr_image_augment calls on one stream overlap (programmatic dependent launch:
+    the next call reads while the previous one writes, and writes early when neither call's
+    buffers overlap the other's) but keep stream-order results, bit for bit against single calls:
+      * disjoint buffers (the early-write path), 12 calls of the paper's batch shape in a ring;
+      * every call into the same output and stats buffers (WAW: the last call's values remain);
+      * a call whose images are the previous call's output bytes (RAW: it must read them finished);
+      * a call writing over the previous call's images (WAR)."""
+    from paper_1906_11633_b200 import vision
+    torch = torch_cuda
+    P = presets.vision_preset()
+    VP = vision.params_from_preset(P)
+    imgs = gen.images(192, 200, 200, 3, seed=21)
+    small = gen.images(8, 64, 48, 3, seed=22)
+    s = torch.cuda.Stream()
+    with torch.cuda.stream(s):
+        X = torch.from_numpy(imgs).cuda()
+        ref = {b: _augment_gpu(torch, P, imgs, b) for b in range(12)}
+        # disjoint ring of 4 outputs / stats, 12 back-to-back calls (the last 4 remain)
+        Y = [torch.empty(X.shape, dtype=torch.float32, device="cuda") for _ in range(4)]
+        ST = [torch.empty(192, 4, dtype=torch.float32, device="cuda") for _ in range(4)]
+        for b in range(12):
+            vision.dr_image_augment(VP, SEED, b, X, Y[b % 4], ST[b % 4], stream=s)
+        s.synchronize()
+        for b in range(8, 12):
+            assert np.array_equal(Y[b % 4].cpu().numpy(), ref[b][0]) and np.array_equal(ST[b % 4].cpu().numpy(), ref[b][1]), b
+        # WAW: every call into the same buffers -- the last one's values remain
+        y, st = Y[0], ST[0]
+        for b in range(6):
+            vision.dr_image_augment(VP, SEED, b, X, y, st, stream=s)
+        s.synchronize()
+        assert np.array_equal(y.cpu().numpy(), ref[5][0]) and np.array_equal(st.cpu().numpy(), ref[5][1])
+        # RAW: the next call's images are the bytes of the previous call's output
+        xs = torch.from_numpy(small).cuda()
+        y1 = torch.empty(xs.shape, dtype=torch.float32, device="cuda")
+        nbytes = y1.numel() * 4
+        y2 = torch.empty((1, nbytes), dtype=torch.float32, device="cuda")
+        vision.dr_image_augment(VP, SEED, 0, xs, y1, None, stream=s)
+        as_img = y1.view(torch.uint8).view(1, nbytes, 1, 1)
+        vision.dr_image_augment(VP, SEED, 1, as_img, y2.view(1, nbytes, 1, 1), None, stream=s)
+        s.synchronize()
+        first = _augment_gpu(torch, P, small, 0, stats=False)[0]
+        again = _augment_gpu(torch, P, np.ascontiguousarray(first).view(np.uint8).reshape(1, nbytes, 1, 1), 1,
+                             stats=False)[0]
+        assert np.array_equal(y2.view(1, nbytes, 1, 1).cpu().numpy(), again)
+        # WAR: a call writing over the previous call's images (as raw bytes)
+        xb = torch.from_numpy(small).cuda()
+        big = torch.empty(xb.numel(), dtype=torch.float32, device="cuda")   # 4x the bytes of xb
+        big_u8 = big.view(torch.uint8)
+        big_u8[: xb.numel()].copy_(xb.view(-1))
+        src = big_u8[: xb.numel()].view(xb.shape)
+        ya = torch.empty(xb.shape, dtype=torch.float32, device="cuda")
+        vision.dr_image_augment(VP, SEED, 2, src, ya, None, stream=s)
+        vision.dr_image_augment(VP, SEED, 3, xs, big.view(xb.shape), None, stream=s)   # overwrites src
+        s.synchronize()
+        assert np.array_equal(ya.cpu().numpy(), _augment_gpu(torch, P, small, 2, stats=False)[0])
+        assert np.array_equal(big.view(xb.shape).cpu().numpy(), _augment_gpu(torch, P, small, 3, stats=False)[0])
+
+
 def test_image_augment_rejects(torch_cuda):
     from paper_1906_11633_b200 import dr, vision
     torch = torch_cuda
