@@ -34,6 +34,7 @@ N_GLOBAL_1M = 1 << 20
 # algorithmic bytes per env-step: inputs + outputs + episode record read
 # + state read/write, for the layer sets the configs use
 BYTES_FULL = 184 + 220 + 344 + 480
+ST_BYTES_PER_ENV = 80 * 4   # state planes per env (dr_internal.h ST_PLANES)
 BYTES_CFG2 = 184 + 220 + 332 + 160 + 4   # + the flags word (FRESH marker) read per step
 
 
@@ -637,6 +638,15 @@ def main():
                 "kernel_ms_avg": kern_ms, "kernel_ms_median": per[len(per) // 2]}
     if split:
         roofline["split"] = split
+    # the working set every step touches (records 384 B + state planes 320 B + the 4-frame input ring
+    # + one output set per env): at config 3's 65,536 envs (109 MB) it largely fits the 126 MB L2, so
+    # part of the algorithmic bytes come from L2 and frac can exceed 1; at 1M (1.7 GB) it cannot
+    l2 = int(getattr(torch.cuda.get_device_properties(torch.cuda.current_device()), "L2_cache_size", 0) or 0)
+    ws = n * (384 + ST_BYTES_PER_ENV + 4 * 184 + 220)
+    roofline["working_set_bytes"] = ws
+    roofline["l2_resident"] = bool(l2 and ws <= 1.25 * l2)
+    if roofline["l2_resident"]:
+        roofline["note"] = "working set ~ L2 size: part of the bytes are L2 hits; frac against HBM overstates"
 
     # ---- e2e: through dr_step_host with pinned host buffers (copies inside the timed region) ----
     e2e = None
