@@ -270,24 +270,24 @@ cudaError_t upload_params(Ctx* c, const dr_params& p, const char** what) {
             const bool on_phys = (lm & DR_PHYS) != 0;
             switch (d.kind) {
             case DR_PHYS_UNIFORM_SCALE:   // base * (a + (b - a) U)
-                if (on_phys) { A = (float)d.a; B = (float)(d.b - d.a); C0 = 0.f; C1 = (float)d.base; src = (uint32_t)u; }
+                if (on_phys) { A = (float)d.a; B = (float)(d.b - d.a); C0 = 0.f; C1 = (float)d.base; src = rs_slot((uint32_t)u); }
                 ++u;
                 break;
             case DR_PHYS_LOGUNIFORM_SCALE:   // base * exp(ln a + (ln b - ln a) U) = base * 2^(log2 a + log2(b/a) U)
                 if (on_phys) {
                     A = (float)std::log2(d.a); B = (float)(std::log2(d.b) - std::log2(d.a)); C0 = 0.f; C1 = (float)d.base;
-                    src = (uint32_t)u | RS_EXP;
+                    src = rs_slot((uint32_t)u) | RS_EXP;
                 }
                 ++u;
                 break;
             case DR_PHYS_ADD_GAUSS:   // base + sigma z
-                if (on_phys) { B = (float)d.a; C0 = (float)d.base; C1 = 1.f; src = RS_OFF_NORMAL + (uint32_t)n; }
+                if (on_phys) { B = (float)d.a; C0 = (float)d.base; C1 = 1.f; src = RS_OFF_NORMAL + rs_slot((uint32_t)n); }
                 ++n;
                 break;
             case DR_PHYS_MUL_LOGNORMAL:   // base * exp(sigma z) = base * 2^(sigma log2(e) z)
                 if (on_phys) {
                     B = (float)(d.a * 1.4426950408889634074); C0 = 0.f; C1 = (float)d.base;
-                    src = (RS_OFF_NORMAL + (uint32_t)n) | RS_EXP;
+                    src = (RS_OFF_NORMAL + rs_slot((uint32_t)n)) | RS_EXP;
                 }
                 ++n;
                 break;

@@ -124,6 +124,9 @@ struct DevConst {
 // (offset u), the n-th normal (offset 256 + n) or the constant 0 (offset 512, draw-free kinds).
 constexpr uint32_t RS_EXP = 1u << 31;
 constexpr uint32_t RS_OFF_NORMAL = MAX_PHYS, RS_OFF_ZERO = 2 * MAX_PHYS;
+// Buffer word of the i-th uniform (or, + RS_OFF_NORMAL, the i-th normal): draw j of Philox block b
+// (i = 4 b + j) at j * 64 + b, bank-conflict-free for the reset's physics-row evaluation.
+constexpr uint32_t rs_slot(uint32_t i) { return (i & 3u) * 64u + (i >> 2); }
 
 // Pointers of the device workspace.
 struct DevPtrs {

@@ -139,10 +139,11 @@ __device__ __forceinline__ float reset_mass(uint32_t g, uint32_t k, const float4
     const float4 d = s_pd[pd_slot(mi)];
     const uint32_t o = s_src[(((mi & 7) >> 2) * 32 + (mi >> 3)) * 4 + (mi & 3)], off = o & ~RS_EXP;
     float x = 0.f;
+    // buffer slot j * 64 + b (rs_slot) -> draw j of Philox block b
     if (off < RS_OFF_NORMAL) {                       // uniform-kind parameter u: word u % 4 of block u / 4
-        x = uni(selw(philox(g, k, CH_PHYS_U, off >> 2), off & 3u));
+        x = uni(selw(philox(g, k, CH_PHYS_U, off & 63u), off >> 6));
     } else if (off < RS_OFF_ZERO) {                  // normal-kind parameter n: normal n % 4 of block n / 4
-        const uint32_t n = off - RS_OFF_NORMAL;
+        const uint32_t sl = off - RS_OFF_NORMAL, n = ((sl & 63u) << 2) | (sl >> 6);
         const uint4 w = philox(g, k, CH_PHYS_N, n >> 2);
         float z0, z1;
         if (n & 2u) box_muller(w.z, w.w, z0, z1);
@@ -256,17 +257,28 @@ __device__ __forceinline__ void reset_phys_warp(const DevPtrs& p, uint32_t e, ui
     // uniform-kind parameter u uses word u % 4 of block u / 4 (channel PHYS_U); normal-kind
     // parameter n uses normal n % 4 of block n / 4 (channel PHYS_N).  Lane l draws uniform block b and
     // normal block b (b = l, l + 32) together: two independent Philox chains interleave.
+    // Draw j of block b sits at buffer word rs_slot(4 b + j) = j * 64 + b (dr_internal.h), so the
+    // evaluation's reads -- lane l mostly needs draws 4 l .. 4 l + 3 -- hit 32 different banks
+    // (the block-contiguous layout made them 4-way bank conflicts).
     const int nb = max(nub, nnb);
     for (int b = lane; b < nb; b += 32) {
+        float4 zu = make_float4(0.f, 0.f, 0.f, 0.f), zn = zu;
         if (b < nub && b < nnb) {
             const Normals8 v = phys_pair_block(g, k, (uint32_t)b);
-            reinterpret_cast<float4*>(dr)[b] = v.a;
-            reinterpret_cast<float4*>(dr + MAX_PHYS)[b] = v.b;
+            zu = v.a;
+            zn = v.b;
         } else if (b < nub) {
             const uint4 w = philox(g, k, CH_PHYS_U, (uint32_t)b);
-            reinterpret_cast<float4*>(dr)[b] = make_float4(uni(w.x), uni(w.y), uni(w.z), uni(w.w));
+            zu = make_float4(uni(w.x), uni(w.y), uni(w.z), uni(w.w));
         } else {
-            reinterpret_cast<float4*>(dr + MAX_PHYS)[b] = normals4_block(g, k, CH_PHYS_N, (uint32_t)b);
+            zn = normals4_block(g, k, CH_PHYS_N, (uint32_t)b);
+        }
+        if (b < nub) {
+            dr[b] = zu.x; dr[64 + b] = zu.y; dr[128 + b] = zu.z; dr[192 + b] = zu.w;
+        }
+        if (b < nnb) {
+            float* q = dr + MAX_PHYS;
+            q[b] = zn.x; q[64 + b] = zn.y; q[128 + b] = zn.z; q[192 + b] = zn.w;
         }
     }
     __syncwarp();
