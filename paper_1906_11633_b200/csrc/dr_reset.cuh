@@ -89,7 +89,7 @@ __device__ __noinline__ Normals8 normals8_block(uint32_t g, uint32_t k, uint32_t
     return z;
 }
 // Physics draws of block b: 4 uniforms of PHYS_U block b (a) and 4 normals of PHYS_N block b (b).
-__device__ __noinline__ Normals8 phys_pair_block(uint32_t g, uint32_t k, uint32_t b) {
+__device__ __forceinline__ Normals8 phys_pair_block(uint32_t g, uint32_t k, uint32_t b) {
     const uint4 wu = philox(g, k, CH_PHYS_U, b);
     const uint4 wn = philox(g, k, CH_PHYS_N, b);
     Normals8 z;
