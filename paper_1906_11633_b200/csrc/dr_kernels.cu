@@ -282,3 +282,18 @@ cudaError_t launch_import(const DevPtrs& p, const void* src, uint32_t lo, uint32
 }
 
 }  // namespace dr
+
+#ifdef DR_PROBE_TIMING
+// A/B probe only: read (or, reset_min != 0, re-arm) the reset kernel's per-CTA stamps.
+extern "C" int dr_debug_probe_read(void* dst, size_t bytes, int reset_min) {
+    if (reset_min) {   // slot 5 (first warp done) collects a minimum
+        static unsigned long long init[4096][8];
+        for (auto& r : init) {
+            for (auto& v : r) v = 0ull;
+            r[5] = ~0ull;
+        }
+        return (int)cudaMemcpyToSymbol(dr::g_probe_reset, init, sizeof(init));
+    }
+    return (int)cudaMemcpyFromSymbol(dst, dr::g_probe_reset, bytes < sizeof(dr::g_probe_reset) ? bytes : sizeof(dr::g_probe_reset));
+}
+#endif

@@ -310,6 +310,17 @@ __device__ __forceinline__ void reset_phys_warp(const DevPtrs& p, uint32_t e, ui
     }
 }
 
+#ifdef DR_PROBE_TIMING   // A/B probe only (scripts/probe_reset_timing.py): per-CTA globaltimer stamps and SM id
+__device__ unsigned long long g_probe_reset[4096][8];
+__device__ __forceinline__ unsigned long long rgtime() {
+    unsigned long long v;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(v));
+    return v;
+}
+#define RPROBE(k) do { if (threadIdx.x == 0 && blockIdx.x < 4096) g_probe_reset[blockIdx.x][k] = rgtime(); } while (0)
+#else
+#define RPROBE(k) (void)0
+#endif
 __global__ void __launch_bounds__(RH_THREADS, DR_RH_MINB) reset_kernel(DevPtrs p, const uint8_t* __restrict__ mask, int first,
                                                               uint32_t n_env) {
     __shared__ float4 s_pd[MAX_PHYS];           // transposed: parameter q at pd_slot(q)
@@ -319,7 +330,16 @@ __global__ void __launch_bounds__(RH_THREADS, DR_RH_MINB) reset_kernel(DevPtrs p
     __shared__ __align__(16) float s_dr[RH_THREADS / 32][RH_DRAW];
     __shared__ uint32_t s_n[1], s_next[1];
     const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
+    RPROBE(0);
+#ifdef DR_PROBE_TIMING
+    if (threadIdx.x == 0 && blockIdx.x < 4096) {
+        uint32_t smid;
+        asm volatile("mov.u32 %0, %%smid;" : "=r"(smid));
+        g_probe_reset[blockIdx.x][6] = smid;
+    }
+#endif
     pdl_wait();   // before any global access (dr_device.cuh)
+    RPROBE(1);
     constexpr int NWR = RH_THREADS / 32;
     static_assert(RH_PASS % (32 * NWR) == 0, "pass = whole chunks per warp");
     stage_phys_tables(p, s_pd, s_src, tid, RH_THREADS);
@@ -386,8 +406,16 @@ __global__ void __launch_bounds__(RH_THREADS, DR_RH_MINB) reset_kernel(DevPtrs p
             cp_commit();
             cp_wait<0>();
             __syncthreads();
+            RPROBE(2);
             work(0, s_n[0], &s_next[0]);
+#ifdef DR_PROBE_TIMING
+            if ((threadIdx.x & 31) == 0 && blockIdx.x < 4096) {
+                atomicMax(&g_probe_reset[blockIdx.x][4], rgtime());   // last warp done
+                atomicMin(&g_probe_reset[blockIdx.x][5], rgtime());   // first warp done
+            }
+#endif
             __syncthreads();
+            RPROBE(3);
         }
     }
     pdl_trigger();
