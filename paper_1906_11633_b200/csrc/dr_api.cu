@@ -352,7 +352,7 @@ namespace {
 struct StreamLast {
     bool used = false;
     void* stream = nullptr;
-    bool aug = false;
+    int kind = LAUNCH_OTHER;
     AugRec rec{};
 };
 StreamLast g_stream_last[8];
@@ -363,7 +363,7 @@ StreamLast* stream_slot(void* stream) {
     return nullptr;
 }
 }  // namespace
-void note_stream_launch(void* stream, const AugRec* aug) {
+void note_stream_launch(void* stream, const AugRec* aug, int kind) {
     StreamLast* sl = stream_slot(stream);
     if (!sl) {
         sl = &g_stream_last[g_stream_next];
@@ -371,7 +371,7 @@ void note_stream_launch(void* stream, const AugRec* aug) {
     }
     sl->used = true;
     sl->stream = stream;
-    sl->aug = aug != nullptr;
+    sl->kind = aug ? LAUNCH_AUGMENT : kind;
     if (aug) sl->rec = *aug;
     // a chained step (no griddepcontrol.wait) may only follow a step of its context directly: the
     // augmentation triggers its dependents at once, so a step behind it must wait for the grid
@@ -379,9 +379,13 @@ void note_stream_launch(void* stream, const AugRec* aug) {
 }
 bool last_launch_is_augment(void* stream, AugRec* prev) {
     const StreamLast* sl = stream_slot(stream);
-    if (!sl || !sl->aug) return false;
+    if (!sl || sl->kind != LAUNCH_AUGMENT) return false;
     *prev = sl->rec;
     return true;
+}
+int last_launch_kind(void* stream) {
+    const StreamLast* sl = stream_slot(stream);
+    return sl ? sl->kind : LAUNCH_UNKNOWN;
 }
 }  // namespace dr
 
@@ -588,7 +592,10 @@ int dr_reset(const uint8_t* env_mask) {
     Ctx* c = g_ctx;
     if (!c) return fail(DR_ENOTINIT, "dr_reset: no context");
     if (g_sticky) return fail(DR_ECUDA, "sticky CUDA error: %s", g_err);
-    cudaError_t e = launch_reset(c->p, env_mask, false, (uint32_t)c->n_env, c->reset_grid, c->stream);
+    // the scan may overlap the previous kernel only if that is a step (it writes neither masks nor
+    // episode counters); behind anything else (another reset: episode counters) the reset waits first
+    const bool early_scan = last_launch_kind(static_cast<void*>(c->stream)) == LAUNCH_STEP;
+    cudaError_t e = launch_reset(c->p, env_mask, false, (uint32_t)c->n_env, c->reset_grid, c->stream, early_scan);
     if (e != cudaSuccess) return cuda_fail(e, "reset_kernel");
     c->chain_next = false;   // the next step must wait for the reset to complete
     c->launches++;
@@ -621,7 +628,7 @@ static int step_common(const float* actions, const float* raw_obs, float* out_ac
     c->t_host++;
     c->launches++;
     ++g_total_launches;
-    note_stream_launch(c->stream, nullptr);
+    note_stream_launch(c->stream, nullptr, LAUNCH_STEP);
     return DR_OK;
 }
 

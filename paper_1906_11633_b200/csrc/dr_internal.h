@@ -159,13 +159,16 @@ struct AugRec {
     const void* st;
     size_t st_bytes;
 };
-void note_stream_launch(void* stream, const AugRec* aug);   // aug: the augmentation's buffers, or NULL (any other kernel)
+enum : int { LAUNCH_UNKNOWN = -1, LAUNCH_OTHER = 0, LAUNCH_AUGMENT = 1, LAUNCH_STEP = 2 };
+// aug: the augmentation's buffers (kind LAUNCH_AUGMENT), or NULL with kind LAUNCH_OTHER / LAUNCH_STEP
+void note_stream_launch(void* stream, const AugRec* aug, int kind = LAUNCH_OTHER);
 bool last_launch_is_augment(void* stream, AugRec* prev);    // and, if so, its buffers
+int last_launch_kind(void* stream);                         // LAUNCH_* (UNKNOWN if not in the table)
 
 // launchers (dr_kernels.cu)
 cudaError_t upload_const(const DevConst& c, cudaStream_t s);
 cudaError_t launch_reset(const DevPtrs& p, const uint8_t* mask, bool first, uint32_t n_env,
-                         int grid, cudaStream_t s);
+                         int grid, cudaStream_t s, bool early_scan = false);
 cudaError_t launch_step(const DevPtrs& p, uint32_t layer_mask, const float* actions,
                         const float* raw_obs, float* out_actions, float* out_obs, float* out_dt,
                         float* out_force, float* out_sub, uint32_t n_env, int grid, int chain, cudaStream_t s);

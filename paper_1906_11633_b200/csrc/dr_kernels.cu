@@ -169,8 +169,8 @@ static cudaError_t launch_k(void (*kernel)(KArgs...), int grid, int block, size_
 }
 
 cudaError_t launch_reset(const DevPtrs& p, const uint8_t* mask, bool first, uint32_t n_env, int grid,
-                         cudaStream_t s) {
-    return launch_k(reset_kernel, grid, RH_THREADS, 0, s, p, mask, first ? 1 : 0, n_env);
+                         cudaStream_t s, bool early_scan) {
+    return launch_k(reset_kernel, grid, RH_THREADS, 0, s, p, mask, first ? 1 : 0, n_env, early_scan ? 1 : 0);
 }
 
 int reset_grid_for(uint32_t n_env, int sm_count) {

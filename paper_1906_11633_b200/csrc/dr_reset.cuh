@@ -321,8 +321,13 @@ __device__ __forceinline__ unsigned long long rgtime() {
 #else
 #define RPROBE(k) (void)0
 #endif
+// early_scan != 0 (the host saw the previous libdr launch on the stream is a step kernel, which
+// writes neither masks nor episode counters nor the physics tables): the first pass's table staging
+// and mask scan run before griddepcontrol.wait, overlapping the step's tail; every write (records,
+// physics rows, FRESH flags) still follows the wait.  Otherwise (e.g. two resets back to back: the
+// previous one wrote the episode counters) the wait comes first.
 __global__ void __launch_bounds__(RH_THREADS, DR_RH_MINB) reset_kernel(DevPtrs p, const uint8_t* __restrict__ mask, int first,
-                                                              uint32_t n_env) {
+                                                              uint32_t n_env, int early_scan) {
     __shared__ float4 s_pd[MAX_PHYS];           // transposed: parameter q at pd_slot(q)
     __shared__ __align__(16) uint32_t s_src[MAX_PHYS];   // transposed: lane l's quad h at [(h * 32 + l) * 4]
     __shared__ uint32_t s_env[1][RH_PASS];
@@ -338,7 +343,8 @@ __global__ void __launch_bounds__(RH_THREADS, DR_RH_MINB) reset_kernel(DevPtrs p
         g_probe_reset[blockIdx.x][6] = smid;
     }
 #endif
-    pdl_wait();   // before any global access (dr_device.cuh)
+    bool waited = !early_scan;
+    if (waited) pdl_wait();   // before any global access (dr_device.cuh)
     RPROBE(1);
     constexpr int NWR = RH_THREADS / 32;
     static_assert(RH_PASS % (32 * NWR) == 0, "pass = whole chunks per warp");
@@ -406,6 +412,10 @@ __global__ void __launch_bounds__(RH_THREADS, DR_RH_MINB) reset_kernel(DevPtrs p
             cp_commit();
             cp_wait<0>();
             __syncthreads();
+            if (!waited) {   // the first pass's reads are done: now the previous kernel must be complete
+                pdl_wait();
+                waited = true;
+            }
             RPROBE(2);
             work(0, s_n[0], &s_next[0]);
 #ifdef DR_PROBE_TIMING
@@ -418,6 +428,7 @@ __global__ void __launch_bounds__(RH_THREADS, DR_RH_MINB) reset_kernel(DevPtrs p
             RPROBE(3);
         }
     }
+    if (!waited) pdl_wait();   // (a CTA without a pass) before the global atomic below
     pdl_trigger();
     if (!first && applied) atomicAdd(&p.ctl[2], (unsigned long long)applied);
 }
