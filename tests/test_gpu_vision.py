@@ -173,6 +173,43 @@ def test_image_augment_back_to_back_stream_order(torch_cuda):
         assert np.array_equal(big.view(xb.shape).cpu().numpy(), _augment_gpu(torch, P, small, 3, stats=False)[0])
 
 
+def test_image_augment_between_steps_on_the_context_stream(torch_cuda):
+    """An augmentation enqueued between two dr_step calls on the DR context's stream (it triggers
+    its dependents at once, so the second step must not chain on the first without waiting): the
+    steps' outputs equal those of the same steps without the augmentation in between, and the
+    augmentation's output equals a single call's."""
+    from paper_1906_11633_b200 import DRContext, vision
+    torch = torch_cuda
+    P = presets.vision_preset()
+    imgs = gen.images(192, 200, 200, 3, seed=31)
+    ref_img = _augment_gpu(torch, P, imgs, 7)[0]
+    n = 65536
+    acts, obs = gen.frames(n, 3)
+    outs = []
+    for with_aug in (False, True):
+        s = torch.cuda.Stream()
+        with torch.cuda.stream(s):
+            ctx = DRContext(presets.preset(presets.FULL), n, SEED, stream=s)
+            X = torch.from_numpy(imgs).cuda()
+            Y = torch.empty(X.shape, dtype=torch.float32, device="cuda")
+            A = [torch.from_numpy(a).cuda() for a in acts]
+            O = [torch.from_numpy(o).cuda() for o in obs]
+            bufs = [(torch.empty(n, 20, device="cuda"), torch.empty(n, 22, device="cuda"),
+                     torch.empty(n, 10, device="cuda"), torch.empty(n, 3, device="cuda")) for _ in range(3)]
+            for t in range(3):   # no copies in between: the launches stay adjacent on the stream
+                ctx.step(A[t], O[t], outs=bufs[t])
+                if with_aug and t < 2:
+                    vision.dr_image_augment(vision.params_from_preset(P), SEED, 7, X, Y, None, stream=s)
+            s.synchronize()
+            got = [(b[0].cpu().numpy(), b[1].cpu().numpy()) for b in bufs]
+            if with_aug:
+                assert np.array_equal(Y.cpu().numpy(), ref_img)
+            ctx.close()
+        outs.append(got)
+    for (a0, o0), (a1, o1) in zip(*outs):
+        assert np.array_equal(a0, a1) and np.array_equal(o0, o1)
+
+
 def test_image_augment_rejects(torch_cuda):
     from paper_1906_11633_b200 import dr, vision
     torch = torch_cuda
