@@ -216,8 +216,8 @@ def test_reset_mask_patterns(torch_cuda):
     """The reset's scan schedule (CTA c owns the interleaved 32-env mask chunks c, c + G, ...): at
     20,011 envs (626 chunks over the 592-CTA grid: some CTAs own two chunks, the last one a ragged
     tail) a contiguous block, the first env alone, every other env and an explicit all-ones mask
-    each give the oracle's records and physics rows for every env, and the next step's stats slot
-    10 counts exactly the resets."""
+    each give the oracle's records and physics rows for every env, as does dr_reset(NULL) (every
+    env), and the next step's stats slot 10 counts exactly the resets."""
     torch = torch_cuda
     P = presets.preset(FULL)
     n = 20011
@@ -226,11 +226,12 @@ def test_reset_mask_patterns(torch_cuda):
     acts, obs = gen.frames(n, 1)
     A, O = torch.from_numpy(acts[0]).cuda(), torch.from_numpy(obs[0]).cuda()
     e = np.arange(n)
-    masks = [((e >= 9000) & (e < 17011)), e == 0, e % 2 == 1, np.ones(n, dtype=bool)]
+    masks = [((e >= 9000) & (e < 17011)), e == 0, e % 2 == 1, np.ones(n, dtype=bool), None]
     try:
         for m in masks:
-            m = m.astype(np.uint8)
-            ctx.reset(torch.from_numpy(m).cuda())
+            dev = None if m is None else torch.from_numpy(m.astype(np.uint8)).cuda()   # None: dr_reset(NULL) = all
+            m = np.ones(n, np.uint8) if m is None else m.astype(np.uint8)
+            ctx.reset(dev)
             orc.reset(m)
             torch.cuda.synchronize()
             compare_records(ctx.export(), [orc.env(i) for i in range(n)], phys_g=ctx.phys(), strict_state=False)
