@@ -180,6 +180,15 @@ def ncu_traffic(workload):
         return None
 
 
+def ncu_entry(workload):
+    """The committed ncu summary entry of a workload (profiles/ncu_step_summary.json), or {}."""
+    try:
+        with open(os.path.join(ROOT, "profiles", "ncu_step_summary.json")) as f:
+            return json.load(f).get(workload, {})
+    except Exception:
+        return {}
+
+
 def run_reference(args):
     """--impl reference: the fp64 CPU oracle, as it stands, on this box's host cores (rank 0 only)."""
     rank = int(os.environ.get("RANK", "0"))
@@ -625,6 +634,19 @@ def main():
                  "reset": {"bound": "issue", "achieved": r_gbs, "unit": "GB/s", "frac_of_hbm": r_gbs / measured_peak()[0],
                            "algorithmic_bytes": r_bytes, "traffic": r_traffic,
                            "traffic_over_algorithmic": (r_traffic / r_bytes) if r_traffic else None}}
+        # the reset's own roofline is instruction issue: one warp-instruction per cycle per SM
+        # sub-partition (4 per SM, B300_MICROARCH.md), at the SM clock sampled under load; the
+        # warp-instructions per launch come from the committed ncu capture of the same kernel
+        w_inst = ncu_entry("cfg5-reset-kernel").get("warp_instructions")
+        if w_inst:
+            n_sm = torch.cuda.get_device_properties(torch.cuda.current_device()).multi_processor_count
+            mhz = clocks.get("sm_mhz") or clocks.get("sm_max_mhz") if isinstance(clocks, dict) else None
+            if mhz:
+                peak_ips = 4 * n_sm * mhz * 1e6
+                ach = w_inst / (r_avg / 1e3)
+                split["reset"]["issue"] = {"warp_instructions_per_launch": w_inst, "achieved": ach, "peak": peak_ips,
+                                           "unit": "warp-instructions/s", "frac": ach / peak_ips, "sm_mhz": mhz,
+                                           "peak_basis": "1 warp-instruction / cycle / SM sub-partition x 4 x SMs x sampled SM clock"}
     per.sort()
     kern_ms = sum(per) / len(per)
     peak, peak_kind = measured_peak()

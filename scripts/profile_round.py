@@ -53,8 +53,9 @@ def main(run, tag):
         wb = float(full["dram__bytes_write.sum"][0]) * scale.get(full["dram__bytes_write.sum"][1], 1)
         js_path = os.path.join(ROOT, "profiles", "ncu_step_summary.json")
         js = json.load(open(js_path)) if os.path.exists(js_path) else {}
+        wi = float(full["smsp__inst_executed.sum"][0]) if "smsp__inst_executed.sum" in full else None
         js["cfg5-reset-kernel"] = {"tag": tag, "dram_bytes_per_launch": rb + wb, "dram_read": rb, "dram_write": wb,
-                                   "resets_per_launch": 104857}
+                                   "resets_per_launch": 104857, "warp_instructions": wi}
         json.dump(js, open(js_path, "w"), indent=1)
     out = []
     for t in ("memcheck", "racecheck", "synccheck", "initcheck"):
