@@ -4,21 +4,22 @@
 // reset_kernel: each CTA scans its interleaved 32-env chunks of the mask (one coalesced 32-byte
 // load and a ballot per warp and chunk), appends the resetting envs (and their next episode index)
 // to a shared-memory list, then
-//   * one thread per resetting env draws the episode record and writes it as 12 whole 32-byte
-//     sectors (one 256-bit store per record group, dr_internal.h): the record of an env is written
-//     in full, so L2 never read-fills a partially written sector from DRAM (the AoSoA record of
-//     round 1 wrote one 4-byte word into each of 89 sectors per reset env: 4.5x the algorithmic
-//     DRAM bytes);
-//   * one warp per resetting env writes its physics row: lanes draw the env's physics Philox
-//     blocks (uniform blocks -> 4 uniforms, normal blocks -> 4 normals) into a per-warp shared-memory
-//     buffer, then lane q evaluates parameters q, q + 32, ..., so every store is a coalesced 128-byte
-//     line of phys[e][*].
+//   * three threads per resetting env draw its episode record in three independent parts and write
+//     it as 12 whole 32-byte sectors (one 256-bit store per record group, dr_internal.h): the
+//     record of an env is written in full, so L2 never read-fills a partially written sector from
+//     DRAM (the AoSoA record of round 1 wrote one 4-byte word into each of 89 sectors per reset
+//     env: 4.5x the algorithmic DRAM bytes);
+//   * one warp per resetting env (pulled from a shared counter) writes its physics row: lane l
+//     draws uniform and normal Philox block l together into the warp's draw buffer (draw-major:
+//     draw j of block b at word 64 j + b, rs_slot), then evaluates parameters 8 l .. 8 l + 7 and
+//     writes them with one 256-bit store (a warp writes its row as 1 KB of contiguous memory).
 // The 60 state planes are not zeroed: one word (FRESH_BIT in the flags plane) marks the env and the
 // step kernel reads a fresh env's state as zero (dr_internal.h).
 #pragma once
 
-// per-warp draw buffer: uniforms at [0, 256), normals at [256, 512), a constant 0 at 512 (the x of
-// draw-free descriptors); rs_src holds, per parameter, the buffer offset of its x | RS_EXP.
+// per-warp draw buffer: uniforms at [0, 256), normals at [256, 512) (both draw-major, rs_slot), a
+// constant 0 at 512 (the x of draw-free descriptors); rs_src holds, per parameter, the buffer offset
+// of its x | RS_EXP.
 constexpr int RH_DRAW = 2 * MAX_PHYS + 4;
 // CTA shape: 256 threads, <= 64 registers (4 CTAs per SM).  Scan schedule: CTA c owns the 32-env
 // mask chunks c, c + G, c + 2 G, ... (G = the grid) and scans up to RH_PASS envs of them into one
