@@ -618,6 +618,26 @@ def main():
             torch.cuda.synchronize()
             r_ms = [ev_a[i].elapsed_time(ev_m[i]) for i in range(D)]
             s_ms = [ev_m[i].elapsed_time(ev_a[i + 1]) for i in range(D)]
+        cold = None
+        l2_bytes = int(getattr(torch.cuda.get_device_properties(torch.cuda.current_device()), "L2_cache_size", 0) or 0)
+        if not cfg["resets"] and l2_bytes and n * (384 + ST_BYTES_PER_ENV + 4 * 184 + 220) <= 1.25 * l2_bytes:
+            # cold-L2 diagnostic (not part of value; SURVEY §8(d) "report warm and cold" for the
+            # L2-borderline configs): each step preceded by a write of 2x the L2 size, events around
+            # the step alone
+            with torch.cuda.stream(lib_stream):
+                flush = torch.empty(2 * l2_bytes // 4, dtype=torch.float32, device="cuda")
+                D = 30
+                ev_c = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(D)]
+                for i in range(D):
+                    flush.fill_(float(i))
+                    ev_c[i][0].record(lib_stream)
+                    one_step(t_base + args.steps + i)
+                    ev_c[i][1].record(lib_stream)
+                torch.cuda.synchronize()
+                c_ms = sorted(a.elapsed_time(b) for a, b in ev_c)
+                del flush
+            cold = {"ms_per_step_median": c_ms[D // 2], "value": n_glob / (c_ms[D // 2] / 1e3),
+                    "method": "each step after a 2x-L2 write, CUDA events around the step, median of 30"}
 
     value = n_glob * args.steps / (elapsed_ms / 1e3)
     split = None
@@ -667,6 +687,10 @@ def main():
     ws = n * (384 + ST_BYTES_PER_ENV + 4 * 184 + 220)
     roofline["working_set_bytes"] = ws
     roofline["l2_resident"] = bool(l2 and ws <= 1.25 * l2)
+    if cold:
+        cold["achieved"] = bytes_step / (cold["ms_per_step_median"] / 1e3) / 1e9
+        cold["frac"] = cold["achieved"] / peak
+        roofline["cold_l2"] = cold
     if roofline["l2_resident"]:
         roofline["note"] = "working set ~ L2 size: part of the bytes are L2 hits; frac against HBM overstates"
 
