@@ -650,7 +650,7 @@ def main():
         r_traffic = ncu_traffic("cfg5-reset-kernel")
         r_gbs = r_bytes / (r_avg / 1e3) / 1e9
         split = {"reset_ms_avg": r_avg, "step_ms_avg": sum(s_ms) / len(s_ms),
-                 "resets_per_step": n // 10, "reset_bytes_per_env": RESET_BYTES,
+                 "resets_per_step": n // 10, "resets_per_s": (n // 10) / (r_avg / 1e3), "reset_bytes_per_env": RESET_BYTES,
                  "reset": {"bound": "issue", "achieved": r_gbs, "unit": "GB/s", "frac_of_hbm": r_gbs / measured_peak()[0],
                            "algorithmic_bytes": r_bytes, "traffic": r_traffic,
                            "traffic_over_algorithmic": (r_traffic / r_bytes) if r_traffic else None}}
@@ -686,6 +686,7 @@ def main():
     l2 = int(getattr(torch.cuda.get_device_properties(torch.cuda.current_device()), "L2_cache_size", 0) or 0)
     ws = n * (384 + ST_BYTES_PER_ENV + 4 * 184 + 220)
     roofline["working_set_bytes"] = ws
+    roofline["l2_bytes"] = l2   # cudaDevAttrL2CacheSize
     roofline["l2_resident"] = bool(l2 and ws <= 1.25 * l2)
     if cold:
         cold["achieved"] = bytes_step / (cold["ms_per_step_median"] / 1e3) / 1e9
