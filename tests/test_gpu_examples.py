@@ -6,10 +6,10 @@ import sys
 
 import pytest
 
-pytestmark = pytest.mark.gpu
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 
 
+@pytest.mark.gpu
 def test_rl_loop_example_runs():
     import torch
     if not torch.cuda.is_available():
@@ -19,3 +19,10 @@ def test_rl_loop_example_runs():
     assert r.returncode == 0, r.stderr[-2000:]
     assert "100 steps of 8192 envs done" in r.stdout, r.stdout
     assert "step 100:" in r.stdout
+
+
+@pytest.mark.parametrize("name", ["rl_loop.py"])
+def test_examples_compile(name):
+    """(CPU) the example scripts are valid Python."""
+    import py_compile
+    py_compile.compile(os.path.join(ROOT, "examples", name), doraise=True)
