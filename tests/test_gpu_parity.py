@@ -238,6 +238,17 @@ def test_reset_mask_patterns(torch_cuda):
             ctx.step(A, O)
             orc.step(acts[0], obs[0])
             assert ctx.last_stats()[10] == int(m.sum())
+        # two resets back to back (the second reads the episode counters the first just wrote, so it
+        # must not scan early), then a step: counts and records as the oracle's
+        m1, m2 = (e % 3 == 0).astype(np.uint8), (e % 5 == 0).astype(np.uint8)
+        ctx.reset(torch.from_numpy(m1).cuda())
+        ctx.reset(torch.from_numpy(m2).cuda())
+        orc.reset(m1)
+        orc.reset(m2)
+        torch.cuda.synchronize()
+        compare_records(ctx.export(), [orc.env(i) for i in range(n)], phys_g=ctx.phys(), strict_state=False)
+        ctx.step(A, O)
+        assert ctx.last_stats()[10] == int(m1.sum() + m2.sum())
     finally:
         ctx.close()
         orc.close()
