@@ -4,7 +4,7 @@
 # default bench and ncu --set full captures of the step, reset and image kernels.  gpurun_out/final_*.
 cd "${GRAFT_REPO_ROOT:-/root/repo}"
 mkdir -p gpurun_out
-O=gpurun_out/r5
+O=gpurun_out/r6
 nvidia-smi > ${O}_nvidia-smi.txt 2>&1
 lscpu > ${O}_lscpu.txt 2>&1
 timeout 300 python -c "import __graft_entry__ as g; g.smoke()" > ${O}_smoke.log 2>&1; echo "smoke rc=$?" >> ${O}_smoke.log
