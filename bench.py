@@ -169,6 +169,18 @@ def measured_peak():
         return 6650.0, "fallback"
 
 
+def mix_ceiling(mix, achieved):
+    """The HBM ceiling of a kernel's own read/write mix (profiles/bw_ceiling.json, measured by
+    scripts/bw_ceiling.cu on a B200): a second denominator beside the copy peak, or None."""
+    try:
+        with open(os.path.join(ROOT, "profiles", "bw_ceiling.json")) as f:
+            d = json.load(f)[mix]
+        return {"gbs": d["gbs"], "frac": achieved / d["gbs"], "mix": d["mix"],
+                "source": "profiles/bw_ceiling.json (scripts/bw_ceiling.cu, PDL, back to back)"}
+    except Exception:
+        return None
+
+
 def ncu_traffic(workload):
     """Per-launch dram bytes of a kernel from the committed ncu summary (profiles/ncu_step_summary.json:
     the step kernel per workload, the reset kernel under "cfg5-reset-kernel"), if any."""
@@ -446,7 +458,8 @@ def run_vision(args):
                 "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                              "frac": achieved / peak, "traffic": None, "peak_kind": peak_kind,
                              "bytes_per_step": bytes_step, "kernel": "dr::image_augment_kernel (+ scene_draw_kernel)",
-                             "kernel_ms_avg": kern_ms, "kernel_ms_median": per[len(per) // 2]},
+                             "kernel_ms_avg": kern_ms, "kernel_ms_median": per[len(per) // 2],
+                             "mix_ceiling": mix_ceiling("vision_1r_4w", achieved)},
                 "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": int(launches), "clocks": clocks}
         print(json.dumps(line), flush=True)
     if world > 1:
@@ -680,6 +693,8 @@ def main():
                 "kernel_ms_avg": kern_ms, "kernel_ms_median": per[len(per) // 2]}
     if split:
         roofline["split"] = split
+    if not cfg["resets"] and cfg["bytes"] == 1228:   # the full pipeline's 768 : 460 mix
+        roofline["mix_ceiling"] = mix_ceiling("step_5r_3w", achieved)
     # the working set every step touches (records 384 B + state planes 320 B + the 4-frame input ring
     # + one output set per env): at config 3's 65,536 envs (109 MB) it largely fits the 126 MB L2, so
     # part of the algorithmic bytes come from L2 and frac can exceed 1; at 1M (1.7 GB) it cannot

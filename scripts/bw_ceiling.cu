@@ -33,6 +33,8 @@ __device__ __forceinline__ void st16(uint4* p, uint4 v) {
 // PDL (programmatic dependent launch, as the vision and step kernels use): the next launch may start
 // once every CTA of this one has begun; each CTA waits for the previous grid before it exits (the
 // ring's buffers are disjoint, so the early reads and writes are safe, as in dr_vision.cu's rule).
+// Small grids let several launches be resident at once: the ring must exceed that depth (use >= 8)
+// or concurrent launches share buffers through L2.
 template <int RV, int WV, int CS, int PDL>
 __global__ void __launch_bounds__(256) mix_kernel(const uint4* __restrict__ in, uint4* __restrict__ out, size_t n,
                                                   uint32_t salt, uint32_t* sink) {
