@@ -42,3 +42,18 @@ def test_reference_arm_non_zero_rank_is_silent():
     r = _run({"RANK": "1", "WORLD_SIZE": "2", "LOCAL_RANK": "1"})
     assert r.returncode == 0, r.stderr
     assert not [l for l in r.stdout.splitlines() if l.startswith("{")]
+
+
+def test_mix_ceiling_reads_the_committed_probe():
+    """roofline.mix_ceiling comes from profiles/bw_ceiling.json, written from the
+    scripts/bw_ceiling.cu runs in profiles/round2_v6_bw_ceiling.txt."""
+    sys.path.insert(0, ROOT)
+    import bench
+    with open(os.path.join(ROOT, "profiles", "bw_ceiling.json")) as f:
+        d = json.load(f)
+    txt = open(os.path.join(ROOT, "profiles", "round2_v6_bw_ceiling.txt")).read()
+    for mix in ("step_5r_3w", "vision_1r_4w", "copy_1r_1w"):
+        assert f'"best_gbs": {d[mix]["gbs"]}' in txt, mix   # the figure is one the probe printed
+        m = bench.mix_ceiling(mix, 0.5 * d[mix]["gbs"])
+        assert m["gbs"] == d[mix]["gbs"] and abs(m["frac"] - 0.5) < 1e-12
+    assert bench.mix_ceiling("no_such_mix", 1.0) is None
