@@ -37,7 +37,7 @@ constexpr int IMG_THREADS = DR_IMG_THREADS;
 #define DR_IMG_PROBE 0   // roofline probes (A/B builds only): 1 = no noise draws, 2 = no output stores
 #endif
 #ifndef DR_IMG_PRE
-#define DR_IMG_PRE 2   // 8-element groups per thread whose noise is drawn while the slice loads
+#define DR_IMG_PRE 1   // 8-element groups per thread whose noise is drawn while the slice loads
 #endif
 #ifndef DR_IMG_MID
 #define DR_IMG_MID 1   // ... and groups drawn between the cluster barrier's arrive and wait
@@ -167,7 +167,20 @@ __device__ __forceinline__ void nz_fold(const NzRaw& q, float kq, float z[8]) {
 __device__ __forceinline__ void img_pdl_trigger() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
 __device__ __forceinline__ void img_pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
 
-__global__ void __launch_bounds__(IMG_THREADS) image_augment_kernel(const ImgArgs a) {
+// Register cap: 10 CTAs of 128 threads per SM (48 registers, no spills with one pre-drawn group)
+// instead of 7 (72 registers, two pre-drawn groups), so more of the next batch's clusters fit beside
+// this batch's and load while it writes.  A/B (us per 192-image batch, three alternating runs,
+// bit-identical): 72 registers 21.56; caps of 8 / 10 / 11 / 16 CTAs 20.93 / 20.82 / 21.34 / 21.37
+// (11 and 16 spill); DR_IMG_MINB=0 restores the uncapped build.
+#ifndef DR_IMG_MINB
+#define DR_IMG_MINB 10
+#endif
+#if DR_IMG_MINB > 0
+#define DR_IMG_BOUNDS __launch_bounds__(IMG_THREADS, DR_IMG_MINB)
+#else
+#define DR_IMG_BOUNDS __launch_bounds__(IMG_THREADS)
+#endif
+__global__ void DR_IMG_BOUNDS image_augment_kernel(const ImgArgs a) {
     img_pdl_trigger();
     if (!a.early_read) img_pdl_wait();   // the previous kernel of the stream may have written the images
     extern __shared__ __align__(128) uint8_t s_img[];
