@@ -4,7 +4,7 @@
 # default bench and ncu --set full captures of the step, reset and image kernels.  gpurun_out/final_*.
 cd "${GRAFT_REPO_ROOT:-/root/repo}"
 mkdir -p gpurun_out
-O=gpurun_out/r6
+O=gpurun_out/${TAG:-r7}
 nvidia-smi > ${O}_nvidia-smi.txt 2>&1
 lscpu > ${O}_lscpu.txt 2>&1
 timeout 300 python -c "import __graft_entry__ as g; g.smoke()" > ${O}_smoke.log 2>&1; echo "smoke rc=$?" >> ${O}_smoke.log
@@ -19,6 +19,9 @@ for n in 524288 262144 131072; do
   timeout 600 python bench.py --n-env $n --steps 4000 --warmup 20 --no-cpu-baseline > ${O}_bench_n$n.log 2>&1
 done
 timeout 300 python scripts/pcie_probe.py > ${O}_pcie.log 2>&1
+nvcc -O3 -std=c++17 -gencode arch=compute_100a,code=sm_100a -o /tmp/bw_ceiling scripts/bw_ceiling.cu && \
+  timeout 300 /tmp/bw_ceiling 1.0 8 20 1 > ${O}_bw_ceiling_1gb_pdl.txt 2>&1 && \
+  timeout 300 /tmp/bw_ceiling 0.115 8 200 1 > ${O}_bw_ceiling_115mb_pdl.txt 2>&1
 timeout 600 ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum --clock-control none \
     -k regex:"step_kernel|reset_kernel|augment|scene|pose|image_" -c 40 --csv --log-file ${O}_launches.csv \
     python bench.py --profile --steps 30 --warmup 5 --no-cpu-baseline > ${O}_ncu_launch.log 2>&1
