@@ -709,6 +709,9 @@ __device__ __forceinline__ unsigned long long* probe_slot(const DevPtrs& p, uint
 #else
 #define DR_PROBE(t, k) (void)0
 #endif
+#ifndef DR_POLL_NS
+#define DR_POLL_NS 64   // back-off of the chained step's readiness poll (A/B knob; 0 = spin)
+#endif
 __device__ __forceinline__ uint32_t step_begin(const DevPtrs& p, uint32_t* s_t, int chain) {
 #ifdef DR_PROBE_TIMING
     const unsigned long long ts0 = gtime();
@@ -736,7 +739,11 @@ __device__ __forceinline__ uint32_t step_begin(const DevPtrs& p, uint32_t* s_t, 
         // tile i on CTA i % G); start once that CTA has published its state stores (cta_ready: before
         // its stats atomics, which are not on this step's path)
         if (chain)
-            while (ld_acquire_u32(p.cta_ready + blockIdx.x) != t) __nanosleep(64);
+            while (ld_acquire_u32(p.cta_ready + blockIdx.x) != t) {
+#if DR_POLL_NS > 0
+                __nanosleep(DR_POLL_NS);
+#endif
+            }
         *s_t = t;
 #ifdef DR_PROBE_TIMING
         probe_slot(p, t)[0] = ts0;
