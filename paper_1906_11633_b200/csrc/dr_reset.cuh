@@ -37,7 +37,10 @@ constexpr int RH_THREADS = DR_RH_THREADS;
 #ifndef DR_RH_PASS
 #define DR_RH_PASS 2048
 #endif
-constexpr uint32_t RH_PASS = DR_RH_PASS;   // envs scanned per pass (the shared-memory list's capacity)
+constexpr uint32_t RH_PASS = DR_RH_PASS;
+#ifndef DR_RESET_EARLY_TRIGGER
+#define DR_RESET_EARLY_TRIGGER 0   // A/B knob: trigger the next launch at the start, not at the end
+#endif   // envs scanned per pass (the shared-memory list's capacity)
 
 __device__ __forceinline__ float sel4(const float z[4], uint32_t r) {
     return r == 0u ? z[0] : (r == 1u ? z[1] : (r == 2u ? z[2] : z[3]));
@@ -344,6 +347,7 @@ __global__ void __launch_bounds__(RH_THREADS, DR_RH_MINB) reset_kernel(DevPtrs p
     }
 #endif
     bool waited = !early_scan;
+    if (DR_RESET_EARLY_TRIGGER) pdl_trigger();
     if (waited) pdl_wait();   // before any global access (dr_device.cuh)
     RPROBE(1);
     constexpr int NWR = RH_THREADS / 32;
@@ -429,6 +433,6 @@ __global__ void __launch_bounds__(RH_THREADS, DR_RH_MINB) reset_kernel(DevPtrs p
         }
     }
     if (!waited) pdl_wait();   // (a CTA without a pass) before the global atomic below
-    pdl_trigger();
+    if (!DR_RESET_EARLY_TRIGGER) pdl_trigger();
     if (!first && applied) atomicAdd(&p.ctl[2], (unsigned long long)applied);
 }

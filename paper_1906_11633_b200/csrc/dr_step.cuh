@@ -709,6 +709,9 @@ __device__ __forceinline__ unsigned long long* probe_slot(const DevPtrs& p, uint
 #else
 #define DR_PROBE(t, k) (void)0
 #endif
+#ifndef DR_STEP_EARLY_TRIGGER
+#define DR_STEP_EARLY_TRIGGER 0   // A/B knob: unchained steps trigger the next launch after the ticket
+#endif
 #ifndef DR_POLL_NS
 #define DR_POLL_NS 64   // back-off of the chained step's readiness poll (A/B knob; 0 = spin)
 #endif
@@ -752,13 +755,13 @@ __device__ __forceinline__ uint32_t step_begin(const DevPtrs& p, uint32_t* s_t, 
 #endif
     }
     __syncthreads();
-    if (chain) pdl_trigger();   // ticket taken (and, for the first CTA, the next slot prepared)
+    if (chain || DR_STEP_EARLY_TRIGGER) pdl_trigger();   // ticket taken (and, for the first CTA, the next slot prepared)
     return *s_t;
 }
 template <uint32_t L, int NT = STEP_THREADS>
 __device__ __forceinline__ void reduce_stats(const DevPtrs& p, const Acc& acc, uint32_t my_envs, uint32_t t,
                                              double* s_red) {
-    pdl_trigger();   // (unchained launches) this CTA's tiles are issued: the next step may launch
+    if (!DR_STEP_EARLY_TRIGGER) pdl_trigger();   // (unchained launches) this CTA's tiles are issued: the next step may launch
     if (threadIdx.x == 0) DR_PROBE(t, 3);
     const int tid = threadIdx.x;
     const int lane = tid & 31, wid = tid >> 5;
