@@ -173,7 +173,7 @@ __device__ __forceinline__ void img_pdl_wait() { asm volatile("griddepcontrol.wa
 // bit-identical): 72 registers 21.56; caps of 8 / 10 / 11 / 16 CTAs 20.93 / 20.82 / 21.34 / 21.37
 // (11 and 16 spill); DR_IMG_MINB=0 restores the uncapped build.
 #ifndef DR_IMG_MINB
-#define DR_IMG_MINB 10
+#define DR_IMG_MINB (1280 / DR_IMG_THREADS)   // 10 CTAs of 128 threads (48 registers); scales with the CTA size
 #endif
 #if DR_IMG_MINB > 0
 #define DR_IMG_BOUNDS __launch_bounds__(IMG_THREADS, DR_IMG_MINB)
